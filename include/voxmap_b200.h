@@ -1,0 +1,255 @@
+/*
+ * voxmap_b200 — C-ABI of the B200-native per-frame map update
+ * (block allocation -> TSDF projective integration -> ESDF -> query).
+ *
+ * This is the drop-in boundary that replaces the reference's C++ mapper API
+ * in /root/reference/proj/include (namespace voxmap).  Every entry point names
+ * the reference interface it replaces (file:line under proj/).  The C++
+ * facade in include/voxmap_b200/voxmap.hpp re-exposes the reference's
+ * signatures (Layer<V>, integrate_depth, update_esdf, query_batch, ...) on
+ * top of these functions; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - Plain C types only: pointers + sizes, POD config structs mirroring the
+ *     reference's config structs field for field.
+ *   - Every function returns vxm_status; on failure vxm_last_error() holds a
+ *     message.  Status codes map 1:1 onto the reference's exception types
+ *     (InvalidPoseError, std::invalid_argument, MapCapacityError).
+ *   - Host-pointer entry points are synchronous (they return the reference's
+ *     by-value results).  *_device entry points take device pointers, are
+ *     stream-ordered on the context's stream, and report errors at
+ *     vxm_context_synchronize().
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with VXM_ERR_CUDA.
+ */
+#ifndef VOXMAP_B200_H_
+#define VOXMAP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status ----------------------------------------------------------- */
+typedef enum {
+  VXM_OK = 0,
+  VXM_ERR_INVALID_POSE = 1,     /* voxmap::InvalidPoseError      pose.hpp:23-26   */
+  VXM_ERR_INVALID_ARGUMENT = 2, /* std::invalid_argument                         */
+  VXM_ERR_CAPACITY = 3,         /* voxmap::MapCapacityError      layer.hpp:28-31  */
+  VXM_ERR_CUDA = 4,             /* device missing / CUDA runtime failure         */
+  VXM_ERR_INTERNAL = 5
+} vxm_status;
+
+/* ---- POD mirrors of the reference types -------------------------------- */
+/* GridIndex (core/indexing.hpp:33-39): lexicographic (x, y, z) order. */
+typedef struct { int32_t x, y, z; } vxm_grid_index;
+
+/* TsdfVoxel (core/voxels.hpp:22-26), 8 bytes. */
+typedef struct { float distance, weight; } vxm_tsdf_voxel;
+
+/* EsdfVoxel (core/voxels.hpp:48-68), 12 bytes, same byte layout. */
+typedef struct {
+  int32_t squared_distance;
+  int16_t parent_x, parent_y, parent_z;
+  uint8_t flags; /* 1 observed, 2 site, 4 inside */
+  uint8_t reserved;
+} vxm_esdf_voxel;
+
+enum { VXM_ESDF_OBSERVED = 1, VXM_ESDF_SITE = 2, VXM_ESDF_INSIDE = 4 };
+enum { VXM_VOXELS_PER_SIDE = 8, VXM_VOXELS_PER_BLOCK = 512 };
+
+/* Layer voxel type. */
+typedef enum { VXM_LAYER_TSDF = 0, VXM_LAYER_ESDF = 1 } vxm_layer_type;
+
+/* CameraIntrinsics (sensor/camera.hpp:24-31). */
+typedef struct {
+  double fu, fv, cu, cv;
+  int32_t width, height;
+  double max_depth;
+} vxm_camera;
+
+/* LidarIntrinsics (sensor/lidar.hpp:27-38). */
+typedef struct {
+  int32_t num_azimuth, num_elevation;
+  double azimuth_start, elevation_start, azimuth_fov, elevation_fov;
+  double min_range, max_range;
+} vxm_lidar;
+
+/* Pose (sensor/pose.hpp:30-60): p_parent = R * p_child + t, R row-major. */
+typedef struct { double R[9]; double t[3]; } vxm_pose;
+
+enum { VXM_WEIGHT_CONSTANT = 0, VXM_WEIGHT_INVERSE_SQUARE = 1 };
+enum { VXM_SAMPLE_NEAREST = 0, VXM_SAMPLE_LINEAR = 1 };
+
+/* IntegratorConfig (integrate/config.hpp:38-56). */
+typedef struct {
+  double truncation;
+  float max_weight;
+  int32_t weighting;
+  double max_integration_distance;
+  int32_t camera_sample;
+  int32_t lidar_sample;
+  float max_sample_gap;
+  int32_t view_pixel_subsample;
+  float hit_log_odds, miss_log_odds, log_odds_min, log_odds_max;
+  int32_t parallel; /* accepted, ignored */
+} vxm_integrator_config;
+
+/* ViewConfig (sensor/view.hpp:27-31). */
+typedef struct {
+  double max_integration_distance;
+  double truncation;
+  int32_t pixel_subsample;
+} vxm_view_config;
+
+/* EsdfConfig (esdf/integrator.hpp:30-40). */
+typedef struct {
+  double site_threshold;
+  float occupied_log_odds_threshold;
+  double max_distance;
+  int32_t parallel; /* accepted, ignored */
+} vxm_esdf_config;
+
+/* QueryConfig (query/query.hpp:41-49) and QueryResult (:30-39). */
+typedef struct { int32_t interpolate; int32_t parallel; } vxm_query_config;
+typedef struct {
+  int32_t known;
+  int32_t pad_;
+  double distance;
+  double gradient[3];
+} vxm_query_result;
+
+/* Reference defaults (config.hpp, esdf/integrator.hpp, query.hpp). */
+void vxm_integrator_config_default(vxm_integrator_config* cfg);
+void vxm_esdf_config_default(vxm_esdf_config* cfg);
+void vxm_query_config_default(vxm_query_config* cfg);
+
+/* ---- opaque handles ---------------------------------------------------- */
+typedef struct vxm_context vxm_context;     /* device + stream + scratch       */
+typedef struct vxm_layer vxm_layer;         /* Layer<V> (core/layer.hpp:47-125) */
+typedef struct vxm_blocklist vxm_blocklist; /* std::vector<GridIndex> result    */
+typedef struct vxm_esdf_state vxm_esdf_state; /* EsdfUpdateState (esdf/integrator.hpp:67-74) */
+
+const char* vxm_last_error(void);
+const char* vxm_version(void);
+
+/* Context: one CUDA device + one stream.  Calls on a context are serialized. */
+vxm_status vxm_context_create(int device, vxm_context** out);
+void vxm_context_destroy(vxm_context* ctx);
+vxm_status vxm_context_synchronize(vxm_context* ctx);
+/* Block-coordinate sharding: this context owns blocks with
+ * floor(g.x / slab) mod world == rank.  world = 1 (default) owns everything. */
+vxm_status vxm_context_set_shard(vxm_context* ctx, int rank, int world, int slab);
+/* Kernel launches issued by this context since creation (bench evidence). */
+uint64_t vxm_context_launch_count(const vxm_context* ctx);
+
+/* ---- block lists ------------------------------------------------------- */
+vxm_status vxm_blocklist_create(vxm_context* ctx, vxm_blocklist** out);
+void vxm_blocklist_destroy(vxm_blocklist* list);
+/* Host view (downloads if the list was produced by a *_device call). */
+vxm_status vxm_blocklist_host(vxm_blocklist* list, const vxm_grid_index** data, uint64_t* n);
+/* Replace contents with a host array (uploads). */
+vxm_status vxm_blocklist_assign(vxm_blocklist* list, const vxm_grid_index* data, uint64_t n);
+
+/* ---- layers (core/layer.hpp) -------------------------------------------- */
+/* Layer(double voxel_size, size_t max_blocks) — layer.hpp:52-57. */
+vxm_status vxm_layer_create(vxm_context* ctx, vxm_layer_type type, double voxel_size,
+                            uint64_t max_blocks, vxm_layer** out);
+void vxm_layer_destroy(vxm_layer* layer);
+double vxm_layer_voxel_size(const vxm_layer* layer);
+/* num_blocks() — layer.hpp:61. */
+vxm_status vxm_layer_num_blocks(vxm_layer* layer, uint64_t* out);
+/* has_block() for a batch of keys — layer.hpp:63. out[i] = 0/1. */
+vxm_status vxm_layer_has_blocks(vxm_layer* layer, const vxm_grid_index* keys, uint64_t n,
+                                uint8_t* out);
+/* sorted_indices() + block bytes — layer.hpp:109-117 (and block_ptr()).
+ * keys_out gets num_blocks sorted keys; voxels_out (may be NULL) gets the
+ * blocks' bytes in the same order (512 voxels each). */
+vxm_status vxm_layer_export(vxm_layer* layer, vxm_grid_index* keys_out, void* voxels_out,
+                            uint64_t capacity);
+/* Read specific blocks (block_ptr) — missing blocks are zero-filled, found[i]=0. */
+vxm_status vxm_layer_read_blocks(vxm_layer* layer, const vxm_grid_index* keys, uint64_t n,
+                                 void* voxels_out, uint8_t* found);
+/* get_or_allocate + overwrite bytes (host writes through block_ptr). */
+vxm_status vxm_layer_write_blocks(vxm_layer* layer, const vxm_grid_index* keys, uint64_t n,
+                                  const void* voxels);
+/* clone() — layer.hpp:98-105. */
+vxm_status vxm_layer_clone(vxm_layer* src, vxm_layer** out);
+
+/* ---- view candidates (sensor/view.hpp:38-48, view.cpp:61-111) ---------- */
+vxm_status vxm_blocks_in_view_camera(vxm_context* ctx, const vxm_pose* T_LS, const vxm_camera* cam,
+                                     const float* depth, int width, int height, double block_size,
+                                     const vxm_view_config* cfg, vxm_blocklist* out);
+vxm_status vxm_blocks_in_view_lidar(vxm_context* ctx, const vxm_pose* T_LS, const vxm_lidar* lidar,
+                                    const float* depth, int width, int height, double block_size,
+                                    const vxm_view_config* cfg, vxm_blocklist* out);
+
+/* ---- TSDF integration (integrate/integrator.hpp:36-45) ------------------ */
+/* integrate_depth(Layer<TsdfVoxel>&, DepthImage, Pose T_LS, CameraIntrinsics,
+ * IntegratorConfig) — integrator.cpp:162-168.  changed_out receives the
+ * sorted changed-block list.  Validates before mutating (integrator.cpp:26-34). */
+vxm_status vxm_integrate_depth_camera(vxm_layer* layer, const float* depth, int width, int height,
+                                      const vxm_pose* T_LS, const vxm_camera* cam,
+                                      const vxm_integrator_config* cfg, vxm_blocklist* changed_out);
+/* LidarIntrinsics overload — integrator.cpp:169-175. */
+vxm_status vxm_integrate_depth_lidar(vxm_layer* layer, const float* depth, int width, int height,
+                                     const vxm_pose* T_LS, const vxm_lidar* lidar,
+                                     const vxm_integrator_config* cfg, vxm_blocklist* changed_out);
+/* Device-resident variants: depth is a device pointer, changed_out stays on
+ * the device (read it with vxm_blocklist_host).  Errors surface at
+ * vxm_context_synchronize(). */
+vxm_status vxm_integrate_depth_camera_device(vxm_layer* layer, const float* depth_dev, int width,
+                                             int height, const vxm_pose* T_LS,
+                                             const vxm_camera* cam,
+                                             const vxm_integrator_config* cfg,
+                                             vxm_blocklist* changed_out);
+vxm_status vxm_integrate_depth_lidar_device(vxm_layer* layer, const float* depth_dev, int width,
+                                            int height, const vxm_pose* T_LS,
+                                            const vxm_lidar* lidar,
+                                            const vxm_integrator_config* cfg,
+                                            vxm_blocklist* changed_out);
+
+/* ---- ESDF (esdf/integrator.hpp:81-120) ---------------------------------- */
+/* update_esdf(Layer<EsdfVoxel>&, const Layer<TsdfVoxel>&, updated, EsdfConfig)
+ * — esdf/integrator.cpp:365-413, 567-572. */
+vxm_status vxm_update_esdf(vxm_layer* esdf, vxm_layer* tsdf, const vxm_grid_index* updated,
+                           uint64_t n, const vxm_esdf_config* cfg, vxm_blocklist* changed_out);
+/* Same, with the updated list taken from a (device-resident) block list,
+ * e.g. the changed_out of a previous integrate call. */
+vxm_status vxm_update_esdf_list(vxm_layer* esdf, vxm_layer* tsdf, vxm_blocklist* updated,
+                                const vxm_esdf_config* cfg, vxm_blocklist* changed_out);
+
+/* Phase API (esdf/integrator.hpp:76-107), used directly by the reference's tests. */
+vxm_status vxm_esdf_state_create(vxm_esdf_state** out);
+void vxm_esdf_state_destroy(vxm_esdf_state* st);
+/* Which: 0 indices_to_update, 1 indices_to_clear, 2 cleared_indices. */
+vxm_status vxm_esdf_state_get(vxm_esdf_state* st, int which, const vxm_grid_index** data,
+                              uint64_t* n);
+vxm_status vxm_esdf_state_set(vxm_esdf_state* st, int which, const vxm_grid_index* data,
+                              uint64_t n);
+/* mark_sites — esdf/integrator.cpp:417-423 (TSDF source). changed is appended. */
+vxm_status vxm_esdf_mark_sites(vxm_layer* esdf, vxm_layer* tsdf, const vxm_grid_index* updated,
+                               uint64_t n, const vxm_esdf_config* cfg, vxm_esdf_state* st,
+                               vxm_blocklist* changed);
+/* clear_invalid — esdf/integrator.cpp:433-486. */
+vxm_status vxm_esdf_clear_invalid(vxm_layer* esdf, const vxm_esdf_config* cfg, vxm_esdf_state* st,
+                                  vxm_blocklist* changed);
+/* lower_esdf — esdf/integrator.cpp:488-565; *rounds receives the round count. */
+vxm_status vxm_esdf_lower(vxm_layer* esdf, vxm_esdf_state* st, const vxm_esdf_config* cfg,
+                          vxm_blocklist* changed, int* rounds);
+
+/* ---- queries (query/query.hpp:59-62, query.cpp:147-161) ----------------- */
+vxm_status vxm_query_batch(vxm_layer* esdf, const double* xyz, uint64_t n, int want_gradient,
+                           const vxm_query_config* cfg, vxm_query_result* out);
+
+/* ---- host utilities ----------------------------------------------------- */
+/* Pose::valid() (pose.hpp:42-50) and Pose::inverse() (:52). */
+int vxm_pose_valid(const vxm_pose* T);
+void vxm_pose_inverse(const vxm_pose* T, vxm_pose* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXMAP_B200_H_ */

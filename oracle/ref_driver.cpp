@@ -1,0 +1,389 @@
+// TEST INFRASTRUCTURE ONLY — never linked into or called by the product.
+//
+// extern "C" driver over the reference's OWN sources (/root/reference/proj/src,
+// compiled unmodified with -Dvoxmap=voxmap_ref against oracle/eigen_shim by
+// oracle/Makefile into oracle/_ref/libvoxmap_ref.so).  Only tests/, smoke()
+// and bench.py's reference/cpu_baseline legs load it, as the checker and as
+// the timed CPU baseline ("cpu_baseline.kind": "reference").
+//
+// It exposes the reference API calls used for parity and timing:
+//   integrate_depth            proj/src/integrate/integrator.cpp:162-175
+//   reference_integrate_depth  proj/src/reference/reference.cpp:334-354
+//   blocks_in_view             proj/src/sensor/view.cpp:61-111
+//   update_esdf / mark_sites / clear_invalid / lower_esdf
+//                              proj/src/esdf/integrator.cpp:417-572
+//   query_batch / reference_query_batch
+//                              proj/src/query/query.cpp:147-161, reference.cpp:378-386
+//   render_depth / orbit_pose  proj/src/io/render.cpp:43-86, dataset.cpp:309-367
+//   brute_force_esdf / compare_esdf / esdf_identical
+//                              proj/src/eval/oracle.cpp:26-151
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "voxmap/core/layer.hpp"
+#include "voxmap/core/voxels.hpp"
+#include "voxmap/esdf/integrator.hpp"
+#include "voxmap/eval/oracle.hpp"
+#include "voxmap/integrate/integrator.hpp"
+#include "voxmap/io/dataset.hpp"
+#include "voxmap/io/render.hpp"
+#include "voxmap/io/scene.hpp"
+#include "voxmap/query/query.hpp"
+#include "voxmap/reference/reference.hpp"
+#include "voxmap/sensor/view.hpp"
+#include "voxmap_b200.h"
+
+namespace vr = voxmap_ref;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RefLayer {
+  int type;
+  vr::Layer<vr::TsdfVoxel>* tsdf = nullptr;
+  vr::Layer<vr::EsdfVoxel>* esdf = nullptr;
+  ~RefLayer() {
+    delete tsdf;
+    delete esdf;
+  }
+};
+
+struct RefState {
+  vr::EsdfUpdateState st;
+};
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return VXM_OK;
+  } catch (const vr::InvalidPoseError& e) {
+    g_err = e.what();
+    return VXM_ERR_INVALID_POSE;
+  } catch (const vr::MapCapacityError& e) {
+    g_err = e.what();
+    return VXM_ERR_CAPACITY;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return VXM_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VXM_ERR_INTERNAL;
+  }
+}
+
+vr::Pose to_pose(const vxm_pose* p) {
+  vr::Pose T;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) T.R(r, c) = p->R[r * 3 + c];
+  for (int i = 0; i < 3; ++i) T.t[i] = p->t[i];
+  return T;
+}
+void from_pose(const vr::Pose& T, vxm_pose* p) {
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) p->R[r * 3 + c] = T.R(r, c);
+  for (int i = 0; i < 3; ++i) p->t[i] = T.t[i];
+}
+vr::CameraIntrinsics to_cam(const vxm_camera* c) {
+  vr::CameraIntrinsics k;
+  k.fu = c->fu; k.fv = c->fv; k.cu = c->cu; k.cv = c->cv;
+  k.width = c->width; k.height = c->height; k.max_depth = c->max_depth;
+  return k;
+}
+vr::LidarIntrinsics to_lidar(const vxm_lidar* l) {
+  vr::LidarIntrinsics k;
+  k.num_azimuth = l->num_azimuth; k.num_elevation = l->num_elevation;
+  k.azimuth_start = l->azimuth_start; k.elevation_start = l->elevation_start;
+  k.azimuth_fov = l->azimuth_fov; k.elevation_fov = l->elevation_fov;
+  k.min_range = l->min_range; k.max_range = l->max_range;
+  return k;
+}
+vr::IntegratorConfig to_icfg(const vxm_integrator_config* c) {
+  vr::IntegratorConfig k;
+  k.truncation = c->truncation;
+  k.max_weight = c->max_weight;
+  k.weighting = c->weighting == VXM_WEIGHT_INVERSE_SQUARE ? vr::WeightMode::kInverseSquareDepth
+                                                          : vr::WeightMode::kConstant;
+  k.max_integration_distance = c->max_integration_distance;
+  k.camera_sample = c->camera_sample == VXM_SAMPLE_LINEAR
+                        ? vr::DepthSampleMode::kLinearForegroundSafe
+                        : vr::DepthSampleMode::kNearest;
+  k.lidar_sample = c->lidar_sample == VXM_SAMPLE_LINEAR
+                       ? vr::DepthSampleMode::kLinearForegroundSafe
+                       : vr::DepthSampleMode::kNearest;
+  k.max_sample_gap = c->max_sample_gap;
+  k.view_pixel_subsample = c->view_pixel_subsample;
+  k.hit_log_odds = c->hit_log_odds;
+  k.miss_log_odds = c->miss_log_odds;
+  k.log_odds_min = c->log_odds_min;
+  k.log_odds_max = c->log_odds_max;
+  k.parallel = c->parallel != 0;
+  return k;
+}
+vr::EsdfConfig to_ecfg(const vxm_esdf_config* c) {
+  vr::EsdfConfig k;
+  k.site_threshold = c->site_threshold;
+  k.occupied_log_odds_threshold = c->occupied_log_odds_threshold;
+  k.max_distance = c->max_distance;
+  k.parallel = c->parallel != 0;
+  return k;
+}
+vr::DepthImage to_depth(const float* d, int w, int h) {
+  vr::DepthImage img(w, h);
+  std::memcpy(img.data.data(), d, sizeof(float) * size_t(w) * h);
+  return img;
+}
+void emit(const std::vector<vr::GridIndex>& v, vxm_grid_index** out, uint64_t* n) {
+  *n = v.size();
+  *out = static_cast<vxm_grid_index*>(std::malloc(sizeof(vxm_grid_index) * (v.size() + 1)));
+  for (size_t i = 0; i < v.size(); ++i) (*out)[i] = {v[i].x, v[i].y, v[i].z};
+}
+std::vector<vr::GridIndex> to_list(const vxm_grid_index* k, uint64_t n) {
+  std::vector<vr::GridIndex> v(n);
+  for (uint64_t i = 0; i < n; ++i) v[i] = {k[i].x, k[i].y, k[i].z};
+  return v;
+}
+
+template <typename V>
+void export_layer(const vr::Layer<V>& L, vxm_grid_index* keys, void* voxels) {
+  const auto idx = L.sorted_indices();
+  for (size_t i = 0; i < idx.size(); ++i) {
+    keys[i] = {idx[i].x, idx[i].y, idx[i].z};
+    if (voxels)
+      std::memcpy(static_cast<char*>(voxels) + i * sizeof(V) * vr::kVoxelsPerBlock,
+                  L.block_ptr(idx[i])->voxels.data(), sizeof(V) * vr::kVoxelsPerBlock);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vxr_last_error() { return g_err.c_str(); }
+void vxr_free(void* p) { std::free(p); }
+
+int vxr_layer_create(int type, double vs, uint64_t max_blocks, void** out) {
+  return guard([&] {
+    auto* L = new RefLayer{type};
+    const size_t mb = max_blocks ? size_t(max_blocks) : size_t{1} << 30;
+    try {
+      if (type == VXM_LAYER_TSDF) L->tsdf = new vr::Layer<vr::TsdfVoxel>(vs, mb);
+      else L->esdf = new vr::Layer<vr::EsdfVoxel>(vs, mb);
+    } catch (...) {
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+void vxr_layer_destroy(void* h) { delete static_cast<RefLayer*>(h); }
+uint64_t vxr_layer_num_blocks(void* h) {
+  auto* L = static_cast<RefLayer*>(h);
+  return L->tsdf ? L->tsdf->num_blocks() : L->esdf->num_blocks();
+}
+int vxr_layer_export(void* h, vxm_grid_index* keys, void* voxels) {
+  return guard([&] {
+    auto* L = static_cast<RefLayer*>(h);
+    if (L->tsdf) export_layer(*L->tsdf, keys, voxels);
+    else export_layer(*L->esdf, keys, voxels);
+  });
+}
+int vxr_layer_write_blocks(void* h, const vxm_grid_index* keys, uint64_t n, const void* voxels) {
+  return guard([&] {
+    auto* L = static_cast<RefLayer*>(h);
+    for (uint64_t i = 0; i < n; ++i) {
+      const vr::GridIndex g{keys[i].x, keys[i].y, keys[i].z};
+      if (L->tsdf)
+        std::memcpy(L->tsdf->get_or_allocate(g).voxels.data(),
+                    static_cast<const char*>(voxels) + i * 4096, 4096);
+      else
+        std::memcpy(L->esdf->get_or_allocate(g).voxels.data(),
+                    static_cast<const char*>(voxels) + i * 6144, 6144);
+    }
+  });
+}
+
+int vxr_blocks_in_view_camera(const vxm_pose* T, const vxm_camera* cam, const float* depth, int w,
+                              int h, double block_size, const vxm_view_config* vc,
+                              vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    const vr::ViewConfig cfg{vc->max_integration_distance, vc->truncation, vc->pixel_subsample};
+    emit(vr::blocks_in_view(to_pose(T), to_cam(cam), to_depth(depth, w, h), block_size, cfg), out,
+         n);
+  });
+}
+int vxr_blocks_in_view_lidar(const vxm_pose* T, const vxm_lidar* li, const float* depth, int w,
+                             int h, double block_size, const vxm_view_config* vc,
+                             vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    const vr::ViewConfig cfg{vc->max_integration_distance, vc->truncation, vc->pixel_subsample};
+    emit(vr::blocks_in_view(to_pose(T), to_lidar(li), to_depth(depth, w, h), block_size, cfg), out,
+         n);
+  });
+}
+
+// serial != 0 selects the serial restatement reference_integrate_depth.
+int vxr_integrate_camera(void* h, const float* depth, int w, int hh, const vxm_pose* T,
+                         const vxm_camera* cam, const vxm_integrator_config* c, int serial,
+                         vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    auto* L = static_cast<RefLayer*>(h);
+    const auto img = to_depth(depth, w, hh);
+    emit(serial ? vr::reference_integrate_depth(*L->tsdf, img, to_pose(T), to_cam(cam), to_icfg(c))
+                : vr::integrate_depth(*L->tsdf, img, to_pose(T), to_cam(cam), to_icfg(c)),
+         out, n);
+  });
+}
+int vxr_integrate_lidar(void* h, const float* depth, int w, int hh, const vxm_pose* T,
+                        const vxm_lidar* li, const vxm_integrator_config* c, int serial,
+                        vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    auto* L = static_cast<RefLayer*>(h);
+    const auto img = to_depth(depth, w, hh);
+    emit(serial
+             ? vr::reference_integrate_depth(*L->tsdf, img, to_pose(T), to_lidar(li), to_icfg(c))
+             : vr::integrate_depth(*L->tsdf, img, to_pose(T), to_lidar(li), to_icfg(c)),
+         out, n);
+  });
+}
+
+int vxr_update_esdf(void* esdf, void* tsdf, const vxm_grid_index* upd, uint64_t nu,
+                    const vxm_esdf_config* c, vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    auto* E = static_cast<RefLayer*>(esdf);
+    auto* T = static_cast<RefLayer*>(tsdf);
+    emit(vr::update_esdf(*E->esdf, *T->tsdf, to_list(upd, nu), to_ecfg(c)), out, n);
+  });
+}
+
+void* vxr_state_create() { return new RefState; }
+void vxr_state_destroy(void* s) { delete static_cast<RefState*>(s); }
+int vxr_state_get(void* s, int which, vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    auto& st = static_cast<RefState*>(s)->st;
+    emit(which == 0 ? st.indices_to_update
+                    : which == 1 ? st.indices_to_clear : st.cleared_indices,
+         out, n);
+  });
+}
+int vxr_state_set(void* s, int which, const vxm_grid_index* k, uint64_t n) {
+  return guard([&] {
+    auto& st = static_cast<RefState*>(s)->st;
+    (which == 0 ? st.indices_to_update
+                : which == 1 ? st.indices_to_clear : st.cleared_indices) = to_list(k, n);
+  });
+}
+int vxr_mark_sites(void* esdf, void* tsdf, const vxm_grid_index* upd, uint64_t nu,
+                   const vxm_esdf_config* c, void* s, vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    std::vector<vr::GridIndex> changed;
+    vr::mark_sites(*static_cast<RefLayer*>(esdf)->esdf, *static_cast<RefLayer*>(tsdf)->tsdf,
+                   to_list(upd, nu), to_ecfg(c), &static_cast<RefState*>(s)->st, &changed);
+    emit(changed, out, n);
+  });
+}
+int vxr_clear_invalid(void* esdf, const vxm_esdf_config* c, void* s, vxm_grid_index** out,
+                      uint64_t* n) {
+  return guard([&] {
+    std::vector<vr::GridIndex> changed;
+    vr::clear_invalid(*static_cast<RefLayer*>(esdf)->esdf, to_ecfg(c),
+                      &static_cast<RefState*>(s)->st, &changed);
+    emit(changed, out, n);
+  });
+}
+int vxr_lower_esdf(void* esdf, void* s, const vxm_esdf_config* c, int* rounds,
+                   vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    std::vector<vr::GridIndex> changed;
+    *rounds = vr::lower_esdf(*static_cast<RefLayer*>(esdf)->esdf, static_cast<RefState*>(s)->st,
+                             to_ecfg(c), &changed);
+    emit(changed, out, n);
+  });
+}
+
+int vxr_query_batch(void* esdf, const double* xyz, uint64_t n, int want_gradient,
+                    const vxm_query_config* qc, int serial, vxm_query_result* out) {
+  return guard([&] {
+    std::vector<Eigen::Vector3d> pts(n);
+    for (uint64_t i = 0; i < n; ++i) pts[i] = Eigen::Vector3d(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+    vr::QueryConfig cfg;
+    cfg.interpolate = qc->interpolate != 0;
+    cfg.parallel = qc->parallel != 0;
+    const auto& E = *static_cast<RefLayer*>(esdf)->esdf;
+    const auto res = serial ? vr::reference_query_batch(E, pts, want_gradient != 0, cfg)
+                            : vr::query_batch(E, pts, want_gradient != 0, cfg);
+    for (uint64_t i = 0; i < n; ++i) {
+      out[i].known = res[i].known;
+      out[i].pad_ = 0;
+      out[i].distance = res[i].distance;
+      for (int a = 0; a < 3; ++a) out[i].gradient[a] = res[i].gradient[a];
+    }
+  });
+}
+
+// Scenes / rendering / trajectories (input generators of the reference).
+int vxr_orbit_pose(const char* scene, int lidar, int k, int total, vxm_pose* out) {
+  return guard([&] {
+    const auto sc = vr::make_scene(scene);
+    from_pose(vr::orbit_pose(sc, lidar ? vr::SensorKind::kLidar : vr::SensorKind::kCamera, k, total),
+              out);
+  });
+}
+int vxr_render_depth_camera(const char* scene, const vxm_pose* T, const vxm_camera* cam,
+                            float* out) {
+  return guard([&] {
+    const auto img = vr::render_depth(vr::make_scene(scene), to_pose(T), to_cam(cam));
+    std::memcpy(out, img.data.data(), sizeof(float) * img.data.size());
+  });
+}
+int vxr_render_depth_lidar(const char* scene, const vxm_pose* T, const vxm_lidar* li, float* out) {
+  return guard([&] {
+    const auto img = vr::render_depth(vr::make_scene(scene), to_pose(T), to_lidar(li));
+    std::memcpy(out, img.data.data(), sizeof(float) * img.data.size());
+  });
+}
+void vxr_default_camera(int w, int h, vxm_camera* out) {
+  const auto c = vr::default_camera_intrinsics(w, h);
+  *out = {c.fu, c.fv, c.cu, c.cv, c.width, c.height, c.max_depth};
+}
+void vxr_default_lidar(int na, int ne, vxm_lidar* out) {
+  const auto l = vr::default_lidar_intrinsics(na, ne);
+  *out = {l.num_azimuth, l.num_elevation, l.azimuth_start, l.elevation_start,
+          l.azimuth_fov,  l.elevation_fov, l.min_range,     l.max_range};
+}
+int vxr_pose_valid(const vxm_pose* T) { return to_pose(T).valid() ? 1 : 0; }
+void vxr_pose_inverse(const vxm_pose* T, vxm_pose* out) { from_pose(to_pose(T).inverse(), out); }
+
+// ESDF oracle utilities.
+int vxr_brute_force_esdf(void* esdf, const vxm_esdf_config* c, void** out) {
+  return guard([&] {
+    auto* L = new RefLayer{VXM_LAYER_ESDF};
+    try {
+      L->esdf = new vr::Layer<vr::EsdfVoxel>(
+          vr::brute_force_esdf(*static_cast<RefLayer*>(esdf)->esdf, to_ecfg(c)));
+    } catch (...) {
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+// stats: compared, exact, within_one_voxel, flag_mismatches (uint64) + max_abs_error (double)
+int vxr_compare_esdf(void* a, void* b, uint64_t* stats4, double* max_abs) {
+  return guard([&] {
+    const auto cmp = vr::compare_esdf(*static_cast<RefLayer*>(a)->esdf,
+                                      *static_cast<RefLayer*>(b)->esdf);
+    stats4[0] = cmp.compared;
+    stats4[1] = cmp.exact;
+    stats4[2] = cmp.within_one_voxel;
+    stats4[3] = cmp.flag_mismatches;
+    *max_abs = cmp.max_abs_error;
+  });
+}
+
+}  // extern "C"
