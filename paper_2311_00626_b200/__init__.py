@@ -1,1 +1,13 @@
-"""B200-native per-frame map update (nvblox / voxmap hot path)."""
+"""B200-native per-frame map update (nvblox / voxmap hot path).
+
+Block allocation -> TSDF projective integration -> ESDF -> queries, as
+hand-written sm_100a CUDA behind the C-ABI in include/voxmap_b200.h.  The
+Python API mirrors the reference's C++ mapper API (see voxmap.py).
+"""
+from .voxmap import (BlockList, CameraIntrinsics, Context, EsdfConfig, EsdfLayer,  # noqa: F401
+                     EsdfUpdateState, IntegratorConfig, InvalidArgumentError, InvalidPoseError,
+                     LidarIntrinsics, MapCapacityError, Pose, TsdfLayer, VoxmapCudaError,
+                     VoxmapError, blocks_in_view, clear_invalid, default_camera_intrinsics,
+                     default_context, default_lidar_intrinsics, esdf_distance, integrate_depth,
+                     integrate_depth_device, lib, lower_esdf, mark_sites, query_batch,
+                     update_esdf)

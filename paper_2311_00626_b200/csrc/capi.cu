@@ -1,0 +1,655 @@
+// extern "C" boundary of libvoxmap_b200 (include/voxmap_b200.h).
+//
+// Each entry point validates its arguments exactly where the reference does
+// (before any mutation), maps C++ errors onto vxm_status codes that mirror
+// the reference's exception types, and dispatches to the device drivers.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <string>
+#include <vector>
+
+#include "runtime.cuh"
+
+using namespace vxm;
+
+struct vxm_context : Context {};
+struct vxm_layer : Layer {};
+struct vxm_blocklist : BlockList {
+  bool sorted_unique = false;  // produced by a device pass in sorted order
+};
+struct vxm_esdf_state : EsdfState {};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+vxm_status guard(F&& f) {
+  try {
+    f();
+    return VXM_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return vxm_status(e.code);
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return VXM_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VXM_ERR_INTERNAL;
+  }
+}
+
+#define REQUIRE_ARG(cond, msg) \
+  do {                         \
+    if (!(cond)) throw Error(VXM_ERR_INVALID_ARGUMENT, msg); \
+  } while (0)
+
+inline double sum3h(double a0, double a1, double a2) { return a0 + (a1 + a2); }
+
+__global__ void k_gather_blocks(const unsigned char* pool, const int32_t* slots, uint32_t n,
+                                uint32_t block_bytes, unsigned char* out) {
+  const uint32_t words = block_bytes / 4;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < uint64_t(n) * words;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(i / words), w = uint32_t(i % words);
+    const int32_t s = slots[b];
+    reinterpret_cast<uint32_t*>(out)[i] =
+        s >= 0 ? reinterpret_cast<const uint32_t*>(pool + size_t(s) * block_bytes)[w] : 0u;
+  }
+}
+__global__ void k_scatter_blocks(unsigned char* pool, const int32_t* slots, uint32_t n,
+                                 uint32_t block_bytes, const unsigned char* in) {
+  const uint32_t words = block_bytes / 4;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < uint64_t(n) * words;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(i / words), w = uint32_t(i % words);
+    const int32_t s = slots[b];
+    if (s >= 0)
+      reinterpret_cast<uint32_t*>(pool + size_t(s) * block_bytes)[w] =
+          reinterpret_cast<const uint32_t*>(in)[i];
+  }
+}
+__global__ void k_lookup(const uint64_t* keys, uint32_t n, HashView h, int32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = h.keys ? hash_find(h, keys[i]) : -1;
+}
+
+uint32_t grid1d(Context* ctx, uint64_t n) {
+  return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, uint64_t(ctx->sm_count) * 8)));
+}
+
+void lookup_host_keys(Layer* L, const vxm_grid_index* keys, uint64_t n, std::vector<int32_t>* slots,
+                      DevBuf* dslots) {
+  Context* ctx = L->ctx;
+  std::vector<uint64_t> k(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    const bool ok = coord_ok(keys[i].x) && coord_ok(keys[i].y) && coord_ok(keys[i].z);
+    k[i] = ok ? pack_key(keys[i].x, keys[i].y, keys[i].z) : kEmptyKey - 1;  // never present
+  }
+  DevBuf dk;
+  dk.ensure(sizeof(uint64_t) * std::max<uint64_t>(n, 1));
+  dslots->ensure(sizeof(int32_t) * std::max<uint64_t>(n, 1));
+  if (n) {
+    VXM_CUDA(cudaMemcpyAsync(dk.p, k.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+    k_lookup<<<grid1d(ctx, n), 256, 0, ctx->stream>>>(dk.as<uint64_t>(), uint32_t(n), L->hash,
+                                                     dslots->as<int32_t>());
+    ctx->count_launch();
+    check_launch(ctx, "k_lookup");
+  }
+  slots->resize(n);
+  if (n)
+    VXM_CUDA(cudaMemcpyAsync(slots->data(), dslots->p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void ensure_sorted_unique(vxm_blocklist* list) {
+  if (list->sorted_unique) return;
+  sort_unique_keys(list->ctx, list);
+  // count after unique is on the device; count_hint stays an upper bound
+  list->sorted_unique = true;
+}
+
+void check_pose(const vxm_pose* T) {
+  if (!vxm_pose_valid(T)) throw Error(VXM_ERR_INVALID_POSE, "integrate: degenerate sensor pose");
+}
+
+void stage_depth(Context* ctx, const float* depth, int w, int h, bool on_device, const float** out) {
+  const size_t bytes = sizeof(float) * size_t(w) * size_t(h);
+  if (on_device) {
+    *out = depth;
+    return;
+  }
+  ctx->depth.ensure(std::max<size_t>(bytes, 4));
+  if (bytes)
+    VXM_CUDA(cudaMemcpyAsync(ctx->depth.p, depth, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  *out = ctx->depth.as<float>();
+}
+
+vxm_status integrate_common(vxm_layer* L, const float* depth, int w, int h, const vxm_pose* T,
+                            const vxm_camera* cam, const vxm_lidar* li,
+                            const vxm_integrator_config* cfg, vxm_blocklist* out, bool on_device) {
+  return guard([&] {
+    REQUIRE_ARG(L && T && cfg && out && (cam || li), "integrate: null argument");
+    REQUIRE_ARG(L->type == VXM_LAYER_TSDF, "integrate: layer is not a TSDF layer");
+    // check_frame — integrator.cpp:26-34 (before any mutation)
+    check_pose(T);
+    const int sw = cam ? cam->width : li->num_azimuth;
+    const int sh = cam ? cam->height : li->num_elevation;
+    if (w != sw || h != sh)
+      throw Error(VXM_ERR_INVALID_ARGUMENT, "integrate: image size does not match intrinsics");
+    REQUIRE_ARG(w == 0 || h == 0 || depth, "integrate: null depth image");
+    Context* ctx = L->ctx;
+    ViewArgs va{};
+    va.T_LS = *T;
+    va.lidar = li != nullptr;
+    if (cam) va.cam = *cam;
+    if (li) va.li = *li;
+    va.width = w;
+    va.height = h;
+    va.block_size = L->vs * kVPS;
+    va.cfg = {cfg->max_integration_distance, cfg->truncation, cfg->view_pixel_subsample};
+    stage_depth(ctx, depth, w, h, on_device, &va.depth_dev);
+    out->ctx = ctx;
+    run_integrate(L, va, *cfg, out);
+    out->sorted_unique = true;
+    if (!on_device) out->fetch();
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vxm_last_error(void) { return g_err.c_str(); }
+const char* vxm_version(void) { return "voxmap_b200 0.1 (sm_100a)"; }
+
+void vxm_integrator_config_default(vxm_integrator_config* c) {
+  auto q = [](float v) { return float(std::nearbyint(double(v) * 4096.0) / 4096.0); };
+  c->truncation = 0.2;
+  c->max_weight = 100.0f;
+  c->weighting = VXM_WEIGHT_CONSTANT;
+  c->max_integration_distance = 5.0;
+  c->camera_sample = VXM_SAMPLE_NEAREST;
+  c->lidar_sample = VXM_SAMPLE_LINEAR;
+  c->max_sample_gap = 0.2f;
+  c->view_pixel_subsample = 8;
+  c->hit_log_odds = q(0.8473f);
+  c->miss_log_odds = q(-0.4055f);
+  c->log_odds_min = -5.0f;
+  c->log_odds_max = 5.0f;
+  c->parallel = 1;
+}
+void vxm_esdf_config_default(vxm_esdf_config* c) {
+  c->site_threshold = 0.05;
+  c->occupied_log_odds_threshold = 0.0f;
+  c->max_distance = 2.0;
+  c->parallel = 1;
+}
+void vxm_query_config_default(vxm_query_config* c) {
+  c->interpolate = 1;
+  c->parallel = 1;
+}
+
+// Pose::valid — pose.hpp:42-50 (same association order as the oracle shim).
+int vxm_pose_valid(const vxm_pose* T) {
+  for (int i = 0; i < 9; ++i)
+    if (!std::isfinite(T->R[i])) return 0;
+  for (int i = 0; i < 3; ++i)
+    if (!std::isfinite(T->t[i])) return 0;
+  const double* m = T->R;
+  auto M = [m](int r, int c) { return m[r * 3 + c]; };
+  const double h012 = M(0, 0) * (M(1, 1) * M(2, 2) - M(1, 2) * M(2, 1));
+  const double h102 = M(0, 1) * (M(1, 0) * M(2, 2) - M(1, 2) * M(2, 0));
+  const double h201 = M(0, 2) * (M(1, 0) * M(2, 1) - M(1, 1) * M(2, 0));
+  const double det = h012 - h102 + h201;
+  double ortho = 0.0;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      const double v = sum3h(M(0, r) * M(0, c), M(1, r) * M(1, c), M(2, r) * M(2, c)) -
+                       (r == c ? 1.0 : 0.0);
+      ortho = std::max(ortho, std::fabs(v));
+    }
+  return std::fabs(det - 1.0) <= 1e-6 && ortho <= 1e-6;
+}
+// Pose::inverse — pose.hpp:52
+void vxm_pose_inverse(const vxm_pose* T, vxm_pose* out) {
+  vxm_pose o;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) o.R[3 * r + c] = T->R[3 * c + r];
+  for (int i = 0; i < 3; ++i)
+    o.t[i] = -sum3h(o.R[3 * i] * T->t[0], o.R[3 * i + 1] * T->t[1], o.R[3 * i + 2] * T->t[2]);
+  *out = o;
+}
+
+vxm_status vxm_context_create(int device, vxm_context** out) {
+  return guard([&] {
+    REQUIRE_ARG(out, "null out");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0)
+      throw Error(VXM_ERR_CUDA, "voxmap_b200: no CUDA device " + std::to_string(device) +
+                                    " (this library has no CPU fallback)");
+    cudaDeviceProp prop{};
+    VXM_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      throw Error(VXM_ERR_CUDA, std::string("voxmap_b200 requires an sm_100 (B200) device, got ") +
+                                    prop.name);
+    VXM_CUDA(cudaSetDevice(device));
+    auto* ctx = new vxm_context();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    VXM_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    VXM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DevStatus)));
+    VXM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DevStatus)));
+    VXM_CUDA(cudaMemset(ctx->d_status, 0, sizeof(DevStatus)));
+    *out = ctx;
+  });
+}
+
+void vxm_context_destroy(vxm_context* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  for (int i = 0; i < 2; ++i)
+    if (ctx->scan.status[i]) cudaFree(ctx->scan.status[i]);
+  if (ctx->scan.tickets) cudaFree(ctx->scan.tickets);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+vxm_status vxm_context_synchronize(vxm_context* ctx) {
+  return guard([&] {
+    ctx->sync_status();
+    const DevStatus& s = *ctx->h_status;
+    if (s.bitmap_overflow) throw Error(VXM_ERR_INTERNAL, "candidate bitmap overflow");
+    if (s.capacity_error || s.pool_overflow)
+      throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+  });
+}
+
+vxm_status vxm_context_set_shard(vxm_context* ctx, int rank, int world, int slab) {
+  return guard([&] {
+    REQUIRE_ARG(world >= 1 && rank >= 0 && rank < world && slab >= 1, "invalid shard");
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->slab = slab;
+  });
+}
+uint64_t vxm_context_launch_count(const vxm_context* ctx) { return ctx ? ctx->launches : 0; }
+
+vxm_status vxm_blocklist_create(vxm_context* ctx, vxm_blocklist** out) {
+  return guard([&] {
+    auto* l = new vxm_blocklist();
+    l->ctx = ctx;
+    l->ensure(1);
+    *out = l;
+  });
+}
+void vxm_blocklist_destroy(vxm_blocklist* l) { delete l; }
+vxm_status vxm_blocklist_host(vxm_blocklist* l, const vxm_grid_index** data, uint64_t* n) {
+  return guard([&] {
+    const auto& h = l->fetch();
+    *data = h.data();
+    *n = h.size();
+  });
+}
+vxm_status vxm_blocklist_assign(vxm_blocklist* l, const vxm_grid_index* data, uint64_t n) {
+  return guard([&] {
+    l->assign_host(data, n);
+    l->sorted_unique = false;
+  });
+}
+
+vxm_status vxm_layer_create(vxm_context* ctx, vxm_layer_type type, double vs, uint64_t max_blocks,
+                            vxm_layer** out) {
+  return guard([&] {
+    REQUIRE_ARG(ctx && out, "null argument");
+    if (!(vs > 0.0)) throw Error(VXM_ERR_INVALID_ARGUMENT, "Layer: voxel_size must be positive");
+    REQUIRE_ARG(type == VXM_LAYER_TSDF || type == VXM_LAYER_ESDF, "unknown layer type");
+    auto* L = new vxm_layer();
+    L->ctx = ctx;
+    L->type = type;
+    L->vs = vs;
+    L->max_blocks = max_blocks ? max_blocks : (uint64_t(1) << 30);
+    VXM_CUDA(cudaMalloc(&L->meta, sizeof(LayerMeta)));
+    VXM_CUDA(cudaMemset(L->meta, 0, sizeof(LayerMeta)));
+    if (type == VXM_LAYER_ESDF) {
+      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * 2));
+      VXM_CUDA(cudaMemset(L->dirty_count, 0, sizeof(uint32_t) * 2));
+    }
+    L->ensure_capacity(std::min<uint64_t>(4096, L->max_blocks));
+    *out = L;
+  });
+}
+void vxm_layer_destroy(vxm_layer* L) {
+  if (!L) return;
+  cudaStreamSynchronize(L->ctx->stream);
+  delete L;
+}
+double vxm_layer_voxel_size(const vxm_layer* L) { return L->vs; }
+vxm_status vxm_layer_num_blocks(vxm_layer* L, uint64_t* out) {
+  return guard([&] {
+    L->refresh();
+    *out = L->num_blocks;
+  });
+}
+vxm_status vxm_layer_has_blocks(vxm_layer* L, const vxm_grid_index* keys, uint64_t n, uint8_t* out) {
+  return guard([&] {
+    std::vector<int32_t> slots;
+    DevBuf ds;
+    lookup_host_keys(L, keys, n, &slots, &ds);
+    for (uint64_t i = 0; i < n; ++i) out[i] = slots[i] >= 0;
+  });
+}
+
+vxm_status vxm_layer_export(vxm_layer* L, vxm_grid_index* keys_out, void* voxels_out,
+                            uint64_t capacity) {
+  return guard([&] {
+    Context* ctx = L->ctx;
+    std::vector<uint64_t> keys;
+    std::vector<int32_t> slots;
+    layer_export_sorted(L, &keys, &slots);
+    const uint64_t n = keys.size();
+    REQUIRE_ARG(capacity >= n, "vxm_layer_export: capacity smaller than num_blocks");
+    for (uint64_t i = 0; i < n; ++i) keys_out[i] = {key_x(keys[i]), key_y(keys[i]), key_z(keys[i])};
+    if (voxels_out && n) {
+      const uint32_t bb = uint32_t(L->block_bytes());
+      DevBuf ds, dout;
+      ds.ensure(sizeof(int32_t) * n);
+      dout.ensure(size_t(bb) * n);
+      VXM_CUDA(cudaMemcpyAsync(ds.p, slots.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                               ctx->stream));
+      k_gather_blocks<<<grid1d(ctx, n * (bb / 4)), 256, 0, ctx->stream>>>(
+          static_cast<const unsigned char*>(L->cur_pool()), ds.as<int32_t>(), uint32_t(n), bb,
+          dout.as<unsigned char>());
+      ctx->count_launch();
+      check_launch(ctx, "k_gather_blocks");
+      VXM_CUDA(cudaMemcpyAsync(voxels_out, dout.p, size_t(bb) * n, cudaMemcpyDeviceToHost, ctx->stream));
+      VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  });
+}
+
+vxm_status vxm_layer_read_blocks(vxm_layer* L, const vxm_grid_index* keys, uint64_t n,
+                                 void* voxels_out, uint8_t* found) {
+  return guard([&] {
+    Context* ctx = L->ctx;
+    L->refresh();
+    std::vector<int32_t> slots;
+    DevBuf ds, dout;
+    lookup_host_keys(L, keys, n, &slots, &ds);
+    if (found)
+      for (uint64_t i = 0; i < n; ++i) found[i] = slots[i] >= 0;
+    if (!n || !voxels_out) return;
+    const uint32_t bb = uint32_t(L->block_bytes());
+    dout.ensure(size_t(bb) * n);
+    k_gather_blocks<<<grid1d(ctx, n * (bb / 4)), 256, 0, ctx->stream>>>(
+        static_cast<const unsigned char*>(L->cur_pool()), ds.as<int32_t>(), uint32_t(n), bb,
+        dout.as<unsigned char>());
+    ctx->count_launch();
+    check_launch(ctx, "k_gather_blocks");
+    VXM_CUDA(cudaMemcpyAsync(voxels_out, dout.p, size_t(bb) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+vxm_status vxm_layer_write_blocks(vxm_layer* L, const vxm_grid_index* keys, uint64_t n,
+                                  const void* voxels) {
+  return guard([&] {
+    Context* ctx = L->ctx;
+    if (!n) return;
+    // last write of a duplicated key wins (sequential get_or_allocate + copy)
+    std::map<std::tuple<int32_t, int32_t, int32_t>, uint64_t> last;
+    for (uint64_t i = 0; i < n; ++i) last[{keys[i].x, keys[i].y, keys[i].z}] = i;
+    std::vector<vxm_grid_index> uk;
+    std::vector<uint64_t> src;
+    for (const auto& kv : last) {
+      uk.push_back({std::get<0>(kv.first), std::get<1>(kv.first), std::get<2>(kv.first)});
+      src.push_back(kv.second);
+    }
+    L->refresh();
+    vxm_blocklist list;
+    list.ctx = ctx;
+    list.assign_host(uk.data(), uk.size());  // already sorted + unique (std::map order)
+    const uint32_t m = uint32_t(uk.size());
+    DevBuf dslots;
+    dslots.ensure(sizeof(int32_t) * m);
+    ctx->reset_status();
+    alloc_key_list(L, &list, dslots.as<int32_t>());
+    const uint32_t bb = uint32_t(L->block_bytes());
+    std::vector<unsigned char> packed(size_t(bb) * m);
+    for (uint32_t i = 0; i < m; ++i)
+      std::memcpy(packed.data() + size_t(i) * bb, static_cast<const unsigned char*>(voxels) + src[i] * bb, bb);
+    DevBuf din;
+    din.ensure(packed.size());
+    VXM_CUDA(cudaMemcpyAsync(din.p, packed.data(), packed.size(), cudaMemcpyHostToDevice, ctx->stream));
+    k_scatter_blocks<<<grid1d(ctx, uint64_t(m) * (bb / 4)), 256, 0, ctx->stream>>>(
+        static_cast<unsigned char*>(L->cur_pool()), dslots.as<int32_t>(), m, bb,
+        din.as<unsigned char>());
+    ctx->count_launch();
+    check_launch(ctx, "k_scatter_blocks");
+    ctx->sync_status();
+    L->refresh();
+    if (ctx->h_status->capacity_error || ctx->h_status->pool_overflow)
+      throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+  });
+}
+
+vxm_status vxm_layer_clone(vxm_layer* src, vxm_layer** out) {
+  return guard([&] {
+    src->refresh();
+    const uint64_t n = src->num_blocks;
+    std::vector<vxm_grid_index> keys(n);
+    std::vector<unsigned char> vox(n * src->block_bytes());
+    vxm_status s = vxm_layer_export(src, keys.data(), vox.data(), n);
+    if (s != VXM_OK) throw Error(s, g_err);
+    vxm_layer* L = nullptr;
+    s = vxm_layer_create(static_cast<vxm_context*>(src->ctx), vxm_layer_type(src->type), src->vs,
+                         src->max_blocks, &L);
+    if (s != VXM_OK) throw Error(s, g_err);
+    if (n) {
+      s = vxm_layer_write_blocks(L, keys.data(), n, vox.data());
+      if (s != VXM_OK) {
+        vxm_layer_destroy(L);
+        throw Error(s, g_err);
+      }
+    }
+    *out = L;
+  });
+}
+
+vxm_status vxm_blocks_in_view_camera(vxm_context* ctx, const vxm_pose* T, const vxm_camera* cam,
+                                     const float* depth, int w, int h, double block_size,
+                                     const vxm_view_config* cfg, vxm_blocklist* out) {
+  return guard([&] {
+    REQUIRE_ARG(ctx && T && cam && cfg && out, "null argument");
+    REQUIRE_ARG(block_size > 0.0, "block_size must be positive");
+    ViewArgs va{};
+    va.T_LS = *T;
+    va.lidar = false;
+    va.cam = *cam;
+    va.width = w;
+    va.height = h;
+    va.block_size = block_size;
+    va.cfg = *cfg;
+    stage_depth(ctx, depth, w, h, false, &va.depth_dev);
+    ctx->reset_status();
+    uint32_t cap = 0;
+    run_view(ctx, va, nullptr, &cap);
+    ctx->sync_status();
+    if (ctx->h_status->bitmap_overflow) throw Error(VXM_ERR_INTERNAL, "candidate bitmap overflow");
+    const uint32_t n = ctx->h_status->n_candidates;
+    out->ctx = ctx;
+    out->ensure(std::max<uint32_t>(n, 1));
+    VXM_CUDA(cudaMemcpyAsync(out->keys.p, ctx->cand_keys.p, sizeof(uint64_t) * n,
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    VXM_CUDA(cudaMemcpyAsync(out->d_count, &ctx->d_status->n_candidates, sizeof(uint32_t),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    out->host_valid = false;
+    out->count_hint = n;
+    out->sorted_unique = true;
+    out->fetch();
+  });
+}
+
+vxm_status vxm_blocks_in_view_lidar(vxm_context* ctx, const vxm_pose* T, const vxm_lidar* li,
+                                    const float* depth, int w, int h, double block_size,
+                                    const vxm_view_config* cfg, vxm_blocklist* out) {
+  return guard([&] {
+    REQUIRE_ARG(ctx && T && li && cfg && out, "null argument");
+    REQUIRE_ARG(block_size > 0.0, "block_size must be positive");
+    REQUIRE_ARG(w == li->num_azimuth && h == li->num_elevation,
+                "blocks_in_view: image size does not match intrinsics");
+    ViewArgs va{};
+    va.T_LS = *T;
+    va.lidar = true;
+    va.li = *li;
+    va.width = w;
+    va.height = h;
+    va.block_size = block_size;
+    va.cfg = *cfg;
+    stage_depth(ctx, depth, w, h, false, &va.depth_dev);
+    ctx->reset_status();
+    uint32_t cap = 0;
+    run_view(ctx, va, nullptr, &cap);
+    ctx->sync_status();
+    if (ctx->h_status->bitmap_overflow) throw Error(VXM_ERR_INTERNAL, "candidate bitmap overflow");
+    const uint32_t n = ctx->h_status->n_candidates;
+    out->ctx = ctx;
+    out->ensure(std::max<uint32_t>(n, 1));
+    VXM_CUDA(cudaMemcpyAsync(out->keys.p, ctx->cand_keys.p, sizeof(uint64_t) * n,
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    VXM_CUDA(cudaMemcpyAsync(out->d_count, &ctx->d_status->n_candidates, sizeof(uint32_t),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    out->host_valid = false;
+    out->count_hint = n;
+    out->sorted_unique = true;
+    out->fetch();
+  });
+}
+
+vxm_status vxm_integrate_depth_camera(vxm_layer* L, const float* depth, int w, int h,
+                                      const vxm_pose* T, const vxm_camera* cam,
+                                      const vxm_integrator_config* cfg, vxm_blocklist* out) {
+  return integrate_common(L, depth, w, h, T, cam, nullptr, cfg, out, false);
+}
+vxm_status vxm_integrate_depth_lidar(vxm_layer* L, const float* depth, int w, int h,
+                                     const vxm_pose* T, const vxm_lidar* li,
+                                     const vxm_integrator_config* cfg, vxm_blocklist* out) {
+  return integrate_common(L, depth, w, h, T, nullptr, li, cfg, out, false);
+}
+vxm_status vxm_integrate_depth_camera_device(vxm_layer* L, const float* depth, int w, int h,
+                                             const vxm_pose* T, const vxm_camera* cam,
+                                             const vxm_integrator_config* cfg, vxm_blocklist* out) {
+  return integrate_common(L, depth, w, h, T, cam, nullptr, cfg, out, true);
+}
+vxm_status vxm_integrate_depth_lidar_device(vxm_layer* L, const float* depth, int w, int h,
+                                            const vxm_pose* T, const vxm_lidar* li,
+                                            const vxm_integrator_config* cfg, vxm_blocklist* out) {
+  return integrate_common(L, depth, w, h, T, nullptr, li, cfg, out, true);
+}
+
+vxm_status vxm_update_esdf_list(vxm_layer* E, vxm_layer* T, vxm_blocklist* updated,
+                                const vxm_esdf_config* cfg, vxm_blocklist* out) {
+  return guard([&] {
+    REQUIRE_ARG(E && T && updated && cfg && out, "null argument");
+    REQUIRE_ARG(E->type == VXM_LAYER_ESDF && T->type == VXM_LAYER_TSDF,
+                "update_esdf: expects (ESDF layer, TSDF layer)");
+    out->ctx = E->ctx;
+    // esdf/integrator.cpp:371-378: empty input returns {} before the size check
+    if (updated->count_hint == 0 || (updated->host_valid && updated->host.empty())) {
+      out->assign_host(nullptr, 0);
+      out->sorted_unique = true;
+      return;
+    }
+    if (E->vs != T->vs)
+      throw Error(VXM_ERR_INVALID_ARGUMENT, "update_esdf: source and ESDF layer voxel sizes differ");
+    ensure_sorted_unique(updated);
+    run_update_esdf(E, T, updated, *cfg, out);
+    out->sorted_unique = true;
+  });
+}
+
+vxm_status vxm_update_esdf(vxm_layer* E, vxm_layer* T, const vxm_grid_index* updated, uint64_t n,
+                           const vxm_esdf_config* cfg, vxm_blocklist* out) {
+  return guard([&] {
+    REQUIRE_ARG(E && T && cfg && out, "null argument");
+    vxm_blocklist list;
+    list.ctx = E->ctx;
+    list.assign_host(updated, n);
+    const vxm_status s = vxm_update_esdf_list(E, T, &list, cfg, out);
+    if (s != VXM_OK) throw Error(s, g_err);
+    out->fetch();
+  });
+}
+
+vxm_status vxm_esdf_state_create(vxm_esdf_state** out) {
+  return guard([&] { *out = new vxm_esdf_state(); });
+}
+void vxm_esdf_state_destroy(vxm_esdf_state* st) { delete st; }
+vxm_status vxm_esdf_state_get(vxm_esdf_state* st, int which, const vxm_grid_index** data,
+                              uint64_t* n) {
+  return guard([&] {
+    REQUIRE_ARG(which >= 0 && which < 3, "state list index");
+    *data = st->lists[which].data();
+    *n = st->lists[which].size();
+  });
+}
+vxm_status vxm_esdf_state_set(vxm_esdf_state* st, int which, const vxm_grid_index* data, uint64_t n) {
+  return guard([&] {
+    REQUIRE_ARG(which >= 0 && which < 3, "state list index");
+    st->lists[which].assign(data, data + n);
+  });
+}
+
+vxm_status vxm_esdf_mark_sites(vxm_layer* E, vxm_layer* T, const vxm_grid_index* updated, uint64_t n,
+                               const vxm_esdf_config* cfg, vxm_esdf_state* st,
+                               vxm_blocklist* changed) {
+  return guard([&] {
+    REQUIRE_ARG(E && T && cfg && st && changed, "null argument");
+    std::vector<vxm_grid_index> ch;
+    if (n) {
+      vxm_blocklist list;
+      list.ctx = E->ctx;
+      list.assign_host(updated, n);
+      ensure_sorted_unique(&list);
+      run_mark_sites(E, T, &list, *cfg, st, &ch);
+    }
+    changed->ctx = E->ctx;
+    changed->assign_host(ch.data(), ch.size());
+  });
+}
+vxm_status vxm_esdf_clear_invalid(vxm_layer* E, const vxm_esdf_config* cfg, vxm_esdf_state* st,
+                                  vxm_blocklist* changed) {
+  return guard([&] {
+    std::vector<vxm_grid_index> ch;
+    run_clear_invalid(E, *cfg, st, &ch);
+    changed->ctx = E->ctx;
+    changed->assign_host(ch.data(), ch.size());
+  });
+}
+vxm_status vxm_esdf_lower(vxm_layer* E, vxm_esdf_state* st, const vxm_esdf_config* cfg,
+                          vxm_blocklist* changed, int* rounds) {
+  return guard([&] {
+    std::vector<vxm_grid_index> ch;
+    const int r = run_lower_esdf(E, st, *cfg, &ch);
+    if (rounds) *rounds = r;
+    changed->ctx = E->ctx;
+    changed->assign_host(ch.data(), ch.size());
+  });
+}
+
+vxm_status vxm_query_batch(vxm_layer* E, const double* xyz, uint64_t n, int want_gradient,
+                           const vxm_query_config* cfg, vxm_query_result* out) {
+  return guard([&] {
+    REQUIRE_ARG(E && cfg && (n == 0 || (xyz && out)), "null argument");
+    REQUIRE_ARG(E->type == VXM_LAYER_ESDF, "query_batch: expects an ESDF layer");
+    run_query(E, xyz, n, want_gradient, cfg->interpolate, out);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,1153 @@
+// ESDF update.
+//
+// Reference: proj/src/esdf/integrator.cpp — relax (:58-88), sweep_block
+// (:96-139), exchange_pair (:144-168), TsdfClassifier (:177-198), mark_impl
+// (:268-348), reset_parented (:352-363), update_impl (:365-413),
+// clear_invalid (:433-486), lower_esdf (:488-565).
+//
+// The reference's update is a full-map recompute whenever any site/side
+// changed: reset every parented voxel to saturation, then lower from ALL
+// blocks with its exact sweep/border schedule.  This file reproduces that
+// schedule bit-for-bit on the GPU:
+//   * mark: CTA per effective block (updated + allocated face neighbours).
+//     The effective set is a 7-way rank merge of the sorted updated list and
+//     its six axis-shifted copies (each shift preserves order), so it is
+//     produced sorted without a sort.
+//   * allocation: look-up + ordered slot assignment + hash insert in one
+//     look-back pass; the sorted set of all ESDF blocks is maintained by a
+//     rank merge (no sort); a 6-neighbour slot table serves the border phase.
+//   * lowering: ONE cooperative persistent kernel runs every round.  Sweeps:
+//     a 64-thread group per dirty block holds the block in shared memory
+//     (bank-conflict-free swizzled SoA), each thread owns one line per
+//     direction and runs the Gauss-Seidel X+/X- (Y, Z) passes in registers
+//     until the block's fixed point.  Borders: a warp per (dirty block, side)
+//     relaxes the 64 face pairs of each axis in turn (x, then y, then z), with
+//     grid-wide barriers between phases exactly where the reference has them.
+//     Round 1 reads the pre-update field and writes the other buffer (fused
+//     reset_parented + snapshot), so the changed set is a block compare of the
+//     two buffers — no O(map) snapshot copy.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "runtime.cuh"
+#include "scan.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace vxm {
+
+void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
+                         const uint32_t* n_ptr, uint32_t n_cap, uint64_t* out, uint32_t* n_out,
+                         const DevStatus* guard);
+
+// ---- voxel register form ---------------------------------------------------------
+struct EV {
+  int sq, px, py, pz;
+  uint32_t f;    // flags
+  uint32_t res;  // reserved byte (preserved)
+};
+__device__ inline EV ev_unpack(uint32_t w0, uint32_t w1, uint32_t w2) {
+  EV v;
+  v.sq = int(w0);
+  v.px = int(int16_t(w1 & 0xffffu));
+  v.py = int(int16_t(w1 >> 16));
+  v.pz = int(int16_t(w2 & 0xffffu));
+  v.f = (w2 >> 16) & 0xffu;
+  v.res = w2 >> 24;
+  return v;
+}
+__device__ inline uint32_t ev_w1(const EV& v) { return (uint32_t(v.px) & 0xffffu) | (uint32_t(v.py) << 16); }
+__device__ inline uint32_t ev_w2(const EV& v) {
+  return (uint32_t(v.pz) & 0xffffu) | (v.f << 16) | (v.res << 24);
+}
+__device__ inline bool ev_has_parent(const EV& v) { return (v.px | v.py | v.pz) != 0; }
+
+struct Limits {
+  int max_sq, cap_sq;
+};
+
+// relax — esdf/integrator.cpp:58-88
+__device__ inline bool relax(EV& v, const EV& u, int dx, int dy, int dz, const Limits& lim) {
+  if (!(u.f & VXM_ESDF_OBSERVED) || (!(u.f & VXM_ESDF_SITE) && !ev_has_parent(u))) return false;
+  if (!(v.f & VXM_ESDF_OBSERVED) || (v.f & VXM_ESDF_SITE)) return false;
+  const int cx = u.px - dx, cy = u.py - dy, cz = u.pz - dz;
+  const int cand = int(uint32_t(cx * cx) + uint32_t(cy * cy) + uint32_t(cz * cz));
+  if (cand == 0) return false;
+  const int limit = (v.f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq;
+  if (cand > limit || cand > v.sq) return false;
+  if (cand == v.sq && ev_has_parent(v)) {
+    const bool less = cx < v.px || (cx == v.px && (cy < v.py || (cy == v.py && cz < v.pz)));
+    if (!less) return false;
+  }
+  v.sq = cand;
+  v.px = int(int16_t(cx));
+  v.py = int(int16_t(cy));
+  v.pz = int(int16_t(cz));
+  return true;
+}
+
+__device__ inline void reset_to_saturated(EV& v, const Limits& lim) {
+  v.sq = (v.f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq;
+  v.px = v.py = v.pz = 0;
+}
+
+// Bank-conflict-free swizzle of the 512 voxels of a block:
+// bank = (x0^z0, x1^z1, x2^y2, y0^z0, y1^z1), high bits (x0, x1, y2, z2).  For
+// the X-, Y- and Z-line phases every warp's 32 accesses hit 32 distinct banks.
+__device__ inline int swz(int x, int y, int z) {
+  const int b0 = (x ^ z) & 1, b1 = ((x >> 1) ^ (z >> 1)) & 1, b2 = ((x >> 2) ^ (y >> 2)) & 1;
+  const int b3 = (y ^ z) & 1, b4 = ((y >> 1) ^ (z >> 1)) & 1;
+  return b0 | (b1 << 1) | (b2 << 2) | (b3 << 3) | (b4 << 4) | ((x & 1) << 5) | (((x >> 1) & 1) << 6) |
+         (((y >> 2) & 1) << 7) | (((z >> 2) & 1) << 8);
+}
+__device__ inline int swz_lin(int lin) { return swz(lin & 7, (lin >> 3) & 7, lin >> 6); }
+
+// Named barrier over one 64-thread group, with an OR reduction of `pred`.
+__device__ inline bool group_sync_or(int id, bool pred) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.s32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, 64, p;\n\t"
+      "selp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(int(pred)), "r"(id)
+      : "memory");
+  return r != 0;
+}
+__device__ inline void group_sync(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
+struct BlockSmem {
+  uint32_t w0[512], w1[512], w2[512];
+};
+
+// One line of 8 voxels along `axis` held in registers.
+template <int AXIS>
+__device__ inline bool sweep_line(BlockSmem& b, int t, const Limits& lim) {
+  // t in [0, 64): the two coordinates orthogonal to AXIS
+  const int c0 = t & 7, c1 = t >> 3;
+  EV v[8];
+  int idx[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int x = AXIS == 0 ? k : c0;
+    const int y = AXIS == 1 ? k : (AXIS == 0 ? c0 : c1);
+    const int z = AXIS == 2 ? k : c1;
+    idx[k] = swz(x, y, z);
+    v[k] = ev_unpack(b.w0[idx[k]], b.w1[idx[k]], b.w2[idx[k]]);
+  }
+  const int dx = AXIS == 0, dy = AXIS == 1, dz = AXIS == 2;
+  uint32_t ch = 0;
+#pragma unroll
+  for (int k = 1; k < 8; ++k)  // X+ (resp. Y+, Z+)
+    if (relax(v[k], v[k - 1], dx, dy, dz, lim)) ch |= 1u << k;
+#pragma unroll
+  for (int k = 6; k >= 0; --k)  // X- (resp. Y-, Z-)
+    if (relax(v[k], v[k + 1], -dx, -dy, -dz, lim)) ch |= 1u << k;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (ch & (1u << k)) {
+      b.w0[idx[k]] = uint32_t(v[k].sq);
+      b.w1[idx[k]] = ev_w1(v[k]);
+      b.w2[idx[k]] = ev_w2(v[k]);
+    }
+  return ch != 0;
+}
+
+// sweep_block — esdf/integrator.cpp:96-139, for one 64-thread group.
+__device__ inline bool sweep_block_group(BlockSmem& b, int t, int bar, const Limits& lim) {
+  bool block_changed = false;
+  while (true) {
+    bool c = sweep_line<0>(b, t, lim);
+    group_sync(bar);
+    c |= sweep_line<1>(b, t, lim);
+    group_sync(bar);
+    c |= sweep_line<2>(b, t, lim);
+    const bool pass_changed = group_sync_or(bar, c);
+    block_changed |= pass_changed;
+    if (!pass_changed) break;
+  }
+  return block_changed;
+}
+
+__device__ inline void load_block(BlockSmem& b, const uint32_t* __restrict__ src, int t) {
+#pragma unroll 4
+  for (int w = t; w < 1536; w += 64) {
+    const uint32_t val = __ldcg(src + w);
+    const int lin = w / 3, f = w - lin * 3;
+    const int s = swz_lin(lin);
+    if (f == 0) b.w0[s] = val;
+    else if (f == 1) b.w1[s] = val;
+    else b.w2[s] = val;
+  }
+}
+__device__ inline void store_block(const BlockSmem& b, uint32_t* __restrict__ dst, int t) {
+#pragma unroll 4
+  for (int w = t; w < 1536; w += 64) {
+    const int lin = w / 3, f = w - lin * 3;
+    const int s = swz_lin(lin);
+    __stcg(dst + w, f == 0 ? b.w0[s] : (f == 1 ? b.w1[s] : b.w2[s]));
+  }
+}
+
+// ---- cooperative lowering kernel ------------------------------------------------
+struct LowerArgs {
+  uint32_t* pool[2];
+  LayerMeta* meta;
+  const int32_t* nbr;
+  uint32_t* stamp_dirty[2];
+  uint32_t* stamp_lchg;
+  int32_t* list[2];
+  uint32_t* count;  // [2]
+  Limits lim;
+  int full;                    // 1: update_esdf (reset + all blocks, ping-pong)
+  const int32_t* seeds;        // seeded mode
+  const uint32_t* n_seeds;
+  DevStatus* status;
+  // changed-set output (full mode)
+  const int32_t* sorted_slots;
+  const uint32_t* stamp_new;
+  const uint32_t* stamp_mark;
+  uint32_t call_epoch;
+  uint32_t lchg_tag;
+  uint8_t* out_flags;
+};
+
+constexpr int kLowerThreads = 256;
+constexpr int kGroups = kLowerThreads / 64;
+
+__device__ inline const EV load_voxel(const uint32_t* pool, int32_t slot, int lin) {
+  const uint32_t* p = pool + size_t(slot) * 1536 + lin * 3;
+  return ev_unpack(__ldcg(p), __ldcg(p + 1), __ldcg(p + 2));
+}
+__device__ inline void store_voxel(uint32_t* pool, int32_t slot, int lin, const EV& v) {
+  uint32_t* p = pool + size_t(slot) * 1536 + lin * 3;
+  __stcg(p, uint32_t(v.sq));
+  __stcg(p + 1, ev_w1(v));
+  __stcg(p + 2, ev_w2(v));
+}
+
+__global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ BlockSmem s_blk[kGroups];
+  const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
+  const int lane = threadIdx.x & 31;
+  const int gid = blockIdx.x * kGroups + g, ngroups = gridDim.x * kGroups;
+  const int wid = (blockIdx.x * kLowerThreads + threadIdx.x) >> 5;
+  const int nwarps = gridDim.x * (kLowerThreads >> 5);
+  const uint32_t n_blocks = a.meta->num_blocks;
+  const uint32_t cur = a.meta->cur;
+  const uint32_t base_epoch = a.meta->round_epoch;
+  const bool failed = a.status->capacity_error || a.status->pool_overflow;
+  const bool lower = !failed && (a.full ? a.status->any_update != 0 : true);
+  uint32_t* const pcur = a.pool[cur];
+  uint32_t* const pnxt = a.pool[cur ^ 1u];
+  uint32_t* const work = a.full ? pnxt : pcur;
+  const Limits lim = a.lim;
+  // Seeded mode: round-1 dirty list = seeds (already filtered to existing).
+  if (!a.full && lower) {
+    const uint32_t ns = *a.n_seeds;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+      const int32_t s = a.seeds[i];
+      a.list[1][i] = s;
+      a.stamp_dirty[1][s] = base_epoch + 1;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.count[1] = ns;
+  }
+  grid.sync();
+  uint32_t r = 0;
+  // while (!dirty.empty()) — an empty round-1 set runs zero rounds (:506)
+  const uint32_t n_first = a.full ? n_blocks : *((volatile uint32_t*)&a.count[1]);
+  if (lower && n_first > 0) {
+    while (true) {
+      ++r;
+      const int cp = int(r & 1u), np = cp ^ 1;
+      const uint32_t ep = base_epoch + r, ep_next = ep + 1;
+      const bool r1_full = a.full && r == 1;
+      const uint32_t n_dirty = r1_full ? n_blocks : *((volatile uint32_t*)&a.count[cp]);
+      const int32_t* dirty = a.list[cp];
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.count[np] = 0;
+      // ---- sweep phase: every dirty block to its internal fixed point
+      for (uint32_t i = gid; i < n_dirty; i += ngroups) {
+        const int32_t s = r1_full ? int32_t(i) : dirty[i];
+        BlockSmem& b = s_blk[g];
+        load_block(b, (r1_full ? pcur : work) + size_t(s) * 1536, t);
+        group_sync(1 + g);
+        if (r1_full) {  // reset_parented — esdf/integrator.cpp:352-363
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int si = swz_lin(t + 64 * k);
+            EV v = ev_unpack(b.w0[si], b.w1[si], b.w2[si]);
+            if ((v.f & VXM_ESDF_OBSERVED) && !(v.f & VXM_ESDF_SITE) && ev_has_parent(v)) {
+              reset_to_saturated(v, lim);
+              b.w0[si] = uint32_t(v.sq);
+              b.w1[si] = ev_w1(v);
+              b.w2[si] = ev_w2(v);
+            }
+          }
+          group_sync(1 + g);
+        }
+        const bool changed = sweep_block_group(b, t, 1 + g, lim);
+        if (r1_full || changed) store_block(b, work + size_t(s) * 1536, t);
+        if (changed && !a.full && t == 0) a.stamp_lchg[s] = a.lchg_tag;
+        group_sync(1 + g);
+      }
+      grid.sync();
+      // ---- border phase, one axis group at a time (esdf/integrator.cpp:517-559)
+      for (int axis = 0; axis < 3; ++axis) {
+        const uint32_t items = 2u * n_dirty;
+        for (uint32_t w = wid; w < items; w += nwarps) {
+          const uint32_t i = w >> 1;
+          const int side = int(w & 1u);
+          const int32_t d = r1_full ? int32_t(i) : dirty[i];
+          int32_t lo, hi;
+          if (side == 0) {
+            hi = a.nbr[size_t(d) * 6 + 2 * axis];  // d + axis
+            lo = d;
+            if (hi < 0) continue;
+          } else {
+            lo = a.nbr[size_t(d) * 6 + 2 * axis + 1];  // d - axis
+            hi = d;
+            if (lo < 0) continue;
+            // the pair (lo, d) is emitted by lo's own side-0 item when lo is dirty
+            if (r1_full || __ldcg(a.stamp_dirty[cp] + lo) == ep) continue;
+          }
+          const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
+          bool ac = false, bc = false;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
+            int la, lb;
+            if (axis == 0) { la = 7 + 8 * i0 + 64 * j0; lb = 0 + 8 * i0 + 64 * j0; }
+            else if (axis == 1) { la = i0 + 8 * 7 + 64 * j0; lb = i0 + 64 * j0; }
+            else { la = i0 + 8 * j0 + 64 * 7; lb = i0 + 8 * j0; }
+            EV va = load_voxel(work, lo, la), vb = load_voxel(work, hi, lb);
+            const bool cb = relax(vb, va, dx, dy, dz, lim);   // exchange_pair :158
+            const bool ca = relax(va, vb, -dx, -dy, -dz, lim);  // :159
+            if (cb) store_voxel(work, hi, lb, vb);
+            if (ca) store_voxel(work, lo, la, va);
+            ac |= ca;
+            bc |= cb;
+          }
+          ac = __any_sync(0xffffffffu, ac);
+          bc = __any_sync(0xffffffffu, bc);
+          if (lane == 0) {
+            const int32_t who[2] = {lo, hi};
+            const bool chg[2] = {ac, bc};
+            for (int q = 0; q < 2; ++q) {
+              if (!chg[q]) continue;
+              if (!a.full) a.stamp_lchg[who[q]] = a.lchg_tag;
+              if (atomicMax(a.stamp_dirty[np] + who[q], ep_next) < ep_next) {
+                const uint32_t slot = atomicAdd(a.count + np, 1u);
+                a.list[np][slot] = who[q];
+              }
+            }
+          }
+        }
+        grid.sync();
+      }
+      if (*((volatile uint32_t*)&a.count[np]) == 0) break;
+    }
+  }
+  // ---- changed set of update_esdf (esdf/integrator.cpp:403-411) -------------
+  if (a.full) {
+    const uint32_t n = n_blocks;
+    for (uint32_t k = wid; k < n; k += nwarps) {
+      const int32_t s = a.sorted_slots[k];
+      bool ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
+      if (!ch && lower) {
+        const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(s) * 1536);
+        const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(s) * 1536);
+        bool diff = false;
+#pragma unroll 4
+        for (int q = lane; q < 384; q += 32) {
+          const uint4 x = __ldcg(p0 + q), y = __ldcg(p1 + q);
+          diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+        }
+        ch = __any_sync(0xffffffffu, diff);
+      }
+      if (lane == 0) a.out_flags[k] = uint8_t(ch);
+    }
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.status->rounds = r;
+    a.meta->round_epoch = base_epoch + r + 2;
+    if (a.full && lower) a.meta->cur = cur ^ 1u;
+  }
+}
+
+// ---- effective set: 7-way rank merge -------------------------------------------
+__device__ inline uint32_t lower_bound_u64(const uint64_t* a, uint32_t n, uint64_t k) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__device__ inline uint32_t upper_bound_u64(const uint64_t* a, uint32_t n, uint64_t k) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] <= k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+// shift j: 0 identity, 1 +x, 2 -x, 3 +y, 4 -y, 5 +z, 6 -z (mark_impl :279-285)
+__device__ inline uint64_t shift7(uint64_t k, int j, int sign) {
+  if (j == 0) return k;
+  const int axis = (j - 1) >> 1;
+  const int s = ((j - 1) & 1) ? -1 : 1;
+  return key_shift(k, axis, s * sign);
+}
+
+__global__ void k_merge7(const uint64_t* __restrict__ upd, const uint32_t* n_ptr,
+                         uint64_t* __restrict__ merged) {
+  const uint32_t n = *n_ptr;
+  const uint32_t total = 7u * n;
+  for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < total;
+       it += gridDim.x * blockDim.x) {
+    const int j = int(it / n);
+    const uint32_t i = it - uint32_t(j) * n;
+    const uint64_t key = shift7(upd[i], j, 1);
+    uint32_t rank = i;
+    for (int q = 0; q < 7; ++q) {
+      if (q == j) continue;
+      const uint64_t probe = shift7(key, q, -1);
+      rank += q < j ? upper_bound_u64(upd, n, probe) : lower_bound_u64(upd, n, probe);
+    }
+    merged[rank] = key;
+  }
+}
+
+// unique + has_block(TSDF) + compaction -> effective keys + TSDF slots.
+__global__ void __launch_bounds__(256) k_select_effective(const uint64_t* __restrict__ merged,
+                                                          const uint32_t* n_upd, HashView tsdf,
+                                                          uint64_t* __restrict__ eff_keys,
+                                                          int32_t* __restrict__ eff_tslot,
+                                                          uint32_t* n_eff, ScanTiles st) {
+  __shared__ uint32_t s_tile, s_scan[64], s_pre;
+  scan_prepare_next(st);
+  const uint32_t n = 7u * (*n_upd);
+  const uint32_t tiles = (n + blockDim.x - 1) / blockDim.x;
+  if (tiles == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_eff = 0;
+    return;
+  }
+  while (true) {
+    const uint32_t tile = scan_take_tile(st, &s_tile);
+    if (tile >= tiles) break;
+    const uint32_t r = tile * blockDim.x + threadIdx.x;
+    bool keep = false;
+    int32_t ts = -1;
+    uint64_t k = 0;
+    if (r < n) {
+      k = merged[r];
+      if (r == 0 || merged[r - 1] != k) {
+        ts = hash_find(tsdf, k);
+        keep = ts >= 0;
+      }
+    }
+    uint32_t ea, eb, ta, tb;
+    block_scan2(keep ? 1u : 0u, 0u, ea, eb, ta, tb, s_scan);
+    if (threadIdx.x == 0) {
+      uint32_t pa, pb;
+      scan_lookback(st, tile, ta, 0u, pa, pb);
+      s_pre = pa;
+      if (tile == tiles - 1) *n_eff = pa + ta;
+    }
+    __syncthreads();
+    if (keep) {
+      eff_keys[s_pre + ea] = k;
+      eff_tslot[s_pre + ea] = ts;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- get_or_allocate over a sorted key list --------------------------------------
+struct AllocListArgs {
+  const uint64_t* keys;
+  const uint32_t* n_ptr;
+  HashView hash;
+  uint64_t* slot_keys;
+  LayerMeta* meta;
+  uint32_t capacity;
+  uint64_t max_blocks;
+  int32_t* slots_out;      // per key: slot, or -1 when capacity was exhausted
+  uint64_t* new_keys;      // sorted new keys
+  int32_t* new_slots;
+  uint32_t* n_new_out;
+  uint32_t* n_old_out;     // num_blocks before this allocation
+  uint32_t* stamp_new;     // may be null
+  uint32_t call_epoch;
+  DevStatus* status;
+};
+
+__global__ void __launch_bounds__(256) k_alloc_list(AllocListArgs a, ScanTiles st) {
+  __shared__ uint32_t s_tile, s_scan[64], s_pre[2], s_base;
+  scan_prepare_next(st);
+  const uint32_t n = *a.n_ptr;
+  const uint32_t tiles = (n + blockDim.x - 1) / blockDim.x;
+  if (tiles == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *a.n_new_out = 0;
+      *a.n_old_out = a.meta->num_blocks;
+    }
+    return;
+  }
+  const uint64_t limit = a.capacity < a.max_blocks ? uint64_t(a.capacity) : a.max_blocks;
+  while (true) {
+    const uint32_t tile = scan_take_tile(st, &s_tile);
+    if (tile >= tiles) break;
+    if (threadIdx.x == 0) s_base = a.meta->num_blocks;
+    const uint32_t i = tile * blockDim.x + threadIdx.x;
+    uint64_t k = 0;
+    int32_t found = -1;
+    bool is_new = false;
+    if (i < n) {
+      k = a.keys[i];
+      found = hash_find_rw(a.hash, k);
+      is_new = found < 0;
+    }
+    uint32_t ea, eb, ta, tb;
+    block_scan2(is_new ? 1u : 0u, 0u, ea, eb, ta, tb, s_scan);
+    if (threadIdx.x == 0) {
+      uint32_t pa, pb;
+      scan_lookback(st, tile, ta, 0u, pa, pb);
+      s_pre[0] = pa;
+    }
+    __syncthreads();
+    const uint32_t base = s_base;
+    if (i < n) {
+      int32_t slot = found;
+      if (is_new) {
+        const uint32_t r = s_pre[0] + ea;
+        const uint64_t s = uint64_t(base) + r;
+        if (s < limit) {
+          hash_insert(a.hash, k, int32_t(s));
+          a.slot_keys[s] = k;
+          slot = int32_t(s);
+          a.new_keys[r] = k;
+          a.new_slots[r] = slot;
+          if (a.stamp_new) a.stamp_new[s] = a.call_epoch;
+        } else {
+          slot = -1;
+        }
+      }
+      a.slots_out[i] = slot;
+    }
+    if (threadIdx.x == 0 && tile == tiles - 1) {
+      const uint32_t total = s_pre[0] + ta;
+      const uint64_t want = uint64_t(base) + total;
+      const uint64_t got = want < limit ? want : limit;
+      *a.n_new_out = uint32_t(got - base);
+      *a.n_old_out = base;
+      if (want > a.capacity && a.capacity < a.max_blocks) a.status->pool_overflow = 1u;
+      if (want > a.max_blocks) a.status->capacity_error = 1u;
+      a.meta->num_blocks = uint32_t(got);
+    }
+    __syncthreads();
+  }
+}
+
+// 6-neighbour table of new ESDF blocks (both directions).
+__global__ void k_nbr_update(const uint64_t* __restrict__ new_keys,
+                             const int32_t* __restrict__ new_slots, const uint32_t* n_ptr,
+                             HashView h, int32_t* nbr) {
+  const uint32_t n = *n_ptr;
+  for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < 6u * n;
+       it += gridDim.x * blockDim.x) {
+    const uint32_t i = it / 6;
+    const int d = int(it - i * 6);
+    const int axis = d >> 1, s = (d & 1) ? -1 : 1;
+    const int32_t me = new_slots[i];
+    const int32_t nb = hash_find(h, key_shift(new_keys[i], axis, s));
+    nbr[size_t(me) * 6 + d] = nb;
+    if (nb >= 0) nbr[size_t(nb) * 6 + (d ^ 1)] = me;
+  }
+}
+
+// Sorted set of all blocks += new (sorted, disjoint) by rank merge.
+__global__ void k_merge_sorted(const uint64_t* __restrict__ ok, const int32_t* __restrict__ os,
+                               const uint32_t* n_old_ptr, const uint64_t* __restrict__ nk,
+                               const int32_t* __restrict__ ns, const uint32_t* n_new_ptr,
+                               uint64_t* __restrict__ out_k, int32_t* __restrict__ out_s) {
+  const uint32_t n_old = *n_old_ptr, n_new = *n_new_ptr;
+  for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < n_old + n_new;
+       it += gridDim.x * blockDim.x) {
+    if (it < n_old) {
+      const uint64_t k = ok[it];
+      const uint32_t r = it + lower_bound_u64(nk, n_new, k);
+      out_k[r] = k;
+      out_s[r] = os[it];
+    } else {
+      const uint32_t j = it - n_old;
+      const uint64_t k = nk[j];
+      const uint32_t r = j + lower_bound_u64(ok, n_old, k);
+      out_k[r] = k;
+      out_s[r] = ns[j];
+    }
+  }
+}
+
+// ---- mark_sites (TSDF source) — esdf/integrator.cpp:177-198, 268-348 ------------
+struct MarkArgs {
+  const uint64_t* eff_keys;
+  const int32_t* eff_tslot;
+  const int32_t* eff_eslot;
+  const uint32_t* n_eff;
+  const float2* tsdf_pool;
+  uint32_t* pools[2];
+  const LayerMeta* meta;
+  float site_threshold;
+  Limits lim;
+  uint32_t* stamp_mark;
+  uint32_t call_epoch;
+  uint8_t* flags;  // per effective block: 1 changed, 2 to_update, 4 to_clear
+  DevStatus* status;
+};
+
+__global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
+  const uint32_t n = *a.n_eff;
+  uint32_t* pool = a.pools[a.meta->cur];
+  for (uint32_t e = blockIdx.x; e < n; e += gridDim.x) {
+    const int32_t es = a.eff_eslot[e];
+    if (es < 0) {  // capacity exhausted before this block (MapCapacityError)
+      if (threadIdx.x == 0) a.flags[e] = 0;
+      continue;
+    }
+    const int32_t ts = a.eff_tslot[e];
+    bool bch = false, bup = false, bcl = false;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int lin = threadIdx.x + 256 * k;
+      const float2 tv = a.tsdf_pool[size_t(ts) * kVPB + lin];
+      const bool observed = tv.y > 0.0f;
+      const bool site = observed && fabsf(tv.x) <= a.site_threshold;
+      const bool inside = observed && tv.x < 0.0f;
+      uint32_t* p = pool + size_t(es) * 1536 + lin * 3;
+      const uint32_t o0 = p[0], o1 = p[1], o2 = p[2];
+      const EV ev = ev_unpack(o0, o1, o2);
+      EV nv = ev;
+      if (!observed) {
+        if (ev.f & VXM_ESDF_SITE) bcl = true;
+        nv = EV{0, 0, 0, 0, 0u, 0u};
+      } else {
+        nv.f = VXM_ESDF_OBSERVED | (site ? VXM_ESDF_SITE : 0) | (inside ? VXM_ESDF_INSIDE : 0);
+        const bool was_obs = ev.f & VXM_ESDF_OBSERVED, was_site = ev.f & VXM_ESDF_SITE;
+        if (site) {
+          nv.sq = 0;
+          nv.px = nv.py = nv.pz = 0;
+          if (!was_obs || !was_site) bup = true;
+        } else if (!was_obs) {
+          reset_to_saturated(nv, a.lim);
+          bup = true;
+        } else if (was_site) {
+          reset_to_saturated(nv, a.lim);
+          bcl = true;
+          bup = true;
+        } else if (bool(ev.f & VXM_ESDF_INSIDE) != inside) {
+          reset_to_saturated(nv, a.lim);
+          bup = true;
+        }
+      }
+      const uint32_t n0 = uint32_t(nv.sq), n1 = ev_w1(nv), n2 = ev_w2(nv);
+      if (n0 != o0 || n1 != o1 || n2 != o2) {
+        p[0] = n0;
+        p[1] = n1;
+        p[2] = n2;
+        bch = true;
+      }
+    }
+    bch = __syncthreads_or(bch);
+    bup = __syncthreads_or(bup);
+    bcl = __syncthreads_or(bcl);
+    if (threadIdx.x == 0) {
+      a.flags[e] = uint8_t((bch ? 1 : 0) | (bup ? 2 : 0) | (bcl ? 4 : 0));
+      if (bch) a.stamp_mark[es] = a.call_epoch;
+      if (bup || bcl) atomicOr(&a.status->any_update, 1u);
+    }
+  }
+}
+
+// ---- clear_invalid — esdf/integrator.cpp:433-486 --------------------------------
+struct ClearArgs {
+  const uint64_t* sorted_keys;
+  const int32_t* sorted_slots;
+  uint32_t n_all;
+  const uint64_t* clear_keys;
+  uint32_t n_clear;
+  int radius;
+  HashView hash;
+  uint32_t* pool;
+  Limits lim;
+  uint8_t* flags;  // per sorted index: 1 = cleared something
+};
+
+__device__ inline int64_t floor_div8(int64_t a) { return a >= 0 ? a / 8 : -((-a + 7) / 8); }
+
+__global__ void __launch_bounds__(256) k_clear(ClearArgs a) {
+  __shared__ int s_scan;
+  for (uint32_t k = blockIdx.x; k < a.n_all; k += gridDim.x) {
+    const uint64_t key = a.sorted_keys[k];
+    const int32_t gx = key_x(key), gy = key_y(key), gz = key_z(key);
+    if (threadIdx.x == 0) s_scan = 0;
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < a.n_clear; c += blockDim.x) {
+      const uint64_t ck = a.clear_keys[c];
+      if (abs(gx - key_x(ck)) <= a.radius && abs(gy - key_y(ck)) <= a.radius &&
+          abs(gz - key_z(ck)) <= a.radius)
+        s_scan = 1;
+    }
+    __syncthreads();
+    const bool scan = s_scan != 0;
+    bool any = false;
+    if (scan) {
+      const int32_t s = a.sorted_slots[k];
+      for (int q = 0; q < 2; ++q) {
+        const int lin = threadIdx.x + 256 * q;
+        uint32_t* p = a.pool + size_t(s) * 1536 + lin * 3;
+        EV v = ev_unpack(p[0], p[1], p[2]);
+        if (!ev_has_parent(v)) continue;
+        const int64_t px = int64_t(gx) * 8 + (lin & 7) + v.px;
+        const int64_t py = int64_t(gy) * 8 + ((lin >> 3) & 7) + v.py;
+        const int64_t pz = int64_t(gz) * 8 + (lin >> 6) + v.pz;
+        const int64_t bx = floor_div8(px), by = floor_div8(py), bz = floor_div8(pz);
+        bool parent_site = false;
+        if (coord_ok(bx) && coord_ok(by) && coord_ok(bz)) {
+          const int32_t ps = hash_find(a.hash, pack_key(int32_t(bx), int32_t(by), int32_t(bz)));
+          if (ps >= 0) {
+            const int plin = int(px - bx * 8) + 8 * int(py - by * 8) + 64 * int(pz - bz * 8);
+            const uint32_t w2 = a.pool[size_t(ps) * 1536 + plin * 3 + 2];
+            parent_site = ((w2 >> 16) & VXM_ESDF_SITE) != 0;
+          }
+        }
+        if (!parent_site) {
+          // only clears parents; reads above only test site bits (never written)
+          reset_to_saturated(v, a.lim);
+          p[0] = uint32_t(v.sq);
+          p[1] = ev_w1(v);
+          p[2] = ev_w2(v);
+          any = true;
+        }
+      }
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) a.flags[k] = uint8_t(any);
+  }
+}
+
+// Flag blocks (in sorted order) whose lowering-change tag matches.
+__global__ void k_flag_tag(const int32_t* sorted_slots, uint32_t n, const uint32_t* stamp,
+                           uint32_t tag, uint8_t* flags) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    flags[k] = uint8_t(stamp[sorted_slots[k]] == tag);
+}
+
+__global__ void k_lookup_slots(const uint64_t* keys, uint32_t n, HashView h, int32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = hash_find(h, keys[i]);
+}
+
+// ---- host drivers -----------------------------------------------------------------
+static Limits limits_for(const vxm_esdf_config& cfg, double vs) {
+  const double r = cfg.max_distance / vs;  // esdf/integrator.hpp:43-54
+  Limits l;
+  l.max_sq = int32_t(std::llround(r * r));
+  l.cap_sq = l.max_sq < 16 ? l.max_sq : 16;
+  return l;
+}
+
+static uint32_t grid_for(Context* ctx, uint64_t n, int per_sm = 8) {
+  return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(std::max<uint64_t>(n, 1), 256),
+                                                           uint64_t(ctx->sm_count) * per_sm)));
+}
+
+// Scratch layout for one ESDF call (ctx->tmp[...]).
+struct EsdfScratch {
+  uint64_t* merged;
+  uint64_t* eff_keys;
+  int32_t* eff_tslot;
+  int32_t* eff_eslot;
+  uint64_t* new_keys;
+  int32_t* new_slots;
+  uint8_t* flags;
+  uint32_t* counts;  // [0] n_eff, [1] n_new, [2] n_old, [3] n_out, [4..] misc
+};
+
+static EsdfScratch esdf_scratch(Context* ctx, uint32_t n_upd_cap, uint32_t n_all_cap) {
+  const uint64_t n7 = 7ull * std::max<uint32_t>(n_upd_cap, 1);
+  const uint64_t nf = std::max<uint64_t>(n7, n_all_cap) + 16;
+  ctx->tmp[0].ensure(sizeof(uint64_t) * n7);
+  ctx->tmp[1].ensure(sizeof(uint64_t) * n7);
+  ctx->tmp[2].ensure(sizeof(int32_t) * n7 * 2);
+  ctx->tmp[3].ensure(sizeof(uint64_t) * n7);
+  ctx->tmp[4].ensure(sizeof(int32_t) * n7 + nf);
+  ctx->tmp[5].ensure(64 * sizeof(uint32_t));
+  EsdfScratch s;
+  s.merged = ctx->tmp[0].as<uint64_t>();
+  s.eff_keys = ctx->tmp[1].as<uint64_t>();
+  s.eff_tslot = ctx->tmp[2].as<int32_t>();
+  s.eff_eslot = s.eff_tslot + n7;
+  s.new_keys = ctx->tmp[3].as<uint64_t>();
+  s.new_slots = ctx->tmp[4].as<int32_t>();
+  s.flags = reinterpret_cast<uint8_t*>(s.new_slots + n7);
+  s.counts = ctx->tmp[5].as<uint32_t>();
+  return s;
+}
+
+// effective set + ESDF allocation + neighbour table + sorted-set merge + mark.
+// `updated` must hold sorted unique keys (device).  Returns the upper bound of
+// the effective count.
+static uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
+                                const vxm_esdf_config& cfg, EsdfScratch& s, uint32_t epoch) {
+  Context* ctx = E->ctx;
+  const uint32_t nu_cap = std::max<uint32_t>(updated->count_hint, 1);
+  const uint32_t n7 = 7u * nu_cap;
+  const uint64_t* upd = updated->keys.as<uint64_t>();
+  k_merge7<<<grid_for(ctx, n7), 256, 0, ctx->stream>>>(upd, updated->d_count, s.merged);
+  ctx->count_launch();
+  {
+    const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
+    k_select_effective<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(
+        s.merged, updated->d_count, T->hash, s.eff_keys, s.eff_tslot, s.counts + 0, st);
+    ctx->count_launch();
+  }
+  {
+    AllocListArgs al{};
+    al.keys = s.eff_keys;
+    al.n_ptr = s.counts + 0;
+    al.hash = E->hash;
+    al.slot_keys = E->slot_keys;
+    al.meta = E->meta;
+    al.capacity = E->capacity;
+    al.max_blocks = E->max_blocks;
+    al.slots_out = s.eff_eslot;
+    al.new_keys = s.new_keys;
+    al.new_slots = s.new_slots;
+    al.n_new_out = s.counts + 1;
+    al.n_old_out = s.counts + 2;
+    al.stamp_new = E->stamp_new;
+    al.call_epoch = epoch;
+    al.status = ctx->d_status;
+    const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
+    k_alloc_list<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(al, st);
+    ctx->count_launch();
+  }
+  k_nbr_update<<<grid_for(ctx, 6ull * n7), 256, 0, ctx->stream>>>(s.new_keys, s.new_slots,
+                                                                 s.counts + 1, E->hash, E->nbr);
+  const int sp = E->sorted_parity;
+  k_merge_sorted<<<grid_for(ctx, uint64_t(E->num_blocks) + n7), 256, 0, ctx->stream>>>(
+      E->sorted_keys[sp], E->sorted_slots[sp], s.counts + 2, s.new_keys, s.new_slots, s.counts + 1,
+      E->sorted_keys[1 - sp], E->sorted_slots[1 - sp]);
+  E->sorted_parity = 1 - sp;
+  MarkArgs m{};
+  m.eff_keys = s.eff_keys;
+  m.eff_tslot = s.eff_tslot;
+  m.eff_eslot = s.eff_eslot;
+  m.n_eff = s.counts + 0;
+  m.tsdf_pool = static_cast<const float2*>(T->pool[0]);
+  m.pools[0] = static_cast<uint32_t*>(E->pool[0]);
+  m.pools[1] = static_cast<uint32_t*>(E->pool[1]);
+  m.meta = E->meta;
+  m.site_threshold = float(cfg.site_threshold);
+  m.lim = limits_for(cfg, E->vs);
+  m.stamp_mark = E->stamp_mark;
+  m.call_epoch = epoch;
+  m.flags = s.flags;
+  m.status = ctx->d_status;
+  k_mark<<<std::max<uint32_t>(1, std::min<uint32_t>(n7, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(m);
+  ctx->count_launch(3);
+  check_launch(ctx, "esdf mark phase");
+  return n7;
+}
+
+static int lower_grid(Context* ctx) {
+  static int cached = -1;
+  if (cached < 0) {
+    int bps = 0;
+    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lower, kLowerThreads, 0));
+    cached = std::max(1, std::min(bps, 4)) * ctx->sm_count;
+  }
+  return cached;
+}
+
+static void launch_lower(Context* ctx, LowerArgs& la) {
+  void* args[] = {&la};
+  const int grid = lower_grid(ctx);
+  VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lower, dim3(grid), dim3(kLowerThreads), args, 0,
+                                       ctx->stream));
+  ctx->count_launch();
+}
+
+static LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
+  LowerArgs la{};
+  la.pool[0] = static_cast<uint32_t*>(E->pool[0]);
+  la.pool[1] = static_cast<uint32_t*>(E->pool[1]);
+  la.meta = E->meta;
+  la.nbr = E->nbr;
+  la.stamp_dirty[0] = E->stamp_dirty[0];
+  la.stamp_dirty[1] = E->stamp_dirty[1];
+  la.stamp_lchg = E->stamp_lchg;
+  la.list[0] = E->dirty_list[0];
+  la.list[1] = E->dirty_list[1];
+  la.count = E->dirty_count;
+  la.lim = limits_for(cfg, E->vs);
+  la.status = E->ctx->d_status;
+  return la;
+}
+
+void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
+                     BlockList* changed_out) {
+  Context* ctx = E->ctx;
+  const uint32_t epoch = ++ctx->call_epoch;
+  ctx->reset_status();
+  E->refresh();
+  const uint32_t n7 = 7u * std::max<uint32_t>(updated->count_hint, 1);
+  // capacity for every effective block (bounded by the logical limit)
+  E->ensure_capacity(std::min<uint64_t>(uint64_t(E->num_blocks) + n7, E->max_blocks));
+  const uint32_t n_all_cap = E->capacity;
+  EsdfScratch s = esdf_scratch(ctx, updated->count_hint, n_all_cap);
+  esdf_mark_phase(E, T, updated, cfg, s, epoch);
+  LowerArgs la = lower_args(E, cfg);
+  la.full = 1;
+  la.sorted_slots = E->sorted_slots[E->sorted_parity];
+  la.stamp_new = E->stamp_new;
+  la.stamp_mark = E->stamp_mark;
+  la.call_epoch = epoch;
+  la.out_flags = s.flags;
+  launch_lower(ctx, la);
+  check_launch(ctx, "k_lower");
+  changed_out->ensure(n_all_cap);
+  launch_compact_keys(ctx, E->sorted_keys[E->sorted_parity], s.flags, &E->meta->num_blocks,
+                      n_all_cap, changed_out->keys.as<uint64_t>(), changed_out->d_count, nullptr);
+  changed_out->host_valid = false;
+  changed_out->count_hint = n_all_cap;
+  ctx->sync_status();
+  E->refresh();
+  if (ctx->h_status->capacity_error || ctx->h_status->pool_overflow)
+    throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+}
+
+static void append_sorted_unique(std::vector<vxm_grid_index>& dst,
+                                 const std::vector<vxm_grid_index>& add) {
+  dst.insert(dst.end(), add.begin(), add.end());
+  auto less = [](const vxm_grid_index& a, const vxm_grid_index& b) {
+    return a.x != b.x ? a.x < b.x : (a.y != b.y ? a.y < b.y : a.z < b.z);
+  };
+  auto eq = [](const vxm_grid_index& a, const vxm_grid_index& b) {
+    return a.x == b.x && a.y == b.y && a.z == b.z;
+  };
+  std::sort(dst.begin(), dst.end(), less);
+  dst.erase(std::unique(dst.begin(), dst.end(), eq), dst.end());
+}
+
+static std::vector<vxm_grid_index> compact_to_host(Context* ctx, const uint64_t* keys,
+                                                   const uint8_t* flags, const uint32_t* n_ptr,
+                                                   uint32_t cap) {
+  BlockList tmp;
+  tmp.ctx = ctx;
+  tmp.ensure(std::max<uint32_t>(cap, 1));
+  launch_compact_keys(ctx, keys, flags, n_ptr, cap, tmp.keys.as<uint64_t>(), tmp.d_count, nullptr);
+  tmp.host_valid = false;
+  return tmp.fetch();
+}
+
+__global__ void k_flags_bit(const uint8_t* in, const uint32_t* n_ptr, uint8_t bit, uint8_t* out) {
+  const uint32_t n = *n_ptr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = (in[i] & bit) ? 1 : 0;
+}
+
+void run_mark_sites(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
+                    EsdfState* st, std::vector<vxm_grid_index>* changed) {
+  Context* ctx = E->ctx;
+  const uint32_t epoch = ++ctx->call_epoch;
+  ctx->reset_status();
+  E->refresh();
+  E->ensure_capacity(std::min<uint64_t>(
+      uint64_t(E->num_blocks) + 7ull * std::max<uint32_t>(updated->count_hint, 1), E->max_blocks));
+  EsdfScratch s = esdf_scratch(ctx, updated->count_hint, 0);
+  const uint32_t n7 = esdf_mark_phase(E, T, updated, cfg, s, epoch);
+  DevBuf bits;
+  bits.ensure(n7 + 16);
+  const char* names[3] = {"changed", "to_update", "to_clear"};
+  std::vector<vxm_grid_index> out[3];
+  for (int b = 0; b < 3; ++b) {
+    k_flags_bit<<<grid_for(ctx, n7), 256, 0, ctx->stream>>>(s.flags, s.counts + 0, uint8_t(1 << b),
+                                                          bits.as<uint8_t>());
+    ctx->count_launch();
+    out[b] = compact_to_host(ctx, s.eff_keys, bits.as<uint8_t>(), s.counts + 0, n7);
+    (void)names;
+  }
+  bits.release();
+  ctx->sync_status();
+  E->refresh();
+  changed->insert(changed->end(), out[0].begin(), out[0].end());
+  append_sorted_unique(st->lists[0], out[1]);
+  append_sorted_unique(st->lists[1], out[2]);
+  if (ctx->h_status->capacity_error || ctx->h_status->pool_overflow)
+    throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+}
+
+void esdf_sorted_export(Layer* E, std::vector<uint64_t>* keys, std::vector<int32_t>* slots) {
+  Context* ctx = E->ctx;
+  const uint32_t n = E->num_blocks;
+  keys->resize(n);
+  slots->resize(n);
+  if (!n) return;
+  VXM_CUDA(cudaMemcpyAsync(keys->data(), E->sorted_keys[E->sorted_parity], sizeof(uint64_t) * n,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  VXM_CUDA(cudaMemcpyAsync(slots->data(), E->sorted_slots[E->sorted_parity], sizeof(int32_t) * n,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void run_clear_invalid(Layer* E, const vxm_esdf_config& cfg, EsdfState* st,
+                       std::vector<vxm_grid_index>* changed) {
+  if (st->lists[1].empty()) return;  // esdf/integrator.cpp:435-437
+  Context* ctx = E->ctx;
+  E->refresh();
+  const uint32_t n_all = E->num_blocks;
+  std::vector<uint64_t> ck(st->lists[1].size());
+  for (size_t i = 0; i < ck.size(); ++i)
+    ck[i] = pack_key(st->lists[1][i].x, st->lists[1][i].y, st->lists[1][i].z);
+  DevBuf dck, dflags, dn;
+  dck.ensure(sizeof(uint64_t) * ck.size());
+  dflags.ensure(n_all + 16);
+  dn.ensure(sizeof(uint32_t));
+  VXM_CUDA(cudaMemcpyAsync(dck.p, ck.data(), sizeof(uint64_t) * ck.size(), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  VXM_CUDA(cudaMemcpyAsync(dn.p, &n_all, sizeof n_all, cudaMemcpyHostToDevice, ctx->stream));
+  ClearArgs a{};
+  a.sorted_keys = E->sorted_keys[E->sorted_parity];
+  a.sorted_slots = E->sorted_slots[E->sorted_parity];
+  a.n_all = n_all;
+  a.clear_keys = dck.as<uint64_t>();
+  a.n_clear = uint32_t(ck.size());
+  a.radius = int(std::ceil(cfg.max_distance / E->vs / kVPS));
+  a.hash = E->hash;
+  a.pool = static_cast<uint32_t*>(E->pool[E->cur_host]);
+  a.lim = limits_for(cfg, E->vs);
+  a.flags = dflags.as<uint8_t>();
+  if (n_all) {
+    k_clear<<<std::max<uint32_t>(1, std::min<uint32_t>(n_all, ctx->sm_count * 8)), 256, 0,
+              ctx->stream>>>(a);
+    ctx->count_launch();
+    check_launch(ctx, "k_clear");
+  }
+  const auto cleared = compact_to_host(ctx, a.sorted_keys, a.flags, dn.as<uint32_t>(), n_all);
+  changed->insert(changed->end(), cleared.begin(), cleared.end());
+  append_sorted_unique(st->lists[2], cleared);
+}
+
+int run_lower_esdf(Layer* E, EsdfState* st, const vxm_esdf_config& cfg,
+                   std::vector<vxm_grid_index>* changed) {
+  Context* ctx = E->ctx;
+  ctx->reset_status();
+  E->refresh();
+  // seeds = (to_update U cleared) n has_block — esdf/integrator.cpp:492-503
+  std::vector<vxm_grid_index> seeds = st->lists[0];
+  append_sorted_unique(seeds, st->lists[2]);
+  std::vector<uint64_t> sk(seeds.size());
+  for (size_t i = 0; i < seeds.size(); ++i) sk[i] = pack_key(seeds[i].x, seeds[i].y, seeds[i].z);
+  const uint32_t ns = uint32_t(sk.size());
+  DevBuf dk, dslots, dn;
+  dk.ensure(sizeof(uint64_t) * (ns + 1));
+  dslots.ensure(sizeof(int32_t) * (ns + 1));
+  dn.ensure(sizeof(uint32_t) * 2);
+  std::vector<int32_t> slots(ns);
+  if (ns) {
+    VXM_CUDA(cudaMemcpyAsync(dk.p, sk.data(), sizeof(uint64_t) * ns, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    k_lookup_slots<<<grid_for(ctx, ns), 256, 0, ctx->stream>>>(dk.as<uint64_t>(), ns, E->hash,
+                                                             dslots.as<int32_t>());
+    ctx->count_launch();
+    VXM_CUDA(cudaMemcpyAsync(slots.data(), dslots.p, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  std::vector<int32_t> live;
+  for (int32_t s : slots)
+    if (s >= 0) live.push_back(s);
+  const uint32_t nl = uint32_t(live.size());
+  if (nl) {
+    VXM_CUDA(cudaMemcpyAsync(dslots.p, live.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice,
+                             ctx->stream));
+  }
+  VXM_CUDA(cudaMemcpyAsync(dn.p, &nl, sizeof nl, cudaMemcpyHostToDevice, ctx->stream));
+  const uint32_t tag = ++ctx->call_epoch;
+  LowerArgs la = lower_args(E, cfg);
+  la.full = 0;
+  la.seeds = dslots.as<int32_t>();
+  la.n_seeds = dn.as<uint32_t>();
+  la.lchg_tag = tag;
+  launch_lower(ctx, la);
+  check_launch(ctx, "k_lower(seeded)");
+  const uint32_t n_all = E->num_blocks;
+  DevBuf dflags, dnall;
+  dflags.ensure(n_all + 16);
+  dnall.ensure(sizeof(uint32_t));
+  VXM_CUDA(cudaMemcpyAsync(dnall.p, &n_all, sizeof n_all, cudaMemcpyHostToDevice, ctx->stream));
+  if (n_all) {
+    k_flag_tag<<<grid_for(ctx, n_all), 256, 0, ctx->stream>>>(
+        E->sorted_slots[E->sorted_parity], n_all, E->stamp_lchg, tag, dflags.as<uint8_t>());
+    ctx->count_launch();
+  }
+  const auto ch = compact_to_host(ctx, E->sorted_keys[E->sorted_parity], dflags.as<uint8_t>(),
+                                  dnall.as<uint32_t>(), n_all);
+  changed->insert(changed->end(), ch.begin(), ch.end());
+  ctx->sync_status();
+  E->refresh();
+  return int(ctx->h_status->rounds);
+}
+
+// Allocation of an arbitrary key list (layer_write_blocks): sorted unique keys
+// on device -> slots (new blocks registered in the ESDF side structures).
+void alloc_key_list(Layer* L, BlockList* keys, int32_t* d_slots_out) {
+  Context* ctx = L->ctx;
+  const uint32_t n = std::max<uint32_t>(keys->count_hint, 1);
+  L->ensure_capacity(std::min<uint64_t>(uint64_t(L->num_blocks) + n, L->max_blocks));
+  EsdfScratch s = esdf_scratch(ctx, n, 0);
+  AllocListArgs al{};
+  al.keys = keys->keys.as<uint64_t>();
+  al.n_ptr = keys->d_count;
+  al.hash = L->hash;
+  al.slot_keys = L->slot_keys;
+  al.meta = L->meta;
+  al.capacity = L->capacity;
+  al.max_blocks = L->max_blocks;
+  al.slots_out = d_slots_out;
+  al.new_keys = s.new_keys;
+  al.new_slots = s.new_slots;
+  al.n_new_out = s.counts + 1;
+  al.n_old_out = s.counts + 2;
+  al.stamp_new = L->type == VXM_LAYER_ESDF ? L->stamp_new : nullptr;
+  al.call_epoch = ++ctx->call_epoch;
+  al.status = ctx->d_status;
+  const ScanTiles st = ctx->next_scan(ceil_div(n, 256));
+  k_alloc_list<<<grid_for(ctx, n, 4), 256, 0, ctx->stream>>>(al, st);
+  ctx->count_launch();
+  if (L->type == VXM_LAYER_ESDF) {
+    k_nbr_update<<<grid_for(ctx, 6ull * n), 256, 0, ctx->stream>>>(s.new_keys, s.new_slots,
+                                                                  s.counts + 1, L->hash, L->nbr);
+    const int sp = L->sorted_parity;
+    k_merge_sorted<<<grid_for(ctx, uint64_t(L->num_blocks) + n), 256, 0, ctx->stream>>>(
+        L->sorted_keys[sp], L->sorted_slots[sp], s.counts + 2, s.new_keys, s.new_slots,
+        s.counts + 1, L->sorted_keys[1 - sp], L->sorted_slots[1 - sp]);
+    L->sorted_parity = 1 - sp;
+    ctx->count_launch(2);
+  }
+  check_launch(ctx, "alloc_key_list");
+}
+
+}  // namespace vxm

@@ -1,0 +1,320 @@
+// TSDF projective integration.
+//
+// Reference: integrate_impl (proj/src/integrate/integrator.cpp:71-134),
+// tsdf_update / weight_for_depth (proj/include/voxmap/integrate/updates.hpp:27-54),
+// CameraIntrinsics::project/contains (sensor/camera.hpp:35-46), LiDAR project
+// (sensor/lidar.hpp:43-55), sample_depth_nearest/linear (sensor/image.hpp:65-106).
+//
+// B200 design: persistent grid, one CTA (256 threads) per candidate block per
+// iteration.  The block's voxel centres are separable, so the 72 products
+// R_SL(i,a) * centre_a(v) are computed once per block into shared memory and
+// every voxel transform is 9 FP64 adds in the reference's association order
+// (bit-exact).  The camera projection's two FP64 divides are replaced by an
+// FP32 pre-filter with a rigorous error bound: nearest-pixel sampling only
+// needs floor(u), floor(v), so whenever [u-E, u+E] contains no integer the
+// FP32 floor is exact; otherwise (rare) the exact FP64 path runs.  Voxels are
+// read only when they project onto a valid pixel (new blocks are known-zero
+// and are not read at all) and written only when their bytes change; each
+// block's changed flag comes from __syncthreads_or and the changed list is an
+// order-preserving compaction of the (sorted) candidate list.
+#include <cmath>
+
+#include "runtime.cuh"
+#include "scan.cuh"
+
+namespace vxm {
+
+struct IntegrateArgs {
+  const uint64_t* cand_keys;
+  const int32_t* cand_slots;
+  const DevStatus* status_ro;
+  float2* pool;
+  uint8_t* changed;
+  const float* depth;
+  int W, H;
+  vxm_pose T_SL;
+  int lidar;
+  double fu, fv, cu, cv;          // camera
+  float fu_f, fv_f, cu_f, cv_f;   // camera, FP32 pre-filter
+  double az0, el0, u_scale, v_scale;  // lidar: N/fov, M/fov_el
+  int na, ne;
+  double vs;
+  double max_voxel_depth;
+  float eps, max_weight, max_gap;
+  int inv_sq, linear;
+};
+
+__device__ inline bool valid_depth_i(float d) { return d > 0.0f && isfinite(d); }
+
+__device__ inline bool sample_nearest_d(const float* img, int W, int H, double u, double v,
+                                        float* out) {
+  const int col = int(floor(u)), row = int(floor(v));
+  if (u < 0.0 || v < 0.0 || col >= W || row >= H) return false;
+  const float d = __ldg(img + size_t(row) * W + col);
+  if (!valid_depth_i(d)) return false;
+  *out = d;
+  return true;
+}
+
+// sample_depth_linear — image.hpp:79-106
+__device__ inline bool sample_linear_d(const float* img, int W, int H, double u, double v,
+                                       float gap, float* out) {
+  const double gu = __dsub_rn(u, 0.5), gv = __dsub_rn(v, 0.5);
+  const int x0 = int(floor(gu)), y0 = int(floor(gv));
+  if (x0 < 0 || y0 < 0 || x0 + 1 >= W || y0 + 1 >= H) return false;
+  const float d00 = __ldg(img + size_t(y0) * W + x0), d10 = __ldg(img + size_t(y0) * W + x0 + 1);
+  const float d01 = __ldg(img + size_t(y0 + 1) * W + x0);
+  const float d11 = __ldg(img + size_t(y0 + 1) * W + x0 + 1);
+  if (!valid_depth_i(d00) || !valid_depth_i(d10) || !valid_depth_i(d01) || !valid_depth_i(d11))
+    return false;
+  float lo = d00, hi = d00;
+  lo = d10 < lo ? d10 : lo; hi = hi < d10 ? d10 : hi;
+  lo = d01 < lo ? d01 : lo; hi = hi < d01 ? d01 : hi;
+  lo = d11 < lo ? d11 : lo; hi = hi < d11 ? d11 : hi;
+  if (__fsub_rn(hi, lo) > gap) return false;
+  const double wx = __dsub_rn(gu, double(x0)), wy = __dsub_rn(gv, double(y0));
+  const double omx = __dsub_rn(1.0, wx), omy = __dsub_rn(1.0, wy);
+  const double top = __dadd_rn(__dmul_rn(omx, double(d00)), __dmul_rn(wx, double(d10)));
+  const double bot = __dadd_rn(__dmul_rn(omx, double(d01)), __dmul_rn(wx, double(d11)));
+  const double d = __dadd_rn(__dmul_rn(omy, top), __dmul_rn(wy, bot));
+  *out = __double2float_rn(d);
+  return true;
+}
+
+// Exact-floor FP32 pre-filter for one projected coordinate.  Returns true and
+// sets *idx when floor(u_exact) is certain; u_exact = (f*x)/z + c in FP64.
+__device__ inline bool fast_floor(float f, float c, float xf, float zf, int* idx) {
+  const float t = __fdiv_rn(__fmul_rn(f, xf), zf);
+  const float u = __fadd_rn(t, c);
+  const float E = __fmul_rn(__fadd_rn(__fadd_rn(fabsf(t), fabsf(c)), fabsf(u)), 9.5367431640625e-07f) +
+                  1e-30f;  // (|t| + |c| + |u|) * 2^-20 >= 16 units of the error
+  const float lo = floorf(__fsub_rn(u, E)), hi = floorf(__fadd_rn(u, E));
+  if (!(lo == hi) || !(fabsf(lo) < 1.0e9f)) return false;
+  *idx = int(lo);
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
+  __shared__ double s_A[3][3][8];  // R_SL(i, axis) * centre_axis(v)
+  const DevStatus* st = a.status_ro;
+  if (st->pool_overflow || st->capacity_error || st->bitmap_overflow) return;
+  const uint32_t n = st->n_candidates;
+  const double* R = a.T_SL.R;
+  for (uint32_t ci = blockIdx.x; ci < n; ci += gridDim.x) {
+    const uint64_t key = a.cand_keys[ci];
+    const int32_t sraw = a.cand_slots[ci];
+    const bool is_new = sraw < 0;
+    const int32_t slot = sraw & 0x7fffffff;
+    if (threadIdx.x < 72) {
+      const int i = threadIdx.x / 24, ax = (threadIdx.x / 8) % 3, v = threadIdx.x % 8;
+      const int32_t g = ax == 0 ? key_x(key) : (ax == 1 ? key_y(key) : key_z(key));
+      // voxel_center — indexing.hpp:113-119: ((g * 8 + v) + 0.5) * vs
+      const double c = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(double(g), 8.0), double(v)), 0.5), a.vs);
+      s_A[i][ax][v] = __dmul_rn(R[3 * i + ax], c);
+    }
+    __syncthreads();
+    float2* blk = a.pool + size_t(slot) * kVPB;
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int lin = threadIdx.x + k * 256;
+      const int vx = lin & 7, vy = (lin >> 3) & 7, vz = lin >> 6;
+      // Pose::operator* — pose.hpp:58-60, rows a0 + (a1 + a2), then + t
+      const double pz = __dadd_rn(__dadd_rn(s_A[2][0][vx], __dadd_rn(s_A[2][1][vy], s_A[2][2][vz])), a.T_SL.t[2]);
+      const double px = __dadd_rn(__dadd_rn(s_A[0][0][vx], __dadd_rn(s_A[0][1][vy], s_A[0][2][vz])), a.T_SL.t[0]);
+      const double py = __dadd_rn(__dadd_rn(s_A[1][0][vx], __dadd_rn(s_A[1][1][vy], s_A[1][2][vz])), a.T_SL.t[1]);
+      double d_v;
+      if (!a.lidar) {
+        d_v = pz;  // CameraIntrinsics::depth_of — camera.hpp:49
+      } else {     // LidarIntrinsics::depth_of — lidar.hpp:62
+        d_v = __dsqrt_rn(__dadd_rn(__dmul_rn(px, px), __dadd_rn(__dmul_rn(py, py), __dmul_rn(pz, pz))));
+      }
+      if (!(d_v > 0.0) || d_v > a.max_voxel_depth) continue;  // integrator.cpp:104-107
+      float s;
+      bool ok;
+      if (!a.lidar) {
+        if (!a.linear) {
+          int col, row;
+          const float xf = __double2float_rn(px), yf = __double2float_rn(py),
+                      zf = __double2float_rn(pz);
+          if (!(fast_floor(a.fu_f, a.cu_f, xf, zf, &col) &&
+                fast_floor(a.fv_f, a.cv_f, yf, zf, &row))) {
+            // exact FP64 projection — camera.hpp:39-40
+            const double u = __dadd_rn(__ddiv_rn(__dmul_rn(a.fu, px), pz), a.cu);
+            const double v = __dadd_rn(__ddiv_rn(__dmul_rn(a.fv, py), pz), a.cv);
+            if (!(u >= 0.0 && u < double(a.W) && v >= 0.0 && v < double(a.H))) continue;
+            col = int(floor(u));
+            row = int(floor(v));
+          }
+          if (col < 0 || row < 0 || col >= a.W || row >= a.H) continue;
+          s = __ldg(a.depth + size_t(row) * a.W + col);
+          ok = valid_depth_i(s);
+        } else {
+          const double u = __dadd_rn(__ddiv_rn(__dmul_rn(a.fu, px), pz), a.cu);
+          const double v = __dadd_rn(__ddiv_rn(__dmul_rn(a.fv, py), pz), a.cv);
+          if (!(u >= 0.0 && u < double(a.W) && v >= 0.0 && v < double(a.H))) continue;
+          ok = sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s);
+        }
+      } else {
+        // LidarIntrinsics::project — lidar.hpp:43-55 (CUDA libm atan2/acos)
+        const double kTwoPi = 6.283185307179586;
+        double az = __dsub_rn(atan2(py, px), a.az0);
+        az = __dsub_rn(az, __dmul_rn(kTwoPi, floor(__ddiv_rn(az, kTwoPi))));
+        const double u = __dmul_rn(az, a.u_scale);
+        double c = __ddiv_rn(pz, d_v);
+        c = c < -1.0 ? -1.0 : (1.0 < c ? 1.0 : c);
+        const double v = __dmul_rn(__dsub_rn(acos(c), a.el0), a.v_scale);
+        if (!(u >= 0.0 && u < double(a.na) && v >= 0.0 && v < double(a.ne))) continue;
+        ok = a.linear ? sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s)
+                      : sample_nearest_d(a.depth, a.W, a.H, u, v, &s);
+      }
+      if (!ok) continue;
+      const float d_p = __fsub_rn(s, __double2float_rn(d_v));  // integrator.cpp:116
+      // tsdf_update — updates.hpp:39-54
+      if (d_p < -a.eps) continue;  // occluded: voxel unchanged
+      float w_new = 1.0f;
+      if (a.inv_sq) {
+        const double dd = __dmul_rn(double(s), double(s));
+        w_new = __double2float_rn(__ddiv_rn(1.0, dd < 1e-6 ? 1e-6 : dd));
+      }
+      const float2 old = is_new ? make_float2(0.0f, 0.0f) : blk[lin];
+      const float d_t = d_p < -a.eps ? -a.eps : (a.eps < d_p ? a.eps : d_p);
+      const float w_sum = __fadd_rn(old.y, w_new);
+      const float avg = __fdiv_rn(__fadd_rn(__fmul_rn(old.y, old.x), __fmul_rn(w_new, d_t)), w_sum);
+      float2 nv;
+      nv.x = avg < -a.eps ? -a.eps : (a.eps < avg ? a.eps : avg);
+      nv.y = a.max_weight < w_sum ? a.max_weight : w_sum;
+      if (__float_as_uint(nv.x) != __float_as_uint(old.x) ||
+          __float_as_uint(nv.y) != __float_as_uint(old.y)) {
+        blk[lin] = nv;
+        any = true;
+      }
+    }
+    const int changed = __syncthreads_or(any);
+    if (threadIdx.x == 0) a.changed[ci] = uint8_t(changed);
+  }
+}
+
+// Order-preserving compaction of keys by flag; count read from the device.
+constexpr int kCompactItems = 4;
+__global__ void __launch_bounds__(256) k_compact_keys(const uint64_t* __restrict__ in,
+                                                      const uint8_t* __restrict__ flags,
+                                                      const uint32_t* n_ptr, uint64_t* out,
+                                                      uint32_t* n_out, ScanTiles st,
+                                                      const DevStatus* guard) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_scan[64];
+  __shared__ uint32_t s_pre;
+  scan_prepare_next(st);
+  const bool skip = guard && (guard->pool_overflow || guard->capacity_error || guard->bitmap_overflow);
+  const uint32_t n = skip ? 0u : *n_ptr;
+  const uint32_t per_tile = blockDim.x * kCompactItems;
+  const uint32_t tiles = (n + per_tile - 1) / per_tile;
+  if (tiles == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = 0;
+    return;
+  }
+  while (true) {
+    const uint32_t tile = scan_take_tile(st, &s_tile);
+    if (tile >= tiles) break;
+    const uint32_t base = tile * per_tile + threadIdx.x * kCompactItems;
+    uint32_t keep = 0;
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k)
+      if (base + k < n && flags[base + k]) keep |= 1u << k;
+    uint32_t ea, eb, ta, tb;
+    block_scan2(__popc(keep), 0u, ea, eb, ta, tb, s_scan);
+    if (threadIdx.x == 0) {
+      uint32_t pa, pb;
+      scan_lookback(st, tile, ta, 0u, pa, pb);
+      s_pre = pa;
+      if (tile == tiles - 1) *n_out = pa + ta;
+    }
+    __syncthreads();
+    uint32_t pos = s_pre + ea;
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k)
+      if (keep & (1u << k)) out[pos++] = in[base + k];
+    __syncthreads();
+  }
+}
+
+void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
+                         const uint32_t* n_ptr, uint32_t n_cap, uint64_t* out, uint32_t* n_out,
+                         const DevStatus* guard) {
+  const uint32_t tiles_cap = ceil_div(std::max<uint32_t>(n_cap, 1), 256 * kCompactItems);
+  const ScanTiles st = ctx->next_scan(tiles_cap);
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_cap, ctx->sm_count * 4));
+  k_compact_keys<<<grid, 256, 0, ctx->stream>>>(in, flags, n_ptr, out, n_out, st, guard);
+  ctx->count_launch();
+  check_launch(ctx, "k_compact_keys");
+}
+
+void run_integrate(Layer* L, const ViewArgs& va, const vxm_integrator_config& cfg,
+                   BlockList* changed_out) {
+  Context* ctx = L->ctx;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    // Headroom: a frame cannot allocate more blocks than it has candidates;
+    // the bound below is generous, the device check catches the rest.
+    L->ensure_capacity(std::min<uint64_t>(uint64_t(L->num_blocks) + 65536, L->max_blocks));
+    ctx->reset_status();
+    const uint32_t nb_before = L->num_blocks;
+    uint32_t cand_cap = 0;
+    run_view(ctx, va, L, &cand_cap);
+    ctx->cand_flags.ensure(cand_cap);
+    IntegrateArgs a{};
+    a.cand_keys = ctx->cand_keys.as<uint64_t>();
+    a.cand_slots = ctx->cand_slots.as<int32_t>();
+    a.status_ro = ctx->d_status;
+    a.pool = static_cast<float2*>(L->pool[0]);
+    a.changed = ctx->cand_flags.as<uint8_t>();
+    a.depth = va.depth_dev;
+    a.W = va.width;
+    a.H = va.height;
+    vxm_pose_inverse(&va.T_LS, &a.T_SL);  // integrator.cpp:89 (host, pinned order)
+    a.lidar = va.lidar ? 1 : 0;
+    a.fu = va.cam.fu; a.fv = va.cam.fv; a.cu = va.cam.cu; a.cv = va.cam.cv;
+    a.fu_f = float(va.cam.fu); a.fv_f = float(va.cam.fv);
+    a.cu_f = float(va.cam.cu); a.cv_f = float(va.cam.cv);
+    a.az0 = va.li.azimuth_start;
+    a.el0 = va.li.elevation_start;
+    a.u_scale = va.li.num_azimuth / va.li.azimuth_fov;
+    a.v_scale = va.li.num_elevation / va.li.elevation_fov;
+    a.na = va.li.num_azimuth;
+    a.ne = va.li.num_elevation;
+    a.vs = L->vs;
+    a.max_voxel_depth = cfg.max_integration_distance + cfg.truncation;
+    a.eps = float(cfg.truncation);
+    a.max_weight = cfg.max_weight;
+    a.max_gap = cfg.max_sample_gap;
+    a.inv_sq = cfg.weighting == VXM_WEIGHT_INVERSE_SQUARE;
+    a.linear = (va.lidar ? cfg.lidar_sample : cfg.camera_sample) == VXM_SAMPLE_LINEAR;
+    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * 8));
+    k_integrate<<<grid, 256, 0, ctx->stream>>>(a);
+    ctx->count_launch();
+    check_launch(ctx, "k_integrate");
+    changed_out->ensure(cand_cap);
+    launch_compact_keys(ctx, ctx->cand_keys.as<uint64_t>(), ctx->cand_flags.as<uint8_t>(),
+                        &ctx->d_status->n_candidates, cand_cap, changed_out->keys.as<uint64_t>(),
+                        changed_out->d_count, ctx->d_status);
+    changed_out->host_valid = false;
+    changed_out->count_hint = cand_cap;
+    ctx->sync_status();
+    const DevStatus& s = *ctx->h_status;
+    L->refresh();
+    if (s.bitmap_overflow)
+      throw Error(VXM_ERR_INTERNAL, "candidate ray left the candidate cube (bitmap bound)");
+    if (s.pool_overflow) {
+      // No voxel was touched: grow to fit and run the frame again (blocks
+      // already inserted are zero and count as existing on the re-run).
+      L->ensure_capacity(std::min<uint64_t>(uint64_t(nb_before) + s.n_new + 1024, L->max_blocks));
+      continue;
+    }
+    if (s.capacity_error) throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+    changed_out->count_hint = s.n_candidates;
+    return;
+  }
+  throw Error(VXM_ERR_INTERNAL, "integrate: pool growth did not converge");
+}
+
+}  // namespace vxm

@@ -1,0 +1,307 @@
+// Host runtime: device memory management for layers (block pool + hash +
+// ESDF side arrays), contexts, block lists and small device utilities.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "runtime.cuh"
+
+namespace vxm {
+
+// ---- DevBuf -------------------------------------------------------------------
+void DevBuf::ensure(size_t n) {
+  if (n <= bytes) return;
+  release();
+  size_t b = std::max<size_t>(n, 256);
+  b = b + b / 4;  // slack so slowly growing sizes do not realloc every call
+  VXM_CUDA(cudaMalloc(&p, b));
+  bytes = b;
+}
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+void check_launch(Context* ctx, const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(VXM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  (void)ctx;
+}
+
+// ---- Context -------------------------------------------------------------------
+ScanTiles Context::next_scan(uint32_t tiles) {
+  tiles = std::max<uint32_t>(tiles, 1);
+  if (tiles > scan.cap) {
+    // Grow both buffers (no pass is in flight across a host call boundary
+    // once the stream is drained).
+    VXM_CUDA(cudaStreamSynchronize(stream));
+    for (int i = 0; i < 2; ++i) {
+      if (scan.status[i]) cudaFree(scan.status[i]);
+      VXM_CUDA(cudaMalloc(&scan.status[i], sizeof(unsigned long long) * tiles * 2));
+      VXM_CUDA(cudaMemset(scan.status[i], 0, sizeof(unsigned long long) * tiles * 2));
+    }
+    if (!scan.tickets) VXM_CUDA(cudaMalloc(&scan.tickets, sizeof(uint32_t) * 2));
+    VXM_CUDA(cudaMemset(scan.tickets, 0, sizeof(uint32_t) * 2));
+    scan.cap = tiles * 2;
+    scan.parity = 0;
+  }
+  ScanTiles st;
+  const int p = scan.parity;
+  st.status = scan.status[p];
+  st.next = scan.status[1 - p];
+  st.ticket = scan.tickets + p;
+  st.next_ticket = scan.tickets + (1 - p);
+  st.n_next = scan.cap;
+  scan.parity = 1 - p;
+  return st;
+}
+
+void Context::reset_status() {
+  VXM_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), stream));
+}
+void Context::sync_status() {
+  VXM_CUDA(cudaMemcpyAsync(h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
+  VXM_CUDA(cudaStreamSynchronize(stream));
+}
+
+// ---- Layer ---------------------------------------------------------------------
+__global__ void k_rehash(HashView h, const uint64_t* slot_keys, uint32_t n) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x)
+    hash_insert(h, slot_keys[s], int32_t(s));
+}
+
+template <typename T>
+static void grow_copy(T** ptr, uint64_t old_elems, uint64_t live_elems, uint64_t new_elems,
+                      int fill_byte, cudaStream_t st) {
+  T* np = nullptr;
+  VXM_CUDA(cudaMalloc(&np, sizeof(T) * std::max<uint64_t>(new_elems, 1)));
+  if (*ptr && live_elems)
+    VXM_CUDA(cudaMemcpyAsync(np, *ptr, sizeof(T) * live_elems, cudaMemcpyDeviceToDevice, st));
+  if (fill_byte >= 0 && new_elems > live_elems)
+    VXM_CUDA(cudaMemsetAsync(np + live_elems, fill_byte, sizeof(T) * (new_elems - live_elems), st));
+  VXM_CUDA(cudaStreamSynchronize(st));
+  if (*ptr) cudaFree(*ptr);
+  *ptr = np;
+  (void)old_elems;
+}
+
+void Layer::refresh() {
+  LayerMeta m;
+  VXM_CUDA(cudaMemcpyAsync(&m, meta, sizeof m, cudaMemcpyDeviceToHost, ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  num_blocks = m.num_blocks;
+  cur_host = m.cur;
+}
+
+void Layer::ensure_capacity(uint64_t need) {
+  if (need <= capacity) return;
+  if (need > (uint64_t(1) << 31) - 1)
+    throw Error(VXM_ERR_CAPACITY, "Layer: device block pool limit (2^31 blocks) exceeded");
+  refresh();
+  uint64_t nc = std::max<uint64_t>({need, uint64_t(capacity) * 2, 4096});
+  nc = (nc + 1023) & ~uint64_t(1023);
+  nc = std::min<uint64_t>(nc, std::max<uint64_t>(max_blocks, need));
+  nc = std::max<uint64_t>(nc, need);
+  cudaStream_t st = ctx->stream;
+  const uint64_t live = num_blocks;
+  const size_t bb = block_bytes();
+  // block pools (byte-typed); ESDF pool[1 - cur] is scratch for the next
+  // full lowering, only its never-used tail must be zero.
+  {
+    unsigned char* p0 = static_cast<unsigned char*>(pool[0]);
+    unsigned char* p1 = static_cast<unsigned char*>(pool[1]);
+    const int c = type == VXM_LAYER_ESDF ? int(cur_host) : 0;
+    unsigned char* pc = c ? p1 : p0;
+    grow_copy(&pc, capacity * bb, live * bb, nc * bb, 0, st);
+    if (type == VXM_LAYER_ESDF) {
+      unsigned char* po = c ? p0 : p1;
+      grow_copy(&po, capacity * bb, 0, nc * bb, 0, st);
+      pool[c] = pc;
+      pool[1 - c] = po;
+    } else {
+      pool[0] = pc;
+    }
+  }
+  grow_copy(&slot_keys, capacity, live, nc, 0xFF, st);
+  if (type == VXM_LAYER_ESDF) {
+    grow_copy(&nbr, capacity * 6ull, live * 6ull, nc * 6ull, 0xFF, st);
+    for (int i = 0; i < 2; ++i) {
+      grow_copy(&sorted_keys[i], capacity, i == sorted_parity ? live : 0, nc, -1, st);
+      grow_copy(&sorted_slots[i], capacity, i == sorted_parity ? live : 0, nc, -1, st);
+      grow_copy(&stamp_dirty[i], capacity, live, nc, 0, st);
+      grow_copy(&dirty_list[i], capacity, 0, nc, -1, st);
+    }
+    grow_copy(&stamp_mark, capacity, live, nc, 0, st);
+    grow_copy(&stamp_new, capacity, live, nc, 0, st);
+    grow_copy(&stamp_lchg, capacity, live, nc, 0, st);
+  }
+  // hash: power of two >= 2 * capacity, rebuilt from slot_keys
+  uint64_t hc = 1024;
+  while (hc < 2 * nc) hc <<= 1;
+  if (hc != hash_cap) {
+    if (hash.keys) cudaFree(hash.keys);
+    if (hash.vals) cudaFree(hash.vals);
+    VXM_CUDA(cudaMalloc(&hash.keys, sizeof(uint64_t) * hc));
+    VXM_CUDA(cudaMalloc(&hash.vals, sizeof(int32_t) * hc));
+    VXM_CUDA(cudaMemsetAsync(hash.keys, 0xFF, sizeof(uint64_t) * hc, st));
+    hash.mask = uint32_t(hc - 1);
+    hash_cap = uint32_t(hc);
+    if (live) {
+      k_rehash<<<std::min<uint32_t>(ceil_div(live, 256), 4096), 256, 0, st>>>(hash, slot_keys,
+                                                                           uint32_t(live));
+      ctx->count_launch();
+      check_launch(ctx, "k_rehash");
+    }
+  }
+  capacity = uint32_t(nc);
+  VXM_CUDA(cudaStreamSynchronize(st));
+}
+
+Layer::~Layer() {
+  for (void* p : {pool[0], pool[1]})
+    if (p) cudaFree(p);
+  if (hash.keys) cudaFree(hash.keys);
+  if (hash.vals) cudaFree(hash.vals);
+  if (slot_keys) cudaFree(slot_keys);
+  if (meta) cudaFree(meta);
+  if (nbr) cudaFree(nbr);
+  for (int i = 0; i < 2; ++i) {
+    if (sorted_keys[i]) cudaFree(sorted_keys[i]);
+    if (sorted_slots[i]) cudaFree(sorted_slots[i]);
+    if (stamp_dirty[i]) cudaFree(stamp_dirty[i]);
+    if (dirty_list[i]) cudaFree(dirty_list[i]);
+  }
+  if (stamp_mark) cudaFree(stamp_mark);
+  if (stamp_new) cudaFree(stamp_new);
+  if (stamp_lchg) cudaFree(stamp_lchg);
+  if (dirty_count) cudaFree(dirty_count);
+}
+
+// ---- BlockList -----------------------------------------------------------------
+void BlockList::ensure(uint32_t n) {
+  if (!d_count) {
+    VXM_CUDA(cudaMalloc(&d_count, sizeof(uint32_t)));
+    VXM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), ctx->stream));
+  }
+  if (n > cap) {
+    // preserve nothing: lists are rewritten by their producer
+    keys.ensure(sizeof(uint64_t) * std::max<uint32_t>(n, 1));
+    cap = uint32_t(keys.bytes / sizeof(uint64_t));
+  }
+}
+
+const std::vector<vxm_grid_index>& BlockList::fetch() {
+  if (host_valid) return host;
+  uint32_t n = 0;
+  if (d_count) {
+    VXM_CUDA(cudaMemcpyAsync(&n, d_count, sizeof n, cudaMemcpyDeviceToHost, ctx->stream));
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  std::vector<uint64_t> k(n);
+  if (n) {
+    VXM_CUDA(cudaMemcpyAsync(k.data(), keys.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  host.resize(n);
+  for (uint32_t i = 0; i < n; ++i) host[i] = {key_x(k[i]), key_y(k[i]), key_z(k[i])};
+  host_valid = true;
+  count_hint = n;
+  return host;
+}
+
+void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
+  ensure(uint32_t(std::max<uint64_t>(n, 1)));
+  std::vector<uint64_t> k(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    if (!coord_ok(data[i].x) || !coord_ok(data[i].y) || !coord_ok(data[i].z))
+      throw Error(VXM_ERR_INVALID_ARGUMENT, "block index outside the supported range (+-2^20)");
+    k[i] = pack_key(data[i].x, data[i].y, data[i].z);
+  }
+  const uint32_t n32 = uint32_t(n);
+  if (n)
+    VXM_CUDA(cudaMemcpyAsync(keys.p, k.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
+                             ctx->stream));
+  VXM_CUDA(cudaMemcpyAsync(d_count, &n32, sizeof n32, cudaMemcpyHostToDevice, ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  host.assign(data, data + n);
+  host_valid = true;
+  count_hint = n32;
+}
+
+BlockList::~BlockList() {
+  keys.release();
+  if (d_count) cudaFree(d_count);
+}
+
+// ---- sorting utilities (API paths only; the hot path never sorts) ---------------
+__global__ void k_count_to_dev(uint32_t* dst, const int* src) { *dst = uint32_t(*src); }
+
+void sort_unique_keys(Context* ctx, BlockList* list) {
+  const uint32_t n = list->count_hint;
+  if (n <= 1) return;
+  DevBuf& t0 = ctx->tmp[0];
+  t0.ensure(sizeof(uint64_t) * n);
+  size_t sort_bytes = 0, uniq_bytes = 0;
+  uint64_t* keys = list->keys.as<uint64_t>();
+  cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, keys, t0.as<uint64_t>(), int(n), 0, 63,
+                                 ctx->stream);
+  cub::DeviceSelect::Unique(nullptr, uniq_bytes, t0.as<uint64_t>(), keys, (int*)nullptr, int(n),
+                            ctx->stream);
+  const size_t work = (std::max(sort_bytes, uniq_bytes) + 255) & ~size_t(255);
+  ctx->cub_tmp.ensure(work + 256);
+  int* d_nsel = reinterpret_cast<int*>(static_cast<char*>(ctx->cub_tmp.p) + work);
+  VXM_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_tmp.p, sort_bytes, keys, t0.as<uint64_t>(),
+                                          int(n), 0, 63, ctx->stream));
+  VXM_CUDA(cub::DeviceSelect::Unique(ctx->cub_tmp.p, uniq_bytes, t0.as<uint64_t>(), keys, d_nsel,
+                                     int(n), ctx->stream));
+  k_count_to_dev<<<1, 1, 0, ctx->stream>>>(list->d_count, d_nsel);
+  ctx->count_launch(3);
+  check_launch(ctx, "sort_unique_keys");
+  list->host_valid = false;
+}
+
+// Sorted (key, slot) export of a TSDF layer (sorted_indices, layer.hpp:109-117).
+__global__ void k_iota_keys(const uint64_t* slot_keys, uint64_t* keys, int32_t* slots, uint32_t n) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    keys[s] = slot_keys[s];
+    slots[s] = int32_t(s);
+  }
+}
+
+void layer_export_sorted(Layer* L, std::vector<uint64_t>* keys, std::vector<int32_t>* slots) {
+  Context* ctx = L->ctx;
+  L->refresh();
+  const uint32_t n = L->num_blocks;
+  keys->resize(n);
+  slots->resize(n);
+  if (!n) return;
+  if (L->type == VXM_LAYER_ESDF) {
+    esdf_sorted_export(L, keys, slots);
+    return;
+  }
+  for (int i = 0; i < 4; ++i) ctx->tmp[i].ensure(sizeof(uint64_t) * n);
+  uint64_t* k_in = ctx->tmp[0].as<uint64_t>();
+  uint64_t* k_out = ctx->tmp[1].as<uint64_t>();
+  int32_t* v_in = ctx->tmp[2].as<int32_t>();
+  int32_t* v_out = ctx->tmp[3].as<int32_t>();
+  k_iota_keys<<<std::min<uint32_t>(ceil_div(n, 256), 4096), 256, 0, ctx->stream>>>(L->slot_keys,
+                                                                                  k_in, v_in, n);
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, k_in, k_out, v_in, v_out, int(n), 0, 63,
+                                  ctx->stream);
+  ctx->cub_tmp.ensure(bytes);
+  VXM_CUDA(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, bytes, k_in, k_out, v_in, v_out, int(n),
+                                           0, 63, ctx->stream));
+  ctx->count_launch(2);
+  check_launch(ctx, "layer_export_sorted");
+  VXM_CUDA(cudaMemcpyAsync(keys->data(), k_out, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  VXM_CUDA(cudaMemcpyAsync(slots->data(), v_out, sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace vxm

@@ -1,0 +1,163 @@
+// Host-side runtime of libvoxmap_b200: contexts, layers (device block pool +
+// open-addressing hash), block lists, scratch management.  Kernels live in
+// view.cu / integrate.cu / esdf.cu / query.cu; the C-ABI in capi.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace vxm {
+
+// Growable device allocation (contents are NOT preserved on growth).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void ensure(size_t n);
+  void release();
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Double-buffered decoupled-look-back scan state (see common.cuh ScanTiles).
+struct ScanState {
+  unsigned long long* status[2] = {nullptr, nullptr};
+  uint32_t* tickets = nullptr;  // [2]
+  uint32_t cap = 0;             // entries per status buffer
+  int parity = 0;
+};
+
+struct Context {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  DevStatus* d_status = nullptr;
+  DevStatus* h_status = nullptr;  // pinned
+  uint64_t launches = 0;
+  ScanState scan;
+  uint32_t call_epoch = 0;
+  // sharding: owner(g) = floor(g.x / slab) mod world
+  int rank = 0, world = 1, slab = 16;
+  // scratch
+  DevBuf depth;           // staged depth image
+  DevBuf bitmap;          // touched-cell bitmap (candidate cube)
+  DevBuf cand_keys;       // uint64 candidate keys (sorted)
+  DevBuf cand_slots;      // int32 slot | new flag
+  DevBuf cand_flags;      // uint8 per candidate (changed)
+  DevBuf lidar_dirs;      // double3 per LiDAR pixel (host glibc LUT)
+  vxm_lidar lut_key{};
+  bool lut_valid = false;
+  DevBuf tmp[6];          // ESDF / list scratch
+  DevBuf cub_tmp;
+
+  // Scan pass bookkeeping: returns the ScanTiles for the next pass with at
+  // most `tiles` tiles, clearing the other buffer for the pass after.
+  ScanTiles next_scan(uint32_t tiles);
+  void count_launch(int n = 1) { launches += uint64_t(n); }
+  void sync_status();  // cudaStreamSynchronize + copy status (already async-copied)
+  void reset_status();
+};
+
+struct Layer {
+  Context* ctx = nullptr;
+  int type = VXM_LAYER_TSDF;
+  double vs = 0.0;
+  uint64_t max_blocks = 0;
+  uint32_t capacity = 0;        // pool slots
+  uint32_t num_blocks = 0;      // host mirror, exact after each synchronous call
+  HashView hash{nullptr, nullptr, 0};
+  uint32_t hash_cap = 0;
+  uint64_t* slot_keys = nullptr;  // slot -> key
+  void* pool[2] = {nullptr, nullptr};
+  LayerMeta* meta = nullptr;    // device
+  uint32_t cur_host = 0;        // host mirror of meta->cur (ESDF)
+  // ESDF-only
+  int32_t* nbr = nullptr;                  // [cap][6] neighbour slots (+x,-x,+y,-y,+z,-z)
+  uint64_t* sorted_keys[2] = {nullptr, nullptr};
+  int32_t* sorted_slots[2] = {nullptr, nullptr};
+  int sorted_parity = 0;
+  uint32_t* stamp_dirty[2] = {nullptr, nullptr};
+  uint32_t* stamp_mark = nullptr;   // call epoch when mark changed the block
+  uint32_t* stamp_new = nullptr;    // call epoch when the block was allocated
+  uint32_t* stamp_lchg = nullptr;   // round epoch of the last lowering change
+  int32_t* dirty_list[2] = {nullptr, nullptr};
+  uint32_t* dirty_count = nullptr;  // [2]
+
+  size_t voxel_bytes() const { return type == VXM_LAYER_TSDF ? 8 : 12; }
+  size_t block_bytes() const { return voxel_bytes() * kVPB; }
+  void* cur_pool() const { return pool[type == VXM_LAYER_ESDF ? cur_host : 0]; }
+  // Grow pool/hash/side arrays so that capacity >= need (requires exact num_blocks).
+  void ensure_capacity(uint64_t need);
+  uint64_t limit() const { return max_blocks; }
+  void refresh();  // sync + read meta (num_blocks, cur)
+  ~Layer();
+};
+
+struct BlockList {
+  Context* ctx = nullptr;
+  DevBuf keys;                 // uint64 packed keys
+  uint32_t* d_count = nullptr; // device count
+  uint32_t cap = 0;            // capacity in keys (upper bound of count)
+  uint32_t count_hint = 0;     // host upper bound of count
+  std::vector<vxm_grid_index> host;
+  bool host_valid = true;
+  void ensure(uint32_t n);
+  const std::vector<vxm_grid_index>& fetch();   // sync + download + unpack
+  void assign_host(const vxm_grid_index* data, uint64_t n);  // upload (sorted as given)
+  ~BlockList();
+};
+
+struct EsdfState {
+  std::vector<vxm_grid_index> lists[3];
+};
+
+// ---- drivers (implemented in the kernel TUs) ----------------------------------
+// view.cu — candidate blocks; when `alloc` != null the candidates are also
+// looked up / allocated in that layer (fused allocation, integrator.cpp:84-87).
+struct ViewArgs {
+  vxm_pose T_LS;
+  bool lidar;
+  vxm_camera cam;
+  vxm_lidar li;
+  const float* depth_dev;
+  int width, height;
+  double block_size;
+  vxm_view_config cfg;
+};
+// Returns the number of candidates only after ctx sync (status.n_candidates).
+void run_view(Context* ctx, const ViewArgs& a, Layer* alloc, uint32_t* cand_cap_out);
+
+// integrate.cu
+void run_integrate(Layer* L, const ViewArgs& a, const vxm_integrator_config& cfg,
+                   BlockList* changed_out);
+
+// esdf.cu
+void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
+                     BlockList* changed_out);
+void run_mark_sites(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
+                    EsdfState* st, std::vector<vxm_grid_index>* changed);
+void run_clear_invalid(Layer* E, const vxm_esdf_config& cfg, EsdfState* st,
+                       std::vector<vxm_grid_index>* changed);
+int run_lower_esdf(Layer* E, EsdfState* st, const vxm_esdf_config& cfg,
+                   std::vector<vxm_grid_index>* changed);
+void esdf_sorted_export(Layer* E, std::vector<uint64_t>* keys, std::vector<int32_t>* slots);
+// get_or_allocate of a sorted unique key list; slots in list order.
+void alloc_key_list(Layer* L, BlockList* keys, int32_t* d_slots_out);
+
+// query.cu
+void run_query(Layer* E, const double* xyz_host, uint64_t n, int want_gradient, int interpolate,
+               vxm_query_result* out_host);
+
+// runtime.cu helpers used by the kernel TUs
+void sort_unique_keys(Context* ctx, BlockList* list);  // device sort + unique (CUB)
+void layer_export_sorted(Layer* L, std::vector<uint64_t>* keys, std::vector<int32_t>* slots);
+void check_launch(Context* ctx, const char* what);
+
+}  // namespace vxm

@@ -1,0 +1,396 @@
+// View candidates + block allocation.
+//
+// Reference: blocks_in_view (proj/src/sensor/view.cpp:61-111), cast_ray
+// (:45-57), traverse_grid (proj/include/voxmap/sensor/traversal.hpp:29-73),
+// dilate_and_sort (view.cpp:25-41), allocation loop (integrator.cpp:84-87).
+//
+// B200 design (no hash sets, no sort):
+//   K_rays    one thread per camera tile (or LiDAR pixel) runs the exact FP64
+//             Amanatides-Woo DDA and sets bits in a dense bitmap over the
+//             cube of cells reachable from the sensor's cell (L2-resident).
+//   K_dilate  one thread per 32-cell bitmap word computes the 27-neighbour
+//             dilation with shifts/ORs, looks every candidate up in the
+//             layer's block hash, and emits (key, slot) in lexicographic
+//             (x, y, z) order through a single-pass decoupled look-back scan;
+//             new blocks get slots num_blocks + rank(new) in sorted order and
+//             are inserted into the hash in the same pass.  The bitmap layout
+//             (x slowest, z fastest) makes word order == GridIndex order, so
+//             the candidate list is sorted for free.
+#include <math_constants.h>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "runtime.cuh"
+#include "scan.cuh"
+
+namespace vxm {
+
+struct Cube {
+  int32_t ox, oy, oz;  // cell of index 0 along each axis (origin cell - r)
+  int32_t S;           // side in cells
+  int32_t SZw;         // 32-bit words per z-row
+  uint32_t* bits;
+  __device__ inline bool locate(int32_t x, int32_t y, int32_t z, uint32_t& word,
+                                uint32_t& mask) const {
+    const int32_t dx = x - ox, dy = y - oy, dz = z - oz;
+    if (dx < 0 || dy < 0 || dz < 0 || dx >= S || dy >= S || dz >= S) return false;
+    word = (uint32_t(dx) * uint32_t(S) + uint32_t(dy)) * uint32_t(SZw) + uint32_t(dz >> 5);
+    mask = 1u << (dz & 31);
+    return true;
+  }
+};
+
+// Pinned-order FP64 helpers (no FMA contraction: TU compiled with --fmad=false,
+// and the explicit __d*_rn intrinsics make the intent independent of flags).
+__device__ inline double sum3(double a0, double a1, double a2) {
+  return __dadd_rn(a0, __dadd_rn(a1, a2));
+}
+__device__ inline void pose_apply(const vxm_pose& T, double x, double y, double z, double out[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    out[i] = __dadd_rn(sum3(__dmul_rn(T.R[3 * i], x), __dmul_rn(T.R[3 * i + 1], y),
+                            __dmul_rn(T.R[3 * i + 2], z)),
+                       T.t[i]);
+}
+
+__device__ inline void mark_cell(const Cube& c, int32_t x, int32_t y, int32_t z,
+                                 DevStatus* status) {
+  uint32_t w, m;
+  if (!c.locate(x, y, z, w, m)) {
+    atomicOr(&status->bitmap_overflow, 1u);
+    return;
+  }
+  if (!(c.bits[w] & m)) atomicOr(c.bits + w, m);
+}
+
+// traverse_grid — traversal.hpp:29-73, visiting into the bitmap.
+__device__ void traverse(const double s[3], const double e[3], double cs, const Cube& cube,
+                         DevStatus* status) {
+  double d[3], t_max[3], t_delta[3];
+  int cell[3], end_cell[3], step[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    d[i] = __dsub_rn(e[i], s[i]);
+    cell[i] = int(floor(__ddiv_rn(s[i], cs)));
+    end_cell[i] = int(floor(__ddiv_rn(e[i], cs)));
+    step[i] = 0;
+    t_max[i] = CUDART_INF;
+    t_delta[i] = CUDART_INF;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    if (d[i] > 0.0) {
+      step[i] = 1;
+      t_delta[i] = __ddiv_rn(cs, d[i]);
+      t_max[i] = __ddiv_rn(__dsub_rn(__dmul_rn(double(cell[i] + 1), cs), s[i]), d[i]);
+    } else if (d[i] < 0.0) {
+      step[i] = -1;
+      t_delta[i] = __ddiv_rn(-cs, d[i]);
+      t_max[i] = __ddiv_rn(__dsub_rn(__dmul_rn(double(cell[i]), cs), s[i]), d[i]);
+    }
+  }
+  mark_cell(cube, cell[0], cell[1], cell[2], status);
+  int guard = abs(end_cell[0] - cell[0]) + abs(end_cell[1] - cell[1]) +
+              abs(end_cell[2] - cell[2]) + 3;
+  while (guard-- > 0) {
+    int axis = 0;
+    if (t_max[1] < t_max[0]) axis = 1;
+    if (t_max[2] < t_max[axis]) axis = 2;
+    if (t_max[axis] > 1.0) break;
+    cell[axis] += step[axis];
+    t_max[axis] = __dadd_rn(t_max[axis], t_delta[axis]);
+    mark_cell(cube, cell[0], cell[1], cell[2], status);
+  }
+}
+
+__device__ inline bool valid_depth(float d) { return d > 0.0f && isfinite(d); }
+
+// reach = std::min(depth, max_int) + truncation — view.cpp:49-51
+__device__ inline double ray_reach(double depth, double max_int, double trunc) {
+  const double capped = max_int < depth ? max_int : depth;
+  return __dadd_rn(capped, trunc);
+}
+
+// Camera: one thread per pixel tile — view.cpp:66-91.
+__global__ void k_rays_camera(const float* __restrict__ depth, int W, int H, int tile,
+                              vxm_camera cam, vxm_pose T, double cs, double max_int, double trunc,
+                              Cube cube, DevStatus* status) {
+  const int tiles_x = (W + tile - 1) / tile;
+  const int tiles_y = (H + tile - 1) / tile;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= tiles_x * tiles_y) return;
+  const int col0 = (t % tiles_x) * tile, row0 = (t / tiles_x) * tile;
+  const int row1 = min(row0 + tile, H), col1 = min(col0 + tile, W);
+  float tile_max = 0.0f;
+  for (int r = row0; r < row1; ++r)
+    for (int c = col0; c < col1; ++c) {
+      const float d = __ldg(depth + size_t(r) * W + c);
+      if (valid_depth(d)) tile_max = tile_max < d ? d : tile_max;
+    }
+  if (tile_max <= 0.0f) return;
+  const double u = 0.5 * double(col0 + col1), v = 0.5 * double(row0 + row1);
+  const double reach = ray_reach(double(tile_max), max_int, trunc);
+  // CameraIntrinsics::unproject — camera.hpp:52-55: (u - cu) / fu * depth
+  const double end_S[3] = {__dmul_rn(__ddiv_rn(__dsub_rn(u, cam.cu), cam.fu), reach),
+                           __dmul_rn(__ddiv_rn(__dsub_rn(v, cam.cv), cam.fv), reach), reach};
+  double end_L[3];
+  pose_apply(T, end_S[0], end_S[1], end_S[2], end_L);
+  traverse(T.t, end_L, cs, cube, status);
+}
+
+// LiDAR: one thread per valid pixel — view.cpp:94-111.  The per-pixel unit
+// directions (lidar.hpp:68-74, glibc sin/cos) come from a host-built LUT.
+__global__ void k_rays_lidar(const float* __restrict__ depth, int W, int H,
+                             const double* __restrict__ dirs, vxm_pose T, double cs,
+                             double max_int, double trunc, Cube cube, DevStatus* status) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= W * H) return;
+  const float d = __ldg(depth + p);
+  if (!valid_depth(d)) return;
+  const double reach = ray_reach(double(d), max_int, trunc);
+  const double end_S[3] = {__dmul_rn(__ldg(dirs + 3 * p), reach),
+                           __dmul_rn(__ldg(dirs + 3 * p + 1), reach),
+                           __dmul_rn(__ldg(dirs + 3 * p + 2), reach)};
+  double end_L[3];
+  pose_apply(T, end_S[0], end_S[1], end_S[2], end_L);
+  traverse(T.t, end_L, cs, cube, status);
+}
+
+__device__ inline uint32_t zdilate(uint32_t prev, uint32_t w, uint32_t next) {
+  return w | (w << 1) | (w >> 1) | (prev >> 31) | (next << 31);
+}
+
+__device__ inline bool owned(int32_t x, int rank, int world, int slab) {
+  if (world <= 1) return true;
+  const int32_t q = x >= 0 ? x / slab : -((-x + slab - 1) / slab);
+  return ((q % world) + world) % world == rank;
+}
+
+struct AllocArgs {
+  HashView hash;           // mask == 0 and keys == nullptr: no allocation
+  uint64_t* slot_keys;
+  LayerMeta* meta;
+  uint32_t capacity;       // physical pool slots
+  uint64_t max_blocks;     // Layer::max_blocks
+};
+
+// Dilation + ordered emission + fused allocation.  One thread per word.
+__global__ void __launch_bounds__(256) k_dilate_alloc(Cube cube, uint32_t n_words, AllocArgs al,
+                                                      int rank, int world, int slab,
+                                                      uint64_t* __restrict__ cand_keys,
+                                                      int32_t* __restrict__ cand_slots,
+                                                      DevStatus* status, ScanTiles st) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_scan[64];
+  __shared__ uint32_t s_pre[2];
+  __shared__ uint32_t s_base;
+  scan_prepare_next(st);
+  const uint32_t tile = scan_take_tile(st, &s_tile);
+  const uint32_t wi = tile * blockDim.x + threadIdx.x;
+  const bool do_alloc = al.hash.keys != nullptr;
+  if (threadIdx.x == 0) s_base = do_alloc ? al.meta->num_blocks : 0u;
+  uint32_t dil = 0;
+  int32_t bx = 0, by = 0, bz0 = 0;
+  if (wi < n_words) {
+    const int32_t S = cube.S, SZw = cube.SZw;
+    const int32_t wz = int32_t(wi % uint32_t(SZw));
+    const uint32_t t = wi / uint32_t(SZw);
+    const int32_t dy = int32_t(t % uint32_t(S)), dx = int32_t(t / uint32_t(S));
+    for (int ddx = -1; ddx <= 1; ++ddx) {
+      const int32_t xx = dx + ddx;
+      if (xx < 0 || xx >= S) continue;
+      for (int ddy = -1; ddy <= 1; ++ddy) {
+        const int32_t yy = dy + ddy;
+        if (yy < 0 || yy >= S) continue;
+        const uint32_t* row = cube.bits + (uint32_t(xx) * uint32_t(S) + uint32_t(yy)) * uint32_t(SZw);
+        const uint32_t w = row[wz];
+        const uint32_t prev = wz > 0 ? row[wz - 1] : 0u;
+        const uint32_t next = wz + 1 < SZw ? row[wz + 1] : 0u;
+        dil |= zdilate(prev, w, next);
+      }
+    }
+    const int32_t zbits = S - wz * 32;  // valid bits in this word
+    if (zbits < 32) dil &= (zbits <= 0 ? 0u : ((1u << zbits) - 1u));
+    bx = cube.ox + dx;
+    by = cube.oy + dy;
+    bz0 = cube.oz + wz * 32;
+    if (!owned(bx, rank, world, slab)) dil = 0;
+  }
+  // count candidates and new blocks
+  uint32_t n_c = __popc(dil), n_new = 0;
+  uint32_t new_mask = 0;
+  if (do_alloc && dil) {
+    for (uint32_t m = dil; m; m &= m - 1) {
+      const int b = __ffs(m) - 1;
+      const uint64_t k = pack_key(bx, by, bz0 + b);
+      if (hash_find_rw(al.hash, k) < 0) {
+        new_mask |= 1u << b;
+        ++n_new;
+      }
+    }
+  }
+  uint32_t ea, eb, ta, tb;
+  block_scan2(n_c, n_new, ea, eb, ta, tb, s_scan);
+  if (threadIdx.x == 0) {
+    uint32_t pa, pb;
+    scan_lookback(st, tile, ta, tb, pa, pb);
+    s_pre[0] = pa;
+    s_pre[1] = pb;
+  }
+  __syncthreads();
+  const uint32_t base = s_base;
+  const uint64_t limit = al.capacity < al.max_blocks ? uint64_t(al.capacity) : al.max_blocks;
+  uint32_t pos = s_pre[0] + ea, npos = s_pre[1] + eb;
+  for (uint32_t m = dil; m; m &= m - 1) {
+    const int b = __ffs(m) - 1;
+    const uint64_t k = pack_key(bx, by, bz0 + b);
+    int32_t slot = 0;
+    if (do_alloc) {
+      if (new_mask & (1u << b)) {
+        const uint64_t s = uint64_t(base) + npos++;
+        if (s < limit) {
+          hash_insert(al.hash, k, int32_t(s));
+          al.slot_keys[s] = k;
+          slot = int32_t(s) | int32_t(0x80000000u);
+        } else {
+          slot = -1;
+        }
+      } else {
+        slot = hash_find_rw(al.hash, k);
+      }
+    }
+    cand_keys[pos] = k;
+    cand_slots[pos] = slot;
+    ++pos;
+  }
+  // The last tile publishes totals (all earlier tiles have read s_base: they
+  // published before this tile's look-back could complete).
+  if (threadIdx.x == 0 && tile == gridDim.x - 1) {
+    const uint32_t total_c = s_pre[0] + ta, total_n = s_pre[1] + tb;
+    status->n_candidates = total_c;
+    status->n_new = total_n;
+    if (do_alloc) {
+      const uint64_t want = uint64_t(base) + total_n;
+      // Physical pool too small (and the logical limit not yet reached):
+      // the host grows the pool and re-runs; otherwise MapCapacityError.
+      if (want > al.capacity && al.capacity < al.max_blocks) status->pool_overflow = 1u;
+      if (want > al.max_blocks) status->capacity_error = 1u;
+      al.meta->num_blocks = uint32_t(want < limit ? want : limit);
+    }
+  }
+}
+
+// ---- host driver ------------------------------------------------------------------
+static void ensure_lidar_lut(Context* ctx, const vxm_lidar& li) {
+  if (ctx->lut_valid && std::memcmp(&ctx->lut_key, &li, sizeof li) == 0) return;
+  const int W = li.num_azimuth, H = li.num_elevation;
+  std::vector<double> dirs(size_t(W) * H * 3);
+  // LidarIntrinsics::ray_direction(col + 0.5, row + 0.5) — lidar.hpp:68-74,
+  // evaluated with the host libm exactly as the reference does.
+  const double raz = li.azimuth_fov / li.num_azimuth;
+  const double rel = li.elevation_fov / li.num_elevation;
+  for (int row = 0; row < H; ++row)
+    for (int col = 0; col < W; ++col) {
+      const double az = li.azimuth_start + (col + 0.5) * raz;
+      const double polar = li.elevation_start + (row + 0.5) * rel;
+      const double sp = std::sin(polar);
+      double* d = &dirs[(size_t(row) * W + col) * 3];
+      d[0] = std::cos(az) * sp;
+      d[1] = std::sin(az) * sp;
+      d[2] = std::cos(polar);
+    }
+  ctx->lidar_dirs.ensure(dirs.size() * sizeof(double));
+  VXM_CUDA(cudaMemcpyAsync(ctx->lidar_dirs.p, dirs.data(), dirs.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->lut_key = li;
+  ctx->lut_valid = true;
+}
+
+void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out) {
+  const double cs = a.block_size;
+  // Cube of cells any ray (plus one dilation ring) can reach.
+  double norm_max;
+  const double reach_max = a.cfg.max_integration_distance + a.cfg.truncation;
+  if (!a.lidar) {
+    const double ax = std::max(std::fabs(a.cam.cu), std::fabs(a.width - a.cam.cu)) / std::fabs(a.cam.fu);
+    const double ay = std::max(std::fabs(a.cam.cv), std::fabs(a.height - a.cam.cv)) / std::fabs(a.cam.fv);
+    norm_max = std::fabs(reach_max) * std::sqrt(1.0 + ax * ax + ay * ay);
+  } else {
+    norm_max = std::fabs(reach_max);
+  }
+  norm_max = norm_max * 1.0001 + 1e-9;
+  const double rc = std::ceil(norm_max / cs) + 3.0;
+  if (!(rc < 1e6)) throw Error(VXM_ERR_INVALID_ARGUMENT, "view volume too large");
+  const int32_t r = int32_t(rc);
+  const int32_t S = 2 * r + 1;
+  const int32_t SZw = (S + 31) / 32;
+  const uint64_t n_words = uint64_t(S) * uint64_t(S) * uint64_t(SZw);
+  if (n_words * 4 > (uint64_t(1) << 31))
+    throw Error(VXM_ERR_INVALID_ARGUMENT,
+                "view volume too large for the candidate bitmap (max_integration_distance / block "
+                "size ratio)");
+  Cube cube;
+  const int64_t ocx = int64_t(std::floor(a.T_LS.t[0] / cs));
+  const int64_t ocy = int64_t(std::floor(a.T_LS.t[1] / cs));
+  const int64_t ocz = int64_t(std::floor(a.T_LS.t[2] / cs));
+  if (!coord_ok(ocx - r) || !coord_ok(ocx + r) || !coord_ok(ocy - r) || !coord_ok(ocy + r) ||
+      !coord_ok(ocz - r) || !coord_ok(ocz + r))
+    throw Error(VXM_ERR_INVALID_ARGUMENT, "sensor position outside the supported block range");
+  cube.ox = int32_t(ocx - r);
+  cube.oy = int32_t(ocy - r);
+  cube.oz = int32_t(ocz - r);
+  cube.S = S;
+  cube.SZw = SZw;
+  ctx->bitmap.ensure(n_words * 4);
+  cube.bits = ctx->bitmap.as<uint32_t>();
+  VXM_CUDA(cudaMemsetAsync(cube.bits, 0, n_words * 4, ctx->stream));
+  ctx->count_launch();
+
+  if (!a.lidar) {
+    const int tile = std::max(1, a.cfg.pixel_subsample);
+    const int nt = ((a.width + tile - 1) / tile) * ((a.height + tile - 1) / tile);
+    if (nt > 0) {
+      k_rays_camera<<<ceil_div(nt, 128), 128, 0, ctx->stream>>>(
+          a.depth_dev, a.width, a.height, tile, a.cam, a.T_LS, cs,
+          a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
+      ctx->count_launch();
+    }
+  } else {
+    ensure_lidar_lut(ctx, a.li);
+    const int np = a.width * a.height;
+    if (np > 0) {
+      k_rays_lidar<<<ceil_div(np, 128), 128, 0, ctx->stream>>>(
+          a.depth_dev, a.width, a.height, ctx->lidar_dirs.as<double>(), a.T_LS, cs,
+          a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
+      ctx->count_launch();
+    }
+  }
+  check_launch(ctx, "k_rays");
+
+  // Candidate arrays: bounded by the cube's cell count.
+  const uint64_t max_cand = uint64_t(S) * S * S;
+  const uint32_t cand_cap = uint32_t(std::min<uint64_t>(max_cand, (uint64_t(1) << 31) - 1));
+  ctx->cand_keys.ensure(sizeof(uint64_t) * cand_cap);
+  ctx->cand_slots.ensure(sizeof(int32_t) * cand_cap);
+  AllocArgs al{};
+  if (L) {
+    al.hash = L->hash;
+    al.slot_keys = L->slot_keys;
+    al.meta = L->meta;
+    al.capacity = L->capacity;
+    al.max_blocks = L->max_blocks;
+  }
+  const uint32_t tiles = ceil_div(n_words, 256);
+  const ScanTiles st = ctx->next_scan(tiles);
+  k_dilate_alloc<<<tiles, 256, 0, ctx->stream>>>(cube, uint32_t(n_words), al, ctx->rank, ctx->world,
+                                                 ctx->slab, ctx->cand_keys.as<uint64_t>(),
+                                                 ctx->cand_slots.as<int32_t>(), ctx->d_status, st);
+  ctx->count_launch();
+  check_launch(ctx, "k_dilate_alloc");
+  if (cand_cap_out) *cand_cap_out = cand_cap;
+}
+
+}  // namespace vxm

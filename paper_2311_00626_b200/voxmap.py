@@ -1,0 +1,397 @@
+"""Python host mirror of the reference's C++ mapper API (namespace ``voxmap``,
+/root/reference/proj/include), over the C-ABI of libvoxmap_b200.so.
+
+Names, argument meaning and error behaviour follow the reference:
+
+=====================================  ==============================================
+reference (proj/include/voxmap/...)    here
+=====================================  ==============================================
+Layer<TsdfVoxel>, Layer<EsdfVoxel>     TsdfLayer, EsdfLayer        core/layer.hpp:47-125
+integrate_depth (camera / lidar)       integrate_depth             integrate/integrator.hpp:36-45
+blocks_in_view                         blocks_in_view              sensor/view.hpp:38-48
+update_esdf / mark_sites /             update_esdf / mark_sites /  esdf/integrator.hpp:81-120
+clear_invalid / lower_esdf             clear_invalid / lower_esdf
+EsdfUpdateState                        EsdfUpdateState             esdf/integrator.hpp:67-74
+query_batch                            query_batch                 query/query.hpp:59-62
+InvalidPoseError / MapCapacityError /  InvalidPoseError / MapCapacityError / InvalidArgumentError
+std::invalid_argument                  (a ValueError)
+=====================================  ==============================================
+
+Block lists are ``(N, 3) int32`` numpy arrays of GridIndex in lexicographic
+order; voxel blocks are numpy structured arrays (TSDF_DTYPE / ESDF_DTYPE).
+There is no CPU fallback: without a B200 every compute call raises
+``VoxmapCudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import _abi as A
+from ._abi import (Camera as CameraIntrinsics, Lidar as LidarIntrinsics,  # noqa: F401
+                   default_camera as default_camera_intrinsics,
+                   default_lidar as default_lidar_intrinsics,
+                   default_integrator_config as IntegratorConfig,
+                   default_esdf_config as EsdfConfig, TSDF_DTYPE, ESDF_DTYPE, QUERY_DTYPE)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libvoxmap_b200.so")
+
+
+class VoxmapError(RuntimeError):
+    pass
+
+
+class InvalidPoseError(VoxmapError):
+    """voxmap::InvalidPoseError (sensor/pose.hpp:23-26)."""
+
+
+class MapCapacityError(VoxmapError):
+    """voxmap::MapCapacityError (core/layer.hpp:28-31)."""
+
+
+class InvalidArgumentError(VoxmapError, ValueError):
+    """std::invalid_argument."""
+
+
+class VoxmapCudaError(VoxmapError):
+    """No usable sm_100 device / CUDA failure (there is no CPU fallback)."""
+
+
+_ERRORS = {A.VXM_ERR_INVALID_POSE: InvalidPoseError, A.VXM_ERR_INVALID_ARGUMENT: InvalidArgumentError,
+           A.VXM_ERR_CAPACITY: MapCapacityError, A.VXM_ERR_CUDA: VoxmapCudaError,
+           A.VXM_ERR_INTERNAL: VoxmapError}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib():
+    """Loads libvoxmap_b200.so (fails loudly when it was not built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                                  "(make -C paper_2311_00626_b200)")
+            L = C.CDLL(LIB_PATH)
+            L.vxm_last_error.restype = C.c_char_p
+            L.vxm_version.restype = C.c_char_p
+            L.vxm_layer_voxel_size.restype = C.c_double
+            L.vxm_context_launch_count.restype = C.c_uint64
+            L.vxm_synth_scene_sdf.restype = C.c_double
+            L.vxm_pose_valid.restype = C.c_int
+            _lib = L
+        return _lib
+
+
+def check(rc):
+    if rc != A.VXM_OK:
+        raise _ERRORS.get(rc, VoxmapError)(lib().vxm_last_error().decode())
+
+
+class Pose:
+    """Pose (sensor/pose.hpp:30-60): p_parent = R @ p_child + t."""
+
+    def __init__(self, R=None, t=None):
+        self.R = np.eye(3) if R is None else np.asarray(R, dtype=np.float64).reshape(3, 3)
+        self.t = np.zeros(3) if t is None else np.asarray(t, dtype=np.float64).reshape(3)
+
+    @staticmethod
+    def from_c(p: A.PoseC) -> "Pose":
+        R, t = A.pose_arrays(p)
+        return Pose(R, t)
+
+    def c(self) -> A.PoseC:
+        return A.pose_c(self.R, self.t)
+
+    def valid(self) -> bool:
+        return bool(lib().vxm_pose_valid(C.byref(self.c())))
+
+    def inverse(self) -> "Pose":
+        o = A.PoseC()
+        lib().vxm_pose_inverse(C.byref(self.c()), C.byref(o))
+        return Pose.from_c(o)
+
+
+def _pose_c(T):
+    return T.c() if isinstance(T, Pose) else T
+
+
+class Context:
+    """One CUDA device + stream (calls on a context are serialized)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().vxm_context_create(C.c_int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def __del__(self):
+        try:
+            lib().vxm_context_destroy(self.h)
+        except Exception:
+            pass
+
+    def synchronize(self):
+        check(lib().vxm_context_synchronize(self.h))
+
+    def set_shard(self, rank: int, world: int, slab: int = 16):
+        check(lib().vxm_context_set_shard(self.h, rank, world, slab))
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().vxm_context_launch_count(self.h))
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("VOXMAP_DEVICE", "0")))
+    return _default_ctx
+
+
+class BlockList:
+    """Library-owned std::vector<GridIndex> (device-resident, host on demand)."""
+
+    def __init__(self, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib().vxm_blocklist_create(self.ctx.h, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().vxm_blocklist_destroy(self.h)
+        except Exception:
+            pass
+
+    def numpy(self) -> np.ndarray:
+        p = C.c_void_p()
+        n = C.c_uint64()
+        check(lib().vxm_blocklist_host(self.h, C.byref(p), C.byref(n)))
+        return A.keys_array(p, n.value)
+
+    def assign(self, keys):
+        k = A.as_keys(keys)
+        check(lib().vxm_blocklist_assign(self.h, A.ptr(k), C.c_uint64(len(k))))
+        return self
+
+
+class _Layer:
+    kind = None
+    dtype = None
+
+    def __init__(self, voxel_size: float, max_blocks: int = 0, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib().vxm_layer_create(self.ctx.h, C.c_int(self.kind), C.c_double(voxel_size),
+                                     C.c_uint64(max_blocks), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().vxm_layer_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def voxel_size(self) -> float:
+        return float(lib().vxm_layer_voxel_size(self.h))
+
+    @property
+    def block_size(self) -> float:
+        return self.voxel_size * A.VOXELS_PER_SIDE
+
+    def num_blocks(self) -> int:
+        n = C.c_uint64()
+        check(lib().vxm_layer_num_blocks(self.h, C.byref(n)))
+        return n.value
+
+    def has_blocks(self, keys) -> np.ndarray:
+        k = A.as_keys(keys)
+        out = np.zeros(len(k), np.uint8)
+        check(lib().vxm_layer_has_blocks(self.h, A.ptr(k), C.c_uint64(len(k)), A.ptr(out)))
+        return out.astype(bool)
+
+    def has_block(self, g) -> bool:
+        return bool(self.has_blocks([g])[0])
+
+    def export(self):
+        """(sorted keys (N,3) int32, voxels (N,512) structured)."""
+        n = self.num_blocks()
+        keys = np.zeros((n, 3), np.int32)
+        vox = np.zeros((n, A.VOXELS_PER_BLOCK), self.dtype)
+        check(lib().vxm_layer_export(self.h, A.ptr(keys), A.ptr(vox), C.c_uint64(n)))
+        return keys, vox
+
+    def sorted_indices(self) -> np.ndarray:
+        n = self.num_blocks()
+        keys = np.zeros((n, 3), np.int32)
+        check(lib().vxm_layer_export(self.h, A.ptr(keys), C.c_void_p(0), C.c_uint64(n)))
+        return keys
+
+    def read_blocks(self, keys):
+        k = A.as_keys(keys)
+        vox = np.zeros((len(k), A.VOXELS_PER_BLOCK), self.dtype)
+        found = np.zeros(len(k), np.uint8)
+        check(lib().vxm_layer_read_blocks(self.h, A.ptr(k), C.c_uint64(len(k)), A.ptr(vox),
+                                          A.ptr(found)))
+        return vox, found.astype(bool)
+
+    def block(self, g):
+        vox, found = self.read_blocks([g])
+        return vox[0] if found[0] else None
+
+    def write_blocks(self, keys, voxels):
+        """get_or_allocate + overwrite (host writes through block_ptr)."""
+        k = A.as_keys(keys)
+        v = np.ascontiguousarray(np.asarray(voxels, self.dtype).reshape(len(k), A.VOXELS_PER_BLOCK))
+        check(lib().vxm_layer_write_blocks(self.h, A.ptr(k), C.c_uint64(len(k)), A.ptr(v)))
+
+    def clone(self):
+        h = C.c_void_p()
+        check(lib().vxm_layer_clone(self.h, C.byref(h)))
+        out = object.__new__(type(self))
+        out.ctx = self.ctx
+        out.h = h
+        return out
+
+
+class TsdfLayer(_Layer):
+    kind = A.LAYER_TSDF
+    dtype = A.TSDF_DTYPE
+
+
+class EsdfLayer(_Layer):
+    kind = A.LAYER_ESDF
+    dtype = A.ESDF_DTYPE
+
+
+def _depth(depth):
+    d = np.ascontiguousarray(depth, dtype=np.float32)
+    if d.ndim != 2:
+        raise InvalidArgumentError("depth image must be 2-D (height, width)")
+    return d
+
+
+def integrate_depth(layer: TsdfLayer, depth, T_LS, intrinsics, cfg=None, out: BlockList | None = None):
+    """integrate_depth (integrate/integrator.hpp:36-45): fuses one frame and
+    returns the sorted indices of the blocks whose bytes changed."""
+    cfg = cfg or IntegratorConfig()
+    d = _depth(depth)
+    out = out or BlockList(layer.ctx)
+    fn = (lib().vxm_integrate_depth_camera if isinstance(intrinsics, A.Camera)
+          else lib().vxm_integrate_depth_lidar)
+    check(fn(layer.h, A.ptr(d), C.c_int(d.shape[1]), C.c_int(d.shape[0]), C.byref(_pose_c(T_LS)),
+             C.byref(intrinsics), C.byref(cfg), out.h))
+    return out.numpy()
+
+
+def integrate_depth_device(layer: TsdfLayer, depth_dev_ptr: int, width: int, height: int, T_LS,
+                           intrinsics, cfg, out: BlockList) -> BlockList:
+    """Device-resident variant (depth already in HBM; changed list stays on device)."""
+    fn = (lib().vxm_integrate_depth_camera_device if isinstance(intrinsics, A.Camera)
+          else lib().vxm_integrate_depth_lidar_device)
+    check(fn(layer.h, C.c_void_p(depth_dev_ptr), C.c_int(width), C.c_int(height),
+             C.byref(_pose_c(T_LS)), C.byref(intrinsics), C.byref(cfg), out.h))
+    return out
+
+
+def blocks_in_view(T_LS, intrinsics, depth, block_size, cfg=None, ctx: Context | None = None):
+    """blocks_in_view (sensor/view.hpp:38-48): sorted unique candidate blocks."""
+    ctx = ctx or default_context()
+    cfg = cfg or A.ViewConfigC(5.0, 0.2, 8)
+    d = _depth(depth)
+    out = BlockList(ctx)
+    fn = (lib().vxm_blocks_in_view_camera if isinstance(intrinsics, A.Camera)
+          else lib().vxm_blocks_in_view_lidar)
+    check(fn(ctx.h, C.byref(_pose_c(T_LS)), C.byref(intrinsics), A.ptr(d), C.c_int(d.shape[1]),
+             C.c_int(d.shape[0]), C.c_double(block_size), C.byref(cfg), out.h))
+    return out.numpy()
+
+
+def update_esdf(esdf: EsdfLayer, tsdf: TsdfLayer, updated, cfg=None, out: BlockList | None = None):
+    """update_esdf (esdf/integrator.hpp:113-116). `updated` may be a BlockList
+    (e.g. the device-resident output of integrate_depth) or an (N,3) array."""
+    cfg = cfg or EsdfConfig()
+    out = out or BlockList(esdf.ctx)
+    if isinstance(updated, BlockList):
+        check(lib().vxm_update_esdf_list(esdf.h, tsdf.h, updated.h, C.byref(cfg), out.h))
+    else:
+        k = A.as_keys(updated)
+        check(lib().vxm_update_esdf(esdf.h, tsdf.h, A.ptr(k), C.c_uint64(len(k)), C.byref(cfg),
+                                    out.h))
+    return out.numpy()
+
+
+class EsdfUpdateState:
+    """EsdfUpdateState (esdf/integrator.hpp:67-74)."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(lib().vxm_esdf_state_create(C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().vxm_esdf_state_destroy(self.h)
+        except Exception:
+            pass
+
+    def _get(self, which):
+        p = C.c_void_p()
+        n = C.c_uint64()
+        check(lib().vxm_esdf_state_get(self.h, C.c_int(which), C.byref(p), C.byref(n)))
+        return A.keys_array(p, n.value)
+
+    def _set(self, which, keys):
+        k = A.as_keys(keys)
+        check(lib().vxm_esdf_state_set(self.h, C.c_int(which), A.ptr(k), C.c_uint64(len(k))))
+
+    indices_to_update = property(lambda s: s._get(0), lambda s, v: s._set(0, v))
+    indices_to_clear = property(lambda s: s._get(1), lambda s, v: s._set(1, v))
+    cleared_indices = property(lambda s: s._get(2), lambda s, v: s._set(2, v))
+
+
+def mark_sites(esdf, tsdf, updated, cfg, state: EsdfUpdateState):
+    k = A.as_keys(updated)
+    out = BlockList(esdf.ctx)
+    check(lib().vxm_esdf_mark_sites(esdf.h, tsdf.h, A.ptr(k), C.c_uint64(len(k)), C.byref(cfg),
+                                    state.h, out.h))
+    return out.numpy()
+
+
+def clear_invalid(esdf, cfg, state: EsdfUpdateState):
+    out = BlockList(esdf.ctx)
+    check(lib().vxm_esdf_clear_invalid(esdf.h, C.byref(cfg), state.h, out.h))
+    return out.numpy()
+
+
+def lower_esdf(esdf, state: EsdfUpdateState, cfg):
+    """Returns (rounds, changed)."""
+    out = BlockList(esdf.ctx)
+    rounds = C.c_int()
+    check(lib().vxm_esdf_lower(esdf.h, state.h, C.byref(cfg), out.h, C.byref(rounds)))
+    return rounds.value, out.numpy()
+
+
+def query_batch(esdf: EsdfLayer, points, want_gradient: bool = False, interpolate: bool = True):
+    """query_batch (query/query.hpp:59-62): structured array (known, distance, gradient)."""
+    x = np.ascontiguousarray(np.asarray(points, np.float64).reshape(-1, 3))
+    out = np.zeros(len(x), A.QUERY_DTYPE)
+    cfg = A.QueryConfigC(int(interpolate), 1)
+    check(lib().vxm_query_batch(esdf.h, A.ptr(x), C.c_uint64(len(x)), C.c_int(int(want_gradient)),
+                                C.byref(cfg), A.ptr(out)))
+    return out
+
+
+def esdf_distance(sq, inside, voxel_size):
+    """esdf_distance (esdf/integrator.hpp:59-63)."""
+    d = np.sqrt(np.asarray(sq, np.float64)) * voxel_size
+    return np.where(inside, -d, d)

@@ -1,0 +1,192 @@
+"""GPU parity: block allocation + TSDF integration vs the CPU oracle.
+
+Mirrors the reference's cross-implementation tests
+(proj/tests/integrate_test.cpp:225-363, sensor_test.cpp:266-327): bitwise
+identical changed lists and layers for the camera path, exact block sets and
+observed masks plus 1e-5 relative values for LiDAR (CUDA vs glibc atan2/acos).
+"""
+import numpy as np
+import pytest
+
+from paper_2311_00626_b200 import _abi as A
+from tests.helpers import camera_frames, layers_identical, lidar_frames, tsdf_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_camera(vx, port, scene, w, h, vs, frames, orbit, cfg):
+    cam, seq = camera_frames(scene, w, h, frames, orbit)
+    g = vx.TsdfLayer(vs)
+    o = port.layer(A.LAYER_TSDF, vs)
+    total = 0
+    for T, d in seq:
+        a = vx.integrate_depth(g, d, T, cam, cfg)
+        b = port.integrate_camera(o, d, T, cam, cfg)
+        total += len(a)  # a frame from inside a solid is legitimately empty
+        assert np.array_equal(a, b), (len(a), len(b))
+    assert total > 0
+    ka, va = g.export()
+    kb, vb = o.export()
+    assert layers_identical(ka, va, kb, vb)
+    return g
+
+
+def test_camera_nearest_bitwise(vx, port):
+    _run_camera(vx, port, "sphere_in_box", 160, 120, 0.05, 3, 8,
+                A.default_integrator_config(truncation=0.2))
+
+
+def test_camera_linear_bitwise(vx, port):
+    _run_camera(vx, port, "sphere_in_box", 160, 120, 0.05, 3, 8,
+                A.default_integrator_config(truncation=0.2, camera_sample=A.SAMPLE_LINEAR))
+
+
+def test_camera_inverse_square_bitwise(vx, port):
+    _run_camera(vx, port, "room", 160, 120, 0.05, 3, 8,
+                A.default_integrator_config(truncation=0.2, weighting=A.WEIGHT_INVERSE_SQUARE))
+
+
+def test_c1_sphere_in_box_640x480_5cm(vx, port):
+    """BASELINE config C1 (first 12 of the 100-frame orbit)."""
+    _run_camera(vx, port, "sphere_in_box", 640, 480, 0.05, 12, 100,
+                A.default_integrator_config(truncation=0.2))
+
+
+def test_c2_room_640x480_2cm(vx, port):
+    """BASELINE config C2 integration part (3 frames), make_replay_config(0.02)."""
+    _run_camera(vx, port, "room", 640, 480, 0.02, 3, 100,
+                A.default_integrator_config(truncation=0.08))
+
+
+def test_lidar_inverse_square(vx, port):
+    li, seq = lidar_frames("sphere_in_box", 180, 16, 3, 8)
+    cfg = A.default_integrator_config(truncation=0.2, weighting=A.WEIGHT_INVERSE_SQUARE)
+    g = vx.TsdfLayer(0.05)
+    o = port.layer(A.LAYER_TSDF, 0.05)
+    for T, d in seq:
+        a = vx.integrate_depth(g, d, T, li, cfg)
+        b = port.integrate_lidar(o, d, T, li, cfg)
+        assert len(a) > 0
+        assert np.array_equal(a, b)
+    ka, va = g.export()
+    kb, vb = o.export()
+    assert np.array_equal(ka, kb)                                   # allocated set exact
+    assert np.array_equal(va["weight"] > 0, vb["weight"] > 0)      # observed mask exact
+    assert tsdf_close(va, vb)
+
+
+def test_changed_list_names_exactly_changed_blocks(vx):
+    """integrate_test.cpp:324-363."""
+    cam, seq = camera_frames("sphere_in_box", 160, 120, 1, 8)
+    T, d = seq[0]
+    cfg = A.default_integrator_config(truncation=0.2)
+    L = vx.TsdfLayer(0.05)
+    first = vx.integrate_depth(L, d, T, cam, cfg)
+    assert len(first)
+    keys = [tuple(k) for k in first]
+    assert keys == sorted(set(keys))
+    assert L.has_blocks(first).all()
+    kb, before = L.export()
+    second = vx.integrate_depth(L, d, T, cam, cfg)
+    assert np.array_equal(first, second)
+    ka, after = L.export()
+    assert np.array_equal(ka, kb)
+    changed = np.array([before[i].tobytes() != after[i].tobytes() for i in range(len(ka))])
+    reported = {tuple(k) for k in second}
+    assert all((tuple(ka[i]) in reported) == changed[i] for i in range(len(ka)))
+    assert (~changed).sum() > 0  # fully occluded candidates are allocated but untouched
+
+
+def test_blocks_in_view_camera_and_lidar(vx, port):
+    cam, seq = camera_frames("room", 320, 240, 2, 8)
+    vcfg = A.ViewConfigC(5.0, 0.2, 8)
+    for T, d in seq:
+        a = vx.blocks_in_view(T, cam, d, 0.4, vcfg)
+        b = port.blocks_in_view_camera(T, cam, d, 0.4, vcfg)
+        assert np.array_equal(a, b)
+    li, seq = lidar_frames("room", 256, 16, 2, 8)
+    for T, d in seq:
+        a = vx.blocks_in_view(T, li, d, 0.4, vcfg)
+        b = port.blocks_in_view_lidar(T, li, d, 0.4, vcfg)
+        assert np.array_equal(a, b)
+
+
+def test_view_candidates_random_depth(vx, port):
+    """sensor_test.cpp:266-327 shape: random depths, subsample 1, 0.8 m blocks."""
+    rng = np.random.default_rng(31)
+    cam = A.Camera(20.0, 20.0, 16.0, 12.0, 32, 24, 10.0)
+    d = rng.uniform(0.3, 8.0, (24, 32)).astype(np.float32)
+    d[5, 5] = 0.0
+    q = np.array([0.9, 0.1, -0.2, 0.3])
+    q /= np.linalg.norm(q)
+    w, x, y, z = q
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                  [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                  [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+    T = A.pose_c(R, [0.4, -0.2, 1.1])
+    vcfg = A.ViewConfigC(5.0, 0.2, 1)
+    assert np.array_equal(vx.blocks_in_view(T, cam, d, 0.8, vcfg),
+                          port.blocks_in_view_camera(T, cam, d, 0.8, vcfg))
+
+
+def test_rejects_malformed_frames_before_mutation(vx):
+    """integrate_test.cpp:447-488."""
+    cam = A.default_camera(64, 48)
+    cfg = A.default_integrator_config()
+    L = vx.TsdfLayer(0.05)
+    with pytest.raises(vx.InvalidArgumentError):
+        vx.integrate_depth(L, np.zeros((48, 32), np.float32), vx.Pose(), cam, cfg)
+    assert L.num_blocks() == 0
+    depth = np.full((48, 64), 2.0, np.float32)
+    bad = vx.Pose(t=[np.nan, 0, 0])
+    with pytest.raises(vx.InvalidPoseError):
+        vx.integrate_depth(L, depth, bad, cam, cfg)
+    with pytest.raises(vx.InvalidPoseError):
+        vx.integrate_depth(L, depth, vx.Pose(R=2.0 * np.eye(3)), cam, cfg)
+    assert L.num_blocks() == 0
+
+
+def test_capacity_error_matches_reference_semantics(vx, port):
+    """layer.hpp:74-86: allocate in sorted candidate order until full, then throw."""
+    cam, seq = camera_frames("sphere_in_box", 160, 120, 1, 8)
+    T, d = seq[0]
+    cfg = A.default_integrator_config(truncation=0.2)
+    g = vx.TsdfLayer(0.05, max_blocks=100)
+    with pytest.raises(vx.MapCapacityError):
+        vx.integrate_depth(g, d, T, cam, cfg)
+    o = port.layer(A.LAYER_TSDF, 0.05, max_blocks=100)
+    from oracle.bindings import OracleError
+    with pytest.raises(OracleError):
+        port.integrate_camera(o, d, T, cam, cfg)
+    ka, va = g.export()
+    kb, vb = o.export()
+    assert len(ka) == 100 and layers_identical(ka, va, kb, vb)
+
+
+def test_pool_growth_across_many_frames(vx, port):
+    """Forces several pool/hash growths (small initial pool) and checks parity."""
+    cam, seq = camera_frames("corridor", 320, 240, 6, 12)
+    cfg = A.default_integrator_config(truncation=0.04)
+    g = vx.TsdfLayer(0.01)
+    o = port.layer(A.LAYER_TSDF, 0.01)
+    for T, d in seq:
+        assert np.array_equal(vx.integrate_depth(g, d, T, cam, cfg), port.integrate_camera(o, d, T, cam, cfg))
+    ka, va = g.export()
+    kb, vb = o.export()
+    assert len(ka) > 4096 and layers_identical(ka, va, kb, vb)
+
+
+@pytest.mark.parametrize("case", ["camera_nearest_sphere_in_box", "camera_linear_sphere_in_box",
+                                  "camera_room_2cm"])
+def test_gpu_matches_reference_golden(vx, case):
+    """Replays the fixtures generated by the reference's own code
+    (tests/golden/make_golden.py) through the GPU path: identical changed lists
+    and identical layer digests (TSDF and ESDF)."""
+    import json
+
+    from tests.test_oracle import GOLDEN, replay_camera
+    with open(GOLDEN) as f:
+        g = json.load(f)
+    replay_camera(g[case], lambda L, d, p, cam, icfg: vx.integrate_depth(L, d, p, cam, icfg),
+                  lambda E, L, ch, e: vx.update_esdf(E, L, ch, e),
+                  lambda kind, vs: vx.TsdfLayer(vs) if kind == A.LAYER_TSDF else vx.EsdfLayer(vs))
