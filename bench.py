@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Per-frame map update benchmark (BASELINE.json metric).
+
+A step is one frame of the workload: integrate_depth (block allocation + TSDF
+integration) followed by update_esdf, for BASELINE config C2 by default
+(synthetic room trajectory, 640x480 depth, 2 cm voxels, ESDF every frame).
+
+  value  device-resident frames/s: depth frames already in HBM, the changed
+         block list stays on the device between integrate and ESDF.
+  e2e    the same frames through the public host API (host depth from pinned
+         memory copied in, changed lists copied out) — the reference-facing path.
+
+Timing: W untimed warm-up frames, then K timed frames; before every timed
+frame a 256 MB buffer is written to flush L2; CUDA events on the library's
+stream bracket each frame; N>1 takes the max over ranks.  `--impl reference`
+times the reference's own CPU implementation (oracle/_ref, OpenMP on all host
+cores) on the same workload instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TSDF voxel updates/s & frames/s (640x480, 2cm) at 1/2/4/8 GPU; ESDF ms/frame"
+UNIT = "frames/s"
+
+CONFIGS = {
+    # name: scene, sensor, size, voxel, truncation, max_int, esdf(site, max_dist), orbit
+    "c2": dict(scene="room", sensor="camera", w=640, h=480, vs=0.02, trunc=0.08, max_int=5.0,
+               esdf=(0.02, 2.0), orbit=100,
+               workload="C2: synthetic room trajectory, 640x480 depth, 2 cm voxels, "
+                        "TSDF integration + ESDF update every frame"),
+    "c1": dict(scene="sphere_in_box", sensor="camera", w=640, h=480, vs=0.05, trunc=0.2,
+               max_int=5.0, esdf=None, orbit=100,
+               workload="C1: sphere_in_box, 640x480 depth, 5 cm voxels, TSDF integration only"),
+    "c3": dict(scene="lidar_yard", sensor="lidar", w=2048, h=64, vs=0.1, trunc=0.4, max_int=100.0,
+               esdf=(0.1, 2.0), orbit=100,
+               workload="C3: 64-beam x 2048-column LiDAR, 10 cm voxels, 100 m range, TSDF + ESDF"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+def make_inputs(cfgname, n_frames, offset=0):
+    from paper_2311_00626_b200 import _abi as A
+    from paper_2311_00626_b200 import synth
+    c = CONFIGS[cfgname]
+    S = synth.Scene(c["scene"])
+    if c["sensor"] == "camera":
+        sensor = A.default_camera(c["w"], c["h"])
+    else:
+        sensor = A.default_lidar(c["w"], c["h"])
+        sensor.max_range = c["max_int"]
+    frames = []
+    for k in range(offset, offset + n_frames):
+        kk = k % c["orbit"]
+        T = S.orbit_pose(kk, c["orbit"], lidar=c["sensor"] == "lidar")
+        d = S.render_camera(T, sensor) if c["sensor"] == "camera" else S.render_lidar(T, sensor)
+        frames.append((T, d))
+    icfg = A.default_integrator_config(truncation=c["trunc"], max_integration_distance=c["max_int"])
+    ecfg = A.default_esdf_config(site_threshold=c["esdf"][0], max_distance=c["esdf"][1]) if c["esdf"] else None
+    return sensor, frames, icfg, ecfg
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu capture summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, device):
+    import numpy as np
+    import torch
+
+    import paper_2311_00626_b200 as vx
+    torch.cuda.set_device(device)
+    c = CONFIGS[args.config]
+    W, K = args.warmup, args.steps
+    sensor, frames, icfg, ecfg = make_inputs(args.config, W + K, offset=rank * 7)
+    ctx = vx.Context(device)
+    ext = torch.cuda.ExternalStream(ctx.stream, device=device)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)
+    dev_frames = torch.from_numpy(np.stack([d for _, d in frames])).to(device)
+    H, Wd = dev_frames.shape[1], dev_frames.shape[2]
+
+    # ---- value: device-resident path --------------------------------------
+    T = vx.TsdfLayer(c["vs"], ctx=ctx)
+    E = vx.EsdfLayer(c["vs"], ctx=ctx) if ecfg else None
+    changed = vx.BlockList(ctx)
+    esdf_out = vx.BlockList(ctx)
+
+    def step(i, marks=None):
+        pose = frames[i][0]
+        vx.integrate_depth_device(T, dev_frames[i].data_ptr(), Wd, H, pose, sensor, icfg, changed)
+        if marks is not None:
+            marks.record(ext)
+        if E is not None:
+            vx.update_esdf_device(E, T, changed, ecfg, esdf_out)
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize(device)
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    ctx.reset_kernel_times()
+    launches0 = ctx.launch_count
+    tot, tsdf_ms, esdf_ms = [], [], []
+    with ClockSampler(device) as clk:
+        for i in range(W, W + K):
+            flush.zero_()
+            torch.cuda.synchronize(device)
+            e0, em, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(ext)
+            step(i, marks=em)
+            e1.record(ext)
+            e1.synchronize()
+            tot.append(e0.elapsed_time(e1))
+            tsdf_ms.append(e0.elapsed_time(em))
+            esdf_ms.append(em.elapsed_time(e1))
+    launches = ctx.launch_count - launches0
+    stats = ctx.stats()
+    kernels = {}
+    for name in ("k_rays", "k_dilate_alloc", "k_integrate", "k_compact", "k_merge7",
+                 "k_select_effective", "k_alloc_list", "k_mark", "k_lower"):
+        ms, n = ctx.kernel_time(name)
+        if n:
+            kernels[name] = {"ms_total": ms, "launches": n, "ms_per_launch": ms / n}
+    ctx.set_profiling(False)
+    total_s = sum(tot) / 1000.0
+
+    # ---- e2e: public host API, host buffers, copies inside the timed region --
+    pinned = [torch.from_numpy(d).pin_memory() for _, d in frames]
+    T2 = vx.TsdfLayer(c["vs"], ctx=ctx)
+    E2 = vx.EsdfLayer(c["vs"], ctx=ctx) if ecfg else None
+    for i in range(W):
+        ch = vx.integrate_depth(T2, pinned[i].numpy(), frames[i][0], sensor, icfg)
+        if E2 is not None:
+            vx.update_esdf(E2, T2, ch, ecfg)
+    e2e_t, h2d, d2h = [], 0, 0
+    for i in range(W, W + K):
+        flush.zero_()
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        ch = vx.integrate_depth(T2, pinned[i].numpy(), frames[i][0], sensor, icfg)
+        h2d += pinned[i].numel() * 4
+        d2h += ch.nbytes
+        if E2 is not None:
+            ech = vx.update_esdf(E2, T2, ch, ecfg)
+            h2d += ch.nbytes
+            d2h += ech.nbytes
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_t)
+
+    # ---- multi-rank: max over ranks ----------------------------------------
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_s, e2e_s], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s, e2e_s = float(t[0]), float(t[1])
+    return dict(total_s=total_s, tot=tot, tsdf_ms=tsdf_ms, esdf_ms=esdf_ms, stats=stats,
+                kernels=kernels, launches=launches, clocks=clk.summary(), e2e_s=e2e_s,
+                h2d=h2d // K, d2h=d2h // K, W=Wd, H=H)
+
+
+def roofline(res, K):
+    peak, peak_src = measured_peaks()
+    st, ks = res["stats"], res["kernels"]
+    # algorithmic bytes per launch
+    bytes_by_kernel = {
+        "k_integrate": 8 * st["voxels_read"] + 8 * st["voxels_updated"] + 4 * st["depth_pixels"],
+        "k_lower": 12288 * st["esdf_blocks"] + 12288 * st["dirty_blocks_after_round1"]
+                   + 3072 * st["pair_exchanges"] + 12288 * st["compared_blocks"],
+    }
+    cand = [k for k in bytes_by_kernel if k in ks]
+    if not cand:
+        return None
+    dom = max(cand, key=lambda k: ks[k]["ms_total"])
+    n = ks[dom]["launches"]
+    per_launch = bytes_by_kernel[dom] / n
+    achieved = per_launch / (ks[dom]["ms_per_launch"] / 1e3) / 1e9
+    out = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+           "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
+           "algorithmic_bytes_per_launch": int(per_launch),
+           "share_of_step": round(ks[dom]["ms_total"] / (res["total_s"] * 1e3), 3),
+           "traffic": ncu_traffic(dom)}
+    others = {}
+    for k in cand:
+        if k != dom:
+            b = bytes_by_kernel[k] / ks[k]["launches"]
+            a = b / (ks[k]["ms_per_launch"] / 1e3) / 1e9
+            others[k] = {"achieved": round(a, 1), "frac": round(a / peak, 4),
+                         "algorithmic_bytes_per_launch": int(b), "traffic": ncu_traffic(k)}
+    out["other_kernels"] = others
+    return out
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_run(cfgname, warmup, steps, budget_s=None):
+    """The reference's own CPU path (oracle/_ref, OpenMP) or the C restatement."""
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    from oracle.bindings import PortOracle, RefOracle, have_ref
+    from paper_2311_00626_b200 import _abi as A
+    c = CONFIGS[cfgname]
+    kind = "reference" if have_ref() else "port"
+    o = RefOracle() if kind == "reference" else PortOracle()
+    sensor, frames, icfg, ecfg = make_inputs(cfgname, warmup + steps)
+    T = o.layer(A.LAYER_TSDF, c["vs"])
+    E = o.layer(A.LAYER_ESDF, c["vs"]) if ecfg else None
+    integ = o.integrate_camera if c["sensor"] == "camera" else o.integrate_lidar
+
+    def step(i):
+        ch = integ(T, frames[i][1], frames[i][0], sensor, icfg)
+        if E is not None:
+            o.update_esdf(E, T, ch, ecfg)
+        return len(ch)
+
+    for i in range(warmup):
+        step(i)
+    times, t_start = [], time.perf_counter()
+    for i in range(warmup, warmup + steps):
+        t0 = time.perf_counter()
+        step(i)
+        times.append(time.perf_counter() - t0)
+        if budget_s and time.perf_counter() - t_start > budget_s:
+            break
+    n = len(times)
+    return dict(value=n / sum(times), kind=kind, cores=cores if kind == "reference" else 1,
+                frames=n, ms_per_step=1e3 * sum(times) / n,
+                sample=f"{c['workload']}; frames {warmup}..{warmup + n - 1} of the orbit after "
+                       f"{warmup} untimed warm-up frames; "
+                       + ("production integrate_depth + update_esdf (OpenMP)" if kind == "reference"
+                          else "oracle/voxmap_oracle.c restatement (serial)"))
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    c = CONFIGS[args.config]
+    config = {"workload": c["workload"], "scene": c["scene"], "sensor": c["sensor"],
+              "image": f"{c['w']}x{c['h']}", "voxel_size_m": c["vs"], "truncation_m": c["trunc"],
+              "esdf": {"site_threshold_m": c["esdf"][0], "max_distance_m": c["esdf"][1]} if c["esdf"] else None,
+              "l2": "flushed (256 MB write) before every timed step",
+              "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference_run(args.config, args.warmup, args.steps)
+        line = {"impl": "reference", "metric": METRIC, "value": round(r["value"], 3), "unit": UNIT,
+                "n_gpus": args.gpus, "steps": r["frames"], "warmup": args.warmup,
+                "ms_per_step": round(r["ms_per_step"], 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32/i32",
+                "data": "synthetic (reference scene + orbit, sphere-traced depth)", "config": config,
+                "cpu_baseline": {"value": round(r["value"], 3), "unit": UNIT, "cores": r["cores"],
+                                 "kind": r["kind"], "sample": r["sample"], "cpu": cpu_model()},
+                "e2e": {"value": round(r["value"], 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    res = run_ours(args, rank, world, local)
+    K = args.steps
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank != 0:
+        return
+    st = res["stats"]
+    value = world * K / res["total_s"]
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * res["total_s"] / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32/i32",
+        "data": "synthetic (reference scene + orbit trajectory, sphere-traced depth rendered on the host)",
+        "config": config,
+        "tsdf_voxel_updates_per_s": round(world * st["voxels_updated"] / res["total_s"], 1),
+        "tsdf_ms_per_frame": round(statistics.mean(res["tsdf_ms"]), 4),
+        "esdf_ms_per_frame": round(statistics.mean(res["esdf_ms"]), 4),
+        "work_per_frame": {k: round(v / K, 1) for k, v in st.items()},
+        "kernels_ms_per_frame": {k: round(v["ms_total"] / K, 4) for k, v in res["kernels"].items()},
+        "roofline": roofline(res, K),
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+        "e2e": {"value": round(world * K / res["e2e_s"], 2), "unit": UNIT,
+                "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
+                "path": "vxm_integrate_depth_camera + vxm_update_esdf (host buffers)"},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            r = cpu_reference_run(args.config, args.warmup, args.steps, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {"value": round(r["value"], 3), "unit": UNIT, "cores": r["cores"],
+                                    "kind": r["kind"], "sample": r["sample"], "cpu": cpu_model()}
+        except Exception as e:  # the CPU baseline is reported, not the measurement
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -144,6 +144,27 @@ vxm_status vxm_context_synchronize(vxm_context* ctx);
 vxm_status vxm_context_set_shard(vxm_context* ctx, int rank, int world, int slab);
 /* Kernel launches issued by this context since creation (bench evidence). */
 uint64_t vxm_context_launch_count(const vxm_context* ctx);
+/* The context's cudaStream_t (as an integer handle) for external event timing. */
+uint64_t vxm_context_stream(const vxm_context* ctx);
+
+/* Work counters accumulated by the device passes (algorithmic-bytes model of
+ * SURVEY §8(d)); reset with vxm_context_reset_stats. */
+typedef struct {
+  uint64_t integrate_calls, candidate_blocks, new_blocks, changed_blocks;
+  uint64_t voxels_read, voxels_updated, depth_pixels;
+  uint64_t esdf_calls, esdf_blocks, effective_blocks, esdf_new_blocks;
+  uint64_t lower_rounds, dirty_blocks_after_round1, pair_exchanges, compared_blocks;
+  uint64_t reserved[8];
+} vxm_stats;
+vxm_status vxm_context_stats(vxm_context* ctx, vxm_stats* out);
+void vxm_context_reset_stats(vxm_context* ctx);
+/* Per-kernel CUDA-event timing on the context stream (off by default). */
+vxm_status vxm_context_set_profiling(vxm_context* ctx, int enable);
+/* Accumulated device time (ms) and launch count of one instrumented kernel
+ * ("k_integrate", "k_lower", "k_dilate_alloc", "k_rays", "k_mark", ...). */
+vxm_status vxm_context_kernel_time(vxm_context* ctx, const char* kernel, double* ms,
+                                   uint64_t* launches);
+void vxm_context_reset_kernel_times(vxm_context* ctx);
 
 /* ---- block lists ------------------------------------------------------- */
 vxm_status vxm_blocklist_create(vxm_context* ctx, vxm_blocklist** out);

@@ -280,6 +280,35 @@ vxm_status vxm_context_set_shard(vxm_context* ctx, int rank, int world, int slab
   });
 }
 uint64_t vxm_context_launch_count(const vxm_context* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t vxm_context_stream(const vxm_context* ctx) {
+  return ctx ? reinterpret_cast<uint64_t>(ctx->stream) : 0;
+}
+vxm_status vxm_context_stats(vxm_context* ctx, vxm_stats* out) {
+  return guard([&] { *out = ctx->stats; });
+}
+void vxm_context_reset_stats(vxm_context* ctx) {
+  if (ctx) ctx->stats = vxm_stats{};
+}
+vxm_status vxm_context_set_profiling(vxm_context* ctx, int enable) {
+  return guard([&] {
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->prof_resolve();
+    ctx->profile = enable != 0;
+  });
+}
+vxm_status vxm_context_kernel_time(vxm_context* ctx, const char* kernel, double* ms,
+                                   uint64_t* launches) {
+  return guard([&] {
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->prof_resolve();
+    auto it = ctx->ktime.find(kernel ? kernel : "");
+    *ms = it == ctx->ktime.end() ? 0.0 : it->second.first;
+    *launches = it == ctx->ktime.end() ? 0 : it->second.second;
+  });
+}
+void vxm_context_reset_kernel_times(vxm_context* ctx) {
+  if (ctx) ctx->ktime.clear();
+}
 
 vxm_status vxm_blocklist_create(vxm_context* ctx, vxm_blocklist** out) {
   return guard([&] {

@@ -126,7 +126,14 @@ struct DevStatus {
   uint32_t rounds;           // lowering rounds of the last lower
   uint32_t n_out;            // generic output count
   uint32_t n_aux;            // generic aux count
-  uint32_t pad[4];
+  // work counters (algorithmic-bytes model)
+  uint32_t vox_read;         // integrate: existing voxels read
+  uint32_t vox_upd;          // integrate: voxels written
+  uint32_t sum_dirty;        // lower: dirty blocks summed over rounds >= 2
+  uint32_t sum_pairs;        // lower: face pairs exchanged
+  uint32_t cmp_blocks;       // lower: blocks compared for the changed set
+  uint32_t n_esdf_blocks;    // ESDF blocks after the update
+  uint32_t pad[2];
 };
 
 // ---- decoupled look-back scan over (a, b) count pairs ------------------------

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
   }
   grid.sync();
   uint32_t r = 0;
+  uint32_t n_pairs = 0, n_cmp = 0;  // per-warp work counters
   // while (!dirty.empty()) — an empty round-1 set runs zero rounds (:506)
   const uint32_t n_first = a.full ? n_blocks : *((volatile uint32_t*)&a.count[1]);
   if (lower && n_first > 0) {
@@ -271,7 +272,10 @@ __global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
       const bool r1_full = a.full && r == 1;
       const uint32_t n_dirty = r1_full ? n_blocks : *((volatile uint32_t*)&a.count[cp]);
       const int32_t* dirty = a.list[cp];
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.count[np] = 0;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.count[np] = 0;
+        if (r > 1 || !a.full) a.status->sum_dirty += n_dirty;
+      }
       // ---- sweep phase: every dirty block to its internal fixed point
       for (uint32_t i = gid; i < n_dirty; i += ngroups) {
         const int32_t s = r1_full ? int32_t(i) : dirty[i];
@@ -336,6 +340,7 @@ __global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
           }
           ac = __any_sync(0xffffffffu, ac);
           bc = __any_sync(0xffffffffu, bc);
+          ++n_pairs;
           if (lane == 0) {
             const int32_t who[2] = {lo, hi};
             const bool chg[2] = {ac, bc};
@@ -370,13 +375,19 @@ __global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
           diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
         }
         ch = __any_sync(0xffffffffu, diff);
+        ++n_cmp;
       }
       if (lane == 0) a.out_flags[k] = uint8_t(ch);
     }
   }
+  if (lane == 0 && (n_pairs | n_cmp)) {
+    atomicAdd(&a.status->sum_pairs, n_pairs);
+    atomicAdd(&a.status->cmp_blocks, n_cmp);
+  }
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.status->rounds = r;
+    a.status->n_esdf_blocks = n_blocks;
     a.meta->round_epoch = base_epoch + r + 2;
     if (a.full && lower) a.meta->cur = cur ^ 1u;
   }
@@ -814,12 +825,16 @@ static uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   const uint32_t nu_cap = std::max<uint32_t>(updated->count_hint, 1);
   const uint32_t n7 = 7u * nu_cap;
   const uint64_t* upd = updated->keys.as<uint64_t>();
+  ctx->prof_begin("k_merge7");
   k_merge7<<<grid_for(ctx, n7), 256, 0, ctx->stream>>>(upd, updated->d_count, s.merged);
+  ctx->prof_end();
   ctx->count_launch();
   {
     const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
+    ctx->prof_begin("k_select_effective");
     k_select_effective<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(
         s.merged, updated->d_count, T->hash, s.eff_keys, s.eff_tslot, s.counts + 0, st);
+    ctx->prof_end();
     ctx->count_launch();
   }
   {
@@ -840,7 +855,9 @@ static uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
     al.call_epoch = epoch;
     al.status = ctx->d_status;
     const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
+    ctx->prof_begin("k_alloc_list");
     k_alloc_list<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(al, st);
+    ctx->prof_end();
     ctx->count_launch();
   }
   k_nbr_update<<<grid_for(ctx, 6ull * n7), 256, 0, ctx->stream>>>(s.new_keys, s.new_slots,
@@ -865,7 +882,9 @@ static uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.call_epoch = epoch;
   m.flags = s.flags;
   m.status = ctx->d_status;
+  ctx->prof_begin("k_mark");
   k_mark<<<std::max<uint32_t>(1, std::min<uint32_t>(n7, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(m);
+  ctx->prof_end();
   ctx->count_launch(3);
   check_launch(ctx, "esdf mark phase");
   return n7;
@@ -884,8 +903,10 @@ static int lower_grid(Context* ctx) {
 static void launch_lower(Context* ctx, LowerArgs& la) {
   void* args[] = {&la};
   const int grid = lower_grid(ctx);
+  ctx->prof_begin("k_lower");
   VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lower, dim3(grid), dim3(kLowerThreads), args, 0,
                                        ctx->stream));
+  ctx->prof_end();
   ctx->count_launch();
 }
 
@@ -932,10 +953,25 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
                       n_all_cap, changed_out->keys.as<uint64_t>(), changed_out->d_count, nullptr);
   changed_out->host_valid = false;
   changed_out->count_hint = n_all_cap;
+  VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_effective, s.counts + 0, sizeof(uint32_t) * 2,
+                           cudaMemcpyDeviceToDevice, ctx->stream));  // n_effective, n_esdf_new
+  VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_out, changed_out->d_count, sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->sync_status();
   E->refresh();
-  if (ctx->h_status->capacity_error || ctx->h_status->pool_overflow)
+  const DevStatus& st = *ctx->h_status;
+  if (st.capacity_error || st.pool_overflow)
     throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+  vxm_stats& w = ctx->stats;
+  w.esdf_calls += 1;
+  w.esdf_blocks += st.n_esdf_blocks;
+  w.effective_blocks += st.n_effective;
+  w.esdf_new_blocks += st.n_esdf_new;
+  w.lower_rounds += st.rounds;
+  w.dirty_blocks_after_round1 += st.sum_dirty;
+  w.pair_exchanges += st.sum_pairs;
+  w.compared_blocks += st.cmp_blocks;
+  w.reserved[0] += st.n_out;  // ESDF changed blocks
 }
 
 static void append_sorted_unique(std::vector<vxm_grid_index>& dst,

@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
   if (st->pool_overflow || st->capacity_error || st->bitmap_overflow) return;
   const uint32_t n = st->n_candidates;
   const double* R = a.T_SL.R;
+  uint32_t n_read = 0, n_upd = 0;  // work counters (algorithmic bytes)
   for (uint32_t ci = blockIdx.x; ci < n; ci += gridDim.x) {
     const uint64_t key = a.cand_keys[ci];
     const int32_t sraw = a.cand_slots[ci];
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
         w_new = __double2float_rn(__ddiv_rn(1.0, dd < 1e-6 ? 1e-6 : dd));
       }
       const float2 old = is_new ? make_float2(0.0f, 0.0f) : blk[lin];
+      n_read += is_new ? 0u : 1u;
       const float d_t = d_p < -a.eps ? -a.eps : (a.eps < d_p ? a.eps : d_p);
       const float w_sum = __fadd_rn(old.y, w_new);
       const float avg = __fdiv_rn(__fadd_rn(__fmul_rn(old.y, old.x), __fmul_rn(w_new, d_t)), w_sum);
@@ -188,10 +190,18 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
           __float_as_uint(nv.y) != __float_as_uint(old.y)) {
         blk[lin] = nv;
         any = true;
+        ++n_upd;
       }
     }
     const int changed = __syncthreads_or(any);
     if (threadIdx.x == 0) a.changed[ci] = uint8_t(changed);
+  }
+  n_read = __reduce_add_sync(0xffffffffu, n_read);
+  n_upd = __reduce_add_sync(0xffffffffu, n_upd);
+  if ((threadIdx.x & 31) == 0 && (n_read | n_upd)) {
+    DevStatus* sw = const_cast<DevStatus*>(st);
+    atomicAdd(&sw->vox_read, n_read);
+    atomicAdd(&sw->vox_upd, n_upd);
   }
 }
 
@@ -245,7 +255,9 @@ void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
   const uint32_t tiles_cap = ceil_div(std::max<uint32_t>(n_cap, 1), 256 * kCompactItems);
   const ScanTiles st = ctx->next_scan(tiles_cap);
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_cap, ctx->sm_count * 4));
+  ctx->prof_begin("k_compact");
   k_compact_keys<<<grid, 256, 0, ctx->stream>>>(in, flags, n_ptr, out, n_out, st, guard);
+  ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "k_compact_keys");
 }
@@ -290,7 +302,9 @@ void run_integrate(Layer* L, const ViewArgs& va, const vxm_integrator_config& cf
     a.inv_sq = cfg.weighting == VXM_WEIGHT_INVERSE_SQUARE;
     a.linear = (va.lidar ? cfg.lidar_sample : cfg.camera_sample) == VXM_SAMPLE_LINEAR;
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * 8));
+    ctx->prof_begin("k_integrate");
     k_integrate<<<grid, 256, 0, ctx->stream>>>(a);
+    ctx->prof_end();
     ctx->count_launch();
     check_launch(ctx, "k_integrate");
     changed_out->ensure(cand_cap);
@@ -299,6 +313,8 @@ void run_integrate(Layer* L, const ViewArgs& va, const vxm_integrator_config& cf
                         changed_out->d_count, ctx->d_status);
     changed_out->host_valid = false;
     changed_out->count_hint = cand_cap;
+    VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_changed, changed_out->d_count, sizeof(uint32_t),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
     ctx->sync_status();
     const DevStatus& s = *ctx->h_status;
     L->refresh();
@@ -312,6 +328,14 @@ void run_integrate(Layer* L, const ViewArgs& va, const vxm_integrator_config& cf
     }
     if (s.capacity_error) throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
     changed_out->count_hint = s.n_candidates;
+    vxm_stats& w = ctx->stats;
+    w.integrate_calls += 1;
+    w.candidate_blocks += s.n_candidates;
+    w.new_blocks += s.n_new;
+    w.changed_blocks += s.n_changed;
+    w.voxels_read += s.vox_read;
+    w.voxels_updated += s.vox_upd;
+    w.depth_pixels += uint64_t(va.width) * uint64_t(va.height);
     return;
   }
   throw Error(VXM_ERR_INTERNAL, "integrate: pool growth did not converge");

@@ -64,6 +64,44 @@ void Context::reset_status() {
 void Context::sync_status() {
   VXM_CUDA(cudaMemcpyAsync(h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
   VXM_CUDA(cudaStreamSynchronize(stream));
+  prof_resolve();
+}
+
+static cudaEvent_t take_event(Context* c) {
+  if (!c->spare_events.empty()) {
+    cudaEvent_t e = c->spare_events.back();
+    c->spare_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  VXM_CUDA(cudaEventCreate(&e));
+  return e;
+}
+void Context::prof_begin(const char* name) {
+  if (!profile) return;
+  prof_name = name;
+  prof_a = take_event(this);
+  VXM_CUDA(cudaEventRecord(prof_a, stream));
+}
+void Context::prof_end() {
+  if (!profile || !prof_name) return;
+  cudaEvent_t b = take_event(this);
+  VXM_CUDA(cudaEventRecord(b, stream));
+  pending.push_back({prof_name, prof_a, b});
+  prof_name = nullptr;
+}
+void Context::prof_resolve() {
+  for (const Pending& p : pending) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      auto& t = ktime[p.name];
+      t.first += ms;
+      t.second += 1;
+    }
+    spare_events.push_back(p.a);
+    spare_events.push_back(p.b);
+  }
+  pending.clear();
 }
 
 // ---- Layer ---------------------------------------------------------------------

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -57,12 +59,28 @@ struct Context {
   DevBuf tmp[6];          // ESDF / list scratch
   DevBuf cub_tmp;
 
+  // work counters and optional per-kernel event timing
+  vxm_stats stats{};
+  bool profile = false;
+  struct Pending {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> spare_events;
+  std::map<std::string, std::pair<double, uint64_t>> ktime;
+  const char* prof_name = nullptr;
+  cudaEvent_t prof_a = nullptr;
+
   // Scan pass bookkeeping: returns the ScanTiles for the next pass with at
   // most `tiles` tiles, clearing the other buffer for the pass after.
   ScanTiles next_scan(uint32_t tiles);
   void count_launch(int n = 1) { launches += uint64_t(n); }
   void sync_status();  // cudaStreamSynchronize + copy status (already async-copied)
   void reset_status();
+  void prof_begin(const char* name);
+  void prof_end();
+  void prof_resolve();  // after a stream sync
 };
 
 struct Layer {

@@ -353,18 +353,22 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
     const int tile = std::max(1, a.cfg.pixel_subsample);
     const int nt = ((a.width + tile - 1) / tile) * ((a.height + tile - 1) / tile);
     if (nt > 0) {
+      ctx->prof_begin("k_rays");
       k_rays_camera<<<ceil_div(nt, 128), 128, 0, ctx->stream>>>(
           a.depth_dev, a.width, a.height, tile, a.cam, a.T_LS, cs,
           a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
+      ctx->prof_end();
       ctx->count_launch();
     }
   } else {
     ensure_lidar_lut(ctx, a.li);
     const int np = a.width * a.height;
     if (np > 0) {
+      ctx->prof_begin("k_rays");
       k_rays_lidar<<<ceil_div(np, 128), 128, 0, ctx->stream>>>(
           a.depth_dev, a.width, a.height, ctx->lidar_dirs.as<double>(), a.T_LS, cs,
           a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
+      ctx->prof_end();
       ctx->count_launch();
     }
   }
@@ -385,9 +389,11 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
   }
   const uint32_t tiles = ceil_div(n_words, 256);
   const ScanTiles st = ctx->next_scan(tiles);
+  ctx->prof_begin("k_dilate_alloc");
   k_dilate_alloc<<<tiles, 256, 0, ctx->stream>>>(cube, uint32_t(n_words), al, ctx->rank, ctx->world,
                                                  ctx->slab, ctx->cand_keys.as<uint64_t>(),
                                                  ctx->cand_slots.as<int32_t>(), ctx->d_status, st);
+  ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "k_dilate_alloc");
   if (cand_cap_out) *cand_cap_out = cand_cap;

@@ -145,6 +145,43 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().vxm_context_launch_count(self.h))
 
+    @property
+    def stream(self) -> int:
+        """cudaStream_t handle (e.g. for torch.cuda.ExternalStream)."""
+        lib().vxm_context_stream.restype = C.c_uint64
+        return int(lib().vxm_context_stream(self.h))
+
+    def stats(self) -> dict:
+        s = Stats()
+        check(lib().vxm_context_stats(self.h, C.byref(s)))
+        return {f: int(getattr(s, f)) for f, _ in Stats._fields_ if f != "reserved"} | {
+            "esdf_changed_blocks": int(s.reserved[0])}
+
+    def reset_stats(self):
+        lib().vxm_context_reset_stats(self.h)
+
+    def set_profiling(self, enable: bool):
+        check(lib().vxm_context_set_profiling(self.h, C.c_int(int(enable))))
+
+    def kernel_time(self, name: str):
+        """(total ms, launches) of one instrumented kernel since the last reset."""
+        ms = C.c_double()
+        n = C.c_uint64()
+        check(lib().vxm_context_kernel_time(self.h, name.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def reset_kernel_times(self):
+        lib().vxm_context_reset_kernel_times(self.h)
+
+
+class Stats(C.Structure):
+    """vxm_stats (include/voxmap_b200.h)."""
+    _fields_ = [(f, C.c_uint64) for f in (
+        "integrate_calls", "candidate_blocks", "new_blocks", "changed_blocks", "voxels_read",
+        "voxels_updated", "depth_pixels", "esdf_calls", "esdf_blocks", "effective_blocks",
+        "esdf_new_blocks", "lower_rounds", "dirty_blocks_after_round1", "pair_exchanges",
+        "compared_blocks")] + [("reserved", C.c_uint64 * 8)]
+
 
 _default_ctx: Context | None = None
 
@@ -328,6 +365,13 @@ def update_esdf(esdf: EsdfLayer, tsdf: TsdfLayer, updated, cfg=None, out: BlockL
         check(lib().vxm_update_esdf(esdf.h, tsdf.h, A.ptr(k), C.c_uint64(len(k)), C.byref(cfg),
                                     out.h))
     return out.numpy()
+
+
+def update_esdf_device(esdf: EsdfLayer, tsdf: TsdfLayer, updated: BlockList, cfg,
+                       out: BlockList) -> BlockList:
+    """Device-resident update_esdf: consumes and produces device block lists."""
+    check(lib().vxm_update_esdf_list(esdf.h, tsdf.h, updated.h, C.byref(cfg), out.h))
+    return out
 
 
 class EsdfUpdateState:
