@@ -17,9 +17,7 @@ using namespace vxm;
 
 struct vxm_context : Context {};
 struct vxm_layer : Layer {};
-struct vxm_blocklist : BlockList {
-  bool sorted_unique = false;  // produced by a device pass in sorted order
-};
+struct vxm_blocklist : BlockList {};
 struct vxm_esdf_state : EsdfState {};
 
 namespace {
@@ -257,6 +255,7 @@ void vxm_context_destroy(vxm_context* ctx) {
   for (int i = 0; i < 2; ++i)
     if (ctx->scan.status[i]) cudaFree(ctx->scan.status[i]);
   if (ctx->scan.tickets) cudaFree(ctx->scan.tickets);
+  delete static_cast<vxm_blocklist*>(ctx->scratch_in);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -329,7 +328,6 @@ vxm_status vxm_blocklist_host(vxm_blocklist* l, const vxm_grid_index** data, uin
 vxm_status vxm_blocklist_assign(vxm_blocklist* l, const vxm_grid_index* data, uint64_t n) {
   return guard([&] {
     l->assign_host(data, n);
-    l->sorted_unique = false;
   });
 }
 
@@ -347,8 +345,8 @@ vxm_status vxm_layer_create(vxm_context* ctx, vxm_layer_type type, double vs, ui
     VXM_CUDA(cudaMalloc(&L->meta, sizeof(LayerMeta)));
     VXM_CUDA(cudaMemset(L->meta, 0, sizeof(LayerMeta)));
     if (type == VXM_LAYER_ESDF) {
-      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * 2));
-      VXM_CUDA(cudaMemset(L->dirty_count, 0, sizeof(uint32_t) * 2));
+      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * 4));
+      VXM_CUDA(cudaMemset(L->dirty_count, 0, sizeof(uint32_t) * 4));
     }
     L->ensure_capacity(std::min<uint64_t>(4096, L->max_blocks));
     *out = L;
@@ -607,10 +605,14 @@ vxm_status vxm_update_esdf(vxm_layer* E, vxm_layer* T, const vxm_grid_index* upd
                            const vxm_esdf_config* cfg, vxm_blocklist* out) {
   return guard([&] {
     REQUIRE_ARG(E && T && cfg && out, "null argument");
-    vxm_blocklist list;
-    list.ctx = E->ctx;
-    list.assign_host(updated, n);
-    const vxm_status s = vxm_update_esdf_list(E, T, &list, cfg, out);
+    Context* ctx = E->ctx;
+    if (!ctx->scratch_in) {  // reused input list: no per-call device allocations
+      ctx->scratch_in = new vxm_blocklist();
+      ctx->scratch_in->ctx = ctx;
+    }
+    vxm_blocklist* list = static_cast<vxm_blocklist*>(ctx->scratch_in);
+    list->assign_host(updated, n);
+    const vxm_status s = vxm_update_esdf_list(E, T, list, cfg, out);
     if (s != VXM_OK) throw Error(s, g_err);
     out->fetch();
   });

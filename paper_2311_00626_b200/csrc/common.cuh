@@ -133,7 +133,8 @@ struct DevStatus {
   uint32_t sum_pairs;        // lower: face pairs exchanged
   uint32_t cmp_blocks;       // lower: blocks compared for the changed set
   uint32_t n_esdf_blocks;    // ESDF blocks after the update
-  uint32_t pad[2];
+  uint32_t meta_blocks;      // copy of the layer's LayerMeta {num_blocks, cur}
+  uint32_t meta_cur;         //   taken with the status read (one sync per call)
 };
 
 // ---- decoupled look-back scan over (a, b) count pairs ------------------------

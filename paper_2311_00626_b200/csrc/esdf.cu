@@ -126,73 +126,374 @@ struct BlockSmem {
   uint32_t w0[512], w1[512], w2[512];
 };
 
-// One line of 8 voxels along `axis` held in registers.
+// ===== sweep v3: one 64-thread group per block, one line per thread ============
+// Working format in shared memory (converted from the reference's 12-byte voxel
+// on load and back on store):
+//   w0  = squared distance
+//   klo = (py + 2^15) << 16 | (pz + 2^15)
+//   khi = (px + 2^15) | flags << 16 | reserved << 24
+// so the parent offset is a 48-bit key (khi & 0xffff) << 32 | klo whose
+// unsigned order is the lexicographic (x, y, z) order used by relax's tie
+// break, and a single-axis step is one 64-bit add.
+constexpr unsigned long long kKeyZero = 0x800080008000ull;  // offset (0, 0, 0)
+
+struct GroupSmem {
+  uint32_t w0[512], klo[512], khi[512];
+  unsigned long long mask[3][2];  // dirty lines per phase (X, Y, Z) by pass parity
+  uint32_t bcast;
+};
+
 template <int AXIS>
-__device__ inline bool sweep_line(BlockSmem& b, int t, const Limits& lim) {
-  // t in [0, 64): the two coordinates orthogonal to AXIS
-  const int c0 = t & 7, c1 = t >> 3;
-  EV v[8];
-  int idx[8];
+__device__ inline int line_idx3(int q, int k) {  // q in [0, 64): the orthogonal coords
+  const int c0 = q & 7, c1 = q >> 3;
+  const int x = AXIS == 0 ? k : c0;
+  const int y = AXIS == 1 ? k : (AXIS == 0 ? c0 : c1);
+  const int z = AXIS == 2 ? k : c1;
+  return swz(x, y, z);
+}
+
+__device__ inline unsigned long long spread8(uint32_t ch) {  // bit k -> bit 8k
+  unsigned long long m = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) m |= (unsigned long long)((ch >> k) & 1u) << (8 * k);
+  return m;
+}
+
+// One line along AXIS (q = index of the two orthogonal coordinates), X+ then X-
+// Gauss-Seidel relaxes in registers — esdf/integrator.cpp:58-88, 96-139.
+template <int AXIS>
+__device__ inline uint32_t sweep_line3(GroupSmem& g, int q, const Limits& lim) {
+  constexpr int sh = AXIS == 0 ? 32 : (AXIS == 1 ? 16 : 0);
+  int sq[8], pa[8], qq[8], idx[8];
+  unsigned long long key[8];
+  uint32_t take = 0, give = 0, in = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const int x = AXIS == 0 ? k : c0;
-    const int y = AXIS == 1 ? k : (AXIS == 0 ? c0 : c1);
-    const int z = AXIS == 2 ? k : c1;
-    idx[k] = swz(x, y, z);
-    v[k] = ev_unpack(b.w0[idx[k]], b.w1[idx[k]], b.w2[idx[k]]);
+    idx[k] = line_idx3<AXIS>(q, k);
+    const uint32_t lo = g.klo[idx[k]], hi = g.khi[idx[k]];
+    sq[k] = int(g.w0[idx[k]]);
+    key[k] = ((unsigned long long)(hi & 0xffffu) << 32) | lo;
+    const int px = int(hi & 0xffffu) - 0x8000, py = int(lo >> 16) - 0x8000,
+              pz = int(lo & 0xffffu) - 0x8000;
+    pa[k] = AXIS == 0 ? px : (AXIS == 1 ? py : pz);
+    const int o1 = AXIS == 0 ? py : px, o2 = AXIS == 2 ? py : pz;
+    qq[k] = int(uint32_t(o1 * o1) + uint32_t(o2 * o2));
+    const uint32_t f = (hi >> 16) & 0xffu;
+    const bool obs = f & VXM_ESDF_OBSERVED, site = f & VXM_ESDF_SITE;
+    take |= uint32_t(obs && !site) << k;
+    give |= uint32_t(obs && (site || key[k] != kKeyZero)) << k;
+    in |= uint32_t((f & VXM_ESDF_INSIDE) != 0) << k;
   }
-  const int dx = AXIS == 0, dy = AXIS == 1, dz = AXIS == 2;
   uint32_t ch = 0;
+  auto relax3 = [&](int k, int j, int s) {
+    const int pc = pa[j] - s;
+    const int cand = int(uint32_t(pc * pc) + uint32_t(qq[j]));
+    const unsigned long long ckey = s > 0 ? key[j] - (1ull << sh) : key[j] + (1ull << sh);
+    const int limk = ((in >> k) & 1u) ? lim.cap_sq : lim.max_sq;
+    const bool better = cand < sq[k] || (cand == sq[k] && (key[k] == kKeyZero || ckey < key[k]));
+    const bool ok = ((give >> j) & (take >> k) & 1u) && cand != 0 && cand <= limk && better;
+    if (ok) {
+      sq[k] = cand;
+      key[k] = ckey;
+      pa[k] = pc;
+      qq[k] = qq[j];
+      give |= 1u << k;
+      ch |= 1u << k;
+    }
+  };
 #pragma unroll
-  for (int k = 1; k < 8; ++k)  // X+ (resp. Y+, Z+)
-    if (relax(v[k], v[k - 1], dx, dy, dz, lim)) ch |= 1u << k;
+  for (int k = 1; k < 8; ++k) relax3(k, k - 1, 1);  // X+ (resp. Y+, Z+)
 #pragma unroll
-  for (int k = 6; k >= 0; --k)  // X- (resp. Y-, Z-)
-    if (relax(v[k], v[k + 1], -dx, -dy, -dz, lim)) ch |= 1u << k;
+  for (int k = 6; k >= 0; --k) relax3(k, k + 1, -1);  // X- (resp. Y-, Z-)
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     if (ch & (1u << k)) {
-      b.w0[idx[k]] = uint32_t(v[k].sq);
-      b.w1[idx[k]] = ev_w1(v[k]);
-      b.w2[idx[k]] = ev_w2(v[k]);
+      g.w0[idx[k]] = uint32_t(sq[k]);
+      g.klo[idx[k]] = uint32_t(key[k]);
+      g.khi[idx[k]] = (g.khi[idx[k]] & 0xffff0000u) | uint32_t(key[k] >> 32);
     }
-  return ch != 0;
+  return ch;
 }
 
-// sweep_block — esdf/integrator.cpp:96-139, for one 64-thread group.
-__device__ inline bool sweep_block_group(BlockSmem& b, int t, int bar, const Limits& lim) {
+// Runs one phase of a pass for the group: only lines marked dirty are swept
+// (an unchanged line is idempotent under its X+/X- sweep), changes mark the
+// lines through the changed voxels for the phases that follow.
+template <int AXIS>
+__device__ inline uint32_t sweep_phase3(GroupSmem& g, int t, int bar, int p, const Limits& lim) {
+  uint32_t ch = 0;
+  if ((g.mask[AXIS][p] >> t) & 1ull) ch = sweep_line3<AXIS>(g, t, lim);
+  if (ch) {
+    const int c0 = t & 7, c1 = t >> 3;
+    if (AXIS == 0) {  // line (y=c0, z=c1): Y-line k + 8z, Z-line k + 8y (this pass)
+      atomicOr(&g.mask[1][p], (unsigned long long)ch << (8 * c1));
+      atomicOr(&g.mask[2][p], (unsigned long long)ch << (8 * c0));
+    } else if (AXIS == 1) {  // line (x=c0, z=c1): X-line k + 8z (next), Z-line x + 8k (this)
+      atomicOr(&g.mask[0][p ^ 1], (unsigned long long)ch << (8 * c1));
+      atomicOr(&g.mask[2][p], spread8(ch) << c0);
+    } else {  // line (x=c0, y=c1): X-line y + 8k, Y-line x + 8k (next pass)
+      atomicOr(&g.mask[0][p ^ 1], spread8(ch) << c1);
+      atomicOr(&g.mask[1][p ^ 1], spread8(ch) << c0);
+    }
+  }
+  return ch;
+}
+
+// sweep_block (esdf/integrator.cpp:96-139) for one group; masks[.][0] hold the
+// initially dirty lines.  Returns whether any voxel changed.
+__device__ inline bool sweep_block3(GroupSmem& g, int t, int bar, const Limits& lim) {
   bool block_changed = false;
-  while (true) {
-    bool c = sweep_line<0>(b, t, lim);
+  for (int pass = 0;; ++pass) {
+    const int p = pass & 1;
+    uint32_t c = sweep_phase3<0>(g, t, bar, p, lim);
     group_sync(bar);
-    c |= sweep_line<1>(b, t, lim);
+    if (t == 0) g.mask[0][p] = 0ull;
+    c |= sweep_phase3<1>(g, t, bar, p, lim);
     group_sync(bar);
-    c |= sweep_line<2>(b, t, lim);
-    const bool pass_changed = group_sync_or(bar, c);
+    if (t == 0) g.mask[1][p] = 0ull;
+    c |= sweep_phase3<2>(g, t, bar, p, lim);
+    const bool pass_changed = group_sync_or(bar, c != 0);
+    if (t == 0) g.mask[2][p] = 0ull;
     block_changed |= pass_changed;
     if (!pass_changed) break;
   }
   return block_changed;
 }
 
-__device__ inline void load_block(BlockSmem& b, const uint32_t* __restrict__ src, int t) {
-#pragma unroll 4
-  for (int w = t; w < 1536; w += 64) {
-    const uint32_t val = __ldcg(src + w);
-    const int lin = w / 3, f = w - lin * 3;
-    const int s = swz_lin(lin);
-    if (f == 0) b.w0[s] = val;
-    else if (f == 1) b.w1[s] = val;
-    else b.w2[s] = val;
+// Global block (reference layout) -> working format in shared memory.
+__device__ inline void load_block3(GroupSmem& g, const uint32_t* __restrict__ src, int t, int bar) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll 3
+  for (int i = 0; i < 6; ++i) {
+    const int q = t + 64 * i;
+    const uint4 v = __ldcg(s4 + q);
+    const uint32_t vals[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int w = 4 * q + e, lin = w / 3, f = w - 3 * lin;
+      const int si = swz_lin(lin);
+      (f == 0 ? g.w0 : (f == 1 ? g.klo : g.khi))[si] = vals[e];  // raw w1 / w2 for now
+    }
+  }
+  group_sync(bar);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int si = swz_lin(t + 64 * i);
+    const uint32_t w1 = g.klo[si], w2 = g.khi[si];
+    g.klo[si] = (((w1 >> 16) ^ 0x8000u) << 16) | ((w2 & 0xffffu) ^ 0x8000u);
+    g.khi[si] = ((w1 & 0xffffu) ^ 0x8000u) | (w2 & 0xffff0000u);
+  }
+  group_sync(bar);
+}
+
+__device__ inline void store_block3(const GroupSmem& g, uint32_t* __restrict__ dst, int t) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll 3
+  for (int i = 0; i < 6; ++i) {
+    const int q = t + 64 * i;
+    uint32_t vals[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int w = 4 * q + e, lin = w / 3, f = w - 3 * lin;
+      const int si = swz_lin(lin);
+      const uint32_t lo = g.klo[si], hi = g.khi[si];
+      vals[e] = f == 0 ? g.w0[si]
+                       : (f == 1 ? (((hi & 0xffffu) ^ 0x8000u) | (((lo >> 16) ^ 0x8000u) << 16))
+                                 : (((lo & 0xffffu) ^ 0x8000u) | (hi & 0xffff0000u)));
+    }
+    __stcg(d4 + q, make_uint4(vals[0], vals[1], vals[2], vals[3]));
   }
 }
-__device__ inline void store_block(const BlockSmem& b, uint32_t* __restrict__ dst, int t) {
-#pragma unroll 4
-  for (int w = t; w < 1536; w += 64) {
-    const int lin = w / 3, f = w - lin * 3;
-    const int s = swz_lin(lin);
-    __stcg(dst + w, f == 0 ? b.w0[s] : (f == 1 ? b.w1[s] : b.w2[s]));
+
+// reset_parented (esdf/integrator.cpp:352-363) on the staged block; returns
+// whether it holds a site (after the reset, sites are the only givers).
+__device__ inline bool reset_block3(GroupSmem& g, int t, int bar, const Limits& lim) {
+  bool any_site = false;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int si = swz_lin(t + 64 * i);
+    const uint32_t lo = g.klo[si], hi = g.khi[si];
+    const uint32_t f = (hi >> 16) & 0xffu;
+    const bool hp = (hi & 0xffffu) != 0x8000u || lo != 0x80008000u;
+    any_site |= (f & (VXM_ESDF_OBSERVED | VXM_ESDF_SITE)) == (VXM_ESDF_OBSERVED | VXM_ESDF_SITE);
+    if ((f & VXM_ESDF_OBSERVED) && !(f & VXM_ESDF_SITE) && hp) {
+      g.w0[si] = uint32_t((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq);
+      g.klo[si] = 0x80008000u;
+      g.khi[si] = (hi & 0xffff0000u) | 0x8000u;
+    }
   }
+  return group_sync_or(bar, any_site);
+}
+
+// Register form of one line of 8 voxels (sweep).  Flags live in bitmasks so
+// relax is branch-free: take = observed && !site, give = observed && (site ||
+// has_parent), hp = has_parent, in = inside.
+struct Line {
+  int sq[8], px[8], py[8], pz[8];
+  uint32_t take, give, hp, in;
+};
+
+template <int AXIS>
+__device__ inline int line_idx(int q, int k) {  // q in [0, 64): the orthogonal coords
+  const int c0 = q & 7, c1 = q >> 3;
+  const int x = AXIS == 0 ? k : c0;
+  const int y = AXIS == 1 ? k : (AXIS == 0 ? c0 : c1);
+  const int z = AXIS == 2 ? k : c1;
+  return swz(x, y, z);
+}
+
+template <int AXIS>
+__device__ inline void load_line(const BlockSmem& b, int q, Line& L) {
+  L.take = L.give = L.hp = L.in = 0u;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = line_idx<AXIS>(q, k);
+    const uint32_t w1 = b.w1[i], w2 = b.w2[i];
+    L.sq[k] = int(b.w0[i]);
+    L.px[k] = int(int16_t(w1 & 0xffffu));
+    L.py[k] = int(int16_t(w1 >> 16));
+    L.pz[k] = int(int16_t(w2 & 0xffffu));
+    const uint32_t f = (w2 >> 16) & 0xffu;
+    const bool obs = f & VXM_ESDF_OBSERVED, site = f & VXM_ESDF_SITE;
+    const bool hp = (L.px[k] | L.py[k] | L.pz[k]) != 0;
+    L.take |= uint32_t(obs && !site) << k;
+    L.give |= uint32_t(obs && (site || hp)) << k;
+    L.hp |= uint32_t(hp) << k;
+    L.in |= uint32_t((f & VXM_ESDF_INSIDE) != 0) << k;
+  }
+}
+
+// relax(v[k] <- v[j]) with step s along AXIS — esdf/integrator.cpp:58-88.
+template <int AXIS>
+__device__ __forceinline__ void relax_line(Line& L, int k, int j, int s, const Limits& lim,
+                                           uint32_t& ch) {
+  int cx = L.px[j], cy = L.py[j], cz = L.pz[j];
+  if (AXIS == 0) cx -= s;
+  else if (AXIS == 1) cy -= s;
+  else cz -= s;
+  const int cand = int(uint32_t(cx * cx) + uint32_t(cy * cy) + uint32_t(cz * cz));
+  const int lim_k = ((L.in >> k) & 1u) ? lim.cap_sq : lim.max_sq;
+  const bool less = cx < L.px[k] || (cx == L.px[k] && (cy < L.py[k] || (cy == L.py[k] && cz < L.pz[k])));
+  const bool better = cand < L.sq[k] || (cand == L.sq[k] && (!((L.hp >> k) & 1u) || less));
+  const bool ok = ((L.give >> j) & (L.take >> k) & 1u) && cand != 0 && cand <= lim_k && better;
+  if (ok) {
+    L.sq[k] = cand;
+    L.px[k] = int(int16_t(cx));
+    L.py[k] = int(int16_t(cy));
+    L.pz[k] = int(int16_t(cz));
+    L.hp |= 1u << k;
+    L.give |= 1u << k;
+    ch |= 1u << k;
+  }
+}
+
+template <int AXIS>
+__device__ inline void store_line(BlockSmem& b, int q, const Line& L, uint32_t ch) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (ch & (1u << k)) {
+      const int i = line_idx<AXIS>(q, k);
+      b.w0[i] = uint32_t(L.sq[k]);
+      b.w1[i] = (uint32_t(L.px[k]) & 0xffffu) | (uint32_t(L.py[k]) << 16);
+      b.w2[i] = (b.w2[i] & 0xffff0000u) | (uint32_t(L.pz[k]) & 0xffffu);
+    }
+}
+
+// One directional phase (X, Y or Z) of sweep_block for a whole block by one
+// warp: lane owns lines `lane` and `lane + 32`, interleaved for ILP.
+template <int AXIS>
+__device__ inline bool sweep_phase_warp(BlockSmem& b, int lane, const Limits& lim) {
+  Line L0, L1;
+  load_line<AXIS>(b, lane, L0);
+  load_line<AXIS>(b, lane + 32, L1);
+  uint32_t c0 = 0, c1 = 0;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {  // X+ (resp. Y+, Z+)
+    relax_line<AXIS>(L0, k, k - 1, 1, lim, c0);
+    relax_line<AXIS>(L1, k, k - 1, 1, lim, c1);
+  }
+#pragma unroll
+  for (int k = 6; k >= 0; --k) {  // X- (resp. Y-, Z-)
+    relax_line<AXIS>(L0, k, k + 1, -1, lim, c0);
+    relax_line<AXIS>(L1, k, k + 1, -1, lim, c1);
+  }
+  store_line<AXIS>(b, lane, L0, c0);
+  store_line<AXIS>(b, lane + 32, L1, c1);
+  return (c0 | c1) != 0;
+}
+
+// sweep_block — esdf/integrator.cpp:96-139: X, Y, Z phases until a pass
+// changes nothing.  Lines of one phase are disjoint, so order within a phase
+// is irrelevant; phases are ordered by __syncwarp.
+__device__ inline bool sweep_block_warp(BlockSmem& b, int lane, const Limits& lim,
+                                        int* passes = nullptr) {
+  bool block_changed = false;
+  int np = 0;
+  while (true) {
+    ++np;
+    bool c = sweep_phase_warp<0>(b, lane, lim);
+    __syncwarp();
+    c |= sweep_phase_warp<1>(b, lane, lim);
+    __syncwarp();
+    c |= sweep_phase_warp<2>(b, lane, lim);
+    const bool pass_changed = __any_sync(0xffffffffu, c);
+    __syncwarp();
+    block_changed |= pass_changed;
+    if (!pass_changed) break;
+  }
+  if (passes) *passes = np;
+  return block_changed;
+}
+
+// Block <-> shared memory (16-byte global accesses, swizzled SoA in smem).
+__device__ inline void load_block_warp(BlockSmem& b, const uint32_t* __restrict__ src, int lane) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll 4
+  for (int i = 0; i < 12; ++i) {
+    const int q = lane + 32 * i;
+    const uint4 v = __ldcg(s4 + q);
+    const uint32_t vals[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int w = 4 * q + e, lin = w / 3, f = w - 3 * lin;
+      const int si = swz_lin(lin);
+      (f == 0 ? b.w0 : (f == 1 ? b.w1 : b.w2))[si] = vals[e];
+    }
+  }
+}
+__device__ inline void store_block_warp(const BlockSmem& b, uint32_t* __restrict__ dst, int lane) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll 4
+  for (int i = 0; i < 12; ++i) {
+    const int q = lane + 32 * i;
+    uint32_t vals[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int w = 4 * q + e, lin = w / 3, f = w - 3 * lin;
+      const int si = swz_lin(lin);
+      vals[e] = (f == 0 ? b.w0 : (f == 1 ? b.w1 : b.w2))[si];
+    }
+    __stcg(d4 + q, make_uint4(vals[0], vals[1], vals[2], vals[3]));
+  }
+}
+
+// reset_parented (esdf/integrator.cpp:352-363) of a staged block; returns
+// whether the block holds any site (the only givers left after the reset).
+__device__ inline bool reset_block_warp(BlockSmem& b, int lane, const Limits& lim) {
+  bool any_site = false;
+#pragma unroll 4
+  for (int i = 0; i < 16; ++i) {
+    const int si = swz_lin(lane + 32 * i);
+    const uint32_t w1 = b.w1[si], w2 = b.w2[si];
+    const uint32_t f = (w2 >> 16) & 0xffu;
+    const bool hp = (w1 | (w2 & 0xffffu)) != 0;
+    any_site |= (f & (VXM_ESDF_OBSERVED | VXM_ESDF_SITE)) == (VXM_ESDF_OBSERVED | VXM_ESDF_SITE);
+    if ((f & VXM_ESDF_OBSERVED) && !(f & VXM_ESDF_SITE) && hp) {
+      b.w0[si] = uint32_t((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq);
+      b.w1[si] = 0u;
+      b.w2[si] = w2 & 0xffff0000u;
+    }
+  }
+  return __any_sync(0xffffffffu, any_site);
 }
 
 // ---- cooperative lowering kernel ------------------------------------------------
@@ -216,10 +517,14 @@ struct LowerArgs {
   uint32_t call_epoch;
   uint32_t lchg_tag;
   uint8_t* out_flags;
+  unsigned long long* trace;  // optional phase timestamps (VXM_TRACE_LOWER)
+  uint32_t* work_ctr;         // [2] dynamic sweep scheduling counters
+  unsigned long long* line_mask;  // [cap][3] lines touched by the last border phase
 };
 
 constexpr int kLowerThreads = 256;
-constexpr int kGroups = kLowerThreads / 64;
+constexpr int kLowerWarps = kLowerThreads / 32;
+constexpr size_t kLowerSmem = sizeof(BlockSmem) * kLowerWarps;
 
 __device__ inline const EV load_voxel(const uint32_t* pool, int32_t slot, int lin) {
   const uint32_t* p = pool + size_t(slot) * 1536 + lin * 3;
@@ -232,12 +537,21 @@ __device__ inline void store_voxel(uint32_t* pool, int32_t slot, int lin, const 
   __stcg(p + 2, ev_w2(v));
 }
 
-__global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
+__global__ void __launch_bounds__(kLowerThreads, 2) k_lower(LowerArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ BlockSmem s_blk[kGroups];
-  const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
+  uint32_t tr = 0;
+  auto stamp = [&]() {
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && tr < 255) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[1 + tr++] = t;
+      a.trace[0] = tr;
+    }
+  };
+  stamp();
+  extern __shared__ BlockSmem s_blk[];  // one staging block per warp
   const int lane = threadIdx.x & 31;
-  const int gid = blockIdx.x * kGroups + g, ngroups = gridDim.x * kGroups;
+  BlockSmem& blk = s_blk[threadIdx.x >> 5];
   const int wid = (blockIdx.x * kLowerThreads + threadIdx.x) >> 5;
   const int nwarps = gridDim.x * (kLowerThreads >> 5);
   const uint32_t n_blocks = a.meta->num_blocks;
@@ -259,7 +573,9 @@ __global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.count[1] = ns;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.work_ctr[0] = a.work_ctr[1] = 0u;
   grid.sync();
+  stamp();
   uint32_t r = 0;
   uint32_t n_pairs = 0, n_cmp = 0;  // per-warp work counters
   // while (!dirty.empty()) — an empty round-1 set runs zero rounds (:506)
@@ -276,32 +592,37 @@ __global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
         a.count[np] = 0;
         if (r > 1 || !a.full) a.status->sum_dirty += n_dirty;
       }
-      // ---- sweep phase: every dirty block to its internal fixed point
-      for (uint32_t i = gid; i < n_dirty; i += ngroups) {
-        const int32_t s = r1_full ? int32_t(i) : dirty[i];
-        BlockSmem& b = s_blk[g];
-        load_block(b, (r1_full ? pcur : work) + size_t(s) * 1536, t);
-        group_sync(1 + g);
-        if (r1_full) {  // reset_parented — esdf/integrator.cpp:352-363
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int si = swz_lin(t + 64 * k);
-            EV v = ev_unpack(b.w0[si], b.w1[si], b.w2[si]);
-            if ((v.f & VXM_ESDF_OBSERVED) && !(v.f & VXM_ESDF_SITE) && ev_has_parent(v)) {
-              reset_to_saturated(v, lim);
-              b.w0[si] = uint32_t(v.sq);
-              b.w1[si] = ev_w1(v);
-              b.w2[si] = ev_w2(v);
-            }
-          }
-          group_sync(1 + g);
+      // ---- sweep phase: every dirty block to its internal fixed point.
+      // A warp per block, blocks handed out dynamically (costs vary a lot).
+      uint32_t* const ctr = a.work_ctr + cp;
+      while (true) {
+        uint32_t i = 0;
+        if (lane == 0) i = atomicAdd(ctr, 1u);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= n_dirty) break;
+        const int32_t s = r1_full ? int32_t(i) : __ldcg(dirty + i);
+        load_block_warp(blk, (r1_full ? pcur : work) + size_t(s) * 1536, lane);
+        __syncwarp();
+        bool sweep = true;
+        if (r1_full) {
+          // After the reset only sites can give a distance: a block without
+          // sites is already at its fixed point (exact skip).
+          sweep = reset_block_warp(blk, lane, lim);
+          __syncwarp();
         }
-        const bool changed = sweep_block_group(b, t, 1 + g, lim);
-        if (r1_full || changed) store_block(b, work + size_t(s) * 1536, t);
-        if (changed && !a.full && t == 0) a.stamp_lchg[s] = a.lchg_tag;
-        group_sync(1 + g);
+        int passes = 0;
+        const bool changed = sweep && sweep_block_warp(blk, lane, lim, &passes);
+        if (a.trace && lane == 0 && r < 60) {  // debug: pass statistics per round
+          atomicMax(a.trace + 128 + r, (unsigned long long)passes);
+          atomicAdd(a.trace + 192 + r, (unsigned long long)passes);
+        }
+        if (r1_full || changed) store_block_warp(blk, work + size_t(s) * 1536, lane);
+        if (changed && !a.full && lane == 0) a.stamp_lchg[s] = a.lchg_tag;
+        __syncwarp();
       }
       grid.sync();
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.work_ctr[np] = 0u;  // next round's counter
+      stamp();
       // ---- border phase, one axis group at a time (esdf/integrator.cpp:517-559)
       for (int axis = 0; axis < 3; ++axis) {
         const uint32_t items = 2u * n_dirty;
@@ -355,6 +676,7 @@ __global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
           }
         }
         grid.sync();
+        stamp();
       }
       if (*((volatile uint32_t*)&a.count[np]) == 0) break;
     }
@@ -385,6 +707,218 @@ __global__ void __launch_bounds__(kLowerThreads) k_lower(LowerArgs a) {
     atomicAdd(&a.status->cmp_blocks, n_cmp);
   }
   grid.sync();
+  stamp();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.status->rounds = r;
+    a.status->n_esdf_blocks = n_blocks;
+    a.meta->round_epoch = base_epoch + r + 2;
+    if (a.full && lower) a.meta->cur = cur ^ 1u;
+  }
+}
+
+// ---- lowering v3: group-per-block sweeps with line masks --------------------------
+constexpr int kL3Threads = 256;
+constexpr int kL3Groups = kL3Threads / 64;
+
+__device__ inline void line_bits(int x, int y, int z, unsigned long long m[3]) {
+  m[0] |= 1ull << (y + 8 * z);  // X-line through the voxel
+  m[1] |= 1ull << (x + 8 * z);  // Y-line
+  m[2] |= 1ull << (x + 8 * y);  // Z-line
+}
+__device__ inline unsigned long long warp_or64(unsigned long long v) {
+  const uint32_t lo = __reduce_or_sync(0xffffffffu, uint32_t(v));
+  const uint32_t hi = __reduce_or_sync(0xffffffffu, uint32_t(v >> 32));
+  return (unsigned long long)hi << 32 | lo;
+}
+
+__global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  uint32_t tr = 0;
+  auto stamp = [&]() {
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && tr < 127) {
+      unsigned long long tm;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+      a.trace[1 + tr++] = tm;
+      a.trace[0] = tr;
+    }
+  };
+  stamp();
+  __shared__ GroupSmem s_grp[kL3Groups];
+  const int g = threadIdx.x >> 6, t = threadIdx.x & 63, lane = threadIdx.x & 31;
+  const int bar = 1 + g;
+  GroupSmem& G = s_grp[g];
+  const int wid = (blockIdx.x * kL3Threads + threadIdx.x) >> 5;
+  const int nwarps = gridDim.x * (kL3Threads >> 5);
+  const uint32_t n_blocks = a.meta->num_blocks;
+  const uint32_t cur = a.meta->cur;
+  const uint32_t base_epoch = a.meta->round_epoch;
+  const bool failed = a.status->capacity_error || a.status->pool_overflow;
+  const bool lower = !failed && (a.full ? a.status->any_update != 0 : true);
+  uint32_t* const pcur = a.pool[cur];
+  uint32_t* const pnxt = a.pool[cur ^ 1u];
+  uint32_t* const work = a.full ? pnxt : pcur;
+  const Limits lim = a.lim;
+  if (!a.full && lower) {  // seeded mode: round-1 dirty list = seeds
+    const uint32_t ns = *a.n_seeds;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+      const int32_t s = a.seeds[i];
+      a.list[1][i] = s;
+      a.stamp_dirty[1][s] = base_epoch + 1;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.count[1] = ns;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.work_ctr[0] = a.work_ctr[1] = 0u;
+  grid.sync();
+  stamp();
+  uint32_t r = 0;
+  uint32_t n_pairs = 0, n_cmp = 0;
+  const uint32_t n_first = a.full ? n_blocks : *((volatile uint32_t*)&a.count[1]);
+  if (lower && n_first > 0) {  // while (!dirty.empty()) — esdf/integrator.cpp:506
+    while (true) {
+      ++r;
+      const int cp = int(r & 1u), np = cp ^ 1;
+      const uint32_t ep = base_epoch + r, ep_next = ep + 1;
+      const bool r1_full = a.full && r == 1;
+      const uint32_t n_dirty = r1_full ? n_blocks : *((volatile uint32_t*)&a.count[cp]);
+      const int32_t* dirty = a.list[cp];
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.count[np] = 0;
+        if (r > 1 || !a.full) a.status->sum_dirty += n_dirty;
+      }
+      // ---- sweep phase (esdf/integrator.cpp:509-513)
+      uint32_t* const ctr = a.work_ctr + cp;
+      while (true) {
+        if (t == 0) G.bcast = atomicAdd(ctr, 1u);
+        group_sync(bar);
+        const uint32_t i = G.bcast;
+        if (i >= n_dirty) break;
+        const int32_t s = r1_full ? int32_t(i) : __ldcg(dirty + i);
+        load_block3(G, (r1_full ? pcur : work) + size_t(s) * 1536, t, bar);
+        if (t == 0) {
+          unsigned long long m0 = ~0ull, m1 = ~0ull, m2 = ~0ull;
+          if (a.full && !r1_full) {  // lines through voxels changed by the last borders
+            m0 = atomicExch(a.line_mask + 3 * size_t(s), 0ull);
+            m1 = atomicExch(a.line_mask + 3 * size_t(s) + 1, 0ull);
+            m2 = atomicExch(a.line_mask + 3 * size_t(s) + 2, 0ull);
+          }
+          G.mask[0][0] = m0;
+          G.mask[1][0] = m1;
+          G.mask[2][0] = m2;
+          G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
+        }
+        bool do_sweep = true;
+        if (r1_full) do_sweep = reset_block3(G, t, bar, lim);  // also orders the mask init
+        else group_sync(bar);
+        const bool changed = do_sweep && sweep_block3(G, t, bar, lim);
+        if (r1_full || changed) store_block3(G, work + size_t(s) * 1536, t);
+        if (changed && !a.full && t == 0) a.stamp_lchg[s] = a.lchg_tag;
+        group_sync(bar);
+      }
+      grid.sync();
+      stamp();
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.work_ctr[np] = 0u;
+      // ---- border phase, one axis group at a time (esdf/integrator.cpp:517-559)
+      for (int axis = 0; axis < 3; ++axis) {
+        const uint32_t items = 2u * n_dirty;
+        for (uint32_t w = wid; w < items; w += nwarps) {
+          const uint32_t i = w >> 1;
+          const int side = int(w & 1u);
+          const int32_t d = r1_full ? int32_t(i) : __ldcg(dirty + i);
+          int32_t lo, hi;
+          if (side == 0) {
+            hi = __ldg(a.nbr + size_t(d) * 6 + 2 * axis);  // d + axis
+            lo = d;
+            if (hi < 0) continue;
+          } else {
+            lo = __ldg(a.nbr + size_t(d) * 6 + 2 * axis + 1);  // d - axis
+            hi = d;
+            if (lo < 0) continue;
+            // pair (lo, d) is handled by lo's side-0 item when lo is dirty
+            if (r1_full || __ldcg(a.stamp_dirty[cp] + lo) == ep) continue;
+          }
+          const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
+          bool ac = false, bc = false;
+          unsigned long long mlo[3] = {0, 0, 0}, mhi[3] = {0, 0, 0};
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
+            int ax, ay, az, bx, by, bz;
+            if (axis == 0) { ax = 7; ay = i0; az = j0; bx = 0; by = i0; bz = j0; }
+            else if (axis == 1) { ax = i0; ay = 7; az = j0; bx = i0; by = 0; bz = j0; }
+            else { ax = i0; ay = j0; az = 7; bx = i0; by = j0; bz = 0; }
+            const int la = ax + 8 * ay + 64 * az, lb = bx + 8 * by + 64 * bz;
+            EV va = load_voxel(work, lo, la), vb = load_voxel(work, hi, lb);
+            const bool cb = relax(vb, va, dx, dy, dz, lim);     // exchange_pair :158
+            const bool ca = relax(va, vb, -dx, -dy, -dz, lim);  // :159
+            if (cb) {
+              store_voxel(work, hi, lb, vb);
+              line_bits(bx, by, bz, mhi);
+            }
+            if (ca) {
+              store_voxel(work, lo, la, va);
+              line_bits(ax, ay, az, mlo);
+            }
+            ac |= ca;
+            bc |= cb;
+          }
+          ac = __any_sync(0xffffffffu, ac);
+          bc = __any_sync(0xffffffffu, bc);
+          ++n_pairs;
+          const int32_t who[2] = {lo, hi};
+          const bool chg[2] = {ac, bc};
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (!chg[q]) continue;
+            if (a.full) {
+              unsigned long long* m = q == 0 ? mlo : mhi;
+              const unsigned long long r0 = warp_or64(m[0]), r1 = warp_or64(m[1]), r2 = warp_or64(m[2]);
+              if (lane == 0) {
+                atomicOr(a.line_mask + 3 * size_t(who[q]), r0);
+                atomicOr(a.line_mask + 3 * size_t(who[q]) + 1, r1);
+                atomicOr(a.line_mask + 3 * size_t(who[q]) + 2, r2);
+              }
+            }
+            if (lane == 0) {
+              if (!a.full) a.stamp_lchg[who[q]] = a.lchg_tag;
+              if (atomicMax(a.stamp_dirty[np] + who[q], ep_next) < ep_next) {
+                const uint32_t slot = atomicAdd(a.count + np, 1u);
+                a.list[np][slot] = who[q];
+              }
+            }
+          }
+        }
+        grid.sync();
+        stamp();
+      }
+      if (*((volatile uint32_t*)&a.count[np]) == 0) break;
+    }
+  }
+  // ---- changed set of update_esdf (esdf/integrator.cpp:403-411) -------------
+  if (a.full) {
+    for (uint32_t k = wid; k < n_blocks; k += nwarps) {
+      const int32_t s = a.sorted_slots[k];
+      bool ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
+      if (!ch && lower) {
+        const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(s) * 1536);
+        const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(s) * 1536);
+        bool diff = false;
+#pragma unroll 4
+        for (int q = lane; q < 384; q += 32) {
+          const uint4 x = __ldcg(p0 + q), y = __ldcg(p1 + q);
+          diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+        }
+        ch = __any_sync(0xffffffffu, diff);
+        ++n_cmp;
+      }
+      if (lane == 0) a.out_flags[k] = uint8_t(ch);
+    }
+  }
+  if (lane == 0 && (n_pairs | n_cmp)) {
+    atomicAdd(&a.status->sum_pairs, n_pairs);
+    atomicAdd(&a.status->cmp_blocks, n_cmp);
+  }
+  grid.sync();
+  stamp();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.status->rounds = r;
     a.status->n_esdf_blocks = n_blocks;
@@ -894,19 +1428,38 @@ static int lower_grid(Context* ctx) {
   static int cached = -1;
   if (cached < 0) {
     int bps = 0;
-    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lower, kLowerThreads, 0));
+    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lower3, kL3Threads, 0));
     cached = std::max(1, std::min(bps, 4)) * ctx->sm_count;
   }
   return cached;
 }
 
 static void launch_lower(Context* ctx, LowerArgs& la) {
+  static const bool trace = std::getenv("VXM_TRACE_LOWER") != nullptr;
+  static DevBuf trace_buf;
+  if (trace) {
+    trace_buf.ensure(256 * sizeof(unsigned long long));
+    VXM_CUDA(cudaMemsetAsync(trace_buf.p, 0, 256 * sizeof(unsigned long long), ctx->stream));
+    la.trace = trace_buf.as<unsigned long long>();
+  }
   void* args[] = {&la};
   const int grid = lower_grid(ctx);
   ctx->prof_begin("k_lower");
-  VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lower, dim3(grid), dim3(kLowerThreads), args, 0,
+  VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lower3, dim3(grid), dim3(kL3Threads), args, 0,
                                        ctx->stream));
   ctx->prof_end();
+  if (trace) {
+    unsigned long long h[256];
+    VXM_CUDA(cudaMemcpyAsync(h, trace_buf.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::fprintf(stderr, "[k_lower grid=%d] phases(us):", grid);
+    for (unsigned long long i = 2; i <= h[0] && i < 128; ++i)
+      std::fprintf(stderr, " %.1f", (h[i] - h[i - 1]) * 1e-3);
+    std::fprintf(stderr, " | total %.1f\n  passes max/total per round:",
+                 h[0] > 1 ? (h[h[0]] - h[1]) * 1e-3 : 0.0);
+    for (int r = 1; r < 60 && h[192 + r]; ++r) std::fprintf(stderr, " %llu/%llu", h[128 + r], h[192 + r]);
+    std::fprintf(stderr, "\n");
+  }
   ctx->count_launch();
 }
 
@@ -922,6 +1475,8 @@ static LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.list[0] = E->dirty_list[0];
   la.list[1] = E->dirty_list[1];
   la.count = E->dirty_count;
+  la.work_ctr = E->dirty_count + 2;
+  la.line_mask = E->line_mask;
   la.lim = limits_for(cfg, E->vs);
   la.status = E->ctx->d_status;
   return la;
@@ -932,7 +1487,7 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
   Context* ctx = E->ctx;
   const uint32_t epoch = ++ctx->call_epoch;
   ctx->reset_status();
-  E->refresh();
+  // E->num_blocks is exact: every call that allocates adopts the meta at its end.
   const uint32_t n7 = 7u * std::max<uint32_t>(updated->count_hint, 1);
   // capacity for every effective block (bounded by the logical limit)
   E->ensure_capacity(std::min<uint64_t>(uint64_t(E->num_blocks) + n7, E->max_blocks));
@@ -957,8 +1512,9 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
                            cudaMemcpyDeviceToDevice, ctx->stream));  // n_effective, n_esdf_new
   VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_out, changed_out->d_count, sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, ctx->stream));
+  E->stage_meta();
   ctx->sync_status();
-  E->refresh();
+  E->adopt_meta();
   const DevStatus& st = *ctx->h_status;
   if (st.capacity_error || st.pool_overflow)
     throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");

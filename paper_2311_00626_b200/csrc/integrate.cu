@@ -315,9 +315,10 @@ void run_integrate(Layer* L, const ViewArgs& va, const vxm_integrator_config& cf
     changed_out->count_hint = cand_cap;
     VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_changed, changed_out->d_count, sizeof(uint32_t),
                              cudaMemcpyDeviceToDevice, ctx->stream));
+    L->stage_meta();
     ctx->sync_status();
     const DevStatus& s = *ctx->h_status;
-    L->refresh();
+    L->adopt_meta();
     if (s.bitmap_overflow)
       throw Error(VXM_ERR_INTERNAL, "candidate ray left the candidate cube (bitmap bound)");
     if (s.pool_overflow) {

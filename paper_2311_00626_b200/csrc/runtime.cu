@@ -133,6 +133,15 @@ void Layer::refresh() {
   cur_host = m.cur;
 }
 
+void Layer::stage_meta() {
+  VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->meta_blocks, meta, 2 * sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+}
+void Layer::adopt_meta() {
+  num_blocks = ctx->h_status->meta_blocks;
+  cur_host = ctx->h_status->meta_cur;
+}
+
 void Layer::ensure_capacity(uint64_t need) {
   if (need <= capacity) return;
   if (need > (uint64_t(1) << 31) - 1)
@@ -174,6 +183,7 @@ void Layer::ensure_capacity(uint64_t need) {
     grow_copy(&stamp_mark, capacity, live, nc, 0, st);
     grow_copy(&stamp_new, capacity, live, nc, 0, st);
     grow_copy(&stamp_lchg, capacity, live, nc, 0, st);
+    grow_copy(&line_mask, capacity * 3ull, live * 3ull, nc * 3ull, 0, st);
   }
   // hash: power of two >= 2 * capacity, rebuilt from slot_keys
   uint64_t hc = 1024;
@@ -215,6 +225,7 @@ Layer::~Layer() {
   if (stamp_new) cudaFree(stamp_new);
   if (stamp_lchg) cudaFree(stamp_lchg);
   if (dirty_count) cudaFree(dirty_count);
+  if (line_mask) cudaFree(line_mask);
 }
 
 // ---- BlockList -----------------------------------------------------------------
@@ -252,21 +263,25 @@ const std::vector<vxm_grid_index>& BlockList::fetch() {
 
 void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
   ensure(uint32_t(std::max<uint64_t>(n, 1)));
-  std::vector<uint64_t> k(n);
+  staging.resize(n + 1);
+  bool sorted = true;
   for (uint64_t i = 0; i < n; ++i) {
     if (!coord_ok(data[i].x) || !coord_ok(data[i].y) || !coord_ok(data[i].z))
       throw Error(VXM_ERR_INVALID_ARGUMENT, "block index outside the supported range (+-2^20)");
-    k[i] = pack_key(data[i].x, data[i].y, data[i].z);
+    staging[i] = pack_key(data[i].x, data[i].y, data[i].z);
+    sorted &= i == 0 || staging[i - 1] < staging[i];  // input validation only
   }
+  staging[n] = n;  // count travels in the same copy (low 32 bits)
   const uint32_t n32 = uint32_t(n);
-  if (n)
-    VXM_CUDA(cudaMemcpyAsync(keys.p, k.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
-                             ctx->stream));
-  VXM_CUDA(cudaMemcpyAsync(d_count, &n32, sizeof n32, cudaMemcpyHostToDevice, ctx->stream));
-  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  VXM_CUDA(cudaMemcpyAsync(keys.p, staging.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  VXM_CUDA(cudaMemcpyAsync(d_count, &staging[n], sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  // staging stays alive (member) until the next assign, so no sync is needed here
   host.assign(data, data + n);
   host_valid = true;
   count_hint = n32;
+  sorted_unique = sorted;
 }
 
 BlockList::~BlockList() {

@@ -71,6 +71,7 @@ struct Context {
   std::map<std::string, std::pair<double, uint64_t>> ktime;
   const char* prof_name = nullptr;
   cudaEvent_t prof_a = nullptr;
+  struct BlockList* scratch_in = nullptr;  // reused host-input list (C-ABI host paths)
 
   // Scan pass bookkeeping: returns the ScanTiles for the next pass with at
   // most `tiles` tiles, clearing the other buffer for the pass after.
@@ -106,7 +107,8 @@ struct Layer {
   uint32_t* stamp_new = nullptr;    // call epoch when the block was allocated
   uint32_t* stamp_lchg = nullptr;   // round epoch of the last lowering change
   int32_t* dirty_list[2] = {nullptr, nullptr};
-  uint32_t* dirty_count = nullptr;  // [2]
+  uint32_t* dirty_count = nullptr;  // [2] dirty counts + [2] sweep work counters
+  unsigned long long* line_mask = nullptr;  // [cap][3] lines changed by border phases
 
   size_t voxel_bytes() const { return type == VXM_LAYER_TSDF ? 8 : 12; }
   size_t block_bytes() const { return voxel_bytes() * kVPB; }
@@ -115,6 +117,10 @@ struct Layer {
   void ensure_capacity(uint64_t need);
   uint64_t limit() const { return max_blocks; }
   void refresh();  // sync + read meta (num_blocks, cur)
+  // Enqueue a copy of the meta into the context status (read by sync_status)
+  // and, after the sync, adopt it: one host round trip per API call.
+  void stage_meta();
+  void adopt_meta();
   ~Layer();
 };
 
@@ -126,6 +132,8 @@ struct BlockList {
   uint32_t count_hint = 0;     // host upper bound of count
   std::vector<vxm_grid_index> host;
   bool host_valid = true;
+  bool sorted_unique = false;  // keys are in strictly increasing GridIndex order
+  std::vector<uint64_t> staging;  // host staging of assign_host (kept alive for async copies)
   void ensure(uint32_t n);
   const std::vector<vxm_grid_index>& fetch();   // sync + download + unpack
   void assign_host(const vxm_grid_index* data, uint64_t n);  // upload (sorted as given)

@@ -237,6 +237,13 @@ class _Layer:
         except Exception:
             pass
 
+    def _result_list(self) -> "BlockList":
+        """Reused result list (results are copied to numpy immediately)."""
+        lst = getattr(self, "_out", None)
+        if lst is None:
+            lst = self._out = BlockList(self.ctx)
+        return lst
+
     @property
     def voxel_size(self) -> float:
         return float(lib().vxm_layer_voxel_size(self.h))
@@ -322,7 +329,7 @@ def integrate_depth(layer: TsdfLayer, depth, T_LS, intrinsics, cfg=None, out: Bl
     returns the sorted indices of the blocks whose bytes changed."""
     cfg = cfg or IntegratorConfig()
     d = _depth(depth)
-    out = out or BlockList(layer.ctx)
+    out = out or layer._result_list()
     fn = (lib().vxm_integrate_depth_camera if isinstance(intrinsics, A.Camera)
           else lib().vxm_integrate_depth_lidar)
     check(fn(layer.h, A.ptr(d), C.c_int(d.shape[1]), C.c_int(d.shape[0]), C.byref(_pose_c(T_LS)),
@@ -357,7 +364,7 @@ def update_esdf(esdf: EsdfLayer, tsdf: TsdfLayer, updated, cfg=None, out: BlockL
     """update_esdf (esdf/integrator.hpp:113-116). `updated` may be a BlockList
     (e.g. the device-resident output of integrate_depth) or an (N,3) array."""
     cfg = cfg or EsdfConfig()
-    out = out or BlockList(esdf.ctx)
+    out = out or esdf._result_list()
     if isinstance(updated, BlockList):
         check(lib().vxm_update_esdf_list(esdf.h, tsdf.h, updated.h, C.byref(cfg), out.h))
     else:
