@@ -1,0 +1,167 @@
+// C++ facade parity test (GPU): the reference's C++ API shape through
+// include/voxmap_b200/voxmap.hpp, checked bit-for-bit against the C oracle
+// (oracle/voxmap_oracle.c).  Mirrors proj/tests/integrate_test.cpp:225-363 and
+// esdf_test.cpp:232-269, 377-398.  Exit code 0 = pass.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "voxmap_b200/voxmap.hpp"
+#include "voxmap_b200_synth.h"
+#include "voxmap_oracle.h"
+
+namespace vb = voxmap_b200;
+
+static int failures = 0;
+#define CHECK(cond)                                                      \
+  do {                                                                   \
+    if (!(cond)) {                                                       \
+      std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+      ++failures;                                                        \
+    }                                                                    \
+  } while (0)
+
+static vb::Pose pose_of(const vxm_pose& p) {
+  vb::Pose T;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) T.R(r, c) = p.R[3 * r + c];
+  T.t = {p.t[0], p.t[1], p.t[2]};
+  return T;
+}
+
+static std::vector<vb::GridIndex> oracle_list(vxm_grid_index* p, uint64_t n) {
+  std::vector<vb::GridIndex> v = vb::from_c(p, n);
+  vxo_free(p);
+  return v;
+}
+
+template <typename V>
+static bool same_layer(const vb::Layer<V>& g, const vxo_layer* o) {
+  const auto keys = g.sorted_indices();
+  const uint64_t n = vxo_layer_num_blocks(o);
+  if (keys.size() != n) return false;
+  std::vector<vxm_grid_index> ok(n);
+  std::vector<V> ov(n * 512);
+  vxo_layer_export(o, ok.data(), ov.data());
+  for (uint64_t i = 0; i < n; ++i) {
+    if (keys[i].x != ok[i].x || keys[i].y != ok[i].y || keys[i].z != ok[i].z) return false;
+    const auto* b = g.block_ptr(keys[i]);
+    if (!b || std::memcmp(b->voxels.data(), ov.data() + i * 512, sizeof(V) * 512) != 0) return false;
+  }
+  return true;
+}
+
+int main() {
+  vxm_scene* scene = nullptr;
+  vxm_synth_scene_create("sphere_in_box", &scene);
+  vb::CameraIntrinsics cam;
+  cam.width = 160;
+  cam.height = 120;
+  cam.fu = cam.fv = cam.cu = 80.0;
+  cam.cv = 60.0;
+  cam.max_depth = 10.0;
+  const vxm_camera cam_c = cam.c();
+  vb::IntegratorConfig cfg;
+  cfg.truncation = 0.2;
+  const vxm_integrator_config cfg_c = cfg.c();
+  vb::EsdfConfig ecfg;
+  ecfg.site_threshold = 0.05;
+  const vxm_esdf_config ecfg_c = ecfg.c();
+
+  vb::Layer<vb::TsdfVoxel> tsdf(0.05);
+  vb::Layer<vb::EsdfVoxel> esdf(0.05);
+  vxo_layer *otsdf = nullptr, *oesdf = nullptr;
+  vxo_layer_create(VXM_LAYER_TSDF, 0.05, 0, &otsdf);
+  vxo_layer_create(VXM_LAYER_ESDF, 0.05, 0, &oesdf);
+
+  for (int k = 0; k < 3; ++k) {  // integrate_test.cpp:243-261 shape
+    vxm_pose p;
+    vxm_synth_orbit_pose(scene, 0, k, 8, &p);
+    vb::DepthImage depth(cam.width, cam.height);
+    vxm_synth_render_camera(scene, &p, &cam_c, depth.data.data());
+    const auto a = vb::integrate_depth(tsdf, depth, pose_of(p), cam, cfg);
+    vxm_grid_index* ob = nullptr;
+    uint64_t on = 0;
+    vxo_integrate_camera(otsdf, depth.data.data(), depth.width, depth.height, &p, &cam_c, &cfg_c, &ob, &on);
+    const auto b = oracle_list(ob, on);
+    CHECK(!a.empty());
+    CHECK(a == b);
+    const auto ea = vb::update_esdf(esdf, tsdf, a, ecfg);
+    const auto bc = vb::to_c(b);
+    vxo_update_esdf(oesdf, otsdf, bc.data(), bc.size(), &ecfg_c, &ob, &on);
+    CHECK(ea == oracle_list(ob, on));
+  }
+  CHECK(same_layer(tsdf, otsdf));
+  CHECK(same_layer(esdf, oesdf));
+
+  // Host writes through block_ptr() are seen by the next device operation
+  // (Layer handles stay valid, layer.hpp:44-46).
+  {
+    const auto keys = tsdf.sorted_indices();
+    auto* blk = tsdf.block_ptr(keys.front());
+    CHECK(blk != nullptr);
+    blk->voxels[0].distance = 0.0f;
+    blk->voxels[0].weight = 1.0f;
+    CHECK(tsdf.block_ptr(keys.front())->voxels[0].weight == 1.0f);
+    const vb::Layer<vb::TsdfVoxel> copy = tsdf.clone();
+    CHECK(copy.block_ptr(keys.front())->voxels[0].weight == 1.0f);
+  }
+
+  // Errors map onto the reference's exception types (integrate_test.cpp:447-488).
+  {
+    vb::Layer<vb::TsdfVoxel> layer(0.05);
+    vb::DepthImage wrong(32, 48);
+    vb::CameraIntrinsics c64 = cam;
+    c64.width = 64;
+    c64.height = 48;
+    bool threw = false;
+    try {
+      vb::integrate_depth(layer, wrong, vb::Pose::identity(), c64, cfg);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    vb::Pose bad;
+    bad.R(0, 0) = 2.0;
+    threw = false;
+    try {
+      vb::DepthImage d(64, 48);
+      vb::integrate_depth(layer, d, bad, c64, cfg);
+    } catch (const vb::InvalidPoseError&) {
+      threw = true;
+    }
+    CHECK(threw);
+    CHECK(layer.num_blocks() == 0);
+  }
+
+  // Queries (query.cpp production order) — bitwise vs the oracle.
+  {
+    std::vector<vb::Vec3> pts;
+    std::vector<double> flat;
+    for (int i = 0; i < 500; ++i) {
+      const vb::Vec3 q{0.1 + 0.0057 * i, 0.3 + 0.0041 * i, 0.2 + 0.0033 * i};
+      pts.push_back(q);
+      flat.insert(flat.end(), {q.x, q.y, q.z});
+    }
+    vb::QueryConfig qc;
+    const auto got = vb::query_batch(esdf, pts, true, qc);
+    std::vector<vxm_query_result> want(pts.size());
+    const vxm_query_config qcc{1, 1};
+    vxo_query_batch(oesdf, flat.data(), pts.size(), 1, &qcc, want.data());
+    int known = 0;
+    for (size_t i = 0; i < pts.size(); ++i) {
+      CHECK(got[i].known == (want[i].known != 0));
+      CHECK(got[i].distance == want[i].distance);
+      CHECK(got[i].gradient.x == want[i].gradient[0] && got[i].gradient.y == want[i].gradient[1] &&
+            got[i].gradient.z == want[i].gradient[2]);
+      known += got[i].known;
+    }
+    CHECK(known > 50);
+  }
+
+  vxo_layer_destroy(otsdf);
+  vxo_layer_destroy(oesdf);
+  vxm_synth_scene_destroy(scene);
+  std::printf("facade_test: %s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
+  return failures ? 1 : 0;
+}
