@@ -242,7 +242,10 @@ vxm_status vxm_context_create(int device, vxm_context** out) {
     VXM_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     VXM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DevStatus)));
     VXM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DevStatus)));
-    VXM_CUDA(cudaMemset(ctx->d_status, 0, sizeof(DevStatus)));
+    // The context stream is non-blocking: every initialisation is ordered on
+    // it, never on the legacy stream (which it does not synchronise with).
+    VXM_CUDA(cudaMemsetAsync(ctx->d_status, 0, sizeof(DevStatus), ctx->stream));
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = ctx;
   });
 }
@@ -343,10 +346,13 @@ vxm_status vxm_layer_create(vxm_context* ctx, vxm_layer_type type, double vs, ui
     L->vs = vs;
     L->max_blocks = max_blocks ? max_blocks : (uint64_t(1) << 30);
     VXM_CUDA(cudaMalloc(&L->meta, sizeof(LayerMeta)));
-    VXM_CUDA(cudaMemset(L->meta, 0, sizeof(LayerMeta)));
+    // stream-ordered zeroing (the context stream does not sync with the
+    // legacy stream, so a plain cudaMemset could land after the first read)
+    VXM_CUDA(cudaMemsetAsync(L->meta, 0, sizeof(LayerMeta), ctx->stream));
     if (type == VXM_LAYER_ESDF) {
-      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * 4));
-      VXM_CUDA(cudaMemset(L->dirty_count, 0, sizeof(uint32_t) * 4));
+      // [0..2] dirty-list counts, [3..6] sweep / pair work counters by parity
+      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * 8));
+      VXM_CUDA(cudaMemsetAsync(L->dirty_count, 0, sizeof(uint32_t) * 8, ctx->stream));
     }
     L->ensure_capacity(std::min<uint64_t>(4096, L->max_blocks));
     *out = L;

@@ -70,29 +70,34 @@ struct HashView {
   uint32_t mask;
 };
 
+// Probing is bounded by the table size (tables are kept at most half full, so
+// the bound is never reached; it only turns a corrupted table into a miss
+// instead of a GPU hang).
 __device__ inline int32_t hash_find(const HashView& h, uint64_t k) {
   uint32_t i = hash_key(k) & h.mask;
-  while (true) {
+  for (uint32_t n = 0; n <= h.mask; ++n) {
     const uint64_t kk = __ldg(h.keys + i);
     if (kk == k) return __ldg(h.vals + i);
     if (kk == kEmptyKey) return -1;
     i = (i + 1) & h.mask;
   }
+  return -1;
 }
 // Mutable-table lookup (no read-only cache): used in kernels that also insert.
 __device__ inline int32_t hash_find_rw(const HashView& h, uint64_t k) {
   uint32_t i = hash_key(k) & h.mask;
-  while (true) {
+  for (uint32_t n = 0; n <= h.mask; ++n) {
     const uint64_t kk = h.keys[i];
     if (kk == k) return h.vals[i];
     if (kk == kEmptyKey) return -1;
     i = (i + 1) & h.mask;
   }
+  return -1;
 }
 // Keys inserted by one launch are unique, so CAS-claim then write the value.
 __device__ inline void hash_insert(const HashView& h, uint64_t k, int32_t v) {
   uint32_t i = hash_key(k) & h.mask;
-  while (true) {
+  for (uint32_t n = 0; n <= h.mask; ++n) {
     const unsigned long long prev =
         atomicCAS(reinterpret_cast<unsigned long long*>(h.keys + i),
                   (unsigned long long)kEmptyKey, (unsigned long long)k);
@@ -135,6 +140,8 @@ struct DevStatus {
   uint32_t n_esdf_blocks;    // ESDF blocks after the update
   uint32_t meta_blocks;      // copy of the layer's LayerMeta {num_blocks, cur}
   uint32_t meta_cur;         //   taken with the status read (one sync per call)
+  uint32_t watchdog;         // a bounded dependency wait expired (internal error)
+  uint32_t pad3[3];
 };
 
 // ---- decoupled look-back scan over (a, b) count pairs ------------------------

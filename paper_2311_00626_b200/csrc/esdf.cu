@@ -122,10 +122,6 @@ __device__ inline void group_sync(int id) {
   asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 
-struct BlockSmem {
-  uint32_t w0[512], w1[512], w2[512];
-};
-
 // ===== sweep v3: one 64-thread group per block, one line per thread ============
 // Working format in shared memory (converted from the reference's 12-byte voxel
 // on load and back on store):
@@ -324,178 +320,6 @@ __device__ inline bool reset_block3(GroupSmem& g, int t, int bar, const Limits& 
   return group_sync_or(bar, any_site);
 }
 
-// Register form of one line of 8 voxels (sweep).  Flags live in bitmasks so
-// relax is branch-free: take = observed && !site, give = observed && (site ||
-// has_parent), hp = has_parent, in = inside.
-struct Line {
-  int sq[8], px[8], py[8], pz[8];
-  uint32_t take, give, hp, in;
-};
-
-template <int AXIS>
-__device__ inline int line_idx(int q, int k) {  // q in [0, 64): the orthogonal coords
-  const int c0 = q & 7, c1 = q >> 3;
-  const int x = AXIS == 0 ? k : c0;
-  const int y = AXIS == 1 ? k : (AXIS == 0 ? c0 : c1);
-  const int z = AXIS == 2 ? k : c1;
-  return swz(x, y, z);
-}
-
-template <int AXIS>
-__device__ inline void load_line(const BlockSmem& b, int q, Line& L) {
-  L.take = L.give = L.hp = L.in = 0u;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = line_idx<AXIS>(q, k);
-    const uint32_t w1 = b.w1[i], w2 = b.w2[i];
-    L.sq[k] = int(b.w0[i]);
-    L.px[k] = int(int16_t(w1 & 0xffffu));
-    L.py[k] = int(int16_t(w1 >> 16));
-    L.pz[k] = int(int16_t(w2 & 0xffffu));
-    const uint32_t f = (w2 >> 16) & 0xffu;
-    const bool obs = f & VXM_ESDF_OBSERVED, site = f & VXM_ESDF_SITE;
-    const bool hp = (L.px[k] | L.py[k] | L.pz[k]) != 0;
-    L.take |= uint32_t(obs && !site) << k;
-    L.give |= uint32_t(obs && (site || hp)) << k;
-    L.hp |= uint32_t(hp) << k;
-    L.in |= uint32_t((f & VXM_ESDF_INSIDE) != 0) << k;
-  }
-}
-
-// relax(v[k] <- v[j]) with step s along AXIS — esdf/integrator.cpp:58-88.
-template <int AXIS>
-__device__ __forceinline__ void relax_line(Line& L, int k, int j, int s, const Limits& lim,
-                                           uint32_t& ch) {
-  int cx = L.px[j], cy = L.py[j], cz = L.pz[j];
-  if (AXIS == 0) cx -= s;
-  else if (AXIS == 1) cy -= s;
-  else cz -= s;
-  const int cand = int(uint32_t(cx * cx) + uint32_t(cy * cy) + uint32_t(cz * cz));
-  const int lim_k = ((L.in >> k) & 1u) ? lim.cap_sq : lim.max_sq;
-  const bool less = cx < L.px[k] || (cx == L.px[k] && (cy < L.py[k] || (cy == L.py[k] && cz < L.pz[k])));
-  const bool better = cand < L.sq[k] || (cand == L.sq[k] && (!((L.hp >> k) & 1u) || less));
-  const bool ok = ((L.give >> j) & (L.take >> k) & 1u) && cand != 0 && cand <= lim_k && better;
-  if (ok) {
-    L.sq[k] = cand;
-    L.px[k] = int(int16_t(cx));
-    L.py[k] = int(int16_t(cy));
-    L.pz[k] = int(int16_t(cz));
-    L.hp |= 1u << k;
-    L.give |= 1u << k;
-    ch |= 1u << k;
-  }
-}
-
-template <int AXIS>
-__device__ inline void store_line(BlockSmem& b, int q, const Line& L, uint32_t ch) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (ch & (1u << k)) {
-      const int i = line_idx<AXIS>(q, k);
-      b.w0[i] = uint32_t(L.sq[k]);
-      b.w1[i] = (uint32_t(L.px[k]) & 0xffffu) | (uint32_t(L.py[k]) << 16);
-      b.w2[i] = (b.w2[i] & 0xffff0000u) | (uint32_t(L.pz[k]) & 0xffffu);
-    }
-}
-
-// One directional phase (X, Y or Z) of sweep_block for a whole block by one
-// warp: lane owns lines `lane` and `lane + 32`, interleaved for ILP.
-template <int AXIS>
-__device__ inline bool sweep_phase_warp(BlockSmem& b, int lane, const Limits& lim) {
-  Line L0, L1;
-  load_line<AXIS>(b, lane, L0);
-  load_line<AXIS>(b, lane + 32, L1);
-  uint32_t c0 = 0, c1 = 0;
-#pragma unroll
-  for (int k = 1; k < 8; ++k) {  // X+ (resp. Y+, Z+)
-    relax_line<AXIS>(L0, k, k - 1, 1, lim, c0);
-    relax_line<AXIS>(L1, k, k - 1, 1, lim, c1);
-  }
-#pragma unroll
-  for (int k = 6; k >= 0; --k) {  // X- (resp. Y-, Z-)
-    relax_line<AXIS>(L0, k, k + 1, -1, lim, c0);
-    relax_line<AXIS>(L1, k, k + 1, -1, lim, c1);
-  }
-  store_line<AXIS>(b, lane, L0, c0);
-  store_line<AXIS>(b, lane + 32, L1, c1);
-  return (c0 | c1) != 0;
-}
-
-// sweep_block — esdf/integrator.cpp:96-139: X, Y, Z phases until a pass
-// changes nothing.  Lines of one phase are disjoint, so order within a phase
-// is irrelevant; phases are ordered by __syncwarp.
-__device__ inline bool sweep_block_warp(BlockSmem& b, int lane, const Limits& lim,
-                                        int* passes = nullptr) {
-  bool block_changed = false;
-  int np = 0;
-  while (true) {
-    ++np;
-    bool c = sweep_phase_warp<0>(b, lane, lim);
-    __syncwarp();
-    c |= sweep_phase_warp<1>(b, lane, lim);
-    __syncwarp();
-    c |= sweep_phase_warp<2>(b, lane, lim);
-    const bool pass_changed = __any_sync(0xffffffffu, c);
-    __syncwarp();
-    block_changed |= pass_changed;
-    if (!pass_changed) break;
-  }
-  if (passes) *passes = np;
-  return block_changed;
-}
-
-// Block <-> shared memory (16-byte global accesses, swizzled SoA in smem).
-__device__ inline void load_block_warp(BlockSmem& b, const uint32_t* __restrict__ src, int lane) {
-  const uint4* s4 = reinterpret_cast<const uint4*>(src);
-#pragma unroll 4
-  for (int i = 0; i < 12; ++i) {
-    const int q = lane + 32 * i;
-    const uint4 v = __ldcg(s4 + q);
-    const uint32_t vals[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int w = 4 * q + e, lin = w / 3, f = w - 3 * lin;
-      const int si = swz_lin(lin);
-      (f == 0 ? b.w0 : (f == 1 ? b.w1 : b.w2))[si] = vals[e];
-    }
-  }
-}
-__device__ inline void store_block_warp(const BlockSmem& b, uint32_t* __restrict__ dst, int lane) {
-  uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll 4
-  for (int i = 0; i < 12; ++i) {
-    const int q = lane + 32 * i;
-    uint32_t vals[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int w = 4 * q + e, lin = w / 3, f = w - 3 * lin;
-      const int si = swz_lin(lin);
-      vals[e] = (f == 0 ? b.w0 : (f == 1 ? b.w1 : b.w2))[si];
-    }
-    __stcg(d4 + q, make_uint4(vals[0], vals[1], vals[2], vals[3]));
-  }
-}
-
-// reset_parented (esdf/integrator.cpp:352-363) of a staged block; returns
-// whether the block holds any site (the only givers left after the reset).
-__device__ inline bool reset_block_warp(BlockSmem& b, int lane, const Limits& lim) {
-  bool any_site = false;
-#pragma unroll 4
-  for (int i = 0; i < 16; ++i) {
-    const int si = swz_lin(lane + 32 * i);
-    const uint32_t w1 = b.w1[si], w2 = b.w2[si];
-    const uint32_t f = (w2 >> 16) & 0xffu;
-    const bool hp = (w1 | (w2 & 0xffffu)) != 0;
-    any_site |= (f & (VXM_ESDF_OBSERVED | VXM_ESDF_SITE)) == (VXM_ESDF_OBSERVED | VXM_ESDF_SITE);
-    if ((f & VXM_ESDF_OBSERVED) && !(f & VXM_ESDF_SITE) && hp) {
-      b.w0[si] = uint32_t((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq);
-      b.w1[si] = 0u;
-      b.w2[si] = w2 & 0xffff0000u;
-    }
-  }
-  return __any_sync(0xffffffffu, any_site);
-}
-
 // ---- cooperative lowering kernel ------------------------------------------------
 struct LowerArgs {
   uint32_t* pool[2];
@@ -518,13 +342,37 @@ struct LowerArgs {
   uint32_t lchg_tag;
   uint8_t* out_flags;
   unsigned long long* trace;  // optional phase timestamps (VXM_TRACE_LOWER)
-  uint32_t* work_ctr;         // [2] dynamic sweep scheduling counters
+  uint32_t* work_ctr;         // [4] dynamic scheduling counters (sweeps, pairs) by parity
   unsigned long long* line_mask;  // [cap][3] lines touched by the last border phase
+  uint32_t* stamp_swept;      // [cap] round epoch when the block's sweep was stored
+  uint32_t* stamp_pair[3];    // [cap] round epoch when pair (b, b + axis) was done
+  int dataflow;               // 1: pair items wait on dependencies; 0: phased barriers
 };
 
-constexpr int kLowerThreads = 256;
-constexpr int kLowerWarps = kLowerThreads / 32;
-constexpr size_t kLowerSmem = sizeof(BlockSmem) * kLowerWarps;
+__device__ inline uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ inline void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Bounded spin (~0.5 s): a missing producer is a bug, never a hang — the
+// watchdog flag turns it into VXM_ERR_INTERNAL on the host.
+__device__ inline void wait_stamp(const uint32_t* p, uint32_t ep, uint32_t* watchdog,
+                                  uint32_t code, int32_t blk) {
+  for (uint32_t it = 0; ld_acquire(p) != ep; ++it) {
+    if (it > (1u << 22)) {
+      if (atomicExch(watchdog, 1u) == 0u) {  // record the first expired wait
+        watchdog[1] = code;
+        watchdog[2] = uint32_t(blk);
+        watchdog[3] = ep * 1000u + (ld_acquire(p) % 1000u);  // expected, seen
+      }
+      return;
+    }
+    __nanosleep(64);
+  }
+}
 
 __device__ inline const EV load_voxel(const uint32_t* pool, int32_t slot, int lin) {
   const uint32_t* p = pool + size_t(slot) * 1536 + lin * 3;
@@ -535,185 +383,6 @@ __device__ inline void store_voxel(uint32_t* pool, int32_t slot, int lin, const 
   __stcg(p, uint32_t(v.sq));
   __stcg(p + 1, ev_w1(v));
   __stcg(p + 2, ev_w2(v));
-}
-
-__global__ void __launch_bounds__(kLowerThreads, 2) k_lower(LowerArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  uint32_t tr = 0;
-  auto stamp = [&]() {
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && tr < 255) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.trace[1 + tr++] = t;
-      a.trace[0] = tr;
-    }
-  };
-  stamp();
-  extern __shared__ BlockSmem s_blk[];  // one staging block per warp
-  const int lane = threadIdx.x & 31;
-  BlockSmem& blk = s_blk[threadIdx.x >> 5];
-  const int wid = (blockIdx.x * kLowerThreads + threadIdx.x) >> 5;
-  const int nwarps = gridDim.x * (kLowerThreads >> 5);
-  const uint32_t n_blocks = a.meta->num_blocks;
-  const uint32_t cur = a.meta->cur;
-  const uint32_t base_epoch = a.meta->round_epoch;
-  const bool failed = a.status->capacity_error || a.status->pool_overflow;
-  const bool lower = !failed && (a.full ? a.status->any_update != 0 : true);
-  uint32_t* const pcur = a.pool[cur];
-  uint32_t* const pnxt = a.pool[cur ^ 1u];
-  uint32_t* const work = a.full ? pnxt : pcur;
-  const Limits lim = a.lim;
-  // Seeded mode: round-1 dirty list = seeds (already filtered to existing).
-  if (!a.full && lower) {
-    const uint32_t ns = *a.n_seeds;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
-      const int32_t s = a.seeds[i];
-      a.list[1][i] = s;
-      a.stamp_dirty[1][s] = base_epoch + 1;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.count[1] = ns;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.work_ctr[0] = a.work_ctr[1] = 0u;
-  grid.sync();
-  stamp();
-  uint32_t r = 0;
-  uint32_t n_pairs = 0, n_cmp = 0;  // per-warp work counters
-  // while (!dirty.empty()) — an empty round-1 set runs zero rounds (:506)
-  const uint32_t n_first = a.full ? n_blocks : *((volatile uint32_t*)&a.count[1]);
-  if (lower && n_first > 0) {
-    while (true) {
-      ++r;
-      const int cp = int(r & 1u), np = cp ^ 1;
-      const uint32_t ep = base_epoch + r, ep_next = ep + 1;
-      const bool r1_full = a.full && r == 1;
-      const uint32_t n_dirty = r1_full ? n_blocks : *((volatile uint32_t*)&a.count[cp]);
-      const int32_t* dirty = a.list[cp];
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.count[np] = 0;
-        if (r > 1 || !a.full) a.status->sum_dirty += n_dirty;
-      }
-      // ---- sweep phase: every dirty block to its internal fixed point.
-      // A warp per block, blocks handed out dynamically (costs vary a lot).
-      uint32_t* const ctr = a.work_ctr + cp;
-      while (true) {
-        uint32_t i = 0;
-        if (lane == 0) i = atomicAdd(ctr, 1u);
-        i = __shfl_sync(0xffffffffu, i, 0);
-        if (i >= n_dirty) break;
-        const int32_t s = r1_full ? int32_t(i) : __ldcg(dirty + i);
-        load_block_warp(blk, (r1_full ? pcur : work) + size_t(s) * 1536, lane);
-        __syncwarp();
-        bool sweep = true;
-        if (r1_full) {
-          // After the reset only sites can give a distance: a block without
-          // sites is already at its fixed point (exact skip).
-          sweep = reset_block_warp(blk, lane, lim);
-          __syncwarp();
-        }
-        int passes = 0;
-        const bool changed = sweep && sweep_block_warp(blk, lane, lim, &passes);
-        if (a.trace && lane == 0 && r < 60) {  // debug: pass statistics per round
-          atomicMax(a.trace + 128 + r, (unsigned long long)passes);
-          atomicAdd(a.trace + 192 + r, (unsigned long long)passes);
-        }
-        if (r1_full || changed) store_block_warp(blk, work + size_t(s) * 1536, lane);
-        if (changed && !a.full && lane == 0) a.stamp_lchg[s] = a.lchg_tag;
-        __syncwarp();
-      }
-      grid.sync();
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.work_ctr[np] = 0u;  // next round's counter
-      stamp();
-      // ---- border phase, one axis group at a time (esdf/integrator.cpp:517-559)
-      for (int axis = 0; axis < 3; ++axis) {
-        const uint32_t items = 2u * n_dirty;
-        for (uint32_t w = wid; w < items; w += nwarps) {
-          const uint32_t i = w >> 1;
-          const int side = int(w & 1u);
-          const int32_t d = r1_full ? int32_t(i) : dirty[i];
-          int32_t lo, hi;
-          if (side == 0) {
-            hi = a.nbr[size_t(d) * 6 + 2 * axis];  // d + axis
-            lo = d;
-            if (hi < 0) continue;
-          } else {
-            lo = a.nbr[size_t(d) * 6 + 2 * axis + 1];  // d - axis
-            hi = d;
-            if (lo < 0) continue;
-            // the pair (lo, d) is emitted by lo's own side-0 item when lo is dirty
-            if (r1_full || __ldcg(a.stamp_dirty[cp] + lo) == ep) continue;
-          }
-          const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
-          bool ac = false, bc = false;
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
-            int la, lb;
-            if (axis == 0) { la = 7 + 8 * i0 + 64 * j0; lb = 0 + 8 * i0 + 64 * j0; }
-            else if (axis == 1) { la = i0 + 8 * 7 + 64 * j0; lb = i0 + 64 * j0; }
-            else { la = i0 + 8 * j0 + 64 * 7; lb = i0 + 8 * j0; }
-            EV va = load_voxel(work, lo, la), vb = load_voxel(work, hi, lb);
-            const bool cb = relax(vb, va, dx, dy, dz, lim);   // exchange_pair :158
-            const bool ca = relax(va, vb, -dx, -dy, -dz, lim);  // :159
-            if (cb) store_voxel(work, hi, lb, vb);
-            if (ca) store_voxel(work, lo, la, va);
-            ac |= ca;
-            bc |= cb;
-          }
-          ac = __any_sync(0xffffffffu, ac);
-          bc = __any_sync(0xffffffffu, bc);
-          ++n_pairs;
-          if (lane == 0) {
-            const int32_t who[2] = {lo, hi};
-            const bool chg[2] = {ac, bc};
-            for (int q = 0; q < 2; ++q) {
-              if (!chg[q]) continue;
-              if (!a.full) a.stamp_lchg[who[q]] = a.lchg_tag;
-              if (atomicMax(a.stamp_dirty[np] + who[q], ep_next) < ep_next) {
-                const uint32_t slot = atomicAdd(a.count + np, 1u);
-                a.list[np][slot] = who[q];
-              }
-            }
-          }
-        }
-        grid.sync();
-        stamp();
-      }
-      if (*((volatile uint32_t*)&a.count[np]) == 0) break;
-    }
-  }
-  // ---- changed set of update_esdf (esdf/integrator.cpp:403-411) -------------
-  if (a.full) {
-    const uint32_t n = n_blocks;
-    for (uint32_t k = wid; k < n; k += nwarps) {
-      const int32_t s = a.sorted_slots[k];
-      bool ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
-      if (!ch && lower) {
-        const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(s) * 1536);
-        const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(s) * 1536);
-        bool diff = false;
-#pragma unroll 4
-        for (int q = lane; q < 384; q += 32) {
-          const uint4 x = __ldcg(p0 + q), y = __ldcg(p1 + q);
-          diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
-        }
-        ch = __any_sync(0xffffffffu, diff);
-        ++n_cmp;
-      }
-      if (lane == 0) a.out_flags[k] = uint8_t(ch);
-    }
-  }
-  if (lane == 0 && (n_pairs | n_cmp)) {
-    atomicAdd(&a.status->sum_pairs, n_pairs);
-    atomicAdd(&a.status->cmp_blocks, n_cmp);
-  }
-  grid.sync();
-  stamp();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.status->rounds = r;
-    a.status->n_esdf_blocks = n_blocks;
-    a.meta->round_epoch = base_epoch + r + 2;
-    if (a.full && lower) a.meta->cur = cur ^ 1u;
-  }
 }
 
 // ---- lowering v3: group-per-block sweeps with line masks --------------------------
@@ -767,7 +436,13 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.count[1] = ns;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.work_ctr[0] = a.work_ctr[1] = 0u;
+  // Dirty-list counts are triple-buffered by round (read r%3, append (r+1)%3,
+  // reset (r+2)%3) because pair items of round r append while other CTAs may
+  // still be starting round r; lists are double-buffered by parity.
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.count[2] = 0u;
+    a.work_ctr[0] = a.work_ctr[1] = a.work_ctr[2] = a.work_ctr[3] = 0u;
+  }
   grid.sync();
   stamp();
   uint32_t r = 0;
@@ -779,10 +454,12 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
       const int cp = int(r & 1u), np = cp ^ 1;
       const uint32_t ep = base_epoch + r, ep_next = ep + 1;
       const bool r1_full = a.full && r == 1;
-      const uint32_t n_dirty = r1_full ? n_blocks : *((volatile uint32_t*)&a.count[cp]);
+      const uint32_t n_dirty = r1_full ? n_blocks : *((volatile uint32_t*)&a.count[r % 3u]);
       const int32_t* dirty = a.list[cp];
       if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.count[np] = 0;
+        a.count[(r + 2u) % 3u] = 0;  // read in round r - 1, appended in round r + 1
+        a.work_ctr[np] = 0u;      // counters of the previous round (finished at the
+        a.work_ctr[2 + np] = 0u;  // last grid barrier) serve the next round
         if (r > 1 || !a.full) a.status->sum_dirty += n_dirty;
       }
       // ---- sweep phase (esdf/integrator.cpp:509-513)
@@ -793,7 +470,10 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
         const uint32_t i = G.bcast;
         if (i >= n_dirty) break;
         const int32_t s = r1_full ? int32_t(i) : __ldcg(dirty + i);
+        unsigned long long tt0 = 0, tt1 = 0, tt2 = 0;
+        if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt0));
         load_block3(G, (r1_full ? pcur : work) + size_t(s) * 1536, t, bar);
+        if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt1));
         if (t == 0) {
           unsigned long long m0 = ~0ull, m1 = ~0ull, m2 = ~0ull;
           if (a.full && !r1_full) {  // lines through voxels changed by the last borders
@@ -810,32 +490,75 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
         if (r1_full) do_sweep = reset_block3(G, t, bar, lim);  // also orders the mask init
         else group_sync(bar);
         const bool changed = do_sweep && sweep_block3(G, t, bar, lim);
+        if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt2));
         if (r1_full || changed) store_block3(G, work + size_t(s) * 1536, t);
         if (changed && !a.full && t == 0) a.stamp_lchg[s] = a.lchg_tag;
+        __threadfence();  // the block's stores before its sweep stamp
         group_sync(bar);
+        if (t == 0) st_release(a.stamp_swept + s, ep);
+        if (a.trace && t == 0 && r < 16) {  // debug: per-block cost breakdown per round
+          unsigned long long tt3;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt3));
+          unsigned long long* d = a.trace + 128 + 8 * r;
+          atomicAdd(d + 0, 1ull);                      // blocks
+          atomicAdd(d + 1, tt1 - tt0);                 // load
+          atomicAdd(d + 2, tt2 - tt1);                 // sweep
+          atomicAdd(d + 3, tt3 - tt2);                 // store
+          atomicMax(d + 4, tt3 - tt0);                 // max block total
+          atomicMax(d + 5, tt2 - tt1);                 // max sweep
+        }
       }
-      grid.sync();
-      stamp();
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.work_ctr[np] = 0u;
-      // ---- border phase, one axis group at a time (esdf/integrator.cpp:517-559)
-      for (int axis = 0; axis < 3; ++axis) {
-        const uint32_t items = 2u * n_dirty;
-        for (uint32_t w = wid; w < items; w += nwarps) {
-          const uint32_t i = w >> 1;
-          const int side = int(w & 1u);
+      // ---- border phase (esdf/integrator.cpp:517-559) as a dataflow: pair items
+      // are taken in axis order (all x, then y, then z) after every sweep was
+      // taken, and each waits only for what the reference's phase order makes
+      // it depend on: the sweeps of its two blocks, and for y (z) the x (x, y)
+      // pairs touching its two blocks.  The graph is acyclic and every producer
+      // is already running when a consumer waits, so no grid barrier is needed
+      // until the round's end.
+      auto is_dirty = [&](int32_t b) {
+        return r1_full || __ldcg(a.stamp_dirty[cp] + b) == ep;
+      };
+      uint32_t* const pctr = a.work_ctr + 2 + cp;
+      const uint32_t per_axis = 2u * n_dirty;
+      // one pair item (warp-uniform); `wait` enables the dataflow dependencies
+      auto do_item = [&](uint32_t w, bool wait) {
+        {
+          const int axis = int(w / per_axis);
+          const uint32_t rest = w - uint32_t(axis) * per_axis;
+          const uint32_t i = rest >> 1;
+          const int side = int(rest & 1u);
           const int32_t d = r1_full ? int32_t(i) : __ldcg(dirty + i);
           int32_t lo, hi;
           if (side == 0) {
             hi = __ldg(a.nbr + size_t(d) * 6 + 2 * axis);  // d + axis
             lo = d;
-            if (hi < 0) continue;
+            if (hi < 0) return;
           } else {
             lo = __ldg(a.nbr + size_t(d) * 6 + 2 * axis + 1);  // d - axis
             hi = d;
-            if (lo < 0) continue;
+            if (lo < 0) return;
             // pair (lo, d) is handled by lo's side-0 item when lo is dirty
-            if (r1_full || __ldcg(a.stamp_dirty[cp] + lo) == ep) continue;
+            if (r1_full || __ldcg(a.stamp_dirty[cp] + lo) == ep) return;
           }
+          // dependencies, one lane each: sweeps of lo/hi (lanes 0-1); pairs of
+          // lower axes touching lo or hi (lanes 2-5: axis 0, 6-9: axis 1)
+          if (wait && lane < 2 + 4 * axis) {
+            if (lane < 2) {
+              const int32_t b = lane == 0 ? lo : hi;
+              if (is_dirty(b)) wait_stamp(a.stamp_swept + b, ep, &a.status->watchdog, 10u + axis, b);
+            } else {
+              const int q = (lane - 2) >> 2;               // the earlier axis
+              const int32_t b = ((lane - 2) & 2) ? hi : lo;
+              int32_t c = b;                               // pair (c, c + q)
+              if (((lane - 2) & 1) == 0) c = __ldg(a.nbr + size_t(b) * 6 + 2 * q + 1);  // b - q
+              if (c >= 0) {
+                const int32_t n = __ldg(a.nbr + size_t(c) * 6 + 2 * q);
+                if (n >= 0 && (is_dirty(c) || is_dirty(n)))
+                  wait_stamp(a.stamp_pair[q] + c, ep, &a.status->watchdog, 20u + 10u * q + axis, c);
+              }
+            }
+          }
+          __syncwarp();
           const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
           bool ac = false, bc = false;
           unsigned long long mlo[3] = {0, 0, 0}, mhi[3] = {0, 0, 0};
@@ -864,6 +587,9 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
           ac = __any_sync(0xffffffffu, ac);
           bc = __any_sync(0xffffffffu, bc);
           ++n_pairs;
+          __threadfence();  // the pair's voxel stores before its stamp
+          __syncwarp();
+          if (lane == 0) st_release(a.stamp_pair[axis] + lo, ep);
           const int32_t who[2] = {lo, hi};
           const bool chg[2] = {ac, bc};
 #pragma unroll
@@ -881,16 +607,33 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
             if (lane == 0) {
               if (!a.full) a.stamp_lchg[who[q]] = a.lchg_tag;
               if (atomicMax(a.stamp_dirty[np] + who[q], ep_next) < ep_next) {
-                const uint32_t slot = atomicAdd(a.count + np, 1u);
+                const uint32_t slot = atomicAdd(a.count + (r + 1u) % 3u, 1u);
                 a.list[np][slot] = who[q];
               }
             }
           }
         }
-        grid.sync();
-        stamp();
+      };
+      if (a.dataflow) {
+        while (true) {
+          uint32_t w = 0;
+          if (lane == 0) w = atomicAdd(pctr, 1u);
+          w = __shfl_sync(0xffffffffu, w, 0);
+          if (w >= 3u * per_axis) break;
+          do_item(w, true);
+        }
+      } else {  // phased: a grid barrier before each axis group, as the reference
+        for (int axis = 0; axis < 3; ++axis) {
+          grid.sync();
+          stamp();
+          for (uint32_t w = uint32_t(axis) * per_axis + wid; w < uint32_t(axis + 1) * per_axis;
+               w += nwarps)
+            do_item(w, false);
+        }
       }
-      if (*((volatile uint32_t*)&a.count[np]) == 0) break;
+      grid.sync();
+      stamp();
+      if (*((volatile uint32_t*)&a.count[(r + 1u) % 3u]) == 0) break;
     }
   }
   // ---- changed set of update_esdf (esdf/integrator.cpp:403-411) -------------
@@ -1455,10 +1198,15 @@ static void launch_lower(Context* ctx, LowerArgs& la) {
     std::fprintf(stderr, "[k_lower grid=%d] phases(us):", grid);
     for (unsigned long long i = 2; i <= h[0] && i < 128; ++i)
       std::fprintf(stderr, " %.1f", (h[i] - h[i - 1]) * 1e-3);
-    std::fprintf(stderr, " | total %.1f\n  passes max/total per round:",
-                 h[0] > 1 ? (h[h[0]] - h[1]) * 1e-3 : 0.0);
-    for (int r = 1; r < 60 && h[192 + r]; ++r) std::fprintf(stderr, " %llu/%llu", h[128 + r], h[192 + r]);
-    std::fprintf(stderr, "\n");
+    std::fprintf(stderr, " | total %.1f\n", h[0] > 1 ? (h[h[0]] - h[1]) * 1e-3 : 0.0);
+    for (int r = 1; r < 16 && h[128 + 8 * r]; ++r) {
+      const unsigned long long* d = h + 128 + 8 * r;
+      std::fprintf(stderr,
+                   "  r%d: %llu blocks, mean load %.2f sweep %.2f store %.2f us; max block %.1f, max "
+                   "sweep %.1f us\n",
+                   r, d[0], d[1] * 1e-3 / d[0], d[2] * 1e-3 / d[0], d[3] * 1e-3 / d[0], d[4] * 1e-3,
+                   d[5] * 1e-3);
+    }
   }
   ctx->count_launch();
 }
@@ -1475,8 +1223,15 @@ static LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.list[0] = E->dirty_list[0];
   la.list[1] = E->dirty_list[1];
   la.count = E->dirty_count;
-  la.work_ctr = E->dirty_count + 2;
+  la.work_ctr = E->dirty_count + 3;  // [0,1,2] list counts, [3..6] work counters
   la.line_mask = E->line_mask;
+  la.stamp_swept = E->stamp_swept;
+  static const int dataflow = [] {
+    const char* e = std::getenv("VXM_LOWER_DATAFLOW");
+    return e ? std::atoi(e) : 1;
+  }();
+  la.dataflow = dataflow;
+  for (int i = 0; i < 3; ++i) la.stamp_pair[i] = E->stamp_pair[i];
   la.lim = limits_for(cfg, E->vs);
   la.status = E->ctx->d_status;
   return la;
@@ -1518,6 +1273,11 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
   const DevStatus& st = *ctx->h_status;
   if (st.capacity_error || st.pool_overflow)
     throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+  if (st.watchdog)
+    throw Error(VXM_ERR_INTERNAL, "ESDF lowering: dependency wait expired (code " +
+                                      std::to_string(st.pad3[0]) + ", block " +
+                                      std::to_string(st.pad3[1]) + ", epoch " +
+                                      std::to_string(st.pad3[2]) + ")");
   vxm_stats& w = ctx->stats;
   w.esdf_calls += 1;
   w.esdf_blocks += st.n_esdf_blocks;

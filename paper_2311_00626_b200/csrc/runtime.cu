@@ -40,10 +40,10 @@ ScanTiles Context::next_scan(uint32_t tiles) {
     for (int i = 0; i < 2; ++i) {
       if (scan.status[i]) cudaFree(scan.status[i]);
       VXM_CUDA(cudaMalloc(&scan.status[i], sizeof(unsigned long long) * tiles * 2));
-      VXM_CUDA(cudaMemset(scan.status[i], 0, sizeof(unsigned long long) * tiles * 2));
+      VXM_CUDA(cudaMemsetAsync(scan.status[i], 0, sizeof(unsigned long long) * tiles * 2, stream));
     }
     if (!scan.tickets) VXM_CUDA(cudaMalloc(&scan.tickets, sizeof(uint32_t) * 2));
-    VXM_CUDA(cudaMemset(scan.tickets, 0, sizeof(uint32_t) * 2));
+    VXM_CUDA(cudaMemsetAsync(scan.tickets, 0, sizeof(uint32_t) * 2, stream));
     scan.cap = tiles * 2;
     scan.parity = 0;
   }
@@ -152,6 +152,8 @@ void Layer::ensure_capacity(uint64_t need) {
   nc = std::min<uint64_t>(nc, std::max<uint64_t>(max_blocks, need));
   nc = std::max<uint64_t>(nc, need);
   cudaStream_t st = ctx->stream;
+  if (num_blocks > capacity)
+    throw Error(VXM_ERR_INTERNAL, "Layer: device block count exceeds the pool capacity");
   const uint64_t live = num_blocks;
   const size_t bb = block_bytes();
   // block pools (byte-typed); ESDF pool[1 - cur] is scratch for the next
@@ -184,6 +186,8 @@ void Layer::ensure_capacity(uint64_t need) {
     grow_copy(&stamp_new, capacity, live, nc, 0, st);
     grow_copy(&stamp_lchg, capacity, live, nc, 0, st);
     grow_copy(&line_mask, capacity * 3ull, live * 3ull, nc * 3ull, 0, st);
+    grow_copy(&stamp_swept, capacity, live, nc, 0, st);
+    for (int a = 0; a < 3; ++a) grow_copy(&stamp_pair[a], capacity, live, nc, 0, st);
   }
   // hash: power of two >= 2 * capacity, rebuilt from slot_keys
   uint64_t hc = 1024;
@@ -226,6 +230,9 @@ Layer::~Layer() {
   if (stamp_lchg) cudaFree(stamp_lchg);
   if (dirty_count) cudaFree(dirty_count);
   if (line_mask) cudaFree(line_mask);
+  if (stamp_swept) cudaFree(stamp_swept);
+  for (uint32_t* p : stamp_pair)
+    if (p) cudaFree(p);
 }
 
 // ---- BlockList -----------------------------------------------------------------

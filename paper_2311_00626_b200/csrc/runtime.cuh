@@ -109,6 +109,8 @@ struct Layer {
   int32_t* dirty_list[2] = {nullptr, nullptr};
   uint32_t* dirty_count = nullptr;  // [2] dirty counts + [2] sweep work counters
   unsigned long long* line_mask = nullptr;  // [cap][3] lines changed by border phases
+  uint32_t* stamp_swept = nullptr;          // round epoch of the block's last sweep
+  uint32_t* stamp_pair[3] = {nullptr, nullptr, nullptr};  // round epoch of pair (b, b+axis)
 
   size_t voxel_bytes() const { return type == VXM_LAYER_TSDF ? 8 : 12; }
   size_t block_bytes() const { return voxel_bytes() * kVPB; }
