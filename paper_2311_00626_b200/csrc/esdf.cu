@@ -134,10 +134,33 @@ __device__ inline void group_sync(int id) {
 constexpr unsigned long long kKeyZero = 0x800080008000ull;  // offset (0, 0, 0)
 
 struct GroupSmem {
-  uint32_t w0[512], klo[512], khi[512];
+  // general format: a[0] = w0, a[1] = klo, a[2] = khi (above);
+  // compact format: a[0..4] = TH, TL, KEY, GQ, FL (below)
+  uint32_t a[5][512];
   unsigned long long mask[3][2];  // dirty lines per phase (X, Y, Z) by pass parity
   uint32_t bcast;
+  uint32_t fast;  // 1: the staged block is in the compact format
 };
+
+// Compact format, used for a block when max_sq <= kFastOff^2 and every voxel
+// has parent components within +-kFastOff, 0 <= sq < 2^29, and (if it can
+// give: observed and a site or parented) sq == |parent|^2 — always the case
+// for fields produced by update_esdf; other blocks keep the general format.
+//   KEY = 10-bit biased parent fields x << 20 | y << 10 | z
+//   GQ  = sq - 1 for a giver (so (other two components)^2 - 1 = GQ - pa^2 for
+//         a line along any axis), 2^30 + sq for a non-giver (its candidate
+//         then exceeds every limit)
+//   TH, TL = the taker threshold: a candidate (cand - 1, key) is accepted iff
+//         it compares below (TH, TL) as a 64-bit pair.  That single compare is
+//         relax's cand != 0, cand <= limit, cand < sq, and the tie rule (an
+//         unparented taker carries bit 30 in TL, so any parented candidate
+//         wins the tie); non-takers have (0, 0)
+//   FL  = flags << 16 | reserved << 24
+// so a relax on the line's dependency chain is IMAD -> 64-bit compare -> SEL.
+constexpr int kFastOff = 510;
+constexpr uint32_t kFastBias = 512u;
+constexpr uint32_t kUnpar = 1u << 30;
+constexpr uint32_t kNoGive = 1u << 30;
 
 template <int AXIS>
 __device__ inline int line_idx3(int q, int k) {  // q in [0, 64): the orthogonal coords
@@ -166,8 +189,8 @@ __device__ inline uint32_t sweep_line3(GroupSmem& g, int q, const Limits& lim) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     idx[k] = line_idx3<AXIS>(q, k);
-    const uint32_t lo = g.klo[idx[k]], hi = g.khi[idx[k]];
-    sq[k] = int(g.w0[idx[k]]);
+    const uint32_t lo = g.a[1][idx[k]], hi = g.a[2][idx[k]];
+    sq[k] = int(g.a[0][idx[k]]);
     key[k] = ((unsigned long long)(hi & 0xffffu) << 32) | lo;
     const int px = int(hi & 0xffffu) - 0x8000, py = int(lo >> 16) - 0x8000,
               pz = int(lo & 0xffffu) - 0x8000;
@@ -204,9 +227,9 @@ __device__ inline uint32_t sweep_line3(GroupSmem& g, int q, const Limits& lim) {
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     if (ch & (1u << k)) {
-      g.w0[idx[k]] = uint32_t(sq[k]);
-      g.klo[idx[k]] = uint32_t(key[k]);
-      g.khi[idx[k]] = (g.khi[idx[k]] & 0xffff0000u) | uint32_t(key[k] >> 32);
+      g.a[0][idx[k]] = uint32_t(sq[k]);
+      g.a[1][idx[k]] = uint32_t(key[k]);
+      g.a[2][idx[k]] = (g.a[2][idx[k]] & 0xffff0000u) | uint32_t(key[k] >> 32);
     }
   return ch;
 }
@@ -214,21 +237,108 @@ __device__ inline uint32_t sweep_line3(GroupSmem& g, int q, const Limits& lim) {
 // Runs one phase of a pass for the group: only lines marked dirty are swept
 // (an unchanged line is idempotent under its X+/X- sweep), changes mark the
 // lines through the changed voxels for the phases that follow.
+
+// sweep_line3 on the compact format — same relax semantics
+// (esdf/integrator.cpp:58-88).  Per voxel in registers: the threshold (th, tl),
+// qm = GQ - pa^2, and the giver's outgoing offset along the line and key,
+// pre-shifted by the step (po, ko), so the chain per relax is one IMAD, one
+// 64-bit compare and the selects.
+template <int AXIS>
+__device__ inline uint32_t sweep_line_fast(GroupSmem& g, int q) {
+  constexpr int sh = AXIS == 0 ? 20 : (AXIS == 1 ? 10 : 0);
+  constexpr uint32_t sb = 1u << sh;
+  uint32_t th[8], tl[8], qm[8], ko[8];
+  int po[8], idx[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    idx[k] = line_idx3<AXIS>(q, k);
+    th[k] = g.a[0][idx[k]];
+    tl[k] = g.a[1][idx[k]];
+    const uint32_t key = g.a[2][idx[k]];
+    const int pa = int((key >> sh) & 1023u) - int(kFastBias);
+    qm[k] = g.a[3][idx[k]] - uint32_t(pa * pa);
+    po[k] = pa - 1;  // outgoing along +axis
+    ko[k] = key - sb;
+  }
+  uint32_t ch = 0;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {  // X+ (resp. Y+, Z+)
+    const int j = k - 1;
+    const uint32_t cm = uint32_t(po[j] * po[j]) + qm[j];  // cand - 1 (mod 2^32)
+    const unsigned long long cv = (unsigned long long)cm << 32 | ko[j];
+    const unsigned long long tv = (unsigned long long)th[k] << 32 | tl[k];
+    if (cv < tv) {
+      th[k] = cm;
+      tl[k] = ko[j];
+      qm[k] = qm[j];
+      po[k] = po[j] - 1;
+      ko[k] = ko[j] - sb;
+      ch |= 1u << k;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // outgoing along -axis
+    po[k] += 2;
+    ko[k] += 2u * sb;
+  }
+#pragma unroll
+  for (int k = 6; k >= 0; --k) {  // X- (resp. Y-, Z-)
+    const int j = k + 1;
+    const uint32_t cm = uint32_t(po[j] * po[j]) + qm[j];
+    const unsigned long long cv = (unsigned long long)cm << 32 | ko[j];
+    const unsigned long long tv = (unsigned long long)th[k] << 32 | tl[k];
+    if (cv < tv) {
+      th[k] = cm;
+      tl[k] = ko[j];
+      qm[k] = qm[j];
+      po[k] = po[j] + 1;
+      ko[k] = ko[j] + sb;
+      ch |= 1u << k;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (ch & (1u << k)) {  // now a giver: sq = cand, parent = key
+      g.a[0][idx[k]] = th[k];
+      g.a[1][idx[k]] = tl[k];
+      g.a[2][idx[k]] = tl[k];
+      g.a[3][idx[k]] = th[k];
+    }
+  return ch;
+}
+
 template <int AXIS>
 __device__ inline uint32_t sweep_phase3(GroupSmem& g, int t, int bar, int p, const Limits& lim) {
   uint32_t ch = 0;
-  if ((g.mask[AXIS][p] >> t) & 1ull) ch = sweep_line3<AXIS>(g, t, lim);
-  if (ch) {
+  if ((g.mask[AXIS][p] >> t) & 1ull) ch = g.fast ? sweep_line_fast<AXIS>(g, t) : sweep_line3<AXIS>(g, t, lim);
+  // Line bits for the phases that follow, OR-reduced over the warp first and
+  // then merged with 32-bit shared atomics (a 64-bit shared atomicOr is a CAS
+  // loop, which serialises under this contention).
+  if (__any_sync(0xffffffffu, ch != 0)) {
     const int c0 = t & 7, c1 = t >> 3;
+    unsigned long long ma, mb;
+    unsigned long long *da, *db;
     if (AXIS == 0) {  // line (y=c0, z=c1): Y-line k + 8z, Z-line k + 8y (this pass)
-      atomicOr(&g.mask[1][p], (unsigned long long)ch << (8 * c1));
-      atomicOr(&g.mask[2][p], (unsigned long long)ch << (8 * c0));
+      ma = (unsigned long long)ch << (8 * c1), da = &g.mask[1][p];
+      mb = (unsigned long long)ch << (8 * c0), db = &g.mask[2][p];
     } else if (AXIS == 1) {  // line (x=c0, z=c1): X-line k + 8z (next), Z-line x + 8k (this)
-      atomicOr(&g.mask[0][p ^ 1], (unsigned long long)ch << (8 * c1));
-      atomicOr(&g.mask[2][p], spread8(ch) << c0);
+      ma = (unsigned long long)ch << (8 * c1), da = &g.mask[0][p ^ 1];
+      mb = spread8(ch) << c0, db = &g.mask[2][p];
     } else {  // line (x=c0, y=c1): X-line y + 8k, Y-line x + 8k (next pass)
-      atomicOr(&g.mask[0][p ^ 1], spread8(ch) << c1);
-      atomicOr(&g.mask[1][p ^ 1], spread8(ch) << c0);
+      ma = spread8(ch) << c1, da = &g.mask[0][p ^ 1];
+      mb = spread8(ch) << c0, db = &g.mask[1][p ^ 1];
+    }
+    const uint32_t a0 = __reduce_or_sync(0xffffffffu, uint32_t(ma));
+    const uint32_t a1 = __reduce_or_sync(0xffffffffu, uint32_t(ma >> 32));
+    const uint32_t b0 = __reduce_or_sync(0xffffffffu, uint32_t(mb));
+    const uint32_t b1 = __reduce_or_sync(0xffffffffu, uint32_t(mb >> 32));
+    if ((t & 31) == 0) {
+      uint32_t* pa = reinterpret_cast<uint32_t*>(da);
+      uint32_t* pb = reinterpret_cast<uint32_t*>(db);
+      if (a0) atomicOr(pa, a0);
+      if (a1) atomicOr(pa + 1, a1);
+      if (b0) atomicOr(pb, b0);
+      if (b1) atomicOr(pb + 1, b1);
     }
   }
   return ch;
@@ -236,9 +346,11 @@ __device__ inline uint32_t sweep_phase3(GroupSmem& g, int t, int bar, int p, con
 
 // sweep_block (esdf/integrator.cpp:96-139) for one group; masks[.][0] hold the
 // initially dirty lines.  Returns whether any voxel changed.
-__device__ inline bool sweep_block3(GroupSmem& g, int t, int bar, const Limits& lim) {
+__device__ inline bool sweep_block3(GroupSmem& g, int t, int bar, const Limits& lim,
+                                    int* n_passes = nullptr) {
   bool block_changed = false;
   for (int pass = 0;; ++pass) {
+    if (n_passes) *n_passes = pass + 1;
     const int p = pass & 1;
     uint32_t c = sweep_phase3<0>(g, t, bar, p, lim);
     group_sync(bar);
@@ -255,69 +367,124 @@ __device__ inline bool sweep_block3(GroupSmem& g, int t, int bar, const Limits& 
   return block_changed;
 }
 
-// Global block (reference layout) -> working format in shared memory.
-__device__ inline void load_block3(GroupSmem& g, const uint32_t* __restrict__ src, int t, int bar) {
+// A block in registers, reference layout: thread t of the group holds voxels
+// lin = 4 * (t + 64 * h) + e (h = 0, 1; e = 0..3) as 3 x 16-byte words each —
+// 48 contiguous bytes per thread and h, so the loads and stores coalesce.
+struct RawBlock {
+  uint32_t w[24];  // voxel (h, e), word f at w[12 * h + 3 * e + f]
+};
+__device__ inline void raw_load(RawBlock& r, const uint32_t* __restrict__ src, int t) {
   const uint4* s4 = reinterpret_cast<const uint4*>(src);
-#pragma unroll 3
-  for (int i = 0; i < 6; ++i) {
-    const int q = t + 64 * i;
-    const uint4 v = __ldcg(s4 + q);
-    const uint32_t vals[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int w = 4 * q + e, lin = w / 3, f = w - 3 * lin;
-      const int si = swz_lin(lin);
-      (f == 0 ? g.w0 : (f == 1 ? g.klo : g.khi))[si] = vals[e];  // raw w1 / w2 for now
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const uint4 v = __ldcg(s4 + 3 * (t + 64 * h) + j);
+      r.w[12 * h + 4 * j] = v.x;
+      r.w[12 * h + 4 * j + 1] = v.y;
+      r.w[12 * h + 4 * j + 2] = v.z;
+      r.w[12 * h + 4 * j + 3] = v.w;
     }
-  }
-  group_sync(bar);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int si = swz_lin(t + 64 * i);
-    const uint32_t w1 = g.klo[si], w2 = g.khi[si];
-    g.klo[si] = (((w1 >> 16) ^ 0x8000u) << 16) | ((w2 & 0xffffu) ^ 0x8000u);
-    g.khi[si] = ((w1 & 0xffffu) ^ 0x8000u) | (w2 & 0xffff0000u);
-  }
-  group_sync(bar);
 }
-
-__device__ inline void store_block3(const GroupSmem& g, uint32_t* __restrict__ dst, int t) {
+__device__ inline void raw_store(const RawBlock& r, uint32_t* __restrict__ dst, int t) {
   uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll 3
-  for (int i = 0; i < 6; ++i) {
-    const int q = t + 64 * i;
-    uint32_t vals[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int w = 4 * q + e, lin = w / 3, f = w - 3 * lin;
-      const int si = swz_lin(lin);
-      const uint32_t lo = g.klo[si], hi = g.khi[si];
-      vals[e] = f == 0 ? g.w0[si]
-                       : (f == 1 ? (((hi & 0xffffu) ^ 0x8000u) | (((lo >> 16) ^ 0x8000u) << 16))
-                                 : (((lo & 0xffffu) ^ 0x8000u) | (hi & 0xffff0000u)));
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      __stcg(d4 + 3 * (t + 64 * h) + j, make_uint4(r.w[12 * h + 4 * j], r.w[12 * h + 4 * j + 1],
+                                                   r.w[12 * h + 4 * j + 2], r.w[12 * h + 4 * j + 3]));
+}
+__device__ inline int raw_lin(int t, int v) { return 4 * (t + 64 * (v >> 2)) + (v & 3); }
+
+// Loads a block (reference layout) into registers; with `reset`, applies
+// reset_parented (esdf/integrator.cpp:352-363) on the way in.  Returns, for
+// the whole group, whether the block holds a site (after the reset, sites are
+// the only givers) and whether it qualifies for the compact format.
+__device__ inline void load_raw3(RawBlock& r, const uint32_t* __restrict__ src, int t, int bar,
+                                 const Limits& lim, bool reset, bool* any_site_out, bool* fast_out) {
+  raw_load(r, src, t);
+  bool out = lim.max_sq > kFastOff * kFastOff, any_site = false;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    uint32_t& w0 = r.w[3 * v];
+    uint32_t& w1 = r.w[3 * v + 1];
+    uint32_t& w2 = r.w[3 * v + 2];
+    const uint32_t f = (w2 >> 16) & 0xffu;
+    const bool obs = f & VXM_ESDF_OBSERVED, site = f & VXM_ESDF_SITE;
+    if (reset && obs && !site && ((w1 | (w2 & 0xffffu)) != 0u)) {
+      w0 = uint32_t((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq);
+      w1 = 0u;
+      w2 &= 0xffff0000u;
     }
-    __stcg(d4 + q, make_uint4(vals[0], vals[1], vals[2], vals[3]));
+    any_site |= obs && site;
+    const int px = int(int16_t(w1 & 0xffffu)), py = int(int16_t(w1 >> 16)), pz = int(int16_t(w2 & 0xffffu));
+    const bool give = obs && (site || (px | py | pz) != 0);
+    out |= w0 >= (1u << 29) || px < -kFastOff || px > kFastOff || py < -kFastOff || py > kFastOff ||
+           pz < -kFastOff || pz > kFastOff || (give && w0 != uint32_t(px * px + py * py + pz * pz));
   }
+  *fast_out = !group_sync_or(bar, out);
+  *any_site_out = reset ? group_sync_or(bar, any_site) : true;
 }
 
-// reset_parented (esdf/integrator.cpp:352-363) on the staged block; returns
-// whether it holds a site (after the reset, sites are the only givers).
-__device__ inline bool reset_block3(GroupSmem& g, int t, int bar, const Limits& lim) {
-  bool any_site = false;
+// Registers -> working format in shared memory (compact or general).
+__device__ inline void stage_block3(GroupSmem& g, const RawBlock& r, int t, int bar, const Limits& lim,
+                                    bool fast) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int si = swz_lin(t + 64 * i);
-    const uint32_t lo = g.klo[si], hi = g.khi[si];
-    const uint32_t f = (hi >> 16) & 0xffu;
-    const bool hp = (hi & 0xffffu) != 0x8000u || lo != 0x80008000u;
-    any_site |= (f & (VXM_ESDF_OBSERVED | VXM_ESDF_SITE)) == (VXM_ESDF_OBSERVED | VXM_ESDF_SITE);
-    if ((f & VXM_ESDF_OBSERVED) && !(f & VXM_ESDF_SITE) && hp) {
-      g.w0[si] = uint32_t((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq);
-      g.klo[si] = 0x80008000u;
-      g.khi[si] = (hi & 0xffff0000u) | 0x8000u;
+  for (int v = 0; v < 8; ++v) {
+    const int si = swz_lin(raw_lin(t, v));
+    const uint32_t w0 = r.w[3 * v], w1 = r.w[3 * v + 1], w2 = r.w[3 * v + 2];
+    if (fast) {
+      const int px = int(int16_t(w1 & 0xffffu)), py = int(int16_t(w1 >> 16)), pz = int(int16_t(w2 & 0xffffu));
+      const uint32_t f = (w2 >> 16) & 0xffu;
+      const bool obs = f & VXM_ESDF_OBSERVED, site = f & VXM_ESDF_SITE;
+      const bool par = (px | py | pz) != 0;
+      const uint32_t key = (uint32_t(px + int(kFastBias)) << 20) | (uint32_t(py + int(kFastBias)) << 10) |
+                           uint32_t(pz + int(kFastBias));
+      const uint32_t lim1 = uint32_t(((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq) + 1);
+      const uint32_t tq = w0 < lim1 ? w0 : lim1;
+      const bool open = obs && !site && tq > 0u;  // a taker with room to improve
+      g.a[0][si] = open ? tq - 1u : 0u;
+      g.a[1][si] = open ? (w0 < lim1 ? (key | (par ? 0u : kUnpar)) : 0u) : 0u;
+      g.a[2][si] = key;
+      g.a[3][si] = (obs && (site || par)) ? w0 - 1u : kNoGive + w0;
+      g.a[4][si] = w2 & 0xffff0000u;
+    } else {
+      g.a[0][si] = w0;
+      g.a[1][si] = (((w1 >> 16) ^ 0x8000u) << 16) | ((w2 & 0xffffu) ^ 0x8000u);
+      g.a[2][si] = ((w1 & 0xffffu) ^ 0x8000u) | (w2 & 0xffff0000u);
     }
   }
-  return group_sync_or(bar, any_site);
+  if (t == 0) g.fast = fast;
+  group_sync(bar);
+}
+
+// Working format in shared memory -> global block (reference layout).
+__device__ inline void store_block3(const GroupSmem& g, uint32_t* __restrict__ dst, int t) {
+  RawBlock r;
+  const bool fast = g.fast;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const int si = swz_lin(raw_lin(t, v));
+    uint32_t w0, w1, w2;
+    if (fast) {
+      const uint32_t key = g.a[2][si], gq = g.a[3][si];
+      w0 = (gq - kNoGive) < (1u << 29) ? gq - kNoGive : gq + 1u;
+      const uint32_t px = ((key >> 20) & 1023u) - kFastBias, py = ((key >> 10) & 1023u) - kFastBias,
+                     pz = (key & 1023u) - kFastBias;
+      w1 = (px & 0xffffu) | (py << 16);
+      w2 = (pz & 0xffffu) | g.a[4][si];
+    } else {
+      const uint32_t lo = g.a[1][si], hi = g.a[2][si];
+      w0 = g.a[0][si];
+      w1 = ((hi & 0xffffu) ^ 0x8000u) | (((lo >> 16) ^ 0x8000u) << 16);
+      w2 = ((lo & 0xffffu) ^ 0x8000u) | (hi & 0xffff0000u);
+    }
+    r.w[3 * v] = w0;
+    r.w[3 * v + 1] = w1;
+    r.w[3 * v + 2] = w2;
+  }
+  raw_store(r, dst, t);
 }
 
 // ---- cooperative lowering kernel ------------------------------------------------
@@ -354,6 +521,11 @@ __device__ inline uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ inline uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ inline void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -361,7 +533,9 @@ __device__ inline void st_release(uint32_t* p, uint32_t v) {
 // watchdog flag turns it into VXM_ERR_INTERNAL on the host.
 __device__ inline void wait_stamp(const uint32_t* p, uint32_t ep, uint32_t* watchdog,
                                   uint32_t code, int32_t blk) {
-  for (uint32_t it = 0; ld_acquire(p) != ep; ++it) {
+  // spin on relaxed loads (an acquire per iteration would invalidate L1 each
+  // time), then one acquire once the stamp is seen
+  for (uint32_t it = 0; ld_relaxed(p) != ep; ++it) {
     if (it > (1u << 22)) {
       if (atomicExch(watchdog, 1u) == 0u) {  // record the first expired wait
         watchdog[1] = code;
@@ -372,6 +546,7 @@ __device__ inline void wait_stamp(const uint32_t* p, uint32_t ep, uint32_t* watc
     }
     __nanosleep(64);
   }
+  (void)ld_acquire(p);
 }
 
 __device__ inline const EV load_voxel(const uint32_t* pool, int32_t slot, int lin) {
@@ -400,7 +575,7 @@ __device__ inline unsigned long long warp_or64(unsigned long long v) {
   return (unsigned long long)hi << 32 | lo;
 }
 
-__global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
+__global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
   cg::grid_group grid = cg::this_grid();
   uint32_t tr = 0;
   auto stamp = [&]() {
@@ -472,8 +647,6 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
         const int32_t s = r1_full ? int32_t(i) : __ldcg(dirty + i);
         unsigned long long tt0 = 0, tt1 = 0, tt2 = 0;
         if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt0));
-        load_block3(G, (r1_full ? pcur : work) + size_t(s) * 1536, t, bar);
-        if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt1));
         if (t == 0) {
           unsigned long long m0 = ~0ull, m1 = ~0ull, m2 = ~0ull;
           if (a.full && !r1_full) {  // lines through voxels changed by the last borders
@@ -486,15 +659,25 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
           G.mask[2][0] = m2;
           G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
         }
-        bool do_sweep = true;
-        if (r1_full) do_sweep = reset_block3(G, t, bar, lim);  // also orders the mask init
-        else group_sync(bar);
-        const bool changed = do_sweep && sweep_block3(G, t, bar, lim);
-        if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt2));
-        if (r1_full || changed) store_block3(G, work + size_t(s) * 1536, t);
+        // (the mask writes are ordered by the barriers below)
+        RawBlock rb;
+        bool any_site, fast;
+        load_raw3(rb, (r1_full ? pcur : work) + size_t(s) * 1536, t, bar, lim, r1_full, &any_site, &fast);
+        bool changed = false;
+        int passes = 0;
+        if (!any_site) {  // round 1, no site: the reset block is already at its fixed point
+          raw_store(rb, work + size_t(s) * 1536, t);
+          if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt1));
+          tt2 = tt1;
+        } else {
+          stage_block3(G, rb, t, bar, lim, fast);
+          if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt1));
+          changed = sweep_block3(G, t, bar, lim, &passes);
+          if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt2));
+          if (r1_full || changed) store_block3(G, work + size_t(s) * 1536, t);
+        }
         if (changed && !a.full && t == 0) a.stamp_lchg[s] = a.lchg_tag;
-        __threadfence();  // the block's stores before its sweep stamp
-        group_sync(bar);
+        group_sync(bar);  // the group's stores before the release of its sweep stamp
         if (t == 0) st_release(a.stamp_swept + s, ep);
         if (a.trace && t == 0 && r < 16) {  // debug: per-block cost breakdown per round
           unsigned long long tt3;
@@ -506,6 +689,8 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
           atomicAdd(d + 3, tt3 - tt2);                 // store
           atomicMax(d + 4, tt3 - tt0);                 // max block total
           atomicMax(d + 5, tt2 - tt1);                 // max sweep
+          atomicAdd(d + 6, (unsigned long long)passes);  // passes
+          atomicMax(d + 7, (unsigned long long)passes);  // max passes
         }
       }
       // ---- border phase (esdf/integrator.cpp:517-559) as a dataflow: pair items
@@ -587,8 +772,7 @@ __global__ void __launch_bounds__(kL3Threads, 3) k_lower3(LowerArgs a) {
           ac = __any_sync(0xffffffffu, ac);
           bc = __any_sync(0xffffffffu, bc);
           ++n_pairs;
-          __threadfence();  // the pair's voxel stores before its stamp
-          __syncwarp();
+          __syncwarp();  // the warp's voxel stores before the release of the pair stamp
           if (lane == 0) st_release(a.stamp_pair[axis] + lo, ep);
           const int32_t who[2] = {lo, hi};
           const bool chg[2] = {ac, bc};
@@ -1203,9 +1387,9 @@ static void launch_lower(Context* ctx, LowerArgs& la) {
       const unsigned long long* d = h + 128 + 8 * r;
       std::fprintf(stderr,
                    "  r%d: %llu blocks, mean load %.2f sweep %.2f store %.2f us; max block %.1f, max "
-                   "sweep %.1f us\n",
+                   "sweep %.1f us; passes mean %.2f max %llu\n",
                    r, d[0], d[1] * 1e-3 / d[0], d[2] * 1e-3 / d[0], d[3] * 1e-3 / d[0], d[4] * 1e-3,
-                   d[5] * 1e-3);
+                   d[5] * 1e-3, double(d[6]) / d[0], d[7]);
     }
   }
   ctx->count_launch();
