@@ -232,6 +232,25 @@ vxm_status vxm_integrate_depth_lidar_device(vxm_layer* layer, const float* depth
                                             const vxm_integrator_config* cfg,
                                             vxm_blocklist* changed_out);
 
+/* ---- fused frame update (replay pipeline step) ---------------------------- */
+/* One frame of the replay pipeline (pipeline.cpp:95-108: integrate the frame,
+ * then update the ESDF from its changed blocks) on a device-resident depth
+ * image, with ONE host round trip for both halves.  Same results as
+ * vxm_integrate_depth_*_device followed by vxm_update_esdf_list; both changed
+ * lists stay on the device.  `esdf` may be NULL (integration only; ecfg and
+ * esdf_changed are then ignored).  The ESDF half's argument errors (layer
+ * types, voxel-size mismatch) are reported before the TSDF is touched. */
+vxm_status vxm_update_frame_camera_device(vxm_layer* tsdf, vxm_layer* esdf, const float* depth_dev,
+                                          int width, int height, const vxm_pose* T_LS,
+                                          const vxm_camera* cam, const vxm_integrator_config* icfg,
+                                          const vxm_esdf_config* ecfg, vxm_blocklist* tsdf_changed,
+                                          vxm_blocklist* esdf_changed);
+vxm_status vxm_update_frame_lidar_device(vxm_layer* tsdf, vxm_layer* esdf, const float* depth_dev,
+                                         int width, int height, const vxm_pose* T_LS,
+                                         const vxm_lidar* lidar, const vxm_integrator_config* icfg,
+                                         const vxm_esdf_config* ecfg, vxm_blocklist* tsdf_changed,
+                                         vxm_blocklist* esdf_changed);
+
 /* ---- ESDF (esdf/integrator.hpp:81-120) ---------------------------------- */
 /* update_esdf(Layer<EsdfVoxel>&, const Layer<TsdfVoxel>&, updated, EsdfConfig)
  * — esdf/integrator.cpp:365-413, 567-572. */

@@ -127,34 +127,84 @@ void stage_depth(Context* ctx, const float* depth, int w, int h, bool on_device,
   *out = ctx->depth.as<float>();
 }
 
+// check_frame — integrator.cpp:26-34 (before any mutation) + view arguments.
+ViewArgs frame_args(vxm_layer* L, const float* depth, int w, int h, const vxm_pose* T,
+                    const vxm_camera* cam, const vxm_lidar* li, const vxm_integrator_config* cfg,
+                    bool on_device) {
+  REQUIRE_ARG(L->type == VXM_LAYER_TSDF, "integrate: layer is not a TSDF layer");
+  check_pose(T);
+  const int sw = cam ? cam->width : li->num_azimuth;
+  const int sh = cam ? cam->height : li->num_elevation;
+  if (w != sw || h != sh)
+    throw Error(VXM_ERR_INVALID_ARGUMENT, "integrate: image size does not match intrinsics");
+  REQUIRE_ARG(w == 0 || h == 0 || depth, "integrate: null depth image");
+  ViewArgs va{};
+  va.T_LS = *T;
+  va.lidar = li != nullptr;
+  if (cam) va.cam = *cam;
+  if (li) va.li = *li;
+  va.width = w;
+  va.height = h;
+  va.block_size = L->vs * kVPS;
+  va.cfg = {cfg->max_integration_distance, cfg->truncation, cfg->view_pixel_subsample};
+  stage_depth(L->ctx, depth, w, h, on_device, &va.depth_dev);
+  return va;
+}
+
 vxm_status integrate_common(vxm_layer* L, const float* depth, int w, int h, const vxm_pose* T,
                             const vxm_camera* cam, const vxm_lidar* li,
                             const vxm_integrator_config* cfg, vxm_blocklist* out, bool on_device) {
   return guard([&] {
     REQUIRE_ARG(L && T && cfg && out && (cam || li), "integrate: null argument");
-    REQUIRE_ARG(L->type == VXM_LAYER_TSDF, "integrate: layer is not a TSDF layer");
-    // check_frame — integrator.cpp:26-34 (before any mutation)
-    check_pose(T);
-    const int sw = cam ? cam->width : li->num_azimuth;
-    const int sh = cam ? cam->height : li->num_elevation;
-    if (w != sw || h != sh)
-      throw Error(VXM_ERR_INVALID_ARGUMENT, "integrate: image size does not match intrinsics");
-    REQUIRE_ARG(w == 0 || h == 0 || depth, "integrate: null depth image");
-    Context* ctx = L->ctx;
-    ViewArgs va{};
-    va.T_LS = *T;
-    va.lidar = li != nullptr;
-    if (cam) va.cam = *cam;
-    if (li) va.li = *li;
-    va.width = w;
-    va.height = h;
-    va.block_size = L->vs * kVPS;
-    va.cfg = {cfg->max_integration_distance, cfg->truncation, cfg->view_pixel_subsample};
-    stage_depth(ctx, depth, w, h, on_device, &va.depth_dev);
-    out->ctx = ctx;
+    const ViewArgs va = frame_args(L, depth, w, h, T, cam, li, cfg, on_device);
+    out->ctx = L->ctx;
     run_integrate(L, va, *cfg, out);
     out->sorted_unique = true;
     if (!on_device) out->fetch();
+  });
+}
+
+// One frame of the replay pipeline (pipeline.cpp:95-108): integrate_depth,
+// then update_esdf on its changed list, enqueued back to back with a single
+// host round trip for both (status, errors, metas).  A TSDF pool overflow
+// touches no voxel and leaves the ESDF update empty, so the frame is re-run
+// after the pool grows.
+vxm_status frame_common(vxm_layer* T, vxm_layer* E, const float* depth, int w, int h,
+                        const vxm_pose* pose, const vxm_camera* cam, const vxm_lidar* li,
+                        const vxm_integrator_config* icfg, const vxm_esdf_config* ecfg,
+                        vxm_blocklist* tout, vxm_blocklist* eout) {
+  return guard([&] {
+    REQUIRE_ARG(T && pose && icfg && tout && (cam || li), "update_frame: null argument");
+    if (E) {
+      REQUIRE_ARG(ecfg && eout, "update_frame: null ESDF argument");
+      REQUIRE_ARG(E->type == VXM_LAYER_ESDF, "update_esdf: expects (ESDF layer, TSDF layer)");
+      REQUIRE_ARG(E->ctx == T->ctx, "update_frame: layers on different contexts");
+      if (E->vs != T->vs)
+        throw Error(VXM_ERR_INVALID_ARGUMENT, "update_esdf: source and ESDF layer voxel sizes differ");
+    }
+    const ViewArgs va = frame_args(T, depth, w, h, pose, cam, li, icfg, true);
+    Context* ctx = T->ctx;
+    tout->ctx = ctx;
+    if (E) eout->ctx = ctx;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      ctx->reset_status();
+      const uint32_t nb_before = T->num_blocks;
+      integrate_launch(T, va, *icfg, tout);
+      tout->sorted_unique = true;
+      if (E) esdf_launch(E, T, tout, *ecfg, eout);
+      T->stage_meta(0);
+      if (E) E->stage_meta(1);
+      ctx->sync_status();
+      T->adopt_meta(0);
+      if (E) E->adopt_meta(1);
+      if (!integrate_finish(T, va, tout, nb_before)) continue;
+      if (E) {
+        esdf_finish(E, eout);
+        eout->sorted_unique = true;
+      }
+      return;
+    }
+    throw Error(VXM_ERR_INTERNAL, "update_frame: pool growth did not converge");
   });
 }
 
@@ -240,6 +290,12 @@ vxm_status vxm_context_create(int device, vxm_context** out) {
     ctx->device = device;
     ctx->sm_count = prop.multiProcessorCount;
     VXM_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    {  // layer pools grow stream-ordered from the device pool; keep what is freed
+      cudaMemPool_t mp;
+      VXM_CUDA(cudaDeviceGetDefaultMemPool(&mp, device));
+      uint64_t keep = ~uint64_t(0);
+      VXM_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     VXM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DevStatus)));
     VXM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DevStatus)));
     // The context stream is non-blocking: every initialisation is ordered on
@@ -452,6 +508,7 @@ vxm_status vxm_layer_write_blocks(vxm_layer* L, const vxm_grid_index* keys, uint
     DevBuf dslots;
     dslots.ensure(sizeof(int32_t) * m);
     ctx->reset_status();
+    L->subset_valid = false;  // blocks not produced by mark_sites
     alloc_key_list(L, &list, dslots.as<int32_t>());
     const uint32_t bb = uint32_t(L->block_bytes());
     std::vector<unsigned char> packed(size_t(bb) * m);
@@ -584,6 +641,21 @@ vxm_status vxm_integrate_depth_lidar_device(vxm_layer* L, const float* depth, in
                                             const vxm_pose* T, const vxm_lidar* li,
                                             const vxm_integrator_config* cfg, vxm_blocklist* out) {
   return integrate_common(L, depth, w, h, T, nullptr, li, cfg, out, true);
+}
+
+vxm_status vxm_update_frame_camera_device(vxm_layer* T, vxm_layer* E, const float* depth, int w,
+                                          int h, const vxm_pose* pose, const vxm_camera* cam,
+                                          const vxm_integrator_config* icfg,
+                                          const vxm_esdf_config* ecfg, vxm_blocklist* tout,
+                                          vxm_blocklist* eout) {
+  return frame_common(T, E, depth, w, h, pose, cam, nullptr, icfg, ecfg, tout, eout);
+}
+vxm_status vxm_update_frame_lidar_device(vxm_layer* T, vxm_layer* E, const float* depth, int w,
+                                         int h, const vxm_pose* pose, const vxm_lidar* li,
+                                         const vxm_integrator_config* icfg,
+                                         const vxm_esdf_config* ecfg, vxm_blocklist* tout,
+                                         vxm_blocklist* eout) {
+  return frame_common(T, E, depth, w, h, pose, nullptr, li, icfg, ecfg, tout, eout);
 }
 
 vxm_status vxm_update_esdf_list(vxm_layer* E, vxm_layer* T, vxm_blocklist* updated,

@@ -142,6 +142,8 @@ struct DevStatus {
   uint32_t meta_cur;         //   taken with the status read (one sync per call)
   uint32_t watchdog;         // a bounded dependency wait expired (internal error)
   uint32_t pad3[3];
+  uint32_t meta2_blocks;     // second layer's meta (fused frame update: TSDF + ESDF)
+  uint32_t meta2_cur;
 };
 
 // ---- decoupled look-back scan over (a, b) count pairs ------------------------

@@ -41,7 +41,7 @@ namespace vxm {
 
 void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
                          const uint32_t* n_ptr, uint32_t n_cap, uint64_t* out, uint32_t* n_out,
-                         const DevStatus* guard);
+                         const DevStatus* guard, const char* prof_name = "k_compact");
 
 // ---- voxel register form ---------------------------------------------------------
 struct EV {
@@ -1421,15 +1421,19 @@ static LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   return la;
 }
 
-void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
-                     BlockList* changed_out) {
+void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
+                 BlockList* changed_out) {
   Context* ctx = E->ctx;
   const uint32_t epoch = ++ctx->call_epoch;
-  ctx->reset_status();
   // E->num_blocks is exact: every call that allocates adopts the meta at its end.
   const uint32_t n7 = 7u * std::max<uint32_t>(updated->count_hint, 1);
-  // capacity for every effective block (bounded by the logical limit)
-  E->ensure_capacity(std::min<uint64_t>(uint64_t(E->num_blocks) + n7, E->max_blocks));
+  // capacity for every effective block: at most 7 per updated block, and at
+  // most one per TSDF block (effective blocks are allocated in the TSDF); when
+  // the ESDF block set is known to be a subset of T's, T's pool bounds it
+  if (E->subset_of == nullptr && E->num_blocks == 0) E->subset_of = T;
+  uint64_t need = uint64_t(E->num_blocks) + std::min<uint64_t>(n7, T->capacity);
+  if (E->subset_valid && E->subset_of == T) need = std::min<uint64_t>(need, T->capacity);
+  E->ensure_capacity(std::min<uint64_t>(need, E->max_blocks));
   const uint32_t n_all_cap = E->capacity;
   EsdfScratch s = esdf_scratch(ctx, updated->count_hint, n_all_cap);
   esdf_mark_phase(E, T, updated, cfg, s, epoch);
@@ -1444,16 +1448,18 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
   check_launch(ctx, "k_lower");
   changed_out->ensure(n_all_cap);
   launch_compact_keys(ctx, E->sorted_keys[E->sorted_parity], s.flags, &E->meta->num_blocks,
-                      n_all_cap, changed_out->keys.as<uint64_t>(), changed_out->d_count, nullptr);
+                      n_all_cap, changed_out->keys.as<uint64_t>(), changed_out->d_count, nullptr,
+                      "k_compact_esdf");
   changed_out->host_valid = false;
   changed_out->count_hint = n_all_cap;
   VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_effective, s.counts + 0, sizeof(uint32_t) * 2,
                            cudaMemcpyDeviceToDevice, ctx->stream));  // n_effective, n_esdf_new
   VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_out, changed_out->d_count, sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, ctx->stream));
-  E->stage_meta();
-  ctx->sync_status();
-  E->adopt_meta();
+}
+
+void esdf_finish(Layer* E, BlockList* changed_out) {
+  Context* ctx = E->ctx;
   const DevStatus& st = *ctx->h_status;
   if (st.capacity_error || st.pool_overflow)
     throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
@@ -1462,6 +1468,7 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
                                       std::to_string(st.pad3[0]) + ", block " +
                                       std::to_string(st.pad3[1]) + ", epoch " +
                                       std::to_string(st.pad3[2]) + ")");
+  changed_out->count_hint = std::min<uint32_t>(changed_out->count_hint, st.n_out);
   vxm_stats& w = ctx->stats;
   w.esdf_calls += 1;
   w.esdf_blocks += st.n_esdf_blocks;
@@ -1472,6 +1479,17 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
   w.pair_exchanges += st.sum_pairs;
   w.compared_blocks += st.cmp_blocks;
   w.reserved[0] += st.n_out;  // ESDF changed blocks
+}
+
+void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
+                     BlockList* changed_out) {
+  Context* ctx = E->ctx;
+  ctx->reset_status();
+  esdf_launch(E, T, updated, cfg, changed_out);
+  E->stage_meta();
+  ctx->sync_status();
+  E->adopt_meta();
+  esdf_finish(E, changed_out);
 }
 
 static void append_sorted_unique(std::vector<vxm_grid_index>& dst,

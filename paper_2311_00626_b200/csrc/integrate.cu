@@ -251,93 +251,106 @@ __global__ void __launch_bounds__(256) k_compact_keys(const uint64_t* __restrict
 
 void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
                          const uint32_t* n_ptr, uint32_t n_cap, uint64_t* out, uint32_t* n_out,
-                         const DevStatus* guard) {
+                         const DevStatus* guard, const char* prof_name) {
   const uint32_t tiles_cap = ceil_div(std::max<uint32_t>(n_cap, 1), 256 * kCompactItems);
   const ScanTiles st = ctx->next_scan(tiles_cap);
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_cap, ctx->sm_count * 4));
-  ctx->prof_begin("k_compact");
+  ctx->prof_begin(prof_name);
   k_compact_keys<<<grid, 256, 0, ctx->stream>>>(in, flags, n_ptr, out, n_out, st, guard);
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "k_compact_keys");
 }
 
+uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_config& cfg,
+                          BlockList* changed_out) {
+  Context* ctx = L->ctx;
+  // Headroom: a frame cannot allocate more blocks than it has candidates;
+  // the bound below is generous, the device check catches the rest.
+  L->ensure_capacity(std::min<uint64_t>(uint64_t(L->num_blocks) + 65536, L->max_blocks));
+  uint32_t cand_cap = 0;
+  run_view(ctx, va, L, &cand_cap);
+  ctx->cand_flags.ensure(cand_cap);
+  IntegrateArgs a{};
+  a.cand_keys = ctx->cand_keys.as<uint64_t>();
+  a.cand_slots = ctx->cand_slots.as<int32_t>();
+  a.status_ro = ctx->d_status;
+  a.pool = static_cast<float2*>(L->pool[0]);
+  a.changed = ctx->cand_flags.as<uint8_t>();
+  a.depth = va.depth_dev;
+  a.W = va.width;
+  a.H = va.height;
+  vxm_pose_inverse(&va.T_LS, &a.T_SL);  // integrator.cpp:89 (host, pinned order)
+  a.lidar = va.lidar ? 1 : 0;
+  a.fu = va.cam.fu; a.fv = va.cam.fv; a.cu = va.cam.cu; a.cv = va.cam.cv;
+  a.fu_f = float(va.cam.fu); a.fv_f = float(va.cam.fv);
+  a.cu_f = float(va.cam.cu); a.cv_f = float(va.cam.cv);
+  a.az0 = va.li.azimuth_start;
+  a.el0 = va.li.elevation_start;
+  a.u_scale = va.li.num_azimuth / va.li.azimuth_fov;
+  a.v_scale = va.li.num_elevation / va.li.elevation_fov;
+  a.na = va.li.num_azimuth;
+  a.ne = va.li.num_elevation;
+  a.vs = L->vs;
+  a.max_voxel_depth = cfg.max_integration_distance + cfg.truncation;
+  a.eps = float(cfg.truncation);
+  a.max_weight = cfg.max_weight;
+  a.max_gap = cfg.max_sample_gap;
+  a.inv_sq = cfg.weighting == VXM_WEIGHT_INVERSE_SQUARE;
+  a.linear = (va.lidar ? cfg.lidar_sample : cfg.camera_sample) == VXM_SAMPLE_LINEAR;
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * 8));
+  ctx->prof_begin("k_integrate");
+  k_integrate<<<grid, 256, 0, ctx->stream>>>(a);
+  ctx->prof_end();
+  ctx->count_launch();
+  check_launch(ctx, "k_integrate");
+  changed_out->ensure(cand_cap);
+  launch_compact_keys(ctx, ctx->cand_keys.as<uint64_t>(), ctx->cand_flags.as<uint8_t>(),
+                      &ctx->d_status->n_candidates, cand_cap, changed_out->keys.as<uint64_t>(),
+                      changed_out->d_count, ctx->d_status, "k_compact");
+  changed_out->host_valid = false;
+  // changed blocks are distinct allocated blocks: bounded by the pool too
+  changed_out->count_hint = std::min<uint32_t>(cand_cap, L->capacity);
+  VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_changed, changed_out->d_count, sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+  return cand_cap;
+}
+
+bool integrate_finish(Layer* L, const ViewArgs& va, BlockList* changed_out, uint32_t nb_before) {
+  Context* ctx = L->ctx;
+  const DevStatus& s = *ctx->h_status;
+  if (s.bitmap_overflow)
+    throw Error(VXM_ERR_INTERNAL, "candidate ray left the candidate cube (bitmap bound)");
+  if (s.pool_overflow) {
+    // No voxel was touched: grow to fit and run the frame again (blocks
+    // already inserted are zero and count as existing on the re-run).
+    L->ensure_capacity(std::min<uint64_t>(uint64_t(nb_before) + s.n_new + 1024, L->max_blocks));
+    return false;
+  }
+  if (s.capacity_error) throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+  changed_out->count_hint = s.n_candidates;
+  vxm_stats& w = ctx->stats;
+  w.integrate_calls += 1;
+  w.candidate_blocks += s.n_candidates;
+  w.new_blocks += s.n_new;
+  w.changed_blocks += s.n_changed;
+  w.voxels_read += s.vox_read;
+  w.voxels_updated += s.vox_upd;
+  w.depth_pixels += uint64_t(va.width) * uint64_t(va.height);
+  return true;
+}
+
 void run_integrate(Layer* L, const ViewArgs& va, const vxm_integrator_config& cfg,
                    BlockList* changed_out) {
   Context* ctx = L->ctx;
   for (int attempt = 0; attempt < 4; ++attempt) {
-    // Headroom: a frame cannot allocate more blocks than it has candidates;
-    // the bound below is generous, the device check catches the rest.
-    L->ensure_capacity(std::min<uint64_t>(uint64_t(L->num_blocks) + 65536, L->max_blocks));
     ctx->reset_status();
     const uint32_t nb_before = L->num_blocks;
-    uint32_t cand_cap = 0;
-    run_view(ctx, va, L, &cand_cap);
-    ctx->cand_flags.ensure(cand_cap);
-    IntegrateArgs a{};
-    a.cand_keys = ctx->cand_keys.as<uint64_t>();
-    a.cand_slots = ctx->cand_slots.as<int32_t>();
-    a.status_ro = ctx->d_status;
-    a.pool = static_cast<float2*>(L->pool[0]);
-    a.changed = ctx->cand_flags.as<uint8_t>();
-    a.depth = va.depth_dev;
-    a.W = va.width;
-    a.H = va.height;
-    vxm_pose_inverse(&va.T_LS, &a.T_SL);  // integrator.cpp:89 (host, pinned order)
-    a.lidar = va.lidar ? 1 : 0;
-    a.fu = va.cam.fu; a.fv = va.cam.fv; a.cu = va.cam.cu; a.cv = va.cam.cv;
-    a.fu_f = float(va.cam.fu); a.fv_f = float(va.cam.fv);
-    a.cu_f = float(va.cam.cu); a.cv_f = float(va.cam.cv);
-    a.az0 = va.li.azimuth_start;
-    a.el0 = va.li.elevation_start;
-    a.u_scale = va.li.num_azimuth / va.li.azimuth_fov;
-    a.v_scale = va.li.num_elevation / va.li.elevation_fov;
-    a.na = va.li.num_azimuth;
-    a.ne = va.li.num_elevation;
-    a.vs = L->vs;
-    a.max_voxel_depth = cfg.max_integration_distance + cfg.truncation;
-    a.eps = float(cfg.truncation);
-    a.max_weight = cfg.max_weight;
-    a.max_gap = cfg.max_sample_gap;
-    a.inv_sq = cfg.weighting == VXM_WEIGHT_INVERSE_SQUARE;
-    a.linear = (va.lidar ? cfg.lidar_sample : cfg.camera_sample) == VXM_SAMPLE_LINEAR;
-    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * 8));
-    ctx->prof_begin("k_integrate");
-    k_integrate<<<grid, 256, 0, ctx->stream>>>(a);
-    ctx->prof_end();
-    ctx->count_launch();
-    check_launch(ctx, "k_integrate");
-    changed_out->ensure(cand_cap);
-    launch_compact_keys(ctx, ctx->cand_keys.as<uint64_t>(), ctx->cand_flags.as<uint8_t>(),
-                        &ctx->d_status->n_candidates, cand_cap, changed_out->keys.as<uint64_t>(),
-                        changed_out->d_count, ctx->d_status);
-    changed_out->host_valid = false;
-    changed_out->count_hint = cand_cap;
-    VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_changed, changed_out->d_count, sizeof(uint32_t),
-                             cudaMemcpyDeviceToDevice, ctx->stream));
+    integrate_launch(L, va, cfg, changed_out);
     L->stage_meta();
     ctx->sync_status();
-    const DevStatus& s = *ctx->h_status;
     L->adopt_meta();
-    if (s.bitmap_overflow)
-      throw Error(VXM_ERR_INTERNAL, "candidate ray left the candidate cube (bitmap bound)");
-    if (s.pool_overflow) {
-      // No voxel was touched: grow to fit and run the frame again (blocks
-      // already inserted are zero and count as existing on the re-run).
-      L->ensure_capacity(std::min<uint64_t>(uint64_t(nb_before) + s.n_new + 1024, L->max_blocks));
-      continue;
-    }
-    if (s.capacity_error) throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
-    changed_out->count_hint = s.n_candidates;
-    vxm_stats& w = ctx->stats;
-    w.integrate_calls += 1;
-    w.candidate_blocks += s.n_candidates;
-    w.new_blocks += s.n_new;
-    w.changed_blocks += s.n_changed;
-    w.voxels_read += s.vox_read;
-    w.voxels_updated += s.vox_upd;
-    w.depth_pixels += uint64_t(va.width) * uint64_t(va.height);
-    return;
+    if (integrate_finish(L, va, changed_out, nb_before)) return;
   }
   throw Error(VXM_ERR_INTERNAL, "integrate: pool growth did not converge");
 }

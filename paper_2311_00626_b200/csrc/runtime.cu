@@ -113,14 +113,15 @@ __global__ void k_rehash(HashView h, const uint64_t* slot_keys, uint32_t n) {
 template <typename T>
 static void grow_copy(T** ptr, uint64_t old_elems, uint64_t live_elems, uint64_t new_elems,
                       int fill_byte, cudaStream_t st) {
+  // Stream-ordered: the context's pool keeps freed memory (release
+  // threshold = max), so growth costs the copy, not a cudaMalloc + device sync.
   T* np = nullptr;
-  VXM_CUDA(cudaMalloc(&np, sizeof(T) * std::max<uint64_t>(new_elems, 1)));
+  VXM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np), sizeof(T) * std::max<uint64_t>(new_elems, 1), st));
   if (*ptr && live_elems)
     VXM_CUDA(cudaMemcpyAsync(np, *ptr, sizeof(T) * live_elems, cudaMemcpyDeviceToDevice, st));
   if (fill_byte >= 0 && new_elems > live_elems)
     VXM_CUDA(cudaMemsetAsync(np + live_elems, fill_byte, sizeof(T) * (new_elems - live_elems), st));
-  VXM_CUDA(cudaStreamSynchronize(st));
-  if (*ptr) cudaFree(*ptr);
+  if (*ptr) VXM_CUDA(cudaFreeAsync(*ptr, st));
   *ptr = np;
   (void)old_elems;
 }
@@ -133,13 +134,14 @@ void Layer::refresh() {
   cur_host = m.cur;
 }
 
-void Layer::stage_meta() {
-  VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->meta_blocks, meta, 2 * sizeof(uint32_t),
+void Layer::stage_meta(int slot) {
+  VXM_CUDA(cudaMemcpyAsync(slot ? &ctx->d_status->meta2_blocks : &ctx->d_status->meta_blocks, meta,
+                           2 * sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, ctx->stream));
 }
-void Layer::adopt_meta() {
-  num_blocks = ctx->h_status->meta_blocks;
-  cur_host = ctx->h_status->meta_cur;
+void Layer::adopt_meta(int slot) {
+  num_blocks = slot ? ctx->h_status->meta2_blocks : ctx->h_status->meta_blocks;
+  cur_host = slot ? ctx->h_status->meta2_cur : ctx->h_status->meta_cur;
 }
 
 void Layer::ensure_capacity(uint64_t need) {
@@ -193,10 +195,10 @@ void Layer::ensure_capacity(uint64_t need) {
   uint64_t hc = 1024;
   while (hc < 2 * nc) hc <<= 1;
   if (hc != hash_cap) {
-    if (hash.keys) cudaFree(hash.keys);
-    if (hash.vals) cudaFree(hash.vals);
-    VXM_CUDA(cudaMalloc(&hash.keys, sizeof(uint64_t) * hc));
-    VXM_CUDA(cudaMalloc(&hash.vals, sizeof(int32_t) * hc));
+    if (hash.keys) VXM_CUDA(cudaFreeAsync(hash.keys, st));
+    if (hash.vals) VXM_CUDA(cudaFreeAsync(hash.vals, st));
+    VXM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&hash.keys), sizeof(uint64_t) * hc, st));
+    VXM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&hash.vals), sizeof(int32_t) * hc, st));
     VXM_CUDA(cudaMemsetAsync(hash.keys, 0xFF, sizeof(uint64_t) * hc, st));
     hash.mask = uint32_t(hc - 1);
     hash_cap = uint32_t(hc);
@@ -208,7 +210,6 @@ void Layer::ensure_capacity(uint64_t need) {
     }
   }
   capacity = uint32_t(nc);
-  VXM_CUDA(cudaStreamSynchronize(st));
 }
 
 Layer::~Layer() {

@@ -72,6 +72,9 @@ struct Context {
   const char* prof_name = nullptr;
   cudaEvent_t prof_a = nullptr;
   struct BlockList* scratch_in = nullptr;  // reused host-input list (C-ABI host paths)
+  // Deferred mode (fused frame update): drivers enqueue their work and leave
+  // the status read, error checks and meta adoption to the caller's one sync.
+  bool deferred = false;
 
   // Scan pass bookkeeping: returns the ScanTiles for the next pass with at
   // most `tiles` tiles, clearing the other buffer for the pass after.
@@ -112,6 +115,11 @@ struct Layer {
   uint32_t* stamp_swept = nullptr;          // round epoch of the block's last sweep
   uint32_t* stamp_pair[3] = {nullptr, nullptr, nullptr};  // round epoch of pair (b, b+axis)
 
+  // ESDF: while every block came from mark_sites against `subset_of`, the
+  // block set is a subset of that TSDF layer's (so bounded by its capacity)
+  const Layer* subset_of = nullptr;
+  bool subset_valid = true;
+
   size_t voxel_bytes() const { return type == VXM_LAYER_TSDF ? 8 : 12; }
   size_t block_bytes() const { return voxel_bytes() * kVPB; }
   void* cur_pool() const { return pool[type == VXM_LAYER_ESDF ? cur_host : 0]; }
@@ -121,8 +129,8 @@ struct Layer {
   void refresh();  // sync + read meta (num_blocks, cur)
   // Enqueue a copy of the meta into the context status (read by sync_status)
   // and, after the sync, adopt it: one host round trip per API call.
-  void stage_meta();
-  void adopt_meta();
+  void stage_meta(int slot = 0);
+  void adopt_meta(int slot = 0);
   ~Layer();
 };
 
@@ -165,10 +173,18 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* alloc, uint32_t* cand_cap_
 // integrate.cu
 void run_integrate(Layer* L, const ViewArgs& a, const vxm_integrator_config& cfg,
                    BlockList* changed_out);
+// Split form for the fused frame update: launch (no sync) and, after the
+// caller's sync, finish (checks + stats; false = pool grown, re-run the frame).
+uint32_t integrate_launch(Layer* L, const ViewArgs& a, const vxm_integrator_config& cfg,
+                          BlockList* changed_out);
+bool integrate_finish(Layer* L, const ViewArgs& a, BlockList* changed_out, uint32_t nb_before);
 
 // esdf.cu
 void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
                      BlockList* changed_out);
+void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
+                 BlockList* changed_out);
+void esdf_finish(Layer* E, BlockList* changed_out);
 void run_mark_sites(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
                     EsdfState* st, std::vector<vxm_grid_index>* changed);
 void run_clear_invalid(Layer* E, const vxm_esdf_config& cfg, EsdfState* st,

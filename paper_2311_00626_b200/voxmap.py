@@ -381,6 +381,20 @@ def update_esdf_device(esdf: EsdfLayer, tsdf: TsdfLayer, updated: BlockList, cfg
     return out
 
 
+def update_frame_device(tsdf: TsdfLayer, esdf: EsdfLayer | None, depth_dev_ptr: int, width: int,
+                        height: int, T_LS, intrinsics, icfg, ecfg, tsdf_out: BlockList,
+                        esdf_out: BlockList | None) -> None:
+    """One replay-pipeline frame (pipeline.cpp:95-108): integrate_depth then
+    update_esdf on a device-resident depth image with one host round trip;
+    both changed lists stay on the device.  `esdf=None` integrates only."""
+    fn = (lib().vxm_update_frame_camera_device if isinstance(intrinsics, A.Camera)
+          else lib().vxm_update_frame_lidar_device)
+    check(fn(tsdf.h, esdf.h if esdf is not None else None, C.c_void_p(depth_dev_ptr),
+             C.c_int(width), C.c_int(height), C.byref(_pose_c(T_LS)), C.byref(intrinsics),
+             C.byref(icfg), C.byref(ecfg) if ecfg is not None else None, tsdf_out.h,
+             esdf_out.h if esdf_out is not None else None))
+
+
 class EsdfUpdateState:
     """EsdfUpdateState (esdf/integrator.hpp:67-74)."""
 
