@@ -930,11 +930,13 @@ __global__ void __launch_bounds__(256) k_select_effective(const uint64_t* __rest
     }
     uint32_t ea, eb, ta, tb;
     block_scan2(keep ? 1u : 0u, 0u, ea, eb, ta, tb, s_scan);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: look-back
       uint32_t pa, pb;
       scan_lookback(st, tile, ta, 0u, pa, pb);
-      s_pre = pa;
-      if (tile == tiles - 1) *n_eff = pa + ta;
+      if (threadIdx.x == 0) {
+        s_pre = pa;
+        if (tile == tiles - 1) *n_eff = pa + ta;
+      }
     }
     __syncthreads();
     if (keep) {
@@ -992,10 +994,12 @@ __global__ void __launch_bounds__(256) k_alloc_list(AllocListArgs a, ScanTiles s
     }
     uint32_t ea, eb, ta, tb;
     block_scan2(is_new ? 1u : 0u, 0u, ea, eb, ta, tb, s_scan);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: look-back
       uint32_t pa, pb;
       scan_lookback(st, tile, ta, 0u, pa, pb);
-      s_pre[0] = pa;
+      if (threadIdx.x == 0) {
+        s_pre[0] = pa;
+      }
     }
     __syncthreads();
     const uint32_t base = s_base;

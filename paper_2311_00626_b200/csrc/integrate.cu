@@ -234,11 +234,13 @@ __global__ void __launch_bounds__(256) k_compact_keys(const uint64_t* __restrict
       if (base + k < n && flags[base + k]) keep |= 1u << k;
     uint32_t ea, eb, ta, tb;
     block_scan2(__popc(keep), 0u, ea, eb, ta, tb, s_scan);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: look-back
       uint32_t pa, pb;
       scan_lookback(st, tile, ta, 0u, pa, pb);
-      s_pre = pa;
-      if (tile == tiles - 1) *n_out = pa + ta;
+      if (threadIdx.x == 0) {
+        s_pre = pa;
+        if (tile == tiles - 1) *n_out = pa + ta;
+      }
     }
     __syncthreads();
     uint32_t pos = s_pre + ea;

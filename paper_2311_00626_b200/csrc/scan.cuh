@@ -69,29 +69,39 @@ __device__ inline uint32_t scan_take_tile(const ScanTiles& st, uint32_t* s_tile)
   return t;
 }
 
-// Thread 0 only: publish this tile's aggregate, look back for the exclusive
-// prefix, publish the inclusive prefix.  Returns the exclusive prefix (a, b).
+// Warp 0 (all 32 lanes): publish this tile's aggregate, look back for the
+// exclusive prefix 32 predecessors at a time, publish the inclusive prefix.
+// Returns the exclusive prefix (a, b) in every lane.
 __device__ inline void scan_lookback(const ScanTiles& st, uint32_t tile, uint32_t agg_a,
                                      uint32_t agg_b, uint32_t& ex_a, uint32_t& ex_b) {
+  const int lane = threadIdx.x & 31;
   volatile unsigned long long* status = st.status;
   if (tile == 0) {
-    atomicExch(st.status, kFlagPre | pack_ab(agg_a, agg_b));
+    if (lane == 0) atomicExch(st.status, kFlagPre | pack_ab(agg_a, agg_b));
     ex_a = ex_b = 0;
     return;
   }
-  atomicExch(st.status + tile, kFlagAgg | pack_ab(agg_a, agg_b));
+  if (lane == 0) atomicExch(st.status + tile, kFlagAgg | pack_ab(agg_a, agg_b));
   uint32_t a = 0, b = 0;
-  int64_t j = int64_t(tile) - 1;
+  int64_t base = int64_t(tile) - 1;
   while (true) {
-    const unsigned long long v = status[j];
+    const int64_t j = base - lane;
+    // tile 0 always publishes an inclusive prefix, so j >= 0 for every lane
+    // that can matter; lanes beyond it read a zero prefix
+    const unsigned long long v = j >= 0 ? status[j] : (2ull << 62);  // kFlagPre
     const unsigned long long f = v & (3ull << 62);
-    if (f == 0) continue;
-    a += unpack_a(v);
-    b += unpack_b(v);
-    if (f == kFlagPre) break;
-    --j;
+    const uint32_t pre = __ballot_sync(0xffffffffu, f == kFlagPre);
+    const uint32_t zero = __ballot_sync(0xffffffffu, f == 0ull);
+    const int first = pre ? __ffs(pre) - 1 : 32;  // nearest inclusive prefix
+    const uint32_t need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
+    if (zero & need) continue;  // a predecessor has not published yet
+    const bool use = (need >> lane) & 1u;
+    a += __reduce_add_sync(0xffffffffu, use ? unpack_a(v) : 0u);
+    b += __reduce_add_sync(0xffffffffu, use ? unpack_b(v) : 0u);
+    if (first < 32) break;
+    base -= 32;
   }
-  atomicExch(st.status + tile, kFlagPre | pack_ab(a + agg_a, b + agg_b));
+  if (lane == 0) atomicExch(st.status + tile, kFlagPre | pack_ab(a + agg_a, b + agg_b));
   ex_a = a;
   ex_b = b;
 }

@@ -62,7 +62,7 @@ __device__ inline void mark_cell(const Cube& c, int32_t x, int32_t y, int32_t z,
     atomicOr(&status->bitmap_overflow, 1u);
     return;
   }
-  if (!(c.bits[w] & m)) atomicOr(c.bits + w, m);
+  atomicOr(c.bits + w, m);  // fire-and-forget (RED): no load on the DDA's critical path
 }
 
 // traverse_grid — traversal.hpp:29-73, visiting into the bitmap.
@@ -124,11 +124,23 @@ __global__ void k_rays_camera(const float* __restrict__ depth, int W, int H, int
   const int col0 = (t % tiles_x) * tile, row0 = (t / tiles_x) * tile;
   const int row1 = min(row0 + tile, H), col1 = min(col0 + tile, W);
   float tile_max = 0.0f;
-  for (int r = row0; r < row1; ++r)
-    for (int c = col0; c < col1; ++c) {
-      const float d = __ldg(depth + size_t(r) * W + c);
-      if (valid_depth(d)) tile_max = tile_max < d ? d : tile_max;
+  if (col1 - col0 == 8 && (W & 3) == 0) {  // 8-wide tile: two aligned float4 per row
+#pragma unroll 8
+    for (int r = row0; r < row1; ++r) {
+      const float4* p = reinterpret_cast<const float4*>(depth + size_t(r) * W + col0);
+      const float4 a = __ldg(p), b = __ldg(p + 1);
+      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (valid_depth(v[i])) tile_max = tile_max < v[i] ? v[i] : tile_max;
     }
+  } else {
+    for (int r = row0; r < row1; ++r)
+      for (int c = col0; c < col1; ++c) {
+        const float d = __ldg(depth + size_t(r) * W + c);
+        if (valid_depth(d)) tile_max = tile_max < d ? d : tile_max;
+      }
+  }
   if (tile_max <= 0.0f) return;
   const double u = 0.5 * double(col0 + col1), v = 0.5 * double(row0 + row1);
   const double reach = ray_reach(double(tile_max), max_int, trunc);
@@ -176,23 +188,52 @@ struct AllocArgs {
   uint64_t max_blocks;     // Layer::max_blocks
 };
 
-// Dilation + ordered emission + fused allocation.  One thread per word.
-__global__ void __launch_bounds__(256) k_dilate_alloc(Cube cube, uint32_t n_words, AllocArgs al,
-                                                      int rank, int world, int slab,
-                                                      uint64_t* __restrict__ cand_keys,
-                                                      int32_t* __restrict__ cand_slots,
-                                                      DevStatus* status, ScanTiles st) {
+// Dilation + ordered emission + fused allocation.  One thread per 32-cell word
+// computes the dilation; the tile's candidates are then processed one per
+// thread (so the hash look-ups of a tile are issued in parallel, not as a
+// serial chain per word): look-up, new-block ranking, one look-back for the
+// (candidates, new blocks) prefix, ordered output with slot assignment and
+// hash insertion of the new blocks.
+constexpr int kDilThreads = 256;
+constexpr int kDilMaxCand = kDilThreads * 32;
+
+struct DilTile {
+  uint32_t dil[kDilThreads];  // dilated word of each thread
+  uint32_t off[kDilThreads];  // exclusive prefix of the words' candidate counts
+};
+
+// Candidate `idx` of the tile: the word that holds it (largest o with
+// off[o] <= idx) and the cell's packed key.
+__device__ inline uint64_t tile_candidate(const DilTile& d, uint32_t idx, uint32_t tile,
+                                          const Cube& cube) {
+  int o = 0;
+#pragma unroll
+  for (int step = kDilThreads / 2; step >= 1; step >>= 1)
+    if (d.off[o + step] <= idx) o += step;
+  const int bit = int(__fns(d.dil[o], 0u, int(idx - d.off[o]) + 1));
+  const uint32_t wi = tile * kDilThreads + uint32_t(o);
+  const int32_t wz = int32_t(wi % uint32_t(cube.SZw));
+  const uint32_t t = wi / uint32_t(cube.SZw);
+  const int32_t dy = int32_t(t % uint32_t(cube.S)), dx = int32_t(t / uint32_t(cube.S));
+  return pack_key(cube.ox + dx, cube.oy + dy, cube.oz + wz * 32 + bit);
+}
+
+__global__ void __launch_bounds__(kDilThreads) k_dilate_alloc(Cube cube, uint32_t n_words, AllocArgs al,
+                                                              int rank, int world, int slab,
+                                                              uint64_t* __restrict__ cand_keys,
+                                                              int32_t* __restrict__ cand_slots,
+                                                              DevStatus* status, ScanTiles st) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_scan[64];
   __shared__ uint32_t s_pre[2];
-  __shared__ uint32_t s_base;
+  __shared__ uint32_t s_base, s_nnew;
+  __shared__ DilTile s_d;
+  __shared__ int32_t s_slot[kDilMaxCand];  // found slot, or -2 - (tile-local new rank)
   scan_prepare_next(st);
   const uint32_t tile = scan_take_tile(st, &s_tile);
   const uint32_t wi = tile * blockDim.x + threadIdx.x;
   const bool do_alloc = al.hash.keys != nullptr;
-  if (threadIdx.x == 0) s_base = do_alloc ? al.meta->num_blocks : 0u;
   uint32_t dil = 0;
-  int32_t bx = 0, by = 0, bz0 = 0;
   if (wi < n_words) {
     const int32_t S = cube.S, SZw = cube.SZw;
     const int32_t wz = int32_t(wi % uint32_t(SZw));
@@ -213,43 +254,51 @@ __global__ void __launch_bounds__(256) k_dilate_alloc(Cube cube, uint32_t n_word
     }
     const int32_t zbits = S - wz * 32;  // valid bits in this word
     if (zbits < 32) dil &= (zbits <= 0 ? 0u : ((1u << zbits) - 1u));
-    bx = cube.ox + dx;
-    by = cube.oy + dy;
-    bz0 = cube.oz + wz * 32;
-    if (!owned(bx, rank, world, slab)) dil = 0;
+    if (!owned(cube.ox + dx, rank, world, slab)) dil = 0;
   }
-  // count candidates and new blocks
-  uint32_t n_c = __popc(dil), n_new = 0;
-  uint32_t new_mask = 0;
-  if (do_alloc && dil) {
-    for (uint32_t m = dil; m; m &= m - 1) {
-      const int b = __ffs(m) - 1;
-      const uint64_t k = pack_key(bx, by, bz0 + b);
-      if (hash_find_rw(al.hash, k) < 0) {
-        new_mask |= 1u << b;
-        ++n_new;
-      }
+  uint32_t ea, eb, n_cand, tb;
+  block_scan2(__popc(dil), 0u, ea, eb, n_cand, tb, s_scan);
+  s_d.dil[threadIdx.x] = dil;
+  s_d.off[threadIdx.x] = ea;
+  if (threadIdx.x == 0) {
+    s_base = do_alloc ? al.meta->num_blocks : 0u;
+    s_nnew = 0u;
+  }
+  __syncthreads();
+  // look-ups, one candidate per thread; new blocks ranked in key order
+  if (do_alloc) {
+    for (uint32_t c0 = 0; c0 < n_cand; c0 += kDilThreads) {
+      const uint32_t idx = c0 + threadIdx.x;
+      int32_t found = 0;
+      if (idx < n_cand) found = hash_find_rw(al.hash, tile_candidate(s_d, idx, tile, cube));
+      const bool is_new = idx < n_cand && found < 0;
+      uint32_t rn, rb, tn, tb2;
+      block_scan2(is_new ? 1u : 0u, 0u, rn, rb, tn, tb2, s_scan);
+      if (idx < n_cand) s_slot[idx] = is_new ? -2 - int32_t(s_nnew + rn) : found;
+      __syncthreads();
+      if (threadIdx.x == 0) s_nnew += tn;
+      __syncthreads();
     }
   }
-  uint32_t ea, eb, ta, tb;
-  block_scan2(n_c, n_new, ea, eb, ta, tb, s_scan);
-  if (threadIdx.x == 0) {
+  const uint32_t n_new = s_nnew;
+  if (threadIdx.x < 32) {  // warp 0: look-back
     uint32_t pa, pb;
-    scan_lookback(st, tile, ta, tb, pa, pb);
-    s_pre[0] = pa;
-    s_pre[1] = pb;
+    scan_lookback(st, tile, n_cand, n_new, pa, pb);
+    if (threadIdx.x == 0) {
+      s_pre[0] = pa;
+      s_pre[1] = pb;
+    }
   }
   __syncthreads();
   const uint32_t base = s_base;
   const uint64_t limit = al.capacity < al.max_blocks ? uint64_t(al.capacity) : al.max_blocks;
-  uint32_t pos = s_pre[0] + ea, npos = s_pre[1] + eb;
-  for (uint32_t m = dil; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    const uint64_t k = pack_key(bx, by, bz0 + b);
+  for (uint32_t idx = threadIdx.x; idx < n_cand; idx += kDilThreads) {
+    const uint64_t k = tile_candidate(s_d, idx, tile, cube);
     int32_t slot = 0;
     if (do_alloc) {
-      if (new_mask & (1u << b)) {
-        const uint64_t s = uint64_t(base) + npos++;
+      slot = s_slot[idx];
+      if (slot <= -2) {
+        const uint64_t s = uint64_t(base) + s_pre[1] + uint32_t(-2 - slot);
         if (s < limit) {
           hash_insert(al.hash, k, int32_t(s));
           al.slot_keys[s] = k;
@@ -257,18 +306,15 @@ __global__ void __launch_bounds__(256) k_dilate_alloc(Cube cube, uint32_t n_word
         } else {
           slot = -1;
         }
-      } else {
-        slot = hash_find_rw(al.hash, k);
       }
     }
-    cand_keys[pos] = k;
-    cand_slots[pos] = slot;
-    ++pos;
+    cand_keys[s_pre[0] + idx] = k;
+    cand_slots[s_pre[0] + idx] = slot;
   }
   // The last tile publishes totals (all earlier tiles have read s_base: they
   // published before this tile's look-back could complete).
   if (threadIdx.x == 0 && tile == gridDim.x - 1) {
-    const uint32_t total_c = s_pre[0] + ta, total_n = s_pre[1] + tb;
+    const uint32_t total_c = s_pre[0] + n_cand, total_n = s_pre[1] + n_new;
     status->n_candidates = total_c;
     status->n_new = total_n;
     if (do_alloc) {
@@ -354,7 +400,8 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
     const int nt = ((a.width + tile - 1) / tile) * ((a.height + tile - 1) / tile);
     if (nt > 0) {
       ctx->prof_begin("k_rays");
-      k_rays_camera<<<ceil_div(nt, 128), 128, 0, ctx->stream>>>(
+      // 32 threads per CTA: the rays are serial DDAs, so spread them over all SMs
+      k_rays_camera<<<ceil_div(nt, 32), 32, 0, ctx->stream>>>(
           a.depth_dev, a.width, a.height, tile, a.cam, a.T_LS, cs,
           a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
       ctx->prof_end();
@@ -365,7 +412,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
     const int np = a.width * a.height;
     if (np > 0) {
       ctx->prof_begin("k_rays");
-      k_rays_lidar<<<ceil_div(np, 128), 128, 0, ctx->stream>>>(
+      k_rays_lidar<<<ceil_div(np, 64), 64, 0, ctx->stream>>>(
           a.depth_dev, a.width, a.height, ctx->lidar_dirs.as<double>(), a.T_LS, cs,
           a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
       ctx->prof_end();
