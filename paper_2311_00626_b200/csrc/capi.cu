@@ -70,6 +70,10 @@ __global__ void k_scatter_blocks(unsigned char* pool, const int32_t* slots, uint
           reinterpret_cast<const uint32_t*>(in)[i];
   }
 }
+__global__ void k_mark_site_any(uint8_t* site_any, const int32_t* slots, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (slots[i] >= 0) site_any[slots[i]] = 1;  // user data: may hold sites
+}
 __global__ void k_lookup(const uint64_t* keys, uint32_t n, HashView h, int32_t* out) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = h.keys ? hash_find(h, keys[i]) : -1;
@@ -406,9 +410,10 @@ vxm_status vxm_layer_create(vxm_context* ctx, vxm_layer_type type, double vs, ui
     // legacy stream, so a plain cudaMemset could land after the first read)
     VXM_CUDA(cudaMemsetAsync(L->meta, 0, sizeof(LayerMeta), ctx->stream));
     if (type == VXM_LAYER_ESDF) {
-      // [0..2] dirty-list counts, [3..6] sweep / pair work counters by parity
-      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * 8));
-      VXM_CUDA(cudaMemsetAsync(L->dirty_count, 0, sizeof(uint32_t) * 8, ctx->stream));
+      // [0..2] dirty-list counts, [3..6] sweep / pair work counters by parity,
+      // [7..10] round-1 split counters (zero between launches)
+      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * 16));
+      VXM_CUDA(cudaMemsetAsync(L->dirty_count, 0, sizeof(uint32_t) * 16, ctx->stream));
     }
     L->ensure_capacity(std::min<uint64_t>(4096, L->max_blocks));
     *out = L;
@@ -522,6 +527,11 @@ vxm_status vxm_layer_write_blocks(vxm_layer* L, const vxm_grid_index* keys, uint
         din.as<unsigned char>());
     ctx->count_launch();
     check_launch(ctx, "k_scatter_blocks");
+    if (L->site_any) {
+      k_mark_site_any<<<grid1d(ctx, m), 256, 0, ctx->stream>>>(L->site_any, dslots.as<int32_t>(), m);
+      ctx->count_launch();
+      check_launch(ctx, "k_mark_site_any");
+    }
     ctx->sync_status();
     L->refresh();
     if (ctx->h_status->capacity_error || ctx->h_status->pool_overflow)

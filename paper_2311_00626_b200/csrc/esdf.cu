@@ -514,6 +514,8 @@ struct LowerArgs {
   uint32_t* stamp_swept;      // [cap] round epoch when the block's sweep was stored
   uint32_t* stamp_pair[3];    // [cap] round epoch when pair (b, b + axis) was done
   int dataflow;               // 1: pair items wait on dependencies; 0: phased barriers
+  const uint8_t* site_any;    // [cap] 0: the block holds no site
+  uint32_t* r1;               // [4] round-1 split: #site, #no-site, group / warp work counters
 };
 
 __device__ inline uint32_t ld_acquire(const uint32_t* p) {
@@ -529,24 +531,29 @@ __device__ inline uint32_t ld_relaxed(const uint32_t* p) {
 __device__ inline void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Pair stamps carry, besides the round epoch, whether the pair changed its
+// lower / upper block (read by the dependent pairs of round 1).
+constexpr uint32_t kStampLoChg = 1u << 31, kStampHiChg = 1u << 30, kStampEp = kStampHiChg - 1u;
+
 // Bounded spin (~0.5 s): a missing producer is a bug, never a hang — the
-// watchdog flag turns it into VXM_ERR_INTERNAL on the host.
-__device__ inline void wait_stamp(const uint32_t* p, uint32_t ep, uint32_t* watchdog,
-                                  uint32_t code, int32_t blk) {
+// watchdog flag turns it into VXM_ERR_INTERNAL on the host.  Returns the
+// stamp word (epoch + change bits).
+__device__ inline uint32_t wait_stamp(const uint32_t* p, uint32_t ep, uint32_t* watchdog,
+                                      uint32_t code, int32_t blk) {
   // spin on relaxed loads (an acquire per iteration would invalidate L1 each
   // time), then one acquire once the stamp is seen
-  for (uint32_t it = 0; ld_relaxed(p) != ep; ++it) {
+  for (uint32_t it = 0; (ld_relaxed(p) & kStampEp) != ep; ++it) {
     if (it > (1u << 22)) {
       if (atomicExch(watchdog, 1u) == 0u) {  // record the first expired wait
         watchdog[1] = code;
         watchdog[2] = uint32_t(blk);
-        watchdog[3] = ep * 1000u + (ld_acquire(p) % 1000u);  // expected, seen
+        watchdog[3] = ep * 1000u + ((ld_acquire(p) & kStampEp) % 1000u);  // expected, seen
       }
-      return;
+      return 0u;
     }
     __nanosleep(64);
   }
-  (void)ld_acquire(p);
+  return ld_acquire(p);
 }
 
 __device__ inline const EV load_voxel(const uint32_t* pool, int32_t slot, int lin) {
@@ -558,6 +565,41 @@ __device__ inline void store_voxel(uint32_t* pool, int32_t slot, int lin, const 
   __stcg(p, uint32_t(v.sq));
   __stcg(p + 1, ev_w1(v));
   __stcg(p + 2, ev_w2(v));
+}
+
+// Round 1, block without sites: reset_parented (esdf/integrator.cpp:352-363)
+// leaves it without givers, so its sweep is the identity — one warp copies the
+// reset block to the work buffer (lane: voxels 4 * (lane + 32 h) .. + 3).
+__device__ inline void warp_reset_copy(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                       int lane, const Limits& lim) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  uint32_t w[48];
+#pragma unroll
+  for (int h = 0; h < 4; ++h)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const uint4 v = __ldcg(s4 + 3 * (lane + 32 * h) + j);
+      w[12 * h + 4 * j] = v.x;
+      w[12 * h + 4 * j + 1] = v.y;
+      w[12 * h + 4 * j + 2] = v.z;
+      w[12 * h + 4 * j + 3] = v.w;
+    }
+#pragma unroll
+  for (int v = 0; v < 16; ++v) {
+    const uint32_t f = (w[3 * v + 2] >> 16) & 0xffu;
+    if ((f & VXM_ESDF_OBSERVED) && !(f & VXM_ESDF_SITE) && ((w[3 * v + 1] | (w[3 * v + 2] & 0xffffu)) != 0u)) {
+      w[3 * v] = uint32_t((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq);
+      w[3 * v + 1] = 0u;
+      w[3 * v + 2] &= 0xffff0000u;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 4; ++h)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      __stcg(d4 + 3 * (lane + 32 * h) + j, make_uint4(w[12 * h + 4 * j], w[12 * h + 4 * j + 1],
+                                                     w[12 * h + 4 * j + 2], w[12 * h + 4 * j + 3]));
 }
 
 // ---- lowering v3: group-per-block sweeps with line masks --------------------------
@@ -618,6 +660,29 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
     a.count[2] = 0u;
     a.work_ctr[0] = a.work_ctr[1] = a.work_ctr[2] = a.work_ctr[3] = 0u;
   }
+  // Round 1 of a full update splits the map: blocks that may hold sites go to
+  // the 64-thread sweep groups (front of list[1]); site-free blocks are only
+  // reset and copied, one warp each (back of list[1]).  Order is irrelevant:
+  // round-1 sweeps are independent.  (a.r1 is zero on entry.)
+  if (a.full && lower) {
+    for (uint32_t b0 = blockIdx.x * kL3Threads + (threadIdx.x & ~31u); b0 < n_blocks;
+         b0 += gridDim.x * kL3Threads) {
+      const uint32_t b = b0 + lane;
+      const bool in = b < n_blocks;
+      const bool site = in && a.site_any[b] != 0;
+      const uint32_t ms = __ballot_sync(0xffffffffu, site), mn = __ballot_sync(0xffffffffu, in && !site);
+      uint32_t bs = 0, bn = 0;
+      if (lane == 0) {
+        if (ms) bs = atomicAdd(a.r1 + 0, __popc(ms));
+        if (mn) bn = atomicAdd(a.r1 + 1, __popc(mn));
+      }
+      bs = __shfl_sync(0xffffffffu, bs, 0);
+      bn = __shfl_sync(0xffffffffu, bn, 0);
+      const uint32_t below = (1u << lane) - 1u;
+      if (site) a.list[1][bs + __popc(ms & below)] = int32_t(b);
+      else if (in) a.list[1][n_blocks - 1u - (bn + __popc(mn & below))] = int32_t(b);
+    }
+  }
   grid.sync();
   stamp();
   uint32_t r = 0;
@@ -638,13 +703,14 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
         if (r > 1 || !a.full) a.status->sum_dirty += n_dirty;
       }
       // ---- sweep phase (esdf/integrator.cpp:509-513)
-      uint32_t* const ctr = a.work_ctr + cp;
+      uint32_t* const ctr = r1_full ? a.r1 + 2 : a.work_ctr + cp;
+      const uint32_t n_grp = r1_full ? *((volatile uint32_t*)(a.r1 + 0)) : n_dirty;
       while (true) {
         if (t == 0) G.bcast = atomicAdd(ctr, 1u);
         group_sync(bar);
         const uint32_t i = G.bcast;
-        if (i >= n_dirty) break;
-        const int32_t s = r1_full ? int32_t(i) : __ldcg(dirty + i);
+        if (i >= n_grp) break;
+        const int32_t s = __ldcg((r1_full ? a.list[1] : dirty) + i);
         unsigned long long tt0 = 0, tt1 = 0, tt2 = 0;
         if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt0));
         if (t == 0) {
@@ -693,6 +759,19 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
           atomicMax(d + 7, (unsigned long long)passes);  // max passes
         }
       }
+      if (r1_full) {  // site-free blocks: reset + copy, one warp each
+        const uint32_t n_ns = *((volatile uint32_t*)(a.r1 + 1));
+        while (true) {
+          uint32_t j = 0;
+          if (lane == 0) j = atomicAdd(a.r1 + 3, 1u);
+          j = __shfl_sync(0xffffffffu, j, 0);
+          if (j >= n_ns) break;
+          const int32_t s = __ldcg(a.list[1] + (n_blocks - 1u - j));
+          warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
+          __syncwarp();  // the warp's stores before the release of the sweep stamp
+          if (lane == 0) st_release(a.stamp_swept + s, ep);
+        }
+      }
       // ---- border phase (esdf/integrator.cpp:517-559) as a dataflow: pair items
       // are taken in axis order (all x, then y, then z) after every sweep was
       // taken, and each waits only for what the reference's phase order makes
@@ -727,23 +806,46 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
           }
           // dependencies, one lane each: sweeps of lo/hi (lanes 0-1); pairs of
           // lower axes touching lo or hi (lanes 2-5: axis 0, 6-9: axis 1)
-          if (wait && lane < 2 + 4 * axis) {
+          bool dep_chg = false;  // the lane's earlier pair changed its block
+          if (lane < 2 + 4 * axis && (wait || r1_full)) {
             if (lane < 2) {
               const int32_t b = lane == 0 ? lo : hi;
-              if (is_dirty(b)) wait_stamp(a.stamp_swept + b, ep, &a.status->watchdog, 10u + axis, b);
+              if (wait && is_dirty(b)) wait_stamp(a.stamp_swept + b, ep, &a.status->watchdog, 10u + axis, b);
             } else {
               const int q = (lane - 2) >> 2;               // the earlier axis
               const int32_t b = ((lane - 2) & 2) ? hi : lo;
-              int32_t c = b;                               // pair (c, c + q)
-              if (((lane - 2) & 1) == 0) c = __ldg(a.nbr + size_t(b) * 6 + 2 * q + 1);  // b - q
+              const bool b_is_hi = ((lane - 2) & 1) == 0;  // pair (b - q, b), else (b, b + q)
+              int32_t c = b;
+              if (b_is_hi) c = __ldg(a.nbr + size_t(b) * 6 + 2 * q + 1);  // b - q
               if (c >= 0) {
                 const int32_t n = __ldg(a.nbr + size_t(c) * 6 + 2 * q);
-                if (n >= 0 && (is_dirty(c) || is_dirty(n)))
-                  wait_stamp(a.stamp_pair[q] + c, ep, &a.status->watchdog, 20u + 10u * q + axis, c);
+                if (n >= 0 && (is_dirty(c) || is_dirty(n))) {
+                  const uint32_t v = wait ? wait_stamp(a.stamp_pair[q] + c, ep, &a.status->watchdog,
+                                                       20u + 10u * q + axis, c)
+                                          : ld_acquire(a.stamp_pair[q] + c);
+                  dep_chg = (v & (b_is_hi ? kStampHiChg : kStampLoChg)) != 0u;
+                }
               }
             }
           }
+          const uint32_t chg_mask = __ballot_sync(0xffffffffu, dep_chg);
           __syncwarp();
+          if (r1_full) {
+            // After reset_parented only sites give, and a pair can only give to
+            // a face through a giver on the other face: a block gives here if
+            // it holds a site or an earlier pair of this round changed it (for a
+            // y (z) pair: the x (x, y) pairs through its faces, whose stamps
+            // were just read).  A pair with no giver on either side is the
+            // identity: skip it.
+            // lanes 2 + 4q + {0, 1} watch lo's pairs, 2 + 4q + {2, 3} hi's
+            constexpr uint32_t lo_lanes = 0x0ccu, hi_lanes = 0x330u;
+            const bool g_lo = a.site_any[lo] != 0 || (chg_mask & lo_lanes) != 0u;
+            const bool g_hi = a.site_any[hi] != 0 || (chg_mask & hi_lanes) != 0u;
+            if (!g_lo && !g_hi) {
+              if (lane == 0) st_release(a.stamp_pair[axis] + lo, ep);
+              return;
+            }
+          }
           const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
           bool ac = false, bc = false;
           unsigned long long mlo[3] = {0, 0, 0}, mhi[3] = {0, 0, 0};
@@ -773,7 +875,8 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
           bc = __any_sync(0xffffffffu, bc);
           ++n_pairs;
           __syncwarp();  // the warp's voxel stores before the release of the pair stamp
-          if (lane == 0) st_release(a.stamp_pair[axis] + lo, ep);
+          if (lane == 0)
+            st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));
           const int32_t who[2] = {lo, hi};
           const bool chg[2] = {ac, bc};
 #pragma unroll
@@ -847,6 +950,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
   grid.sync();
   stamp();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.r1[0] = a.r1[1] = a.r1[2] = a.r1[3] = 0u;  // zero for the next launch
     a.status->rounds = r;
     a.status->n_esdf_blocks = n_blocks;
     a.meta->round_epoch = base_epoch + r + 2;
@@ -1090,6 +1194,7 @@ struct MarkArgs {
   uint32_t call_epoch;
   uint8_t* flags;  // per effective block: 1 changed, 2 to_update, 4 to_clear
   DevStatus* status;
+  uint8_t* site_any;  // per ESDF slot: the block holds a site after marking
 };
 
 __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
@@ -1102,7 +1207,7 @@ __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
       continue;
     }
     const int32_t ts = a.eff_tslot[e];
-    bool bch = false, bup = false, bcl = false;
+    bool bch = false, bup = false, bcl = false, bsite = false;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int lin = threadIdx.x + 256 * k;
@@ -1110,6 +1215,7 @@ __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
       const bool observed = tv.y > 0.0f;
       const bool site = observed && fabsf(tv.x) <= a.site_threshold;
       const bool inside = observed && tv.x < 0.0f;
+      bsite |= site;
       uint32_t* p = pool + size_t(es) * 1536 + lin * 3;
       const uint32_t o0 = p[0], o1 = p[1], o2 = p[2];
       const EV ev = ev_unpack(o0, o1, o2);
@@ -1147,7 +1253,9 @@ __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
     bch = __syncthreads_or(bch);
     bup = __syncthreads_or(bup);
     bcl = __syncthreads_or(bcl);
+    bsite = __syncthreads_or(bsite);
     if (threadIdx.x == 0) {
+      a.site_any[es] = bsite ? 1 : 0;
       a.flags[e] = uint8_t((bch ? 1 : 0) | (bup ? 2 : 0) | (bcl ? 4 : 0));
       if (bch) a.stamp_mark[es] = a.call_epoch;
       if (bup || bcl) atomicOr(&a.status->any_update, 1u);
@@ -1347,6 +1455,7 @@ static uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.call_epoch = epoch;
   m.flags = s.flags;
   m.status = ctx->d_status;
+  m.site_any = E->site_any;
   ctx->prof_begin("k_mark");
   k_mark<<<std::max<uint32_t>(1, std::min<uint32_t>(n7, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(m);
   ctx->prof_end();
@@ -1414,6 +1523,8 @@ static LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.work_ctr = E->dirty_count + 3;  // [0,1,2] list counts, [3..6] work counters
   la.line_mask = E->line_mask;
   la.stamp_swept = E->stamp_swept;
+  la.site_any = E->site_any;
+  la.r1 = E->dirty_count + 7;
   static const int dataflow = [] {
     const char* e = std::getenv("VXM_LOWER_DATAFLOW");
     return e ? std::atoi(e) : 1;
