@@ -551,7 +551,7 @@ __device__ inline uint32_t wait_stamp(const uint32_t* p, uint32_t ep, uint32_t* 
       }
       return 0u;
     }
-    __nanosleep(64);
+    __nanosleep(20);
   }
   return ld_acquire(p);
 }
@@ -694,6 +694,11 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
       const int cp = int(r & 1u), np = cp ^ 1;
       const uint32_t ep = base_epoch + r, ep_next = ep + 1;
       const bool r1_full = a.full && r == 1;
+      if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && r < 16) {
+        unsigned long long tm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+        a.trace[256 + 4 * r + 3] = tm;  // round start (block 0)
+      }
       const uint32_t n_dirty = r1_full ? n_blocks : *((volatile uint32_t*)&a.count[r % 3u]);
       const int32_t* dirty = a.list[cp];
       if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -748,6 +753,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
         if (a.trace && t == 0 && r < 16) {  // debug: per-block cost breakdown per round
           unsigned long long tt3;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt3));
+          atomicMax(a.trace + 256 + 4 * r, tt3);  // last sweep end
           unsigned long long* d = a.trace + 128 + 8 * r;
           atomicAdd(d + 0, 1ull);                      // blocks
           atomicAdd(d + 1, tt1 - tt0);                 // load
@@ -761,15 +767,25 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
       }
       if (r1_full) {  // site-free blocks: reset + copy, one warp each
         const uint32_t n_ns = *((volatile uint32_t*)(a.r1 + 1));
+        constexpr uint32_t kCopyChunk = 2;
+        uint32_t j = 0, j_end = 0;
         while (true) {
-          uint32_t j = 0;
-          if (lane == 0) j = atomicAdd(a.r1 + 3, 1u);
-          j = __shfl_sync(0xffffffffu, j, 0);
+          if (j == j_end) {
+            if (lane == 0) j = atomicAdd(a.r1 + 3, kCopyChunk);
+            j = __shfl_sync(0xffffffffu, j, 0);
+            j_end = j + kCopyChunk;
+          }
           if (j >= n_ns) break;
           const int32_t s = __ldcg(a.list[1] + (n_blocks - 1u - j));
+          ++j;
           warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
           __syncwarp();  // the warp's stores before the release of the sweep stamp
           if (lane == 0) st_release(a.stamp_swept + s, ep);
+          if (a.trace && lane == 0 && r < 16) {
+            unsigned long long tm;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+            atomicMax(a.trace + 256 + 4 * r + 2, tm);  // last copy end
+          }
         }
       }
       // ---- border phase (esdf/integrator.cpp:517-559) as a dataflow: pair items
@@ -783,14 +799,17 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
         return r1_full || __ldcg(a.stamp_dirty[cp] + b) == ep;
       };
       uint32_t* const pctr = a.work_ctr + 2 + cp;
-      const uint32_t per_axis = 2u * n_dirty;
+      // items per axis: (dirty block, side); in round 1 of a full update every
+      // block is dirty, so each pair is its lower block's side-0 item
+      const uint32_t sides = r1_full ? 1u : 2u;
+      const uint32_t per_axis = sides * n_dirty;
       // one pair item (warp-uniform); `wait` enables the dataflow dependencies
       auto do_item = [&](uint32_t w, bool wait) {
         {
           const int axis = int(w / per_axis);
           const uint32_t rest = w - uint32_t(axis) * per_axis;
-          const uint32_t i = rest >> 1;
-          const int side = int(rest & 1u);
+          const uint32_t i = r1_full ? rest : rest >> 1;
+          const int side = r1_full ? 0 : int(rest & 1u);
           const int32_t d = r1_full ? int32_t(i) : __ldcg(dirty + i);
           int32_t lo, hi;
           if (side == 0) {
@@ -877,6 +896,12 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
           __syncwarp();  // the warp's voxel stores before the release of the pair stamp
           if (lane == 0)
             st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));
+          if (a.trace && lane == 0 && r < 16) {
+            unsigned long long tm;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+            atomicMax(a.trace + 256 + 4 * r + 1, tm);  // last pair end
+            if (r == 1 || r == 3) atomicMax(a.trace + 320 + 4 * r + axis, tm);  // per axis
+          }
           const int32_t who[2] = {lo, hi};
           const bool chg[2] = {ac, bc};
 #pragma unroll
@@ -902,11 +927,14 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower3(LowerArgs a) {
         }
       };
       if (a.dataflow) {
+        // one item per claim: a warp blocked on a dependency must not hold
+        // later items (claiming chunks serialises the chains measurably)
+        const uint32_t n_items = 3u * per_axis;
         while (true) {
           uint32_t w = 0;
           if (lane == 0) w = atomicAdd(pctr, 1u);
           w = __shfl_sync(0xffffffffu, w, 0);
-          if (w >= 3u * per_axis) break;
+          if (w >= n_items) break;
           do_item(w, true);
         }
       } else {  // phased: a grid barrier before each axis group, as the reference
@@ -1478,8 +1506,8 @@ static void launch_lower(Context* ctx, LowerArgs& la) {
   static const bool trace = std::getenv("VXM_TRACE_LOWER") != nullptr;
   static DevBuf trace_buf;
   if (trace) {
-    trace_buf.ensure(256 * sizeof(unsigned long long));
-    VXM_CUDA(cudaMemsetAsync(trace_buf.p, 0, 256 * sizeof(unsigned long long), ctx->stream));
+    trace_buf.ensure(512 * sizeof(unsigned long long));
+    VXM_CUDA(cudaMemsetAsync(trace_buf.p, 0, 512 * sizeof(unsigned long long), ctx->stream));
     la.trace = trace_buf.as<unsigned long long>();
   }
   void* args[] = {&la};
@@ -1489,7 +1517,7 @@ static void launch_lower(Context* ctx, LowerArgs& la) {
                                        ctx->stream));
   ctx->prof_end();
   if (trace) {
-    unsigned long long h[256];
+    unsigned long long h[512];
     VXM_CUDA(cudaMemcpyAsync(h, trace_buf.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     VXM_CUDA(cudaStreamSynchronize(ctx->stream));
     std::fprintf(stderr, "[k_lower grid=%d] phases(us):", grid);
@@ -1503,6 +1531,18 @@ static void launch_lower(Context* ctx, LowerArgs& la) {
                    "sweep %.1f us; passes mean %.2f max %llu\n",
                    r, d[0], d[1] * 1e-3 / d[0], d[2] * 1e-3 / d[0], d[3] * 1e-3 / d[0], d[4] * 1e-3,
                    d[5] * 1e-3, double(d[6]) / d[0], d[7]);
+    }
+    for (int r = 1; r < 16 && h[256 + 4 * r + 3]; ++r) {
+      const unsigned long long* e = h + 256 + 4 * r;
+      const double t0 = double(e[3]);
+      const double nxt = (r + 1 < 16 && h[256 + 4 * (r + 1) + 3]) ? double(h[256 + 4 * (r + 1) + 3]) : 0.0;
+      std::fprintf(stderr, "  r%d timeline (us from round start): last sweep %.1f, last copy %.1f, last pair %.1f, next round %.1f",
+                   r, e[0] ? (e[0] - t0) * 1e-3 : 0.0, e[2] ? (e[2] - t0) * 1e-3 : 0.0,
+                   e[1] ? (e[1] - t0) * 1e-3 : 0.0, nxt ? (nxt - t0) * 1e-3 : 0.0);
+      if (r == 1 || r == 3)
+        std::fprintf(stderr, "; pair axes x %.1f y %.1f z %.1f", (h[320 + 4 * r] - t0) * 1e-3,
+                     (h[320 + 4 * r + 1] - t0) * 1e-3, (h[320 + 4 * r + 2] - t0) * 1e-3);
+      std::fprintf(stderr, "\n");
     }
   }
   ctx->count_launch();
