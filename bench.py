@@ -49,7 +49,7 @@ CONFIGS = {
 
 
 TSDF_KERNELS = ("k_rays", "k_dilate_alloc", "k_integrate", "k_compact")
-ESDF_KERNELS = ("k_merge7", "k_select_effective", "k_alloc_list", "k_mark", "k_lower", "k_compact_esdf")
+ESDF_KERNELS = ("k_merge7", "k_effective_alloc", "k_mark", "k_lower", "k_compact_esdf")
 
 
 def log(*a):

@@ -1207,6 +1207,138 @@ __global__ void k_merge_sorted(const uint64_t* __restrict__ ok, const int32_t* _
   }
 }
 
+// unique + has_block(TSDF) + ESDF get_or_allocate in one ordered pass
+// (mark_impl :279-295): per merged element one thread; tiles publish the
+// (effective, new) count pair through one look-back; new blocks get slots
+// num_blocks + rank(new) in key order, as the reference's sorted loop does.
+__global__ void __launch_bounds__(256) k_effective_alloc(const uint64_t* __restrict__ merged,
+                                                         const uint32_t* n_upd, HashView tsdf,
+                                                         uint64_t* __restrict__ eff_keys,
+                                                         int32_t* __restrict__ eff_tslot,
+                                                         uint32_t* n_eff, AllocListArgs a,
+                                                         ScanTiles st) {
+  __shared__ uint32_t s_tile, s_scan[64], s_pre[2], s_base;
+  scan_prepare_next(st);
+  const uint32_t n = 7u * (*n_upd);
+  const uint32_t tiles = (n + blockDim.x - 1) / blockDim.x;
+  if (tiles == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *n_eff = 0;
+      *a.n_new_out = 0;
+      *a.n_old_out = a.meta->num_blocks;
+    }
+    return;
+  }
+  const uint64_t limit = a.capacity < a.max_blocks ? uint64_t(a.capacity) : a.max_blocks;
+  while (true) {
+    const uint32_t tile = scan_take_tile(st, &s_tile);
+    if (tile >= tiles) break;
+    if (threadIdx.x == 0) s_base = a.meta->num_blocks;
+    const uint32_t r = tile * blockDim.x + threadIdx.x;
+    bool keep = false, is_new = false;
+    int32_t ts = -1, found = -1;
+    uint64_t k = 0;
+    if (r < n) {
+      k = merged[r];
+      if (r == 0 || merged[r - 1] != k) {
+        ts = hash_find(tsdf, k);
+        keep = ts >= 0;
+        if (keep) {
+          found = hash_find_rw(a.hash, k);
+          is_new = found < 0;
+        }
+      }
+    }
+    uint32_t ea, eb, ta, tb;
+    block_scan2(keep ? 1u : 0u, is_new ? 1u : 0u, ea, eb, ta, tb, s_scan);
+    if (threadIdx.x < 32) {  // warp 0: look-back
+      uint32_t pa, pb;
+      scan_lookback(st, tile, ta, tb, pa, pb);
+      if (threadIdx.x == 0) {
+        s_pre[0] = pa;
+        s_pre[1] = pb;
+      }
+    }
+    __syncthreads();
+    const uint32_t base = s_base;
+    if (keep) {
+      const uint32_t e = s_pre[0] + ea;
+      int32_t slot = found;
+      if (is_new) {
+        const uint32_t q = s_pre[1] + eb;
+        const uint64_t sl = uint64_t(base) + q;
+        if (sl < limit) {
+          hash_insert(a.hash, k, int32_t(sl));
+          a.slot_keys[sl] = k;
+          slot = int32_t(sl);
+          a.new_keys[q] = k;
+          a.new_slots[q] = slot;
+          if (a.stamp_new) a.stamp_new[sl] = a.call_epoch;
+        } else {
+          slot = -1;
+        }
+      }
+      eff_keys[e] = k;
+      eff_tslot[e] = ts;
+      a.slots_out[e] = slot;
+    }
+    if (threadIdx.x == 0 && tile == tiles - 1) {
+      *n_eff = s_pre[0] + ta;
+      const uint64_t want = uint64_t(base) + s_pre[1] + tb;
+      const uint64_t got = want < limit ? want : limit;
+      *a.n_new_out = uint32_t(got - base);
+      *a.n_old_out = base;
+      if (want > a.capacity && a.capacity < a.max_blocks) a.status->pool_overflow = 1u;
+      if (want > a.max_blocks) a.status->capacity_error = 1u;
+      a.meta->num_blocks = uint32_t(got);
+    }
+    __syncthreads();
+  }
+}
+
+// Side structures of the new blocks (neighbour table, sorted set), done by
+// k_mark's CTAs after their marking: neither depends on the other.
+struct PostAllocArgs {
+  const uint64_t* new_keys;
+  const int32_t* new_slots;
+  const uint32_t* n_new;
+  const uint32_t* n_old;
+  HashView hash;
+  int32_t* nbr;
+  const uint64_t* old_sorted_k;
+  const int32_t* old_sorted_s;
+  uint64_t* out_sorted_k;
+  int32_t* out_sorted_s;
+};
+__device__ inline void post_alloc(const PostAllocArgs& p) {
+  const uint32_t n_new = *p.n_new, n_old = *p.n_old;
+  const uint32_t gsz = gridDim.x * blockDim.x;
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t it = gtid; it < 6u * n_new; it += gsz) {  // k_nbr_update
+    const uint32_t i = it / 6;
+    const int d = int(it - i * 6);
+    const int axis = d >> 1, s = (d & 1) ? -1 : 1;
+    const int32_t me = p.new_slots[i];
+    const int32_t nb = hash_find(p.hash, key_shift(p.new_keys[i], axis, s));
+    p.nbr[size_t(me) * 6 + d] = nb;
+    if (nb >= 0) p.nbr[size_t(nb) * 6 + (d ^ 1)] = me;
+  }
+  for (uint32_t it = gtid; it < n_old + n_new; it += gsz) {  // k_merge_sorted
+    if (it < n_old) {
+      const uint64_t k = p.old_sorted_k[it];
+      const uint32_t r = it + lower_bound_u64(p.new_keys, n_new, k);
+      p.out_sorted_k[r] = k;
+      p.out_sorted_s[r] = p.old_sorted_s[it];
+    } else {
+      const uint32_t j = it - n_old;
+      const uint64_t k = p.new_keys[j];
+      const uint32_t r = j + lower_bound_u64(p.old_sorted_k, n_old, k);
+      p.out_sorted_k[r] = k;
+      p.out_sorted_s[r] = p.new_slots[j];
+    }
+  }
+}
+
 // ---- mark_sites (TSDF source) — esdf/integrator.cpp:177-198, 268-348 ------------
 struct MarkArgs {
   const uint64_t* eff_keys;
@@ -1223,72 +1355,109 @@ struct MarkArgs {
   uint8_t* flags;  // per effective block: 1 changed, 2 to_update, 4 to_clear
   DevStatus* status;
   uint8_t* site_any;  // per ESDF slot: the block holds a site after marking
+  PostAllocArgs post;
 };
 
+// One warp per effective block: lane l holds voxels 4 * (l + 32 h) + e
+// (h = 0..3, e = 0..3), so the ESDF block (3 x 16-byte words per 4 voxels)
+// and the TSDF block (2 x 16-byte words per 4 voxels) load and store
+// coalesced, all in flight at once; the block flags are warp ballots.
 __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
   const uint32_t n = *a.n_eff;
   uint32_t* pool = a.pools[a.meta->cur];
-  for (uint32_t e = blockIdx.x; e < n; e += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += nwarps) {
     const int32_t es = a.eff_eslot[e];
     if (es < 0) {  // capacity exhausted before this block (MapCapacityError)
-      if (threadIdx.x == 0) a.flags[e] = 0;
+      if (lane == 0) a.flags[e] = 0;
       continue;
     }
     const int32_t ts = a.eff_tslot[e];
+    const uint4* t4 = reinterpret_cast<const uint4*>(a.tsdf_pool + size_t(ts) * kVPB);
+    uint4* e4 = reinterpret_cast<uint4*>(pool + size_t(es) * 1536);
     bool bch = false, bup = false, bcl = false, bsite = false;
+    uint32_t w[48];
+    float tv[32];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int lin = threadIdx.x + 256 * k;
-      const float2 tv = a.tsdf_pool[size_t(ts) * kVPB + lin];
-      const bool observed = tv.y > 0.0f;
-      const bool site = observed && fabsf(tv.x) <= a.site_threshold;
-      const bool inside = observed && tv.x < 0.0f;
-      bsite |= site;
-      uint32_t* p = pool + size_t(es) * 1536 + lin * 3;
-      const uint32_t o0 = p[0], o1 = p[1], o2 = p[2];
-      const EV ev = ev_unpack(o0, o1, o2);
-      EV nv = ev;
-      if (!observed) {
-        if (ev.f & VXM_ESDF_SITE) bcl = true;
-        nv = EV{0, 0, 0, 0, 0u, 0u};
-      } else {
-        nv.f = VXM_ESDF_OBSERVED | (site ? VXM_ESDF_SITE : 0) | (inside ? VXM_ESDF_INSIDE : 0);
-        const bool was_obs = ev.f & VXM_ESDF_OBSERVED, was_site = ev.f & VXM_ESDF_SITE;
-        if (site) {
-          nv.sq = 0;
-          nv.px = nv.py = nv.pz = 0;
-          if (!was_obs || !was_site) bup = true;
-        } else if (!was_obs) {
-          reset_to_saturated(nv, a.lim);
-          bup = true;
-        } else if (was_site) {
-          reset_to_saturated(nv, a.lim);
-          bcl = true;
-          bup = true;
-        } else if (bool(ev.f & VXM_ESDF_INSIDE) != inside) {
-          reset_to_saturated(nv, a.lim);
-          bup = true;
-        }
+    for (int h = 0; h < 4; ++h) {  // all loads in flight before any use
+      const int q = lane + 32 * h;  // voxels 4q .. 4q + 3
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const uint4 v = __ldcg(e4 + 3 * q + j);
+        w[12 * h + 4 * j] = v.x; w[12 * h + 4 * j + 1] = v.y;
+        w[12 * h + 4 * j + 2] = v.z; w[12 * h + 4 * j + 3] = v.w;
       }
-      const uint32_t n0 = uint32_t(nv.sq), n1 = ev_w1(nv), n2 = ev_w2(nv);
-      if (n0 != o0 || n1 != o1 || n2 != o2) {
-        p[0] = n0;
-        p[1] = n1;
-        p[2] = n2;
-        bch = true;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint4 v = __ldcg(t4 + 2 * q + j);
+        tv[8 * h + 4 * j] = __uint_as_float(v.x); tv[8 * h + 4 * j + 1] = __uint_as_float(v.y);
+        tv[8 * h + 4 * j + 2] = __uint_as_float(v.z); tv[8 * h + 4 * j + 3] = __uint_as_float(v.w);
       }
     }
-    bch = __syncthreads_or(bch);
-    bup = __syncthreads_or(bup);
-    bcl = __syncthreads_or(bcl);
-    bsite = __syncthreads_or(bsite);
-    if (threadIdx.x == 0) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int q = lane + 32 * h;
+      bool ch = false;
+#pragma unroll
+      for (int v4 = 0; v4 < 4; ++v4) {
+        const int v = 4 * h + v4;
+        const float dist = tv[2 * v], weight = tv[2 * v + 1];
+        const bool observed = weight > 0.0f;
+        const bool site = observed && fabsf(dist) <= a.site_threshold;
+        const bool inside = observed && dist < 0.0f;
+        bsite |= site;
+        const uint32_t o0 = w[3 * v], o1 = w[3 * v + 1], o2 = w[3 * v + 2];
+        const EV ev = ev_unpack(o0, o1, o2);
+        EV nv = ev;
+        if (!observed) {
+          if (ev.f & VXM_ESDF_SITE) bcl = true;
+          nv = EV{0, 0, 0, 0, 0u, 0u};
+        } else {
+          nv.f = VXM_ESDF_OBSERVED | (site ? VXM_ESDF_SITE : 0) | (inside ? VXM_ESDF_INSIDE : 0);
+          const bool was_obs = ev.f & VXM_ESDF_OBSERVED, was_site = ev.f & VXM_ESDF_SITE;
+          if (site) {
+            nv.sq = 0;
+            nv.px = nv.py = nv.pz = 0;
+            if (!was_obs || !was_site) bup = true;
+          } else if (!was_obs) {
+            reset_to_saturated(nv, a.lim);
+            bup = true;
+          } else if (was_site) {
+            reset_to_saturated(nv, a.lim);
+            bcl = true;
+            bup = true;
+          } else if (bool(ev.f & VXM_ESDF_INSIDE) != inside) {
+            reset_to_saturated(nv, a.lim);
+            bup = true;
+          }
+        }
+        const uint32_t n0 = uint32_t(nv.sq), n1 = ev_w1(nv), n2 = ev_w2(nv);
+        ch |= (n0 != o0) | (n1 != o1) | (n2 != o2);
+        w[3 * v] = n0;
+        w[3 * v + 1] = n1;
+        w[3 * v + 2] = n2;
+      }
+      if (ch) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          __stcg(e4 + 3 * q + j, make_uint4(w[12 * h + 4 * j], w[12 * h + 4 * j + 1],
+                                            w[12 * h + 4 * j + 2], w[12 * h + 4 * j + 3]));
+      }
+      bch |= ch;
+    }
+    bch = __any_sync(0xffffffffu, bch);
+    bup = __any_sync(0xffffffffu, bup);
+    bcl = __any_sync(0xffffffffu, bcl);
+    bsite = __any_sync(0xffffffffu, bsite);
+    if (lane == 0) {
       a.site_any[es] = bsite ? 1 : 0;
       a.flags[e] = uint8_t((bch ? 1 : 0) | (bup ? 2 : 0) | (bcl ? 4 : 0));
       if (bch) a.stamp_mark[es] = a.call_epoch;
       if (bup || bcl) atomicOr(&a.status->any_update, 1u);
     }
   }
+  post_alloc(a.post);
 }
 
 // ---- clear_invalid — esdf/integrator.cpp:433-486 --------------------------------
@@ -1431,17 +1600,7 @@ static uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   ctx->prof_end();
   ctx->count_launch();
   {
-    const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
-    ctx->prof_begin("k_select_effective");
-    k_select_effective<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(
-        s.merged, updated->d_count, T->hash, s.eff_keys, s.eff_tslot, s.counts + 0, st);
-    ctx->prof_end();
-    ctx->count_launch();
-  }
-  {
     AllocListArgs al{};
-    al.keys = s.eff_keys;
-    al.n_ptr = s.counts + 0;
     al.hash = E->hash;
     al.slot_keys = E->slot_keys;
     al.meta = E->meta;
@@ -1456,17 +1615,16 @@ static uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
     al.call_epoch = epoch;
     al.status = ctx->d_status;
     const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
-    ctx->prof_begin("k_alloc_list");
-    k_alloc_list<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(al, st);
+    ctx->prof_begin("k_effective_alloc");
+    k_effective_alloc<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(
+        s.merged, updated->d_count, T->hash, s.eff_keys, s.eff_tslot, s.counts + 0, al, st);
     ctx->prof_end();
     ctx->count_launch();
   }
-  k_nbr_update<<<grid_for(ctx, 6ull * n7), 256, 0, ctx->stream>>>(s.new_keys, s.new_slots,
-                                                                 s.counts + 1, E->hash, E->nbr);
   const int sp = E->sorted_parity;
-  k_merge_sorted<<<grid_for(ctx, uint64_t(E->num_blocks) + n7), 256, 0, ctx->stream>>>(
-      E->sorted_keys[sp], E->sorted_slots[sp], s.counts + 2, s.new_keys, s.new_slots, s.counts + 1,
-      E->sorted_keys[1 - sp], E->sorted_slots[1 - sp]);
+  PostAllocArgs pa{s.new_keys, s.new_slots, s.counts + 1, s.counts + 2, E->hash, E->nbr,
+                   E->sorted_keys[sp], E->sorted_slots[sp], E->sorted_keys[1 - sp],
+                   E->sorted_slots[1 - sp]};
   E->sorted_parity = 1 - sp;
   MarkArgs m{};
   m.eff_keys = s.eff_keys;
@@ -1484,10 +1642,16 @@ static uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.flags = s.flags;
   m.status = ctx->d_status;
   m.site_any = E->site_any;
+  m.post = pa;
   ctx->prof_begin("k_mark");
-  k_mark<<<std::max<uint32_t>(1, std::min<uint32_t>(n7, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(m);
+  static int mark_per_sm = 0;  // one wave of warps, each takes blocks until done
+  if (!mark_per_sm) {
+    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mark_per_sm, k_mark, 256, 0));
+    mark_per_sm = std::max(mark_per_sm, 1);
+  }
+  k_mark<<<ctx->sm_count * mark_per_sm, 256, 0, ctx->stream>>>(m);
   ctx->prof_end();
-  ctx->count_launch(3);
+  ctx->count_launch();
   check_launch(ctx, "esdf mark phase");
   return n7;
 }

@@ -84,7 +84,8 @@ __device__ inline bool sample_linear_d(const float* img, int W, int H, double u,
 // Exact-floor FP32 pre-filter for one projected coordinate.  Returns true and
 // sets *idx when floor(u_exact) is certain; u_exact = (f*x)/z + c in FP64.
 __device__ inline bool fast_floor(float f, float c, float xf, float zf, int* idx) {
-  const float t = __fdiv_rn(__fmul_rn(f, xf), zf);
+  // approximate division (<= 2 ulp): the bound E below covers >= 16 units
+  const float t = __fdividef(__fmul_rn(f, xf), zf);
   const float u = __fadd_rn(t, c);
   const float E = __fmul_rn(__fadd_rn(__fadd_rn(fabsf(t), fabsf(c)), fabsf(u)), 9.5367431640625e-07f) +
                   1e-30f;  // (|t| + |c| + |u|) * 2^-20 >= 16 units of the error
@@ -94,7 +95,7 @@ __device__ inline bool fast_floor(float f, float c, float xf, float zf, int* idx
   return true;
 }
 
-__global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
+__global__ void __launch_bounds__(256, 6) k_integrate(IntegrateArgs a) {
   __shared__ double s_A[3][3][8];  // R_SL(i, axis) * centre_axis(v)
   const DevStatus* st = a.status_ro;
   if (st->pool_overflow || st->capacity_error || st->bitmap_overflow) return;
@@ -300,7 +301,12 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   a.max_gap = cfg.max_sample_gap;
   a.inv_sq = cfg.weighting == VXM_WEIGHT_INVERSE_SQUARE;
   a.linear = (va.lidar ? cfg.lidar_sample : cfg.camera_sample) == VXM_SAMPLE_LINEAR;
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * 8));
+  static int per_sm = 0;  // resident CTAs per SM: the persistent grid is one wave
+  if (!per_sm) {
+    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_integrate, 256, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * per_sm));
   ctx->prof_begin("k_integrate");
   k_integrate<<<grid, 256, 0, ctx->stream>>>(a);
   ctx->prof_end();
