@@ -1,6 +1,9 @@
 // Micro-benchmark: cycles per sweep pass / phase of the ESDF block sweep in
 // isolation (one 64-thread group per CTA).  Build: make -C tools/micro
 #include "esdf.cu"
+#ifndef NOMASK
+#define NOMASK 0
+#endif
 #include <cstdio>
 #include <vector>
 namespace vxm {
@@ -19,13 +22,13 @@ __global__ void k_sweep_micro(const uint32_t* src, Limits lim, long long* clk, i
     }
     group_sync(1);
     long long c0 = clock64();
-    uint32_t c = sweep_phase3<0>(G, t, 1, 0, lim);
+    uint32_t c = NOMASK ? sweep_line_fast<0>(G, t) : sweep_phase3<0>(G, t, 1, 0, lim);
     group_sync(1);
     long long c1 = clock64();
-    c |= sweep_phase3<1>(G, t, 1, 0, lim);
+    c |= NOMASK ? sweep_line_fast<1>(G, t) : sweep_phase3<1>(G, t, 1, 0, lim);
     group_sync(1);
     long long c2 = clock64();
-    c |= sweep_phase3<2>(G, t, 1, 0, lim);
+    c |= NOMASK ? sweep_line_fast<2>(G, t) : sweep_phase3<2>(G, t, 1, 0, lim);
     group_sync_or(1, c != 0);
     long long c3 = clock64();
     acc[0] += c1 - c0; acc[1] += c2 - c1; acc[2] += c3 - c2; acc[3] += c3 - c0;
