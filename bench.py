@@ -27,6 +27,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -42,8 +44,13 @@ CONFIGS = {
     "c1": dict(scene="sphere_in_box", sensor="camera", w=640, h=480, vs=0.05, trunc=0.2,
                max_int=5.0, esdf=None, orbit=100,
                workload="C1: sphere_in_box, 640x480 depth, 5 cm voxels, TSDF integration only"),
+    "c5": dict(scene="sphere_world", sensor="none", w=512, h=512, vs=0.02, trunc=0.08, max_int=0.0,
+               esdf=(0.02, 2.0), orbit=0,
+               workload="C5: ESDF full recompute of a dense 512^3-voxel SphereWorld volume "
+                        "(262,144 blocks); each step alternates between two volumes so every "
+                        "update resets and re-lowers the whole map"),
     "c3": dict(scene="lidar_yard", sensor="lidar", w=2048, h=64, vs=0.1, trunc=0.4, max_int=100.0,
-               esdf=(0.1, 2.0), orbit=100,
+               esdf=(0.1, 2.0), orbit=100, reserve=1 << 20,
                workload="C3: 64-beam x 2048-column LiDAR, 10 cm voxels, 100 m range, TSDF + ESDF"),
 }
 
@@ -142,11 +149,12 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu capture summary."""
+def ncu_traffic(kernel, config="c2"):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu capture summary
+    of this config (null when no capture of this config is committed)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kernel)
+            return json.load(f).get(config, {}).get(kernel)
     except Exception:
         return None
 
@@ -170,6 +178,10 @@ def run_ours(args, rank, world, device):
     # ---- value: device-resident path --------------------------------------
     T = vx.TsdfLayer(c["vs"], ctx=ctx)
     E = vx.EsdfLayer(c["vs"], ctx=ctx) if ecfg else None
+    if c.get("reserve"):  # pre-size the pools (the map grows every frame)
+        T.reserve(c["reserve"])
+        if E is not None:
+            E.reserve(c["reserve"])
     changed = vx.BlockList(ctx)
     esdf_out = vx.BlockList(ctx)
 
@@ -200,8 +212,13 @@ def run_ours(args, rank, world, device):
 
     # ---- per-kernel breakdown: the same frames replayed on fresh layers with
     # CUDA events around every kernel (outside the timed region above) -------
+    del T, E
     Tp = vx.TsdfLayer(c["vs"], ctx=ctx)
     Ep = vx.EsdfLayer(c["vs"], ctx=ctx) if ecfg else None
+    if c.get("reserve"):
+        Tp.reserve(c["reserve"])
+        if Ep is not None:
+            Ep.reserve(c["reserve"])
     for i in range(W):
         step(Tp, Ep, i)
     ctx.set_profiling(True)
@@ -217,14 +234,18 @@ def run_ours(args, rank, world, device):
         if n:
             kernels[name] = {"ms_total": ms, "launches": n, "ms_per_launch": ms / n}
     ctx.set_profiling(False)
-    del Tp, Ep
     tsdf_ms = sum(kernels[k]["ms_total"] for k in TSDF_KERNELS if k in kernels) / K
     esdf_ms = sum(kernels[k]["ms_total"] for k in ESDF_KERNELS if k in kernels) / K
 
     # ---- e2e: public host API, host buffers, copies inside the timed region --
     pinned = [torch.from_numpy(d).pin_memory() for _, d in frames]
+    del Tp, Ep
     T2 = vx.TsdfLayer(c["vs"], ctx=ctx)
     E2 = vx.EsdfLayer(c["vs"], ctx=ctx) if ecfg else None
+    if c.get("reserve"):
+        T2.reserve(c["reserve"])
+        if E2 is not None:
+            E2.reserve(c["reserve"])
     for i in range(W):
         ch = vx.integrate_depth(T2, pinned[i].numpy(), frames[i][0], sensor, icfg)
         if E2 is not None:
@@ -255,7 +276,7 @@ def run_ours(args, rank, world, device):
                 h2d=h2d // K, d2h=d2h // K, W=Wd, H=H)
 
 
-def roofline(res, K):
+def roofline(res, K, config="c2"):
     peak, peak_src = measured_peaks()
     st, ks = res["stats"], res["kernels"]
     # algorithmic bytes per launch
@@ -275,14 +296,14 @@ def roofline(res, K):
            "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
            "algorithmic_bytes_per_launch": int(per_launch),
            "share_of_step": round(ks[dom]["ms_total"] / (res["total_s"] * 1e3), 3),
-           "traffic": ncu_traffic(dom)}
+           "traffic": ncu_traffic(dom, config)}
     others = {}
     for k in cand:
         if k != dom:
             b = bytes_by_kernel[k] / ks[k]["launches"]
             a = b / (ks[k]["ms_per_launch"] / 1e3) / 1e9
             others[k] = {"achieved": round(a, 1), "frac": round(a / peak, 4),
-                         "algorithmic_bytes_per_launch": int(b), "traffic": ncu_traffic(k)}
+                         "algorithmic_bytes_per_launch": int(b), "traffic": ncu_traffic(k, config)}
     out["other_kernels"] = others
     return out
 
@@ -337,6 +358,116 @@ def cpu_model():
 
 
 # ---------------------------------------------------------------------------
+C5_SIDE = 512
+
+
+def c5_volumes(side=C5_SIDE):
+    from paper_2311_00626_b200 import synth
+    ka, va = synth.sphere_world(side, 0.02, 0.08, seed=2311)
+    kb, vb = synth.sphere_world(side, 0.02, 0.08, seed=2312)
+    assert np.array_equal(ka, kb)
+    return ka, va, vb
+
+
+def run_c5(args, rank, world, device):
+    import torch
+
+    import paper_2311_00626_b200 as vx
+    from paper_2311_00626_b200 import _abi as A
+    torch.cuda.set_device(device)
+    W, K = args.warmup, args.steps
+    keys, va, vb = c5_volumes()
+    ctx = vx.Context(device)
+    ext = torch.cuda.ExternalStream(ctx.stream, device=device)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)
+    Ts = [vx.TsdfLayer(0.02, ctx=ctx), vx.TsdfLayer(0.02, ctx=ctx)]
+    Ts[0].write_blocks(keys, va)
+    Ts[1].write_blocks(keys, vb)
+    del va, vb
+    ecfg = A.default_esdf_config(site_threshold=0.02, max_distance=2.0)
+    upd = vx.BlockList(ctx)
+    upd.assign(keys)
+    out = vx.BlockList(ctx)
+    E = vx.EsdfLayer(0.02, ctx=ctx)
+    for i in range(W):
+        vx.update_esdf_device(E, Ts[i % 2], upd, ecfg, out)
+    torch.cuda.synchronize(device)
+    ctx.reset_stats()
+    launches0 = ctx.launch_count
+    tot = []
+    with ClockSampler(device) as clk:
+        for i in range(W, W + K):
+            flush.zero_()
+            torch.cuda.synchronize(device)
+            e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            e0.record(ext)
+            vx.update_esdf_device(E, Ts[i % 2], upd, ecfg, out)
+            e1.record(ext)
+            e1.synchronize()
+            tot.append(e0.elapsed_time(e1))
+    launches = ctx.launch_count - launches0
+    stats = ctx.stats()
+    total_s = sum(tot) / 1000.0
+    # per-kernel breakdown on extra steps (events around each kernel)
+    ctx.set_profiling(True)
+    ctx.reset_kernel_times()
+    for i in range(W + K, W + 2 * K):
+        flush.zero_()
+        torch.cuda.synchronize(device)
+        vx.update_esdf_device(E, Ts[i % 2], upd, ecfg, out)
+    torch.cuda.synchronize(device)
+    kernels = {}
+    for name in ESDF_KERNELS:
+        ms, n = ctx.kernel_time(name)
+        if n:
+            kernels[name] = {"ms_total": ms, "launches": n, "ms_per_launch": ms / n}
+    ctx.set_profiling(False)
+    # e2e: the public host API (host key list in, host changed list out)
+    e2e_t, h2d, d2h = [], 0, 0
+    for i in range(W + 2 * K, W + 3 * K):
+        flush.zero_()
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        ch = vx.update_esdf(E, Ts[i % 2], keys, ecfg)
+        e2e_t.append(time.perf_counter() - t0)
+        h2d += keys.nbytes
+        d2h += ch.nbytes
+    return dict(total_s=total_s, tot=tot, tsdf_ms=0.0, esdf_ms=total_s * 1e3 / K, stats=stats,
+                kernels=kernels, launches=launches, clocks=clk.summary(), e2e_s=sum(e2e_t),
+                h2d=h2d // K, d2h=d2h // K, n_blocks=len(keys))
+
+
+def cpu_reference_c5(steps, side=C5_SIDE):
+    """The reference's update_esdf (oracle/_ref, OpenMP) on the same volumes."""
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    from oracle.bindings import PortOracle, RefOracle, have_ref
+    from paper_2311_00626_b200 import _abi as A
+    kind = "reference" if have_ref() else "port"
+    o = RefOracle() if kind == "reference" else PortOracle()
+    keys, va, vb = c5_volumes(side)
+    Ts = [o.layer(A.LAYER_TSDF, 0.02), o.layer(A.LAYER_TSDF, 0.02)]
+    o.write_blocks(Ts[0], keys, va)
+    o.write_blocks(Ts[1], keys, vb)
+    del va, vb
+    ecfg = A.default_esdf_config(site_threshold=0.02, max_distance=2.0)
+    E = o.layer(A.LAYER_ESDF, 0.02)
+    o.update_esdf(E, Ts[0], keys, ecfg)  # warm-up (allocation)
+    times = []
+    for i in range(1, 1 + steps):
+        t0 = time.perf_counter()
+        o.update_esdf(E, Ts[i % 2], keys, ecfg)
+        times.append(time.perf_counter() - t0)
+    n = len(times)
+    return dict(value=n / sum(times), kind=kind, cores=cores if kind == "reference" else 1, frames=n,
+                ms_per_step=1e3 * sum(times) / n,
+                sample=f"C5 {side}^3 SphereWorld, {n} full update_esdf call(s) alternating two volumes "
+                       f"after one untimed allocation call; "
+                       + ("production update_esdf (OpenMP)" if kind == "reference"
+                          else "oracle/voxmap_oracle.c restatement (serial)"))
+
+
+# ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -359,10 +490,17 @@ def main():
               "l2": "flushed (256 MB write) before every timed step",
               "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single"}
 
+    if args.config == "c5":
+        config = {"workload": c["workload"], "volume_voxels": f"{C5_SIDE}^3", "voxel_size_m": c["vs"],
+                  "truncation_m": c["trunc"],
+                  "esdf": {"site_threshold_m": c["esdf"][0], "max_distance_m": c["esdf"][1]},
+                  "l2": "flushed (256 MB write) before every timed step; map 1.6 GB ESDF + 2 GB TSDF",
+                  "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single"}
     if args.impl == "reference":
         if rank != 0:
             return
-        r = cpu_reference_run(args.config, args.warmup, args.steps)
+        r = (cpu_reference_c5(max(1, min(args.steps, 3))) if args.config == "c5"
+             else cpu_reference_run(args.config, args.warmup, args.steps))
         line = {"impl": "reference", "metric": METRIC, "value": round(r["value"], 3), "unit": UNIT,
                 "n_gpus": args.gpus, "steps": r["frames"], "warmup": args.warmup,
                 "ms_per_step": round(r["ms_per_step"], 3), "higher_is_better": True,
@@ -380,7 +518,7 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    res = run_ours(args, rank, world, local)
+    res = (run_c5 if args.config == "c5" else run_ours)(args, rank, world, local)
     K = args.steps
     if world > 1:
         import torch.distributed as dist
@@ -395,13 +533,14 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32/i32",
         "data": "synthetic (reference scene + orbit trajectory, sphere-traced depth rendered on the host)",
         "config": config,
-        "tsdf_voxel_updates_per_s": round(world * st["voxels_updated"] / res["total_s"], 1),
+        "tsdf_voxel_updates_per_s": (round(world * st["voxels_updated"] / res["total_s"], 1)
+                                     if args.config != "c5" else None),
         # kernel time per frame (CUDA events around each kernel, separate replay)
         "tsdf_ms_per_frame": round(res["tsdf_ms"], 4),
         "esdf_ms_per_frame": round(res["esdf_ms"], 4),
         "work_per_frame": {k: round(v / K, 1) for k, v in st.items()},
         "kernels_ms_per_frame": {k: round(v["ms_total"] / K, 4) for k, v in res["kernels"].items()},
-        "roofline": roofline(res, K),
+        "roofline": roofline(res, K, args.config),
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
         "e2e": {"value": round(world * K / res["e2e_s"], 2), "unit": UNIT,
@@ -409,9 +548,14 @@ def main():
                 "path": "vxm_integrate_depth_camera + vxm_update_esdf (host buffers)"},
         "value_path": "vxm_update_frame_camera_device (depth in HBM, one host round trip per frame)",
     }
+    if args.config == "c5":
+        line["e2e"]["path"] = "vxm_update_esdf (host key list in, host changed list out)"
+        line["value_path"] = "vxm_update_esdf_list (updated list and map in HBM)"
+        line["unit_note"] = "a step (frame) is one full update_esdf of the 512^3 map"
     if not args.no_cpu_baseline and world == 1:
         try:
-            r = cpu_reference_run(args.config, args.warmup, args.steps, budget_s=args.cpu_budget)
+            r = (cpu_reference_c5(1) if args.config == "c5" else
+                 cpu_reference_run(args.config, args.warmup, args.steps, budget_s=args.cpu_budget))
             line["cpu_baseline"] = {"value": round(r["value"], 3), "unit": UNIT, "cores": r["cores"],
                                     "kind": r["kind"], "sample": r["sample"], "cpu": cpu_model()}
         except Exception as e:  # the CPU baseline is reported, not the measurement

@@ -182,6 +182,10 @@ void vxm_layer_destroy(vxm_layer* layer);
 double vxm_layer_voxel_size(const vxm_layer* layer);
 /* num_blocks() — layer.hpp:61. */
 vxm_status vxm_layer_num_blocks(vxm_layer* layer, uint64_t* out);
+/* Pre-sizes the device block pool for n blocks (capped at max_blocks) so that
+ * later frames do not pay pool growth; no effect on results.  (The reference
+ * allocates per block; nvblox pre-sizes its GPU hash the same way.) */
+vxm_status vxm_layer_reserve(vxm_layer* layer, uint64_t n_blocks);
 /* has_block() for a batch of keys — layer.hpp:63. out[i] = 0/1. */
 vxm_status vxm_layer_has_blocks(vxm_layer* layer, const vxm_grid_index* keys, uint64_t n,
                                 uint8_t* out);

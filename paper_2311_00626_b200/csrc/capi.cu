@@ -425,6 +425,12 @@ void vxm_layer_destroy(vxm_layer* L) {
   delete L;
 }
 double vxm_layer_voxel_size(const vxm_layer* L) { return L->vs; }
+vxm_status vxm_layer_reserve(vxm_layer* L, uint64_t n) {
+  return guard([&] {
+    REQUIRE_ARG(L, "null argument");
+    L->ensure_capacity(std::min<uint64_t>(n, L->max_blocks));
+  });
+}
 vxm_status vxm_layer_num_blocks(vxm_layer* L, uint64_t* out) {
   return guard([&] {
     L->refresh();

@@ -5,6 +5,10 @@
 #include <algorithm>
 #include <cstring>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "runtime.cuh"
 
 namespace vxm {
@@ -146,6 +150,9 @@ void Layer::adopt_meta(int slot) {
 
 void Layer::ensure_capacity(uint64_t need) {
   if (need <= capacity) return;
+  static const bool trace = std::getenv("VXM_TRACE_GROW") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  const uint32_t cap_before = capacity;
   if (need > (uint64_t(1) << 31) - 1)
     throw Error(VXM_ERR_CAPACITY, "Layer: device block pool limit (2^31 blocks) exceeded");
   refresh();
@@ -211,6 +218,13 @@ void Layer::ensure_capacity(uint64_t need) {
     }
   }
   capacity = uint32_t(nc);
+  if (trace) {
+    VXM_CUDA(cudaStreamSynchronize(st));
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    std::fprintf(stderr, "[grow %s] %u -> %u blocks (need %llu, live %llu): %.2f ms\n",
+                 type == VXM_LAYER_ESDF ? "esdf" : "tsdf", cap_before, capacity,
+                 (unsigned long long)need, (unsigned long long)live, ms);
+  }
 }
 
 Layer::~Layer() {

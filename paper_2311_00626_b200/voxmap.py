@@ -252,6 +252,10 @@ class _Layer:
     def block_size(self) -> float:
         return self.voxel_size * A.VOXELS_PER_SIDE
 
+    def reserve(self, n_blocks: int) -> None:
+        """Pre-size the device pool (vxm_layer_reserve); results are unaffected."""
+        check(lib().vxm_layer_reserve(self.h, C.c_uint64(n_blocks)))
+
     def num_blocks(self) -> int:
         n = C.c_uint64()
         check(lib().vxm_layer_num_blocks(self.h, C.byref(n)))
