@@ -39,7 +39,8 @@ typedef enum {
   VXM_ERR_INVALID_ARGUMENT = 2, /* std::invalid_argument                         */
   VXM_ERR_CAPACITY = 3,         /* voxmap::MapCapacityError      layer.hpp:28-31  */
   VXM_ERR_CUDA = 4,             /* device missing / CUDA runtime failure         */
-  VXM_ERR_INTERNAL = 5
+  VXM_ERR_INTERNAL = 5,
+  VXM_ERR_IO = 6                /* voxmap::IoError          serialization.hpp:24-27 */
 } vxm_status;
 
 /* ---- POD mirrors of the reference types -------------------------------- */
@@ -235,6 +236,20 @@ vxm_status vxm_integrate_depth_lidar_device(vxm_layer* layer, const float* depth
                                             const vxm_lidar* lidar,
                                             const vxm_integrator_config* cfg,
                                             vxm_blocklist* changed_out);
+
+/* ---- snapshots (core/serialization.hpp:29-35, FORMATS.md "VXLF") -------- */
+/* save_snapshot (serialization.cpp:88-110): VXLF v1, little-endian; layers in
+ * the reference's order (tsdf, then esdf), blocks in sorted GridIndex order, so
+ * equal maps give byte-identical files.  Either layer may be NULL; both must
+ * have `voxel_size`.  Errors: VXM_ERR_IO (cannot open / write failed). */
+vxm_status vxm_snapshot_save(const char* path, double voxel_size, vxm_layer* tsdf, vxm_layer* esdf);
+/* load_snapshot (serialization.cpp:112-158): creates the layers found in the
+ * file on `ctx` (NULL when absent).  VXM_ERR_IO on bad magic, unsupported
+ * version, invalid voxel size, truncated payload, voxel size mismatch, unknown
+ * layer name, and for the occupancy / color layers this library does not
+ * implement (out of scope). */
+vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* voxel_size_out,
+                             vxm_layer** tsdf_out, vxm_layer** esdf_out);
 
 /* ---- fused frame update (replay pipeline step) ---------------------------- */
 /* One frame of the replay pipeline (pipeline.cpp:95-108: integrate the frame,

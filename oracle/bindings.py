@@ -213,6 +213,20 @@ class RefOracle(_Base):
                                              C.c_int(int(serial)), A.ptr(out)))
         return out
 
+    def save_snapshot(self, path, voxel_size, tsdf=None, esdf=None):
+        self._check(self.lib.vxr_snapshot_save(os.fsencode(path), C.c_double(voxel_size),
+                                               tsdf.h if tsdf is not None else None,
+                                               esdf.h if esdf is not None else None))
+
+    def load_snapshot(self, path):
+        vs = C.c_double()
+        th, eh = C.c_void_p(), C.c_void_p()
+        self._check(self.lib.vxr_snapshot_load(os.fsencode(path), C.byref(vs), C.byref(th),
+                                               C.byref(eh)))
+        return (vs.value,
+                OracleLayer(self, th, A.LAYER_TSDF, vs.value) if th.value else None,
+                OracleLayer(self, eh, A.LAYER_ESDF, vs.value) if eh.value else None)
+
     def orbit_pose(self, scene, k, total, lidar=False):
         p = A.PoseC()
         self._check(self.lib.vxr_orbit_pose(scene.encode(), C.c_int(int(lidar)), C.c_int(k),

@@ -27,6 +27,7 @@
 #include "voxmap/core/layer.hpp"
 #include "voxmap/core/voxels.hpp"
 #include "voxmap/esdf/integrator.hpp"
+#include "voxmap/core/serialization.hpp"
 #include "voxmap/eval/oracle.hpp"
 #include "voxmap/integrate/integrator.hpp"
 #include "voxmap/io/dataset.hpp"
@@ -383,6 +384,34 @@ int vxr_compare_esdf(void* a, void* b, uint64_t* stats4, double* max_abs) {
     stats4[2] = cmp.within_one_voxel;
     stats4[3] = cmp.flag_mismatches;
     *max_abs = cmp.max_abs_error;
+  });
+}
+
+// save_snapshot / load_snapshot (core/serialization.cpp:88-158) on a cake
+// that borrows the driver's layers.
+int vxr_snapshot_save(const char* path, double vs, void* tsdf, void* esdf) {
+  return guard([&] {
+    vr::LayerCake cake(vs);
+    if (tsdf) cake.tsdf.reset(static_cast<RefLayer*>(tsdf)->tsdf);
+    if (esdf) cake.esdf.reset(static_cast<RefLayer*>(esdf)->esdf);
+    try {
+      vr::save_snapshot(cake, path);
+    } catch (...) {
+      cake.tsdf.release();
+      cake.esdf.release();
+      throw;
+    }
+    cake.tsdf.release();
+    cake.esdf.release();
+  });
+}
+int vxr_snapshot_load(const char* path, double* vs, void** tsdf, void** esdf) {
+  return guard([&] {
+    vr::LayerCake cake = vr::load_snapshot(path);
+    *vs = cake.voxel_size;
+    *tsdf = *esdf = nullptr;
+    if (cake.tsdf) *tsdf = new RefLayer{VXM_LAYER_TSDF, cake.tsdf.release(), nullptr};
+    if (cake.esdf) *esdf = new RefLayer{VXM_LAYER_ESDF, nullptr, cake.esdf.release()};
   });
 }
 

@@ -16,6 +16,7 @@ VXM_ERR_INVALID_ARGUMENT = 2
 VXM_ERR_CAPACITY = 3
 VXM_ERR_CUDA = 4
 VXM_ERR_INTERNAL = 5
+VXM_ERR_IO = 6
 
 LAYER_TSDF = 0
 LAYER_ESDF = 1

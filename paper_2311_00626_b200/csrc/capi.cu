@@ -778,3 +778,150 @@ vxm_status vxm_query_batch(vxm_layer* E, const double* xyz, uint64_t n, int want
 }
 
 }  // extern "C"
+
+// ---- VXLF snapshots — core/serialization.cpp:20-158 (format: FORMATS.md) ------
+namespace {
+constexpr char kVxlfMagic[4] = {'V', 'X', 'L', 'F'};
+constexpr uint32_t kVxlfVersion = 1;
+
+struct File {
+  FILE* f = nullptr;
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+void io_fail(const std::string& m) { throw Error(VXM_ERR_IO, m); }
+template <typename T>
+void put(FILE* f, const T& v) {
+  if (std::fwrite(&v, sizeof(T), 1, f) != 1) io_fail("snapshot: write failed");
+}
+template <typename T>
+void get(FILE* f, T* v) {
+  if (std::fread(v, sizeof(T), 1, f) != 1) io_fail("snapshot: truncated file");
+}
+
+// write_layer — serialization.cpp:42-60: name, voxel bytes, count, then per
+// block (x, y, z) and the voxel payload, in sorted order.  The device gathers
+// the sorted blocks (vxm_layer_export); records are streamed in chunks.
+void write_layer(FILE* f, const char* name, vxm_layer* L) {
+  const uint32_t name_len = uint32_t(std::strlen(name));
+  put(f, name_len);
+  if (std::fwrite(name, 1, name_len, f) != name_len) io_fail("snapshot: write failed");
+  const uint32_t vb = uint32_t(L->voxel_bytes());
+  put(f, vb);
+  L->refresh();
+  const uint64_t n = L->num_blocks;
+  put(f, n);
+  std::vector<vxm_grid_index> keys(n);
+  std::vector<unsigned char> vox(n * L->block_bytes());
+  vxm_status st = vxm_layer_export(L, keys.data(), vox.data(), n);
+  if (st != VXM_OK) throw Error(st, g_err);
+  const size_t bb = L->block_bytes();
+  for (uint64_t i = 0; i < n; ++i) {
+    put(f, keys[i].x);
+    put(f, keys[i].y);
+    put(f, keys[i].z);
+    if (std::fwrite(vox.data() + i * bb, 1, bb, f) != bb) io_fail("snapshot: write failed");
+  }
+}
+
+// read_layer — serialization.cpp:62-82
+void read_layer(FILE* f, vxm_layer* L) {
+  uint32_t vb = 0;
+  get(f, &vb);
+  if (vb != L->voxel_bytes()) io_fail("snapshot: voxel size mismatch for layer payload");
+  uint64_t n = 0;
+  get(f, &n);
+  const size_t bb = L->block_bytes();
+  std::vector<vxm_grid_index> keys;
+  std::vector<unsigned char> vox;
+  for (uint64_t i = 0; i < n; ++i) {
+    vxm_grid_index g;
+    get(f, &g.x);
+    get(f, &g.y);
+    get(f, &g.z);
+    keys.push_back(g);
+    vox.resize(keys.size() * bb);
+    if (std::fread(vox.data() + (keys.size() - 1) * bb, 1, bb, f) != bb)
+      io_fail("snapshot: truncated block payload");
+  }
+  if (!keys.empty()) {
+    const vxm_status st = vxm_layer_write_blocks(L, keys.data(), keys.size(), vox.data());
+    if (st != VXM_OK) throw Error(st, g_err);
+  }
+}
+}  // namespace
+
+extern "C" {
+vxm_status vxm_snapshot_save(const char* path, double vs, vxm_layer* tsdf, vxm_layer* esdf) {
+  return guard([&] {
+    REQUIRE_ARG(path, "null argument");
+    REQUIRE_ARG(!tsdf || tsdf->type == VXM_LAYER_TSDF, "snapshot: tsdf argument is not a TSDF layer");
+    REQUIRE_ARG(!esdf || esdf->type == VXM_LAYER_ESDF, "snapshot: esdf argument is not an ESDF layer");
+    REQUIRE_ARG((!tsdf || tsdf->vs == vs) && (!esdf || esdf->vs == vs),
+                "snapshot: layer voxel size differs from the snapshot's");
+    File out;
+    out.f = std::fopen(path, "wb");
+    if (!out.f) io_fail(std::string("snapshot: cannot open for writing: ") + path);
+    if (std::fwrite(kVxlfMagic, 1, 4, out.f) != 4) io_fail("snapshot: write failed");
+    put(out.f, kVxlfVersion);
+    put(out.f, vs);  // f64
+    const uint32_t count = (tsdf ? 1u : 0u) + (esdf ? 1u : 0u);
+    put(out.f, count);
+    if (tsdf) write_layer(out.f, "tsdf", tsdf);  // serialization.cpp:102-105 order
+    if (esdf) write_layer(out.f, "esdf", esdf);
+    if (std::fflush(out.f) != 0) io_fail(std::string("snapshot: write failed: ") + path);
+  });
+}
+
+vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* vs_out, vxm_layer** tsdf_out,
+                             vxm_layer** esdf_out) {
+  vxm_layer* T = nullptr;
+  vxm_layer* E = nullptr;
+  const vxm_status st = guard([&] {
+    REQUIRE_ARG(ctx && path && tsdf_out && esdf_out, "null argument");
+    File in;
+    in.f = std::fopen(path, "rb");
+    if (!in.f) io_fail(std::string("snapshot: cannot open: ") + path);
+    char magic[4];
+    if (std::fread(magic, 1, 4, in.f) != 4 || std::memcmp(magic, kVxlfMagic, 4) != 0)
+      io_fail("snapshot: bad magic");
+    uint32_t version = 0;
+    get(in.f, &version);
+    if (version != kVxlfVersion) io_fail("snapshot: unsupported version " + std::to_string(version));
+    double vs = 0.0;
+    get(in.f, &vs);
+    if (!(vs > 0.0)) io_fail("snapshot: invalid voxel size");
+    uint32_t count = 0;
+    get(in.f, &count);
+    for (uint32_t i = 0; i < count; ++i) {
+      uint32_t name_len = 0;
+      get(in.f, &name_len);
+      if (name_len > 64) io_fail("snapshot: layer name too long");
+      std::string name(name_len, '\0');
+      if (std::fread(name.data(), 1, name_len, in.f) != name_len) io_fail("snapshot: truncated layer name");
+      if (name == "tsdf" || name == "esdf") {
+        vxm_layer*& L = name == "tsdf" ? T : E;
+        if (!L) {
+          const vxm_status s = vxm_layer_create(ctx, name == "tsdf" ? VXM_LAYER_TSDF : VXM_LAYER_ESDF, vs,
+                                                0, &L);
+          if (s != VXM_OK) throw Error(s, g_err);
+        }
+        read_layer(in.f, L);
+      } else if (name == "occupancy" || name == "color") {
+        io_fail("snapshot: layer '" + name + "' is not implemented by this library");
+      } else {
+        io_fail("snapshot: unknown layer name '" + name + "'");
+      }
+    }
+    *vs_out = vs;
+    *tsdf_out = T;
+    *esdf_out = E;
+  });
+  if (st != VXM_OK) {
+    vxm_layer_destroy(T);
+    vxm_layer_destroy(E);
+  }
+  return st;
+}
+}  // extern "C"

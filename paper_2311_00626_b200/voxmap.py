@@ -60,9 +60,13 @@ class VoxmapCudaError(VoxmapError):
     """No usable sm_100 device / CUDA failure (there is no CPU fallback)."""
 
 
+class IoError(VoxmapError):
+    """voxmap::IoError (core/serialization.hpp:24-27)."""
+
+
 _ERRORS = {A.VXM_ERR_INVALID_POSE: InvalidPoseError, A.VXM_ERR_INVALID_ARGUMENT: InvalidArgumentError,
            A.VXM_ERR_CAPACITY: MapCapacityError, A.VXM_ERR_CUDA: VoxmapCudaError,
-           A.VXM_ERR_INTERNAL: VoxmapError}
+           A.VXM_ERR_INTERNAL: VoxmapError, A.VXM_ERR_IO: IoError}
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -315,10 +319,41 @@ class TsdfLayer(_Layer):
     kind = A.LAYER_TSDF
     dtype = A.TSDF_DTYPE
 
+    @classmethod
+    def _adopt(cls, h, ctx):
+        obj = cls.__new__(cls)
+        obj.ctx, obj.h = ctx, h
+        return obj
+
 
 class EsdfLayer(_Layer):
     kind = A.LAYER_ESDF
     dtype = A.ESDF_DTYPE
+
+    @classmethod
+    def _adopt(cls, h, ctx):
+        obj = cls.__new__(cls)
+        obj.ctx, obj.h = ctx, h
+        return obj
+
+
+def save_snapshot(path: str, voxel_size: float, tsdf: TsdfLayer | None = None,
+                  esdf: EsdfLayer | None = None) -> None:
+    """save_snapshot (core/serialization.hpp:31): VXLF v1, byte-identical to the
+    reference's for equal maps."""
+    check(lib().vxm_snapshot_save(os.fsencode(path), C.c_double(voxel_size),
+                                  tsdf.h if tsdf is not None else None,
+                                  esdf.h if esdf is not None else None))
+
+
+def load_snapshot(path: str, ctx: Context | None = None):
+    """load_snapshot (core/serialization.hpp:35) -> (voxel_size, tsdf | None, esdf | None)."""
+    ctx = ctx or default_context()
+    vs = C.c_double()
+    th, eh = C.c_void_p(), C.c_void_p()
+    check(lib().vxm_snapshot_load(ctx.h, os.fsencode(path), C.byref(vs), C.byref(th), C.byref(eh)))
+    return (vs.value, TsdfLayer._adopt(th, ctx) if th.value else None,
+            EsdfLayer._adopt(eh, ctx) if eh.value else None)
 
 
 def _depth(depth):
