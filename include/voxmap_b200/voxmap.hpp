@@ -49,6 +49,10 @@ class DeviceError : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
 };
+class IoError : public std::runtime_error {  // core/serialization.hpp:24-27
+ public:
+  using std::runtime_error::runtime_error;
+};
 
 inline void check(vxm_status s) {
   if (s == VXM_OK) return;
@@ -57,6 +61,7 @@ inline void check(vxm_status s) {
     case VXM_ERR_INVALID_POSE: throw InvalidPoseError(msg);
     case VXM_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case VXM_ERR_CAPACITY: throw MapCapacityError(msg);
+    case VXM_ERR_IO: throw IoError(msg);
     default: throw DeviceError(msg);
   }
 }
@@ -167,6 +172,9 @@ class Layer {
     voxel_size_ = voxel_size;
     max_blocks_ = max_blocks;
   }
+  // Adopts a C-ABI layer handle (e.g. from vxm_snapshot_load).
+  Layer(vxm_layer* adopt, double voxel_size, Context& ctx)
+      : h_(adopt), ctx_(&ctx), voxel_size_(voxel_size), max_blocks_(size_t{1} << 30) {}
   ~Layer() {
     if (h_) vxm_layer_destroy(h_);
   }
@@ -184,6 +192,11 @@ class Layer {
 
   double voxel_size() const { return voxel_size_; }
   double block_size() const { return voxel_size_ * kVoxelsPerSide; }
+  // The C-ABI handle, with host-side edits uploaded first.
+  vxm_layer* c_handle() const {
+    flush();
+    return h_;
+  }
   size_t num_blocks() const {
     flush();
     uint64_t n = 0;
@@ -558,6 +571,38 @@ inline std::vector<QueryResult> query_batch(const Layer<EsdfVoxel>& esdf,
     out[i].gradient = {r[i].gradient[0], r[i].gradient[1], r[i].gradient[2]};
   }
   return out;
+}
+
+// ---- snapshots (core/layer_cake.hpp:27-57, core/serialization.hpp:29-35) --------
+// The layers of a LayerCake this library implements (TSDF, ESDF).
+struct LayerCake {
+  explicit LayerCake(double vs) : voxel_size(vs) {}
+  double voxel_size;
+  std::unique_ptr<Layer<TsdfVoxel>> tsdf;
+  std::unique_ptr<Layer<EsdfVoxel>> esdf;
+  Layer<TsdfVoxel>& require_tsdf() {
+    if (!tsdf) tsdf = std::make_unique<Layer<TsdfVoxel>>(voxel_size);
+    return *tsdf;
+  }
+  Layer<EsdfVoxel>& require_esdf() {
+    if (!esdf) esdf = std::make_unique<Layer<EsdfVoxel>>(voxel_size);
+    return *esdf;
+  }
+};
+
+inline void save_snapshot(const LayerCake& cake, const std::string& path) {
+  check(vxm_snapshot_save(path.c_str(), cake.voxel_size, cake.tsdf ? cake.tsdf->c_handle() : nullptr,
+                          cake.esdf ? cake.esdf->c_handle() : nullptr));
+}
+
+inline LayerCake load_snapshot(const std::string& path, Context& ctx = default_context()) {
+  double vs = 0.0;
+  vxm_layer *t = nullptr, *e = nullptr;
+  check(vxm_snapshot_load(ctx.handle(), path.c_str(), &vs, &t, &e));
+  LayerCake cake(vs);
+  if (t) cake.tsdf = std::make_unique<Layer<TsdfVoxel>>(t, vs, ctx);
+  if (e) cake.esdf = std::make_unique<Layer<EsdfVoxel>>(e, vs, ctx);
+  return cake;
 }
 
 }  // namespace voxmap_b200

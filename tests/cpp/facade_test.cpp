@@ -159,6 +159,38 @@ int main() {
     CHECK(known > 50);
   }
 
+  // snapshots (core/serialization.hpp:29-35): save -> load round trip
+  {
+    const std::string path = "/tmp/vxm_facade_test.vxlf";
+    vb::LayerCake cake(tsdf.voxel_size());
+    cake.tsdf = std::make_unique<vb::Layer<vb::TsdfVoxel>>(tsdf.clone());
+    cake.esdf = std::make_unique<vb::Layer<vb::EsdfVoxel>>(esdf.clone());
+    vb::save_snapshot(cake, path);
+    vb::LayerCake back = vb::load_snapshot(path);
+    CHECK(back.voxel_size == tsdf.voxel_size());
+    CHECK(back.tsdf && back.esdf);
+    auto same = [](const auto& a, const auto& b) {
+      const auto ka = a.sorted_indices(), kb = b.sorted_indices();
+      if (ka != kb) return false;
+      for (const auto& g : ka)
+        if (std::memcmp(a.block_ptr(g)->voxels.data(), b.block_ptr(g)->voxels.data(),
+                        sizeof(a.block_ptr(g)->voxels)) != 0)
+          return false;
+      return true;
+    };
+    CHECK(same(*back.tsdf, tsdf));
+    CHECK(same(*back.esdf, esdf));
+    CHECK(same_layer(*back.esdf, oesdf));
+    bool threw = false;
+    try {
+      vb::load_snapshot("/tmp/does-not-exist.vxlf");
+    } catch (const vb::IoError&) {
+      threw = true;
+    }
+    CHECK(threw);
+    std::remove(path.c_str());
+  }
+
   vxo_layer_destroy(otsdf);
   vxo_layer_destroy(oesdf);
   vxm_synth_scene_destroy(scene);
