@@ -251,6 +251,19 @@ vxm_status vxm_snapshot_save(const char* path, double voxel_size, vxm_layer* tsd
 vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* voxel_size_out,
                              vxm_layer** tsdf_out, vxm_layer** esdf_out);
 
+/* ---- block-sharded ESDF ------------------------------------ */
+/* One update_esdf (esdf/integrator.cpp:365-413) over a map sharded by block x:
+ * shard p of n_shards (its own context — same GPU or another — configured with
+ * vxm_context_set_shard(ctx, p, n_shards, slab)) owns the blocks with
+ * floor(x / slab) mod n_shards == p, holds them in esdf[p] / tsdf[p] and passes
+ * its changed TSDF list updated[p].  Each lowering round the shards exchange
+ * their slab-boundary x-faces (peer copies) and agree on termination.  The union
+ * of esdf[] and of changed_out[] equals update_esdf over the union map,
+ * bit-for-bit. */
+vxm_status vxm_update_esdf_sharded(int n_shards, vxm_layer* const* esdf, vxm_layer* const* tsdf,
+                                   vxm_blocklist* const* updated, const vxm_esdf_config* cfg,
+                                   vxm_blocklist* const* changed_out);
+
 /* ---- fused frame update (replay pipeline step) ---------------------------- */
 /* One frame of the replay pipeline (pipeline.cpp:95-108: integrate the frame,
  * then update the ESDF from its changed blocks) on a device-resident depth

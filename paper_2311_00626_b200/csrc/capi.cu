@@ -674,6 +674,38 @@ vxm_status vxm_update_frame_lidar_device(vxm_layer* T, vxm_layer* E, const float
   return frame_common(T, E, depth, w, h, pose, nullptr, li, icfg, ecfg, tout, eout);
 }
 
+vxm_status vxm_update_esdf_sharded(int P, vxm_layer* const* esdf, vxm_layer* const* tsdf,
+                                   vxm_blocklist* const* updated, const vxm_esdf_config* cfg,
+                                   vxm_blocklist* const* out) {
+  return guard([&] {
+    REQUIRE_ARG(P >= 1 && esdf && tsdf && updated && cfg && out, "null argument");
+    std::vector<Layer*> E(P), T(P);
+    std::vector<BlockList*> U(P), O(P);
+    int slab = 0;
+    for (int p = 0; p < P; ++p) {
+      REQUIRE_ARG(esdf[p] && tsdf[p] && updated[p] && out[p], "null argument");
+      REQUIRE_ARG(esdf[p]->type == VXM_LAYER_ESDF && tsdf[p]->type == VXM_LAYER_TSDF,
+                  "update_esdf: expects (ESDF layer, TSDF layer)");
+      Context* ctx = esdf[p]->ctx;
+      REQUIRE_ARG(tsdf[p]->ctx == ctx, "update_esdf_sharded: shard layers on different contexts");
+      REQUIRE_ARG(ctx->world == P && ctx->rank == p,
+                  "update_esdf_sharded: shard p's context must be set_shard(p, n_shards, slab)");
+      if (p == 0) slab = ctx->slab;
+      REQUIRE_ARG(ctx->slab == slab, "update_esdf_sharded: shards disagree on the slab width");
+      for (int q = 0; q < p; ++q)
+        REQUIRE_ARG(esdf[q]->ctx != ctx, "update_esdf_sharded: one context per shard");
+      if (esdf[p]->vs != tsdf[p]->vs || esdf[p]->vs != esdf[0]->vs)
+        throw Error(VXM_ERR_INVALID_ARGUMENT, "update_esdf: source and ESDF layer voxel sizes differ");
+      ensure_sorted_unique(updated[p]);
+      E[p] = esdf[p];
+      T[p] = tsdf[p];
+      U[p] = updated[p];
+      O[p] = out[p];
+    }
+    run_update_esdf_sharded(P, E.data(), T.data(), U.data(), *cfg, slab, O.data());
+  });
+}
+
 vxm_status vxm_update_esdf_list(vxm_layer* E, vxm_layer* T, vxm_blocklist* updated,
                                 const vxm_esdf_config* cfg, vxm_blocklist* out) {
   return guard([&] {

@@ -185,6 +185,9 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
                      BlockList* changed_out);
 void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
                  BlockList* changed_out);
+// shard.cu — one update_esdf over a block-sharded map (P shards, one context each)
+void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
+                             const vxm_esdf_config& cfg, int slab, BlockList** out);
 void esdf_finish(Layer* E, BlockList* changed_out);
 void run_mark_sites(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
                     EsdfState* st, std::vector<vxm_grid_index>* changed);

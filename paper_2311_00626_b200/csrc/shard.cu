@@ -1,0 +1,588 @@
+// Block-sharded ESDF update.
+//
+// Shard p of P owns the blocks with floor(x / slab) mod P == p (the same
+// ownership the candidate pass uses, view.cu), each shard in its own context
+// (same GPU or another one).  update_esdf over the union map
+// (esdf/integrator.cpp:365-413) decomposes as follows:
+//   * effective set / mark_sites: voxel-local.  Every shard runs the mark phase
+//     with the UNION of the shards' updated lists; filtering by its own TSDF hash
+//     keeps exactly its share of the reference's effective set.
+//   * "if anything to update, reset + lower from all blocks": a global OR.
+//   * lowering rounds (:488-565): sweeps are block-local; y and z pairs never
+//     cross an x-slab boundary; an x pair (lo, hi) across a boundary is computed
+//     by BOTH owners from the same inputs — the two post-sweep, pre-pair faces,
+//     exchanged between the neighbours every round with the blocks' dirty bits
+//     (pair existence, :530-538) — and each keeps its own side, so the result
+//     is bit-identical to exchange_pair (:144-168); the next dirty list is
+//     local; termination is a global sum.
+// Rounds are driven from the host: sweep kernel -> face pack -> peer copies
+// (cudaMemcpyPeerAsync; NCCL send/recv for one process per GPU) -> border
+// kernel (x pairs incl. the cross pairs, grid barrier, y, barrier, z).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "esdf_host.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace vxm {
+
+struct ShardRound {
+  uint32_t r, ep;         // round (1-based), its epoch (base + r)
+  uint32_t cur;           // pool holding the field before this update
+  int lowered;            // the update lowered (the new field is in pool cur ^ 1)
+  uint32_t n_blocks, n_dirty;
+  uint32_t* ctr;          // [2] work counters, zeroed by the host per launch
+  int rank, world, slab;
+  const uint64_t* bnd_keys;  // this shard's boundary blocks, sorted by key
+  const int32_t* bnd_slots;
+  uint32_t n_bnd;
+  uint64_t* snd_keys;
+  uint8_t* snd_dirty;
+  uint32_t* snd_faces;       // [n_bnd][2 faces (x = 0, x = 7)][64][3 words]
+  const uint64_t* rcv_keys[2];  // [0] from the -x neighbour, [1] from the +x neighbour
+  const uint8_t* rcv_dirty[2];
+  const uint32_t* rcv_faces[2];
+  uint32_t n_rcv[2];
+};
+
+__device__ inline int shard_owner(int32_t x, int world, int slab) {
+  const int32_t q = x >= 0 ? x / slab : -((-x + slab - 1) / slab);
+  return ((q % world) + world) % world;
+}
+
+// ---- sweeps of round r (round 1: reset_parented + sweep of every block) ------
+__global__ void __launch_bounds__(kL3Threads, 2) k_shard_sweep(LowerArgs a, ShardRound sr) {
+  __shared__ GroupSmem s_grp[kL3Groups];
+  const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
+  const int bar = 1 + g;
+  GroupSmem& G = s_grp[g];
+  const bool r1 = sr.r == 1;
+  uint32_t* const pcur = a.pool[sr.cur];
+  uint32_t* const work = a.pool[sr.cur ^ 1u];
+  const int32_t* dirty = a.list[sr.r & 1u];
+  const uint32_t n = r1 ? sr.n_blocks : sr.n_dirty;
+  const Limits lim = a.lim;
+  while (true) {
+    if (t == 0) G.bcast = atomicAdd(sr.ctr, 1u);
+    group_sync(bar);
+    const uint32_t i = G.bcast;
+    if (i >= n) break;
+    const int32_t s = r1 ? int32_t(i) : __ldcg(dirty + i);
+    if (t == 0) {
+      unsigned long long m0 = ~0ull, m1 = ~0ull, m2 = ~0ull;
+      if (!r1) {  // lines through voxels changed by the last borders
+        m0 = atomicExch(a.line_mask + 3 * size_t(s), 0ull);
+        m1 = atomicExch(a.line_mask + 3 * size_t(s) + 1, 0ull);
+        m2 = atomicExch(a.line_mask + 3 * size_t(s) + 2, 0ull);
+      }
+      G.mask[0][0] = m0;
+      G.mask[1][0] = m1;
+      G.mask[2][0] = m2;
+      G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
+    }
+    RawBlock rb;
+    bool any_site, fast;
+    load_raw3(rb, (r1 ? pcur : work) + size_t(s) * 1536, t, bar, lim, r1, &any_site, &fast);
+    if (!any_site) {
+      raw_store(rb, work + size_t(s) * 1536, t);
+    } else {
+      stage_block3(G, rb, t, bar, lim, fast);
+      const bool changed = sweep_block3(G, t, bar, lim);
+      if (r1 || changed) store_block3(G, work + size_t(s) * 1536, t);
+    }
+    group_sync(bar);
+  }
+}
+
+// ---- boundary faces + dirty bits, after the sweeps -----------------------------
+__global__ void k_shard_pack(LowerArgs a, ShardRound sr) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t* work = a.pool[sr.cur ^ 1u];
+  const uint32_t cp = sr.r & 1u;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < sr.n_bnd; k += nwarps) {
+    const int32_t s = sr.bnd_slots[k];
+    if (lane == 0) {
+      sr.snd_keys[k] = sr.bnd_keys[k];
+      sr.snd_dirty[k] = uint8_t(sr.r == 1 || __ldcg(a.stamp_dirty[cp] + s) == sr.ep);
+    }
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int q = lane + 32 * j, lin = (f ? 7 : 0) + 8 * (q & 7) + 64 * (q >> 3);
+        const uint32_t* src = work + size_t(s) * 1536 + lin * 3;
+        uint32_t* dst = sr.snd_faces + ((size_t(k) * 2 + f) * 64 + q) * 3;
+        dst[0] = __ldcg(src);
+        dst[1] = __ldcg(src + 1);
+        dst[2] = __ldcg(src + 2);
+      }
+  }
+}
+
+__device__ inline int64_t find_key(const uint64_t* keys, uint32_t n, uint64_t k) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (keys[mid] < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < n && keys[lo] == k) ? int64_t(lo) : -1;
+}
+
+// Marks `who` changed by a border pair: line masks for its next sweep, next
+// round's dirty list (esdf/integrator.cpp:552-556).
+__device__ inline void mark_changed(const LowerArgs& a, uint32_t r, uint32_t ep_next, int np,
+                                    int32_t who, unsigned long long m[3], int lane) {
+  const unsigned long long r0 = warp_or64(m[0]), r1 = warp_or64(m[1]), r2 = warp_or64(m[2]);
+  if (lane == 0) {
+    atomicOr(a.line_mask + 3 * size_t(who), r0);
+    atomicOr(a.line_mask + 3 * size_t(who) + 1, r1);
+    atomicOr(a.line_mask + 3 * size_t(who) + 2, r2);
+    if (atomicMax(a.stamp_dirty[np] + who, ep_next) < ep_next) {
+      const uint32_t slot = atomicAdd(a.count + (r + 1u) % 3u, 1u);
+      a.list[np][slot] = who;
+    }
+  }
+}
+
+// ---- border phase of round r: x (local + cross-shard), y, z ---------------------
+__global__ void __launch_bounds__(kL3Threads, 2) k_shard_border(LowerArgs a, ShardRound sr) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const uint32_t wid = (blockIdx.x * kL3Threads + threadIdx.x) >> 5;
+  const uint32_t nwarps = gridDim.x * (kL3Threads >> 5);
+  const uint32_t r = sr.r, ep = sr.ep, ep_next = ep + 1;
+  const int cp = int(r & 1u), np = cp ^ 1;
+  const bool r1 = r == 1;
+  uint32_t* const work = a.pool[sr.cur ^ 1u];
+  const int32_t* dirty = a.list[cp];
+  const uint32_t n_dirty = r1 ? sr.n_blocks : sr.n_dirty;
+  const uint32_t sides = r1 ? 1u : 2u;
+  const uint32_t per_axis = sides * n_dirty;
+  const Limits lim = a.lim;
+  uint32_t n_pairs = 0;
+  for (int axis = 0; axis < 3; ++axis) {
+    if (axis > 0) grid.sync();
+    const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
+    // pairs with both blocks on this shard (k_lower3's items, phased)
+    for (uint32_t w = wid; w < per_axis; w += nwarps) {
+      const uint32_t i = r1 ? w : w >> 1;
+      const int side = r1 ? 0 : int(w & 1u);
+      const int32_t d = r1 ? int32_t(i) : __ldcg(dirty + i);
+      int32_t lo, hi;
+      if (side == 0) {
+        hi = __ldg(a.nbr + size_t(d) * 6 + 2 * axis);
+        lo = d;
+        if (hi < 0) continue;
+      } else {
+        lo = __ldg(a.nbr + size_t(d) * 6 + 2 * axis + 1);
+        hi = d;
+        if (lo < 0) continue;
+        if (__ldcg(a.stamp_dirty[cp] + lo) == ep) continue;  // lo's side-0 item has it
+      }
+      bool ac = false, bc = false;
+      unsigned long long mlo[3] = {0, 0, 0}, mhi[3] = {0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
+        int ax, ay, az, bx, by, bz;
+        if (axis == 0) { ax = 7; ay = i0; az = j0; bx = 0; by = i0; bz = j0; }
+        else if (axis == 1) { ax = i0; ay = 7; az = j0; bx = i0; by = 0; bz = j0; }
+        else { ax = i0; ay = j0; az = 7; bx = i0; by = j0; bz = 0; }
+        const int la = ax + 8 * ay + 64 * az, lb = bx + 8 * by + 64 * bz;
+        EV va = load_voxel(work, lo, la), vb = load_voxel(work, hi, lb);
+        const bool cb = relax(vb, va, dx, dy, dz, lim);     // exchange_pair :158
+        const bool ca = relax(va, vb, -dx, -dy, -dz, lim);  // :159
+        if (cb) {
+          store_voxel(work, hi, lb, vb);
+          line_bits(bx, by, bz, mhi);
+        }
+        if (ca) {
+          store_voxel(work, lo, la, va);
+          line_bits(ax, ay, az, mlo);
+        }
+        ac |= ca;
+        bc |= cb;
+      }
+      ac = __any_sync(0xffffffffu, ac);
+      bc = __any_sync(0xffffffffu, bc);
+      ++n_pairs;
+      if (ac) mark_changed(a, r, ep_next, np, lo, mlo, lane);
+      if (bc) mark_changed(a, r, ep_next, np, hi, mhi, lane);
+    }
+    if (axis != 0) continue;
+    // x pairs across a slab boundary: this shard's side of exchange_pair on the
+    // two pre-pair faces (ours from the pool — only this pair touches it — and
+    // the neighbour's from the exchanged snapshot)
+    for (uint32_t w = wid; w < 2u * sr.n_bnd; w += nwarps) {
+      const uint32_t k = w >> 1;
+      const int s = (w & 1u) ? -1 : 1;
+      const uint64_t bkey = sr.bnd_keys[k];
+      if (shard_owner(key_x(bkey) + s, sr.world, sr.slab) == sr.rank) continue;
+      const int side = s > 0 ? 1 : 0;
+      const int64_t e = find_key(sr.rcv_keys[side], sr.n_rcv[side], key_shift(bkey, 0, s));
+      if (e < 0) continue;  // no neighbour block: no pair
+      const int32_t b = sr.bnd_slots[k];
+      const bool b_dirty = r1 || __ldcg(a.stamp_dirty[cp] + b) == ep;
+      if (!b_dirty && !sr.rcv_dirty[side][e]) continue;  // pair not in this round's set
+      // the neighbour's face towards us: its x = 0 face when it is hi, x = 7 when lo
+      const uint32_t* rf = sr.rcv_faces[side] + (size_t(e) * 2 + (s > 0 ? 0 : 1)) * 64 * 3;
+      bool chg = false;
+      unsigned long long m[3] = {0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int q = lane + 32 * j, y = q & 7, z = q >> 3;
+        const EV vr = ev_unpack(__ldcg(rf + 3 * q), __ldcg(rf + 3 * q + 1), __ldcg(rf + 3 * q + 2));
+        if (s > 0) {  // (lo = b, hi = neighbour)
+          const int la = 7 + 8 * y + 64 * z;
+          EV va = load_voxel(work, b, la), vb = vr;
+          relax(vb, va, 1, 0, 0, lim);
+          if (relax(va, vb, -1, 0, 0, lim)) {
+            store_voxel(work, b, la, va);
+            line_bits(7, y, z, m);
+            chg = true;
+          }
+        } else {  // (lo = neighbour, hi = b)
+          const int lb = 8 * y + 64 * z;
+          EV va = vr, vb = load_voxel(work, b, lb);
+          if (relax(vb, va, 1, 0, 0, lim)) {
+            store_voxel(work, b, lb, vb);
+            line_bits(0, y, z, m);
+            chg = true;
+          }
+        }
+      }
+      chg = __any_sync(0xffffffffu, chg);
+      ++n_pairs;
+      if (chg) mark_changed(a, r, ep_next, np, b, m, lane);
+    }
+  }
+  if (lane == 0 && n_pairs) atomicAdd(&a.status->sum_pairs, n_pairs);
+}
+
+// ---- changed set of the update (esdf/integrator.cpp:403-411) -------------------
+__global__ void k_shard_changed(LowerArgs a, ShardRound sr) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t* p0 = a.pool[sr.cur];
+  const uint32_t* p1 = a.pool[sr.cur ^ 1u];
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < sr.n_blocks; k += nwarps) {
+    const int32_t s = a.sorted_slots[k];
+    bool ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
+    if (!ch && sr.lowered) {
+      const uint4* q0 = reinterpret_cast<const uint4*>(p0 + size_t(s) * 1536);
+      const uint4* q1 = reinterpret_cast<const uint4*>(p1 + size_t(s) * 1536);
+      bool diff = false;
+      for (int q = lane; q < 384; q += 32) {
+        const uint4 x = __ldcg(q0 + q), y = __ldcg(q1 + q);
+        diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+      }
+      ch = __any_sync(0xffffffffu, diff);
+    }
+    if (lane == 0) a.out_flags[k] = uint8_t(ch);
+  }
+}
+
+__global__ void k_shard_meta(LayerMeta* meta, uint32_t round_epoch, uint32_t cur) {
+  meta->round_epoch = round_epoch;
+  meta->cur = cur;
+}
+
+__global__ void k_boundary_flags(const uint64_t* keys, const uint32_t* n_ptr, int slab,
+                                 uint8_t* flags) {
+  const uint32_t n = *n_ptr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t x = key_x(keys[i]);
+    const int32_t m = ((x % slab) + slab) % slab;
+    flags[i] = uint8_t(m == 0 || m == slab - 1);
+  }
+}
+
+// ---- host driver -------------------------------------------------------------------
+namespace {
+
+struct ShardState {
+  Layer* E;
+  Layer* T;
+  Context* ctx;
+  BlockList uni;              // union of the updated lists (sorted, unique)
+  EsdfScratch s;
+  uint32_t epoch = 0, n7 = 0, n_all_cap = 0, base = 0, cur = 0, n_blocks = 0;
+  DevBuf ctr, bnd_keys, bnd_slots, bnd_flags, bnd_n, cub_tmp;
+  uint32_t n_bnd = 0;
+  DevBuf snd_keys, snd_dirty, snd_faces;
+  DevBuf rcv_keys[2], rcv_dirty[2], rcv_faces[2];
+  uint32_t n_rcv[2] = {0, 0};
+  uint32_t n_dirty = 0;
+  LowerArgs la{};
+};
+
+void use(Context* c) { VXM_CUDA(cudaSetDevice(c->device)); }
+
+void sync_all(std::vector<ShardState>& sh) {
+  for (auto& x : sh) {
+    use(x.ctx);
+    VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
+  }
+}
+
+void copy_to(const ShardState& dst, void* d, const ShardState& src, const void* s, size_t bytes) {
+  if (!bytes) return;
+  use(dst.ctx);
+  if (dst.ctx->device == src.ctx->device)
+    VXM_CUDA(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, dst.ctx->stream));
+  else
+    VXM_CUDA(cudaMemcpyPeerAsync(d, dst.ctx->device, s, src.ctx->device, bytes, dst.ctx->stream));
+}
+
+ShardRound round_args(ShardState& x, uint32_t r, int rank, int world, int slab) {
+  ShardRound sr{};
+  sr.r = r;
+  sr.ep = x.base + r;
+  sr.cur = x.cur;
+  sr.n_blocks = x.n_blocks;
+  sr.n_dirty = x.n_dirty;
+  sr.ctr = x.ctr.as<uint32_t>();
+  sr.rank = rank;
+  sr.world = world;
+  sr.slab = slab;
+  sr.bnd_keys = x.bnd_keys.as<uint64_t>();
+  sr.bnd_slots = x.bnd_slots.as<int32_t>();
+  sr.n_bnd = x.n_bnd;
+  sr.snd_keys = x.snd_keys.as<uint64_t>();
+  sr.snd_dirty = x.snd_dirty.as<uint8_t>();
+  sr.snd_faces = x.snd_faces.as<uint32_t>();
+  for (int i = 0; i < 2; ++i) {
+    sr.rcv_keys[i] = x.rcv_keys[i].as<uint64_t>();
+    sr.rcv_dirty[i] = x.rcv_dirty[i].as<uint8_t>();
+    sr.rcv_faces[i] = x.rcv_faces[i].as<uint32_t>();
+    sr.n_rcv[i] = x.n_rcv[i];
+  }
+  return sr;
+}
+
+int grid_of(const void* kernel, Context* c) {
+  int bps = 0;
+  VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, kL3Threads, 0));
+  return std::max(1, std::min(bps, 4)) * c->sm_count;
+}
+
+}  // namespace
+
+void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
+                             const vxm_esdf_config& cfg, int slab, BlockList** out) {
+  std::vector<ShardState> sh(P);
+  for (int p = 0; p < P; ++p) {
+    sh[p].E = E[p];
+    sh[p].T = T[p];
+    sh[p].ctx = E[p]->ctx;
+  }
+  // 1. union of the updated lists (every shard marks against all of them)
+  sync_all(sh);
+  std::vector<uint32_t> n_upd(P);
+  uint64_t total = 0;
+  for (int p = 0; p < P; ++p) {
+    use(updated[p]->ctx);
+    VXM_CUDA(cudaMemcpy(&n_upd[p], updated[p]->d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    total += n_upd[p];
+  }
+  if (total == 0) {  // esdf/integrator.cpp:371-378
+    for (int p = 0; p < P; ++p) out[p]->assign_host(nullptr, 0);
+    return;
+  }
+  for (int q = 0; q < P; ++q) {
+    ShardState& x = sh[q];
+    use(x.ctx);
+    x.uni.ctx = x.ctx;
+    x.uni.ensure(uint32_t(total));
+    uint64_t off = 0;
+    for (int p = 0; p < P; ++p) {
+      ShardState src{};
+      src.ctx = updated[p]->ctx;
+      copy_to(x, x.uni.keys.as<uint64_t>() + off, src, updated[p]->keys.p, sizeof(uint64_t) * n_upd[p]);
+      off += n_upd[p];
+    }
+    const uint32_t t32 = uint32_t(total);
+    VXM_CUDA(cudaMemcpyAsync(x.uni.d_count, &t32, sizeof t32, cudaMemcpyHostToDevice, x.ctx->stream));
+    x.uni.count_hint = t32;
+    x.uni.host_valid = false;
+    sort_unique_keys(x.ctx, &x.uni);
+    x.uni.sorted_unique = true;
+  }
+  // 2. mark phase on every shard; global "anything to update"
+  bool any_update = false;
+  for (auto& x : sh) {
+    use(x.ctx);
+    Context* ctx = x.ctx;
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->reset_status();
+    x.epoch = ++ctx->call_epoch;
+    x.n7 = 7u * std::max<uint32_t>(x.uni.count_hint, 1);
+    x.E->ensure_capacity(std::min<uint64_t>(uint64_t(x.E->num_blocks) + x.n7, x.E->max_blocks));
+    x.n_all_cap = x.E->capacity;
+    x.s = esdf_scratch(ctx, x.uni.count_hint, x.n_all_cap);
+    esdf_mark_phase(x.E, x.T, &x.uni, cfg, x.s, x.epoch);
+    x.E->stage_meta();
+    ctx->sync_status();
+    x.E->adopt_meta();
+    const DevStatus& st = *ctx->h_status;
+    if (st.capacity_error || st.pool_overflow)
+      throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+    any_update |= st.any_update != 0;
+    LayerMeta m;
+    VXM_CUDA(cudaMemcpy(&m, x.E->meta, sizeof m, cudaMemcpyDeviceToHost));
+    x.base = m.round_epoch;
+    x.cur = m.cur;
+    x.n_blocks = m.num_blocks;
+    x.la = lower_args(x.E, cfg);
+    x.la.full = 1;
+    x.la.sorted_slots = x.E->sorted_slots[x.E->sorted_parity];
+    x.la.stamp_new = x.E->stamp_new;
+    x.la.stamp_mark = x.E->stamp_mark;
+    x.la.call_epoch = x.epoch;
+    x.la.out_flags = x.s.flags;
+  }
+  uint32_t rounds = 0;
+  if (any_update) {
+    // boundary blocks of every shard (sorted), exchange buffers
+    for (int p = 0; p < P; ++p) {
+      ShardState& x = sh[p];
+      use(x.ctx);
+      cudaStream_t st = x.ctx->stream;
+      const uint32_t n = std::max<uint32_t>(x.n_blocks, 1);
+      x.bnd_flags.ensure(n);
+      x.bnd_keys.ensure(sizeof(uint64_t) * n);
+      x.bnd_slots.ensure(sizeof(int32_t) * n);
+      x.bnd_n.ensure(2 * sizeof(uint32_t));
+      x.ctr.ensure(4 * sizeof(uint32_t));
+      const uint64_t* keys = x.E->sorted_keys[x.E->sorted_parity];
+      const int32_t* slots = x.E->sorted_slots[x.E->sorted_parity];
+      k_boundary_flags<<<grid_for(x.ctx, n), 256, 0, st>>>(keys, &x.E->meta->num_blocks, slab,
+                                                             x.bnd_flags.as<uint8_t>());
+      size_t b1 = 0, b2 = 0;
+      cub::DeviceSelect::Flagged(nullptr, b1, keys, x.bnd_flags.as<uint8_t>(), x.bnd_keys.as<uint64_t>(),
+                                 x.bnd_n.as<uint32_t>(), int(x.n_blocks), st);
+      cub::DeviceSelect::Flagged(nullptr, b2, slots, x.bnd_flags.as<uint8_t>(), x.bnd_slots.as<int32_t>(),
+                                 x.bnd_n.as<uint32_t>() + 1, int(x.n_blocks), st);
+      x.cub_tmp.ensure(std::max(b1, b2));
+      VXM_CUDA(cub::DeviceSelect::Flagged(x.cub_tmp.p, b1, keys, x.bnd_flags.as<uint8_t>(),
+                                          x.bnd_keys.as<uint64_t>(), x.bnd_n.as<uint32_t>(),
+                                          int(x.n_blocks), st));
+      VXM_CUDA(cub::DeviceSelect::Flagged(x.cub_tmp.p, b2, slots, x.bnd_flags.as<uint8_t>(),
+                                          x.bnd_slots.as<int32_t>(), x.bnd_n.as<uint32_t>() + 1,
+                                          int(x.n_blocks), st));
+      x.ctx->count_launch(3);
+      VXM_CUDA(cudaMemcpyAsync(&x.n_bnd, x.bnd_n.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      VXM_CUDA(cudaStreamSynchronize(st));
+      const uint32_t nb = std::max<uint32_t>(x.n_bnd, 1);
+      x.snd_keys.ensure(sizeof(uint64_t) * nb);
+      x.snd_dirty.ensure(nb);
+      x.snd_faces.ensure(sizeof(uint32_t) * 384 * nb);
+    }
+    for (int p = 0; p < P; ++p) {  // [0]: from the -x neighbour, [1]: from the +x one
+      ShardState& x = sh[p];
+      const int nbr[2] = {(p - 1 + P) % P, (p + 1) % P};
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t nb = std::max<uint32_t>(sh[nbr[i]].n_bnd, 1);
+        use(x.ctx);
+        x.rcv_keys[i].ensure(sizeof(uint64_t) * nb);
+        x.rcv_dirty[i].ensure(nb);
+        x.rcv_faces[i].ensure(sizeof(uint32_t) * 384 * nb);
+        x.n_rcv[i] = sh[nbr[i]].n_bnd;
+      }
+    }
+    const int g_sweep = grid_of((const void*)k_shard_sweep, sh[0].ctx);
+    const int g_border = grid_of((const void*)k_shard_border, sh[0].ctx);
+    for (auto& x : sh) x.n_dirty = x.n_blocks;
+    uint32_t r = 0;
+    while (true) {
+      ++r;
+      for (int p = 0; p < P; ++p) {
+        ShardState& x = sh[p];
+        use(x.ctx);
+        cudaStream_t st = x.ctx->stream;
+        VXM_CUDA(cudaMemsetAsync(x.ctr.p, 0, 4 * sizeof(uint32_t), st));
+        ShardRound sr = round_args(x, r, p, P, slab);
+        k_shard_sweep<<<g_sweep, kL3Threads, 0, st>>>(x.la, sr);
+        k_shard_pack<<<grid_for(x.ctx, uint64_t(x.n_bnd) * 32), 256, 0, st>>>(x.la, sr);
+        x.ctx->count_launch(2);
+        check_launch(x.ctx, "k_shard_sweep");
+      }
+      sync_all(sh);
+      for (int p = 0; p < P; ++p) {  // peer copies of the boundary snapshots
+        const ShardState& src = sh[p];
+        const int to[2] = {(p + 1) % P, (p - 1 + P) % P};  // our +x side is their -x side
+        for (int i = 0; i < 2; ++i) {
+          ShardState& dst = sh[to[i]];
+          const int slot = i == 0 ? 0 : 1;
+          copy_to(dst, dst.rcv_keys[slot].p, src, src.snd_keys.p, sizeof(uint64_t) * src.n_bnd);
+          copy_to(dst, dst.rcv_dirty[slot].p, src, src.snd_dirty.p, src.n_bnd);
+          copy_to(dst, dst.rcv_faces[slot].p, src, src.snd_faces.p, sizeof(uint32_t) * 384 * src.n_bnd);
+        }
+      }
+      for (int p = 0; p < P; ++p) {
+        ShardState& x = sh[p];
+        use(x.ctx);
+        cudaStream_t st = x.ctx->stream;
+        VXM_CUDA(cudaMemsetAsync(x.la.count + (r + 1u) % 3u, 0, sizeof(uint32_t), st));
+        ShardRound sr = round_args(x, r, p, P, slab);
+        void* args[] = {&x.la, &sr};
+        VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_shard_border, dim3(g_border),
+                                             dim3(kL3Threads), args, 0, st));
+        x.ctx->count_launch();
+      }
+      uint64_t next = 0;
+      for (int p = 0; p < P; ++p) {
+        ShardState& x = sh[p];
+        use(x.ctx);
+        VXM_CUDA(cudaMemcpyAsync(&x.n_dirty, x.la.count + (r + 1u) % 3u, sizeof(uint32_t),
+                                 cudaMemcpyDeviceToHost, x.ctx->stream));
+        VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
+        next += x.n_dirty;
+      }
+      if (next == 0) break;  // while (!dirty.empty()) — esdf/integrator.cpp:506
+    }
+    rounds = r;
+    for (auto& x : sh) {
+      use(x.ctx);
+      ShardRound sr = round_args(x, r, 0, P, slab);
+      sr.lowered = 1;
+      k_shard_changed<<<grid_for(x.ctx, uint64_t(x.n_blocks) * 32), 256, 0, x.ctx->stream>>>(x.la, sr);
+      k_shard_meta<<<1, 1, 0, x.ctx->stream>>>(x.E->meta, x.base + r + 2, x.cur ^ 1u);
+      x.ctx->count_launch(2);
+    }
+  } else {  // nothing to lower anywhere: changed = new or marked blocks
+    for (auto& x : sh) {
+      use(x.ctx);
+      ShardRound sr = round_args(x, 0, 0, P, slab);
+      sr.lowered = 0;
+      k_shard_changed<<<grid_for(x.ctx, uint64_t(x.n_blocks) * 32), 256, 0, x.ctx->stream>>>(x.la, sr);
+      x.ctx->count_launch();
+    }
+  }
+  for (int p = 0; p < P; ++p) {
+    ShardState& x = sh[p];
+    use(x.ctx);
+    out[p]->ctx = x.ctx;
+    out[p]->ensure(x.n_all_cap);
+    launch_compact_keys(x.ctx, x.E->sorted_keys[x.E->sorted_parity], x.s.flags, &x.E->meta->num_blocks,
+                        x.n_all_cap, out[p]->keys.as<uint64_t>(), out[p]->d_count, nullptr,
+                        "k_compact_esdf");
+    out[p]->host_valid = false;
+    out[p]->count_hint = x.n_all_cap;
+    out[p]->sorted_unique = true;
+    x.E->stage_meta();
+    x.ctx->sync_status();
+    x.E->adopt_meta();
+    vxm_stats& w = x.ctx->stats;
+    w.esdf_calls += 1;
+    w.esdf_blocks += x.n_blocks;
+    w.lower_rounds += rounds;
+  }
+}
+
+}  // namespace vxm

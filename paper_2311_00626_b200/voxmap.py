@@ -413,6 +413,26 @@ def update_esdf(esdf: EsdfLayer, tsdf: TsdfLayer, updated, cfg=None, out: BlockL
     return out.numpy()
 
 
+def update_esdf_sharded(esdf_shards, tsdf_shards, updated, cfg, out=None):
+    """update_esdf over a block-sharded map (vxm_update_esdf_sharded): shard p's
+    context must be set_shard(p, P, slab); `updated[p]` is shard p's changed list
+    (BlockList or (N,3) array).  Returns the per-shard changed lists."""
+    P = len(esdf_shards)
+    lists = []
+    for p in range(P):
+        u = updated[p]
+        if not isinstance(u, BlockList):
+            bl = BlockList(esdf_shards[p].ctx)
+            bl.assign(u)
+            u = bl
+        lists.append(u)
+    out = out or [BlockList(esdf_shards[p].ctx) for p in range(P)]
+    arr = lambda xs: (C.c_void_p * P)(*[x.h.value for x in xs])  # noqa: E731
+    check(lib().vxm_update_esdf_sharded(C.c_int(P), arr(esdf_shards), arr(tsdf_shards), arr(lists),
+                                        C.byref(cfg), arr(out)))
+    return [o.numpy() for o in out]
+
+
 def update_esdf_device(esdf: EsdfLayer, tsdf: TsdfLayer, updated: BlockList, cfg,
                        out: BlockList) -> BlockList:
     """Device-resident update_esdf: consumes and produces device block lists."""
