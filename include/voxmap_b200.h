@@ -264,6 +264,30 @@ vxm_status vxm_update_esdf_sharded(int n_shards, vxm_layer* const* esdf, vxm_lay
                                    vxm_blocklist* const* updated, const vxm_esdf_config* cfg,
                                    vxm_blocklist* const* changed_out);
 
+/* The same update as steps, for one process per shard (the caller moves the
+ * exchange buffers between neighbours and reduces the flags / counts, e.g. with
+ * NCCL through torch.distributed — paper_2311_00626_b200/dist.py):
+ *   begin(union of all shards' updated lists) -> local any_update;   OR-reduce
+ *   if the OR is set: plan -> n_boundary;   all-gather n_boundary
+ *     exchange_buffers(n of the -x neighbour (rank-1), n of the +x one (rank+1))
+ *     for round = 1, 2, ...: sweep(round); send `send` to both neighbours, receive
+ *       the -x neighbour's into recv_left and the +x one's into recv_right;
+ *       border(round) -> next_dirty;  sum-reduce; stop at 0
+ *   finish(lowered = the OR) -> changed blocks; frees the handle. */
+typedef struct vxm_shard_update vxm_shard_update;
+vxm_status vxm_shard_update_begin(vxm_layer* esdf, vxm_layer* tsdf, vxm_blocklist* updated_union,
+                                  const vxm_esdf_config* cfg, vxm_shard_update** out,
+                                  int* local_any_update);
+vxm_status vxm_shard_update_plan(vxm_shard_update* su, uint32_t* n_boundary);
+vxm_status vxm_shard_update_exchange_buffers(vxm_shard_update* su, uint32_t n_left, uint32_t n_right,
+                                             void** send, uint64_t* send_bytes, void** recv_left,
+                                             uint64_t* recv_left_bytes, void** recv_right,
+                                             uint64_t* recv_right_bytes);
+vxm_status vxm_shard_update_sweep(vxm_shard_update* su, uint32_t round);
+vxm_status vxm_shard_update_border(vxm_shard_update* su, uint32_t round, uint32_t* next_dirty);
+vxm_status vxm_shard_update_finish(vxm_shard_update* su, int lowered, vxm_blocklist* changed_out);
+void vxm_shard_update_destroy(vxm_shard_update* su);
+
 /* ---- fused frame update (replay pipeline step) ---------------------------- */
 /* One frame of the replay pipeline (pipeline.cpp:95-108: integrate the frame,
  * then update the ESDF from its changed blocks) on a device-resident depth

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "runtime.cuh"
+#include "shard.cuh"
 
 using namespace vxm;
 
@@ -705,6 +706,92 @@ vxm_status vxm_update_esdf_sharded(int P, vxm_layer* const* esdf, vxm_layer* con
     run_update_esdf_sharded(P, E.data(), T.data(), U.data(), *cfg, slab, O.data());
   });
 }
+
+struct vxm_shard_update {
+  vxm::ShardUpdate x;
+};
+
+vxm_status vxm_shard_update_begin(vxm_layer* E, vxm_layer* T, vxm_blocklist* uni,
+                                  const vxm_esdf_config* cfg, vxm_shard_update** out, int* any) {
+  vxm_shard_update* su = nullptr;
+  const vxm_status st = guard([&] {
+    REQUIRE_ARG(E && T && uni && cfg && out && any, "null argument");
+    REQUIRE_ARG(E->type == VXM_LAYER_ESDF && T->type == VXM_LAYER_TSDF,
+                "update_esdf: expects (ESDF layer, TSDF layer)");
+    REQUIRE_ARG(E->ctx == T->ctx && uni->ctx == E->ctx, "shard update: objects on different contexts");
+    if (E->vs != T->vs)
+      throw Error(VXM_ERR_INVALID_ARGUMENT, "update_esdf: source and ESDF layer voxel sizes differ");
+    su = new vxm_shard_update();
+    ShardUpdate& x = su->x;
+    x.E = E;
+    x.T = T;
+    x.ctx = E->ctx;
+    x.rank = x.ctx->rank;
+    x.world = x.ctx->world;
+    x.slab = x.ctx->slab;
+    ensure_sorted_unique(uni);
+    // a private copy of the union (the caller's list may be reused)
+    x.uni.ctx = x.ctx;
+    const uint32_t n = std::max<uint32_t>(uni->count_hint, 1);
+    x.uni.ensure(n);
+    VXM_CUDA(cudaMemcpyAsync(x.uni.keys.p, uni->keys.p, sizeof(uint64_t) * uni->count_hint,
+                             cudaMemcpyDeviceToDevice, x.ctx->stream));
+    VXM_CUDA(cudaMemcpyAsync(x.uni.d_count, uni->d_count, sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                             x.ctx->stream));
+    x.uni.count_hint = uni->count_hint;
+    x.uni.host_valid = false;
+    x.uni.sorted_unique = true;
+    shard_begin(x, *cfg);
+    *any = x.local_any ? 1 : 0;
+    *out = su;
+  });
+  if (st != VXM_OK) delete su;
+  return st;
+}
+vxm_status vxm_shard_update_plan(vxm_shard_update* su, uint32_t* n) {
+  return guard([&] {
+    REQUIRE_ARG(su && n, "null argument");
+    shard_plan(su->x);
+    *n = su->x.n_bnd;
+  });
+}
+vxm_status vxm_shard_update_exchange_buffers(vxm_shard_update* su, uint32_t n_left, uint32_t n_right,
+                                             void** send, uint64_t* send_bytes, void** recv_left,
+                                             uint64_t* recv_left_bytes, void** recv_right,
+                                             uint64_t* recv_right_bytes) {
+  return guard([&] {
+    REQUIRE_ARG(su && send && send_bytes && recv_left && recv_left_bytes && recv_right && recv_right_bytes,
+                "null argument");
+    shard_set_neighbours(su->x, n_left, n_right);
+    *send = su->x.snd.p;
+    *send_bytes = xbuf_bytes(su->x.n_bnd);
+    *recv_left = su->x.rcv[0].p;
+    *recv_left_bytes = xbuf_bytes(n_left);
+    *recv_right = su->x.rcv[1].p;
+    *recv_right_bytes = xbuf_bytes(n_right);
+  });
+}
+vxm_status vxm_shard_update_sweep(vxm_shard_update* su, uint32_t round) {
+  return guard([&] {
+    REQUIRE_ARG(su && round >= 1, "invalid argument");
+    shard_sweep(su->x, round);
+  });
+}
+vxm_status vxm_shard_update_border(vxm_shard_update* su, uint32_t round, uint32_t* next) {
+  return guard([&] {
+    REQUIRE_ARG(su && next && round >= 1, "invalid argument");
+    *next = shard_border(su->x, round);
+  });
+}
+vxm_status vxm_shard_update_finish(vxm_shard_update* su, int lowered, vxm_blocklist* out) {
+  const vxm_status st = guard([&] {
+    REQUIRE_ARG(su && out, "null argument");
+    shard_finish(su->x, lowered != 0, out);
+  });
+  delete su;
+  return st;
+}
+void vxm_shard_update_destroy(vxm_shard_update* su) { delete su; }
 
 vxm_status vxm_update_esdf_list(vxm_layer* E, vxm_layer* T, vxm_blocklist* updated,
                                 const vxm_esdf_config* cfg, vxm_blocklist* out) {

@@ -23,7 +23,7 @@
 #include <algorithm>
 #include <vector>
 
-#include "esdf_host.cuh"
+#include "shard.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -303,63 +303,39 @@ __global__ void k_boundary_flags(const uint64_t* keys, const uint32_t* n_ptr, in
 }
 
 // ---- host driver -------------------------------------------------------------------
+// One shard's state through one sharded update.  The exchange between rounds
+// is the caller's: in-process peer copies (run_update_esdf_sharded below) or
+// a collective library when each shard is its own process (the step C-ABI,
+// driven by paper_2311_00626_b200/dist.py over torch.distributed).
+//
 namespace {
-
-struct ShardState {
-  Layer* E;
-  Layer* T;
-  Context* ctx;
-  BlockList uni;              // union of the updated lists (sorted, unique)
-  EsdfScratch s;
-  uint32_t epoch = 0, n7 = 0, n_all_cap = 0, base = 0, cur = 0, n_blocks = 0;
-  DevBuf ctr, bnd_keys, bnd_slots, bnd_flags, bnd_n, cub_tmp;
-  uint32_t n_bnd = 0;
-  DevBuf snd_keys, snd_dirty, snd_faces;
-  DevBuf rcv_keys[2], rcv_dirty[2], rcv_faces[2];
-  uint32_t n_rcv[2] = {0, 0};
-  uint32_t n_dirty = 0;
-  LowerArgs la{};
-};
 
 void use(Context* c) { VXM_CUDA(cudaSetDevice(c->device)); }
 
-void sync_all(std::vector<ShardState>& sh) {
-  for (auto& x : sh) {
-    use(x.ctx);
-    VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
-  }
-}
-
-void copy_to(const ShardState& dst, void* d, const ShardState& src, const void* s, size_t bytes) {
-  if (!bytes) return;
-  use(dst.ctx);
-  if (dst.ctx->device == src.ctx->device)
-    VXM_CUDA(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, dst.ctx->stream));
-  else
-    VXM_CUDA(cudaMemcpyPeerAsync(d, dst.ctx->device, s, src.ctx->device, bytes, dst.ctx->stream));
-}
-
-ShardRound round_args(ShardState& x, uint32_t r, int rank, int world, int slab) {
+ShardRound round_args(ShardUpdate& x, uint32_t r) {
   ShardRound sr{};
   sr.r = r;
   sr.ep = x.base + r;
   sr.cur = x.cur;
+  sr.lowered = 1;
   sr.n_blocks = x.n_blocks;
   sr.n_dirty = x.n_dirty;
   sr.ctr = x.ctr.as<uint32_t>();
-  sr.rank = rank;
-  sr.world = world;
-  sr.slab = slab;
+  sr.rank = x.rank;
+  sr.world = x.world;
+  sr.slab = x.slab;
   sr.bnd_keys = x.bnd_keys.as<uint64_t>();
   sr.bnd_slots = x.bnd_slots.as<int32_t>();
   sr.n_bnd = x.n_bnd;
-  sr.snd_keys = x.snd_keys.as<uint64_t>();
-  sr.snd_dirty = x.snd_dirty.as<uint8_t>();
-  sr.snd_faces = x.snd_faces.as<uint32_t>();
+  const XView sv = xview(x.snd.p, x.n_bnd);
+  sr.snd_keys = sv.keys;
+  sr.snd_dirty = sv.dirty;
+  sr.snd_faces = sv.faces;
   for (int i = 0; i < 2; ++i) {
-    sr.rcv_keys[i] = x.rcv_keys[i].as<uint64_t>();
-    sr.rcv_dirty[i] = x.rcv_dirty[i].as<uint8_t>();
-    sr.rcv_faces[i] = x.rcv_faces[i].as<uint32_t>();
+    const XView rv = xview(x.rcv[i].p, x.n_rcv[i]);
+    sr.rcv_keys[i] = rv.keys;
+    sr.rcv_dirty[i] = rv.dirty;
+    sr.rcv_faces[i] = rv.faces;
     sr.n_rcv[i] = x.n_rcv[i];
   }
   return sr;
@@ -373,20 +349,177 @@ int grid_of(const void* kernel, Context* c) {
 
 }  // namespace
 
+// Mark phase against the union list (synchronous); x.local_any = this shard
+// has blocks to update / clear.
+void shard_begin(ShardUpdate& x, const vxm_esdf_config& cfg) {
+  Context* ctx = x.ctx;
+  use(ctx);
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->reset_status();
+  x.epoch = ++ctx->call_epoch;
+  const uint32_t n7 = 7u * std::max<uint32_t>(x.uni.count_hint, 1);
+  x.E->ensure_capacity(std::min<uint64_t>(uint64_t(x.E->num_blocks) + n7, x.E->max_blocks));
+  x.n_all_cap = x.E->capacity;
+  x.s = esdf_scratch(ctx, x.uni.count_hint, x.n_all_cap);
+  esdf_mark_phase(x.E, x.T, &x.uni, cfg, x.s, x.epoch);
+  x.E->stage_meta();
+  ctx->sync_status();
+  x.E->adopt_meta();
+  const DevStatus& st = *ctx->h_status;
+  if (st.capacity_error || st.pool_overflow)
+    throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
+  x.local_any = st.any_update != 0;
+  LayerMeta m;
+  VXM_CUDA(cudaMemcpy(&m, x.E->meta, sizeof m, cudaMemcpyDeviceToHost));
+  x.base = m.round_epoch;
+  x.cur = m.cur;
+  x.n_blocks = m.num_blocks;
+  x.n_dirty = x.n_blocks;
+  x.la = lower_args(x.E, cfg);
+  x.la.full = 1;
+  x.la.sorted_slots = x.E->sorted_slots[x.E->sorted_parity];
+  x.la.stamp_new = x.E->stamp_new;
+  x.la.stamp_mark = x.E->stamp_mark;
+  x.la.call_epoch = x.epoch;
+  x.la.out_flags = x.s.flags;
+}
+
+// Boundary blocks (x mod slab in {0, slab - 1}), sorted; the send buffer.
+void shard_plan(ShardUpdate& x) {
+  use(x.ctx);
+  cudaStream_t st = x.ctx->stream;
+  const uint32_t n = std::max<uint32_t>(x.n_blocks, 1);
+  x.bnd_flags.ensure(n);
+  x.bnd_keys.ensure(sizeof(uint64_t) * n);
+  x.bnd_slots.ensure(sizeof(int32_t) * n);
+  x.bnd_n.ensure(2 * sizeof(uint32_t));
+  x.ctr.ensure(4 * sizeof(uint32_t));
+  const uint64_t* keys = x.E->sorted_keys[x.E->sorted_parity];
+  const int32_t* slots = x.E->sorted_slots[x.E->sorted_parity];
+  k_boundary_flags<<<grid_for(x.ctx, n), 256, 0, st>>>(keys, &x.E->meta->num_blocks, x.slab,
+                                                         x.bnd_flags.as<uint8_t>());
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceSelect::Flagged(nullptr, b1, keys, x.bnd_flags.as<uint8_t>(), x.bnd_keys.as<uint64_t>(),
+                             x.bnd_n.as<uint32_t>(), int(x.n_blocks), st);
+  cub::DeviceSelect::Flagged(nullptr, b2, slots, x.bnd_flags.as<uint8_t>(), x.bnd_slots.as<int32_t>(),
+                             x.bnd_n.as<uint32_t>() + 1, int(x.n_blocks), st);
+  x.cub_tmp.ensure(std::max(b1, b2));
+  VXM_CUDA(cub::DeviceSelect::Flagged(x.cub_tmp.p, b1, keys, x.bnd_flags.as<uint8_t>(),
+                                      x.bnd_keys.as<uint64_t>(), x.bnd_n.as<uint32_t>(), int(x.n_blocks),
+                                      st));
+  VXM_CUDA(cub::DeviceSelect::Flagged(x.cub_tmp.p, b2, slots, x.bnd_flags.as<uint8_t>(),
+                                      x.bnd_slots.as<int32_t>(), x.bnd_n.as<uint32_t>() + 1,
+                                      int(x.n_blocks), st));
+  x.ctx->count_launch(3);
+  check_launch(x.ctx, "shard_plan");
+  VXM_CUDA(cudaMemcpyAsync(&x.n_bnd, x.bnd_n.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  VXM_CUDA(cudaStreamSynchronize(st));
+  x.snd.ensure(std::max<size_t>(xbuf_bytes(x.n_bnd), 8));
+}
+
+void shard_set_neighbours(ShardUpdate& x, uint32_t n_left, uint32_t n_right) {
+  use(x.ctx);
+  x.n_rcv[0] = n_left;
+  x.n_rcv[1] = n_right;
+  for (int i = 0; i < 2; ++i) x.rcv[i].ensure(std::max<size_t>(xbuf_bytes(x.n_rcv[i]), 8));
+}
+
+// Sweeps of round r and the pack of the send buffer (completed on return).
+void shard_sweep(ShardUpdate& x, uint32_t r) {
+  use(x.ctx);
+  cudaStream_t st = x.ctx->stream;
+  static int g_sweep = 0;
+  if (!g_sweep) g_sweep = grid_of((const void*)k_shard_sweep, x.ctx);
+  VXM_CUDA(cudaMemsetAsync(x.ctr.p, 0, 4 * sizeof(uint32_t), st));
+  ShardRound sr = round_args(x, r);
+  k_shard_sweep<<<g_sweep, kL3Threads, 0, st>>>(x.la, sr);
+  k_shard_pack<<<grid_for(x.ctx, uint64_t(std::max<uint32_t>(x.n_bnd, 1)) * 32), 256, 0, st>>>(x.la, sr);
+  x.ctx->count_launch(2);
+  check_launch(x.ctx, "k_shard_sweep");
+  VXM_CUDA(cudaStreamSynchronize(st));
+}
+
+// Border phase of round r (the receive buffers hold the neighbours' snapshots);
+// returns this shard's next dirty count.
+uint32_t shard_border(ShardUpdate& x, uint32_t r) {
+  use(x.ctx);
+  cudaStream_t st = x.ctx->stream;
+  static int g_border = 0;
+  if (!g_border) g_border = grid_of((const void*)k_shard_border, x.ctx);
+  VXM_CUDA(cudaMemsetAsync(x.la.count + (r + 1u) % 3u, 0, sizeof(uint32_t), st));
+  ShardRound sr = round_args(x, r);
+  void* args[] = {&x.la, &sr};
+  VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_shard_border, dim3(g_border), dim3(kL3Threads),
+                                       args, 0, st));
+  x.ctx->count_launch();
+  VXM_CUDA(cudaMemcpyAsync(&x.n_dirty, x.la.count + (r + 1u) % 3u, sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, st));
+  VXM_CUDA(cudaStreamSynchronize(st));
+  x.rounds = r;
+  return x.n_dirty;
+}
+
+// Changed set (esdf/integrator.cpp:403-411) and meta; `lowered`: the global
+// decision of this update.
+void shard_finish(ShardUpdate& x, bool lowered, BlockList* out) {
+  use(x.ctx);
+  cudaStream_t st = x.ctx->stream;
+  ShardRound sr = round_args(x, x.rounds);
+  sr.lowered = lowered ? 1 : 0;
+  k_shard_changed<<<grid_for(x.ctx, uint64_t(std::max<uint32_t>(x.n_blocks, 1)) * 32), 256, 0, st>>>(x.la, sr);
+  x.ctx->count_launch();
+  if (lowered) {
+    k_shard_meta<<<1, 1, 0, st>>>(x.E->meta, x.base + x.rounds + 2, x.cur ^ 1u);
+    x.ctx->count_launch();
+  }
+  out->ctx = x.ctx;
+  out->ensure(x.n_all_cap);
+  launch_compact_keys(x.ctx, x.E->sorted_keys[x.E->sorted_parity], x.s.flags, &x.E->meta->num_blocks,
+                      x.n_all_cap, out->keys.as<uint64_t>(), out->d_count, nullptr, "k_compact_esdf");
+  out->host_valid = false;
+  out->count_hint = x.n_all_cap;
+  out->sorted_unique = true;
+  x.E->stage_meta();
+  x.ctx->sync_status();
+  x.E->adopt_meta();
+  vxm_stats& w = x.ctx->stats;
+  w.esdf_calls += 1;
+  w.esdf_blocks += x.n_blocks;
+  w.lower_rounds += lowered ? x.rounds : 0;
+}
+
+// All shards in this process (one context each): exchange by peer copies.
 void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
                              const vxm_esdf_config& cfg, int slab, BlockList** out) {
-  std::vector<ShardState> sh(P);
+  std::vector<ShardUpdate> sh(P);
   for (int p = 0; p < P; ++p) {
     sh[p].E = E[p];
     sh[p].T = T[p];
     sh[p].ctx = E[p]->ctx;
+    sh[p].rank = p;
+    sh[p].world = P;
+    sh[p].slab = slab;
   }
-  // 1. union of the updated lists (every shard marks against all of them)
-  sync_all(sh);
+  auto copy_to = [&](ShardUpdate& dst, void* d, Context* src_ctx, const void* s, size_t bytes) {
+    if (!bytes) return;
+    use(dst.ctx);
+    if (dst.ctx->device == src_ctx->device)
+      VXM_CUDA(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, dst.ctx->stream));
+    else
+      VXM_CUDA(cudaMemcpyPeerAsync(d, dst.ctx->device, s, src_ctx->device, bytes, dst.ctx->stream));
+  };
+  auto sync_all = [&] {
+    for (auto& x : sh) {
+      use(x.ctx);
+      VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
+    }
+  };
+  // union of the updated lists: every shard marks against all of them
   std::vector<uint32_t> n_upd(P);
   uint64_t total = 0;
   for (int p = 0; p < P; ++p) {
     use(updated[p]->ctx);
+    VXM_CUDA(cudaStreamSynchronize(updated[p]->ctx->stream));
     VXM_CUDA(cudaMemcpy(&n_upd[p], updated[p]->d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
     total += n_upd[p];
   }
@@ -394,16 +527,15 @@ void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
     for (int p = 0; p < P; ++p) out[p]->assign_host(nullptr, 0);
     return;
   }
-  for (int q = 0; q < P; ++q) {
-    ShardState& x = sh[q];
+  bool any = false;
+  for (auto& x : sh) {
     use(x.ctx);
     x.uni.ctx = x.ctx;
     x.uni.ensure(uint32_t(total));
     uint64_t off = 0;
     for (int p = 0; p < P; ++p) {
-      ShardState src{};
-      src.ctx = updated[p]->ctx;
-      copy_to(x, x.uni.keys.as<uint64_t>() + off, src, updated[p]->keys.p, sizeof(uint64_t) * n_upd[p]);
+      copy_to(x, x.uni.keys.as<uint64_t>() + off, updated[p]->ctx, updated[p]->keys.p,
+              sizeof(uint64_t) * n_upd[p]);
       off += n_upd[p];
     }
     const uint32_t t32 = uint32_t(total);
@@ -412,177 +544,28 @@ void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
     x.uni.host_valid = false;
     sort_unique_keys(x.ctx, &x.uni);
     x.uni.sorted_unique = true;
+    shard_begin(x, cfg);
+    any |= x.local_any;
   }
-  // 2. mark phase on every shard; global "anything to update"
-  bool any_update = false;
-  for (auto& x : sh) {
-    use(x.ctx);
-    Context* ctx = x.ctx;
-    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
-    ctx->reset_status();
-    x.epoch = ++ctx->call_epoch;
-    x.n7 = 7u * std::max<uint32_t>(x.uni.count_hint, 1);
-    x.E->ensure_capacity(std::min<uint64_t>(uint64_t(x.E->num_blocks) + x.n7, x.E->max_blocks));
-    x.n_all_cap = x.E->capacity;
-    x.s = esdf_scratch(ctx, x.uni.count_hint, x.n_all_cap);
-    esdf_mark_phase(x.E, x.T, &x.uni, cfg, x.s, x.epoch);
-    x.E->stage_meta();
-    ctx->sync_status();
-    x.E->adopt_meta();
-    const DevStatus& st = *ctx->h_status;
-    if (st.capacity_error || st.pool_overflow)
-      throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
-    any_update |= st.any_update != 0;
-    LayerMeta m;
-    VXM_CUDA(cudaMemcpy(&m, x.E->meta, sizeof m, cudaMemcpyDeviceToHost));
-    x.base = m.round_epoch;
-    x.cur = m.cur;
-    x.n_blocks = m.num_blocks;
-    x.la = lower_args(x.E, cfg);
-    x.la.full = 1;
-    x.la.sorted_slots = x.E->sorted_slots[x.E->sorted_parity];
-    x.la.stamp_new = x.E->stamp_new;
-    x.la.stamp_mark = x.E->stamp_mark;
-    x.la.call_epoch = x.epoch;
-    x.la.out_flags = x.s.flags;
-  }
-  uint32_t rounds = 0;
-  if (any_update) {
-    // boundary blocks of every shard (sorted), exchange buffers
-    for (int p = 0; p < P; ++p) {
-      ShardState& x = sh[p];
-      use(x.ctx);
-      cudaStream_t st = x.ctx->stream;
-      const uint32_t n = std::max<uint32_t>(x.n_blocks, 1);
-      x.bnd_flags.ensure(n);
-      x.bnd_keys.ensure(sizeof(uint64_t) * n);
-      x.bnd_slots.ensure(sizeof(int32_t) * n);
-      x.bnd_n.ensure(2 * sizeof(uint32_t));
-      x.ctr.ensure(4 * sizeof(uint32_t));
-      const uint64_t* keys = x.E->sorted_keys[x.E->sorted_parity];
-      const int32_t* slots = x.E->sorted_slots[x.E->sorted_parity];
-      k_boundary_flags<<<grid_for(x.ctx, n), 256, 0, st>>>(keys, &x.E->meta->num_blocks, slab,
-                                                             x.bnd_flags.as<uint8_t>());
-      size_t b1 = 0, b2 = 0;
-      cub::DeviceSelect::Flagged(nullptr, b1, keys, x.bnd_flags.as<uint8_t>(), x.bnd_keys.as<uint64_t>(),
-                                 x.bnd_n.as<uint32_t>(), int(x.n_blocks), st);
-      cub::DeviceSelect::Flagged(nullptr, b2, slots, x.bnd_flags.as<uint8_t>(), x.bnd_slots.as<int32_t>(),
-                                 x.bnd_n.as<uint32_t>() + 1, int(x.n_blocks), st);
-      x.cub_tmp.ensure(std::max(b1, b2));
-      VXM_CUDA(cub::DeviceSelect::Flagged(x.cub_tmp.p, b1, keys, x.bnd_flags.as<uint8_t>(),
-                                          x.bnd_keys.as<uint64_t>(), x.bnd_n.as<uint32_t>(),
-                                          int(x.n_blocks), st));
-      VXM_CUDA(cub::DeviceSelect::Flagged(x.cub_tmp.p, b2, slots, x.bnd_flags.as<uint8_t>(),
-                                          x.bnd_slots.as<int32_t>(), x.bnd_n.as<uint32_t>() + 1,
-                                          int(x.n_blocks), st));
-      x.ctx->count_launch(3);
-      VXM_CUDA(cudaMemcpyAsync(&x.n_bnd, x.bnd_n.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-      VXM_CUDA(cudaStreamSynchronize(st));
-      const uint32_t nb = std::max<uint32_t>(x.n_bnd, 1);
-      x.snd_keys.ensure(sizeof(uint64_t) * nb);
-      x.snd_dirty.ensure(nb);
-      x.snd_faces.ensure(sizeof(uint32_t) * 384 * nb);
-    }
-    for (int p = 0; p < P; ++p) {  // [0]: from the -x neighbour, [1]: from the +x one
-      ShardState& x = sh[p];
-      const int nbr[2] = {(p - 1 + P) % P, (p + 1) % P};
-      for (int i = 0; i < 2; ++i) {
-        const uint32_t nb = std::max<uint32_t>(sh[nbr[i]].n_bnd, 1);
-        use(x.ctx);
-        x.rcv_keys[i].ensure(sizeof(uint64_t) * nb);
-        x.rcv_dirty[i].ensure(nb);
-        x.rcv_faces[i].ensure(sizeof(uint32_t) * 384 * nb);
-        x.n_rcv[i] = sh[nbr[i]].n_bnd;
-      }
-    }
-    const int g_sweep = grid_of((const void*)k_shard_sweep, sh[0].ctx);
-    const int g_border = grid_of((const void*)k_shard_border, sh[0].ctx);
-    for (auto& x : sh) x.n_dirty = x.n_blocks;
-    uint32_t r = 0;
-    while (true) {
-      ++r;
-      for (int p = 0; p < P; ++p) {
-        ShardState& x = sh[p];
-        use(x.ctx);
-        cudaStream_t st = x.ctx->stream;
-        VXM_CUDA(cudaMemsetAsync(x.ctr.p, 0, 4 * sizeof(uint32_t), st));
-        ShardRound sr = round_args(x, r, p, P, slab);
-        k_shard_sweep<<<g_sweep, kL3Threads, 0, st>>>(x.la, sr);
-        k_shard_pack<<<grid_for(x.ctx, uint64_t(x.n_bnd) * 32), 256, 0, st>>>(x.la, sr);
-        x.ctx->count_launch(2);
-        check_launch(x.ctx, "k_shard_sweep");
-      }
-      sync_all(sh);
-      for (int p = 0; p < P; ++p) {  // peer copies of the boundary snapshots
-        const ShardState& src = sh[p];
-        const int to[2] = {(p + 1) % P, (p - 1 + P) % P};  // our +x side is their -x side
-        for (int i = 0; i < 2; ++i) {
-          ShardState& dst = sh[to[i]];
-          const int slot = i == 0 ? 0 : 1;
-          copy_to(dst, dst.rcv_keys[slot].p, src, src.snd_keys.p, sizeof(uint64_t) * src.n_bnd);
-          copy_to(dst, dst.rcv_dirty[slot].p, src, src.snd_dirty.p, src.n_bnd);
-          copy_to(dst, dst.rcv_faces[slot].p, src, src.snd_faces.p, sizeof(uint32_t) * 384 * src.n_bnd);
-        }
-      }
-      for (int p = 0; p < P; ++p) {
-        ShardState& x = sh[p];
-        use(x.ctx);
-        cudaStream_t st = x.ctx->stream;
-        VXM_CUDA(cudaMemsetAsync(x.la.count + (r + 1u) % 3u, 0, sizeof(uint32_t), st));
-        ShardRound sr = round_args(x, r, p, P, slab);
-        void* args[] = {&x.la, &sr};
-        VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_shard_border, dim3(g_border),
-                                             dim3(kL3Threads), args, 0, st));
-        x.ctx->count_launch();
+  if (any) {
+    for (auto& x : sh) shard_plan(x);
+    for (int p = 0; p < P; ++p)  // [0]: from the -x neighbour, [1]: from the +x one
+      shard_set_neighbours(sh[p], sh[(p - 1 + P) % P].n_bnd, sh[(p + 1) % P].n_bnd);
+    for (uint32_t r = 1;; ++r) {
+      for (auto& x : sh) shard_sweep(x, r);
+      for (int p = 0; p < P; ++p) {  // our snapshot: the +x neighbour's [0], the -x one's [1]
+        ShardUpdate& src = sh[p];
+        copy_to(sh[(p + 1) % P], sh[(p + 1) % P].rcv[0].p, src.ctx, src.snd.p, xbuf_bytes(src.n_bnd));
+        copy_to(sh[(p - 1 + P) % P], sh[(p - 1 + P) % P].rcv[1].p, src.ctx, src.snd.p,
+                xbuf_bytes(src.n_bnd));
       }
       uint64_t next = 0;
-      for (int p = 0; p < P; ++p) {
-        ShardState& x = sh[p];
-        use(x.ctx);
-        VXM_CUDA(cudaMemcpyAsync(&x.n_dirty, x.la.count + (r + 1u) % 3u, sizeof(uint32_t),
-                                 cudaMemcpyDeviceToHost, x.ctx->stream));
-        VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
-        next += x.n_dirty;
-      }
+      for (auto& x : sh) next += shard_border(x, r);
       if (next == 0) break;  // while (!dirty.empty()) — esdf/integrator.cpp:506
     }
-    rounds = r;
-    for (auto& x : sh) {
-      use(x.ctx);
-      ShardRound sr = round_args(x, r, 0, P, slab);
-      sr.lowered = 1;
-      k_shard_changed<<<grid_for(x.ctx, uint64_t(x.n_blocks) * 32), 256, 0, x.ctx->stream>>>(x.la, sr);
-      k_shard_meta<<<1, 1, 0, x.ctx->stream>>>(x.E->meta, x.base + r + 2, x.cur ^ 1u);
-      x.ctx->count_launch(2);
-    }
-  } else {  // nothing to lower anywhere: changed = new or marked blocks
-    for (auto& x : sh) {
-      use(x.ctx);
-      ShardRound sr = round_args(x, 0, 0, P, slab);
-      sr.lowered = 0;
-      k_shard_changed<<<grid_for(x.ctx, uint64_t(x.n_blocks) * 32), 256, 0, x.ctx->stream>>>(x.la, sr);
-      x.ctx->count_launch();
-    }
   }
-  for (int p = 0; p < P; ++p) {
-    ShardState& x = sh[p];
-    use(x.ctx);
-    out[p]->ctx = x.ctx;
-    out[p]->ensure(x.n_all_cap);
-    launch_compact_keys(x.ctx, x.E->sorted_keys[x.E->sorted_parity], x.s.flags, &x.E->meta->num_blocks,
-                        x.n_all_cap, out[p]->keys.as<uint64_t>(), out[p]->d_count, nullptr,
-                        "k_compact_esdf");
-    out[p]->host_valid = false;
-    out[p]->count_hint = x.n_all_cap;
-    out[p]->sorted_unique = true;
-    x.E->stage_meta();
-    x.ctx->sync_status();
-    x.E->adopt_meta();
-    vxm_stats& w = x.ctx->stats;
-    w.esdf_calls += 1;
-    w.esdf_blocks += x.n_blocks;
-    w.lower_rounds += rounds;
-  }
+  for (int p = 0; p < P; ++p) shard_finish(sh[p], any, out[p]);
+  sync_all();
 }
 
 }  // namespace vxm

@@ -1,0 +1,84 @@
+"""GPU parity: one shard per process (paper_2311_00626_b200/dist.py) — two
+processes on the same B200, gloo for the exchange (staged through the host;
+NCCL moves the device buffers directly when each process has its own GPU).
+Each rank integrates every frame into its own shard and runs
+update_esdf_distributed; rank 0 also keeps the single map.  The union of the
+ranks' changed lists and ESDF layers equals the single-map update bit-for-bit.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, slab, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2311_00626_b200 as vx
+        from paper_2311_00626_b200 import _abi as A
+        from paper_2311_00626_b200.dist import update_esdf_distributed
+        from tests.helpers import camera_frames
+        vs = 0.04
+        cam, seq = camera_frames("room", 320, 240, 3, 16)
+        icfg = A.default_integrator_config(truncation=0.16)
+        ecfg = A.default_esdf_config(site_threshold=0.04, max_distance=1.0)
+        ctx = vx.Context(0)
+        ctx.set_shard(rank, world, slab)
+        T, E = vx.TsdfLayer(vs, ctx=ctx), vx.EsdfLayer(vs, ctx=ctx)
+        single = (vx.TsdfLayer(vs), vx.EsdfLayer(vs)) if rank == 0 else None
+        frames = []
+        for pose, d in seq:
+            ch = vx.integrate_depth(T, d, pose, cam, icfg)
+            ech = update_esdf_distributed(E, T, ch, ecfg)
+            want = None
+            if single is not None:
+                a = vx.integrate_depth(single[0], d, pose, cam, icfg)
+                want = vx.update_esdf(single[1], single[0], a, ecfg)
+            frames.append((ech, want))
+        mine = E.export()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (frames, mine))
+        if rank == 0:
+            ok = True
+            for f in range(len(seq)):
+                parts = np.concatenate([g[0][f][0] for g in gathered]).reshape(-1, 3)
+                parts = parts[np.lexsort((parts[:, 2], parts[:, 1], parts[:, 0]))]
+                ok &= np.array_equal(parts, gathered[0][0][f][1])
+            k = np.concatenate([g[1][0] for g in gathered])
+            v = np.concatenate([g[1][1] for g in gathered])
+            order = np.lexsort((k[:, 2], k[:, 1], k[:, 0]))
+            ks, vs_ = single[1].export()
+            ok &= np.array_equal(k[order], ks) and v[order].tobytes() == vs_.tobytes()
+            q.put(bool(ok))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,slab", [(2, 3), (3, 2)])
+def test_distributed_esdf_equals_single_map(world, slab):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, slab, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok
