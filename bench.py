@@ -49,6 +49,10 @@ CONFIGS = {
                workload="C5: ESDF full recompute of a dense 512^3-voxel SphereWorld volume "
                         "(262,144 blocks); each step alternates between two volumes so every "
                         "update resets and re-lowers the whole map"),
+    "c4": dict(scene="building", sensor="camera", w=640, h=480, vs=0.01, trunc=0.04, max_int=5.0,
+               esdf=(0.01, 2.0), orbit=100, reserve=1 << 19,
+               workload="C4 (single GPU): synthetic building walkthrough, 640x480 depth, 1 cm "
+                        "voxels, TSDF integration + ESDF update every frame"),
     "c3": dict(scene="lidar_yard", sensor="lidar", w=2048, h=64, vs=0.1, trunc=0.4, max_int=100.0,
                esdf=(0.1, 2.0), orbit=100, reserve=1 << 20,
                workload="C3: 64-beam x 2048-column LiDAR, 10 cm voxels, 100 m range, TSDF + ESDF"),

@@ -103,3 +103,20 @@ def test_c3_lidar_two_frames_vs_reference(vx, ref):
         eb = ref.update_esdf(Eo, Tf, a, ecfg)
         assert np.array_equal(ea, eb)
     assert layers_identical(*E.export(), *ref.export(Eo))
+
+
+def test_c4_building_1cm_two_frames_vs_reference(vx, ref):
+    """C4 at 1 cm (building walkthrough, 640x480): camera path bit-exact."""
+    from tests.helpers import camera_frames
+    cam, seq = camera_frames("building", 640, 480, 2, 100)
+    icfg = A.default_integrator_config(truncation=0.04)
+    ecfg = A.default_esdf_config(site_threshold=0.01, max_distance=2.0)
+    T, E = vx.TsdfLayer(0.01), vx.EsdfLayer(0.01)
+    To, Eo = ref.layer(A.LAYER_TSDF, 0.01), ref.layer(A.LAYER_ESDF, 0.01)
+    for pose, d in seq:
+        a = vx.integrate_depth(T, d, pose, cam, icfg)
+        b = ref.integrate_camera(To, d, pose, cam, icfg)
+        assert np.array_equal(a, b)
+        assert np.array_equal(vx.update_esdf(E, T, a, ecfg), ref.update_esdf(Eo, To, b, ecfg))
+    assert layers_identical(*T.export(), *ref.export(To))
+    assert layers_identical(*E.export(), *ref.export(Eo))
