@@ -237,6 +237,36 @@ vxm_status vxm_integrate_depth_lidar_device(vxm_layer* layer, const float* depth
                                             const vxm_integrator_config* cfg,
                                             vxm_blocklist* changed_out);
 
+/* ---- replay (io/pipeline.hpp:27-72, pipeline.cpp:54-148) ------------------- */
+/* ReplayConfig (TSDF source; occupancy / color / mesh are out of scope). */
+typedef struct {
+  double voxel_size;
+  int32_t update_every;  /* derive the ESDF every this many frames (+ after the last) */
+  vxm_integrator_config integrator;
+  vxm_esdf_config esdf;
+} vxm_replay_config;
+/* FrameTiming: wall-clock ms per stage of one frame (0 when skipped). */
+typedef struct {
+  int32_t frame;
+  double tsdf_ms, color_ms, esdf_ms, mesh_ms;
+} vxm_frame_timing;
+/* make_replay_config (pipeline.cpp:46-52): truncation 4 voxels, site threshold 1. */
+void vxm_replay_config_make(double voxel_size, vxm_replay_config* out);
+/* replay (pipeline.cpp:54-148) over in-memory frames: n_frames depth images
+ * (host, n_frames x height x width, row-major) with their poses; integrates every
+ * frame and, every update_every frames and after the last one, folds the blocks
+ * changed since the previous update into the ESDF.  Creates *tsdf_out and
+ * *esdf_out on ctx; timings has n_frames entries.  Errors as the reference: no
+ * frames or update_every < 1 -> VXM_ERR_INVALID_ARGUMENT. */
+vxm_status vxm_replay_camera(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_camera* cam,
+                             int n_frames, int width, int height, const float* depth,
+                             const vxm_pose* poses, vxm_layer** tsdf_out, vxm_layer** esdf_out,
+                             vxm_frame_timing* timings);
+vxm_status vxm_replay_lidar(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_lidar* lidar,
+                            int n_frames, int width, int height, const float* depth,
+                            const vxm_pose* poses, vxm_layer** tsdf_out, vxm_layer** esdf_out,
+                            vxm_frame_timing* timings);
+
 /* ---- snapshots (core/serialization.hpp:29-35, FORMATS.md "VXLF") -------- */
 /* save_snapshot (serialization.cpp:88-110): VXLF v1, little-endian; layers in
  * the reference's order (tsdf, then esdf), blocks in sorted GridIndex order, so

@@ -11,4 +11,5 @@ from .voxmap import (BlockList, CameraIntrinsics, Context, EsdfConfig, EsdfLayer
                      default_context, default_lidar_intrinsics, esdf_distance, integrate_depth,
                      integrate_depth_device, lib, lower_esdf, mark_sites, query_batch,
                      update_esdf, update_esdf_device, update_frame_device,
-                     IoError, save_snapshot, load_snapshot, update_esdf_sharded)
+                     IoError, save_snapshot, load_snapshot, update_esdf_sharded,
+                     make_replay_config, replay, write_timing_csv)

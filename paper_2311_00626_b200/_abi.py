@@ -79,6 +79,16 @@ class EsdfConfigC(C.Structure):
                 ("max_distance", C.c_double), ("parallel", C.c_int32)]
 
 
+class ReplayConfigC(C.Structure):
+    """vxm_replay_config — ReplayConfig (io/pipeline.hpp:27-35), TSDF source."""
+    _fields_ = [("voxel_size", C.c_double), ("update_every", C.c_int32),
+                ("integrator", IntegratorConfigC), ("esdf", EsdfConfigC)]
+
+
+FRAME_TIMING_DTYPE = np.dtype([("frame", "<i4"), ("pad_", "<i4"), ("tsdf_ms", "<f8"),
+                               ("color_ms", "<f8"), ("esdf_ms", "<f8"), ("mesh_ms", "<f8")])
+
+
 class QueryConfigC(C.Structure):
     _fields_ = [("interpolate", C.c_int32), ("parallel", C.c_int32)]
 

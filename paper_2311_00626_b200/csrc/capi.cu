@@ -4,6 +4,7 @@
 // (before any mutation), maps C++ errors onto vxm_status codes that mirror
 // the reference's exception types, and dispatches to the device drivers.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -1042,5 +1043,105 @@ vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* vs_out,
     vxm_layer_destroy(E);
   }
   return st;
+}
+}  // extern "C"
+
+// ---- replay — io/pipeline.cpp:46-148 --------------------------------------------
+namespace {
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+vxm_status replay_common(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_camera* cam,
+                         const vxm_lidar* li, int n, int w, int h, const float* depth,
+                         const vxm_pose* poses, vxm_layer** tsdf_out, vxm_layer** esdf_out,
+                         vxm_frame_timing* timings) {
+  vxm_layer* T = nullptr;
+  vxm_layer* E = nullptr;
+  const vxm_status st = guard([&] {
+    REQUIRE_ARG(ctx && cfg && (cam || li) && tsdf_out && esdf_out && timings, "null argument");
+    if (n <= 0) throw Error(VXM_ERR_INVALID_ARGUMENT, "replay: dataset has no frames");
+    if (cfg->update_every < 1) throw Error(VXM_ERR_INVALID_ARGUMENT, "replay: update_every must be >= 1");
+    REQUIRE_ARG(depth && poses, "null argument");
+    vxm_status s = vxm_layer_create(ctx, VXM_LAYER_TSDF, cfg->voxel_size, 0, &T);
+    if (s != VXM_OK) throw Error(s, g_err);
+    s = vxm_layer_create(ctx, VXM_LAYER_ESDF, cfg->voxel_size, 0, &E);
+    if (s != VXM_OK) throw Error(s, g_err);
+    vxm_blocklist changed, esdf_changed, pending;
+    changed.ctx = esdf_changed.ctx = pending.ctx = ctx;
+    uint32_t n_pending = 0;  // keys in `pending` (unsorted, may repeat until folded)
+    DevBuf grow;
+    const size_t frame_px = size_t(w) * size_t(h);
+    for (int k = 0; k < n; ++k) {
+      vxm_frame_timing& t = timings[k];
+      t = vxm_frame_timing{k, 0.0, 0.0, 0.0, 0.0};
+      const auto t0 = std::chrono::steady_clock::now();
+      const ViewArgs va = frame_args(T, depth + size_t(k) * frame_px, w, h, &poses[k], cam, li,
+                                     &cfg->integrator, false);
+      run_integrate(T, va, cfg->integrator, &changed);
+      t.tsdf_ms = ms_since(t0);
+      // pending ∪= changed (pipeline.cpp:38-43; folded with one sort at the update)
+      const uint32_t n_ch = ctx->h_status->n_changed;
+      if (n_ch) {
+        if (n_pending + n_ch > pending.cap) {
+          const uint32_t cap = std::max<uint32_t>(2 * (n_pending + n_ch), 4096);
+          grow.ensure(sizeof(uint64_t) * cap);
+          if (n_pending)
+            VXM_CUDA(cudaMemcpyAsync(grow.p, pending.keys.p, sizeof(uint64_t) * n_pending,
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+          pending.ensure(cap);
+          if (n_pending)
+            VXM_CUDA(cudaMemcpyAsync(pending.keys.p, grow.p, sizeof(uint64_t) * n_pending,
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        VXM_CUDA(cudaMemcpyAsync(pending.keys.as<uint64_t>() + n_pending, changed.keys.p,
+                                 sizeof(uint64_t) * n_ch, cudaMemcpyDeviceToDevice, ctx->stream));
+        n_pending += n_ch;
+      }
+      const bool last = k + 1 == n;
+      const bool on_cadence = (k + 1) % cfg->update_every == 0;
+      if ((on_cadence || last) && n_pending > 0) {  // derive_layers (mesh: out of scope)
+        const auto t1 = std::chrono::steady_clock::now();
+        VXM_CUDA(cudaMemcpyAsync(pending.d_count, &n_pending, sizeof n_pending, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        pending.count_hint = n_pending;
+        pending.host_valid = false;
+        pending.sorted_unique = false;
+        sort_unique_keys(ctx, &pending);
+        pending.sorted_unique = true;
+        run_update_esdf(E, T, &pending, cfg->esdf, &esdf_changed);
+        t.esdf_ms = ms_since(t1);
+        n_pending = 0;
+      }
+    }
+    *tsdf_out = T;
+    *esdf_out = E;
+  });
+  if (st != VXM_OK) {
+    vxm_layer_destroy(T);
+    vxm_layer_destroy(E);
+  }
+  return st;
+}
+}  // namespace
+
+extern "C" {
+void vxm_replay_config_make(double voxel_size, vxm_replay_config* out) {
+  out->voxel_size = voxel_size;
+  out->update_every = 4;
+  vxm_integrator_config_default(&out->integrator);
+  vxm_esdf_config_default(&out->esdf);
+  out->integrator.truncation = 4.0 * voxel_size;
+  out->esdf.site_threshold = voxel_size;
+}
+vxm_status vxm_replay_camera(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_camera* cam,
+                             int n, int w, int h, const float* depth, const vxm_pose* poses,
+                             vxm_layer** tsdf_out, vxm_layer** esdf_out, vxm_frame_timing* timings) {
+  return replay_common(ctx, cfg, cam, nullptr, n, w, h, depth, poses, tsdf_out, esdf_out, timings);
+}
+vxm_status vxm_replay_lidar(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_lidar* li, int n,
+                            int w, int h, const float* depth, const vxm_pose* poses,
+                            vxm_layer** tsdf_out, vxm_layer** esdf_out, vxm_frame_timing* timings) {
+  return replay_common(ctx, cfg, nullptr, li, n, w, h, depth, poses, tsdf_out, esdf_out, timings);
 }
 }  // extern "C"

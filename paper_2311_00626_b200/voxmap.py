@@ -337,6 +337,44 @@ class EsdfLayer(_Layer):
         return obj
 
 
+def make_replay_config(voxel_size: float) -> A.ReplayConfigC:
+    """make_replay_config (io/pipeline.cpp:46-52)."""
+    c = A.ReplayConfigC()
+    lib().vxm_replay_config_make(C.c_double(voxel_size), C.byref(c))
+    return c
+
+
+def replay(frames, intrinsics, cfg: A.ReplayConfigC, ctx: Context | None = None):
+    """replay (io/pipeline.cpp:54-148) over in-memory frames [(T_WS, depth), ...]:
+    returns (tsdf, esdf, timings) with FrameTiming records (FRAME_TIMING_DTYPE)."""
+    ctx = ctx or default_context()
+    n = len(frames)
+    if n:
+        depth = np.ascontiguousarray(np.stack([_depth(d) for _, d in frames]), np.float32)
+        h, w = depth.shape[1], depth.shape[2]
+        poses = (A.PoseC * n)(*[_pose_c(T) for T, _ in frames])
+    else:
+        depth, h, w, poses = np.zeros((0, 0, 0), np.float32), 0, 0, (A.PoseC * 1)()
+    timings = np.zeros(max(n, 1), A.FRAME_TIMING_DTYPE)
+    th, eh = C.c_void_p(), C.c_void_p()
+    fn = lib().vxm_replay_camera if isinstance(intrinsics, A.Camera) else lib().vxm_replay_lidar
+    check(fn(ctx.h, C.byref(cfg), C.byref(intrinsics), C.c_int(n), C.c_int(w), C.c_int(h), A.ptr(depth),
+             poses, C.byref(th), C.byref(eh), A.ptr(timings)))
+    return TsdfLayer._adopt(th, ctx), EsdfLayer._adopt(eh, ctx), timings[:n]
+
+
+def write_timing_csv(timings, path: str) -> None:
+    """write_timing_csv (io/pipeline.cpp:150-168): frame,tsdf_ms,color_ms,esdf_ms,mesh_ms."""
+    try:
+        with open(path, "w", newline="") as f:
+            f.write("frame,tsdf_ms,color_ms,esdf_ms,mesh_ms\n")
+            for t in timings:
+                f.write("%d,%.3f,%.3f,%.3f,%.3f\n" % (t["frame"], t["tsdf_ms"], t["color_ms"],
+                                                     t["esdf_ms"], t["mesh_ms"]))
+    except OSError as e:
+        raise IoError(f"cannot open for writing: {path}") from e
+
+
 def save_snapshot(path: str, voxel_size: float, tsdf: TsdfLayer | None = None,
                   esdf: EsdfLayer | None = None) -> None:
     """save_snapshot (core/serialization.hpp:31): VXLF v1, byte-identical to the
