@@ -95,111 +95,199 @@ __device__ inline bool fast_floor(float f, float c, float xf, float zf, int* idx
   return true;
 }
 
-__global__ void __launch_bounds__(256, 6) k_integrate(IntegrateArgs a) {
-  __shared__ double s_A[3][3][8];  // R_SL(i, axis) * centre_axis(v)
+// One voxel: projection, sample, tsdf_update (integrator.cpp:98-123); returns
+// whether its bytes changed.  p = T_SL * centre (FP64, pinned order).
+__device__ inline bool integrate_voxel(const IntegrateArgs& a, float2* blk, int lin, double px,
+                                       double py, double pz, bool is_new, uint32_t& n_read,
+                                       uint32_t& n_upd) {
+  double d_v;
+  if (!a.lidar) {
+    d_v = pz;  // CameraIntrinsics::depth_of — camera.hpp:49
+  } else {     // LidarIntrinsics::depth_of — lidar.hpp:62
+    d_v = __dsqrt_rn(__dadd_rn(__dmul_rn(px, px), __dadd_rn(__dmul_rn(py, py), __dmul_rn(pz, pz))));
+  }
+  if (!(d_v > 0.0) || d_v > a.max_voxel_depth) return false;  // integrator.cpp:104-107
+  float s;
+  bool ok;
+  float2 old = make_float2(0.0f, 0.0f);
+  bool have_old = false;
+  if (!a.lidar) {
+    if (!a.linear) {
+      int col, row;
+      const float xf = __double2float_rn(px), yf = __double2float_rn(py), zf = __double2float_rn(pz);
+      if (!(fast_floor(a.fu_f, a.cu_f, xf, zf, &col) && fast_floor(a.fv_f, a.cv_f, yf, zf, &row))) {
+        // exact FP64 projection — camera.hpp:39-40
+        const double u = __dadd_rn(__ddiv_rn(__dmul_rn(a.fu, px), pz), a.cu);
+        const double v = __dadd_rn(__ddiv_rn(__dmul_rn(a.fv, py), pz), a.cv);
+        if (!(u >= 0.0 && u < double(a.W) && v >= 0.0 && v < double(a.H))) return false;
+        col = int(floor(u));
+        row = int(floor(v));
+      }
+      if (col < 0 || row < 0 || col >= a.W || row >= a.H) return false;
+      // the old voxel is loaded together with the depth sample (one round trip)
+      if (!is_new) {
+        old = blk[lin];
+        have_old = true;
+      }
+      s = __ldg(a.depth + size_t(row) * a.W + col);
+      ok = valid_depth_i(s);
+    } else {
+      const double u = __dadd_rn(__ddiv_rn(__dmul_rn(a.fu, px), pz), a.cu);
+      const double v = __dadd_rn(__ddiv_rn(__dmul_rn(a.fv, py), pz), a.cv);
+      if (!(u >= 0.0 && u < double(a.W) && v >= 0.0 && v < double(a.H))) return false;
+      ok = sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s);
+    }
+  } else {
+    // LidarIntrinsics::project — lidar.hpp:43-55 (CUDA libm atan2/acos)
+    const double kTwoPi = 6.283185307179586;
+    double az = __dsub_rn(atan2(py, px), a.az0);
+    az = __dsub_rn(az, __dmul_rn(kTwoPi, floor(__ddiv_rn(az, kTwoPi))));
+    const double u = __dmul_rn(az, a.u_scale);
+    double c = __ddiv_rn(pz, d_v);
+    c = c < -1.0 ? -1.0 : (1.0 < c ? 1.0 : c);
+    const double v = __dmul_rn(__dsub_rn(acos(c), a.el0), a.v_scale);
+    if (!(u >= 0.0 && u < double(a.na) && v >= 0.0 && v < double(a.ne))) return false;
+    ok = a.linear ? sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s)
+                  : sample_nearest_d(a.depth, a.W, a.H, u, v, &s);
+  }
+  if (!ok) return false;
+  const float d_p = __fsub_rn(s, __double2float_rn(d_v));  // integrator.cpp:116
+  // tsdf_update — updates.hpp:39-54
+  if (d_p < -a.eps) return false;  // occluded: voxel unchanged
+  float w_new = 1.0f;
+  if (a.inv_sq) {
+    const double dd = __dmul_rn(double(s), double(s));
+    w_new = __double2float_rn(__ddiv_rn(1.0, dd < 1e-6 ? 1e-6 : dd));
+  }
+  if (!is_new && !have_old) old = blk[lin];
+  n_read += is_new ? 0u : 1u;
+  const float d_t = d_p < -a.eps ? -a.eps : (a.eps < d_p ? a.eps : d_p);
+  const float w_sum = __fadd_rn(old.y, w_new);
+  const float avg = __fdiv_rn(__fadd_rn(__fmul_rn(old.y, old.x), __fmul_rn(w_new, d_t)), w_sum);
+  float2 nv;
+  nv.x = avg < -a.eps ? -a.eps : (a.eps < avg ? a.eps : avg);
+  nv.y = a.max_weight < w_sum ? a.max_weight : w_sum;
+  if (__float_as_uint(nv.x) != __float_as_uint(old.x) || __float_as_uint(nv.y) != __float_as_uint(old.y)) {
+    blk[lin] = nv;
+    ++n_upd;
+    return true;
+  }
+  return false;
+}
+
+// One warp per candidate block, 16 voxels per lane (lin = lane + 32 j): many
+// independent voxels per lane hide the depth-gather and voxel latencies, and
+// there is no block-wide barrier.  The per-axis products R_SL(i, a) *
+// centre_a(v) are formed per lane (bit-identical to the reference's
+// R * centre rows, pose.hpp:58-60 with the pinned a0 + (a1 + a2) order).
+__global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
   const DevStatus* st = a.status_ro;
   if (st->pool_overflow || st->capacity_error || st->bitmap_overflow) return;
   const uint32_t n = st->n_candidates;
   const double* R = a.T_SL.R;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   uint32_t n_read = 0, n_upd = 0;  // work counters (algorithmic bytes)
-  for (uint32_t ci = blockIdx.x; ci < n; ci += gridDim.x) {
+  for (uint32_t ci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ci < n; ci += nwarps) {
     const uint64_t key = a.cand_keys[ci];
     const int32_t sraw = a.cand_slots[ci];
     const bool is_new = sraw < 0;
     const int32_t slot = sraw & 0x7fffffff;
-    if (threadIdx.x < 72) {
-      const int i = threadIdx.x / 24, ax = (threadIdx.x / 8) % 3, v = threadIdx.x % 8;
-      const int32_t g = ax == 0 ? key_x(key) : (ax == 1 ? key_y(key) : key_z(key));
-      // voxel_center — indexing.hpp:113-119: ((g * 8 + v) + 0.5) * vs
-      const double c = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(double(g), 8.0), double(v)), 0.5), a.vs);
-      s_A[i][ax][v] = __dmul_rn(R[3 * i + ax], c);
-    }
-    __syncthreads();
     float2* blk = a.pool + size_t(slot) * kVPB;
-    bool any = false;
+    // voxel_center — indexing.hpp:113-119: ((g * 8 + v) + 0.5) * vs
+    auto centre = [&](int32_t g, int v) {
+      return __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(double(g), 8.0), double(v)), 0.5), a.vs);
+    };
+    const int vx = lane & 7, vy0 = lane >> 3;
+    const double cx = centre(key_x(key), vx);
+    const double cy0 = centre(key_y(key), vy0), cy1 = centre(key_y(key), vy0 + 4);
+    double Ax[3], Ay0[3], Ay1[3];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int lin = threadIdx.x + k * 256;
-      const int vx = lin & 7, vy = (lin >> 3) & 7, vz = lin >> 6;
-      // Pose::operator* — pose.hpp:58-60, rows a0 + (a1 + a2), then + t
-      const double pz = __dadd_rn(__dadd_rn(s_A[2][0][vx], __dadd_rn(s_A[2][1][vy], s_A[2][2][vz])), a.T_SL.t[2]);
-      const double px = __dadd_rn(__dadd_rn(s_A[0][0][vx], __dadd_rn(s_A[0][1][vy], s_A[0][2][vz])), a.T_SL.t[0]);
-      const double py = __dadd_rn(__dadd_rn(s_A[1][0][vx], __dadd_rn(s_A[1][1][vy], s_A[1][2][vz])), a.T_SL.t[1]);
-      double d_v;
-      if (!a.lidar) {
-        d_v = pz;  // CameraIntrinsics::depth_of — camera.hpp:49
-      } else {     // LidarIntrinsics::depth_of — lidar.hpp:62
-        d_v = __dsqrt_rn(__dadd_rn(__dmul_rn(px, px), __dadd_rn(__dmul_rn(py, py), __dmul_rn(pz, pz))));
-      }
-      if (!(d_v > 0.0) || d_v > a.max_voxel_depth) continue;  // integrator.cpp:104-107
-      float s;
-      bool ok;
-      if (!a.lidar) {
-        if (!a.linear) {
+    for (int i = 0; i < 3; ++i) {
+      Ax[i] = __dmul_rn(R[3 * i], cx);
+      Ay0[i] = __dmul_rn(R[3 * i + 1], cy0);
+      Ay1[i] = __dmul_rn(R[3 * i + 1], cy1);
+    }
+    const int32_t gz = key_z(key);
+    bool any = false;
+    auto centre_p = [&](int j, double& px, double& py, double& pz) {
+      const double cz = centre(gz, j >> 1);
+      const double* Ay = (j & 1) ? Ay1 : Ay0;
+      pz = __dadd_rn(__dadd_rn(Ax[2], __dadd_rn(Ay[2], __dmul_rn(R[8], cz))), a.T_SL.t[2]);
+      px = __dadd_rn(__dadd_rn(Ax[0], __dadd_rn(Ay[0], __dmul_rn(R[2], cz))), a.T_SL.t[0]);
+      py = __dadd_rn(__dadd_rn(Ax[1], __dadd_rn(Ay[1], __dmul_rn(R[5], cz))), a.T_SL.t[1]);
+    };
+    if (!a.lidar && !a.linear) {
+      // camera, nearest sampling (the hot configuration): per chunk of 4 voxels
+      // all depth samples and old voxels are loaded before any is used
+#pragma unroll 1
+      for (int j0 = 0; j0 < 16; j0 += 4) {
+        float sd[4];
+        float2 ov[4];
+        float dv[4];
+        uint32_t live = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double px, py, pz;
+          centre_p(j0 + q, px, py, pz);
+          const int lin = lane + 32 * (j0 + q);
+          sd[q] = 0.0f;
+          ov[q] = make_float2(0.0f, 0.0f);
+          dv[q] = __double2float_rn(pz);
+          if (!(pz > 0.0) || pz > a.max_voxel_depth) continue;  // integrator.cpp:104-107
           int col, row;
-          const float xf = __double2float_rn(px), yf = __double2float_rn(py),
-                      zf = __double2float_rn(pz);
-          if (!(fast_floor(a.fu_f, a.cu_f, xf, zf, &col) &&
-                fast_floor(a.fv_f, a.cv_f, yf, zf, &row))) {
-            // exact FP64 projection — camera.hpp:39-40
-            const double u = __dadd_rn(__ddiv_rn(__dmul_rn(a.fu, px), pz), a.cu);
+          const float xf = __double2float_rn(px), yf = __double2float_rn(py), zf = dv[q];
+          if (!(fast_floor(a.fu_f, a.cu_f, xf, zf, &col) && fast_floor(a.fv_f, a.cv_f, yf, zf, &row))) {
+            const double u = __dadd_rn(__ddiv_rn(__dmul_rn(a.fu, px), pz), a.cu);  // camera.hpp:39-40
             const double v = __dadd_rn(__ddiv_rn(__dmul_rn(a.fv, py), pz), a.cv);
             if (!(u >= 0.0 && u < double(a.W) && v >= 0.0 && v < double(a.H))) continue;
             col = int(floor(u));
             row = int(floor(v));
           }
           if (col < 0 || row < 0 || col >= a.W || row >= a.H) continue;
-          s = __ldg(a.depth + size_t(row) * a.W + col);
-          ok = valid_depth_i(s);
-        } else {
-          const double u = __dadd_rn(__ddiv_rn(__dmul_rn(a.fu, px), pz), a.cu);
-          const double v = __dadd_rn(__ddiv_rn(__dmul_rn(a.fv, py), pz), a.cv);
-          if (!(u >= 0.0 && u < double(a.W) && v >= 0.0 && v < double(a.H))) continue;
-          ok = sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s);
+          sd[q] = __ldg(a.depth + size_t(row) * a.W + col);
+          if (!is_new) ov[q] = __ldcs(reinterpret_cast<const float2*>(blk) + lin);
+          live |= 1u << q;
         }
-      } else {
-        // LidarIntrinsics::project — lidar.hpp:43-55 (CUDA libm atan2/acos)
-        const double kTwoPi = 6.283185307179586;
-        double az = __dsub_rn(atan2(py, px), a.az0);
-        az = __dsub_rn(az, __dmul_rn(kTwoPi, floor(__ddiv_rn(az, kTwoPi))));
-        const double u = __dmul_rn(az, a.u_scale);
-        double c = __ddiv_rn(pz, d_v);
-        c = c < -1.0 ? -1.0 : (1.0 < c ? 1.0 : c);
-        const double v = __dmul_rn(__dsub_rn(acos(c), a.el0), a.v_scale);
-        if (!(u >= 0.0 && u < double(a.na) && v >= 0.0 && v < double(a.ne))) continue;
-        ok = a.linear ? sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s)
-                      : sample_nearest_d(a.depth, a.W, a.H, u, v, &s);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!((live >> q) & 1u) || !valid_depth_i(sd[q])) continue;
+          const float d_p = __fsub_rn(sd[q], dv[q]);  // integrator.cpp:116
+          if (d_p < -a.eps) continue;                 // tsdf_update — updates.hpp:39-54
+          float w_new = 1.0f;
+          if (a.inv_sq) {
+            const double dd = __dmul_rn(double(sd[q]), double(sd[q]));
+            w_new = __double2float_rn(__ddiv_rn(1.0, dd < 1e-6 ? 1e-6 : dd));
+          }
+          n_read += is_new ? 0u : 1u;
+          const float2 o = ov[q];
+          const float d_t = d_p < -a.eps ? -a.eps : (a.eps < d_p ? a.eps : d_p);
+          const float w_sum = __fadd_rn(o.y, w_new);
+          const float avg = __fdiv_rn(__fadd_rn(__fmul_rn(o.y, o.x), __fmul_rn(w_new, d_t)), w_sum);
+          float2 nv;
+          nv.x = avg < -a.eps ? -a.eps : (a.eps < avg ? a.eps : avg);
+          nv.y = a.max_weight < w_sum ? a.max_weight : w_sum;
+          if (__float_as_uint(nv.x) != __float_as_uint(o.x) || __float_as_uint(nv.y) != __float_as_uint(o.y)) {
+            blk[lane + 32 * (j0 + q)] = nv;
+            ++n_upd;
+            any = true;
+          }
+        }
       }
-      if (!ok) continue;
-      const float d_p = __fsub_rn(s, __double2float_rn(d_v));  // integrator.cpp:116
-      // tsdf_update — updates.hpp:39-54
-      if (d_p < -a.eps) continue;  // occluded: voxel unchanged
-      float w_new = 1.0f;
-      if (a.inv_sq) {
-        const double dd = __dmul_rn(double(s), double(s));
-        w_new = __double2float_rn(__ddiv_rn(1.0, dd < 1e-6 ? 1e-6 : dd));
-      }
-      const float2 old = is_new ? make_float2(0.0f, 0.0f) : blk[lin];
-      n_read += is_new ? 0u : 1u;
-      const float d_t = d_p < -a.eps ? -a.eps : (a.eps < d_p ? a.eps : d_p);
-      const float w_sum = __fadd_rn(old.y, w_new);
-      const float avg = __fdiv_rn(__fadd_rn(__fmul_rn(old.y, old.x), __fmul_rn(w_new, d_t)), w_sum);
-      float2 nv;
-      nv.x = avg < -a.eps ? -a.eps : (a.eps < avg ? a.eps : avg);
-      nv.y = a.max_weight < w_sum ? a.max_weight : w_sum;
-      if (__float_as_uint(nv.x) != __float_as_uint(old.x) ||
-          __float_as_uint(nv.y) != __float_as_uint(old.y)) {
-        blk[lin] = nv;
-        any = true;
-        ++n_upd;
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < 16; ++j) {
+        double px, py, pz;
+        centre_p(j, px, py, pz);
+        any |= integrate_voxel(a, blk, lane + 32 * j, px, py, pz, is_new, n_read, n_upd);
       }
     }
-    const int changed = __syncthreads_or(any);
-    if (threadIdx.x == 0) a.changed[ci] = uint8_t(changed);
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) a.changed[ci] = uint8_t(any);
   }
   n_read = __reduce_add_sync(0xffffffffu, n_read);
   n_upd = __reduce_add_sync(0xffffffffu, n_upd);
-  if ((threadIdx.x & 31) == 0 && (n_read | n_upd)) {
+  if (lane == 0 && (n_read | n_upd)) {
     DevStatus* sw = const_cast<DevStatus*>(st);
     atomicAdd(&sw->vox_read, n_read);
     atomicAdd(&sw->vox_upd, n_upd);
