@@ -1041,8 +1041,18 @@ static int lower_grid(Context* ctx) {
   return cached;
 }
 
+void launch_lower_xr(Context* ctx, LowerArgs& la);  // lower_xr.cu
+
 static void launch_lower(Context* ctx, LowerArgs& la) {
   static const bool trace = std::getenv("VXM_TRACE_LOWER") != nullptr;
+  static const bool xround = [] {
+    const char* e = std::getenv("VXM_LOWER_XROUND");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  if (la.full && la.dataflow && xround && !trace) {  // update_esdf: cross-round dataflow
+    launch_lower_xr(ctx, la);
+    return;
+  }
   static DevBuf trace_buf;
   if (trace) {
     trace_buf.ensure(512 * sizeof(unsigned long long));
@@ -1104,6 +1114,10 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.stamp_swept = E->stamp_swept;
   la.site_any = E->site_any;
   la.r1 = E->dirty_count + 7;
+  la.ring = E->dirty_count + 16;
+  la.dlist[0] = E->dlist[0];
+  la.dlist[1] = E->dlist[1];
+  la.capacity = E->capacity;
   static const int dataflow = [] {
     const char* e = std::getenv("VXM_LOWER_DATAFLOW");
     return e ? std::atoi(e) : 1;

@@ -483,6 +483,11 @@ struct LowerArgs {
   int dataflow;               // 1: pair items wait on dependencies; 0: phased barriers
   const uint8_t* site_any;    // [cap] 0: the block holds no site
   uint32_t* r1;               // [4] round-1 split: #site, #no-site, group / warp work counters
+  uint32_t* ring;             // cross-round lowering: [0..3] dirty counts, [4..7] sweep claims,
+                              // [8..11] pair claims, [12..15] pairs done (by round % 4), [16] last
+                              // completed round
+  unsigned long long* dlist[2];  // (epoch << 32 | slot) dirty lists by round parity
+  uint32_t capacity;             // slots of the layer (bounds every per-round list)
 };
 
 __device__ inline uint32_t ld_acquire(const uint32_t* p) {

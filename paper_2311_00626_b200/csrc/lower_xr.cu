@@ -1,0 +1,394 @@
+// Cross-round dataflow lowering for update_esdf (esdf/integrator.cpp:352-413,
+// 488-565): the same schedule as k_lower3 (esdf.cu) without a grid barrier
+// between rounds.
+//
+// k_lower3 ends every round with a grid barrier (the next dirty list must be
+// complete).  Here a round's end is a counter: every pair item of round R
+// increments done[R]; the item that completes the round zeroes the counters
+// of round R + 2 and publishes last_done = R.  Meanwhile sweep groups already
+// take round R + 1's dirty blocks as the pairs of round R append them (list
+// entries carry their round's epoch, so a slot is read only once written);
+// a block's sweep of round R + 1 waits only for the pairs of round R that
+// touch it (the reference's order: those pairs are the only writers of the
+// block since its last sweep).  Pair items of round R + 1 are taken once
+// round R is complete (their enumeration needs the final dirty list).  Every
+// wait is on an item some running warp has already claimed, and waits point
+// from round R + 1 to round R or from one axis to a lower one, so there is no
+// cycle.  The result is bit-identical to the barrier schedule.
+#include "esdf_lower.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace vxm {
+
+namespace {
+
+constexpr int kRingCnt = 0, kRingSwc = 4, kRingPc = 8, kRingDone = 12, kRingLast = 16;
+
+__device__ inline unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ GroupSmem s_grp[kL3Groups];
+  const int g = threadIdx.x >> 6, t = threadIdx.x & 63, lane = threadIdx.x & 31;
+  const int bar = 1 + g;
+  GroupSmem& G = s_grp[g];
+  const int wid = (blockIdx.x * kL3Threads + threadIdx.x) >> 5;
+  const int nwarps = gridDim.x * (kL3Threads >> 5);
+  const uint32_t n_blocks = a.meta->num_blocks;
+  const uint32_t cur = a.meta->cur;
+  const uint32_t base_epoch = a.meta->round_epoch;
+  const bool failed = a.status->capacity_error || a.status->pool_overflow;
+  const bool lower = !failed && a.status->any_update != 0;
+  uint32_t* const pcur = a.pool[cur];
+  uint32_t* const pnxt = a.pool[cur ^ 1u];
+  uint32_t* const work = pnxt;
+  const Limits lim = a.lim;
+  uint32_t* const ring = a.ring;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int q = 1; q <= 2; ++q) {  // rounds 1 and 2; later rounds are zeroed by round R - 2
+      ring[kRingCnt + q] = 0u;
+      ring[kRingSwc + q] = ring[kRingPc + q] = ring[kRingDone + q] = 0u;
+    }
+    ring[kRingLast] = 0u;
+  }
+  // round-1 split by site_any (as k_lower3)
+  if (lower) {
+    for (uint32_t b0 = blockIdx.x * kL3Threads + (threadIdx.x & ~31u); b0 < n_blocks;
+         b0 += gridDim.x * kL3Threads) {
+      const uint32_t b = b0 + lane;
+      const bool in = b < n_blocks;
+      const bool site = in && a.site_any[b] != 0;
+      const uint32_t ms = __ballot_sync(0xffffffffu, site), mn = __ballot_sync(0xffffffffu, in && !site);
+      uint32_t bs = 0, bn = 0;
+      if (lane == 0) {
+        if (ms) bs = atomicAdd(a.r1 + 0, __popc(ms));
+        if (mn) bn = atomicAdd(a.r1 + 1, __popc(mn));
+      }
+      bs = __shfl_sync(0xffffffffu, bs, 0);
+      bn = __shfl_sync(0xffffffffu, bn, 0);
+      const uint32_t below = (1u << lane) - 1u;
+      if (site) a.list[1][bs + __popc(ms & below)] = int32_t(b);
+      else if (in) a.list[1][n_blocks - 1u - (bn + __popc(mn & below))] = int32_t(b);
+    }
+  }
+  grid.sync();
+  uint32_t n_pairs = 0, n_cmp = 0, rounds = 0;
+  if (lower && n_blocks > 0) {
+    for (uint32_t R = 1;; ++R) {
+      const uint32_t ep = base_epoch + R, ep_next = ep + 1;
+      const int cp = int(R & 1u), np = cp ^ 1;
+      const bool r1 = R == 1;
+      const int q4 = int(R & 3u), q4n = int((R + 1u) & 3u);
+      // ---- sweeps of round R (esdf/integrator.cpp:509-513) -------------------
+      if (r1) {
+        const uint32_t n_grp = *((volatile uint32_t*)(a.r1 + 0));
+        while (true) {
+          if (t == 0) G.bcast = atomicAdd(a.r1 + 2, 1u);
+          group_sync(bar);
+          const uint32_t i = G.bcast;
+          if (i >= n_grp) break;
+          const int32_t s = __ldcg(a.list[1] + i);
+          if (t == 0) {
+            G.mask[0][0] = G.mask[1][0] = G.mask[2][0] = ~0ull;
+            G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
+          }
+          RawBlock rb;
+          bool any_site, fast;
+          load_raw3(rb, pcur + size_t(s) * 1536, t, bar, lim, true, &any_site, &fast);
+          if (!any_site) {
+            raw_store(rb, work + size_t(s) * 1536, t);
+          } else {
+            stage_block3(G, rb, t, bar, lim, fast);
+            sweep_block3(G, t, bar, lim);
+            store_block3(G, work + size_t(s) * 1536, t);
+          }
+          group_sync(bar);
+          if (t == 0) st_release(a.stamp_swept + s, ep);
+        }
+        const uint32_t n_ns = *((volatile uint32_t*)(a.r1 + 1));
+        constexpr uint32_t kCopyChunk = 2;
+        uint32_t j = 0, j_end = 0;
+        while (true) {  // site-free blocks: reset + copy, one warp each
+          if (j == j_end) {
+            if (lane == 0) j = atomicAdd(a.r1 + 3, kCopyChunk);
+            j = __shfl_sync(0xffffffffu, j, 0);
+            j_end = j + kCopyChunk;
+          }
+          if (j >= n_ns) break;
+          const int32_t s = __ldcg(a.list[1] + (n_blocks - 1u - j));
+          ++j;
+          warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
+          __syncwarp();
+          if (lane == 0) st_release(a.stamp_swept + s, ep);
+        }
+      } else {
+        const unsigned long long* dl = a.dlist[cp];
+        while (true) {
+          if (t == 0) {
+            // claim the next dirty block of round R; its slot is written by the
+            // round R - 1 pair that changed it (epoch-tagged), or the list ends
+            // once round R - 1 is complete
+            const uint32_t i = atomicAdd(ring + kRingSwc + q4, 1u);
+            int32_t s = -1;
+            for (uint32_t it = 0; i < a.capacity; ++it) {  // (a round never lists more)
+              const unsigned long long e = ld_relaxed64(dl + i);
+              if (uint32_t(e >> 32) == ep) {
+                s = int32_t(uint32_t(e));
+                break;
+              }
+              if (ld_acquire(ring + kRingLast) + 1u >= R &&
+                  i >= *((volatile uint32_t*)(ring + kRingCnt + q4))) {
+                const unsigned long long e2 = ld_relaxed64(dl + i);  // (written before the count)
+                if (uint32_t(e2 >> 32) == ep) s = int32_t(uint32_t(e2));
+                break;
+              }
+              if (it > (1u << 24)) {  // a lost producer is a bug, never a hang
+                if (atomicExch(&a.status->watchdog, 1u) == 0u) a.status->pad3[0] = 40u;
+                break;
+              }
+              __nanosleep(32);
+            }
+            G.bcast = uint32_t(s);
+          }
+          group_sync(bar);
+          const int32_t s = int32_t(G.bcast);
+          if (s < 0) break;
+          // the block's round R - 1 pairs (the reference's only writers of it since
+          // its last sweep) must be complete: lanes 0-5 of the group's first warp
+          if (t < 6) {
+            const int q = t >> 1;
+            const int32_t c = __ldg(a.nbr + size_t(s) * 6 + t);  // +q (even t) / -q (odd t)
+            if (c >= 0) {
+              const uint32_t epp = ep - 1;  // round R - 1
+              const bool r1p = R - 1 == 1;
+              const bool exists = r1p || __ldcg(a.stamp_dirty[np] + s) == epp ||
+                                  __ldcg(a.stamp_dirty[np] + c) == epp;
+              if (exists) {
+                const int32_t lo = (t & 1) ? c : s;
+                wait_stamp(a.stamp_pair[q] + lo, epp, &a.status->watchdog, 30u + q, lo);
+              }
+            }
+          }
+          group_sync(bar);  // every wait done before the masks and voxels are read
+          if (t == 0) {
+            G.mask[0][0] = atomicExch(a.line_mask + 3 * size_t(s), 0ull);
+            G.mask[1][0] = atomicExch(a.line_mask + 3 * size_t(s) + 1, 0ull);
+            G.mask[2][0] = atomicExch(a.line_mask + 3 * size_t(s) + 2, 0ull);
+            G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
+          }
+          group_sync(bar);
+          RawBlock rb;
+          bool any_site, fast;
+          load_raw3(rb, work + size_t(s) * 1536, t, bar, lim, false, &any_site, &fast);
+          stage_block3(G, rb, t, bar, lim, fast);
+          if (sweep_block3(G, t, bar, lim)) store_block3(G, work + size_t(s) * 1536, t);
+          group_sync(bar);  // the group's stores before the release of its sweep stamp
+          if (t == 0) st_release(a.stamp_swept + s, ep);
+        }
+      }
+      // ---- border phase of round R (esdf/integrator.cpp:517-559) ----------------
+      if (!r1) {  // enumeration needs the final round-R list: round R - 1 complete
+        for (uint32_t it = 0; ld_acquire(ring + kRingLast) + 1u < R; ++it) {
+          if (it > (1u << 24)) {
+            if (atomicExch(&a.status->watchdog, 1u) == 0u) a.status->pad3[0] = 41u;
+            break;
+          }
+          __nanosleep(32);
+        }
+      }
+      const uint32_t n_dirty = r1 ? n_blocks : *((volatile uint32_t*)(ring + kRingCnt + q4));
+      if (n_dirty == 0) break;  // while (!dirty.empty()) — esdf/integrator.cpp:506
+      rounds = R;
+      const unsigned long long* dl = a.dlist[cp];
+      auto dirty_at = [&](uint32_t i) -> int32_t { return r1 ? int32_t(i) : int32_t(uint32_t(__ldcg(dl + i))); };
+      auto is_dirty = [&](int32_t b) { return r1 || __ldcg(a.stamp_dirty[cp] + b) == ep; };
+      const uint32_t sides = r1 ? 1u : 2u;
+      const uint32_t per_axis = sides * n_dirty;
+      const uint32_t n_items = 3u * per_axis;
+      while (true) {
+        uint32_t w = 0;
+        if (lane == 0) w = atomicAdd(ring + kRingPc + q4, 1u);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= n_items) break;
+        const int axis = int(w / per_axis);
+        const uint32_t rest = w - uint32_t(axis) * per_axis;
+        const uint32_t i = r1 ? rest : rest >> 1;
+        const int side = r1 ? 0 : int(rest & 1u);
+        const int32_t d = dirty_at(i);
+        int32_t lo = -1, hi = -1;
+        if (side == 0) {
+          hi = __ldg(a.nbr + size_t(d) * 6 + 2 * axis);  // d + axis
+          lo = d;
+        } else {
+          lo = __ldg(a.nbr + size_t(d) * 6 + 2 * axis + 1);  // d - axis
+          hi = d;
+          if (lo >= 0 && is_dirty(lo)) lo = -1;  // lo's side-0 item has this pair
+        }
+        if (lo >= 0 && hi >= 0) {
+          bool dep_chg = false;
+          if (lane < 2 + 4 * axis) {
+            if (lane < 2) {
+              const int32_t b = lane == 0 ? lo : hi;
+              if (is_dirty(b)) wait_stamp(a.stamp_swept + b, ep, &a.status->watchdog, 10u + axis, b);
+            } else {
+              const int q = (lane - 2) >> 2;
+              const int32_t b = ((lane - 2) & 2) ? hi : lo;
+              const bool b_is_hi = ((lane - 2) & 1) == 0;
+              int32_t c = b;
+              if (b_is_hi) c = __ldg(a.nbr + size_t(b) * 6 + 2 * q + 1);
+              if (c >= 0) {
+                const int32_t n = __ldg(a.nbr + size_t(c) * 6 + 2 * q);
+                if (n >= 0 && (is_dirty(c) || is_dirty(n))) {
+                  const uint32_t v =
+                      wait_stamp(a.stamp_pair[q] + c, ep, &a.status->watchdog, 20u + 10u * q + axis, c);
+                  dep_chg = (v & (b_is_hi ? kStampHiChg : kStampLoChg)) != 0u;
+                }
+              }
+            }
+          }
+          const uint32_t chg_mask = __ballot_sync(0xffffffffu, dep_chg);
+          __syncwarp();
+          bool skip = false;
+          if (r1) {  // no giver on either face: the pair is the identity (k_lower3)
+            constexpr uint32_t lo_lanes = 0x0ccu, hi_lanes = 0x330u;
+            const bool g_lo = a.site_any[lo] != 0 || (chg_mask & lo_lanes) != 0u;
+            const bool g_hi = a.site_any[hi] != 0 || (chg_mask & hi_lanes) != 0u;
+            skip = !g_lo && !g_hi;
+          }
+          if (skip) {
+            if (lane == 0) st_release(a.stamp_pair[axis] + lo, ep);
+          } else {
+            const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
+            bool ac = false, bc = false;
+            unsigned long long mlo[3] = {0, 0, 0}, mhi[3] = {0, 0, 0};
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
+              int ax, ay, az, bx, by, bz;
+              if (axis == 0) { ax = 7; ay = i0; az = j0; bx = 0; by = i0; bz = j0; }
+              else if (axis == 1) { ax = i0; ay = 7; az = j0; bx = i0; by = 0; bz = j0; }
+              else { ax = i0; ay = j0; az = 7; bx = i0; by = j0; bz = 0; }
+              const int la = ax + 8 * ay + 64 * az, lb = bx + 8 * by + 64 * bz;
+              EV va = load_voxel(work, lo, la), vb = load_voxel(work, hi, lb);
+              const bool cb = relax(vb, va, dx, dy, dz, lim);     // exchange_pair :158
+              const bool ca = relax(va, vb, -dx, -dy, -dz, lim);  // :159
+              if (cb) {
+                store_voxel(work, hi, lb, vb);
+                line_bits(bx, by, bz, mhi);
+              }
+              if (ca) {
+                store_voxel(work, lo, la, va);
+                line_bits(ax, ay, az, mlo);
+              }
+              ac |= ca;
+              bc |= cb;
+            }
+            ac = __any_sync(0xffffffffu, ac);
+            bc = __any_sync(0xffffffffu, bc);
+            ++n_pairs;
+            // line masks before the release: a round R + 1 sweep of the block may
+            // start as soon as its pairs' stamps are out
+            const int32_t who[2] = {lo, hi};
+            const bool chg[2] = {ac, bc};
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+              if (!chg[qq]) continue;
+              unsigned long long* m = qq == 0 ? mlo : mhi;
+              const unsigned long long r0 = warp_or64(m[0]), r1m = warp_or64(m[1]), r2 = warp_or64(m[2]);
+              if (lane == 0) {
+                atomicOr(a.line_mask + 3 * size_t(who[qq]), r0);
+                atomicOr(a.line_mask + 3 * size_t(who[qq]) + 1, r1m);
+                atomicOr(a.line_mask + 3 * size_t(who[qq]) + 2, r2);
+              }
+            }
+            __syncwarp();
+            if (lane == 0)
+              st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));
+            if (lane == 0) {
+#pragma unroll
+              for (int qq = 0; qq < 2; ++qq) {
+                if (!chg[qq]) continue;
+                if (atomicMax(a.stamp_dirty[np] + who[qq], ep_next) < ep_next) {
+                  const uint32_t slot = atomicAdd(ring + kRingCnt + q4n, 1u);
+                  *(volatile unsigned long long*)(a.dlist[np] + slot) =
+                      (unsigned long long)ep_next << 32 | uint32_t(who[qq]);
+                }
+              }
+            }
+          }
+        }
+        // round accounting: the item completing round R publishes it
+        if (lane == 0) {
+          __threadfence();
+          const uint32_t done = atomicAdd(ring + kRingDone + q4, 1u) + 1u;
+          if (done == n_items) {
+            __threadfence();
+            const int q4nn = int((R + 2u) & 3u);
+            ring[kRingCnt + q4nn] = 0u;
+            ring[kRingSwc + q4nn] = ring[kRingPc + q4nn] = ring[kRingDone + q4nn] = 0u;
+            if (R > 1) a.status->sum_dirty += n_dirty;
+            __threadfence();
+            st_release(ring + kRingLast, R);
+          }
+        }
+      }
+      // the next round's sweeps re-form the groups (both warps)
+      group_sync(bar);
+    }
+  }
+  grid.sync();
+  // ---- changed set of update_esdf (esdf/integrator.cpp:403-411) ------------------
+  for (uint32_t k = wid; k < n_blocks; k += nwarps) {
+    const int32_t s = a.sorted_slots[k];
+    bool ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
+    if (!ch && lower) {
+      const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(s) * 1536);
+      const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(s) * 1536);
+      bool diff = false;
+#pragma unroll 4
+      for (int q = lane; q < 384; q += 32) {
+        const uint4 x = __ldcg(p0 + q), y = __ldcg(p1 + q);
+        diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+      }
+      ch = __any_sync(0xffffffffu, diff);
+      ++n_cmp;
+    }
+    if (lane == 0) a.out_flags[k] = uint8_t(ch);
+  }
+  if (lane == 0 && (n_pairs | n_cmp)) {
+    atomicAdd(&a.status->sum_pairs, n_pairs);
+    atomicAdd(&a.status->cmp_blocks, n_cmp);
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.r1[0] = a.r1[1] = a.r1[2] = a.r1[3] = 0u;  // zero for the next launch
+    a.status->rounds = rounds;
+    a.status->n_esdf_blocks = n_blocks;
+    a.meta->round_epoch = base_epoch + rounds + 2;
+    if (lower) a.meta->cur = cur ^ 1u;
+  }
+}
+
+void launch_lower_xr(Context* ctx, LowerArgs& la) {
+  static int grid = 0;
+  if (!grid) {
+    int bps = 0;
+    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lower_xr, kL3Threads, 0));
+    grid = std::max(1, std::min(bps, 4)) * ctx->sm_count;
+  }
+  void* args[] = {&la};
+  ctx->prof_begin("k_lower");
+  VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lower_xr, dim3(grid), dim3(kL3Threads), args, 0,
+                                       ctx->stream));
+  ctx->prof_end();
+  ctx->count_launch();
+}
+
+}  // namespace vxm

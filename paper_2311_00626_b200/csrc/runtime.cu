@@ -197,6 +197,7 @@ void Layer::ensure_capacity(uint64_t need) {
     grow_copy(&line_mask, capacity * 3ull, live * 3ull, nc * 3ull, 0, st);
     grow_copy(&stamp_swept, capacity, live, nc, 0, st);
     grow_copy(&site_any, capacity, live, nc, 0, st);
+    for (int i = 0; i < 2; ++i) grow_copy(&dlist[i], capacity, 0, nc, 0, st);
     for (int a = 0; a < 3; ++a) grow_copy(&stamp_pair[a], capacity, live, nc, 0, st);
   }
   // hash: power of two >= 2 * capacity, rebuilt from slot_keys
@@ -248,6 +249,8 @@ Layer::~Layer() {
   if (line_mask) cudaFree(line_mask);
   if (stamp_swept) cudaFree(stamp_swept);
   if (site_any) cudaFree(site_any);
+  for (unsigned long long* p : dlist)
+    if (p) cudaFree(p);
   for (uint32_t* p : stamp_pair)
     if (p) cudaFree(p);
 }
