@@ -19,6 +19,14 @@
 
 namespace cg = cooperative_groups;
 
+// Line masks (which lines a round's pairs touched) let a sweep skip idempotent
+// lines; here they would have to be published before each pair's release,
+// which lengthens the pair chains — the sweeps of rounds >= 2 start from all
+// lines instead (the same result: an unchanged line is idempotent).
+#ifndef XR_LINE_MASKS
+#define XR_LINE_MASKS 0
+#endif
+
 namespace vxm {
 
 namespace {
@@ -177,10 +185,14 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
             }
           }
           group_sync(bar);  // every wait done before the masks and voxels are read
-          if (t == 0) {
+          if (t == 0) {  // XR_MASKS
+#if XR_LINE_MASKS
             G.mask[0][0] = atomicExch(a.line_mask + 3 * size_t(s), 0ull);
             G.mask[1][0] = atomicExch(a.line_mask + 3 * size_t(s) + 1, 0ull);
             G.mask[2][0] = atomicExch(a.line_mask + 3 * size_t(s) + 2, 0ull);
+#else
+            G.mask[0][0] = G.mask[1][0] = G.mask[2][0] = ~0ull;
+#endif
             G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
           }
           group_sync(bar);
@@ -297,6 +309,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
             // start as soon as its pairs' stamps are out
             const int32_t who[2] = {lo, hi};
             const bool chg[2] = {ac, bc};
+#if XR_LINE_MASKS
 #pragma unroll
             for (int qq = 0; qq < 2; ++qq) {
               if (!chg[qq]) continue;
@@ -308,6 +321,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
                 atomicOr(a.line_mask + 3 * size_t(who[qq]) + 2, r2);
               }
             }
+#endif
             __syncwarp();
             if (lane == 0)
               st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));
