@@ -1043,13 +1043,21 @@ static int lower_grid(Context* ctx) {
 
 void launch_lower_xr(Context* ctx, LowerArgs& la);  // lower_xr.cu
 
-static void launch_lower(Context* ctx, LowerArgs& la) {
+// The cross-round kernel removes the per-round barrier and overlaps rounds:
+// a win while rounds are latency-bound (maps of up to tens of thousands of
+// blocks, e.g. C2: 0.26 -> 0.18 ms).  Very large maps are throughput-bound
+// (thousands of dirty blocks per group-round), where the per-block dependency
+// waits cost more than the barrier: they keep the barrier schedule.
+constexpr uint32_t kXrMaxBlocks = 48 * 1024;
+
+static void launch_lower(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
   static const bool trace = std::getenv("VXM_TRACE_LOWER") != nullptr;
-  static const bool xround = [] {
-    const char* e = std::getenv("VXM_LOWER_XROUND");
-    return e ? std::atoi(e) != 0 : true;
+  static const int xround = [] {
+    const char* e = std::getenv("VXM_LOWER_XROUND");  // 0 never, 1 by map size, 2 always
+    return e ? std::atoi(e) : 1;
   }();
-  if (la.full && la.dataflow && xround && !trace) {  // update_esdf: cross-round dataflow
+  if (la.full && la.dataflow && !trace &&
+      (xround == 2 || (xround == 1 && n_blocks_hint <= kXrMaxBlocks))) {  // update_esdf
     launch_lower_xr(ctx, la);
     return;
   }
@@ -1118,6 +1126,7 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.dlist[0] = E->dlist[0];
   la.dlist[1] = E->dlist[1];
   la.capacity = E->capacity;
+  for (int i = 0; i < 3; ++i) la.pair_face[i] = E->pair_face[i];
   static const int dataflow = [] {
     const char* e = std::getenv("VXM_LOWER_DATAFLOW");
     return e ? std::atoi(e) : 1;
@@ -1152,7 +1161,7 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
   la.stamp_mark = E->stamp_mark;
   la.call_epoch = epoch;
   la.out_flags = s.flags;
-  launch_lower(ctx, la);
+  launch_lower(ctx, la, E->num_blocks);
   check_launch(ctx, "k_lower");
   changed_out->ensure(n_all_cap);
   launch_compact_keys(ctx, E->sorted_keys[E->sorted_parity], s.flags, &E->meta->num_blocks,
@@ -1353,7 +1362,7 @@ int run_lower_esdf(Layer* E, EsdfState* st, const vxm_esdf_config& cfg,
   la.seeds = dslots.as<int32_t>();
   la.n_seeds = dn.as<uint32_t>();
   la.lchg_tag = tag;
-  launch_lower(ctx, la);
+  launch_lower(ctx, la, E->num_blocks);
   check_launch(ctx, "k_lower(seeded)");
   const uint32_t n_all = E->num_blocks;
   DevBuf dflags, dnall;

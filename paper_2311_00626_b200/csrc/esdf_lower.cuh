@@ -488,6 +488,7 @@ struct LowerArgs {
                               // completed round
   unsigned long long* dlist[2];  // (epoch << 32 | slot) dirty lists by round parity
   uint32_t capacity;             // slots of the layer (bounds every per-round list)
+  unsigned long long* pair_face[3];  // [cap][2] (by lower block): face voxels the pair changed
 };
 
 __device__ inline uint32_t ld_acquire(const uint32_t* p) {

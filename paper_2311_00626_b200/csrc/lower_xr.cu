@@ -19,19 +19,43 @@
 
 namespace cg = cooperative_groups;
 
-// Line masks (which lines a round's pairs touched) let a sweep skip idempotent
-// lines; here they would have to be published before each pair's release,
-// which lengthens the pair chains — the sweeps of rounds >= 2 start from all
-// lines instead (the same result: an unchanged line is idempotent).
-#ifndef XR_LINE_MASKS
-#define XR_LINE_MASKS 0
-#endif
+// Line masks (which lines a round's pairs touched, so a sweep skips idempotent
+// lines): a pair stores the 64-bit masks of the face voxels it changed next to
+// its stamp, before the stamp's release — plain stores ordered by the release
+// it pays anyway, no atomics — and a sweep derives its lines from the faces of
+// the pairs it waits for.
 
 namespace vxm {
 
 namespace {
 
 constexpr int kRingCnt = 0, kRingSwc = 4, kRingPc = 8, kRingDone = 12, kRingLast = 16;
+
+// Lines of a block through the voxels of one face (bit i0 + 8 j0 of F) that a
+// pair along `axis` changed; `face` is the face's coordinate (0 or 7).  The
+// same bits line_bits() sets voxel by voxel.
+__device__ inline void face_lines(unsigned long long F, int axis, int face, unsigned long long m[3]) {
+  uint32_t rows = 0, cols = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t byte = uint32_t(F >> (8 * j)) & 0xffu;
+    rows |= uint32_t(byte != 0u) << j;
+    cols |= byte;
+  }
+  if (axis == 0) {         // (i0, j0) = (y, z), x = face
+    m[0] |= F;
+    m[1] |= spread8(rows) << face;
+    m[2] |= spread8(cols) << face;
+  } else if (axis == 1) {  // (i0, j0) = (x, z), y = face
+    m[0] |= spread8(rows) << face;
+    m[1] |= F;
+    m[2] |= (unsigned long long)cols << (8 * face);
+  } else {                 // (i0, j0) = (x, y), z = face
+    m[0] |= (unsigned long long)rows << (8 * face);
+    m[1] |= (unsigned long long)cols << (8 * face);
+    m[2] |= F;
+  }
+}
 
 __device__ inline unsigned long long ld_relaxed64(const unsigned long long* p) {
   unsigned long long v;
@@ -169,33 +193,36 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
           const int32_t s = int32_t(G.bcast);
           if (s < 0) break;
           // the block's round R - 1 pairs (the reference's only writers of it since
-          // its last sweep) must be complete: lanes 0-5 of the group's first warp
-          if (t < 6) {
-            const int q = t >> 1;
-            const int32_t c = __ldg(a.nbr + size_t(s) * 6 + t);  // +q (even t) / -q (odd t)
-            if (c >= 0) {
-              const uint32_t epp = ep - 1;  // round R - 1
-              const bool r1p = R - 1 == 1;
-              const bool exists = r1p || __ldcg(a.stamp_dirty[np] + s) == epp ||
-                                  __ldcg(a.stamp_dirty[np] + c) == epp;
-              if (exists) {
-                const int32_t lo = (t & 1) ? c : s;
-                wait_stamp(a.stamp_pair[q] + lo, epp, &a.status->watchdog, 30u + q, lo);
+          // its last sweep) must be complete: lanes 0-5 of the group's first warp;
+          // the faces they changed give the lines to sweep first
+          if (t < 32) {
+            unsigned long long m[3] = {0, 0, 0};
+            if (t < 6) {
+              const int q = t >> 1;
+              const int32_t c = __ldg(a.nbr + size_t(s) * 6 + t);  // +q (even t) / -q (odd t)
+              if (c >= 0) {
+                const uint32_t epp = ep - 1;  // round R - 1
+                const bool r1p = R - 1 == 1;
+                const bool exists = r1p || __ldcg(a.stamp_dirty[np] + s) == epp ||
+                                    __ldcg(a.stamp_dirty[np] + c) == epp;
+                if (exists) {
+                  const bool s_lo = (t & 1) == 0;  // pair (s, c) or (c, s)
+                  const int32_t lo = s_lo ? s : c;
+                  const uint32_t v = wait_stamp(a.stamp_pair[q] + lo, epp, &a.status->watchdog, 30u + q, lo);
+                  if (v & (s_lo ? kStampLoChg : kStampHiChg))
+                    face_lines(__ldcg(a.pair_face[q] + 2 * size_t(lo) + (s_lo ? 0 : 1)), q, s_lo ? 7 : 0, m);
+                }
               }
+            }
+            const unsigned long long m0 = warp_or64(m[0]), m1 = warp_or64(m[1]), m2 = warp_or64(m[2]);
+            if (t == 0) {
+              G.mask[0][0] = m0;
+              G.mask[1][0] = m1;
+              G.mask[2][0] = m2;
+              G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
             }
           }
           group_sync(bar);  // every wait done before the masks and voxels are read
-          if (t == 0) {  // XR_MASKS
-#if XR_LINE_MASKS
-            G.mask[0][0] = atomicExch(a.line_mask + 3 * size_t(s), 0ull);
-            G.mask[1][0] = atomicExch(a.line_mask + 3 * size_t(s) + 1, 0ull);
-            G.mask[2][0] = atomicExch(a.line_mask + 3 * size_t(s) + 2, 0ull);
-#else
-            G.mask[0][0] = G.mask[1][0] = G.mask[2][0] = ~0ull;
-#endif
-            G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
-          }
-          group_sync(bar);
           RawBlock rb;
           bool any_site, fast;
           load_raw3(rb, work + size_t(s) * 1536, t, bar, lim, false, &any_site, &fast);
@@ -278,8 +305,8 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
             if (lane == 0) st_release(a.stamp_pair[axis] + lo, ep);
           } else {
             const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
-            bool ac = false, bc = false;
-            unsigned long long mlo[3] = {0, 0, 0}, mhi[3] = {0, 0, 0};
+            // the faces this pair changes, bit = face position lane + 32 k
+            unsigned long long flo = 0, fhi = 0;
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
@@ -291,37 +318,19 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
               EV va = load_voxel(work, lo, la), vb = load_voxel(work, hi, lb);
               const bool cb = relax(vb, va, dx, dy, dz, lim);     // exchange_pair :158
               const bool ca = relax(va, vb, -dx, -dy, -dz, lim);  // :159
-              if (cb) {
-                store_voxel(work, hi, lb, vb);
-                line_bits(bx, by, bz, mhi);
-              }
-              if (ca) {
-                store_voxel(work, lo, la, va);
-                line_bits(ax, ay, az, mlo);
-              }
-              ac |= ca;
-              bc |= cb;
+              if (cb) store_voxel(work, hi, lb, vb);
+              if (ca) store_voxel(work, lo, la, va);
+              flo |= (unsigned long long)__ballot_sync(0xffffffffu, ca) << (32 * k);
+              fhi |= (unsigned long long)__ballot_sync(0xffffffffu, cb) << (32 * k);
             }
-            ac = __any_sync(0xffffffffu, ac);
-            bc = __any_sync(0xffffffffu, bc);
             ++n_pairs;
-            // line masks before the release: a round R + 1 sweep of the block may
-            // start as soon as its pairs' stamps are out
+            const bool ac = flo != 0ull, bc = fhi != 0ull;
             const int32_t who[2] = {lo, hi};
             const bool chg[2] = {ac, bc};
-#if XR_LINE_MASKS
-#pragma unroll
-            for (int qq = 0; qq < 2; ++qq) {
-              if (!chg[qq]) continue;
-              unsigned long long* m = qq == 0 ? mlo : mhi;
-              const unsigned long long r0 = warp_or64(m[0]), r1m = warp_or64(m[1]), r2 = warp_or64(m[2]);
-              if (lane == 0) {
-                atomicOr(a.line_mask + 3 * size_t(who[qq]), r0);
-                atomicOr(a.line_mask + 3 * size_t(who[qq]) + 1, r1m);
-                atomicOr(a.line_mask + 3 * size_t(who[qq]) + 2, r2);
-              }
+            if (lane == 0) {  // the changed faces, published by the release below
+              if (ac) a.pair_face[axis][2 * size_t(lo)] = flo;
+              if (bc) a.pair_face[axis][2 * size_t(lo) + 1] = fhi;
             }
-#endif
             __syncwarp();
             if (lane == 0)
               st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));

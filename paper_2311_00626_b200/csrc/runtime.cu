@@ -198,6 +198,7 @@ void Layer::ensure_capacity(uint64_t need) {
     grow_copy(&stamp_swept, capacity, live, nc, 0, st);
     grow_copy(&site_any, capacity, live, nc, 0, st);
     for (int i = 0; i < 2; ++i) grow_copy(&dlist[i], capacity, 0, nc, 0, st);
+    for (int i = 0; i < 3; ++i) grow_copy(&pair_face[i], capacity * 2ull, 0, nc * 2ull, 0, st);
     for (int a = 0; a < 3; ++a) grow_copy(&stamp_pair[a], capacity, live, nc, 0, st);
   }
   // hash: power of two >= 2 * capacity, rebuilt from slot_keys
@@ -250,6 +251,8 @@ Layer::~Layer() {
   if (stamp_swept) cudaFree(stamp_swept);
   if (site_any) cudaFree(site_any);
   for (unsigned long long* p : dlist)
+    if (p) cudaFree(p);
+  for (unsigned long long* p : pair_face)
     if (p) cudaFree(p);
   for (uint32_t* p : stamp_pair)
     if (p) cudaFree(p);

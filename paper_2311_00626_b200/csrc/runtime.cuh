@@ -113,6 +113,7 @@ struct Layer {
   uint32_t* dirty_count = nullptr;  // [64]: list counts, work counters, round-1 split counters,
                                     // [16..32] the cross-round lowering's per-round ring
   unsigned long long* dlist[2] = {nullptr, nullptr};  // [cap] (epoch << 32 | slot) dirty lists
+  unsigned long long* pair_face[3] = {nullptr, nullptr, nullptr};  // [cap][2] faces a pair changed
   unsigned long long* line_mask = nullptr;  // [cap][3] lines changed by border phases
   uint32_t* stamp_swept = nullptr;          // round epoch of the block's last sweep
   uint8_t* site_any = nullptr;              // 0: the block holds no site (exact or conservative 1)

@@ -1,0 +1,21 @@
+"""Every lowering kernel the library may select is bit-identical to the
+oracle: the cross-round kernel (k_lower_xr, maps up to kXrMaxBlocks), the
+barrier-per-round dataflow kernel (k_lower3, larger maps) and its phased form
+(grid barrier before every border axis).  The selection is process-wide, so
+each variant runs tests/lower_variant_check.py in its own process."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("env", [{"VXM_LOWER_XROUND": "2"}, {"VXM_LOWER_XROUND": "0"},
+                                 {"VXM_LOWER_XROUND": "0", "VXM_LOWER_DATAFLOW": "0"}])
+def test_lowering_variant_bitwise(env):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "lower_variant_check.py")],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
