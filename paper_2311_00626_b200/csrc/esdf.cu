@@ -1056,7 +1056,7 @@ static void launch_lower(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
     const char* e = std::getenv("VXM_LOWER_XROUND");  // 0 never, 1 by map size, 2 always
     return e ? std::atoi(e) : 1;
   }();
-  if (la.full && la.dataflow && !trace &&
+  if (la.full && la.dataflow && !trace &&  // (VXM_TRACE_LOWER traces k_lower3)
       (xround == 2 || (xround == 1 && n_blocks_hint <= kXrMaxBlocks))) {  // update_esdf
     launch_lower_xr(ctx, la);
     return;
@@ -1127,6 +1127,7 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.dlist[1] = E->dlist[1];
   la.capacity = E->capacity;
   for (int i = 0; i < 3; ++i) la.pair_face[i] = E->pair_face[i];
+
   static const int dataflow = [] {
     const char* e = std::getenv("VXM_LOWER_DATAFLOW");
     return e ? std::atoi(e) : 1;

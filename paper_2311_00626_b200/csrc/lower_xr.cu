@@ -15,6 +15,9 @@
 // wait is on an item some running warp has already claimed, and waits point
 // from round R + 1 to round R or from one axis to a lower one, so there is no
 // cycle.  The result is bit-identical to the barrier schedule.
+#include <cstdio>
+#include <cstdlib>
+
 #include "esdf_lower.cuh"
 
 namespace cg = cooperative_groups;
@@ -30,6 +33,10 @@ namespace vxm {
 namespace {
 
 constexpr int kRingCnt = 0, kRingSwc = 4, kRingPc = 8, kRingDone = 12, kRingLast = 16;
+#ifndef XR_R1_CHUNK
+#define XR_R1_CHUNK 1
+#endif
+constexpr uint32_t kR1Chunk = XR_R1_CHUNK;
 
 // Lines of a block through the voxels of one face (bit i0 + 8 j0 of F) that a
 // pair along `axis` changed; `face` is the face's coordinate (0 or 7).  The
@@ -111,6 +118,11 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
     }
   }
   grid.sync();
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long tm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+    a.trace[0] = tm;
+  }
   uint32_t n_pairs = 0, n_cmp = 0, rounds = 0;
   if (lower && n_blocks > 0) {
     for (uint32_t R = 1;; ++R) {
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
                 }
               }
             }
-            const unsigned long long m0 = warp_or64(m[0]), m1 = warp_or64(m[1]), m2 = warp_or64(m[2]);
+            unsigned long long m0 = warp_or64(m[0]), m1 = warp_or64(m[1]), m2 = warp_or64(m[2]);
             if (t == 0) {
               G.mask[0][0] = m0;
               G.mask[1][0] = m1;
@@ -251,13 +263,21 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
       const uint32_t sides = r1 ? 1u : 2u;
       const uint32_t per_axis = sides * n_dirty;
       const uint32_t n_items = 3u * per_axis;
+      uint32_t my_done = 0;
+      // one item per claim: a warp blocked on a dependency must not hold later
+      // items (measured on C2: chunks of 4 / 16 in round 1 cost 2 % / 34 %)
+      const uint32_t chunk = r1 ? kR1Chunk : 1u;
+      uint32_t w = 0, w_end = 0;
       while (true) {
-        uint32_t w = 0;
-        if (lane == 0) w = atomicAdd(ring + kRingPc + q4, 1u);
-        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w == w_end) {
+          if (lane == 0) w = atomicAdd(ring + kRingPc + q4, chunk);
+          w = __shfl_sync(0xffffffffu, w, 0);
+          w_end = w + chunk;
+        }
         if (w >= n_items) break;
-        const int axis = int(w / per_axis);
-        const uint32_t rest = w - uint32_t(axis) * per_axis;
+        const uint32_t wi = w++;
+        const int axis = int(wi / per_axis);
+        const uint32_t rest = wi - uint32_t(axis) * per_axis;
         const uint32_t i = r1 ? rest : rest >> 1;
         const int side = r1 ? 0 : int(rest & 1u);
         const int32_t d = dirty_at(i);
@@ -347,19 +367,26 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
             }
           }
         }
-        // round accounting: the item completing round R publishes it
-        if (lane == 0) {
+        ++my_done;
+      }
+      // round accounting, one atomic per warp: the warp whose items complete
+      // round R publishes it (every item this warp claimed is done here)
+      if (lane == 0 && my_done) {
+        __threadfence();
+        const uint32_t done = atomicAdd(ring + kRingDone + q4, my_done) + my_done;
+        if (done == n_items) {
           __threadfence();
-          const uint32_t done = atomicAdd(ring + kRingDone + q4, 1u) + 1u;
-          if (done == n_items) {
-            __threadfence();
-            const int q4nn = int((R + 2u) & 3u);
-            ring[kRingCnt + q4nn] = 0u;
-            ring[kRingSwc + q4nn] = ring[kRingPc + q4nn] = ring[kRingDone + q4nn] = 0u;
-            if (R > 1) a.status->sum_dirty += n_dirty;
-            __threadfence();
-            st_release(ring + kRingLast, R);
+          const int q4nn = int((R + 2u) & 3u);
+          ring[kRingCnt + q4nn] = 0u;
+          ring[kRingSwc + q4nn] = ring[kRingPc + q4nn] = ring[kRingDone + q4nn] = 0u;
+          if (R > 1) a.status->sum_dirty += n_dirty;
+          if (a.trace && R < 64) {  // VXM_TRACE_XR: round completion times
+            unsigned long long tm;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+            a.trace[R] = tm;
           }
+          __threadfence();
+          st_release(ring + kRingLast, R);
         }
       }
       // the next round's sweeps re-form the groups (both warps)
@@ -400,6 +427,13 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
 }
 
 void launch_lower_xr(Context* ctx, LowerArgs& la) {
+  static const bool trace = std::getenv("VXM_TRACE_XR") != nullptr;
+  static DevBuf trace_buf;
+  if (trace) {
+    trace_buf.ensure(64 * sizeof(unsigned long long));
+    VXM_CUDA(cudaMemsetAsync(trace_buf.p, 0, 64 * sizeof(unsigned long long), ctx->stream));
+    la.trace = trace_buf.as<unsigned long long>();
+  }
   static int grid = 0;
   if (!grid) {
     int bps = 0;
@@ -412,6 +446,15 @@ void launch_lower_xr(Context* ctx, LowerArgs& la) {
                                        ctx->stream));
   ctx->prof_end();
   ctx->count_launch();
+  if (trace) {
+    unsigned long long h[64];
+    VXM_CUDA(cudaMemcpyAsync(h, trace_buf.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::fprintf(stderr, "[k_lower_xr] round ends (us):");
+    for (int r = 1; r < 64 && h[r]; ++r) std::fprintf(stderr, " %.1f", (h[r] - h[0]) * 1e-3);
+    std::fprintf(stderr, "\n");
+    la.trace = nullptr;
+  }
 }
 
 }  // namespace vxm
