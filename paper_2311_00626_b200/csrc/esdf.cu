@@ -1170,10 +1170,8 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
                       "k_compact_esdf");
   changed_out->host_valid = false;
   changed_out->count_hint = n_all_cap;
-  VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_effective, s.counts + 0, sizeof(uint32_t) * 2,
-                           cudaMemcpyDeviceToDevice, ctx->stream));  // n_effective, n_esdf_new
-  VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_out, changed_out->d_count, sizeof(uint32_t),
-                           cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->queue_copy(s.counts + 0, &ctx->d_status->n_effective, 2);  // n_effective, n_esdf_new
+  ctx->queue_copy(changed_out->d_count, &ctx->d_status->n_out);
 }
 
 void esdf_finish(Layer* E, BlockList* changed_out) {

@@ -407,8 +407,7 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   changed_out->host_valid = false;
   // changed blocks are distinct allocated blocks: bounded by the pool too
   changed_out->count_hint = std::min<uint32_t>(cand_cap, L->capacity);
-  VXM_CUDA(cudaMemcpyAsync(&ctx->d_status->n_changed, changed_out->d_count, sizeof(uint32_t),
-                           cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->queue_copy(changed_out->d_count, &ctx->d_status->n_changed);
   return cand_cap;
 }
 

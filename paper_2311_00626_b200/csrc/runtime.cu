@@ -63,9 +63,32 @@ ScanTiles Context::next_scan(uint32_t tiles) {
 }
 
 void Context::reset_status() {
+  status_copies.clear();  // (copies queued by an operation that threw are dropped)
   VXM_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), stream));
 }
+struct WordCopies {
+  const uint32_t* src[16];
+  uint32_t* dst[16];
+  int n;
+};
+__global__ void k_copy_words(WordCopies c) {
+  if (threadIdx.x < c.n) *c.dst[threadIdx.x] = *c.src[threadIdx.x];
+}
+void Context::flush_copies() {
+  size_t i = 0;
+  while (i < status_copies.size()) {
+    WordCopies c{};
+    for (; i < status_copies.size() && c.n < 16; ++i, ++c.n) {
+      c.src[c.n] = status_copies[i].src;
+      c.dst[c.n] = status_copies[i].dst;
+    }
+    k_copy_words<<<1, 32, 0, stream>>>(c);
+    count_launch();
+  }
+  status_copies.clear();
+}
 void Context::sync_status() {
+  flush_copies();
   VXM_CUDA(cudaMemcpyAsync(h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
   VXM_CUDA(cudaStreamSynchronize(stream));
   prof_resolve();
@@ -139,9 +162,7 @@ void Layer::refresh() {
 }
 
 void Layer::stage_meta(int slot) {
-  VXM_CUDA(cudaMemcpyAsync(slot ? &ctx->d_status->meta2_blocks : &ctx->d_status->meta_blocks, meta,
-                           2 * sizeof(uint32_t),
-                           cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->queue_copy(&meta->num_blocks, slot ? &ctx->d_status->meta2_blocks : &ctx->d_status->meta_blocks, 2);
 }
 void Layer::adopt_meta(int slot) {
   num_blocks = slot ? ctx->h_status->meta2_blocks : ctx->h_status->meta_blocks;

@@ -49,7 +49,9 @@ struct Context {
   int rank = 0, world = 1, slab = 16;
   // scratch
   DevBuf depth;           // staged depth image
-  DevBuf bitmap;          // touched-cell bitmap (candidate cube)
+  DevBuf bitmap[2];       // touched-cell bitmaps (candidate cube), alternating by call:
+  int bitmap_parity = 0;  //   the call on one clears the other for the next call
+  uint64_t bitmap_clean[2] = {0, 0};  // words known zero in each
   DevBuf cand_keys;       // uint64 candidate keys (sorted)
   DevBuf cand_slots;      // int32 slot | new flag
   DevBuf cand_flags;      // uint8 per candidate (changed)
@@ -80,7 +82,19 @@ struct Context {
   // most `tiles` tiles, clearing the other buffer for the pass after.
   ScanTiles next_scan(uint32_t tiles);
   void count_launch(int n = 1) { launches += uint64_t(n); }
-  void sync_status();  // cudaStreamSynchronize + copy status (already async-copied)
+  void sync_status();  // flush the queued status copies, copy status to the host, sync
+  // Small device-to-device word copies into the status (counts, metas) are
+  // queued and done by ONE kernel before the status read, instead of one
+  // cudaMemcpyAsync each (each is a separate stream operation).
+  struct WordCopy {
+    const uint32_t* src;
+    uint32_t* dst;
+  };
+  std::vector<WordCopy> status_copies;
+  void queue_copy(const uint32_t* src, uint32_t* dst, int n_words = 1) {
+    for (int i = 0; i < n_words; ++i) status_copies.push_back({src + i, dst + i});
+  }
+  void flush_copies();
   void reset_status();
   void prof_begin(const char* name);
   void prof_end();

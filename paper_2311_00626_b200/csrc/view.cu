@@ -222,7 +222,9 @@ __global__ void __launch_bounds__(kDilThreads) k_dilate_alloc(Cube cube, uint32_
                                                               int rank, int world, int slab,
                                                               uint64_t* __restrict__ cand_keys,
                                                               int32_t* __restrict__ cand_slots,
-                                                              DevStatus* status, ScanTiles st) {
+                                                              DevStatus* status, ScanTiles st,
+                                                              uint32_t* __restrict__ clear_bits,
+                                                              uint32_t clear_words) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_scan[64];
   __shared__ uint32_t s_pre[2];
@@ -230,6 +232,8 @@ __global__ void __launch_bounds__(kDilThreads) k_dilate_alloc(Cube cube, uint32_
   __shared__ DilTile s_d;
   __shared__ int32_t s_slot[kDilMaxCand];  // found slot, or -2 - (tile-local new rank)
   scan_prepare_next(st);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < clear_words; i += gridDim.x * blockDim.x)
+    clear_bits[i] = 0u;  // the next call's bitmap
   const uint32_t tile = scan_take_tile(st, &s_tile);
   const uint32_t wi = tile * blockDim.x + threadIdx.x;
   const bool do_alloc = al.hash.keys != nullptr;
@@ -390,10 +394,21 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
   cube.oz = int32_t(ocz - r);
   cube.S = S;
   cube.SZw = SZw;
-  ctx->bitmap.ensure(n_words * 4);
-  cube.bits = ctx->bitmap.as<uint32_t>();
-  VXM_CUDA(cudaMemsetAsync(cube.bits, 0, n_words * 4, ctx->stream));
-  ctx->count_launch();
+  // This call's bitmap was zeroed by the previous call's k_dilate_alloc (or is
+  // zeroed here); k_dilate_alloc zeroes the other one for the next call.
+  const int bp = ctx->bitmap_parity;
+  ctx->bitmap_parity ^= 1;
+  DevBuf& bm = ctx->bitmap[bp];
+  if (bm.bytes < n_words * 4) ctx->bitmap_clean[bp] = 0;
+  bm.ensure(n_words * 4);
+  cube.bits = bm.as<uint32_t>();
+  if (ctx->bitmap_clean[bp] < n_words) {
+    VXM_CUDA(cudaMemsetAsync(cube.bits, 0, n_words * 4, ctx->stream));
+    ctx->count_launch();
+  }
+  ctx->bitmap_clean[bp] = 0;
+  DevBuf& other = ctx->bitmap[bp ^ 1];
+  const uint64_t other_words = other.bytes / 4;
 
   if (!a.lidar) {
     const int tile = std::max(1, a.cfg.pixel_subsample);
@@ -439,7 +454,9 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
   ctx->prof_begin("k_dilate_alloc");
   k_dilate_alloc<<<tiles, 256, 0, ctx->stream>>>(cube, uint32_t(n_words), al, ctx->rank, ctx->world,
                                                  ctx->slab, ctx->cand_keys.as<uint64_t>(),
-                                                 ctx->cand_slots.as<int32_t>(), ctx->d_status, st);
+                                                 ctx->cand_slots.as<int32_t>(), ctx->d_status, st,
+                                                 other.as<uint32_t>(), uint32_t(other_words));
+  ctx->bitmap_clean[bp ^ 1] = other_words;
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "k_dilate_alloc");
