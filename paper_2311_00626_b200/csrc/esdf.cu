@@ -971,7 +971,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   const uint32_t n7 = 7u * nu_cap;
   const uint64_t* upd = updated->keys.as<uint64_t>();
   ctx->prof_begin("k_merge7");
-  k_merge7<<<grid_for(ctx, n7), 256, 0, ctx->stream>>>(upd, updated->d_count, s.merged);
+  k_merge7<<<grid_for(ctx, n7, 2), 256, 0, ctx->stream>>>(upd, updated->d_count, s.merged);
   ctx->prof_end();
   ctx->count_launch();
   {
@@ -991,7 +991,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
     al.status = ctx->d_status;
     const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
     ctx->prof_begin("k_effective_alloc");
-    k_effective_alloc<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(
+    k_effective_alloc<<<grid_for(ctx, n7, 1), 256, 0, ctx->stream>>>(
         s.merged, updated->d_count, T->hash, s.eff_keys, s.eff_tslot, s.counts + 0, al, st);
     ctx->prof_end();
     ctx->count_launch();

@@ -345,7 +345,7 @@ void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
                          const DevStatus* guard, const char* prof_name) {
   const uint32_t tiles_cap = ceil_div(std::max<uint32_t>(n_cap, 1), 256 * kCompactItems);
   const ScanTiles st = ctx->next_scan(tiles_cap);
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_cap, ctx->sm_count * 4));
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_cap, ctx->sm_count));
   ctx->prof_begin(prof_name);
   k_compact_keys<<<grid, 256, 0, ctx->stream>>>(in, flags, n_ptr, out, n_out, st, guard);
   ctx->prof_end();

@@ -55,17 +55,32 @@ __device__ inline void pose_apply(const vxm_pose& T, double x, double y, double 
                        T.t[i]);
 }
 
+// Sets the cell's bit with a fire-and-forget RED (no load on the DDA's critical
+// path).  With DEDUP (LiDAR: 131k rays, thousands per warp-step near the
+// sensor) lanes at the same step that hit the same word combine their bits and
+// one of them issues the RED, so the hot words near the sensor do not
+// serialise in L2; the camera's 4800 rays gain nothing from it.
+template <bool DEDUP>
 __device__ inline void mark_cell(const Cube& c, int32_t x, int32_t y, int32_t z,
                                  DevStatus* status) {
-  uint32_t w, m;
-  if (!c.locate(x, y, z, w, m)) {
+  uint32_t w = 0xffffffffu, m = 0u;
+  const bool ok = c.locate(x, y, z, w, m);
+  uint32_t mm = m;
+  if (DEDUP) {
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, w);
+    mm = __reduce_or_sync(peers, m);
+    if ((threadIdx.x & 31) != __ffs(peers) - 1) return;
+  }
+  if (!ok) {
     atomicOr(&status->bitmap_overflow, 1u);
     return;
   }
-  atomicOr(c.bits + w, m);  // fire-and-forget (RED): no load on the DDA's critical path
+  atomicOr(c.bits + w, mm);
 }
 
 // traverse_grid — traversal.hpp:29-73, visiting into the bitmap.
+template <bool DEDUP>
 __device__ void traverse(const double s[3], const double e[3], double cs, const Cube& cube,
                          DevStatus* status) {
   double d[3], t_max[3], t_delta[3];
@@ -91,17 +106,31 @@ __device__ void traverse(const double s[3], const double e[3], double cs, const 
       t_max[i] = __ddiv_rn(__dsub_rn(__dmul_rn(double(cell[i]), cs), s[i]), d[i]);
     }
   }
-  mark_cell(cube, cell[0], cell[1], cell[2], status);
+  mark_cell<DEDUP>(cube, cell[0], cell[1], cell[2], status);
   int guard = abs(end_cell[0] - cell[0]) + abs(end_cell[1] - cell[1]) +
               abs(end_cell[2] - cell[2]) + 3;
+  // the stepping state in named registers (dynamic indexing of the arrays
+  // would put them in local memory, one load per step on the critical path)
+  int cx = cell[0], cy = cell[1], cz = cell[2];
+  double tx = t_max[0], ty = t_max[1], tz = t_max[2];
   while (guard-- > 0) {
-    int axis = 0;
-    if (t_max[1] < t_max[0]) axis = 1;
-    if (t_max[2] < t_max[axis]) axis = 2;
-    if (t_max[axis] > 1.0) break;
-    cell[axis] += step[axis];
-    t_max[axis] = __dadd_rn(t_max[axis], t_delta[axis]);
-    mark_cell(cube, cell[0], cell[1], cell[2], status);
+    // axis = 0; if (t_max[1] < t_max[0]) axis = 1; if (t_max[2] < t_max[axis]) axis = 2;
+    const bool y_first = ty < tx;
+    const double t_xy = y_first ? ty : tx;
+    const bool z_first = tz < t_xy;
+    const double t_min = z_first ? tz : t_xy;
+    if (t_min > 1.0) break;
+    if (z_first) {
+      cz += step[2];
+      tz = __dadd_rn(tz, t_delta[2]);
+    } else if (y_first) {
+      cy += step[1];
+      ty = __dadd_rn(ty, t_delta[1]);
+    } else {
+      cx += step[0];
+      tx = __dadd_rn(tx, t_delta[0]);
+    }
+    mark_cell<DEDUP>(cube, cx, cy, cz, status);
   }
 }
 
@@ -149,7 +178,7 @@ __global__ void k_rays_camera(const float* __restrict__ depth, int W, int H, int
                            __dmul_rn(__ddiv_rn(__dsub_rn(v, cam.cv), cam.fv), reach), reach};
   double end_L[3];
   pose_apply(T, end_S[0], end_S[1], end_S[2], end_L);
-  traverse(T.t, end_L, cs, cube, status);
+  traverse<false>(T.t, end_L, cs, cube, status);
 }
 
 // LiDAR: one thread per valid pixel — view.cpp:94-111.  The per-pixel unit
@@ -167,7 +196,7 @@ __global__ void k_rays_lidar(const float* __restrict__ depth, int W, int H,
                            __dmul_rn(__ldg(dirs + 3 * p + 2), reach)};
   double end_L[3];
   pose_apply(T, end_S[0], end_S[1], end_S[2], end_L);
-  traverse(T.t, end_L, cs, cube, status);
+  traverse<true>(T.t, end_L, cs, cube, status);
 }
 
 __device__ inline uint32_t zdilate(uint32_t prev, uint32_t w, uint32_t next) {
