@@ -50,6 +50,9 @@ typedef struct { int32_t x, y, z; } vxm_grid_index;
 /* TsdfVoxel (core/voxels.hpp:22-26), 8 bytes. */
 typedef struct { float distance, weight; } vxm_tsdf_voxel;
 
+/* OccupancyVoxel (core/voxels.hpp:28-32), 4 bytes: log-odds, 0 = unobserved prior. */
+typedef struct { float log_odds; } vxm_occupancy_voxel;
+
 /* EsdfVoxel (core/voxels.hpp:48-68), 12 bytes, same byte layout. */
 typedef struct {
   int32_t squared_distance;
@@ -61,8 +64,8 @@ typedef struct {
 enum { VXM_ESDF_OBSERVED = 1, VXM_ESDF_SITE = 2, VXM_ESDF_INSIDE = 4 };
 enum { VXM_VOXELS_PER_SIDE = 8, VXM_VOXELS_PER_BLOCK = 512 };
 
-/* Layer voxel type. */
-typedef enum { VXM_LAYER_TSDF = 0, VXM_LAYER_ESDF = 1 } vxm_layer_type;
+/* Layer voxel type: Layer<TsdfVoxel>, Layer<EsdfVoxel>, Layer<OccupancyVoxel>. */
+typedef enum { VXM_LAYER_TSDF = 0, VXM_LAYER_ESDF = 1, VXM_LAYER_OCCUPANCY = 2 } vxm_layer_type;
 
 /* CameraIntrinsics (sensor/camera.hpp:24-31). */
 typedef struct {
@@ -212,10 +215,13 @@ vxm_status vxm_blocks_in_view_lidar(vxm_context* ctx, const vxm_pose* T_LS, cons
                                     const float* depth, int width, int height, double block_size,
                                     const vxm_view_config* cfg, vxm_blocklist* out);
 
-/* ---- TSDF integration (integrate/integrator.hpp:36-45) ------------------ */
+/* ---- depth integration (integrate/integrator.hpp:36-55) ----------------- */
 /* integrate_depth(Layer<TsdfVoxel>&, DepthImage, Pose T_LS, CameraIntrinsics,
- * IntegratorConfig) — integrator.cpp:162-168.  changed_out receives the
- * sorted changed-block list.  Validates before mutating (integrator.cpp:26-34). */
+ * IntegratorConfig) — integrator.cpp:162-168; with an occupancy layer, the
+ * Layer<OccupancyVoxel>& overload (integrator.cpp:176-189: occupancy_update,
+ * updates.hpp:59-72).  The layer's type selects the overload.  changed_out
+ * receives the sorted changed-block list.  Validates before mutating
+ * (integrator.cpp:26-34). */
 vxm_status vxm_integrate_depth_camera(vxm_layer* layer, const float* depth, int width, int height,
                                       const vxm_pose* T_LS, const vxm_camera* cam,
                                       const vxm_integrator_config* cfg, vxm_blocklist* changed_out);
@@ -238,12 +244,13 @@ vxm_status vxm_integrate_depth_lidar_device(vxm_layer* layer, const float* depth
                                             vxm_blocklist* changed_out);
 
 /* ---- replay (io/pipeline.hpp:27-72, pipeline.cpp:54-148) ------------------- */
-/* ReplayConfig (TSDF source; occupancy / color / mesh are out of scope). */
+/* ReplayConfig (pipeline.hpp:27-36; color / mesh are out of scope). */
 typedef struct {
   double voxel_size;
   int32_t update_every;  /* derive the ESDF every this many frames (+ after the last) */
   vxm_integrator_config integrator;
   vxm_esdf_config esdf;
+  int32_t use_occupancy; /* fuse occupancy instead of the TSDF (pipeline.cpp:73-77, 95-101) */
 } vxm_replay_config;
 /* FrameTiming: wall-clock ms per stage of one frame (0 when skipped). */
 typedef struct {
@@ -255,8 +262,8 @@ void vxm_replay_config_make(double voxel_size, vxm_replay_config* out);
 /* replay (pipeline.cpp:54-148) over in-memory frames: n_frames depth images
  * (host, n_frames x height x width, row-major) with their poses; integrates every
  * frame and, every update_every frames and after the last one, folds the blocks
- * changed since the previous update into the ESDF.  Creates *tsdf_out and
- * *esdf_out on ctx; timings has n_frames entries.  Errors as the reference: no
+ * changed since the previous update into the ESDF.  Creates *tsdf_out (the
+ * source layer: an occupancy layer when cfg->use_occupancy) and *esdf_out on ctx; timings has n_frames entries.  Errors as the reference: no
  * frames or update_every < 1 -> VXM_ERR_INVALID_ARGUMENT. */
 vxm_status vxm_replay_camera(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_camera* cam,
                              int n_frames, int width, int height, const float* depth,
@@ -280,6 +287,14 @@ vxm_status vxm_snapshot_save(const char* path, double voxel_size, vxm_layer* tsd
  * implement (out of scope). */
 vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* voxel_size_out,
                              vxm_layer** tsdf_out, vxm_layer** esdf_out);
+/* The same over the LayerCake's tsdf / occupancy / esdf layers (layer_cake.hpp:
+ * 29-33; written in the reference's order tsdf, occupancy, esdf).  The color
+ * layer is not implemented (load fails with VXM_ERR_IO when a file holds one). */
+vxm_status vxm_snapshot_save_layers(const char* path, double voxel_size, vxm_layer* tsdf,
+                                    vxm_layer* occupancy, vxm_layer* esdf);
+vxm_status vxm_snapshot_load_layers(vxm_context* ctx, const char* path, double* voxel_size_out,
+                                    vxm_layer** tsdf_out, vxm_layer** occupancy_out,
+                                    vxm_layer** esdf_out);
 
 /* ---- block-sharded ESDF ------------------------------------ */
 /* One update_esdf (esdf/integrator.cpp:365-413) over a map sharded by block x:
@@ -339,7 +354,10 @@ vxm_status vxm_update_frame_lidar_device(vxm_layer* tsdf, vxm_layer* esdf, const
 
 /* ---- ESDF (esdf/integrator.hpp:81-120) ---------------------------------- */
 /* update_esdf(Layer<EsdfVoxel>&, const Layer<TsdfVoxel>&, updated, EsdfConfig)
- * — esdf/integrator.cpp:365-413, 567-572. */
+ * — esdf/integrator.cpp:365-413, 567-572.  `tsdf` may be an occupancy layer:
+ * the Layer<OccupancyVoxel> overload (:574-579, OccupancyClassifier :200-266).
+ * The same holds for vxm_update_esdf_list, vxm_esdf_mark_sites and the
+ * frame step (vxm_update_frame_*); the sharded update takes TSDF sources. */
 vxm_status vxm_update_esdf(vxm_layer* esdf, vxm_layer* tsdf, const vxm_grid_index* updated,
                            uint64_t n, const vxm_esdf_config* cfg, vxm_blocklist* changed_out);
 /* Same, with the updated list taken from a (device-resident) block list,
@@ -355,7 +373,7 @@ vxm_status vxm_esdf_state_get(vxm_esdf_state* st, int which, const vxm_grid_inde
                               uint64_t* n);
 vxm_status vxm_esdf_state_set(vxm_esdf_state* st, int which, const vxm_grid_index* data,
                               uint64_t n);
-/* mark_sites — esdf/integrator.cpp:417-423 (TSDF source). changed is appended. */
+/* mark_sites — esdf/integrator.cpp:417-431 (TSDF or occupancy source). changed is appended. */
 vxm_status vxm_esdf_mark_sites(vxm_layer* esdf, vxm_layer* tsdf, const vxm_grid_index* updated,
                                uint64_t n, const vxm_esdf_config* cfg, vxm_esdf_state* st,
                                vxm_blocklist* changed);

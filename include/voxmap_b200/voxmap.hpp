@@ -26,6 +26,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
@@ -81,6 +82,9 @@ struct TsdfVoxel {
   float distance = 0.0f;
   float weight = 0.0f;
 };
+struct OccupancyVoxel {  // core/voxels.hpp:28-32
+  float log_odds = 0.0f;
+};
 struct EsdfVoxel {
   static constexpr uint8_t kObserved = 1, kSite = 2, kInside = 4;
   int32_t squared_distance = 0;
@@ -92,7 +96,8 @@ struct EsdfVoxel {
   bool has_parent() const { return parent_x || parent_y || parent_z; }
   friend bool operator==(const EsdfVoxel&, const EsdfVoxel&) = default;
 };
-static_assert(sizeof(TsdfVoxel) == sizeof(vxm_tsdf_voxel) && sizeof(EsdfVoxel) == sizeof(vxm_esdf_voxel));
+static_assert(sizeof(TsdfVoxel) == sizeof(vxm_tsdf_voxel) && sizeof(EsdfVoxel) == sizeof(vxm_esdf_voxel) &&
+              sizeof(OccupancyVoxel) == sizeof(vxm_occupancy_voxel));
 
 template <typename V>
 struct VoxelBlock {
@@ -108,6 +113,10 @@ struct LayerTraits<TsdfVoxel> {
 template <>
 struct LayerTraits<EsdfVoxel> {
   static constexpr vxm_layer_type type = VXM_LAYER_ESDF;
+};
+template <>
+struct LayerTraits<OccupancyVoxel> {
+  static constexpr vxm_layer_type type = VXM_LAYER_OCCUPANCY;
 };
 
 struct GridHash {
@@ -426,8 +435,12 @@ inline std::vector<GridIndex> from_c(const vxm_grid_index* p, uint64_t n) {
   return out;
 }
 
-// ---- integrate/integrator.hpp:36-45 -----------------------------------------------
-inline std::vector<GridIndex> integrate_depth(Layer<TsdfVoxel>& layer, const DepthImage& depth,
+// ---- integrate/integrator.hpp:36-55 (TSDF and occupancy overloads) ---------------
+template <typename V>
+concept SourceVoxel = std::is_same_v<V, TsdfVoxel> || std::is_same_v<V, OccupancyVoxel>;
+
+template <SourceVoxel V>
+inline std::vector<GridIndex> integrate_depth(Layer<V>& layer, const DepthImage& depth,
                                               const Pose& T_LS, const CameraIntrinsics& camera,
                                               const IntegratorConfig& cfg) {
   const vxm_pose p = T_LS.c();
@@ -438,7 +451,8 @@ inline std::vector<GridIndex> integrate_depth(Layer<TsdfVoxel>& layer, const Dep
                                    &cam, &k, out.handle()));
   return out.to_vector();
 }
-inline std::vector<GridIndex> integrate_depth(Layer<TsdfVoxel>& layer, const DepthImage& depth,
+template <SourceVoxel V>
+inline std::vector<GridIndex> integrate_depth(Layer<V>& layer, const DepthImage& depth,
                                               const Pose& T_LS, const LidarIntrinsics& lidar,
                                               const IntegratorConfig& cfg) {
   const vxm_pose p = T_LS.c();
@@ -503,7 +517,8 @@ struct StateHandle {
 };
 }  // namespace detail
 
-inline void mark_sites(Layer<EsdfVoxel>& esdf, const Layer<TsdfVoxel>& source,
+template <SourceVoxel V>
+inline void mark_sites(Layer<EsdfVoxel>& esdf, const Layer<V>& source,
                        const std::vector<GridIndex>& updated_blocks, const EsdfConfig& cfg,
                        EsdfUpdateState* state, std::vector<GridIndex>* changed) {
   detail::StateHandle st(*state);
@@ -537,7 +552,8 @@ inline int lower_esdf(Layer<EsdfVoxel>& esdf, const EsdfUpdateState& state, cons
   changed->insert(changed->end(), c.begin(), c.end());
   return rounds;
 }
-inline std::vector<GridIndex> update_esdf(Layer<EsdfVoxel>& esdf, const Layer<TsdfVoxel>& source,
+template <SourceVoxel V>
+inline std::vector<GridIndex> update_esdf(Layer<EsdfVoxel>& esdf, const Layer<V>& source,
                                           const std::vector<GridIndex>& updated_blocks,
                                           const EsdfConfig& cfg) {
   const auto u = to_c(updated_blocks);
@@ -574,15 +590,20 @@ inline std::vector<QueryResult> query_batch(const Layer<EsdfVoxel>& esdf,
 }
 
 // ---- snapshots (core/layer_cake.hpp:27-57, core/serialization.hpp:29-35) --------
-// The layers of a LayerCake this library implements (TSDF, ESDF).
+// The layers of a LayerCake this library implements (TSDF, occupancy, ESDF).
 struct LayerCake {
   explicit LayerCake(double vs) : voxel_size(vs) {}
   double voxel_size;
   std::unique_ptr<Layer<TsdfVoxel>> tsdf;
+  std::unique_ptr<Layer<OccupancyVoxel>> occupancy;
   std::unique_ptr<Layer<EsdfVoxel>> esdf;
   Layer<TsdfVoxel>& require_tsdf() {
     if (!tsdf) tsdf = std::make_unique<Layer<TsdfVoxel>>(voxel_size);
     return *tsdf;
+  }
+  Layer<OccupancyVoxel>& require_occupancy() {
+    if (!occupancy) occupancy = std::make_unique<Layer<OccupancyVoxel>>(voxel_size);
+    return *occupancy;
   }
   Layer<EsdfVoxel>& require_esdf() {
     if (!esdf) esdf = std::make_unique<Layer<EsdfVoxel>>(voxel_size);
@@ -591,16 +612,19 @@ struct LayerCake {
 };
 
 inline void save_snapshot(const LayerCake& cake, const std::string& path) {
-  check(vxm_snapshot_save(path.c_str(), cake.voxel_size, cake.tsdf ? cake.tsdf->c_handle() : nullptr,
-                          cake.esdf ? cake.esdf->c_handle() : nullptr));
+  check(vxm_snapshot_save_layers(path.c_str(), cake.voxel_size,
+                                 cake.tsdf ? cake.tsdf->c_handle() : nullptr,
+                                 cake.occupancy ? cake.occupancy->c_handle() : nullptr,
+                                 cake.esdf ? cake.esdf->c_handle() : nullptr));
 }
 
 inline LayerCake load_snapshot(const std::string& path, Context& ctx = default_context()) {
   double vs = 0.0;
-  vxm_layer *t = nullptr, *e = nullptr;
-  check(vxm_snapshot_load(ctx.handle(), path.c_str(), &vs, &t, &e));
+  vxm_layer *t = nullptr, *o = nullptr, *e = nullptr;
+  check(vxm_snapshot_load_layers(ctx.handle(), path.c_str(), &vs, &t, &o, &e));
   LayerCake cake(vs);
   if (t) cake.tsdf = std::make_unique<Layer<TsdfVoxel>>(t, vs, ctx);
+  if (o) cake.occupancy = std::make_unique<Layer<OccupancyVoxel>>(o, vs, ctx);
   if (e) cake.esdf = std::make_unique<Layer<EsdfVoxel>>(e, vs, ctx);
   return cake;
 }

@@ -63,7 +63,7 @@ class _Base:
     def export(self, layer):
         n = int(self._f("layer_num_blocks")(layer.h))
         keys = np.zeros((n, 3), np.int32)
-        dt = A.TSDF_DTYPE if layer.kind == A.LAYER_TSDF else A.ESDF_DTYPE
+        dt = A.layer_dtype(layer.kind)
         vox = np.zeros((n, 512), dt)
         self._check(self._f("layer_export")(layer.h, A.ptr(keys), A.ptr(vox)))
         return keys, vox
@@ -213,19 +213,20 @@ class RefOracle(_Base):
                                              C.c_int(int(serial)), A.ptr(out)))
         return out
 
-    def save_snapshot(self, path, voxel_size, tsdf=None, esdf=None):
+    def save_snapshot(self, path, voxel_size, tsdf=None, esdf=None, occupancy=None):
+        h = lambda L: L.h if L is not None else None  # noqa: E731
         self._check(self.lib.vxr_snapshot_save(os.fsencode(path), C.c_double(voxel_size),
-                                               tsdf.h if tsdf is not None else None,
-                                               esdf.h if esdf is not None else None))
+                                               h(tsdf), h(occupancy), h(esdf)))
 
-    def load_snapshot(self, path):
+    def load_snapshot(self, path, with_occupancy=False):
+        """(vs, tsdf, esdf) or, with_occupancy, (vs, tsdf, occupancy, esdf)."""
         vs = C.c_double()
-        th, eh = C.c_void_p(), C.c_void_p()
+        th, oh, eh = C.c_void_p(), C.c_void_p(), C.c_void_p()
         self._check(self.lib.vxr_snapshot_load(os.fsencode(path), C.byref(vs), C.byref(th),
-                                               C.byref(eh)))
-        return (vs.value,
-                OracleLayer(self, th, A.LAYER_TSDF, vs.value) if th.value else None,
-                OracleLayer(self, eh, A.LAYER_ESDF, vs.value) if eh.value else None)
+                                               C.byref(oh), C.byref(eh)))
+        mk = lambda h, kind: OracleLayer(self, h, kind, vs.value) if h.value else None  # noqa: E731
+        t, o, e = mk(th, A.LAYER_TSDF), mk(oh, A.LAYER_OCCUPANCY), mk(eh, A.LAYER_ESDF)
+        return (vs.value, t, o, e) if with_occupancy else (vs.value, t, e)
 
     def orbit_pose(self, scene, k, total, lidar=False):
         p = A.PoseC()

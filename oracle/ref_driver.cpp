@@ -48,9 +48,11 @@ struct RefLayer {
   int type;
   vr::Layer<vr::TsdfVoxel>* tsdf = nullptr;
   vr::Layer<vr::EsdfVoxel>* esdf = nullptr;
+  vr::Layer<vr::OccupancyVoxel>* occ = nullptr;
   ~RefLayer() {
     delete tsdf;
     delete esdf;
+    delete occ;
   }
 };
 
@@ -174,6 +176,7 @@ int vxr_layer_create(int type, double vs, uint64_t max_blocks, void** out) {
     const size_t mb = max_blocks ? size_t(max_blocks) : size_t{1} << 30;
     try {
       if (type == VXM_LAYER_TSDF) L->tsdf = new vr::Layer<vr::TsdfVoxel>(vs, mb);
+      else if (type == VXM_LAYER_OCCUPANCY) L->occ = new vr::Layer<vr::OccupancyVoxel>(vs, mb);
       else L->esdf = new vr::Layer<vr::EsdfVoxel>(vs, mb);
     } catch (...) {
       delete L;
@@ -185,12 +188,13 @@ int vxr_layer_create(int type, double vs, uint64_t max_blocks, void** out) {
 void vxr_layer_destroy(void* h) { delete static_cast<RefLayer*>(h); }
 uint64_t vxr_layer_num_blocks(void* h) {
   auto* L = static_cast<RefLayer*>(h);
-  return L->tsdf ? L->tsdf->num_blocks() : L->esdf->num_blocks();
+  return L->tsdf ? L->tsdf->num_blocks() : L->occ ? L->occ->num_blocks() : L->esdf->num_blocks();
 }
 int vxr_layer_export(void* h, vxm_grid_index* keys, void* voxels) {
   return guard([&] {
     auto* L = static_cast<RefLayer*>(h);
     if (L->tsdf) export_layer(*L->tsdf, keys, voxels);
+    else if (L->occ) export_layer(*L->occ, keys, voxels);
     else export_layer(*L->esdf, keys, voxels);
   });
 }
@@ -202,6 +206,9 @@ int vxr_layer_write_blocks(void* h, const vxm_grid_index* keys, uint64_t n, cons
       if (L->tsdf)
         std::memcpy(L->tsdf->get_or_allocate(g).voxels.data(),
                     static_cast<const char*>(voxels) + i * 4096, 4096);
+      else if (L->occ)
+        std::memcpy(L->occ->get_or_allocate(g).voxels.data(),
+                    static_cast<const char*>(voxels) + i * 2048, 2048);
       else
         std::memcpy(L->esdf->get_or_allocate(g).voxels.data(),
                     static_cast<const char*>(voxels) + i * 6144, 6144);
@@ -235,9 +242,14 @@ int vxr_integrate_camera(void* h, const float* depth, int w, int hh, const vxm_p
   return guard([&] {
     auto* L = static_cast<RefLayer*>(h);
     const auto img = to_depth(depth, w, hh);
-    emit(serial ? vr::reference_integrate_depth(*L->tsdf, img, to_pose(T), to_cam(cam), to_icfg(c))
-                : vr::integrate_depth(*L->tsdf, img, to_pose(T), to_cam(cam), to_icfg(c)),
-         out, n);
+    if (L->occ)  // Layer<OccupancyVoxel> overload (integrator.cpp:176-182)
+      emit(serial ? vr::reference_integrate_depth(*L->occ, img, to_pose(T), to_cam(cam), to_icfg(c))
+                  : vr::integrate_depth(*L->occ, img, to_pose(T), to_cam(cam), to_icfg(c)),
+           out, n);
+    else
+      emit(serial ? vr::reference_integrate_depth(*L->tsdf, img, to_pose(T), to_cam(cam), to_icfg(c))
+                  : vr::integrate_depth(*L->tsdf, img, to_pose(T), to_cam(cam), to_icfg(c)),
+           out, n);
   });
 }
 int vxr_integrate_lidar(void* h, const float* depth, int w, int hh, const vxm_pose* T,
@@ -246,10 +258,16 @@ int vxr_integrate_lidar(void* h, const float* depth, int w, int hh, const vxm_po
   return guard([&] {
     auto* L = static_cast<RefLayer*>(h);
     const auto img = to_depth(depth, w, hh);
-    emit(serial
-             ? vr::reference_integrate_depth(*L->tsdf, img, to_pose(T), to_lidar(li), to_icfg(c))
-             : vr::integrate_depth(*L->tsdf, img, to_pose(T), to_lidar(li), to_icfg(c)),
-         out, n);
+    if (L->occ)  // integrator.cpp:183-189
+      emit(serial
+               ? vr::reference_integrate_depth(*L->occ, img, to_pose(T), to_lidar(li), to_icfg(c))
+               : vr::integrate_depth(*L->occ, img, to_pose(T), to_lidar(li), to_icfg(c)),
+           out, n);
+    else
+      emit(serial
+               ? vr::reference_integrate_depth(*L->tsdf, img, to_pose(T), to_lidar(li), to_icfg(c))
+               : vr::integrate_depth(*L->tsdf, img, to_pose(T), to_lidar(li), to_icfg(c)),
+           out, n);
   });
 }
 
@@ -258,7 +276,10 @@ int vxr_update_esdf(void* esdf, void* tsdf, const vxm_grid_index* upd, uint64_t 
   return guard([&] {
     auto* E = static_cast<RefLayer*>(esdf);
     auto* T = static_cast<RefLayer*>(tsdf);
-    emit(vr::update_esdf(*E->esdf, *T->tsdf, to_list(upd, nu), to_ecfg(c)), out, n);
+    if (T->occ)  // Layer<OccupancyVoxel> overload (esdf/integrator.cpp:574-579)
+      emit(vr::update_esdf(*E->esdf, *T->occ, to_list(upd, nu), to_ecfg(c)), out, n);
+    else
+      emit(vr::update_esdf(*E->esdf, *T->tsdf, to_list(upd, nu), to_ecfg(c)), out, n);
   });
 }
 
@@ -283,8 +304,13 @@ int vxr_mark_sites(void* esdf, void* tsdf, const vxm_grid_index* upd, uint64_t n
                    const vxm_esdf_config* c, void* s, vxm_grid_index** out, uint64_t* n) {
   return guard([&] {
     std::vector<vr::GridIndex> changed;
-    vr::mark_sites(*static_cast<RefLayer*>(esdf)->esdf, *static_cast<RefLayer*>(tsdf)->tsdf,
-                   to_list(upd, nu), to_ecfg(c), &static_cast<RefState*>(s)->st, &changed);
+    auto* T = static_cast<RefLayer*>(tsdf);
+    if (T->occ)
+      vr::mark_sites(*static_cast<RefLayer*>(esdf)->esdf, *T->occ, to_list(upd, nu), to_ecfg(c),
+                     &static_cast<RefState*>(s)->st, &changed);
+    else
+      vr::mark_sites(*static_cast<RefLayer*>(esdf)->esdf, *T->tsdf, to_list(upd, nu), to_ecfg(c),
+                     &static_cast<RefState*>(s)->st, &changed);
     emit(changed, out, n);
   });
 }
@@ -389,28 +415,37 @@ int vxr_compare_esdf(void* a, void* b, uint64_t* stats4, double* max_abs) {
 
 // save_snapshot / load_snapshot (core/serialization.cpp:88-158) on a cake
 // that borrows the driver's layers.
-int vxr_snapshot_save(const char* path, double vs, void* tsdf, void* esdf) {
+int vxr_snapshot_save(const char* path, double vs, void* tsdf, void* occ, void* esdf) {
   return guard([&] {
     vr::LayerCake cake(vs);
     if (tsdf) cake.tsdf.reset(static_cast<RefLayer*>(tsdf)->tsdf);
+    if (occ) cake.occupancy.reset(static_cast<RefLayer*>(occ)->occ);
     if (esdf) cake.esdf.reset(static_cast<RefLayer*>(esdf)->esdf);
+    const auto release = [&] {
+      cake.tsdf.release();
+      cake.occupancy.release();
+      cake.esdf.release();
+    };
     try {
       vr::save_snapshot(cake, path);
     } catch (...) {
-      cake.tsdf.release();
-      cake.esdf.release();
+      release();
       throw;
     }
-    cake.tsdf.release();
-    cake.esdf.release();
+    release();
   });
 }
-int vxr_snapshot_load(const char* path, double* vs, void** tsdf, void** esdf) {
+int vxr_snapshot_load(const char* path, double* vs, void** tsdf, void** occ, void** esdf) {
   return guard([&] {
     vr::LayerCake cake = vr::load_snapshot(path);
     *vs = cake.voxel_size;
-    *tsdf = *esdf = nullptr;
+    *tsdf = *occ = *esdf = nullptr;
     if (cake.tsdf) *tsdf = new RefLayer{VXM_LAYER_TSDF, cake.tsdf.release(), nullptr};
+    if (cake.occupancy) {
+      auto* L = new RefLayer{VXM_LAYER_OCCUPANCY};
+      L->occ = cake.occupancy.release();
+      *occ = L;
+    }
     if (cake.esdf) *esdf = new RefLayer{VXM_LAYER_ESDF, nullptr, cake.esdf.release()};
   });
 }

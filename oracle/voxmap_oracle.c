@@ -192,7 +192,7 @@ static void gvec_emit(gvec* a, vxm_grid_index** out, uint64_t* n) {
 /* Layer<V> — include/voxmap/core/layer.hpp:47-125                          */
 
 struct vxo_layer {
-  int type; /* VXM_LAYER_TSDF / VXM_LAYER_ESDF */
+  int type; /* VXM_LAYER_TSDF / VXM_LAYER_ESDF / VXM_LAYER_OCCUPANCY */
   double vs;
   uint64_t max_blocks;
   size_t vbytes; /* voxel bytes */
@@ -208,7 +208,9 @@ int vxo_layer_create(int type, double vs, uint64_t max_blocks, vxo_layer** out) 
   L->type = type;
   L->vs = vs;
   L->max_blocks = max_blocks ? max_blocks : (1ull << 30);
-  L->vbytes = type == VXM_LAYER_TSDF ? sizeof(vxm_tsdf_voxel) : sizeof(vxm_esdf_voxel);
+  L->vbytes = type == VXM_LAYER_TSDF   ? sizeof(vxm_tsdf_voxel)
+              : type == VXM_LAYER_ESDF ? sizeof(vxm_esdf_voxel)
+                                       : sizeof(vxm_occupancy_voxel);
   *out = L;
   return VXM_OK;
 }
@@ -486,6 +488,18 @@ static vxm_tsdf_voxel tsdf_update(vxm_tsdf_voxel vox, float d_p, float w_new,
   out.weight = cfg->max_weight < w_sum ? cfg->max_weight : w_sum;
   return out;
 }
+/* quantize_log_odds — integrate/config.hpp:29-31 */
+static float quantize_log_odds(float v) { return (float)(nearbyint((double)v * 4096.0) / 4096.0); }
+/* occupancy_update — updates.hpp:59-72 */
+static float occupancy_update(float lo, float d_p, const vxm_integrator_config* cfg) {
+  const float eps = (float)cfg->truncation;
+  if (d_p < -eps) return lo;
+  const float inc = d_p <= 0.0f ? quantize_log_odds(cfg->hit_log_odds)
+                                : quantize_log_odds(cfg->miss_log_odds);
+  const float v = lo + inc;
+  const float lo_min = quantize_log_odds(cfg->log_odds_min), lo_max = quantize_log_odds(cfg->log_odds_max);
+  return v < lo_min ? lo_min : (lo_max < v ? lo_max : v);
+}
 /* weight_for_depth — updates.hpp:27-32 */
 static float weight_for_depth(double d, const vxm_integrator_config* cfg) {
   if (cfg->weighting == VXM_WEIGHT_INVERSE_SQUARE) {
@@ -530,6 +544,8 @@ static int integrate_impl(vxo_layer* L, const float* depth, int W, int H, const 
   for (uint64_t i = 0; i < cand.n; ++i) {
     const gidx g = cand.v[i];
     vxm_tsdf_voxel* blk = (vxm_tsdf_voxel*)block_ptr(L, g);
+    float* oblk = (float*)blk; /* Layer<OccupancyVoxel> (integrator.cpp:148-158) */
+    const int occ = L->type == VXM_LAYER_OCCUPANCY;
     int block_changed = 0;
     for (int lin = 0; lin < VPB; ++lin) {
       const int vx = lin % VPS, vy = (lin / VPS) % VPS, vz = lin / (VPS * VPS);
@@ -554,6 +570,14 @@ static int integrate_impl(vxo_layer* L, const float* depth, int W, int H, const 
                                                 : sample_linear(depth, W, H, u, w, cfg->max_sample_gap, &s);
       if (!ok) continue;
       const float d_p = s - (float)d_v;
+      if (occ) {
+        const float nv = occupancy_update(oblk[lin], d_p, cfg);
+        if (memcmp(&nv, &oblk[lin], sizeof nv) != 0) {
+          oblk[lin] = nv;
+          block_changed = 1;
+        }
+        continue;
+      }
       const vxm_tsdf_voxel nv = tsdf_update(blk[lin], d_p, weight_for_depth((double)s, cfg), cfg);
       if (memcmp(&nv, &blk[lin], sizeof nv) != 0) {
         blk[lin] = nv;
@@ -709,7 +733,37 @@ static gidx gstep(gidx g, int axis, int s) {
   return g;
 }
 
-/* mark_impl with TsdfClassifier — esdf/integrator.cpp:177-198, 268-348 */
+/* OccupancyClassifier — esdf/integrator.cpp:200-266 */
+static int occ_observed(float lo) { return lo != 0.0f; }
+static int occ_free(float lo, float thr) { return occ_observed(lo) && !(lo > thr); }
+static void occ_classify(const vxo_layer* occ, gidx g, const float* blk, int lin, float thr,
+                         int* observed, int* site, int* inside) {
+  const float lo = blk[lin];
+  *observed = occ_observed(lo);
+  *site = *inside = 0;
+  if (!*observed) return;
+  *inside = lo > thr;
+  if (!*inside) return; /* free voxels are never sites */
+  const int v[3] = {lin % VPS, (lin / VPS) % VPS, lin / (VPS * VPS)};
+  for (int n = 0; n < 6; ++n) { /* steps {+x,-x,+y,-y,+z,-z} */
+    const int axis = n / 2, step = (n & 1) ? -1 : 1;
+    int c[3] = {v[0], v[1], v[2]};
+    c[axis] += step;
+    const float* nb = NULL;
+    if (c[axis] >= 0 && c[axis] < VPS) {
+      nb = blk;
+    } else {
+      nb = (const float*)block_ptr(occ, gstep(g, axis, step));
+      c[axis] = (c[axis] + VPS) % VPS;
+    }
+    if (nb && occ_free(nb[c[0] + VPS * (c[1] + VPS * c[2])], thr)) {
+      *site = 1;
+      return;
+    }
+  }
+}
+
+/* mark_impl with TsdfClassifier / OccupancyClassifier — esdf/integrator.cpp:177-348 */
 static int mark_sites(vxo_layer* esdf, const vxo_layer* tsdf, const gidx* upd, uint64_t nu,
                       const vxm_esdf_config* cfg, vxo_state* st, gvec* changed) {
   const limits_t lim = limits_for(cfg, esdf->vs);
@@ -734,10 +788,16 @@ static int mark_sites(vxo_layer* esdf, const vxo_layer* tsdf, const gidx* upd, u
     const vxm_tsdf_voxel* src = (const vxm_tsdf_voxel*)block_ptr(tsdf, g);
     int bchanged = 0, bupdate = 0, bclear = 0;
     for (int lin = 0; lin < VPB; ++lin) {
-      const vxm_tsdf_voxel tv = src[lin];
-      const int observed = tv.weight > 0.0f;
-      const int site = observed && fabsf(tv.distance) <= site_threshold;
-      const int inside = observed && tv.distance < 0.0f;
+      int observed, site, inside;
+      if (tsdf->type == VXM_LAYER_OCCUPANCY) {
+        occ_classify(tsdf, g, (const float*)src, lin, cfg->occupied_log_odds_threshold, &observed,
+                     &site, &inside);
+      } else {
+        const vxm_tsdf_voxel tv = src[lin];
+        observed = tv.weight > 0.0f;
+        site = observed && fabsf(tv.distance) <= site_threshold;
+        inside = observed && tv.distance < 0.0f;
+      }
       ev_t* ev = &blk[lin];
       ev_t nv = *ev;
       if (!observed) {

@@ -1,6 +1,6 @@
 """B200-native per-frame map update (nvblox / voxmap hot path).
 
-Block allocation -> TSDF projective integration -> ESDF -> queries, as
+Block allocation -> TSDF / occupancy projective integration -> ESDF -> queries, as
 hand-written sm_100a CUDA behind the C-ABI in include/voxmap_b200.h.  The
 Python API mirrors the reference's C++ mapper API (see voxmap.py).
 """
@@ -12,4 +12,4 @@ from .voxmap import (BlockList, CameraIntrinsics, Context, EsdfConfig, EsdfLayer
                      integrate_depth_device, lib, lower_esdf, mark_sites, query_batch,
                      update_esdf, update_esdf_device, update_frame_device,
                      IoError, save_snapshot, load_snapshot, update_esdf_sharded,
-                     make_replay_config, replay, write_timing_csv)
+                     make_replay_config, replay, write_timing_csv, OccupancyLayer)

@@ -20,6 +20,7 @@ VXM_ERR_IO = 6
 
 LAYER_TSDF = 0
 LAYER_ESDF = 1
+LAYER_OCCUPANCY = 2
 
 WEIGHT_CONSTANT = 0
 WEIGHT_INVERSE_SQUARE = 1
@@ -37,7 +38,12 @@ ESDF_INSIDE = 4
 TSDF_DTYPE = np.dtype([("distance", "<f4"), ("weight", "<f4")])
 ESDF_DTYPE = np.dtype([("squared_distance", "<i4"), ("parent_x", "<i2"), ("parent_y", "<i2"),
                        ("parent_z", "<i2"), ("flags", "u1"), ("reserved", "u1")])
-assert TSDF_DTYPE.itemsize == 8 and ESDF_DTYPE.itemsize == 12
+OCCUPANCY_DTYPE = np.dtype([("log_odds", "<f4")])
+assert TSDF_DTYPE.itemsize == 8 and ESDF_DTYPE.itemsize == 12 and OCCUPANCY_DTYPE.itemsize == 4
+
+
+def layer_dtype(kind):
+    return {LAYER_TSDF: TSDF_DTYPE, LAYER_ESDF: ESDF_DTYPE, LAYER_OCCUPANCY: OCCUPANCY_DTYPE}[kind]
 
 
 class GridIndex(C.Structure):
@@ -80,9 +86,10 @@ class EsdfConfigC(C.Structure):
 
 
 class ReplayConfigC(C.Structure):
-    """vxm_replay_config — ReplayConfig (io/pipeline.hpp:27-35), TSDF source."""
+    """vxm_replay_config — ReplayConfig (io/pipeline.hpp:27-35)."""
     _fields_ = [("voxel_size", C.c_double), ("update_every", C.c_int32),
-                ("integrator", IntegratorConfigC), ("esdf", EsdfConfigC)]
+                ("integrator", IntegratorConfigC), ("esdf", EsdfConfigC),
+                ("use_occupancy", C.c_int32)]
 
 
 FRAME_TIMING_DTYPE = np.dtype([("frame", "<i4"), ("pad_", "<i4"), ("tsdf_ms", "<f8"),

@@ -117,6 +117,12 @@ void ensure_sorted_unique(vxm_blocklist* list) {
   list->sorted_unique = true;
 }
 
+// The ESDF's source layer: Layer<TsdfVoxel> or Layer<OccupancyVoxel>
+// (esdf/integrator.hpp:81-120 overloads).
+bool is_source(const vxm_layer* L) {
+  return L->type == VXM_LAYER_TSDF || L->type == VXM_LAYER_OCCUPANCY;
+}
+
 void check_pose(const vxm_pose* T) {
   if (!vxm_pose_valid(T)) throw Error(VXM_ERR_INVALID_POSE, "integrate: degenerate sensor pose");
 }
@@ -137,7 +143,8 @@ void stage_depth(Context* ctx, const float* depth, int w, int h, bool on_device,
 ViewArgs frame_args(vxm_layer* L, const float* depth, int w, int h, const vxm_pose* T,
                     const vxm_camera* cam, const vxm_lidar* li, const vxm_integrator_config* cfg,
                     bool on_device) {
-  REQUIRE_ARG(L->type == VXM_LAYER_TSDF, "integrate: layer is not a TSDF layer");
+  REQUIRE_ARG(L->type == VXM_LAYER_TSDF || L->type == VXM_LAYER_OCCUPANCY,
+              "integrate: layer is not a TSDF or occupancy layer");
   check_pose(T);
   const int sw = cam ? cam->width : li->num_azimuth;
   const int sh = cam ? cam->height : li->num_elevation;
@@ -183,7 +190,7 @@ vxm_status frame_common(vxm_layer* T, vxm_layer* E, const float* depth, int w, i
     REQUIRE_ARG(T && pose && icfg && tout && (cam || li), "update_frame: null argument");
     if (E) {
       REQUIRE_ARG(ecfg && eout, "update_frame: null ESDF argument");
-      REQUIRE_ARG(E->type == VXM_LAYER_ESDF, "update_esdf: expects (ESDF layer, TSDF layer)");
+      REQUIRE_ARG(E->type == VXM_LAYER_ESDF, "update_esdf: expects (ESDF layer, TSDF or occupancy layer)");
       REQUIRE_ARG(E->ctx == T->ctx, "update_frame: layers on different contexts");
       if (E->vs != T->vs)
         throw Error(VXM_ERR_INVALID_ARGUMENT, "update_esdf: source and ESDF layer voxel sizes differ");
@@ -401,7 +408,8 @@ vxm_status vxm_layer_create(vxm_context* ctx, vxm_layer_type type, double vs, ui
   return guard([&] {
     REQUIRE_ARG(ctx && out, "null argument");
     if (!(vs > 0.0)) throw Error(VXM_ERR_INVALID_ARGUMENT, "Layer: voxel_size must be positive");
-    REQUIRE_ARG(type == VXM_LAYER_TSDF || type == VXM_LAYER_ESDF, "unknown layer type");
+    REQUIRE_ARG(type == VXM_LAYER_TSDF || type == VXM_LAYER_ESDF || type == VXM_LAYER_OCCUPANCY,
+                "unknown layer type");
     auto* L = new vxm_layer();
     L->ctx = ctx;
     L->type = type;
@@ -798,8 +806,8 @@ vxm_status vxm_update_esdf_list(vxm_layer* E, vxm_layer* T, vxm_blocklist* updat
                                 const vxm_esdf_config* cfg, vxm_blocklist* out) {
   return guard([&] {
     REQUIRE_ARG(E && T && updated && cfg && out, "null argument");
-    REQUIRE_ARG(E->type == VXM_LAYER_ESDF && T->type == VXM_LAYER_TSDF,
-                "update_esdf: expects (ESDF layer, TSDF layer)");
+    REQUIRE_ARG(E->type == VXM_LAYER_ESDF && is_source(T),
+                "update_esdf: expects (ESDF layer, TSDF or occupancy layer)");
     out->ctx = E->ctx;
     // esdf/integrator.cpp:371-378: empty input returns {} before the size check
     if (updated->count_hint == 0 || (updated->host_valid && updated->host.empty())) {
@@ -856,6 +864,8 @@ vxm_status vxm_esdf_mark_sites(vxm_layer* E, vxm_layer* T, const vxm_grid_index*
                                vxm_blocklist* changed) {
   return guard([&] {
     REQUIRE_ARG(E && T && cfg && st && changed, "null argument");
+    REQUIRE_ARG(E->type == VXM_LAYER_ESDF && is_source(T),
+                "mark_sites: expects (ESDF layer, TSDF or occupancy layer)");
     std::vector<vxm_grid_index> ch;
     if (n) {
       vxm_blocklist list;
@@ -973,12 +983,15 @@ void read_layer(FILE* f, vxm_layer* L) {
 }  // namespace
 
 extern "C" {
-vxm_status vxm_snapshot_save(const char* path, double vs, vxm_layer* tsdf, vxm_layer* esdf) {
+vxm_status vxm_snapshot_save_layers(const char* path, double vs, vxm_layer* tsdf, vxm_layer* occ,
+                                    vxm_layer* esdf) {
   return guard([&] {
     REQUIRE_ARG(path, "null argument");
     REQUIRE_ARG(!tsdf || tsdf->type == VXM_LAYER_TSDF, "snapshot: tsdf argument is not a TSDF layer");
+    REQUIRE_ARG(!occ || occ->type == VXM_LAYER_OCCUPANCY,
+                "snapshot: occupancy argument is not an occupancy layer");
     REQUIRE_ARG(!esdf || esdf->type == VXM_LAYER_ESDF, "snapshot: esdf argument is not an ESDF layer");
-    REQUIRE_ARG((!tsdf || tsdf->vs == vs) && (!esdf || esdf->vs == vs),
+    REQUIRE_ARG((!tsdf || tsdf->vs == vs) && (!occ || occ->vs == vs) && (!esdf || esdf->vs == vs),
                 "snapshot: layer voxel size differs from the snapshot's");
     File out;
     out.f = std::fopen(path, "wb");
@@ -986,17 +999,22 @@ vxm_status vxm_snapshot_save(const char* path, double vs, vxm_layer* tsdf, vxm_l
     if (std::fwrite(kVxlfMagic, 1, 4, out.f) != 4) io_fail("snapshot: write failed");
     put(out.f, kVxlfVersion);
     put(out.f, vs);  // f64
-    const uint32_t count = (tsdf ? 1u : 0u) + (esdf ? 1u : 0u);
+    const uint32_t count = (tsdf ? 1u : 0u) + (occ ? 1u : 0u) + (esdf ? 1u : 0u);
     put(out.f, count);
     if (tsdf) write_layer(out.f, "tsdf", tsdf);  // serialization.cpp:102-105 order
+    if (occ) write_layer(out.f, "occupancy", occ);
     if (esdf) write_layer(out.f, "esdf", esdf);
     if (std::fflush(out.f) != 0) io_fail(std::string("snapshot: write failed: ") + path);
   });
 }
+vxm_status vxm_snapshot_save(const char* path, double vs, vxm_layer* tsdf, vxm_layer* esdf) {
+  return vxm_snapshot_save_layers(path, vs, tsdf, nullptr, esdf);
+}
 
-vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* vs_out, vxm_layer** tsdf_out,
-                             vxm_layer** esdf_out) {
+vxm_status vxm_snapshot_load_layers(vxm_context* ctx, const char* path, double* vs_out,
+                                    vxm_layer** tsdf_out, vxm_layer** occ_out, vxm_layer** esdf_out) {
   vxm_layer* T = nullptr;
+  vxm_layer* O = nullptr;
   vxm_layer* E = nullptr;
   const vxm_status st = guard([&] {
     REQUIRE_ARG(ctx && path && tsdf_out && esdf_out, "null argument");
@@ -1020,15 +1038,19 @@ vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* vs_out,
       if (name_len > 64) io_fail("snapshot: layer name too long");
       std::string name(name_len, '\0');
       if (std::fread(name.data(), 1, name_len, in.f) != name_len) io_fail("snapshot: truncated layer name");
-      if (name == "tsdf" || name == "esdf") {
-        vxm_layer*& L = name == "tsdf" ? T : E;
+      if (name == "tsdf" || name == "esdf" || (name == "occupancy" && occ_out)) {
+        vxm_layer*& L = name == "tsdf" ? T : name == "esdf" ? E : O;
         if (!L) {
-          const vxm_status s = vxm_layer_create(ctx, name == "tsdf" ? VXM_LAYER_TSDF : VXM_LAYER_ESDF, vs,
-                                                0, &L);
+          const vxm_layer_type type = name == "tsdf"   ? VXM_LAYER_TSDF
+                                      : name == "esdf" ? VXM_LAYER_ESDF
+                                                       : VXM_LAYER_OCCUPANCY;
+          const vxm_status s = vxm_layer_create(ctx, type, vs, 0, &L);
           if (s != VXM_OK) throw Error(s, g_err);
         }
         read_layer(in.f, L);
-      } else if (name == "occupancy" || name == "color") {
+      } else if (name == "occupancy") {
+        io_fail("snapshot: the file holds an occupancy layer (use vxm_snapshot_load_layers)");
+      } else if (name == "color") {
         io_fail("snapshot: layer '" + name + "' is not implemented by this library");
       } else {
         io_fail("snapshot: unknown layer name '" + name + "'");
@@ -1036,13 +1058,19 @@ vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* vs_out,
     }
     *vs_out = vs;
     *tsdf_out = T;
+    if (occ_out) *occ_out = O;
     *esdf_out = E;
   });
   if (st != VXM_OK) {
     vxm_layer_destroy(T);
+    vxm_layer_destroy(O);
     vxm_layer_destroy(E);
   }
   return st;
+}
+vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* vs_out, vxm_layer** tsdf_out,
+                             vxm_layer** esdf_out) {
+  return vxm_snapshot_load_layers(ctx, path, vs_out, tsdf_out, nullptr, esdf_out);
 }
 }  // extern "C"
 
@@ -1063,7 +1091,9 @@ vxm_status replay_common(vxm_context* ctx, const vxm_replay_config* cfg, const v
     if (n <= 0) throw Error(VXM_ERR_INVALID_ARGUMENT, "replay: dataset has no frames");
     if (cfg->update_every < 1) throw Error(VXM_ERR_INVALID_ARGUMENT, "replay: update_every must be >= 1");
     REQUIRE_ARG(depth && poses, "null argument");
-    vxm_status s = vxm_layer_create(ctx, VXM_LAYER_TSDF, cfg->voxel_size, 0, &T);
+    // the source layer: TSDF, or occupancy with use_occupancy (pipeline.cpp:95-101)
+    vxm_status s = vxm_layer_create(ctx, cfg->use_occupancy ? VXM_LAYER_OCCUPANCY : VXM_LAYER_TSDF,
+                                    cfg->voxel_size, 0, &T);
     if (s != VXM_OK) throw Error(s, g_err);
     s = vxm_layer_create(ctx, VXM_LAYER_ESDF, cfg->voxel_size, 0, &E);
     if (s != VXM_OK) throw Error(s, g_err);
@@ -1129,6 +1159,7 @@ extern "C" {
 void vxm_replay_config_make(double voxel_size, vxm_replay_config* out) {
   out->voxel_size = voxel_size;
   out->update_every = 4;
+  out->use_occupancy = 0;
   vxm_integrator_config_default(&out->integrator);
   vxm_esdf_config_default(&out->esdf);
   out->integrator.truncation = 4.0 * voxel_size;

@@ -725,13 +725,15 @@ __device__ inline void post_alloc(const PostAllocArgs& p) {
   }
 }
 
-// ---- mark_sites (TSDF source) — esdf/integrator.cpp:177-198, 268-348 ------------
+// ---- mark_sites — esdf/integrator.cpp:177-266 (classifiers), 268-348 ------------
 struct MarkArgs {
   const uint64_t* eff_keys;
   const int32_t* eff_tslot;
   const int32_t* eff_eslot;
   const uint32_t* n_eff;
-  const float2* tsdf_pool;
+  const void* src_pool;  // TSDF (float2) or occupancy (float) blocks
+  HashView src_hash;     // occupancy: the 6 face-neighbour blocks
+  float occ_threshold;   // EsdfConfig::occupied_log_odds_threshold
   uint32_t* pools[2];
   const LayerMeta* meta;
   float site_threshold;
@@ -744,10 +746,39 @@ struct MarkArgs {
   PostAllocArgs post;
 };
 
+// OccupancyClassifier (esdf/integrator.cpp:200-266): observed = log_odds != 0;
+// inside = occupied = observed && log_odds > threshold; a site is an occupied
+// voxel with an observed-free 6-neighbour, looked up in the face-neighbour
+// block across a border (absent neighbour block: no neighbour).
+__device__ inline bool occ_free(float lo, float thr) { return lo != 0.0f && !(lo > thr); }
+
+__device__ inline bool occ_has_free_neighbour(const float* src, int32_t self, const int32_t nb[6],
+                                              int lin, float thr) {
+  const int x = lin & 7, y = (lin >> 3) & 7, z = lin >> 6;
+  const int c[3] = {x, y, z};
+#pragma unroll
+  for (int n = 0; n < 6; ++n) {  // {+x, -x, +y, -y, +z, -z} (:229-231)
+    const int axis = n >> 1, step = (n & 1) ? -1 : 1;
+    const int m = c[axis] + step;
+    int32_t blk = self;
+    int nl;
+    if (m >= 0 && m < 8) {
+      nl = lin + step * (axis == 0 ? 1 : axis == 1 ? 8 : 64);
+    } else {
+      blk = nb[n];
+      nl = lin + step * (axis == 0 ? -7 : axis == 1 ? -56 : -448);  // wrap (N + m) % N
+    }
+    if (blk >= 0 && occ_free(__ldg(src + size_t(blk) * kVPB + nl), thr)) return true;
+  }
+  return false;
+}
+
 // One warp per effective block: lane l holds voxels 4 * (l + 32 h) + e
 // (h = 0..3, e = 0..3), so the ESDF block (3 x 16-byte words per 4 voxels)
-// and the TSDF block (2 x 16-byte words per 4 voxels) load and store
-// coalesced, all in flight at once; the block flags are warp ballots.
+// and the source block (TSDF: 2, occupancy: 1 x 16-byte words per 4 voxels)
+// load and store coalesced, all in flight at once; the block flags are warp
+// ballots.
+template <bool OCC>
 __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
   const uint32_t n = *a.n_eff;
   uint32_t* pool = a.pools[a.meta->cur];
@@ -760,11 +791,20 @@ __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
       continue;
     }
     const int32_t ts = a.eff_tslot[e];
-    const uint4* t4 = reinterpret_cast<const uint4*>(a.tsdf_pool + size_t(ts) * kVPB);
+    constexpr int kSrcWords = OCC ? 1 : 2;  // 16-byte source words per 4 voxels
+    const uint4* t4 = reinterpret_cast<const uint4*>(
+        static_cast<const unsigned char*>(a.src_pool) + size_t(ts) * kVPB * 4 * kSrcWords);
     uint4* e4 = reinterpret_cast<uint4*>(pool + size_t(es) * 1536);
     bool bch = false, bup = false, bcl = false, bsite = false;
     uint32_t w[48];
-    float tv[32];
+    float tv[16 * kSrcWords];
+    int32_t nb[6];
+    if (OCC) {  // BlockCtx::neighbors (:216-226): lanes 0..5 probe, then broadcast
+      int32_t mine = -1;
+      if (lane < 6) mine = hash_find(a.src_hash, key_shift(a.eff_keys[e], lane >> 1, (lane & 1) ? -1 : 1));
+#pragma unroll
+      for (int n = 0; n < 6; ++n) nb[n] = __shfl_sync(0xffffffffu, mine, n);
+    }
 #pragma unroll
     for (int h = 0; h < 4; ++h) {  // all loads in flight before any use
       const int q = lane + 32 * h;  // voxels 4q .. 4q + 3
@@ -775,10 +815,11 @@ __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
         w[12 * h + 4 * j + 2] = v.z; w[12 * h + 4 * j + 3] = v.w;
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint4 v = __ldcg(t4 + 2 * q + j);
-        tv[8 * h + 4 * j] = __uint_as_float(v.x); tv[8 * h + 4 * j + 1] = __uint_as_float(v.y);
-        tv[8 * h + 4 * j + 2] = __uint_as_float(v.z); tv[8 * h + 4 * j + 3] = __uint_as_float(v.w);
+      for (int j = 0; j < kSrcWords; ++j) {
+        const uint4 v = __ldcg(t4 + kSrcWords * q + j);
+        const int o = 4 * kSrcWords * h + 4 * j;
+        tv[o] = __uint_as_float(v.x); tv[o + 1] = __uint_as_float(v.y);
+        tv[o + 2] = __uint_as_float(v.z); tv[o + 3] = __uint_as_float(v.w);
       }
     }
 #pragma unroll
@@ -788,10 +829,19 @@ __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
 #pragma unroll
       for (int v4 = 0; v4 < 4; ++v4) {
         const int v = 4 * h + v4;
-        const float dist = tv[2 * v], weight = tv[2 * v + 1];
-        const bool observed = weight > 0.0f;
-        const bool site = observed && fabsf(dist) <= a.site_threshold;
-        const bool inside = observed && dist < 0.0f;
+        bool observed, site, inside;
+        if (!OCC) {  // TsdfClassifier — :177-198
+          const float dist = tv[2 * v], weight = tv[2 * v + 1];
+          observed = weight > 0.0f;
+          site = observed && fabsf(dist) <= a.site_threshold;
+          inside = observed && dist < 0.0f;
+        } else {     // OccupancyClassifier — :200-266
+          const float lo = tv[v];
+          observed = lo != 0.0f;
+          inside = observed && lo > a.occ_threshold;
+          site = inside && occ_has_free_neighbour(static_cast<const float*>(a.src_pool), ts, nb,
+                                                  4 * q + v4, a.occ_threshold);
+        }
         bsite |= site;
         const uint32_t o0 = w[3 * v], o1 = w[3 * v + 1], o2 = w[3 * v + 2];
         const EV ev = ev_unpack(o0, o1, o2);
@@ -971,7 +1021,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   const uint32_t n7 = 7u * nu_cap;
   const uint64_t* upd = updated->keys.as<uint64_t>();
   ctx->prof_begin("k_merge7");
-  k_merge7<<<grid_for(ctx, n7, 2), 256, 0, ctx->stream>>>(upd, updated->d_count, s.merged);
+  k_merge7<<<grid_for(ctx, n7), 256, 0, ctx->stream>>>(upd, updated->d_count, s.merged);
   ctx->prof_end();
   ctx->count_launch();
   {
@@ -991,7 +1041,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
     al.status = ctx->d_status;
     const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
     ctx->prof_begin("k_effective_alloc");
-    k_effective_alloc<<<grid_for(ctx, n7, 1), 256, 0, ctx->stream>>>(
+    k_effective_alloc<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(
         s.merged, updated->d_count, T->hash, s.eff_keys, s.eff_tslot, s.counts + 0, al, st);
     ctx->prof_end();
     ctx->count_launch();
@@ -1006,7 +1056,10 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.eff_tslot = s.eff_tslot;
   m.eff_eslot = s.eff_eslot;
   m.n_eff = s.counts + 0;
-  m.tsdf_pool = static_cast<const float2*>(T->pool[0]);
+  const bool occ = T->type == VXM_LAYER_OCCUPANCY;
+  m.src_pool = T->pool[0];
+  m.src_hash = T->hash;
+  m.occ_threshold = cfg.occupied_log_odds_threshold;
   m.pools[0] = static_cast<uint32_t*>(E->pool[0]);
   m.pools[1] = static_cast<uint32_t*>(E->pool[1]);
   m.meta = E->meta;
@@ -1019,12 +1072,16 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.site_any = E->site_any;
   m.post = pa;
   ctx->prof_begin("k_mark");
-  static int mark_per_sm = 0;  // one wave of warps, each takes blocks until done
-  if (!mark_per_sm) {
-    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mark_per_sm, k_mark, 256, 0));
-    mark_per_sm = std::max(mark_per_sm, 1);
+  static int mark_per_sm[2] = {0, 0};  // one wave of warps, each takes blocks until done
+  if (!mark_per_sm[occ]) {
+    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mark_per_sm[occ],
+                                                           occ ? k_mark<true> : k_mark<false>, 256, 0));
+    mark_per_sm[occ] = std::max(mark_per_sm[occ], 1);
   }
-  k_mark<<<ctx->sm_count * mark_per_sm, 256, 0, ctx->stream>>>(m);
+  if (occ)
+    k_mark<true><<<ctx->sm_count * mark_per_sm[occ], 256, 0, ctx->stream>>>(m);
+  else
+    k_mark<false><<<ctx->sm_count * mark_per_sm[occ], 256, 0, ctx->stream>>>(m);
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "esdf mark phase");

@@ -1,7 +1,10 @@
-// TSDF projective integration.
+// TSDF / occupancy projective integration (
+// occupancy: §8(f) rank 3).
 //
-// Reference: integrate_impl (proj/src/integrate/integrator.cpp:71-134),
-// tsdf_update / weight_for_depth (proj/include/voxmap/integrate/updates.hpp:27-54),
+// Reference: integrate_impl (proj/src/integrate/integrator.cpp:71-134) with
+// integrate_tsdf / integrate_occupancy (:136-158), tsdf_update /
+// weight_for_depth (proj/include/voxmap/integrate/updates.hpp:27-54),
+// occupancy_update (updates.hpp:59-72), quantize_log_odds (config.hpp:29-31),
 // CameraIntrinsics::project/contains (sensor/camera.hpp:35-46), LiDAR project
 // (sensor/lidar.hpp:43-55), sample_depth_nearest/linear (sensor/image.hpp:65-106).
 //
@@ -28,7 +31,7 @@ struct IntegrateArgs {
   const uint64_t* cand_keys;
   const int32_t* cand_slots;
   const DevStatus* status_ro;
-  float2* pool;
+  void* pool;  // float2 (TSDF) or float (occupancy log-odds) per voxel
   uint8_t* changed;
   const float* depth;
   int W, H;
@@ -42,6 +45,44 @@ struct IntegrateArgs {
   double max_voxel_depth;
   float eps, max_weight, max_gap;
   int inv_sq, linear;
+  float hit, miss, lo_min, lo_max;  // occupancy: quantize_log_odds of the config values
+};
+
+// The per-voxel update of each layer kind (the reference's UpdateFn,
+// integrator.cpp:136-158).  apply() runs after the common occlusion test
+// d_p < -eps (both updates return the voxel unchanged there) and returns
+// whether the voxel's bytes change.
+template <bool OCC>
+struct VoxOps;
+template <>
+struct VoxOps<false> {  // tsdf_update — updates.hpp:39-54
+  using V = float2;
+  __device__ static V zero() { return make_float2(0.0f, 0.0f); }
+  __device__ static V load_cs(const V* p) { return __ldcs(p); }
+  __device__ static bool apply(const IntegrateArgs& a, V o, float d_p, float s, V& nv) {
+    float w_new = 1.0f;
+    if (a.inv_sq) {  // weight_for_depth — updates.hpp:27-32
+      const double dd = __dmul_rn(double(s), double(s));
+      w_new = __double2float_rn(__ddiv_rn(1.0, dd < 1e-6 ? 1e-6 : dd));
+    }
+    const float d_t = d_p < -a.eps ? -a.eps : (a.eps < d_p ? a.eps : d_p);
+    const float w_sum = __fadd_rn(o.y, w_new);
+    const float avg = __fdiv_rn(__fadd_rn(__fmul_rn(o.y, o.x), __fmul_rn(w_new, d_t)), w_sum);
+    nv.x = avg < -a.eps ? -a.eps : (a.eps < avg ? a.eps : avg);
+    nv.y = a.max_weight < w_sum ? a.max_weight : w_sum;
+    return __float_as_uint(nv.x) != __float_as_uint(o.x) || __float_as_uint(nv.y) != __float_as_uint(o.y);
+  }
+};
+template <>
+struct VoxOps<true> {  // occupancy_update — updates.hpp:59-72
+  using V = float;
+  __device__ static V zero() { return 0.0f; }
+  __device__ static V load_cs(const V* p) { return __ldcs(p); }
+  __device__ static bool apply(const IntegrateArgs& a, V o, float d_p, float, V& nv) {
+    const float v = __fadd_rn(o, d_p <= 0.0f ? a.hit : a.miss);
+    nv = v < a.lo_min ? a.lo_min : (a.lo_max < v ? a.lo_max : v);  // std::clamp
+    return __float_as_uint(nv) != __float_as_uint(o);
+  }
 };
 
 __device__ inline bool valid_depth_i(float d) { return d > 0.0f && isfinite(d); }
@@ -95,9 +136,10 @@ __device__ inline bool fast_floor(float f, float c, float xf, float zf, int* idx
   return true;
 }
 
-// One voxel: projection, sample, tsdf_update (integrator.cpp:98-123); returns
+// One voxel: projection, sample, update (integrator.cpp:98-123); returns
 // whether its bytes changed.  p = T_SL * centre (FP64, pinned order).
-__device__ inline bool integrate_voxel(const IntegrateArgs& a, float2* blk, int lin, double px,
+template <bool OCC>
+__device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<OCC>::V* blk, int lin, double px,
                                        double py, double pz, bool is_new, uint32_t& n_read,
                                        uint32_t& n_upd) {
   double d_v;
@@ -107,9 +149,11 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, float2* blk, int 
     d_v = __dsqrt_rn(__dadd_rn(__dmul_rn(px, px), __dadd_rn(__dmul_rn(py, py), __dmul_rn(pz, pz))));
   }
   if (!(d_v > 0.0) || d_v > a.max_voxel_depth) return false;  // integrator.cpp:104-107
+  using Ops = VoxOps<OCC>;
+  using V = typename Ops::V;
   float s;
   bool ok;
-  float2 old = make_float2(0.0f, 0.0f);
+  V old = Ops::zero();
   bool have_old = false;
   if (!a.lidar) {
     if (!a.linear) {
@@ -152,22 +196,11 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, float2* blk, int 
   }
   if (!ok) return false;
   const float d_p = __fsub_rn(s, __double2float_rn(d_v));  // integrator.cpp:116
-  // tsdf_update — updates.hpp:39-54
-  if (d_p < -a.eps) return false;  // occluded: voxel unchanged
-  float w_new = 1.0f;
-  if (a.inv_sq) {
-    const double dd = __dmul_rn(double(s), double(s));
-    w_new = __double2float_rn(__ddiv_rn(1.0, dd < 1e-6 ? 1e-6 : dd));
-  }
+  if (d_p < -a.eps) return false;  // occluded: voxel unchanged (updates.hpp:42, :62)
   if (!is_new && !have_old) old = blk[lin];
   n_read += is_new ? 0u : 1u;
-  const float d_t = d_p < -a.eps ? -a.eps : (a.eps < d_p ? a.eps : d_p);
-  const float w_sum = __fadd_rn(old.y, w_new);
-  const float avg = __fdiv_rn(__fadd_rn(__fmul_rn(old.y, old.x), __fmul_rn(w_new, d_t)), w_sum);
-  float2 nv;
-  nv.x = avg < -a.eps ? -a.eps : (a.eps < avg ? a.eps : avg);
-  nv.y = a.max_weight < w_sum ? a.max_weight : w_sum;
-  if (__float_as_uint(nv.x) != __float_as_uint(old.x) || __float_as_uint(nv.y) != __float_as_uint(old.y)) {
+  V nv;
+  if (Ops::apply(a, old, d_p, s, nv)) {
     blk[lin] = nv;
     ++n_upd;
     return true;
@@ -180,7 +213,10 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, float2* blk, int 
 // there is no block-wide barrier.  The per-axis products R_SL(i, a) *
 // centre_a(v) are formed per lane (bit-identical to the reference's
 // R * centre rows, pose.hpp:58-60 with the pinned a0 + (a1 + a2) order).
+template <bool OCC>
 __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
+  using Ops = VoxOps<OCC>;
+  using V = typename Ops::V;
   const DevStatus* st = a.status_ro;
   if (st->pool_overflow || st->capacity_error || st->bitmap_overflow) return;
   const uint32_t n = st->n_candidates;
@@ -193,7 +229,7 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
     const int32_t sraw = a.cand_slots[ci];
     const bool is_new = sraw < 0;
     const int32_t slot = sraw & 0x7fffffff;
-    float2* blk = a.pool + size_t(slot) * kVPB;
+    V* blk = static_cast<V*>(a.pool) + size_t(slot) * kVPB;
     // voxel_center — indexing.hpp:113-119: ((g * 8 + v) + 0.5) * vs
     auto centre = [&](int32_t g, int v) {
       return __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(double(g), 8.0), double(v)), 0.5), a.vs);
@@ -223,7 +259,7 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
 #pragma unroll 1
       for (int j0 = 0; j0 < 16; j0 += 4) {
         float sd[4];
-        float2 ov[4];
+        V ov[4];
         float dv[4];
         uint32_t live = 0;
 #pragma unroll
@@ -232,7 +268,7 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
           centre_p(j0 + q, px, py, pz);
           const int lin = lane + 32 * (j0 + q);
           sd[q] = 0.0f;
-          ov[q] = make_float2(0.0f, 0.0f);
+          ov[q] = Ops::zero();
           dv[q] = __double2float_rn(pz);
           if (!(pz > 0.0) || pz > a.max_voxel_depth) continue;  // integrator.cpp:104-107
           int col, row;
@@ -246,28 +282,17 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
           }
           if (col < 0 || row < 0 || col >= a.W || row >= a.H) continue;
           sd[q] = __ldg(a.depth + size_t(row) * a.W + col);
-          if (!is_new) ov[q] = __ldcs(reinterpret_cast<const float2*>(blk) + lin);
+          if (!is_new) ov[q] = Ops::load_cs(blk + lin);
           live |= 1u << q;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (!((live >> q) & 1u) || !valid_depth_i(sd[q])) continue;
           const float d_p = __fsub_rn(sd[q], dv[q]);  // integrator.cpp:116
-          if (d_p < -a.eps) continue;                 // tsdf_update — updates.hpp:39-54
-          float w_new = 1.0f;
-          if (a.inv_sq) {
-            const double dd = __dmul_rn(double(sd[q]), double(sd[q]));
-            w_new = __double2float_rn(__ddiv_rn(1.0, dd < 1e-6 ? 1e-6 : dd));
-          }
+          if (d_p < -a.eps) continue;                 // occluded (updates.hpp:42, :62)
           n_read += is_new ? 0u : 1u;
-          const float2 o = ov[q];
-          const float d_t = d_p < -a.eps ? -a.eps : (a.eps < d_p ? a.eps : d_p);
-          const float w_sum = __fadd_rn(o.y, w_new);
-          const float avg = __fdiv_rn(__fadd_rn(__fmul_rn(o.y, o.x), __fmul_rn(w_new, d_t)), w_sum);
-          float2 nv;
-          nv.x = avg < -a.eps ? -a.eps : (a.eps < avg ? a.eps : avg);
-          nv.y = a.max_weight < w_sum ? a.max_weight : w_sum;
-          if (__float_as_uint(nv.x) != __float_as_uint(o.x) || __float_as_uint(nv.y) != __float_as_uint(o.y)) {
+          V nv;
+          if (Ops::apply(a, ov[q], d_p, sd[q], nv)) {
             blk[lane + 32 * (j0 + q)] = nv;
             ++n_upd;
             any = true;
@@ -279,7 +304,7 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
       for (int j = 0; j < 16; ++j) {
         double px, py, pz;
         centre_p(j, px, py, pz);
-        any |= integrate_voxel(a, blk, lane + 32 * j, px, py, pz, is_new, n_read, n_upd);
+        any |= integrate_voxel<OCC>(a, blk, lane + 32 * j, px, py, pz, is_new, n_read, n_upd);
       }
     }
     any = __any_sync(0xffffffffu, any);
@@ -345,12 +370,17 @@ void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
                          const DevStatus* guard, const char* prof_name) {
   const uint32_t tiles_cap = ceil_div(std::max<uint32_t>(n_cap, 1), 256 * kCompactItems);
   const ScanTiles st = ctx->next_scan(tiles_cap);
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_cap, ctx->sm_count));
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_cap, ctx->sm_count * 4));
   ctx->prof_begin(prof_name);
   k_compact_keys<<<grid, 256, 0, ctx->stream>>>(in, flags, n_ptr, out, n_out, st, guard);
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "k_compact_keys");
+}
+
+// quantize_log_odds — integrate/config.hpp:29-31 (host, as the reference)
+static float quantize_log_odds(float v) {
+  return static_cast<float>(std::nearbyint(double(v) * 4096.0) / 4096.0);
 }
 
 uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_config& cfg,
@@ -366,7 +396,7 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   a.cand_keys = ctx->cand_keys.as<uint64_t>();
   a.cand_slots = ctx->cand_slots.as<int32_t>();
   a.status_ro = ctx->d_status;
-  a.pool = static_cast<float2*>(L->pool[0]);
+  a.pool = L->pool[0];
   a.changed = ctx->cand_flags.as<uint8_t>();
   a.depth = va.depth_dev;
   a.W = va.width;
@@ -389,14 +419,23 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   a.max_gap = cfg.max_sample_gap;
   a.inv_sq = cfg.weighting == VXM_WEIGHT_INVERSE_SQUARE;
   a.linear = (va.lidar ? cfg.lidar_sample : cfg.camera_sample) == VXM_SAMPLE_LINEAR;
-  static int per_sm = 0;  // resident CTAs per SM: the persistent grid is one wave
-  if (!per_sm) {
-    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_integrate, 256, 0));
-    per_sm = std::max(per_sm, 1);
+  a.hit = quantize_log_odds(cfg.hit_log_odds);
+  a.miss = quantize_log_odds(cfg.miss_log_odds);
+  a.lo_min = quantize_log_odds(cfg.log_odds_min);
+  a.lo_max = quantize_log_odds(cfg.log_odds_max);
+  const bool occ = L->type == VXM_LAYER_OCCUPANCY;
+  static int per_sm[2] = {0, 0};  // resident CTAs per SM: the persistent grid is one wave
+  if (!per_sm[occ]) {
+    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm[occ], occ ? k_integrate<true> : k_integrate<false>, 256, 0));
+    per_sm[occ] = std::max(per_sm[occ], 1);
   }
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * per_sm));
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * per_sm[occ]));
   ctx->prof_begin("k_integrate");
-  k_integrate<<<grid, 256, 0, ctx->stream>>>(a);
+  if (occ)
+    k_integrate<true><<<grid, 256, 0, ctx->stream>>>(a);
+  else
+    k_integrate<false><<<grid, 256, 0, ctx->stream>>>(a);
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "k_integrate");

@@ -6,8 +6,10 @@ Names, argument meaning and error behaviour follow the reference:
 =====================================  ==============================================
 reference (proj/include/voxmap/...)    here
 =====================================  ==============================================
-Layer<TsdfVoxel>, Layer<EsdfVoxel>     TsdfLayer, EsdfLayer        core/layer.hpp:47-125
-integrate_depth (camera / lidar)       integrate_depth             integrate/integrator.hpp:36-45
+Layer<TsdfVoxel>, Layer<EsdfVoxel>,    TsdfLayer, EsdfLayer,       core/layer.hpp:47-125
+Layer<OccupancyVoxel>                  OccupancyLayer
+integrate_depth (camera / lidar;       integrate_depth             integrate/integrator.hpp:36-55
+TSDF or occupancy layer)
 blocks_in_view                         blocks_in_view              sensor/view.hpp:38-48
 update_esdf / mark_sites /             update_esdf / mark_sites /  esdf/integrator.hpp:81-120
 clear_invalid / lower_esdf             clear_invalid / lower_esdf
@@ -18,7 +20,9 @@ std::invalid_argument                  (a ValueError)
 =====================================  ==============================================
 
 Block lists are ``(N, 3) int32`` numpy arrays of GridIndex in lexicographic
-order; voxel blocks are numpy structured arrays (TSDF_DTYPE / ESDF_DTYPE).
+order; voxel blocks are numpy structured arrays (TSDF_DTYPE / ESDF_DTYPE /
+OCCUPANCY_DTYPE).  update_esdf / mark_sites take a TSDF or an occupancy source
+layer, as the reference's overloads do.
 There is no CPU fallback: without a B200 every compute call raises
 ``VoxmapCudaError``.
 """
@@ -35,7 +39,8 @@ from ._abi import (Camera as CameraIntrinsics, Lidar as LidarIntrinsics,  # noqa
                    default_camera as default_camera_intrinsics,
                    default_lidar as default_lidar_intrinsics,
                    default_integrator_config as IntegratorConfig,
-                   default_esdf_config as EsdfConfig, TSDF_DTYPE, ESDF_DTYPE, QUERY_DTYPE)
+                   default_esdf_config as EsdfConfig, TSDF_DTYPE, ESDF_DTYPE, QUERY_DTYPE,
+                   OCCUPANCY_DTYPE)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libvoxmap_b200.so")
 
@@ -337,6 +342,18 @@ class EsdfLayer(_Layer):
         return obj
 
 
+class OccupancyLayer(_Layer):
+    """Layer<OccupancyVoxel> (core/voxels.hpp:28-32): log-odds, 0 = unobserved."""
+    kind = A.LAYER_OCCUPANCY
+    dtype = A.OCCUPANCY_DTYPE
+
+    @classmethod
+    def _adopt(cls, h, ctx):
+        obj = cls.__new__(cls)
+        obj.ctx, obj.h = ctx, h
+        return obj
+
+
 def make_replay_config(voxel_size: float) -> A.ReplayConfigC:
     """make_replay_config (io/pipeline.cpp:46-52)."""
     c = A.ReplayConfigC()
@@ -346,7 +363,8 @@ def make_replay_config(voxel_size: float) -> A.ReplayConfigC:
 
 def replay(frames, intrinsics, cfg: A.ReplayConfigC, ctx: Context | None = None):
     """replay (io/pipeline.cpp:54-148) over in-memory frames [(T_WS, depth), ...]:
-    returns (tsdf, esdf, timings) with FrameTiming records (FRAME_TIMING_DTYPE)."""
+    returns (source, esdf, timings) with FrameTiming records (FRAME_TIMING_DTYPE);
+    source is the TsdfLayer, or the OccupancyLayer when cfg.use_occupancy."""
     ctx = ctx or default_context()
     n = len(frames)
     if n:
@@ -360,7 +378,8 @@ def replay(frames, intrinsics, cfg: A.ReplayConfigC, ctx: Context | None = None)
     fn = lib().vxm_replay_camera if isinstance(intrinsics, A.Camera) else lib().vxm_replay_lidar
     check(fn(ctx.h, C.byref(cfg), C.byref(intrinsics), C.c_int(n), C.c_int(w), C.c_int(h), A.ptr(depth),
              poses, C.byref(th), C.byref(eh), A.ptr(timings)))
-    return TsdfLayer._adopt(th, ctx), EsdfLayer._adopt(eh, ctx), timings[:n]
+    src = (OccupancyLayer if cfg.use_occupancy else TsdfLayer)._adopt(th, ctx)
+    return src, EsdfLayer._adopt(eh, ctx), timings[:n]
 
 
 def write_timing_csv(timings, path: str) -> None:
@@ -376,22 +395,27 @@ def write_timing_csv(timings, path: str) -> None:
 
 
 def save_snapshot(path: str, voxel_size: float, tsdf: TsdfLayer | None = None,
-                  esdf: EsdfLayer | None = None) -> None:
+                  esdf: EsdfLayer | None = None, occupancy: OccupancyLayer | None = None) -> None:
     """save_snapshot (core/serialization.hpp:31): VXLF v1, byte-identical to the
-    reference's for equal maps."""
-    check(lib().vxm_snapshot_save(os.fsencode(path), C.c_double(voxel_size),
-                                  tsdf.h if tsdf is not None else None,
-                                  esdf.h if esdf is not None else None))
+    reference's for equal maps (layers tsdf, occupancy, esdf)."""
+    h = lambda L: L.h if L is not None else None  # noqa: E731
+    check(lib().vxm_snapshot_save_layers(os.fsencode(path), C.c_double(voxel_size), h(tsdf),
+                                         h(occupancy), h(esdf)))
 
 
-def load_snapshot(path: str, ctx: Context | None = None):
-    """load_snapshot (core/serialization.hpp:35) -> (voxel_size, tsdf | None, esdf | None)."""
+def load_snapshot(path: str, ctx: Context | None = None, with_occupancy: bool = False):
+    """load_snapshot (core/serialization.hpp:35) -> (voxel_size, tsdf | None, esdf | None),
+    or (voxel_size, tsdf, occupancy, esdf) with_occupancy."""
     ctx = ctx or default_context()
     vs = C.c_double()
-    th, eh = C.c_void_p(), C.c_void_p()
-    check(lib().vxm_snapshot_load(ctx.h, os.fsencode(path), C.byref(vs), C.byref(th), C.byref(eh)))
-    return (vs.value, TsdfLayer._adopt(th, ctx) if th.value else None,
-            EsdfLayer._adopt(eh, ctx) if eh.value else None)
+    th, oh, eh = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    check(lib().vxm_snapshot_load_layers(ctx.h, os.fsencode(path), C.byref(vs), C.byref(th),
+                                         C.byref(oh) if with_occupancy else None, C.byref(eh)))
+    t = TsdfLayer._adopt(th, ctx) if th.value else None
+    e = EsdfLayer._adopt(eh, ctx) if eh.value else None
+    if with_occupancy:
+        return vs.value, t, (OccupancyLayer._adopt(oh, ctx) if oh.value else None), e
+    return vs.value, t, e
 
 
 def _depth(depth):
@@ -401,9 +425,10 @@ def _depth(depth):
     return d
 
 
-def integrate_depth(layer: TsdfLayer, depth, T_LS, intrinsics, cfg=None, out: BlockList | None = None):
-    """integrate_depth (integrate/integrator.hpp:36-45): fuses one frame and
-    returns the sorted indices of the blocks whose bytes changed."""
+def integrate_depth(layer, depth, T_LS, intrinsics, cfg=None, out: BlockList | None = None):
+    """integrate_depth (integrate/integrator.hpp:36-55): fuses one frame into a
+    TsdfLayer (tsdf_update) or an OccupancyLayer (occupancy_update) and returns
+    the sorted indices of the blocks whose bytes changed."""
     cfg = cfg or IntegratorConfig()
     d = _depth(depth)
     out = out or layer._result_list()
@@ -437,9 +462,10 @@ def blocks_in_view(T_LS, intrinsics, depth, block_size, cfg=None, ctx: Context |
     return out.numpy()
 
 
-def update_esdf(esdf: EsdfLayer, tsdf: TsdfLayer, updated, cfg=None, out: BlockList | None = None):
-    """update_esdf (esdf/integrator.hpp:113-116). `updated` may be a BlockList
-    (e.g. the device-resident output of integrate_depth) or an (N,3) array."""
+def update_esdf(esdf: EsdfLayer, tsdf, updated, cfg=None, out: BlockList | None = None):
+    """update_esdf (esdf/integrator.hpp:113-120) from a TsdfLayer or an
+    OccupancyLayer source. `updated` may be a BlockList (e.g. the
+    device-resident output of integrate_depth) or an (N,3) array."""
     cfg = cfg or EsdfConfig()
     out = out or esdf._result_list()
     if isinstance(updated, BlockList):

@@ -191,6 +191,45 @@ int main() {
     std::remove(path.c_str());
   }
 
+  // Occupancy overloads (integrator.cpp:176-189, esdf/integrator.cpp:574-579)
+  // and the cake's occupancy layer in a snapshot.
+  {
+    vb::Layer<vb::OccupancyVoxel> occ(0.05);
+    vb::Layer<vb::EsdfVoxel> oesdf2(0.05);
+    vxo_layer *oocc = nullptr, *oe2 = nullptr;
+    vxo_layer_create(VXM_LAYER_OCCUPANCY, 0.05, 0, &oocc);
+    vxo_layer_create(VXM_LAYER_ESDF, 0.05, 0, &oe2);
+    for (int k = 0; k < 3; ++k) {
+      vxm_pose p;
+      vxm_synth_orbit_pose(scene, 0, k, 8, &p);
+      vb::DepthImage depth(cam.width, cam.height);
+      vxm_synth_render_camera(scene, &p, &cam_c, depth.data.data());
+      const auto a = vb::integrate_depth(occ, depth, pose_of(p), cam, cfg);
+      vxm_grid_index* ob = nullptr;
+      uint64_t on = 0;
+      vxo_integrate_camera(oocc, depth.data.data(), depth.width, depth.height, &p, &cam_c, &cfg_c, &ob, &on);
+      const auto b = oracle_list(ob, on);
+      CHECK(!a.empty());
+      CHECK(a == b);
+      const auto ea = vb::update_esdf(oesdf2, occ, a, ecfg);
+      const auto bc = vb::to_c(b);
+      vxo_update_esdf(oe2, oocc, bc.data(), bc.size(), &ecfg_c, &ob, &on);
+      CHECK(ea == oracle_list(ob, on));
+    }
+    CHECK(same_layer(occ, oocc));
+    CHECK(same_layer(oesdf2, oe2));
+    const std::string path = "/tmp/vxm_facade_test_occ.vxlf";
+    vb::LayerCake cake(0.05);
+    cake.occupancy = std::make_unique<vb::Layer<vb::OccupancyVoxel>>(occ.clone());
+    vb::save_snapshot(cake, path);
+    vb::LayerCake back = vb::load_snapshot(path);
+    CHECK(!back.tsdf && back.occupancy && !back.esdf);
+    CHECK(back.occupancy && same_layer(*back.occupancy, oocc));
+    std::remove(path.c_str());
+    vxo_layer_destroy(oocc);
+    vxo_layer_destroy(oe2);
+  }
+
   vxo_layer_destroy(otsdf);
   vxo_layer_destroy(oesdf);
   vxm_synth_scene_destroy(scene);
