@@ -53,6 +53,12 @@ typedef struct { float distance, weight; } vxm_tsdf_voxel;
 /* OccupancyVoxel (core/voxels.hpp:28-32), 4 bytes: log-odds, 0 = unobserved prior. */
 typedef struct { float log_odds; } vxm_occupancy_voxel;
 
+/* ColorVoxel (core/voxels.hpp:34-41), 8 bytes. */
+typedef struct {
+  uint8_t r, g, b, reserved;
+  float weight;
+} vxm_color_voxel;
+
 /* EsdfVoxel (core/voxels.hpp:48-68), 12 bytes, same byte layout. */
 typedef struct {
   int32_t squared_distance;
@@ -65,7 +71,12 @@ enum { VXM_ESDF_OBSERVED = 1, VXM_ESDF_SITE = 2, VXM_ESDF_INSIDE = 4 };
 enum { VXM_VOXELS_PER_SIDE = 8, VXM_VOXELS_PER_BLOCK = 512 };
 
 /* Layer voxel type: Layer<TsdfVoxel>, Layer<EsdfVoxel>, Layer<OccupancyVoxel>. */
-typedef enum { VXM_LAYER_TSDF = 0, VXM_LAYER_ESDF = 1, VXM_LAYER_OCCUPANCY = 2 } vxm_layer_type;
+typedef enum {
+  VXM_LAYER_TSDF = 0,
+  VXM_LAYER_ESDF = 1,
+  VXM_LAYER_OCCUPANCY = 2,
+  VXM_LAYER_COLOR = 3
+} vxm_layer_type;
 
 /* CameraIntrinsics (sensor/camera.hpp:24-31). */
 typedef struct {
@@ -243,6 +254,65 @@ vxm_status vxm_integrate_depth_lidar_device(vxm_layer* layer, const float* depth
                                             const vxm_integrator_config* cfg,
                                             vxm_blocklist* changed_out);
 
+/* ---- color fusion (integrate/integrator.hpp:57-66, integrator.cpp:191-273) -- */
+/* integrate_color(Layer<ColorVoxel>&, ColorImage, DepthImage, Pose T_LS,
+ * CameraIntrinsics, const Layer<TsdfVoxel>&, IntegratorConfig): fuses an RGB
+ * image (host, row-major width x height x 3) into the voxels of the TSDF
+ * surface band (weight > 0, |distance| <= truncation); color blocks are
+ * allocated only where the TSDF block holds band voxels.  The depth image
+ * (host) selects the candidate blocks.  Errors as the reference (before any
+ * mutation): degenerate pose, color size != intrinsics, depth size mismatch. */
+vxm_status vxm_integrate_color(vxm_layer* color, const uint8_t* rgb, int width, int height,
+                               const float* depth, int depth_width, int depth_height,
+                               const vxm_pose* T_LS, const vxm_camera* cam, vxm_layer* tsdf,
+                               const vxm_integrator_config* cfg, vxm_blocklist* changed_out);
+
+/* ---- meshing (mesh/marching_cubes.hpp:24-78, mesh_layer.hpp, ply.hpp) ---- */
+/* MeshConfig (marching_cubes.hpp:24-33). */
+typedef struct {
+  float min_weight; /* corners with weight below this leave a cube inactive */
+  int32_t parallel; /* accepted, ignored */
+} vxm_mesh_config;
+void vxm_mesh_config_default(vxm_mesh_config* cfg);
+/* MeshLayer (mesh_layer.hpp:27-66): per-block meshes, host-resident (the
+ * device computes them).  A block view's arrays stay valid until the block is
+ * re-meshed or the layer destroyed. */
+typedef struct vxm_mesh_layer vxm_mesh_layer;
+typedef struct {
+  uint64_t n_vertices, n_triangles, n_colors; /* n_colors: 0 or n_vertices */
+  const float* vertices;     /* 3 per vertex, metres, layer frame */
+  const float* normals;      /* 3 per vertex, unit, along +gradient */
+  const uint8_t* colors;     /* 3 per vertex (when meshed with a color layer) */
+  const uint32_t* triangles; /* 3 block-local vertex indices per triangle */
+} vxm_mesh_block_view;
+vxm_status vxm_mesh_layer_create(vxm_context* ctx, double voxel_size, vxm_mesh_layer** out);
+void vxm_mesh_layer_destroy(vxm_mesh_layer* mesh);
+double vxm_mesh_layer_voxel_size(const vxm_mesh_layer* mesh);
+uint64_t vxm_mesh_layer_num_blocks(const vxm_mesh_layer* mesh);
+/* sorted_indices (mesh_layer.hpp:47-55) into keys_out[capacity]. */
+vxm_status vxm_mesh_layer_sorted_indices(const vxm_mesh_layer* mesh, vxm_grid_index* keys_out,
+                                         uint64_t capacity);
+/* block_ptr (mesh_layer.hpp:37-40): *found = 0 when absent. */
+vxm_status vxm_mesh_layer_block(const vxm_mesh_layer* mesh, const vxm_grid_index* g,
+                                vxm_mesh_block_view* out, int* found);
+vxm_status vxm_mesh_layer_erase(vxm_mesh_layer* mesh, const vxm_grid_index* g);
+/* mesh_block (marching_cubes.cpp:95-209), stored into mesh at g (as
+ * get_or_create(g) = mesh_block(...)).  VXM_ERR_INVALID_ARGUMENT when the TSDF
+ * block is not allocated.  color may be NULL (no vertex colors). */
+vxm_status vxm_mesh_block(vxm_mesh_layer* mesh, vxm_layer* tsdf, const vxm_grid_index* g,
+                          const vxm_mesh_config* cfg, vxm_layer* color);
+/* update_mesh (marching_cubes.cpp:211-242): re-meshes every allocated block of
+ * updated U its -x/-y/-z neighbours; remeshed_out gets those targets (sorted). */
+vxm_status vxm_update_mesh(vxm_mesh_layer* mesh, vxm_layer* tsdf, const vxm_grid_index* updated,
+                           uint64_t n, const vxm_mesh_config* cfg, vxm_layer* color,
+                           vxm_blocklist* remeshed_out);
+vxm_status vxm_update_mesh_list(vxm_mesh_layer* mesh, vxm_layer* tsdf, vxm_blocklist* updated,
+                                const vxm_mesh_config* cfg, vxm_layer* color,
+                                vxm_blocklist* remeshed_out);
+/* save_mesh_ply (ply.cpp:33-105): binary little-endian PLY, blocks in sorted
+ * order, byte-identical to the reference's.  VXM_ERR_IO when it cannot write. */
+vxm_status vxm_save_mesh_ply(const vxm_mesh_layer* mesh, const char* path);
+
 /* ---- replay (io/pipeline.hpp:27-72, pipeline.cpp:54-148) ------------------- */
 /* ReplayConfig (pipeline.hpp:27-36; color / mesh are out of scope). */
 typedef struct {
@@ -287,14 +357,15 @@ vxm_status vxm_snapshot_save(const char* path, double voxel_size, vxm_layer* tsd
  * implement (out of scope). */
 vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* voxel_size_out,
                              vxm_layer** tsdf_out, vxm_layer** esdf_out);
-/* The same over the LayerCake's tsdf / occupancy / esdf layers (layer_cake.hpp:
- * 29-33; written in the reference's order tsdf, occupancy, esdf).  The color
- * layer is not implemented (load fails with VXM_ERR_IO when a file holds one). */
+/* The same over the LayerCake's tsdf / occupancy / color / esdf layers
+ * (layer_cake.hpp:29-33; written in the reference's order tsdf, occupancy,
+ * color, esdf).  Any layer argument may be NULL; a NULL out pointer makes a
+ * file holding that layer fail with VXM_ERR_IO. */
 vxm_status vxm_snapshot_save_layers(const char* path, double voxel_size, vxm_layer* tsdf,
-                                    vxm_layer* occupancy, vxm_layer* esdf);
+                                    vxm_layer* occupancy, vxm_layer* color, vxm_layer* esdf);
 vxm_status vxm_snapshot_load_layers(vxm_context* ctx, const char* path, double* voxel_size_out,
                                     vxm_layer** tsdf_out, vxm_layer** occupancy_out,
-                                    vxm_layer** esdf_out);
+                                    vxm_layer** color_out, vxm_layer** esdf_out);
 
 /* ---- block-sharded ESDF ------------------------------------ */
 /* One update_esdf (esdf/integrator.cpp:365-413) over a map sharded by block x:

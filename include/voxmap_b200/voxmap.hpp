@@ -85,6 +85,10 @@ struct TsdfVoxel {
 struct OccupancyVoxel {  // core/voxels.hpp:28-32
   float log_odds = 0.0f;
 };
+struct ColorVoxel {  // core/voxels.hpp:34-41
+  uint8_t r = 0, g = 0, b = 0, reserved = 0;
+  float weight = 0.0f;
+};
 struct EsdfVoxel {
   static constexpr uint8_t kObserved = 1, kSite = 2, kInside = 4;
   int32_t squared_distance = 0;
@@ -97,7 +101,8 @@ struct EsdfVoxel {
   friend bool operator==(const EsdfVoxel&, const EsdfVoxel&) = default;
 };
 static_assert(sizeof(TsdfVoxel) == sizeof(vxm_tsdf_voxel) && sizeof(EsdfVoxel) == sizeof(vxm_esdf_voxel) &&
-              sizeof(OccupancyVoxel) == sizeof(vxm_occupancy_voxel));
+              sizeof(OccupancyVoxel) == sizeof(vxm_occupancy_voxel) &&
+              sizeof(ColorVoxel) == sizeof(vxm_color_voxel));
 
 template <typename V>
 struct VoxelBlock {
@@ -117,6 +122,10 @@ struct LayerTraits<EsdfVoxel> {
 template <>
 struct LayerTraits<OccupancyVoxel> {
   static constexpr vxm_layer_type type = VXM_LAYER_OCCUPANCY;
+};
+template <>
+struct LayerTraits<ColorVoxel> {
+  static constexpr vxm_layer_type type = VXM_LAYER_COLOR;
 };
 
 struct GridHash {
@@ -589,14 +598,127 @@ inline std::vector<QueryResult> query_batch(const Layer<EsdfVoxel>& esdf,
   return out;
 }
 
+// ---- color fusion (integrate/integrator.hpp:57-66) ----------------------------------
+struct ColorImage {  // sensor/image.hpp:41-55
+  int width = 0, height = 0;
+  std::vector<std::array<uint8_t, 3>> data;
+  ColorImage() = default;
+  ColorImage(int w, int h) : width(w), height(h), data(size_t(w) * h) {}
+  std::array<uint8_t, 3>& at(int col, int row) { return data[size_t(row) * width + col]; }
+  const std::array<uint8_t, 3>& at(int col, int row) const { return data[size_t(row) * width + col]; }
+};
+inline std::vector<GridIndex> integrate_color(Layer<ColorVoxel>& color_layer, const ColorImage& color,
+                                              const DepthImage& depth, const Pose& T_LS,
+                                              const CameraIntrinsics& camera,
+                                              const Layer<TsdfVoxel>& tsdf_layer,
+                                              const IntegratorConfig& cfg) {
+  const vxm_pose p = T_LS.c();
+  const vxm_camera cam = camera.c();
+  const vxm_integrator_config k = cfg.c();
+  BlockList out(color_layer.context());
+  check(vxm_integrate_color(color_layer.device(), color.data.empty() ? nullptr : color.data[0].data(),
+                            color.width, color.height, depth.data.data(), depth.width, depth.height,
+                            &p, &cam, tsdf_layer.device(), &k, out.handle()));
+  return out.to_vector();
+}
+
+// ---- meshing (mesh/marching_cubes.hpp, mesh_layer.hpp, ply.hpp) ---------------------
+struct MeshConfig {  // marching_cubes.hpp:24-33
+  float min_weight = 1e-4f;
+  bool parallel = true;
+  vxm_mesh_config c() const { return {min_weight, parallel ? 1 : 0}; }
+};
+struct MeshBlock {  // mesh_layer.hpp:16-25
+  std::vector<std::array<float, 3>> vertices, normals;
+  std::vector<std::array<uint8_t, 3>> colors;
+  std::vector<std::array<uint32_t, 3>> triangles;
+  bool empty() const { return triangles.empty(); }
+};
+// MeshLayer (mesh_layer.hpp:27-66) over the library's mesh layer; block_ptr
+// copies the block out (stable until the next call on the same block).
+class MeshLayer {
+ public:
+  explicit MeshLayer(double voxel_size, Context& ctx = default_context()) : ctx_(&ctx) {
+    check(vxm_mesh_layer_create(ctx.handle(), voxel_size, &h_));
+  }
+  ~MeshLayer() { vxm_mesh_layer_destroy(h_); }
+  MeshLayer(const MeshLayer&) = delete;
+  MeshLayer& operator=(const MeshLayer&) = delete;
+  double voxel_size() const { return vxm_mesh_layer_voxel_size(h_); }
+  size_t num_blocks() const { return size_t(vxm_mesh_layer_num_blocks(h_)); }
+  std::vector<GridIndex> sorted_indices() const {
+    std::vector<vxm_grid_index> k(num_blocks());
+    check(vxm_mesh_layer_sorted_indices(h_, k.data(), k.size()));
+    return from_c(k.data(), k.size());
+  }
+  const MeshBlock* block_ptr(const GridIndex& g) const {
+    const vxm_grid_index k{g.x, g.y, g.z};
+    vxm_mesh_block_view v{};
+    int found = 0;
+    check(vxm_mesh_layer_block(h_, &k, &v, &found));
+    if (!found) return nullptr;
+    MeshBlock& b = cache_[g];
+    b.vertices.resize(v.n_vertices);
+    b.normals.resize(v.n_vertices);
+    b.colors.resize(v.n_colors);
+    b.triangles.resize(v.n_triangles);
+    if (v.n_vertices) {
+      std::memcpy(b.vertices.data(), v.vertices, 12 * v.n_vertices);
+      std::memcpy(b.normals.data(), v.normals, 12 * v.n_vertices);
+    }
+    if (v.n_colors) std::memcpy(b.colors.data(), v.colors, 3 * v.n_colors);
+    if (v.n_triangles) std::memcpy(b.triangles.data(), v.triangles, 12 * v.n_triangles);
+    return &b;
+  }
+  void erase(const GridIndex& g) {
+    const vxm_grid_index k{g.x, g.y, g.z};
+    check(vxm_mesh_layer_erase(h_, &k));
+    cache_.erase(g);
+  }
+  vxm_mesh_layer* handle() const { return h_; }
+  Context& context() const { return *ctx_; }
+
+ private:
+  vxm_mesh_layer* h_ = nullptr;
+  Context* ctx_;
+  mutable std::unordered_map<GridIndex, MeshBlock, GridHash> cache_;
+};
+inline MeshBlock mesh_block(const Layer<TsdfVoxel>& tsdf, const GridIndex& g, const MeshConfig& cfg = {},
+                            const Layer<ColorVoxel>* color = nullptr) {
+  MeshLayer tmp(tsdf.voxel_size(), tsdf.context());
+  const vxm_grid_index k{g.x, g.y, g.z};
+  const vxm_mesh_config c = cfg.c();
+  check(vxm_mesh_block(tmp.handle(), tsdf.device(), &k, &c, color ? color->device() : nullptr));
+  return *tmp.block_ptr(g);
+}
+inline std::vector<GridIndex> update_mesh(MeshLayer& mesh, const Layer<TsdfVoxel>& tsdf,
+                                          const std::vector<GridIndex>& updated_blocks,
+                                          const MeshConfig& cfg = {},
+                                          const Layer<ColorVoxel>* color = nullptr) {
+  const auto u = to_c(updated_blocks);
+  const vxm_mesh_config c = cfg.c();
+  BlockList out(mesh.context());
+  check(vxm_update_mesh(mesh.handle(), tsdf.device(), u.data(), u.size(), &c,
+                        color ? color->device() : nullptr, out.handle()));
+  return out.to_vector();
+}
+inline void save_mesh_ply(const MeshLayer& mesh, const std::string& path) {
+  check(vxm_save_mesh_ply(mesh.handle(), path.c_str()));
+}
+
 // ---- snapshots (core/layer_cake.hpp:27-57, core/serialization.hpp:29-35) --------
-// The layers of a LayerCake this library implements (TSDF, occupancy, ESDF).
+// The LayerCake's voxel layers (TSDF, occupancy, color, ESDF).
 struct LayerCake {
   explicit LayerCake(double vs) : voxel_size(vs) {}
   double voxel_size;
   std::unique_ptr<Layer<TsdfVoxel>> tsdf;
   std::unique_ptr<Layer<OccupancyVoxel>> occupancy;
+  std::unique_ptr<Layer<ColorVoxel>> color;
   std::unique_ptr<Layer<EsdfVoxel>> esdf;
+  Layer<ColorVoxel>& require_color() {
+    if (!color) color = std::make_unique<Layer<ColorVoxel>>(voxel_size);
+    return *color;
+  }
   Layer<TsdfVoxel>& require_tsdf() {
     if (!tsdf) tsdf = std::make_unique<Layer<TsdfVoxel>>(voxel_size);
     return *tsdf;
@@ -615,16 +737,18 @@ inline void save_snapshot(const LayerCake& cake, const std::string& path) {
   check(vxm_snapshot_save_layers(path.c_str(), cake.voxel_size,
                                  cake.tsdf ? cake.tsdf->c_handle() : nullptr,
                                  cake.occupancy ? cake.occupancy->c_handle() : nullptr,
+                                 cake.color ? cake.color->c_handle() : nullptr,
                                  cake.esdf ? cake.esdf->c_handle() : nullptr));
 }
 
 inline LayerCake load_snapshot(const std::string& path, Context& ctx = default_context()) {
   double vs = 0.0;
-  vxm_layer *t = nullptr, *o = nullptr, *e = nullptr;
-  check(vxm_snapshot_load_layers(ctx.handle(), path.c_str(), &vs, &t, &o, &e));
+  vxm_layer *t = nullptr, *o = nullptr, *cl = nullptr, *e = nullptr;
+  check(vxm_snapshot_load_layers(ctx.handle(), path.c_str(), &vs, &t, &o, &cl, &e));
   LayerCake cake(vs);
   if (t) cake.tsdf = std::make_unique<Layer<TsdfVoxel>>(t, vs, ctx);
   if (o) cake.occupancy = std::make_unique<Layer<OccupancyVoxel>>(o, vs, ctx);
+  if (cl) cake.color = std::make_unique<Layer<ColorVoxel>>(cl, vs, ctx);
   if (e) cake.esdf = std::make_unique<Layer<EsdfVoxel>>(e, vs, ctx);
   return cake;
 }

@@ -132,6 +132,44 @@ class OracleLayer:
         return self.owner.export(self)
 
 
+class OracleMesh:
+    """voxmap_ref::MeshLayer handle; block(g) -> (vertices, normals, colors, triangles)."""
+
+    def __init__(self, owner, vs):
+        self.owner = owner
+        owner.lib.vxr_mesh_create.restype = C.c_void_p
+        owner.lib.vxr_mesh_num_blocks.restype = C.c_uint64
+        self.h = C.c_void_p(owner.lib.vxr_mesh_create(C.c_double(vs)))
+
+    def __del__(self):
+        try:
+            self.owner.lib.vxr_mesh_destroy(self.h)
+        except Exception:
+            pass
+
+    def sorted_indices(self):
+        n = int(self.owner.lib.vxr_mesh_num_blocks(self.h))
+        keys = np.zeros((n, 3), np.int32)
+        self.owner.lib.vxr_mesh_keys(self.h, A.ptr(keys))
+        return keys
+
+    def block(self, g):
+        k = A.as_keys([g])
+        nv, nt, nc = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        pv, pn, pt = C.POINTER(C.c_float)(), C.POINTER(C.c_float)(), C.POINTER(C.c_uint32)()
+        pc = C.POINTER(C.c_uint8)()
+        self.owner._check(self.owner.lib.vxr_mesh_block_get(
+            self.h, A.ptr(k), C.byref(nv), C.byref(nt), C.byref(pv), C.byref(pn), C.byref(pc),
+            C.byref(nc), C.byref(pt)))
+
+        def arr(p, n, dt):
+            if n == 0:
+                return np.zeros((0, 3), dt)
+            return np.ctypeslib.as_array(p, shape=(3 * n,)).reshape(n, 3).astype(dt, copy=True)
+        return (arr(pv, nv.value, np.float32), arr(pn, nv.value, np.float32),
+                arr(pc, nc.value, np.uint8), arr(pt, nt.value, np.uint32))
+
+
 class OracleState:
     def __init__(self, owner):
         self.owner = owner
@@ -213,20 +251,61 @@ class RefOracle(_Base):
                                              C.c_int(int(serial)), A.ptr(out)))
         return out
 
-    def save_snapshot(self, path, voxel_size, tsdf=None, esdf=None, occupancy=None):
+    def save_snapshot(self, path, voxel_size, tsdf=None, esdf=None, occupancy=None, color=None):
         h = lambda L: L.h if L is not None else None  # noqa: E731
         self._check(self.lib.vxr_snapshot_save(os.fsencode(path), C.c_double(voxel_size),
-                                               h(tsdf), h(occupancy), h(esdf)))
+                                               h(tsdf), h(occupancy), h(color), h(esdf)))
 
-    def load_snapshot(self, path, with_occupancy=False):
-        """(vs, tsdf, esdf) or, with_occupancy, (vs, tsdf, occupancy, esdf)."""
+    def load_snapshot(self, path, with_occupancy=False, with_color=False):
+        """(vs, tsdf, [occupancy,] [color,] esdf)."""
         vs = C.c_double()
-        th, oh, eh = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        th, oh, ch, eh = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         self._check(self.lib.vxr_snapshot_load(os.fsencode(path), C.byref(vs), C.byref(th),
-                                               C.byref(oh), C.byref(eh)))
+                                               C.byref(oh), C.byref(ch), C.byref(eh)))
         mk = lambda h, kind: OracleLayer(self, h, kind, vs.value) if h.value else None  # noqa: E731
-        t, o, e = mk(th, A.LAYER_TSDF), mk(oh, A.LAYER_OCCUPANCY), mk(eh, A.LAYER_ESDF)
-        return (vs.value, t, o, e) if with_occupancy else (vs.value, t, e)
+        out = [vs.value, mk(th, A.LAYER_TSDF)]
+        if with_occupancy:
+            out.append(mk(oh, A.LAYER_OCCUPANCY))
+        if with_color:
+            out.append(mk(ch, A.LAYER_COLOR))
+        out.append(mk(eh, A.LAYER_ESDF))
+        return tuple(out)
+
+    # --- color + meshing (integrator.cpp:191-273, marching_cubes.cpp, ply.cpp) ---
+    def integrate_color(self, color, rgb, depth, T, cam, tsdf, cfg):
+        c = np.ascontiguousarray(rgb, np.uint8)
+        d = np.ascontiguousarray(depth, np.float32)
+        return self._list(self.lib.vxr_integrate_color, color.h, A.ptr(c), C.c_int(c.shape[1]),
+                          C.c_int(c.shape[0]), A.ptr(d), C.byref(T), C.byref(cam), tsdf.h,
+                          C.byref(cfg))
+
+    def render_color(self, scene, T, cam):
+        out = np.zeros((cam.height, cam.width, 3), np.uint8)
+        self._check(self.lib.vxr_render_color_camera(scene.encode(), C.byref(T), C.byref(cam),
+                                                     A.ptr(out)))
+        return out
+
+    def mc_tri_table(self):
+        self.lib.vxr_mc_tri_table.restype = C.POINTER(C.c_int8)
+        p = self.lib.vxr_mc_tri_table()
+        return np.array([p[i] for i in range(256 * 16)], np.int8).reshape(256, 16)
+
+    def mesh_layer(self, voxel_size):
+        return OracleMesh(self, voxel_size)
+
+    def update_mesh(self, mesh, tsdf, updated, min_weight=1e-4, color=None):
+        u = A.as_keys(updated)
+        return self._list(self.lib.vxr_update_mesh, mesh.h, tsdf.h, A.ptr(u), C.c_uint64(len(u)),
+                          C.c_float(min_weight), color.h if color is not None else None)
+
+    def mesh_block(self, mesh, tsdf, g, min_weight=1e-4, color=None):
+        k = A.as_keys([g])
+        self._check(self.lib.vxr_mesh_block(mesh.h, tsdf.h, A.ptr(k), C.c_float(min_weight),
+                                            color.h if color is not None else None))
+        return mesh.block(g)
+
+    def save_mesh_ply(self, mesh, path):
+        self._check(self.lib.vxr_save_mesh_ply(mesh.h, os.fsencode(path)))
 
     def orbit_pose(self, scene, k, total, lidar=False):
         p = A.PoseC()

@@ -33,6 +33,9 @@
 #include "voxmap/io/dataset.hpp"
 #include "voxmap/io/render.hpp"
 #include "voxmap/io/scene.hpp"
+#include "voxmap/mesh/marching_cubes.hpp"
+#include "voxmap/mesh/mesh_layer.hpp"
+#include "voxmap/mesh/ply.hpp"
 #include "voxmap/query/query.hpp"
 #include "voxmap/reference/reference.hpp"
 #include "voxmap/sensor/view.hpp"
@@ -49,10 +52,12 @@ struct RefLayer {
   vr::Layer<vr::TsdfVoxel>* tsdf = nullptr;
   vr::Layer<vr::EsdfVoxel>* esdf = nullptr;
   vr::Layer<vr::OccupancyVoxel>* occ = nullptr;
+  vr::Layer<vr::ColorVoxel>* color = nullptr;
   ~RefLayer() {
     delete tsdf;
     delete esdf;
     delete occ;
+    delete color;
   }
 };
 
@@ -177,6 +182,7 @@ int vxr_layer_create(int type, double vs, uint64_t max_blocks, void** out) {
     try {
       if (type == VXM_LAYER_TSDF) L->tsdf = new vr::Layer<vr::TsdfVoxel>(vs, mb);
       else if (type == VXM_LAYER_OCCUPANCY) L->occ = new vr::Layer<vr::OccupancyVoxel>(vs, mb);
+      else if (type == VXM_LAYER_COLOR) L->color = new vr::Layer<vr::ColorVoxel>(vs, mb);
       else L->esdf = new vr::Layer<vr::EsdfVoxel>(vs, mb);
     } catch (...) {
       delete L;
@@ -188,13 +194,17 @@ int vxr_layer_create(int type, double vs, uint64_t max_blocks, void** out) {
 void vxr_layer_destroy(void* h) { delete static_cast<RefLayer*>(h); }
 uint64_t vxr_layer_num_blocks(void* h) {
   auto* L = static_cast<RefLayer*>(h);
-  return L->tsdf ? L->tsdf->num_blocks() : L->occ ? L->occ->num_blocks() : L->esdf->num_blocks();
+  return L->tsdf    ? L->tsdf->num_blocks()
+         : L->occ   ? L->occ->num_blocks()
+         : L->color ? L->color->num_blocks()
+                    : L->esdf->num_blocks();
 }
 int vxr_layer_export(void* h, vxm_grid_index* keys, void* voxels) {
   return guard([&] {
     auto* L = static_cast<RefLayer*>(h);
     if (L->tsdf) export_layer(*L->tsdf, keys, voxels);
     else if (L->occ) export_layer(*L->occ, keys, voxels);
+    else if (L->color) export_layer(*L->color, keys, voxels);
     else export_layer(*L->esdf, keys, voxels);
   });
 }
@@ -209,6 +219,9 @@ int vxr_layer_write_blocks(void* h, const vxm_grid_index* keys, uint64_t n, cons
       else if (L->occ)
         std::memcpy(L->occ->get_or_allocate(g).voxels.data(),
                     static_cast<const char*>(voxels) + i * 2048, 2048);
+      else if (L->color)
+        std::memcpy(L->color->get_or_allocate(g).voxels.data(),
+                    static_cast<const char*>(voxels) + i * 4096, 4096);
       else
         std::memcpy(L->esdf->get_or_allocate(g).voxels.data(),
                     static_cast<const char*>(voxels) + i * 6144, 6144);
@@ -415,15 +428,17 @@ int vxr_compare_esdf(void* a, void* b, uint64_t* stats4, double* max_abs) {
 
 // save_snapshot / load_snapshot (core/serialization.cpp:88-158) on a cake
 // that borrows the driver's layers.
-int vxr_snapshot_save(const char* path, double vs, void* tsdf, void* occ, void* esdf) {
+int vxr_snapshot_save(const char* path, double vs, void* tsdf, void* occ, void* color, void* esdf) {
   return guard([&] {
     vr::LayerCake cake(vs);
     if (tsdf) cake.tsdf.reset(static_cast<RefLayer*>(tsdf)->tsdf);
     if (occ) cake.occupancy.reset(static_cast<RefLayer*>(occ)->occ);
+    if (color) cake.color.reset(static_cast<RefLayer*>(color)->color);
     if (esdf) cake.esdf.reset(static_cast<RefLayer*>(esdf)->esdf);
     const auto release = [&] {
       cake.tsdf.release();
       cake.occupancy.release();
+      cake.color.release();
       cake.esdf.release();
     };
     try {
@@ -435,11 +450,17 @@ int vxr_snapshot_save(const char* path, double vs, void* tsdf, void* occ, void* 
     release();
   });
 }
-int vxr_snapshot_load(const char* path, double* vs, void** tsdf, void** occ, void** esdf) {
+int vxr_snapshot_load(const char* path, double* vs, void** tsdf, void** occ, void** color,
+                      void** esdf) {
   return guard([&] {
     vr::LayerCake cake = vr::load_snapshot(path);
     *vs = cake.voxel_size;
-    *tsdf = *occ = *esdf = nullptr;
+    *tsdf = *occ = *color = *esdf = nullptr;
+    if (cake.color) {
+      auto* L = new RefLayer{VXM_LAYER_COLOR};
+      L->color = cake.color.release();
+      *color = L;
+    }
     if (cake.tsdf) *tsdf = new RefLayer{VXM_LAYER_TSDF, cake.tsdf.release(), nullptr};
     if (cake.occupancy) {
       auto* L = new RefLayer{VXM_LAYER_OCCUPANCY};
@@ -448,6 +469,79 @@ int vxr_snapshot_load(const char* path, double* vs, void** tsdf, void** occ, voi
     }
     if (cake.esdf) *esdf = new RefLayer{VXM_LAYER_ESDF, nullptr, cake.esdf.release()};
   });
+}
+
+// ---- color + meshing (integrator.cpp:191-273, marching_cubes.cpp:95-242, ply.cpp) ----
+vr::ColorImage to_color(const uint8_t* rgb, int w, int h) {
+  vr::ColorImage img(w, h);
+  std::memcpy(img.data.data(), rgb, size_t(w) * h * 3);
+  return img;
+}
+int vxr_integrate_color(void* color, const uint8_t* rgb, int w, int h, const float* depth,
+                        const vxm_pose* T, const vxm_camera* cam, void* tsdf,
+                        const vxm_integrator_config* c, vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    emit(vr::integrate_color(*static_cast<RefLayer*>(color)->color, to_color(rgb, w, h),
+                             to_depth(depth, w, h), to_pose(T), to_cam(cam),
+                             *static_cast<RefLayer*>(tsdf)->tsdf, to_icfg(c)),
+         out, n);
+  });
+}
+int vxr_render_color_camera(const char* scene, const vxm_pose* T, const vxm_camera* cam, uint8_t* out) {
+  return guard([&] {
+    const auto img = vr::render_color(vr::make_scene(scene), to_pose(T), to_cam(cam));
+    std::memcpy(out, img.data.data(), img.data.size() * 3);
+  });
+}
+const int8_t* vxr_mc_tri_table() { return &vr::mc::kTriTable[0][0]; }
+
+void* vxr_mesh_create(double vs) { return new vr::MeshLayer(vs); }
+void vxr_mesh_destroy(void* m) { delete static_cast<vr::MeshLayer*>(m); }
+uint64_t vxr_mesh_num_blocks(void* m) { return static_cast<vr::MeshLayer*>(m)->num_blocks(); }
+void vxr_mesh_keys(void* m, vxm_grid_index* keys) {
+  const auto idx = static_cast<vr::MeshLayer*>(m)->sorted_indices();
+  for (size_t i = 0; i < idx.size(); ++i) keys[i] = {idx[i].x, idx[i].y, idx[i].z};
+}
+// Pointers into the MeshBlock's arrays (valid until the block is re-meshed).
+int vxr_mesh_block_get(void* m, const vxm_grid_index* g, uint64_t* nv, uint64_t* nt,
+                       const float** verts, const float** normals, const uint8_t** colors,
+                       uint64_t* ncolors, const uint32_t** tris) {
+  return guard([&] {
+    const vr::MeshBlock* b = static_cast<vr::MeshLayer*>(m)->block_ptr({g->x, g->y, g->z});
+    if (!b) throw std::invalid_argument("mesh block not present");
+    static_assert(sizeof(Eigen::Vector3f) == 12 && sizeof(std::array<uint32_t, 3>) == 12);
+    *nv = b->vertices.size();
+    *nt = b->triangles.size();
+    *ncolors = b->colors.size();
+    *verts = b->vertices.empty() ? nullptr : b->vertices[0].data();
+    *normals = b->normals.empty() ? nullptr : b->normals[0].data();
+    *colors = b->colors.empty() ? nullptr : b->colors[0].data();
+    *tris = b->triangles.empty() ? nullptr : b->triangles[0].data();
+  });
+}
+int vxr_update_mesh(void* m, void* tsdf, const vxm_grid_index* upd, uint64_t nu, float min_weight,
+                    void* color, vxm_grid_index** out, uint64_t* n) {
+  return guard([&] {
+    vr::MeshConfig cfg;
+    cfg.min_weight = min_weight;
+    emit(vr::update_mesh(*static_cast<vr::MeshLayer*>(m), *static_cast<RefLayer*>(tsdf)->tsdf,
+                         to_list(upd, nu), cfg,
+                         color ? static_cast<RefLayer*>(color)->color : nullptr),
+         out, n);
+  });
+}
+int vxr_mesh_block(void* m, void* tsdf, const vxm_grid_index* g, float min_weight, void* color) {
+  return guard([&] {
+    vr::MeshConfig cfg;
+    cfg.min_weight = min_weight;
+    const vr::GridIndex k{g->x, g->y, g->z};
+    static_cast<vr::MeshLayer*>(m)->get_or_create(k) = vr::mesh_block(
+        *static_cast<RefLayer*>(tsdf)->tsdf, k, cfg,
+        color ? static_cast<RefLayer*>(color)->color : nullptr);
+  });
+}
+int vxr_save_mesh_ply(void* m, const char* path) {
+  return guard([&] { vr::save_mesh_ply(*static_cast<vr::MeshLayer*>(m), path); });
 }
 
 }  // extern "C"

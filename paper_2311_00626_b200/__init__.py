@@ -12,4 +12,6 @@ from .voxmap import (BlockList, CameraIntrinsics, Context, EsdfConfig, EsdfLayer
                      integrate_depth_device, lib, lower_esdf, mark_sites, query_batch,
                      update_esdf, update_esdf_device, update_frame_device,
                      IoError, save_snapshot, load_snapshot, update_esdf_sharded,
-                     make_replay_config, replay, write_timing_csv, OccupancyLayer)
+                     make_replay_config, replay, write_timing_csv, OccupancyLayer,
+                     ColorLayer, MeshLayer, MeshBlock, integrate_color, mesh_block, update_mesh,
+                     save_mesh_ply)

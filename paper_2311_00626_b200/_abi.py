@@ -21,6 +21,7 @@ VXM_ERR_IO = 6
 LAYER_TSDF = 0
 LAYER_ESDF = 1
 LAYER_OCCUPANCY = 2
+LAYER_COLOR = 3
 
 WEIGHT_CONSTANT = 0
 WEIGHT_INVERSE_SQUARE = 1
@@ -39,11 +40,14 @@ TSDF_DTYPE = np.dtype([("distance", "<f4"), ("weight", "<f4")])
 ESDF_DTYPE = np.dtype([("squared_distance", "<i4"), ("parent_x", "<i2"), ("parent_y", "<i2"),
                        ("parent_z", "<i2"), ("flags", "u1"), ("reserved", "u1")])
 OCCUPANCY_DTYPE = np.dtype([("log_odds", "<f4")])
+COLOR_DTYPE = np.dtype([("r", "u1"), ("g", "u1"), ("b", "u1"), ("reserved", "u1"), ("weight", "<f4")])
 assert TSDF_DTYPE.itemsize == 8 and ESDF_DTYPE.itemsize == 12 and OCCUPANCY_DTYPE.itemsize == 4
+assert COLOR_DTYPE.itemsize == 8
 
 
 def layer_dtype(kind):
-    return {LAYER_TSDF: TSDF_DTYPE, LAYER_ESDF: ESDF_DTYPE, LAYER_OCCUPANCY: OCCUPANCY_DTYPE}[kind]
+    return {LAYER_TSDF: TSDF_DTYPE, LAYER_ESDF: ESDF_DTYPE, LAYER_OCCUPANCY: OCCUPANCY_DTYPE,
+            LAYER_COLOR: COLOR_DTYPE}[kind]
 
 
 class GridIndex(C.Structure):
@@ -94,6 +98,24 @@ class ReplayConfigC(C.Structure):
 
 FRAME_TIMING_DTYPE = np.dtype([("frame", "<i4"), ("pad_", "<i4"), ("tsdf_ms", "<f8"),
                                ("color_ms", "<f8"), ("esdf_ms", "<f8"), ("mesh_ms", "<f8")])
+
+
+class MeshConfigC(C.Structure):
+    """vxm_mesh_config — MeshConfig (mesh/marching_cubes.hpp:24-33)."""
+    _fields_ = [("min_weight", C.c_float), ("parallel", C.c_int32)]
+
+
+def default_mesh_config(**kw):
+    c = MeshConfigC(1e-4, 1)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+class MeshBlockViewC(C.Structure):
+    _fields_ = [("n_vertices", C.c_uint64), ("n_triangles", C.c_uint64), ("n_colors", C.c_uint64),
+                ("vertices", C.POINTER(C.c_float)), ("normals", C.POINTER(C.c_float)),
+                ("colors", C.POINTER(C.c_uint8)), ("triangles", C.POINTER(C.c_uint32))]
 
 
 class QueryConfigC(C.Structure):

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "runtime.cuh"
+#include "mesh.cuh"
 #include "shard.cuh"
 
 using namespace vxm;
@@ -408,7 +409,8 @@ vxm_status vxm_layer_create(vxm_context* ctx, vxm_layer_type type, double vs, ui
   return guard([&] {
     REQUIRE_ARG(ctx && out, "null argument");
     if (!(vs > 0.0)) throw Error(VXM_ERR_INVALID_ARGUMENT, "Layer: voxel_size must be positive");
-    REQUIRE_ARG(type == VXM_LAYER_TSDF || type == VXM_LAYER_ESDF || type == VXM_LAYER_OCCUPANCY,
+    REQUIRE_ARG(type == VXM_LAYER_TSDF || type == VXM_LAYER_ESDF || type == VXM_LAYER_OCCUPANCY ||
+                    type == VXM_LAYER_COLOR,
                 "unknown layer type");
     auto* L = new vxm_layer();
     L->ctx = ctx;
@@ -984,14 +986,16 @@ void read_layer(FILE* f, vxm_layer* L) {
 
 extern "C" {
 vxm_status vxm_snapshot_save_layers(const char* path, double vs, vxm_layer* tsdf, vxm_layer* occ,
-                                    vxm_layer* esdf) {
+                                    vxm_layer* color, vxm_layer* esdf) {
   return guard([&] {
     REQUIRE_ARG(path, "null argument");
     REQUIRE_ARG(!tsdf || tsdf->type == VXM_LAYER_TSDF, "snapshot: tsdf argument is not a TSDF layer");
     REQUIRE_ARG(!occ || occ->type == VXM_LAYER_OCCUPANCY,
                 "snapshot: occupancy argument is not an occupancy layer");
+    REQUIRE_ARG(!color || color->type == VXM_LAYER_COLOR, "snapshot: color argument is not a color layer");
     REQUIRE_ARG(!esdf || esdf->type == VXM_LAYER_ESDF, "snapshot: esdf argument is not an ESDF layer");
-    REQUIRE_ARG((!tsdf || tsdf->vs == vs) && (!occ || occ->vs == vs) && (!esdf || esdf->vs == vs),
+    REQUIRE_ARG((!tsdf || tsdf->vs == vs) && (!occ || occ->vs == vs) && (!color || color->vs == vs) &&
+                    (!esdf || esdf->vs == vs),
                 "snapshot: layer voxel size differs from the snapshot's");
     File out;
     out.f = std::fopen(path, "wb");
@@ -999,22 +1003,25 @@ vxm_status vxm_snapshot_save_layers(const char* path, double vs, vxm_layer* tsdf
     if (std::fwrite(kVxlfMagic, 1, 4, out.f) != 4) io_fail("snapshot: write failed");
     put(out.f, kVxlfVersion);
     put(out.f, vs);  // f64
-    const uint32_t count = (tsdf ? 1u : 0u) + (occ ? 1u : 0u) + (esdf ? 1u : 0u);
+    const uint32_t count = (tsdf ? 1u : 0u) + (occ ? 1u : 0u) + (color ? 1u : 0u) + (esdf ? 1u : 0u);
     put(out.f, count);
     if (tsdf) write_layer(out.f, "tsdf", tsdf);  // serialization.cpp:102-105 order
     if (occ) write_layer(out.f, "occupancy", occ);
+    if (color) write_layer(out.f, "color", color);
     if (esdf) write_layer(out.f, "esdf", esdf);
     if (std::fflush(out.f) != 0) io_fail(std::string("snapshot: write failed: ") + path);
   });
 }
 vxm_status vxm_snapshot_save(const char* path, double vs, vxm_layer* tsdf, vxm_layer* esdf) {
-  return vxm_snapshot_save_layers(path, vs, tsdf, nullptr, esdf);
+  return vxm_snapshot_save_layers(path, vs, tsdf, nullptr, nullptr, esdf);
 }
 
 vxm_status vxm_snapshot_load_layers(vxm_context* ctx, const char* path, double* vs_out,
-                                    vxm_layer** tsdf_out, vxm_layer** occ_out, vxm_layer** esdf_out) {
+                                    vxm_layer** tsdf_out, vxm_layer** occ_out, vxm_layer** color_out,
+                                    vxm_layer** esdf_out) {
   vxm_layer* T = nullptr;
   vxm_layer* O = nullptr;
+  vxm_layer* Cl = nullptr;
   vxm_layer* E = nullptr;
   const vxm_status st = guard([&] {
     REQUIRE_ARG(ctx && path && tsdf_out && esdf_out, "null argument");
@@ -1038,20 +1045,21 @@ vxm_status vxm_snapshot_load_layers(vxm_context* ctx, const char* path, double* 
       if (name_len > 64) io_fail("snapshot: layer name too long");
       std::string name(name_len, '\0');
       if (std::fread(name.data(), 1, name_len, in.f) != name_len) io_fail("snapshot: truncated layer name");
-      if (name == "tsdf" || name == "esdf" || (name == "occupancy" && occ_out)) {
-        vxm_layer*& L = name == "tsdf" ? T : name == "esdf" ? E : O;
+      if (name == "tsdf" || name == "esdf" || (name == "occupancy" && occ_out) ||
+          (name == "color" && color_out)) {
+        vxm_layer*& L = name == "tsdf" ? T : name == "esdf" ? E : name == "color" ? Cl : O;
         if (!L) {
-          const vxm_layer_type type = name == "tsdf"   ? VXM_LAYER_TSDF
-                                      : name == "esdf" ? VXM_LAYER_ESDF
-                                                       : VXM_LAYER_OCCUPANCY;
+          const vxm_layer_type type = name == "tsdf"    ? VXM_LAYER_TSDF
+                                      : name == "esdf"  ? VXM_LAYER_ESDF
+                                      : name == "color" ? VXM_LAYER_COLOR
+                                                        : VXM_LAYER_OCCUPANCY;
           const vxm_status s = vxm_layer_create(ctx, type, vs, 0, &L);
           if (s != VXM_OK) throw Error(s, g_err);
         }
         read_layer(in.f, L);
-      } else if (name == "occupancy") {
-        io_fail("snapshot: the file holds an occupancy layer (use vxm_snapshot_load_layers)");
-      } else if (name == "color") {
-        io_fail("snapshot: layer '" + name + "' is not implemented by this library");
+      } else if (name == "occupancy" || name == "color") {
+        io_fail("snapshot: the file holds a" + std::string(name == "occupancy" ? "n " : " ") + name +
+                " layer (use vxm_snapshot_load_layers)");
       } else {
         io_fail("snapshot: unknown layer name '" + name + "'");
       }
@@ -1059,18 +1067,20 @@ vxm_status vxm_snapshot_load_layers(vxm_context* ctx, const char* path, double* 
     *vs_out = vs;
     *tsdf_out = T;
     if (occ_out) *occ_out = O;
+    if (color_out) *color_out = Cl;
     *esdf_out = E;
   });
   if (st != VXM_OK) {
     vxm_layer_destroy(T);
     vxm_layer_destroy(O);
+    vxm_layer_destroy(Cl);
     vxm_layer_destroy(E);
   }
   return st;
 }
 vxm_status vxm_snapshot_load(vxm_context* ctx, const char* path, double* vs_out, vxm_layer** tsdf_out,
                              vxm_layer** esdf_out) {
-  return vxm_snapshot_load_layers(ctx, path, vs_out, tsdf_out, nullptr, esdf_out);
+  return vxm_snapshot_load_layers(ctx, path, vs_out, tsdf_out, nullptr, nullptr, esdf_out);
 }
 }  // extern "C"
 
@@ -1174,5 +1184,187 @@ vxm_status vxm_replay_lidar(vxm_context* ctx, const vxm_replay_config* cfg, cons
                             int w, int h, const float* depth, const vxm_pose* poses,
                             vxm_layer** tsdf_out, vxm_layer** esdf_out, vxm_frame_timing* timings) {
   return replay_common(ctx, cfg, nullptr, li, n, w, h, depth, poses, tsdf_out, esdf_out, timings);
+}
+}  // extern "C"
+
+// ---- color fusion + meshing + PLY -----------------------
+struct vxm_mesh_layer : MeshLayerH {};
+
+namespace {
+// save_mesh_ply — ply.cpp:33-105: header, vertices (x y z nx ny nz [r g b]) of
+// the non-empty blocks in sorted order, then faces with global indices.
+void write_ply(const MeshLayerH& M, const char* path) {
+  uint64_t nv = 0, nf = 0;
+  bool with_color = true;
+  for (const auto& kv : M.blocks) {
+    const MeshBlockH& b = kv.second;
+    if (b.triangles.empty()) continue;
+    nv += b.vertices.size() / 3;
+    nf += b.triangles.size() / 3;
+    with_color = with_color && b.colors.size() == b.vertices.size();
+  }
+  if (nv == 0) with_color = false;
+  File out;
+  out.f = std::fopen(path, "wb");
+  if (!out.f) io_fail(std::string("cannot open for writing: ") + path);
+  std::string hdr = "ply\nformat binary_little_endian 1.0\nelement vertex " + std::to_string(nv) +
+                    "\nproperty float x\nproperty float y\nproperty float z\n"
+                    "property float nx\nproperty float ny\nproperty float nz\n";
+  if (with_color) hdr += "property uchar red\nproperty uchar green\nproperty uchar blue\n";
+  hdr += "element face " + std::to_string(nf) + "\nproperty list uchar int vertex_indices\nend_header\n";
+  std::vector<unsigned char> buf(hdr.begin(), hdr.end());
+  auto raw = [&buf](const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    buf.insert(buf.end(), c, c + n);
+  };
+  for (const auto& kv : M.blocks) {
+    const MeshBlockH& b = kv.second;
+    if (b.triangles.empty()) continue;
+    const size_t n = b.vertices.size() / 3;
+    for (size_t i = 0; i < n; ++i) {
+      raw(&b.vertices[3 * i], 12);
+      raw(&b.normals[3 * i], 12);
+      if (with_color) raw(&b.colors[3 * i], 3);
+    }
+  }
+  uint32_t offset = 0;
+  for (const auto& kv : M.blocks) {
+    const MeshBlockH& b = kv.second;
+    if (b.triangles.empty()) continue;
+    for (size_t t = 0; t < b.triangles.size(); t += 3) {
+      const unsigned char three = 3;
+      raw(&three, 1);
+      for (int k = 0; k < 3; ++k) {
+        const int32_t v = int32_t(b.triangles[t + k] + offset);
+        raw(&v, 4);
+      }
+    }
+    offset += uint32_t(b.vertices.size() / 3);
+  }
+  if (std::fwrite(buf.data(), 1, buf.size(), out.f) != buf.size() || std::fflush(out.f) != 0)
+    io_fail(std::string("failed while writing: ") + path);
+}
+}  // namespace
+
+extern "C" {
+vxm_status vxm_integrate_color(vxm_layer* C, const uint8_t* rgb, int w, int h, const float* depth,
+                               int dw, int dh, const vxm_pose* T, const vxm_camera* cam,
+                               vxm_layer* tsdf, const vxm_integrator_config* cfg, vxm_blocklist* out) {
+  return guard([&] {
+    REQUIRE_ARG(C && T && cam && tsdf && cfg && out, "integrate_color: null argument");
+    REQUIRE_ARG(C->type == VXM_LAYER_COLOR, "integrate_color: layer is not a color layer");
+    REQUIRE_ARG(tsdf->type == VXM_LAYER_TSDF, "integrate_color: source is not a TSDF layer");
+    REQUIRE_ARG(C->ctx == tsdf->ctx, "integrate_color: layers on different contexts");
+    check_pose(T);  // check_frame — integrator.cpp:26-34, 198
+    if (w != cam->width || h != cam->height)
+      throw Error(VXM_ERR_INVALID_ARGUMENT, "integrate: image size does not match intrinsics");
+    if (dw != cam->width || dh != cam->height)
+      throw Error(VXM_ERR_INVALID_ARGUMENT, "integrate_color: depth size mismatch");
+    REQUIRE_ARG(w == 0 || h == 0 || (rgb && depth), "integrate_color: null image");
+    ViewArgs va{};
+    va.T_LS = *T;
+    va.lidar = false;
+    va.cam = *cam;
+    va.width = w;
+    va.height = h;
+    va.block_size = C->vs * kVPS;
+    va.cfg = {cfg->max_integration_distance, cfg->truncation, cfg->view_pixel_subsample};
+    stage_depth(C->ctx, depth, w, h, false, &va.depth_dev);
+    out->ctx = C->ctx;
+    run_integrate_color(C, tsdf, rgb, va, *cfg, out);
+  });
+}
+
+void vxm_mesh_config_default(vxm_mesh_config* c) {
+  c->min_weight = 1e-4f;  // marching_cubes.hpp:27
+  c->parallel = 1;
+}
+vxm_status vxm_mesh_layer_create(vxm_context* ctx, double vs, vxm_mesh_layer** out) {
+  return guard([&] {
+    REQUIRE_ARG(ctx && out, "null argument");
+    auto* m = new vxm_mesh_layer();
+    m->ctx = ctx;
+    m->vs = vs;
+    *out = m;
+  });
+}
+void vxm_mesh_layer_destroy(vxm_mesh_layer* m) { delete m; }
+double vxm_mesh_layer_voxel_size(const vxm_mesh_layer* m) { return m->vs; }
+uint64_t vxm_mesh_layer_num_blocks(const vxm_mesh_layer* m) { return m ? m->blocks.size() : 0; }
+vxm_status vxm_mesh_layer_sorted_indices(const vxm_mesh_layer* m, vxm_grid_index* keys, uint64_t cap) {
+  return guard([&] {
+    REQUIRE_ARG(m && (keys || m->blocks.empty()), "null argument");
+    REQUIRE_ARG(cap >= m->blocks.size(), "mesh sorted_indices: capacity smaller than num_blocks");
+    uint64_t i = 0;
+    for (const auto& kv : m->blocks) keys[i++] = {key_x(kv.first), key_y(kv.first), key_z(kv.first)};
+  });
+}
+vxm_status vxm_mesh_layer_block(const vxm_mesh_layer* m, const vxm_grid_index* g, vxm_mesh_block_view* out,
+                                int* found) {
+  return guard([&] {
+    REQUIRE_ARG(m && g && out && found, "null argument");
+    *out = vxm_mesh_block_view{};
+    *found = 0;
+    if (!(coord_ok(g->x) && coord_ok(g->y) && coord_ok(g->z))) return;
+    const auto it = m->blocks.find(pack_key(g->x, g->y, g->z));
+    if (it == m->blocks.end()) return;
+    const MeshBlockH& b = it->second;
+    *found = 1;
+    out->n_vertices = b.vertices.size() / 3;
+    out->n_triangles = b.triangles.size() / 3;
+    out->n_colors = b.colors.size() / 3;
+    out->vertices = b.vertices.data();
+    out->normals = b.normals.data();
+    out->colors = b.colors.data();
+    out->triangles = b.triangles.data();
+  });
+}
+vxm_status vxm_mesh_layer_erase(vxm_mesh_layer* m, const vxm_grid_index* g) {
+  return guard([&] {
+    REQUIRE_ARG(m && g, "null argument");
+    if (coord_ok(g->x) && coord_ok(g->y) && coord_ok(g->z)) m->blocks.erase(pack_key(g->x, g->y, g->z));
+  });
+}
+vxm_status vxm_mesh_block(vxm_mesh_layer* m, vxm_layer* T, const vxm_grid_index* g, const vxm_mesh_config* cfg,
+                          vxm_layer* color) {
+  return guard([&] {
+    REQUIRE_ARG(m && T && g && cfg, "null argument");
+    REQUIRE_ARG(T->type == VXM_LAYER_TSDF, "mesh_block: source is not a TSDF layer");
+    REQUIRE_ARG(!color || color->type == VXM_LAYER_COLOR, "mesh_block: color is not a color layer");
+    vxm_blocklist one;
+    one.ctx = T->ctx;
+    one.assign_host(g, 1);
+    T->refresh();
+    run_mesh_blocks(m, T, &one, cfg->min_weight, color);
+  });
+}
+vxm_status vxm_update_mesh_list(vxm_mesh_layer* m, vxm_layer* T, vxm_blocklist* updated,
+                                const vxm_mesh_config* cfg, vxm_layer* color, vxm_blocklist* out) {
+  return guard([&] {
+    REQUIRE_ARG(m && T && updated && cfg && out, "null argument");
+    REQUIRE_ARG(T->type == VXM_LAYER_TSDF, "update_mesh: source is not a TSDF layer");
+    REQUIRE_ARG(!color || color->type == VXM_LAYER_COLOR, "update_mesh: color is not a color layer");
+    const auto targets = run_update_mesh(m, T, updated, cfg->min_weight, color);
+    out->ctx = T->ctx;
+    out->assign_host(targets.data(), targets.size());
+    out->sorted_unique = true;
+  });
+}
+vxm_status vxm_update_mesh(vxm_mesh_layer* m, vxm_layer* T, const vxm_grid_index* updated, uint64_t n,
+                           const vxm_mesh_config* cfg, vxm_layer* color, vxm_blocklist* out) {
+  return guard([&] {
+    REQUIRE_ARG(T && (updated || n == 0), "null argument");
+    vxm_blocklist list;
+    list.ctx = T->ctx;
+    list.assign_host(updated, n);
+    const vxm_status s = vxm_update_mesh_list(m, T, &list, cfg, color, out);
+    if (s != VXM_OK) throw Error(s, g_err);
+  });
+}
+vxm_status vxm_save_mesh_ply(const vxm_mesh_layer* m, const char* path) {
+  return guard([&] {
+    REQUIRE_ARG(m && path, "null argument");
+    write_ply(*m, path);
+  });
 }
 }  // extern "C"

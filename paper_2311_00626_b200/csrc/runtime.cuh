@@ -138,7 +138,9 @@ struct Layer {
   const Layer* subset_of = nullptr;
   bool subset_valid = true;
 
-  size_t voxel_bytes() const { return type == VXM_LAYER_TSDF ? 8 : type == VXM_LAYER_ESDF ? 12 : 4; }
+  size_t voxel_bytes() const {
+    return type == VXM_LAYER_ESDF ? 12 : type == VXM_LAYER_OCCUPANCY ? 4 : 8;  // TSDF, color: 8
+  }
   size_t block_bytes() const { return voxel_bytes() * kVPB; }
   void* cur_pool() const { return pool[type == VXM_LAYER_ESDF ? cur_host : 0]; }
   // Grow pool/hash/side arrays so that capacity >= need (requires exact num_blocks).

@@ -7,7 +7,11 @@ Names, argument meaning and error behaviour follow the reference:
 reference (proj/include/voxmap/...)    here
 =====================================  ==============================================
 Layer<TsdfVoxel>, Layer<EsdfVoxel>,    TsdfLayer, EsdfLayer,       core/layer.hpp:47-125
-Layer<OccupancyVoxel>                  OccupancyLayer
+Layer<OccupancyVoxel>,                 OccupancyLayer, ColorLayer
+Layer<ColorVoxel>
+integrate_color                        integrate_color             integrate/integrator.hpp:57-66
+MeshLayer / mesh_block / update_mesh   MeshLayer / mesh_block /    mesh/marching_cubes.hpp:35-78
+/ save_mesh_ply                        update_mesh / save_mesh_ply mesh/ply.hpp:27-29
 integrate_depth (camera / lidar;       integrate_depth             integrate/integrator.hpp:36-55
 TSDF or occupancy layer)
 blocks_in_view                         blocks_in_view              sensor/view.hpp:38-48
@@ -342,6 +346,129 @@ class EsdfLayer(_Layer):
         return obj
 
 
+class ColorLayer(_Layer):
+    """Layer<ColorVoxel> (core/voxels.hpp:34-41)."""
+    kind = A.LAYER_COLOR
+    dtype = A.COLOR_DTYPE
+
+    @classmethod
+    def _adopt(cls, h, ctx):
+        obj = cls.__new__(cls)
+        obj.ctx, obj.h = ctx, h
+        return obj
+
+
+class MeshBlock:
+    """MeshBlock (mesh/mesh_layer.hpp:16-25): numpy copies of one block's mesh."""
+
+    def __init__(self, vertices, normals, colors, triangles):
+        self.vertices, self.normals, self.colors, self.triangles = vertices, normals, colors, triangles
+
+    def empty(self) -> bool:
+        return len(self.triangles) == 0
+
+
+class MeshLayer:
+    """MeshLayer (mesh/mesh_layer.hpp:27-66); meshes are computed on the device."""
+
+    def __init__(self, voxel_size: float, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib().vxm_mesh_layer_create(self.ctx.h, C.c_double(voxel_size), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().vxm_mesh_layer_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def voxel_size(self) -> float:
+        lib().vxm_mesh_layer_voxel_size.restype = C.c_double
+        return float(lib().vxm_mesh_layer_voxel_size(self.h))
+
+    def num_blocks(self) -> int:
+        lib().vxm_mesh_layer_num_blocks.restype = C.c_uint64
+        return int(lib().vxm_mesh_layer_num_blocks(self.h))
+
+    def sorted_indices(self) -> np.ndarray:
+        n = self.num_blocks()
+        keys = np.zeros((n, 3), np.int32)
+        check(lib().vxm_mesh_layer_sorted_indices(self.h, A.ptr(keys), C.c_uint64(n)))
+        return keys
+
+    def block(self, g):
+        """block_ptr: MeshBlock or None."""
+        k = A.as_keys([g])
+        v = A.MeshBlockViewC()
+        found = C.c_int()
+        check(lib().vxm_mesh_layer_block(self.h, A.ptr(k), C.byref(v), C.byref(found)))
+        if not found.value:
+            return None
+
+        def arr(p, n, dt, w):
+            if n == 0:
+                return np.zeros((0, w), dt)
+            return np.ctypeslib.as_array(p, shape=(n * w,)).reshape(n, w).astype(dt, copy=True)
+        return MeshBlock(arr(v.vertices, v.n_vertices, np.float32, 3),
+                         arr(v.normals, v.n_vertices, np.float32, 3),
+                         arr(v.colors, v.n_colors, np.uint8, 3),
+                         arr(v.triangles, v.n_triangles, np.uint32, 3))
+
+    def erase(self, g) -> None:
+        check(lib().vxm_mesh_layer_erase(self.h, A.ptr(A.as_keys([g]))))
+
+
+def _color(rgb):
+    c = np.ascontiguousarray(rgb, dtype=np.uint8)
+    if c.ndim != 3 or c.shape[2] != 3:
+        raise InvalidArgumentError("color image must be (height, width, 3) uint8")
+    return c
+
+
+def integrate_color(color: ColorLayer, rgb, depth, T_LS, camera, tsdf: TsdfLayer, cfg=None,
+                    out: BlockList | None = None):
+    """integrate_color (integrate/integrator.hpp:57-66): fuses an RGB image
+    ((H, W, 3) uint8) into the TSDF surface band; returns the changed blocks."""
+    cfg = cfg or IntegratorConfig()
+    c, d = _color(rgb), _depth(depth)
+    out = out or color._result_list()
+    check(lib().vxm_integrate_color(color.h, A.ptr(c), C.c_int(c.shape[1]), C.c_int(c.shape[0]),
+                                    A.ptr(d), C.c_int(d.shape[1]), C.c_int(d.shape[0]),
+                                    C.byref(_pose_c(T_LS)), C.byref(camera), tsdf.h, C.byref(cfg),
+                                    out.h))
+    return out.numpy()
+
+
+def mesh_block(mesh: MeshLayer, tsdf: TsdfLayer, g, cfg=None, color: ColorLayer | None = None):
+    """mesh_block (mesh/marching_cubes.hpp:67-69): meshes block g into `mesh`
+    (get_or_create(g) = mesh_block(...)) and returns its MeshBlock."""
+    cfg = cfg or A.default_mesh_config()
+    check(lib().vxm_mesh_block(mesh.h, tsdf.h, A.ptr(A.as_keys([g])), C.byref(cfg),
+                               color.h if color is not None else None))
+    return mesh.block(g)
+
+
+def update_mesh(mesh: MeshLayer, tsdf: TsdfLayer, updated, cfg=None, color: ColorLayer | None = None):
+    """update_mesh (mesh/marching_cubes.hpp:71-78): returns the re-meshed blocks."""
+    cfg = cfg or A.default_mesh_config()
+    out = BlockList(mesh.ctx)
+    cl = color.h if color is not None else None
+    if isinstance(updated, BlockList):
+        check(lib().vxm_update_mesh_list(mesh.h, tsdf.h, updated.h, C.byref(cfg), cl, out.h))
+    else:
+        k = A.as_keys(updated)
+        check(lib().vxm_update_mesh(mesh.h, tsdf.h, A.ptr(k), C.c_uint64(len(k)), C.byref(cfg), cl,
+                                    out.h))
+    return out.numpy()
+
+
+def save_mesh_ply(mesh: MeshLayer, path: str) -> None:
+    """save_mesh_ply (mesh/ply.hpp:27-29)."""
+    check(lib().vxm_save_mesh_ply(mesh.h, os.fsencode(path)))
+
+
 class OccupancyLayer(_Layer):
     """Layer<OccupancyVoxel> (core/voxels.hpp:28-32): log-odds, 0 = unobserved."""
     kind = A.LAYER_OCCUPANCY
@@ -395,27 +522,33 @@ def write_timing_csv(timings, path: str) -> None:
 
 
 def save_snapshot(path: str, voxel_size: float, tsdf: TsdfLayer | None = None,
-                  esdf: EsdfLayer | None = None, occupancy: OccupancyLayer | None = None) -> None:
+                  esdf: EsdfLayer | None = None, occupancy: OccupancyLayer | None = None,
+                  color: ColorLayer | None = None) -> None:
     """save_snapshot (core/serialization.hpp:31): VXLF v1, byte-identical to the
-    reference's for equal maps (layers tsdf, occupancy, esdf)."""
+    reference's for equal maps (layers tsdf, occupancy, color, esdf)."""
     h = lambda L: L.h if L is not None else None  # noqa: E731
     check(lib().vxm_snapshot_save_layers(os.fsencode(path), C.c_double(voxel_size), h(tsdf),
-                                         h(occupancy), h(esdf)))
+                                         h(occupancy), h(color), h(esdf)))
 
 
-def load_snapshot(path: str, ctx: Context | None = None, with_occupancy: bool = False):
-    """load_snapshot (core/serialization.hpp:35) -> (voxel_size, tsdf | None, esdf | None),
-    or (voxel_size, tsdf, occupancy, esdf) with_occupancy."""
+def load_snapshot(path: str, ctx: Context | None = None, with_occupancy: bool = False,
+                  with_color: bool = False):
+    """load_snapshot (core/serialization.hpp:35) -> (voxel_size, tsdf | None, esdf | None);
+    with_occupancy / with_color insert the occupancy / color layer before the ESDF:
+    (voxel_size, tsdf, [occupancy,] [color,] esdf)."""
     ctx = ctx or default_context()
     vs = C.c_double()
-    th, oh, eh = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    th, oh, ch, eh = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
     check(lib().vxm_snapshot_load_layers(ctx.h, os.fsencode(path), C.byref(vs), C.byref(th),
-                                         C.byref(oh) if with_occupancy else None, C.byref(eh)))
-    t = TsdfLayer._adopt(th, ctx) if th.value else None
-    e = EsdfLayer._adopt(eh, ctx) if eh.value else None
+                                         C.byref(oh) if with_occupancy else None,
+                                         C.byref(ch) if with_color else None, C.byref(eh)))
+    out = [vs.value, TsdfLayer._adopt(th, ctx) if th.value else None]
     if with_occupancy:
-        return vs.value, t, (OccupancyLayer._adopt(oh, ctx) if oh.value else None), e
-    return vs.value, t, e
+        out.append(OccupancyLayer._adopt(oh, ctx) if oh.value else None)
+    if with_color:
+        out.append(ColorLayer._adopt(ch, ctx) if ch.value else None)
+    out.append(EsdfLayer._adopt(eh, ctx) if eh.value else None)
+    return tuple(out)
 
 
 def _depth(depth):
