@@ -314,34 +314,46 @@ vxm_status vxm_update_mesh_list(vxm_mesh_layer* mesh, vxm_layer* tsdf, vxm_block
 vxm_status vxm_save_mesh_ply(const vxm_mesh_layer* mesh, const char* path);
 
 /* ---- replay (io/pipeline.hpp:27-72, pipeline.cpp:54-148) ------------------- */
-/* ReplayConfig (pipeline.hpp:27-36; color / mesh are out of scope). */
+/* ReplayConfig (pipeline.hpp:27-36). */
 typedef struct {
   double voxel_size;
-  int32_t update_every;  /* derive the ESDF every this many frames (+ after the last) */
+  int32_t update_every;  /* derive ESDF + mesh every this many frames (+ after the last) */
   vxm_integrator_config integrator;
   vxm_esdf_config esdf;
   int32_t use_occupancy; /* fuse occupancy instead of the TSDF (pipeline.cpp:73-77, 95-101) */
+  int32_t with_color;    /* fuse color (camera datasets only, pipeline.cpp:111-117) */
+  vxm_mesh_config mesh;
 } vxm_replay_config;
 /* FrameTiming: wall-clock ms per stage of one frame (0 when skipped). */
 typedef struct {
   int32_t frame;
   double tsdf_ms, color_ms, esdf_ms, mesh_ms;
 } vxm_frame_timing;
+/* ReplayResult's LayerCake (pipeline.hpp:54-57): the layers replay created
+ * (NULL when never required, as the reference's lazily created layers). */
+typedef struct {
+  vxm_layer* source;     /* TSDF, or occupancy with use_occupancy */
+  vxm_layer* esdf;
+  vxm_layer* color;
+  vxm_mesh_layer* mesh;
+} vxm_replay_result;
 /* make_replay_config (pipeline.cpp:46-52): truncation 4 voxels, site threshold 1. */
 void vxm_replay_config_make(double voxel_size, vxm_replay_config* out);
 /* replay (pipeline.cpp:54-148) over in-memory frames: n_frames depth images
- * (host, n_frames x height x width, row-major) with their poses; integrates every
- * frame and, every update_every frames and after the last one, folds the blocks
- * changed since the previous update into the ESDF.  Creates *tsdf_out (the
- * source layer: an occupancy layer when cfg->use_occupancy) and *esdf_out on ctx; timings has n_frames entries.  Errors as the reference: no
- * frames or update_every < 1 -> VXM_ERR_INVALID_ARGUMENT. */
+ * (host, n_frames x height x width, row-major) with their poses, and for the
+ * camera optionally their color images (host, n_frames x height x width x 3, or
+ * NULL: frames without color).  Integrates every frame (and its color with
+ * with_color) and, every update_every frames and after the last one, folds the
+ * blocks changed since the previous update into the ESDF and (TSDF source) the
+ * mesh.  timings has n_frames entries.  Errors as the reference: no frames,
+ * update_every < 1, color with occupancy or LiDAR -> VXM_ERR_INVALID_ARGUMENT. */
 vxm_status vxm_replay_camera(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_camera* cam,
                              int n_frames, int width, int height, const float* depth,
-                             const vxm_pose* poses, vxm_layer** tsdf_out, vxm_layer** esdf_out,
+                             const uint8_t* rgb, const vxm_pose* poses, vxm_replay_result* out,
                              vxm_frame_timing* timings);
 vxm_status vxm_replay_lidar(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_lidar* lidar,
                             int n_frames, int width, int height, const float* depth,
-                            const vxm_pose* poses, vxm_layer** tsdf_out, vxm_layer** esdf_out,
+                            const vxm_pose* poses, vxm_replay_result* out,
                             vxm_frame_timing* timings);
 
 /* ---- snapshots (core/serialization.hpp:29-35, FORMATS.md "VXLF") -------- */

@@ -89,17 +89,6 @@ class EsdfConfigC(C.Structure):
                 ("max_distance", C.c_double), ("parallel", C.c_int32)]
 
 
-class ReplayConfigC(C.Structure):
-    """vxm_replay_config — ReplayConfig (io/pipeline.hpp:27-35)."""
-    _fields_ = [("voxel_size", C.c_double), ("update_every", C.c_int32),
-                ("integrator", IntegratorConfigC), ("esdf", EsdfConfigC),
-                ("use_occupancy", C.c_int32)]
-
-
-FRAME_TIMING_DTYPE = np.dtype([("frame", "<i4"), ("pad_", "<i4"), ("tsdf_ms", "<f8"),
-                               ("color_ms", "<f8"), ("esdf_ms", "<f8"), ("mesh_ms", "<f8")])
-
-
 class MeshConfigC(C.Structure):
     """vxm_mesh_config — MeshConfig (mesh/marching_cubes.hpp:24-33)."""
     _fields_ = [("min_weight", C.c_float), ("parallel", C.c_int32)]
@@ -110,6 +99,22 @@ def default_mesh_config(**kw):
     for k, v in kw.items():
         setattr(c, k, v)
     return c
+
+
+class ReplayConfigC(C.Structure):
+    """vxm_replay_config — ReplayConfig (io/pipeline.hpp:27-36)."""
+    _fields_ = [("voxel_size", C.c_double), ("update_every", C.c_int32),
+                ("integrator", IntegratorConfigC), ("esdf", EsdfConfigC),
+                ("use_occupancy", C.c_int32), ("with_color", C.c_int32), ("mesh", MeshConfigC)]
+
+
+class ReplayResultC(C.Structure):
+    _fields_ = [("source", C.c_void_p), ("esdf", C.c_void_p), ("color", C.c_void_p),
+                ("mesh", C.c_void_p)]
+
+
+FRAME_TIMING_DTYPE = np.dtype([("frame", "<i4"), ("pad_", "<i4"), ("tsdf_ms", "<f8"),
+                               ("color_ms", "<f8"), ("esdf_ms", "<f8"), ("mesh_ms", "<f8")])
 
 
 class MeshBlockViewC(C.Structure):

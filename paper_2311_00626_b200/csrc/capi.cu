@@ -22,6 +22,7 @@ struct vxm_context : Context {};
 struct vxm_layer : Layer {};
 struct vxm_blocklist : BlockList {};
 struct vxm_esdf_state : EsdfState {};
+struct vxm_mesh_layer : MeshLayerH {};
 
 namespace {
 thread_local std::string g_err;
@@ -1092,23 +1093,25 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
 
 vxm_status replay_common(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_camera* cam,
                          const vxm_lidar* li, int n, int w, int h, const float* depth,
-                         const vxm_pose* poses, vxm_layer** tsdf_out, vxm_layer** esdf_out,
+                         const uint8_t* rgb, const vxm_pose* poses, vxm_replay_result* res,
                          vxm_frame_timing* timings) {
   vxm_layer* T = nullptr;
   vxm_layer* E = nullptr;
+  vxm_layer* Cl = nullptr;
+  vxm_mesh_layer* M = nullptr;
   const vxm_status st = guard([&] {
-    REQUIRE_ARG(ctx && cfg && (cam || li) && tsdf_out && esdf_out && timings, "null argument");
+    REQUIRE_ARG(ctx && cfg && (cam || li) && res && timings, "null argument");
     if (n <= 0) throw Error(VXM_ERR_INVALID_ARGUMENT, "replay: dataset has no frames");
     if (cfg->update_every < 1) throw Error(VXM_ERR_INVALID_ARGUMENT, "replay: update_every must be >= 1");
+    if (cfg->with_color && (cfg->use_occupancy || !cam))
+      throw Error(VXM_ERR_INVALID_ARGUMENT, "replay: color needs a camera dataset fused into a TSDF map");
     REQUIRE_ARG(depth && poses, "null argument");
     // the source layer: TSDF, or occupancy with use_occupancy (pipeline.cpp:95-101)
     vxm_status s = vxm_layer_create(ctx, cfg->use_occupancy ? VXM_LAYER_OCCUPANCY : VXM_LAYER_TSDF,
                                     cfg->voxel_size, 0, &T);
     if (s != VXM_OK) throw Error(s, g_err);
-    s = vxm_layer_create(ctx, VXM_LAYER_ESDF, cfg->voxel_size, 0, &E);
-    if (s != VXM_OK) throw Error(s, g_err);
-    vxm_blocklist changed, esdf_changed, pending;
-    changed.ctx = esdf_changed.ctx = pending.ctx = ctx;
+    vxm_blocklist changed, esdf_changed, pending, color_changed;
+    changed.ctx = esdf_changed.ctx = pending.ctx = color_changed.ctx = ctx;
     uint32_t n_pending = 0;  // keys in `pending` (unsorted, may repeat until folded)
     DevBuf grow;
     const size_t frame_px = size_t(w) * size_t(h);
@@ -1138,10 +1141,25 @@ vxm_status replay_common(vxm_context* ctx, const vxm_replay_config* cfg, const v
                                  sizeof(uint64_t) * n_ch, cudaMemcpyDeviceToDevice, ctx->stream));
         n_pending += n_ch;
       }
+      if (cfg->with_color && rgb) {  // pipeline.cpp:111-117
+        const auto tc = std::chrono::steady_clock::now();
+        if (!Cl) {
+          s = vxm_layer_create(ctx, VXM_LAYER_COLOR, cfg->voxel_size, 0, &Cl);
+          if (s != VXM_OK) throw Error(s, g_err);
+        }
+        const ViewArgs vc = frame_args(T, depth + size_t(k) * frame_px, w, h, &poses[k], cam, nullptr,
+                                       &cfg->integrator, false);
+        run_integrate_color(Cl, T, rgb + size_t(k) * frame_px * 3, vc, cfg->integrator, &color_changed);
+        t.color_ms = ms_since(tc);
+      }
       const bool last = k + 1 == n;
       const bool on_cadence = (k + 1) % cfg->update_every == 0;
-      if ((on_cadence || last) && n_pending > 0) {  // derive_layers (mesh: out of scope)
+      if ((on_cadence || last) && n_pending > 0) {  // derive_layers (pipeline.cpp:71-86)
         const auto t1 = std::chrono::steady_clock::now();
+        if (!E) {
+          s = vxm_layer_create(ctx, VXM_LAYER_ESDF, cfg->voxel_size, 0, &E);
+          if (s != VXM_OK) throw Error(s, g_err);
+        }
         VXM_CUDA(cudaMemcpyAsync(pending.d_count, &n_pending, sizeof n_pending, cudaMemcpyHostToDevice,
                                  ctx->stream));
         pending.count_hint = n_pending;
@@ -1151,15 +1169,25 @@ vxm_status replay_common(vxm_context* ctx, const vxm_replay_config* cfg, const v
         pending.sorted_unique = true;
         run_update_esdf(E, T, &pending, cfg->esdf, &esdf_changed);
         t.esdf_ms = ms_since(t1);
+        if (!cfg->use_occupancy) {
+          const auto t2 = std::chrono::steady_clock::now();
+          if (!M) {
+            s = vxm_mesh_layer_create(ctx, cfg->voxel_size, &M);
+            if (s != VXM_OK) throw Error(s, g_err);
+          }
+          run_update_mesh(M, T, &pending, cfg->mesh.min_weight, Cl);
+          t.mesh_ms = ms_since(t2);
+        }
         n_pending = 0;
       }
     }
-    *tsdf_out = T;
-    *esdf_out = E;
+    *res = vxm_replay_result{T, E, Cl, M};
   });
   if (st != VXM_OK) {
     vxm_layer_destroy(T);
     vxm_layer_destroy(E);
+    vxm_layer_destroy(Cl);
+    vxm_mesh_layer_destroy(M);
   }
   return st;
 }
@@ -1170,25 +1198,26 @@ void vxm_replay_config_make(double voxel_size, vxm_replay_config* out) {
   out->voxel_size = voxel_size;
   out->update_every = 4;
   out->use_occupancy = 0;
+  out->with_color = 0;
+  vxm_mesh_config_default(&out->mesh);
   vxm_integrator_config_default(&out->integrator);
   vxm_esdf_config_default(&out->esdf);
   out->integrator.truncation = 4.0 * voxel_size;
   out->esdf.site_threshold = voxel_size;
 }
 vxm_status vxm_replay_camera(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_camera* cam,
-                             int n, int w, int h, const float* depth, const vxm_pose* poses,
-                             vxm_layer** tsdf_out, vxm_layer** esdf_out, vxm_frame_timing* timings) {
-  return replay_common(ctx, cfg, cam, nullptr, n, w, h, depth, poses, tsdf_out, esdf_out, timings);
+                             int n, int w, int h, const float* depth, const uint8_t* rgb,
+                             const vxm_pose* poses, vxm_replay_result* out, vxm_frame_timing* timings) {
+  return replay_common(ctx, cfg, cam, nullptr, n, w, h, depth, rgb, poses, out, timings);
 }
 vxm_status vxm_replay_lidar(vxm_context* ctx, const vxm_replay_config* cfg, const vxm_lidar* li, int n,
                             int w, int h, const float* depth, const vxm_pose* poses,
-                            vxm_layer** tsdf_out, vxm_layer** esdf_out, vxm_frame_timing* timings) {
-  return replay_common(ctx, cfg, nullptr, li, n, w, h, depth, poses, tsdf_out, esdf_out, timings);
+                            vxm_replay_result* out, vxm_frame_timing* timings) {
+  return replay_common(ctx, cfg, nullptr, li, n, w, h, depth, nullptr, poses, out, timings);
 }
 }  // extern "C"
 
 // ---- color fusion + meshing + PLY -----------------------
-struct vxm_mesh_layer : MeshLayerH {};
 
 namespace {
 // save_mesh_ply — ply.cpp:33-105: header, vertices (x y z nx ny nz [r g b]) of

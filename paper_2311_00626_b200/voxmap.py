@@ -488,25 +488,49 @@ def make_replay_config(voxel_size: float) -> A.ReplayConfigC:
     return c
 
 
-def replay(frames, intrinsics, cfg: A.ReplayConfigC, ctx: Context | None = None):
-    """replay (io/pipeline.cpp:54-148) over in-memory frames [(T_WS, depth), ...]:
-    returns (source, esdf, timings) with FrameTiming records (FRAME_TIMING_DTYPE);
-    source is the TsdfLayer, or the OccupancyLayer when cfg.use_occupancy."""
+def replay_cake(frames, intrinsics, cfg: A.ReplayConfigC, ctx: Context | None = None):
+    """replay (io/pipeline.cpp:54-148) over in-memory frames [(T_WS, depth) or
+    (T_WS, depth, rgb), ...] -> (cake, timings): cake is a dict of the layers
+    replay created ("source": TsdfLayer / OccupancyLayer, "esdf", "color",
+    "mesh"; None when never required) and timings the FrameTiming records
+    (FRAME_TIMING_DTYPE)."""
     ctx = ctx or default_context()
     n = len(frames)
+    rgb = None
     if n:
-        depth = np.ascontiguousarray(np.stack([_depth(d) for _, d in frames]), np.float32)
+        depth = np.ascontiguousarray(np.stack([_depth(f[1]) for f in frames]), np.float32)
         h, w = depth.shape[1], depth.shape[2]
-        poses = (A.PoseC * n)(*[_pose_c(T) for T, _ in frames])
+        poses = (A.PoseC * n)(*[_pose_c(f[0]) for f in frames])
+        if all(len(f) > 2 and f[2] is not None for f in frames):
+            rgb = np.ascontiguousarray(np.stack([_color(f[2]) for f in frames]))
     else:
         depth, h, w, poses = np.zeros((0, 0, 0), np.float32), 0, 0, (A.PoseC * 1)()
     timings = np.zeros(max(n, 1), A.FRAME_TIMING_DTYPE)
-    th, eh = C.c_void_p(), C.c_void_p()
-    fn = lib().vxm_replay_camera if isinstance(intrinsics, A.Camera) else lib().vxm_replay_lidar
-    check(fn(ctx.h, C.byref(cfg), C.byref(intrinsics), C.c_int(n), C.c_int(w), C.c_int(h), A.ptr(depth),
-             poses, C.byref(th), C.byref(eh), A.ptr(timings)))
-    src = (OccupancyLayer if cfg.use_occupancy else TsdfLayer)._adopt(th, ctx)
-    return src, EsdfLayer._adopt(eh, ctx), timings[:n]
+    res = A.ReplayResultC()
+    if isinstance(intrinsics, A.Camera):
+        check(lib().vxm_replay_camera(ctx.h, C.byref(cfg), C.byref(intrinsics), C.c_int(n), C.c_int(w),
+                                      C.c_int(h), A.ptr(depth), A.ptr(rgb) if rgb is not None else None,
+                                      poses, C.byref(res), A.ptr(timings)))
+    else:
+        check(lib().vxm_replay_lidar(ctx.h, C.byref(cfg), C.byref(intrinsics), C.c_int(n), C.c_int(w),
+                                     C.c_int(h), A.ptr(depth), poses, C.byref(res), A.ptr(timings)))
+    src_cls = OccupancyLayer if cfg.use_occupancy else TsdfLayer
+    mesh = None
+    if res.mesh:
+        mesh = MeshLayer.__new__(MeshLayer)
+        mesh.ctx, mesh.h = ctx, C.c_void_p(res.mesh)
+    cake = {"source": src_cls._adopt(C.c_void_p(res.source), ctx) if res.source else None,
+            "esdf": EsdfLayer._adopt(C.c_void_p(res.esdf), ctx) if res.esdf else None,
+            "color": ColorLayer._adopt(C.c_void_p(res.color), ctx) if res.color else None,
+            "mesh": mesh}
+    return cake, timings[:n]
+
+
+def replay(frames, intrinsics, cfg: A.ReplayConfigC, ctx: Context | None = None):
+    """replay (io/pipeline.cpp:54-148) -> (source, esdf, timings); see replay_cake
+    for the color and mesh layers."""
+    cake, timings = replay_cake(frames, intrinsics, cfg, ctx)
+    return cake["source"], cake["esdf"], timings
 
 
 def write_timing_csv(timings, path: str) -> None:

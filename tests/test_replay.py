@@ -42,7 +42,40 @@ def test_replay_matches_reference_pipeline(vx, ref, update_every):
     assert layers_identical(*E.export(), *ref.export(Eo))
     assert list(timings["frame"]) == list(range(len(frames)))
     assert list(np.nonzero(timings["esdf_ms"] > 0)[0]) == derived
-    assert np.all(timings["tsdf_ms"] > 0) and np.all(timings["mesh_ms"] == 0)
+    assert np.all(timings["tsdf_ms"] > 0)
+    assert list(np.nonzero(timings["mesh_ms"] > 0)[0]) == derived
+
+
+@pytest.mark.gpu
+def test_replay_with_color_and_mesh_matches_reference_pipeline(vx, ref):
+    """derive_layers with update_mesh(..., cake.color) and per-frame
+    integrate_color (pipeline.cpp:71-86, 111-117)."""
+    from tests.test_mesh import _same_mesh
+    cam, frames = camera_frames("room", 320, 240, 5, 16)
+    frames = [(T, d, ref.render_color("room", T, cam)) for T, d in frames]
+    cfg = vx.make_replay_config(0.04)
+    cfg.update_every = 2
+    cfg.with_color = 1
+    cake, timings = vx.replay_cake(frames, cam, cfg)
+    To, Eo = ref.layer(A.LAYER_TSDF, 0.04), ref.layer(A.LAYER_ESDF, 0.04)
+    Co, Mo = ref.layer(A.LAYER_COLOR, 0.04), ref.mesh_layer(0.04)
+    pending = np.zeros((0, 3), np.int32)
+    derived = []
+    for k, (pose, d, rgb) in enumerate(frames):
+        pending = np.unique(np.concatenate([pending, ref.integrate_camera(To, d, pose, cam, cfg.integrator)]),
+                            axis=0)
+        ref.integrate_color(Co, rgb, d, pose, cam, To, cfg.integrator)
+        if ((k + 1) % 2 == 0 or k + 1 == len(frames)) and len(pending):
+            ref.update_esdf(Eo, To, pending, cfg.esdf)
+            ref.update_mesh(Mo, To, pending, cfg.mesh.min_weight, Co)
+            pending = np.zeros((0, 3), np.int32)
+            derived.append(k)
+    assert layers_identical(*cake["source"].export(), *ref.export(To))
+    assert layers_identical(*cake["esdf"].export(), *ref.export(Eo))
+    assert layers_identical(*cake["color"].export(), *ref.export(Co))
+    assert _same_mesh(cake["mesh"], Mo)
+    assert list(np.nonzero(timings["mesh_ms"] > 0)[0]) == derived
+    assert np.all(timings["color_ms"] > 0)
 
 
 @pytest.mark.gpu
@@ -53,6 +86,11 @@ def test_replay_argument_errors(vx):
         vx.replay([], cam, cfg)
     cfg.update_every = 0
     with pytest.raises(vx.InvalidArgumentError, match="update_every"):
+        vx.replay(frames, cam, cfg)
+    cfg.update_every = 1
+    cfg.with_color = 1
+    cfg.use_occupancy = 1
+    with pytest.raises(vx.InvalidArgumentError, match="color needs a camera"):
         vx.replay(frames, cam, cfg)
 
 
