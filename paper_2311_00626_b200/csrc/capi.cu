@@ -125,6 +125,56 @@ bool is_source(const vxm_layer* L) {
   return L->type == VXM_LAYER_TSDF || L->type == VXM_LAYER_OCCUPANCY;
 }
 
+// VXM_TRACE_HOST=1: host-side phase times of the host-buffer entry points (µs).
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  char buf[256];
+  int len = 0;
+  explicit HostTrace(const char* name) : on(std::getenv("VXM_TRACE_HOST") != nullptr) {
+    if (on) {
+      t0 = std::chrono::steady_clock::now();
+      len = std::snprintf(buf, sizeof buf, "%s:", name);
+      g_host_trace = this;
+    }
+  }
+  // device-side marks (events on the context stream), printed at the end
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8];
+  const char* ev_name[8];
+  int n_ev = 0;
+  void dev_mark(cudaStream_t s, const char* what) {
+    if (!on || n_ev >= 8) return;
+    stream = s;
+    cudaEventCreate(&ev[n_ev]);
+    cudaEventRecord(ev[n_ev], s);
+    ev_name[n_ev++] = what;
+  }
+  void mark(const char* what) {
+    if (!on || len >= int(sizeof buf) - 32) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    len += std::snprintf(buf + len, sizeof buf - len, " %s %.1f", what, us);
+  }
+  ~HostTrace() {
+    if (on) {
+      if (n_ev > 1) {
+        cudaStreamSynchronize(stream);
+        len += std::snprintf(buf + len, sizeof buf - len, " | dev");
+        for (int i = 1; i < n_ev && len < int(sizeof buf) - 32; ++i) {
+          float ms = 0.0f;
+          cudaEventElapsedTime(&ms, ev[0], ev[i]);
+          len += std::snprintf(buf + len, sizeof buf - len, " %s %.1f", ev_name[i], 1e3 * ms);
+        }
+      }
+      for (int i = 0; i < n_ev; ++i) cudaEventDestroy(ev[i]);
+      std::fprintf(stderr, "%s\n", buf);
+      g_host_trace = nullptr;
+    }
+  }
+  static thread_local HostTrace* g_host_trace;
+};
+thread_local HostTrace* HostTrace::g_host_trace = nullptr;
+
 void check_pose(const vxm_pose* T) {
   if (!vxm_pose_valid(T)) throw Error(VXM_ERR_INVALID_POSE, "integrate: degenerate sensor pose");
 }
@@ -171,11 +221,24 @@ vxm_status integrate_common(vxm_layer* L, const float* depth, int w, int h, cons
                             const vxm_integrator_config* cfg, vxm_blocklist* out, bool on_device) {
   return guard([&] {
     REQUIRE_ARG(L && T && cfg && out && (cam || li), "integrate: null argument");
+    HostTrace tr("integrate");
+    tr.dev_mark(L->ctx->stream, "start");
     const ViewArgs va = frame_args(L, depth, w, h, T, cam, li, cfg, on_device);
+    tr.mark("staged");
+    tr.dev_mark(L->ctx->stream, "h2d");
     out->ctx = L->ctx;
-    run_integrate(L, va, *cfg, out);
+    out->want_host = !on_device;  // unpacked to mapped host memory before the one sync
+    try {
+      run_integrate(L, va, *cfg, out);
+    } catch (...) {
+      out->want_host = false;
+      throw;
+    }
+    tr.mark("synced");
+    out->want_host = false;
     out->sorted_unique = true;
     if (!on_device) out->fetch();
+    tr.mark("fetched");
   });
 }
 
@@ -224,6 +287,15 @@ vxm_status frame_common(vxm_layer* T, vxm_layer* E, const float* depth, int w, i
 }
 
 }  // namespace
+
+namespace vxm {
+void host_trace_mark(const char* what) {
+  if (HostTrace::g_host_trace) HostTrace::g_host_trace->mark(what);
+}
+void host_trace_dev(Context* ctx, const char* what) {
+  if (HostTrace::g_host_trace) HostTrace::g_host_trace->dev_mark(ctx->stream, what);
+}
+}  // namespace vxm
 
 extern "C" {
 
@@ -609,6 +681,7 @@ vxm_status vxm_blocks_in_view_camera(vxm_context* ctx, const vxm_pose* T, const 
     VXM_CUDA(cudaMemcpyAsync(out->d_count, &ctx->d_status->n_candidates, sizeof(uint32_t),
                              cudaMemcpyDeviceToDevice, ctx->stream));
     out->host_valid = false;
+    out->host_pending = false;
     out->count_hint = n;
     out->sorted_unique = true;
     out->fetch();
@@ -645,6 +718,7 @@ vxm_status vxm_blocks_in_view_lidar(vxm_context* ctx, const vxm_pose* T, const v
     VXM_CUDA(cudaMemcpyAsync(out->d_count, &ctx->d_status->n_candidates, sizeof(uint32_t),
                              cudaMemcpyDeviceToDevice, ctx->stream));
     out->host_valid = false;
+    out->host_pending = false;
     out->count_hint = n;
     out->sorted_unique = true;
     out->fetch();
@@ -752,6 +826,7 @@ vxm_status vxm_shard_update_begin(vxm_layer* E, vxm_layer* T, vxm_blocklist* uni
                              x.ctx->stream));
     x.uni.count_hint = uni->count_hint;
     x.uni.host_valid = false;
+    x.uni.host_pending = false;
     x.uni.sorted_unique = true;
     shard_begin(x, *cfg);
     *any = x.local_any ? 1 : 0;
@@ -835,11 +910,19 @@ vxm_status vxm_update_esdf(vxm_layer* E, vxm_layer* T, const vxm_grid_index* upd
       ctx->scratch_in = new vxm_blocklist();
       ctx->scratch_in->ctx = ctx;
     }
+    HostTrace tr("update_esdf");
+    tr.dev_mark(ctx->stream, "start");
     vxm_blocklist* list = static_cast<vxm_blocklist*>(ctx->scratch_in);
     list->assign_host(updated, n);
+    tr.mark("assigned");
+    tr.dev_mark(ctx->stream, "h2d");
+    out->want_host = true;  // unpacked to mapped host memory before the one sync
     const vxm_status s = vxm_update_esdf_list(E, T, list, cfg, out);
+    out->want_host = false;
     if (s != VXM_OK) throw Error(s, g_err);
+    tr.mark("synced");
     out->fetch();
+    tr.mark("fetched");
   });
 }
 
@@ -1164,6 +1247,7 @@ vxm_status replay_common(vxm_context* ctx, const vxm_replay_config* cfg, const v
                                  ctx->stream));
         pending.count_hint = n_pending;
         pending.host_valid = false;
+        pending.host_pending = false;
         pending.sorted_unique = false;
         sort_unique_keys(ctx, &pending);
         pending.sorted_unique = true;

@@ -156,6 +156,7 @@ void run_integrate_color(Layer* C, Layer* T, const uint8_t* rgb_host, const View
                       ctx->d_status, "k_compact");
   work.count_hint = cand_cap;
   work.host_valid = false;
+  work.host_pending = false;
   work.sorted_unique = true;
   // get_or_allocate of the work blocks (integrator.cpp:226)
   DevBuf slots;
@@ -193,6 +194,7 @@ void run_integrate_color(Layer* C, Layer* T, const uint8_t* rgb_host, const View
                       "k_compact");
   changed_out->count_hint = cand_cap;
   changed_out->host_valid = false;
+  changed_out->host_pending = false;
   changed_out->sorted_unique = true;
   C->stage_meta();
   ctx->sync_status();

@@ -1226,7 +1226,9 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
                       n_all_cap, changed_out->keys.as<uint64_t>(), changed_out->d_count, nullptr,
                       "k_compact_esdf");
   changed_out->host_valid = false;
+  changed_out->host_pending = false;
   changed_out->count_hint = n_all_cap;
+  if (changed_out->want_host) changed_out->enqueue_host();  // host result, same sync
   ctx->queue_copy(s.counts + 0, &ctx->d_status->n_effective, 2);  // n_effective, n_esdf_new
   ctx->queue_copy(changed_out->d_count, &ctx->d_status->n_out);
 }
@@ -1260,6 +1262,8 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
   ctx->reset_status();
   esdf_launch(E, T, updated, cfg, changed_out);
   E->stage_meta();
+  host_trace_mark("launched");
+  host_trace_dev(ctx, "kernels");
   ctx->sync_status();
   E->adopt_meta();
   esdf_finish(E, changed_out);
@@ -1286,6 +1290,7 @@ static std::vector<vxm_grid_index> compact_to_host(Context* ctx, const uint64_t*
   tmp.ensure(std::max<uint32_t>(cap, 1));
   launch_compact_keys(ctx, keys, flags, n_ptr, cap, tmp.keys.as<uint64_t>(), tmp.d_count, nullptr);
   tmp.host_valid = false;
+  tmp.host_pending = false;
   return tmp.fetch();
 }
 

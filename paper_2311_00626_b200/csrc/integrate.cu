@@ -431,6 +431,7 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
     per_sm[occ] = std::max(per_sm[occ], 1);
   }
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * per_sm[occ]));
+  host_trace_dev(ctx, "dilate");
   ctx->prof_begin("k_integrate");
   if (occ)
     k_integrate<true><<<grid, 256, 0, ctx->stream>>>(a);
@@ -444,8 +445,10 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
                       &ctx->d_status->n_candidates, cand_cap, changed_out->keys.as<uint64_t>(),
                       changed_out->d_count, ctx->d_status, "k_compact");
   changed_out->host_valid = false;
+  changed_out->host_pending = false;
   // changed blocks are distinct allocated blocks: bounded by the pool too
   changed_out->count_hint = std::min<uint32_t>(cand_cap, L->capacity);
+  if (changed_out->want_host) changed_out->enqueue_host();  // host result, same sync
   ctx->queue_copy(changed_out->d_count, &ctx->d_status->n_changed);
   return cand_cap;
 }
@@ -482,6 +485,8 @@ void run_integrate(Layer* L, const ViewArgs& va, const vxm_integrator_config& cf
     const uint32_t nb_before = L->num_blocks;
     integrate_launch(L, va, cfg, changed_out);
     L->stage_meta();
+    host_trace_mark("launched");
+    host_trace_dev(ctx, "kernels");
     ctx->sync_status();
     L->adopt_meta();
     if (integrate_finish(L, va, changed_out, nb_before)) return;

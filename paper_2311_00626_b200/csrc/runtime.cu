@@ -292,8 +292,45 @@ void BlockList::ensure(uint32_t n) {
   }
 }
 
+__global__ void k_emit_host(const uint64_t* __restrict__ keys, const uint32_t* n_ptr,
+                            vxm_grid_index* out, uint32_t* out_n, uint32_t cap) {
+  const uint32_t n = min(*n_ptr, cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_n = n;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    out[i] = vxm_grid_index{key_x(k), key_y(k), key_z(k)};
+  }
+}
+
+void BlockList::enqueue_host() {
+  const uint32_t need = std::max<uint32_t>(count_hint, 1);
+  if (need > mapped_cap) {
+    if (mapped) VXM_CUDA(cudaFreeHost(mapped));
+    mapped_cap = std::max<uint32_t>(need, 4096);
+    VXM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mapped), sizeof(vxm_grid_index) * mapped_cap,
+                           cudaHostAllocMapped));
+  }
+  if (!mapped_count)
+    VXM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mapped_count), sizeof(uint32_t), cudaHostAllocMapped));
+  const uint32_t grid = std::min<uint32_t>(ceil_div(need, 256), uint32_t(ctx->sm_count));
+  k_emit_host<<<std::max<uint32_t>(grid, 1), 256, 0, ctx->stream>>>(keys.as<uint64_t>(), d_count, mapped,
+                                                                    mapped_count, mapped_cap);
+  ctx->count_launch();
+  check_launch(ctx, "k_emit_host");
+  host_pending = true;
+}
+
 const std::vector<vxm_grid_index>& BlockList::fetch() {
   if (host_valid) return host;
+  if (host_pending) {  // unpacked by k_emit_host into mapped memory
+    VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint32_t n = *mapped_count;
+    host.assign(mapped, mapped + n);
+    host_pending = false;
+    host_valid = true;
+    count_hint = n;
+    return host;
+  }
   uint32_t n = 0;
   if (d_count) {
     VXM_CUDA(cudaMemcpyAsync(&n, d_count, sizeof n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -314,7 +351,15 @@ const std::vector<vxm_grid_index>& BlockList::fetch() {
 
 void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
   ensure(uint32_t(std::max<uint64_t>(n, 1)));
-  staging.resize(n + 1);
+  host_pending = false;
+  if (n + 1 > staging_cap) {
+    if (staging) {
+      VXM_CUDA(cudaStreamSynchronize(ctx->stream));  // a previous upload may still read it
+      VXM_CUDA(cudaFreeHost(staging));
+    }
+    staging_cap = std::max<uint64_t>(n + 1, 4096);
+    VXM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&staging), sizeof(uint64_t) * staging_cap));
+  }
   bool sorted = true;
   for (uint64_t i = 0; i < n; ++i) {
     if (!coord_ok(data[i].x) || !coord_ok(data[i].y) || !coord_ok(data[i].z))
@@ -324,11 +369,12 @@ void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
   }
   staging[n] = n;  // count travels in the same copy (low 32 bits)
   const uint32_t n32 = uint32_t(n);
-  VXM_CUDA(cudaMemcpyAsync(keys.p, staging.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
+  VXM_CUDA(cudaMemcpyAsync(keys.p, staging, sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
                            ctx->stream));
   VXM_CUDA(cudaMemcpyAsync(d_count, &staging[n], sizeof(uint32_t), cudaMemcpyHostToDevice,
                            ctx->stream));
-  // staging stays alive (member) until the next assign, so no sync is needed here
+  // staging (pinned) stays alive until the next assign; calls that reuse the
+  // list synchronise the stream before returning
   host.assign(data, data + n);
   host_valid = true;
   count_hint = n32;
@@ -336,6 +382,10 @@ void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
 }
 
 BlockList::~BlockList() {
+  if (ctx && (staging || mapped)) cudaStreamSynchronize(ctx->stream);
+  if (staging) cudaFreeHost(staging);
+  if (mapped) cudaFreeHost(mapped);
+  if (mapped_count) cudaFreeHost(mapped_count);
   keys.release();
   if (d_count) cudaFree(d_count);
 }
@@ -365,6 +415,7 @@ void sort_unique_keys(Context* ctx, BlockList* list) {
   ctx->count_launch(3);
   check_launch(ctx, "sort_unique_keys");
   list->host_valid = false;
+  list->host_pending = false;
 }
 
 // Sorted (key, slot) export of a TSDF layer (sorted_indices, layer.hpp:109-117).

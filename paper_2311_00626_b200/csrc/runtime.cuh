@@ -163,7 +163,19 @@ struct BlockList {
   std::vector<vxm_grid_index> host;
   bool host_valid = true;
   bool sorted_unique = false;  // keys are in strictly increasing GridIndex order
-  std::vector<uint64_t> staging;  // host staging of assign_host (kept alive for async copies)
+  // pinned host staging of assign_host (alive until the next assign, so the
+  // upload is a true async DMA)
+  uint64_t* staging = nullptr;
+  uint64_t staging_cap = 0;
+  // Host-bound results: the producer enqueues enqueue_host() before its one
+  // status sync; a kernel unpacks the list into mapped pinned memory, so
+  // fetch() needs no further round trip.
+  bool want_host = false;
+  bool host_pending = false;
+  vxm_grid_index* mapped = nullptr;  // cudaHostAllocMapped, mapped_cap entries
+  uint32_t* mapped_count = nullptr;
+  uint32_t mapped_cap = 0;
+  void enqueue_host();
   void ensure(uint32_t n);
   const std::vector<vxm_grid_index>& fetch();   // sync + download + unpack
   void assign_host(const vxm_grid_index* data, uint64_t n);  // upload (sorted as given)
@@ -226,5 +238,7 @@ void run_query(Layer* E, const double* xyz_host, uint64_t n, int want_gradient, 
 void sort_unique_keys(Context* ctx, BlockList* list);  // device sort + unique (CUB)
 void layer_export_sorted(Layer* L, std::vector<uint64_t>* keys, std::vector<int32_t>* slots);
 void check_launch(Context* ctx, const char* what);
+void host_trace_mark(const char* what);  // capi.cu (VXM_TRACE_HOST)
+void host_trace_dev(Context* ctx, const char* what);
 
 }  // namespace vxm

@@ -477,6 +477,7 @@ void shard_finish(ShardUpdate& x, bool lowered, BlockList* out) {
   launch_compact_keys(x.ctx, x.E->sorted_keys[x.E->sorted_parity], x.s.flags, &x.E->meta->num_blocks,
                       x.n_all_cap, out->keys.as<uint64_t>(), out->d_count, nullptr, "k_compact_esdf");
   out->host_valid = false;
+  out->host_pending = false;
   out->count_hint = x.n_all_cap;
   out->sorted_unique = true;
   x.E->stage_meta();
@@ -542,6 +543,7 @@ void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
     VXM_CUDA(cudaMemcpyAsync(x.uni.d_count, &t32, sizeof t32, cudaMemcpyHostToDevice, x.ctx->stream));
     x.uni.count_hint = t32;
     x.uni.host_valid = false;
+    x.uni.host_pending = false;
     sort_unique_keys(x.ctx, &x.uni);
     x.uni.sorted_unique = true;
     shard_begin(x, cfg);

@@ -439,6 +439,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
   DevBuf& other = ctx->bitmap[bp ^ 1];
   const uint64_t other_words = other.bytes / 4;
 
+  host_trace_dev(ctx, "memset");
   if (!a.lidar) {
     const int tile = std::max(1, a.cfg.pixel_subsample);
     const int nt = ((a.width + tile - 1) / tile) * ((a.height + tile - 1) / tile);
@@ -480,6 +481,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
   }
   const uint32_t tiles = ceil_div(n_words, 256);
   const ScanTiles st = ctx->next_scan(tiles);
+  host_trace_dev(ctx, "rays");
   ctx->prof_begin("k_dilate_alloc");
   k_dilate_alloc<<<tiles, 256, 0, ctx->stream>>>(cube, uint32_t(n_words), al, ctx->rank, ctx->world,
                                                  ctx->slab, ctx->cand_keys.as<uint64_t>(),
