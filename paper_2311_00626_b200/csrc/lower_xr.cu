@@ -33,10 +33,6 @@ namespace vxm {
 namespace {
 
 constexpr int kRingCnt = 0, kRingSwc = 4, kRingPc = 8, kRingDone = 12, kRingLast = 16;
-#ifndef XR_R1_CHUNK
-#define XR_R1_CHUNK 1
-#endif
-constexpr uint32_t kR1Chunk = XR_R1_CHUNK;
 
 // Lines of a block through the voxels of one face (bit i0 + 8 j0 of F) that a
 // pair along `axis` changed; `face` is the face's coordinate (0 or 7).  The
@@ -265,17 +261,13 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
       const uint32_t n_items = 3u * per_axis;
       uint32_t my_done = 0;
       // one item per claim: a warp blocked on a dependency must not hold later
-      // items (measured on C2: chunks of 4 / 16 in round 1 cost 2 % / 34 %)
-      const uint32_t chunk = r1 ? kR1Chunk : 1u;
-      uint32_t w = 0, w_end = 0;
+      // items (measured on C2: chunks of 4 / 16 in round 1 cost 2 % / 34 %;
+      // prefetching the next claim during the current item costs 4 %)
       while (true) {
-        if (w == w_end) {
-          if (lane == 0) w = atomicAdd(ring + kRingPc + q4, chunk);
-          w = __shfl_sync(0xffffffffu, w, 0);
-          w_end = w + chunk;
-        }
-        if (w >= n_items) break;
-        const uint32_t wi = w++;
+        uint32_t wi = 0;
+        if (lane == 0) wi = atomicAdd(ring + kRingPc + q4, 1u);
+        wi = __shfl_sync(0xffffffffu, wi, 0);
+        if (wi >= n_items) break;
         const int axis = int(wi / per_axis);
         const uint32_t rest = wi - uint32_t(axis) * per_axis;
         const uint32_t i = r1 ? rest : rest >> 1;
@@ -384,6 +376,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
             unsigned long long tm;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
             a.trace[R] = tm;
+            a.trace[64 + R] = n_dirty;
           }
           __threadfence();
           st_release(ring + kRingLast, R);
@@ -430,8 +423,8 @@ void launch_lower_xr(Context* ctx, LowerArgs& la) {
   static const bool trace = std::getenv("VXM_TRACE_XR") != nullptr;
   static DevBuf trace_buf;
   if (trace) {
-    trace_buf.ensure(64 * sizeof(unsigned long long));
-    VXM_CUDA(cudaMemsetAsync(trace_buf.p, 0, 64 * sizeof(unsigned long long), ctx->stream));
+    trace_buf.ensure(128 * sizeof(unsigned long long));
+    VXM_CUDA(cudaMemsetAsync(trace_buf.p, 0, 128 * sizeof(unsigned long long), ctx->stream));
     la.trace = trace_buf.as<unsigned long long>();
   }
   static int grid = 0;
@@ -447,11 +440,11 @@ void launch_lower_xr(Context* ctx, LowerArgs& la) {
   ctx->prof_end();
   ctx->count_launch();
   if (trace) {
-    unsigned long long h[64];
+    unsigned long long h[128];
     VXM_CUDA(cudaMemcpyAsync(h, trace_buf.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     VXM_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::fprintf(stderr, "[k_lower_xr] round ends (us):");
-    for (int r = 1; r < 64 && h[r]; ++r) std::fprintf(stderr, " %.1f", (h[r] - h[0]) * 1e-3);
+    std::fprintf(stderr, "[k_lower_xr] round ends (us) / dirty blocks:");
+    for (int r = 1; r < 64 && h[r]; ++r) std::fprintf(stderr, " %.1f/%llu", (h[r] - h[0]) * 1e-3, h[64 + r]);
     std::fprintf(stderr, "\n");
     la.trace = nullptr;
   }

@@ -1,15 +1,22 @@
 #!/bin/bash
-# ncu evidence for profiles/: launch lists (per-launch durations) of the C2
+# ncu evidence for profiles/: the launch list (per-launch durations) of the C2
 # bench command, and one --set full capture per dominant kernel and config.
 set -x
 mkdir -p gpurun_out
 NCU="ncu --clock-control none"
 $NCU --metrics gpu__time_duration.sum -c 600 --csv --log-file gpurun_out/launches_c2.csv \
   python bench.py --steps 4 --warmup 3 --no-cpu-baseline > gpurun_out/launches_c2.log 2>&1
-$NCU --set full --import-source on -k regex:k_lower3 --launch-skip 5 --launch-count 1 -f -o gpurun_out/c2_lower python tools/frames.py c2 7 > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:k_integrate --launch-skip 5 --launch-count 1 -f -o gpurun_out/c2_integrate python tools/frames.py c2 7 > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:k_mark --launch-skip 5 --launch-count 1 -f -o gpurun_out/c2_mark python tools/frames.py c2 7 > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:k_lower3 --launch-skip 2 --launch-count 1 -f -o gpurun_out/c5_lower python tools/c5_steps.py 3 > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:k_integrate --launch-skip 4 --launch-count 1 -f -o gpurun_out/c3_integrate python tools/frames.py c3 6 > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:k_lower3 --launch-skip 4 --launch-count 1 -f -o gpurun_out/c3_lower python tools/frames.py c3 6 > /dev/null 2>&1
+full() {  # name regex skip script args...
+  local name=$1 rx=$2 skip=$3; shift 3
+  $NCU --set full --import-source on -k regex:$rx --launch-skip $skip --launch-count 1 -f \
+    -o gpurun_out/$name "$@" > /dev/null 2>&1
+}
+full c2_lower k_lower 5 python tools/frames.py c2 7
+full c2_integrate k_integrate 5 python tools/frames.py c2 7
+full c2_mark k_mark 5 python tools/frames.py c2 7
+full c2_rays k_rays 5 python tools/frames.py c2 7
+full c2_dilate k_dilate 5 python tools/frames.py c2 7
+full c3_integrate k_integrate 4 python tools/frames.py c3 6
+full c3_lower k_lower 4 python tools/frames.py c3 6
+full c5_lower k_lower 2 python tools/c5_steps.py 3
 ls -la gpurun_out/*.ncu-rep
