@@ -57,7 +57,7 @@ def main():
                 br = rd * scale.get(units.get("dram__bytes_read.sum"), 1)
                 bw = wr * scale.get(units.get("dram__bytes_write.sum"), 1)
                 # keyed by the bench's per-kernel timing names
-                traffic.setdefault(cfg, {})[{"k_lower3": "k_lower"}.get(kern, kern)] = int(br + bw)
+                traffic.setdefault(cfg, {})[{"k_lower3": "k_lower", "k_lower_xr": "k_lower"}.get(kern, kern)] = int(br + bw)
     out = os.path.join(ROOT, "profiles", f"{tag}_ncu_full_summary.csv")
     with open(out, "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=list(summary[0].keys()))
@@ -70,7 +70,7 @@ def main():
     for d in summary:
         print(d["config"], d["kernel"], "dur", d["gpu__time_duration.sum"], d["gpu__time_duration.sum.unit"],
               "dram%", d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"],
-              "traffic", traffic[d["config"]].get({"k_lower3": "k_lower"}.get(d["kernel"], d["kernel"])))
+              "traffic", traffic[d["config"]].get({"k_lower3": "k_lower", "k_lower_xr": "k_lower"}.get(d["kernel"], d["kernel"])))
 
 
 if __name__ == "__main__":
