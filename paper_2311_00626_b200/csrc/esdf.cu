@@ -1102,16 +1102,17 @@ void launch_lower_xr(Context* ctx, LowerArgs& la);  // lower_xr.cu
 
 // The cross-round kernel removes the per-round barrier and overlaps rounds:
 // a win while rounds are latency-bound (maps of up to tens of thousands of
-// blocks, e.g. C2: 0.26 -> 0.18 ms).  Very large maps are throughput-bound
-// (thousands of dirty blocks per group-round), where the per-block dependency
-// waits cost more than the barrier: they keep the barrier schedule.
+// blocks, e.g. C2: 0.26 -> 0.18 ms), and, with the current dataflow, also on
+// the throughput-bound large maps (k_lower on C3 / C4 / C5: -1 / -2 / -2 %),
+// so it is the default for every map (VXM_LOWER_XROUND=1 keeps the barrier
+// schedule above kXrMaxBlocks, 0 always).
 constexpr uint32_t kXrMaxBlocks = 48 * 1024;
 
 static void launch_lower(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
   static const bool trace = std::getenv("VXM_TRACE_LOWER") != nullptr;
   static const int xround = [] {
     const char* e = std::getenv("VXM_LOWER_XROUND");  // 0 never, 1 by map size, 2 always
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   if (la.full && la.dataflow && !trace &&  // (VXM_TRACE_LOWER traces k_lower3)
       (xround == 2 || (xround == 1 && n_blocks_hint <= kXrMaxBlocks))) {  // update_esdf

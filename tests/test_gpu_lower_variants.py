@@ -1,6 +1,6 @@
 """Every lowering kernel the library may select is bit-identical to the
-oracle: the cross-round kernel (k_lower_xr, maps up to kXrMaxBlocks), the
-barrier-per-round dataflow kernel (k_lower3, larger maps) and its phased form
+oracle: the cross-round kernel (k_lower_xr, the default for every map), the
+barrier-per-round dataflow kernel (k_lower3, VXM_LOWER_XROUND=0/1) and its phased form
 (grid barrier before every border axis).  The selection is process-wide, so
 each variant runs tests/lower_variant_check.py in its own process."""
 import os
