@@ -242,7 +242,9 @@ def run_ours(args, rank, world, device):
     esdf_ms = sum(kernels[k]["ms_total"] for k in ESDF_KERNELS if k in kernels) / K
 
     # ---- e2e: public host API, host buffers, copies inside the timed region --
-    pinned = [torch.from_numpy(d).pin_memory() for _, d in frames]
+    # frames staged in page-locked buffers (vxm_host_alloc, full-rate DMA)
+    pinned_bufs = [vx.pinned_like(np.ascontiguousarray(d, np.float32)) for _, d in frames]
+    pinned = [torch.from_numpy(b.array) for b in pinned_bufs]
     del Tp, Ep
     T2 = vx.TsdfLayer(c["vs"], ctx=ctx)
     E2 = vx.EsdfLayer(c["vs"], ctx=ctx) if ecfg else None

@@ -226,6 +226,13 @@ vxm_status vxm_blocks_in_view_lidar(vxm_context* ctx, const vxm_pose* T_LS, cons
                                     const float* depth, int width, int height, double block_size,
                                     const vxm_view_config* cfg, vxm_blocklist* out);
 
+/* ---- page-locked host buffers ------------------------------------------- */
+/* Host memory the DMA engines read at full PCIe rate (cudaHostAlloc), for
+ * depth / color frames handed to the host-buffer entry points (any host
+ * pointer works; pageable or differently registered memory uploads slower). */
+vxm_status vxm_host_alloc(uint64_t bytes, void** out);
+void vxm_host_free(void* p);
+
 /* ---- depth integration (integrate/integrator.hpp:36-55) ----------------- */
 /* integrate_depth(Layer<TsdfVoxel>&, DepthImage, Pose T_LS, CameraIntrinsics,
  * IntegratorConfig) — integrator.cpp:162-168; with an occupancy layer, the

@@ -14,4 +14,4 @@ from .voxmap import (BlockList, CameraIntrinsics, Context, EsdfConfig, EsdfLayer
                      IoError, save_snapshot, load_snapshot, update_esdf_sharded,
                      make_replay_config, replay, write_timing_csv, OccupancyLayer,
                      ColorLayer, MeshLayer, MeshBlock, integrate_color, mesh_block, update_mesh,
-                     save_mesh_ply, replay_cake)
+                     save_mesh_ply, replay_cake, HostBuffer, pinned_like)

@@ -455,6 +455,17 @@ void vxm_context_reset_kernel_times(vxm_context* ctx) {
   if (ctx) ctx->ktime.clear();
 }
 
+vxm_status vxm_host_alloc(uint64_t bytes, void** out) {
+  return guard([&] {
+    REQUIRE_ARG(out, "null argument");
+    *out = nullptr;
+    VXM_CUDA(cudaHostAlloc(out, std::max<uint64_t>(bytes, 1), cudaHostAllocDefault));
+  });
+}
+void vxm_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 vxm_status vxm_blocklist_create(vxm_context* ctx, vxm_blocklist** out) {
   return guard([&] {
     auto* l = new vxm_blocklist();

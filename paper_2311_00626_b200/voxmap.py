@@ -420,6 +420,32 @@ class MeshLayer:
         check(lib().vxm_mesh_layer_erase(self.h, A.ptr(A.as_keys([g]))))
 
 
+class HostBuffer:
+    """Page-locked host buffer (vxm_host_alloc) viewed as a numpy array: frames
+    staged here upload at full PCIe rate through the host-buffer entry points."""
+
+    def __init__(self, shape, dtype=np.float32):
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        check(lib().vxm_host_alloc(C.c_uint64(self.nbytes), C.byref(p)))
+        self._p = p
+        buf = (C.c_ubyte * max(self.nbytes, 1)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def __del__(self):
+        try:
+            lib().vxm_host_free(self._p)
+        except Exception:
+            pass
+
+
+def pinned_like(a):
+    """A page-locked copy of array `a` (HostBuffer); keep the buffer alive."""
+    hb = HostBuffer(a.shape, a.dtype)
+    hb.array[...] = a
+    return hb
+
+
 def _color(rgb):
     c = np.ascontiguousarray(rgb, dtype=np.uint8)
     if c.ndim != 3 or c.shape[2] != 3:

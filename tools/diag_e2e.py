@@ -13,7 +13,11 @@ import paper_2311_00626_b200 as vx  # noqa: E402
 
 N = 24
 sensor, frames, icfg, ecfg = bench.make_inputs("c2", N)
-pinned = [torch.from_numpy(d).pin_memory() for _, d in frames]
+if os.environ.get("DIAG_TORCH_PIN") == "1":
+    pinned = [torch.from_numpy(d).pin_memory() for _, d in frames]
+else:
+    pinned_bufs = [vx.pinned_like(np.ascontiguousarray(d, np.float32)) for _, d in frames]
+    pinned = [torch.from_numpy(b.array) for b in pinned_bufs]
 ctx = vx.default_context()
 ext = torch.cuda.ExternalStream(ctx.stream)
 T = vx.TsdfLayer(0.02)
