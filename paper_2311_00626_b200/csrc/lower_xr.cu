@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
           ring[kRingCnt + q4nn] = 0u;
           ring[kRingSwc + q4nn] = ring[kRingPc + q4nn] = ring[kRingDone + q4nn] = 0u;
           if (R > 1) a.status->sum_dirty += n_dirty;
-          if (a.trace && R < 64) {  // VXM_TRACE_XR: round completion times
+          if (a.trace && R < 62) {  // VXM_TRACE_XR: round completion times
             unsigned long long tm;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
             a.trace[R] = tm;
@@ -387,6 +387,11 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
     }
   }
   grid.sync();
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long tm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+    a.trace[62] = tm;
+  }
   // ---- changed set of update_esdf (esdf/integrator.cpp:403-411) ------------------
   for (uint32_t k = wid; k < n_blocks; k += nwarps) {
     const int32_t s = a.sorted_slots[k];
@@ -395,11 +400,16 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
       const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(s) * 1536);
       const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(s) * 1536);
       bool diff = false;
-#pragma unroll 4
-      for (int q = lane; q < 384; q += 32) {
-        const uint4 x = __ldcg(p0 + q), y = __ldcg(p1 + q);
-        diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+      // all 24 loads of the lane in flight at once (the phase is latency-bound)
+      uint4 x[12], y[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) {
+        x[q] = __ldcg(p0 + lane + 32 * q);
+        y[q] = __ldcg(p1 + lane + 32 * q);
       }
+#pragma unroll
+      for (int q = 0; q < 12; ++q)
+        diff |= (x[q].x != y[q].x) | (x[q].y != y[q].y) | (x[q].z != y[q].z) | (x[q].w != y[q].w);
       ch = __any_sync(0xffffffffu, diff);
       ++n_cmp;
     }
@@ -411,6 +421,11 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
   }
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.trace) {
+      unsigned long long tm;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+      a.trace[63] = tm;
+    }
     a.r1[0] = a.r1[1] = a.r1[2] = a.r1[3] = 0u;  // zero for the next launch
     a.status->rounds = rounds;
     a.status->n_esdf_blocks = n_blocks;
@@ -444,7 +459,9 @@ void launch_lower_xr(Context* ctx, LowerArgs& la) {
     VXM_CUDA(cudaMemcpyAsync(h, trace_buf.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     VXM_CUDA(cudaStreamSynchronize(ctx->stream));
     std::fprintf(stderr, "[k_lower_xr] round ends (us) / dirty blocks:");
-    for (int r = 1; r < 64 && h[r]; ++r) std::fprintf(stderr, " %.1f/%llu", (h[r] - h[0]) * 1e-3, h[64 + r]);
+    for (int r = 1; r < 62 && h[r]; ++r) std::fprintf(stderr, " %.1f/%llu", (h[r] - h[0]) * 1e-3, h[64 + r]);
+    if (h[62] && h[63])
+      std::fprintf(stderr, " | lowered %.1f, compared %.1f", (h[62] - h[0]) * 1e-3, (h[63] - h[0]) * 1e-3);
     std::fprintf(stderr, "\n");
     la.trace = nullptr;
   }
