@@ -141,12 +141,24 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
           }
           RawBlock rb;
           bool any_site, fast;
+          unsigned long long tm0 = 0, tm1 = 0;
+          if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm0));
           load_raw3(rb, pcur + size_t(s) * 1536, t, bar, lim, true, &any_site, &fast);
           if (!any_site) {
             raw_store(rb, work + size_t(s) * 1536, t);
           } else {
             stage_block3(G, rb, t, bar, lim, fast);
-            sweep_block3(G, t, bar, lim);
+            int passes = 0;
+            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm1));
+            sweep_block3(G, t, bar, lim, &passes);
+            if (a.trace && t == 0) {  // VXM_TRACE_XR: round-1 sweep statistics
+              unsigned long long tm2;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm2));
+              atomicAdd(a.trace + 54, tm1 - tm0);
+              atomicAdd(a.trace + 55, tm2 - tm1);
+              atomicAdd(a.trace + 56, (unsigned long long)passes);
+              atomicAdd(a.trace + 57, 1ull);
+            }
             store_block3(G, work + size_t(s) * 1536, t);
           }
           group_sync(bar);
@@ -167,6 +179,11 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
           warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
           __syncwarp();
           if (lane == 0) st_release(a.stamp_swept + s, ep);
+        }
+        if (a.trace && lane == 0) {  // VXM_TRACE_XR: end of the round-1 sweeps / copies
+          unsigned long long tm;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+          atomicMax(a.trace + 60, tm);
         }
       } else {
         const unsigned long long* dl = a.dlist[cp];
@@ -282,7 +299,16 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
           hi = d;
           if (lo >= 0 && is_dirty(lo)) lo = -1;  // lo's side-0 item has this pair
         }
-        if (lo >= 0 && hi >= 0) {
+        // round 1: whether a side can give is known before any wait (after the
+        // reset only sites give); the loads are issued ahead of the waits
+        const bool site_lo = r1 && lo >= 0 && a.site_any[lo] != 0;
+        const bool site_hi = r1 && hi >= 0 && a.site_any[hi] != 0;
+        if (lo >= 0 && hi >= 0 && r1 && axis == 0 && !site_lo && !site_hi) {
+          // identity x pair of round 1 (no giver on either face, no lower axis):
+          // released without waiting — every reader of lo / hi also waits for
+          // the blocks' own sweep stamps, or for a non-identity pair that did
+          if (lane == 0) st_release(a.stamp_pair[0] + lo, ep);
+        } else if (lo >= 0 && hi >= 0) {
           bool dep_chg = false;
           if (lane < 2 + 4 * axis) {
             if (lane < 2) {
@@ -309,8 +335,8 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
           bool skip = false;
           if (r1) {  // no giver on either face: the pair is the identity (k_lower3)
             constexpr uint32_t lo_lanes = 0x0ccu, hi_lanes = 0x330u;
-            const bool g_lo = a.site_any[lo] != 0 || (chg_mask & lo_lanes) != 0u;
-            const bool g_hi = a.site_any[hi] != 0 || (chg_mask & hi_lanes) != 0u;
+            const bool g_lo = site_lo || (chg_mask & lo_lanes) != 0u;
+            const bool g_hi = site_hi || (chg_mask & hi_lanes) != 0u;
             skip = !g_lo && !g_hi;
           }
           if (skip) {
@@ -372,7 +398,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
           ring[kRingCnt + q4nn] = 0u;
           ring[kRingSwc + q4nn] = ring[kRingPc + q4nn] = ring[kRingDone + q4nn] = 0u;
           if (R > 1) a.status->sum_dirty += n_dirty;
-          if (a.trace && R < 62) {  // VXM_TRACE_XR: round completion times
+          if (a.trace && R < 54) {  // VXM_TRACE_XR: round completion times
             unsigned long long tm;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
             a.trace[R] = tm;
@@ -425,6 +451,8 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
       unsigned long long tm;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
       a.trace[63] = tm;
+      a.trace[58] = a.r1[0];  // round-1 blocks with sites (swept) / without (copied)
+      a.trace[59] = a.r1[1];
     }
     a.r1[0] = a.r1[1] = a.r1[2] = a.r1[3] = 0u;  // zero for the next launch
     a.status->rounds = rounds;
@@ -459,7 +487,11 @@ void launch_lower_xr(Context* ctx, LowerArgs& la) {
     VXM_CUDA(cudaMemcpyAsync(h, trace_buf.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     VXM_CUDA(cudaStreamSynchronize(ctx->stream));
     std::fprintf(stderr, "[k_lower_xr] round ends (us) / dirty blocks:");
-    for (int r = 1; r < 62 && h[r]; ++r) std::fprintf(stderr, " %.1f/%llu", (h[r] - h[0]) * 1e-3, h[64 + r]);
+    for (int r = 1; r < 54 && h[r]; ++r) std::fprintf(stderr, " %.1f/%llu", (h[r] - h[0]) * 1e-3, h[64 + r]);
+    if (h[60]) std::fprintf(stderr, " | r1 sweeps %.1f (%llu swept, %llu copied)", (h[60] - h[0]) * 1e-3, h[58], h[59]);
+    if (h[57])
+      std::fprintf(stderr, " | r1 sweep: load+stage %.2f us, sweep %.2f us, %.2f passes", h[54] * 1e-3 / h[57],
+                   h[55] * 1e-3 / h[57], double(h[56]) / h[57]);
     if (h[62] && h[63])
       std::fprintf(stderr, " | lowered %.1f, compared %.1f", (h[62] - h[0]) * 1e-3, (h[63] - h[0]) * 1e-3);
     std::fprintf(stderr, "\n");
