@@ -165,6 +165,15 @@ __device__ inline uint32_t unpack_a(unsigned long long v) { return uint32_t(v >>
 __device__ inline uint32_t unpack_b(unsigned long long v) { return uint32_t(v) & 0x7fffffffu; }
 
 // ---- misc --------------------------------------------------------------------
+// Programmatic dependent launch (PDL): the kernels of the per-frame chain are
+// launched with programmatic stream serialization (launch_pdl), so a kernel's
+// CTAs are dispatched while its predecessor drains.  Every such kernel calls
+// pdl_wait() before touching memory (it returns once the predecessor has
+// completed and flushed) and pdl_trigger() to let its own successor launch.
+// Both are no-ops in a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 #define VXM_CUDA(call)                                                             \
   do {                                                                             \
     cudaError_t e_ = (call);                                                       \

@@ -448,6 +448,8 @@ __device__ inline uint64_t shift7(uint64_t k, int j, int sign) {
 
 __global__ void k_merge7(const uint64_t* __restrict__ upd, const uint32_t* n_ptr,
                          uint64_t* __restrict__ merged) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   const uint32_t n = *n_ptr;
   const uint32_t total = 7u * n;
   for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < total;
@@ -603,6 +605,8 @@ __global__ void __launch_bounds__(256) k_effective_alloc(const uint64_t* __restr
                                                          int32_t* __restrict__ eff_tslot,
                                                          uint32_t* n_eff, AllocListArgs a,
                                                          ScanTiles st) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   __shared__ uint32_t s_tile, s_scan[64], s_pre[2], s_base;
   scan_prepare_next(st);
   const uint32_t n = 7u * (*n_upd);
@@ -780,6 +784,8 @@ __device__ inline bool occ_has_free_neighbour(const float* src, int32_t self, co
 // ballots.
 template <bool OCC>
 __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   const uint32_t n = *a.n_eff;
   uint32_t* pool = a.pools[a.meta->cur];
   const int lane = threadIdx.x & 31;
@@ -1021,7 +1027,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   const uint32_t n7 = 7u * nu_cap;
   const uint64_t* upd = updated->keys.as<uint64_t>();
   ctx->prof_begin("k_merge7");
-  k_merge7<<<grid_for(ctx, n7), 256, 0, ctx->stream>>>(upd, updated->d_count, s.merged);
+  launch_pdl(ctx->stream, k_merge7, dim3(grid_for(ctx, n7)), dim3(256), 0, upd, updated->d_count, s.merged);
   ctx->prof_end();
   ctx->count_launch();
   {
@@ -1041,7 +1047,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
     al.status = ctx->d_status;
     const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
     ctx->prof_begin("k_effective_alloc");
-    k_effective_alloc<<<grid_for(ctx, n7, 4), 256, 0, ctx->stream>>>(
+    launch_pdl(ctx->stream, k_effective_alloc, dim3(grid_for(ctx, n7, 4)), dim3(256), 0, 
         s.merged, updated->d_count, T->hash, s.eff_keys, s.eff_tslot, s.counts + 0, al, st);
     ctx->prof_end();
     ctx->count_launch();
@@ -1079,9 +1085,9 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
     mark_per_sm[occ] = std::max(mark_per_sm[occ], 1);
   }
   if (occ)
-    k_mark<true><<<ctx->sm_count * mark_per_sm[occ], 256, 0, ctx->stream>>>(m);
+    launch_pdl(ctx->stream, k_mark<true>, dim3(ctx->sm_count * mark_per_sm[occ]), dim3(256), 0, m);
   else
-    k_mark<false><<<ctx->sm_count * mark_per_sm[occ], 256, 0, ctx->stream>>>(m);
+    launch_pdl(ctx->stream, k_mark<false>, dim3(ctx->sm_count * mark_per_sm[occ]), dim3(256), 0, m);
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "esdf mark phase");

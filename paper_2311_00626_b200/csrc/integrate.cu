@@ -219,6 +219,8 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<O
 // the register-unbounded build).
 template <bool OCC, bool FASTCAM>
 __global__ void __launch_bounds__(256, FASTCAM ? 4 : 3) k_integrate(IntegrateArgs a) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   using Ops = VoxOps<OCC>;
   using V = typename Ops::V;
   const DevStatus* st = a.status_ro;
@@ -330,6 +332,8 @@ __global__ void __launch_bounds__(256) k_compact_keys(const uint64_t* __restrict
                                                       const uint32_t* n_ptr, uint64_t* out,
                                                       uint32_t* n_out, ScanTiles st,
                                                       const DevStatus* guard) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_scan[64];
   __shared__ uint32_t s_pre;
@@ -376,7 +380,7 @@ void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
   const ScanTiles st = ctx->next_scan(tiles_cap);
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_cap, ctx->sm_count * 4));
   ctx->prof_begin(prof_name);
-  k_compact_keys<<<grid, 256, 0, ctx->stream>>>(in, flags, n_ptr, out, n_out, st, guard);
+  launch_pdl(ctx->stream, k_compact_keys, dim3(grid), dim3(256), 0, in, flags, n_ptr, out, n_out, st, guard);
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "k_compact_keys");
@@ -440,7 +444,7 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * per_sm[kv]));
   host_trace_dev(ctx, "dilate");
   ctx->prof_begin("k_integrate");
-  kern<<<grid, 256, 0, ctx->stream>>>(a);
+  launch_pdl(ctx->stream, kern, dim3(grid), dim3(256), 0, a);
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "k_integrate");

@@ -62,6 +62,11 @@ ScanTiles Context::next_scan(uint32_t tiles) {
   return st;
 }
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("VXM_NO_PDL") == nullptr;
+  return on;
+}
+
 void Context::reset_status() {
   status_copies.clear();  // (copies queued by an operation that threw are dropped)
   VXM_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), stream));
@@ -72,6 +77,8 @@ struct WordCopies {
   int n;
 };
 __global__ void k_copy_words(WordCopies c) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x < c.n) *c.dst[threadIdx.x] = *c.src[threadIdx.x];
 }
 void Context::flush_copies() {
@@ -82,7 +89,7 @@ void Context::flush_copies() {
       c.src[c.n] = status_copies[i].src;
       c.dst[c.n] = status_copies[i].dst;
     }
-    k_copy_words<<<1, 32, 0, stream>>>(c);
+    launch_pdl(stream, k_copy_words, dim3(1), dim3(32), 0, c);
     count_launch();
   }
   status_copies.clear();
@@ -294,6 +301,8 @@ void BlockList::ensure(uint32_t n) {
 
 __global__ void k_emit_host(const uint64_t* __restrict__ keys, const uint32_t* n_ptr,
                             vxm_grid_index* out, uint32_t* out_n, uint32_t cap) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t n = min(*n_ptr, cap);
   if (blockIdx.x == 0 && threadIdx.x == 0) *out_n = n;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -313,8 +322,9 @@ void BlockList::enqueue_host() {
   if (!mapped_count)
     VXM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mapped_count), sizeof(uint32_t), cudaHostAllocMapped));
   const uint32_t grid = std::min<uint32_t>(ceil_div(need, 256), uint32_t(ctx->sm_count));
-  k_emit_host<<<std::max<uint32_t>(grid, 1), 256, 0, ctx->stream>>>(keys.as<uint64_t>(), d_count, mapped,
-                                                                    mapped_count, mapped_cap);
+  launch_pdl(ctx->stream, k_emit_host, dim3(std::max<uint32_t>(grid, 1)), dim3(256), 0,
+             keys.as<const uint64_t>(), static_cast<const uint32_t*>(d_count), mapped, mapped_count,
+             mapped_cap);
   ctx->count_launch();
   check_launch(ctx, "k_emit_host");
   host_pending = true;

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <map>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -185,6 +186,28 @@ struct BlockList {
 struct EsdfState {
   std::vector<vxm_grid_index> lists[3];
 };
+
+// Launch with programmatic stream serialization (see pdl_wait in common.cuh);
+// VXM_NO_PDL=1 falls back to plain launches.
+bool pdl_enabled();
+template <typename... P, typename... A>
+inline void launch_pdl(cudaStream_t s, void (*k)(P...), dim3 g, dim3 b, size_t smem, A&&... args) {
+  if (!pdl_enabled()) {
+    k<<<g, b, smem, s>>>(std::forward<A>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VXM_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...));
+}
 
 // ---- drivers (implemented in the kernel TUs) ----------------------------------
 // view.cu — candidate blocks; when `alloc` != null the candidates are also

@@ -146,6 +146,8 @@ __device__ inline double ray_reach(double depth, double max_int, double trunc) {
 __global__ void k_rays_camera(const float* __restrict__ depth, int W, int H, int tile,
                               vxm_camera cam, vxm_pose T, double cs, double max_int, double trunc,
                               Cube cube, DevStatus* status) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   const int tiles_x = (W + tile - 1) / tile;
   const int tiles_y = (H + tile - 1) / tile;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -186,6 +188,8 @@ __global__ void k_rays_camera(const float* __restrict__ depth, int W, int H, int
 __global__ void k_rays_lidar(const float* __restrict__ depth, int W, int H,
                              const double* __restrict__ dirs, vxm_pose T, double cs,
                              double max_int, double trunc, Cube cube, DevStatus* status) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= W * H) return;
   const float d = __ldg(depth + p);
@@ -254,6 +258,8 @@ __global__ void __launch_bounds__(kDilThreads) k_dilate_alloc(Cube cube, uint32_
                                                               DevStatus* status, ScanTiles st,
                                                               uint32_t* __restrict__ clear_bits,
                                                               uint32_t clear_words) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_scan[64];
   __shared__ uint32_t s_pre[2];
@@ -446,7 +452,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
     if (nt > 0) {
       ctx->prof_begin("k_rays");
       // 32 threads per CTA: the rays are serial DDAs, so spread them over all SMs
-      k_rays_camera<<<ceil_div(nt, 32), 32, 0, ctx->stream>>>(
+      launch_pdl(ctx->stream, k_rays_camera, dim3(ceil_div(nt, 32)), dim3(32), 0, 
           a.depth_dev, a.width, a.height, tile, a.cam, a.T_LS, cs,
           a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
       ctx->prof_end();
@@ -457,7 +463,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
     const int np = a.width * a.height;
     if (np > 0) {
       ctx->prof_begin("k_rays");
-      k_rays_lidar<<<ceil_div(np, 64), 64, 0, ctx->stream>>>(
+      launch_pdl(ctx->stream, k_rays_lidar, dim3(ceil_div(np, 64)), dim3(64), 0, 
           a.depth_dev, a.width, a.height, ctx->lidar_dirs.as<double>(), a.T_LS, cs,
           a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
       ctx->prof_end();
@@ -483,7 +489,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
   const ScanTiles st = ctx->next_scan(tiles);
   host_trace_dev(ctx, "rays");
   ctx->prof_begin("k_dilate_alloc");
-  k_dilate_alloc<<<tiles, 256, 0, ctx->stream>>>(cube, uint32_t(n_words), al, ctx->rank, ctx->world,
+  launch_pdl(ctx->stream, k_dilate_alloc, dim3(tiles), dim3(256), 0, cube, uint32_t(n_words), al, ctx->rank, ctx->world,
                                                  ctx->slab, ctx->cand_keys.as<uint64_t>(),
                                                  ctx->cand_slots.as<int32_t>(), ctx->d_status, st,
                                                  other.as<uint32_t>(), uint32_t(other_words));
