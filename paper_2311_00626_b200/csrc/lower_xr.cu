@@ -69,6 +69,8 @@ __device__ inline unsigned long long ld_relaxed64(const unsigned long long* p) {
 }  // namespace
 
 __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
+  pdl_wait();  // see launch_pdl
+  pdl_trigger();
   cg::grid_group grid = cg::this_grid();
   __shared__ GroupSmem s_grp[kL3Groups];
   const int g = threadIdx.x >> 6, t = threadIdx.x & 63, lane = threadIdx.x & 31;
@@ -478,8 +480,23 @@ void launch_lower_xr(Context* ctx, LowerArgs& la) {
   }
   void* args[] = {&la};
   ctx->prof_begin("k_lower");
-  VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lower_xr, dim3(grid), dim3(kL3Threads), args, 0,
-                                       ctx->stream));
+  if (pdl_enabled()) {  // cooperative + programmatic serialization (see launch_pdl)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kL3Threads);
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    VXM_CUDA(cudaLaunchKernelEx(&cfg, k_lower_xr, la));
+  } else {
+    VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lower_xr, dim3(grid), dim3(kL3Threads), args, 0,
+                                         ctx->stream));
+  }
   ctx->prof_end();
   ctx->count_launch();
   if (trace) {
