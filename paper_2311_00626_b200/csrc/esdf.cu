@@ -1104,7 +1104,7 @@ static int lower_grid(Context* ctx) {
   return cached;
 }
 
-void launch_lower_xr(Context* ctx, LowerArgs& la);  // lower_xr.cu
+bool launch_lower_xr(Context* ctx, LowerArgs& la);  // lower_xr.cu: true when it compacted
 
 // The cross-round kernel removes the per-round barrier and overlaps rounds:
 // a win while rounds are latency-bound (maps of up to tens of thousands of
@@ -1114,7 +1114,8 @@ void launch_lower_xr(Context* ctx, LowerArgs& la);  // lower_xr.cu
 // schedule above kXrMaxBlocks, 0 always).
 constexpr uint32_t kXrMaxBlocks = 48 * 1024;
 
-static void launch_lower(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
+// Returns whether the kernel also wrote the changed list (la.out_keys).
+static bool launch_lower(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
   static const bool trace = std::getenv("VXM_TRACE_LOWER") != nullptr;
   static const int xround = [] {
     const char* e = std::getenv("VXM_LOWER_XROUND");  // 0 never, 1 by map size, 2 always
@@ -1122,8 +1123,7 @@ static void launch_lower(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
   }();
   if (la.full && la.dataflow && !trace &&  // (VXM_TRACE_LOWER traces k_lower3)
       (xround == 2 || (xround == 1 && n_blocks_hint <= kXrMaxBlocks))) {  // update_esdf
-    launch_lower_xr(ctx, la);
-    return;
+    return launch_lower_xr(ctx, la);
   }
   static DevBuf trace_buf;
   if (trace) {
@@ -1167,6 +1167,7 @@ static void launch_lower(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
     }
   }
   ctx->count_launch();
+  return false;
 }
 
 LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
@@ -1226,12 +1227,15 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
   la.stamp_mark = E->stamp_mark;
   la.call_epoch = epoch;
   la.out_flags = s.flags;
-  launch_lower(ctx, la, E->num_blocks);
-  check_launch(ctx, "k_lower");
   changed_out->ensure(n_all_cap);
-  launch_compact_keys(ctx, E->sorted_keys[E->sorted_parity], s.flags, &E->meta->num_blocks,
-                      n_all_cap, changed_out->keys.as<uint64_t>(), changed_out->d_count, nullptr,
-                      "k_compact_esdf");
+  la.sorted_keys = E->sorted_keys[E->sorted_parity];
+  la.out_keys = changed_out->keys.as<uint64_t>();
+  la.out_n = changed_out->d_count;
+  if (!launch_lower(ctx, la, E->num_blocks))  // the cross-round kernel compacts in-kernel
+    launch_compact_keys(ctx, E->sorted_keys[E->sorted_parity], s.flags, &E->meta->num_blocks,
+                        n_all_cap, changed_out->keys.as<uint64_t>(), changed_out->d_count, nullptr,
+                        "k_compact_esdf");
+  check_launch(ctx, "k_lower");
   changed_out->host_valid = false;
   changed_out->host_pending = false;
   changed_out->count_hint = n_all_cap;

@@ -475,6 +475,11 @@ struct LowerArgs {
   uint32_t call_epoch;
   uint32_t lchg_tag;
   uint8_t* out_flags;
+  // k_lower_xr: the changed list itself (sorted keys -> ordered compaction), or null
+  const uint64_t* sorted_keys;
+  uint64_t* out_keys;
+  uint32_t* out_n;
+  uint32_t* cta_cnt;  // [grid] per-CTA changed counts (scratch)
   unsigned long long* trace;  // optional phase timestamps (VXM_TRACE_LOWER)
   uint32_t* work_ctr;         // [4] dynamic scheduling counters (sweeps, pairs) by parity
   unsigned long long* line_mask;  // [cap][3] lines touched by the last border phase

@@ -421,7 +421,16 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
     a.trace[62] = tm;
   }
   // ---- changed set of update_esdf (esdf/integrator.cpp:403-411) ------------------
-  for (uint32_t k = wid; k < n_blocks; k += nwarps) {
+  // Each CTA compares a contiguous chunk of the sorted order (one warp per
+  // block); with out_keys the CTA then writes its changed keys at its prefix
+  // over the CTAs' counts — the ordered compaction, without another launch.
+  __shared__ uint32_t s_cnt, s_pre, s_wsum[kL3Threads / 32];
+  const uint32_t chunk = (n_blocks + gridDim.x - 1) / gridDim.x;
+  const uint32_t k0 = min(n_blocks, blockIdx.x * chunk), k1 = min(n_blocks, k0 + chunk);
+  const int warp_in_cta = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_cnt = 0u;
+  __syncthreads();
+  for (uint32_t k = k0 + warp_in_cta; k < k1; k += kL3Threads / 32) {
     const int32_t s = a.sorted_slots[k];
     bool ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
     if (!ch && lower) {
@@ -441,11 +450,46 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
       ch = __any_sync(0xffffffffu, diff);
       ++n_cmp;
     }
-    if (lane == 0) a.out_flags[k] = uint8_t(ch);
+    if (lane == 0) {
+      a.out_flags[k] = uint8_t(ch);
+      if (ch) atomicAdd(&s_cnt, 1u);
+    }
   }
   if (lane == 0 && (n_pairs | n_cmp)) {
     atomicAdd(&a.status->sum_pairs, n_pairs);
     atomicAdd(&a.status->cmp_blocks, n_cmp);
+  }
+  __syncthreads();
+  if (a.out_keys && threadIdx.x == 0) a.cta_cnt[blockIdx.x] = s_cnt;
+  if (a.out_keys) {
+    grid.sync();
+    if (threadIdx.x < 32) {  // prefix over the CTAs before this one
+      uint32_t sum = 0;
+      for (uint32_t c = lane; c < blockIdx.x; c += 32) sum += __ldcg(a.cta_cnt + c);
+      sum = __reduce_add_sync(0xffffffffu, sum);
+      if (lane == 0) {
+        s_pre = sum;
+        if (blockIdx.x == gridDim.x - 1) *a.out_n = sum + s_cnt;
+      }
+    }
+    __syncthreads();
+    uint32_t base = s_pre;
+    for (uint32_t t0 = k0; t0 < k1; t0 += kL3Threads) {  // this CTA's flags, in order
+      const uint32_t k = t0 + threadIdx.x;
+      const bool f = k < k1 && a.out_flags[k] != 0;
+      const uint32_t m = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s_wsum[warp_in_cta] = __popc(m);
+      __syncthreads();
+      uint32_t off = base, tile = 0;
+      for (int w = 0; w < kL3Threads / 32; ++w) {
+        const uint32_t c = s_wsum[w];
+        if (w < warp_in_cta) off += c;
+        tile += c;
+      }
+      if (f) a.out_keys[off + __popc(m & ((1u << lane) - 1u))] = a.sorted_keys[k];
+      base += tile;
+      __syncthreads();
+    }
   }
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -464,7 +508,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_lower_xr(LowerArgs a) {
   }
 }
 
-void launch_lower_xr(Context* ctx, LowerArgs& la) {
+bool launch_lower_xr(Context* ctx, LowerArgs& la) {
   static const bool trace = std::getenv("VXM_TRACE_XR") != nullptr;
   static DevBuf trace_buf;
   if (trace) {
@@ -478,6 +522,8 @@ void launch_lower_xr(Context* ctx, LowerArgs& la) {
     VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lower_xr, kL3Threads, 0));
     grid = std::max(1, std::min(bps, 4)) * ctx->sm_count;
   }
+  ctx->lower_cta.ensure(sizeof(uint32_t) * grid);  // per-CTA counts of the in-kernel compaction
+  la.cta_cnt = ctx->lower_cta.as<uint32_t>();
   void* args[] = {&la};
   ctx->prof_begin("k_lower");
   if (pdl_enabled()) {  // cooperative + programmatic serialization (see launch_pdl)
@@ -514,6 +560,7 @@ void launch_lower_xr(Context* ctx, LowerArgs& la) {
     std::fprintf(stderr, "\n");
     la.trace = nullptr;
   }
+  return la.out_keys != nullptr;
 }
 
 }  // namespace vxm

@@ -60,6 +60,7 @@ struct Context {
   vxm_lidar lut_key{};
   bool lut_valid = false;
   DevBuf tmp[6];          // ESDF / list scratch
+  DevBuf lower_cta;       // k_lower_xr: per-CTA counts of the changed-list compaction
   DevBuf cub_tmp;
 
   // work counters and optional per-kernel event timing
