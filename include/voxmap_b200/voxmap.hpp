@@ -78,6 +78,68 @@ struct Vec3 {
   double operator[](int i) const { return i == 0 ? x : (i == 1 ? y : z); }
   bool operator==(const Vec3&) const = default;
 };
+
+// ---- index algebra (core/indexing.hpp:33-139) --------------
+struct VoxelIndex {  // voxel inside a block, 0..7 per axis
+  int32_t x = 0, y = 0, z = 0;
+  friend auto operator<=>(const VoxelIndex&, const VoxelIndex&) = default;
+};
+struct GlobalVoxelIndex {  // voxel in the whole map
+  int64_t x = 0, y = 0, z = 0;
+  friend auto operator<=>(const GlobalVoxelIndex&, const GlobalVoxelIndex&) = default;
+};
+// x-fastest linear index inside a block: x + 8 (y + 8 z)
+inline int linear_voxel_index(const VoxelIndex& v) {
+  return v.x + kVoxelsPerSide * (v.y + kVoxelsPerSide * v.z);
+}
+inline VoxelIndex voxel_index_from_linear(int lin) {
+  const int x = lin % kVoxelsPerSide, r = lin / kVoxelsPerSide;
+  return VoxelIndex{x, r % kVoxelsPerSide, r / kVoxelsPerSide};
+}
+// floor(a / 8), also for negative a
+inline int64_t floor_div_side(int64_t a) {
+  return a >= 0 ? a / kVoxelsPerSide : -((kVoxelsPerSide - 1 - a) / kVoxelsPerSide);
+}
+inline GlobalVoxelIndex global_voxel_index(const GridIndex& g, const VoxelIndex& v) {
+  return GlobalVoxelIndex{int64_t(g.x) * kVoxelsPerSide + v.x, int64_t(g.y) * kVoxelsPerSide + v.y,
+                          int64_t(g.z) * kVoxelsPerSide + v.z};
+}
+inline GridIndex block_of_global_voxel(const GlobalVoxelIndex& gv) {
+  return GridIndex{int32_t(floor_div_side(gv.x)), int32_t(floor_div_side(gv.y)),
+                   int32_t(floor_div_side(gv.z))};
+}
+inline VoxelIndex local_voxel_of_global(const GlobalVoxelIndex& gv) {
+  const GridIndex b = block_of_global_voxel(gv);
+  return VoxelIndex{int32_t(gv.x - int64_t(b.x) * kVoxelsPerSide), int32_t(gv.y - int64_t(b.y) * kVoxelsPerSide),
+                    int32_t(gv.z - int64_t(b.z) * kVoxelsPerSide)};
+}
+// global voxel containing a metric position: floor(p / voxel_size) per axis
+inline GlobalVoxelIndex position_to_global_voxel(const Vec3& p, double voxel_size) {
+  return GlobalVoxelIndex{int64_t(std::floor(p.x / voxel_size)), int64_t(std::floor(p.y / voxel_size)),
+                          int64_t(std::floor(p.z / voxel_size))};
+}
+inline void position_to_indices(const Vec3& p, double voxel_size, GridIndex* block, VoxelIndex* voxel) {
+  const GlobalVoxelIndex gv = position_to_global_voxel(p, voxel_size);
+  *block = block_of_global_voxel(gv);
+  *voxel = local_voxel_of_global(gv);
+}
+inline GridIndex position_to_block_index(const Vec3& p, double voxel_size) {
+  return block_of_global_voxel(position_to_global_voxel(p, voxel_size));
+}
+// voxel centre: ((8 g + v) + 0.5) * voxel_size, the reference's association
+inline Vec3 voxel_center(const GridIndex& g, const VoxelIndex& v, double voxel_size) {
+  return Vec3{(double(g.x) * kVoxelsPerSide + v.x + 0.5) * voxel_size,
+              (double(g.y) * kVoxelsPerSide + v.y + 0.5) * voxel_size,
+              (double(g.z) * kVoxelsPerSide + v.z + 0.5) * voxel_size};
+}
+inline Vec3 global_voxel_center(const GlobalVoxelIndex& gv, double voxel_size) {
+  return Vec3{(double(gv.x) + 0.5) * voxel_size, (double(gv.y) + 0.5) * voxel_size,
+              (double(gv.z) + 0.5) * voxel_size};
+}
+inline Vec3 block_origin(const GridIndex& g, double voxel_size) {
+  const double edge = kVoxelsPerSide * voxel_size;
+  return Vec3{g.x * edge, g.y * edge, g.z * edge};
+}
 struct TsdfVoxel {
   float distance = 0.0f;
   float weight = 0.0f;
@@ -107,6 +169,8 @@ static_assert(sizeof(TsdfVoxel) == sizeof(vxm_tsdf_voxel) && sizeof(EsdfVoxel) =
 template <typename V>
 struct VoxelBlock {
   std::array<V, kVoxelsPerBlock> voxels{};
+  V& voxel(const VoxelIndex& v) { return voxels[size_t(linear_voxel_index(v))]; }
+  const V& voxel(const VoxelIndex& v) const { return voxels[size_t(linear_voxel_index(v))]; }
 };
 
 template <typename V>
@@ -251,6 +315,15 @@ class Layer {
     }
     host_dirty_.push_back(g);
     return *it->second;
+  }
+  // voxel lookup by global voxel index; nullptr when the block is absent (layer.hpp:88-96)
+  const V* voxel_ptr(const GlobalVoxelIndex& gv) const {
+    const BlockType* b = block_ptr(block_of_global_voxel(gv));
+    return b ? &b->voxel(local_voxel_of_global(gv)) : nullptr;
+  }
+  V* voxel_ptr(const GlobalVoxelIndex& gv) {
+    BlockType* b = block_ptr(block_of_global_voxel(gv));
+    return b ? &b->voxel(local_voxel_of_global(gv)) : nullptr;
   }
   std::vector<GridIndex> sorted_indices() const {
     flush();

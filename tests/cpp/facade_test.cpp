@@ -51,7 +51,39 @@ static bool same_layer(const vb::Layer<V>& g, const vxo_layer* o) {
   return true;
 }
 
+// Index algebra KATs — core_test.cpp:30-71 (host inline, no device).
+static void index_kats() {
+  const double vs = 0.05;
+  vb::GridIndex g;
+  vb::VoxelIndex v;
+  vb::position_to_indices({0.0, 0.0, 0.0}, vs, &g, &v);
+  CHECK((g == vb::GridIndex{0, 0, 0}) && (v == vb::VoxelIndex{0, 0, 0}));
+  vb::position_to_indices({-0.01, 0.0, 0.0}, vs, &g, &v);
+  CHECK((g == vb::GridIndex{-1, 0, 0}) && (v == vb::VoxelIndex{7, 0, 0}));
+  vb::position_to_indices({0.43, 0.05, -0.40}, vs, &g, &v);
+  CHECK((g == vb::GridIndex{1, 0, -1}) && (v == vb::VoxelIndex{0, 1, 0}));
+  const vb::Vec3 c0 = vb::voxel_center({0, 0, 0}, {0, 0, 0}, vs);
+  CHECK(c0.x == 0.025 && c0.y == 0.025 && c0.z == 0.025);
+  const vb::Vec3 cn = vb::voxel_center({-1, 0, 0}, {7, 0, 0}, vs);
+  CHECK(cn.x == -0.025 && cn.y == 0.025 && cn.z == 0.025);
+  unsigned st = 7;
+  auto rnd = [&st](int lo, int hi) {
+    st = st * 1103515245u + 12345u;
+    return lo + int((st >> 8) % unsigned(hi - lo + 1));
+  };
+  for (int i = 0; i < 1000; ++i) {
+    const vb::GridIndex gg{rnd(-50, 50), rnd(-50, 50), rnd(-50, 50)};
+    const vb::VoxelIndex vv{rnd(0, 7), rnd(0, 7), rnd(0, 7)};
+    vb::position_to_indices(vb::voxel_center(gg, vv, vs), vs, &g, &v);
+    CHECK(g == gg && v == vv);
+    CHECK(vb::voxel_index_from_linear(vb::linear_voxel_index(vv)) == vv);
+    CHECK(vb::local_voxel_of_global(vb::global_voxel_index(gg, vv)) == vv);
+    CHECK(vb::block_of_global_voxel(vb::global_voxel_index(gg, vv)) == gg);
+  }
+}
+
 int main() {
+  index_kats();
   vxm_scene* scene = nullptr;
   vxm_synth_scene_create("sphere_in_box", &scene);
   vb::CameraIntrinsics cam;
@@ -217,6 +249,13 @@ int main() {
       CHECK(ea == oracle_list(ob, on));
     }
     CHECK(same_layer(occ, oocc));
+    {  // voxel_ptr (layer.hpp:88-96): the block's voxel or nullptr
+      const auto keys = occ.sorted_indices();
+      const vb::GlobalVoxelIndex gv = vb::global_voxel_index(keys.front(), {3, 4, 5});
+      const vb::OccupancyVoxel* p = occ.voxel_ptr(gv);
+      CHECK(p != nullptr && p == &occ.block_ptr(keys.front())->voxel({3, 4, 5}));
+      CHECK(occ.voxel_ptr(vb::GlobalVoxelIndex{1 << 24, 0, 0}) == nullptr);
+    }
     CHECK(same_layer(oesdf2, oe2));
     const std::string path = "/tmp/vxm_facade_test_occ.vxlf";
     vb::LayerCake cake(0.05);
