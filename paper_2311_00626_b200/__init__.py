@@ -14,4 +14,7 @@ from .voxmap import (BlockList, CameraIntrinsics, Context, EsdfConfig, EsdfLayer
                      IoError, save_snapshot, load_snapshot, update_esdf_sharded,
                      make_replay_config, replay, write_timing_csv, OccupancyLayer,
                      ColorLayer, MeshLayer, MeshBlock, integrate_color, mesh_block, update_mesh,
-                     save_mesh_ply, replay_cake, HostBuffer, pinned_like)
+                     save_mesh_ply, replay_cake, HostBuffer, pinned_like,
+                     linear_voxel_index, voxel_index_from_linear, global_voxel_index,
+                     block_of_global_voxel, local_voxel_of_global, position_to_global_voxel,
+                     position_to_indices, voxel_center, block_origin)

@@ -309,6 +309,11 @@ class _Layer:
         vox, found = self.read_blocks([g])
         return vox[0] if found[0] else None
 
+    def voxel(self, gv):
+        """voxel_ptr (layer.hpp:88-96): the voxel at a global voxel index, or None."""
+        blk = self.block(tuple(int(c) for c in block_of_global_voxel(gv)))
+        return None if blk is None else blk[int(linear_voxel_index(local_voxel_of_global(gv)))]
+
     def write_blocks(self, keys, voxels):
         """get_or_allocate + overwrite (host writes through block_ptr)."""
         k = A.as_keys(keys)
@@ -760,6 +765,52 @@ def query_batch(esdf: EsdfLayer, points, want_gradient: bool = False, interpolat
     check(lib().vxm_query_batch(esdf.h, A.ptr(x), C.c_uint64(len(x)), C.c_int(int(want_gradient)),
                                 C.byref(cfg), A.ptr(out)))
     return out
+
+
+# ---- index algebra (core/indexing.hpp:33-139), vectorised --
+def linear_voxel_index(v):
+    """x-fastest index inside a block: x + 8 (y + 8 z); v: (..., 3) ints."""
+    v = np.asarray(v)
+    return v[..., 0] + A.VOXELS_PER_SIDE * (v[..., 1] + A.VOXELS_PER_SIDE * v[..., 2])
+
+
+def voxel_index_from_linear(lin):
+    lin = np.asarray(lin)
+    n = A.VOXELS_PER_SIDE
+    return np.stack([lin % n, (lin // n) % n, lin // (n * n)], axis=-1)
+
+
+def global_voxel_index(g, v):
+    return np.asarray(g, np.int64) * A.VOXELS_PER_SIDE + np.asarray(v, np.int64)
+
+
+def block_of_global_voxel(gv):
+    """floor(gv / 8) per axis (floor_div_side, correct for negatives)."""
+    return np.floor_divide(np.asarray(gv, np.int64), A.VOXELS_PER_SIDE).astype(np.int32)
+
+
+def local_voxel_of_global(gv):
+    return np.mod(np.asarray(gv, np.int64), A.VOXELS_PER_SIDE).astype(np.int32)
+
+
+def position_to_global_voxel(p, voxel_size):
+    """floor(p / voxel_size) per axis (indexing.hpp:96-102)."""
+    return np.floor(np.asarray(p, np.float64) / voxel_size).astype(np.int64)
+
+
+def position_to_indices(p, voxel_size):
+    """(block index, voxel index) containing metric position(s) p."""
+    gv = position_to_global_voxel(p, voxel_size)
+    return block_of_global_voxel(gv), local_voxel_of_global(gv)
+
+
+def voxel_center(g, v, voxel_size):
+    """((8 g + v) + 0.5) * voxel_size, the reference's association (indexing.hpp:113-119)."""
+    return ((np.asarray(g, np.float64) * A.VOXELS_PER_SIDE + np.asarray(v)) + 0.5) * voxel_size
+
+
+def block_origin(g, voxel_size):
+    return np.asarray(g, np.float64) * (A.VOXELS_PER_SIDE * voxel_size)
 
 
 def esdf_distance(sq, inside, voxel_size):
