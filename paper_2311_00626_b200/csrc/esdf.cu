@@ -1104,7 +1104,7 @@ static int lower_grid(Context* ctx) {
   return cached;
 }
 
-bool launch_lower_xr(Context* ctx, LowerArgs& la);  // lower_xr.cu: true when it compacted
+bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint);  // lower_xr.cu: true when it compacted
 
 // The cross-round kernel removes the per-round barrier and overlaps rounds:
 // a win while rounds are latency-bound (maps of up to tens of thousands of
@@ -1123,7 +1123,7 @@ static bool launch_lower(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
   }();
   if (la.full && la.dataflow && !trace &&  // (VXM_TRACE_LOWER traces k_lower3)
       (xround == 2 || (xround == 1 && n_blocks_hint <= kXrMaxBlocks))) {  // update_esdf
-    return launch_lower_xr(ctx, la);
+    return launch_lower_xr(ctx, la, n_blocks_hint);
   }
   static DevBuf trace_buf;
   if (trace) {
