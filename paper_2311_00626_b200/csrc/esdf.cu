@@ -1199,6 +1199,7 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   }();
   la.dataflow = dataflow;
   for (int i = 0; i < 3; ++i) la.stamp_pair[i] = E->stamp_pair[i];
+  la.stamp_r1same = E->stamp_r1same;
   la.lim = limits_for(cfg, E->vs);
   la.status = E->ctx->d_status;
   return la;

@@ -485,6 +485,7 @@ struct LowerArgs {
   unsigned long long* line_mask;  // [cap][3] lines touched by the last border phase
   uint32_t* stamp_swept;      // [cap] round epoch when the block's sweep was stored
   uint32_t* stamp_pair[3];    // [cap] round epoch when pair (b, b + axis) was done
+  uint32_t* stamp_r1same;     // [cap] call epoch: the round-1 reset + copy left the block unchanged
   int dataflow;               // 1: pair items wait on dependencies; 0: phased barriers
   const uint8_t* site_any;    // [cap] 0: the block holds no site
   uint32_t* r1;               // [4] round-1 split: #site, #no-site, group / warp work counters
@@ -548,7 +549,8 @@ __device__ inline void store_voxel(uint32_t* pool, int32_t slot, int lin, const 
 // Round 1, block without sites: reset_parented (esdf/integrator.cpp:352-363)
 // leaves it without givers, so its sweep is the identity — one warp copies the
 // reset block to the work buffer (lane: voxels 4 * (lane + 32 h) .. + 3).
-__device__ inline void warp_reset_copy(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+// Returns (warp-uniform) whether the reset changed any voxel.
+__device__ inline bool warp_reset_copy(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                                        int lane, const Limits& lim) {
   const uint4* s4 = reinterpret_cast<const uint4*>(src);
   uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -563,11 +565,14 @@ __device__ inline void warp_reset_copy(const uint32_t* __restrict__ src, uint32_
       w[12 * h + 4 * j + 2] = v.z;
       w[12 * h + 4 * j + 3] = v.w;
     }
+  bool changed = false;
 #pragma unroll
   for (int v = 0; v < 16; ++v) {
     const uint32_t f = (w[3 * v + 2] >> 16) & 0xffu;
     if ((f & VXM_ESDF_OBSERVED) && !(f & VXM_ESDF_SITE) && ((w[3 * v + 1] | (w[3 * v + 2] & 0xffffu)) != 0u)) {
-      w[3 * v] = uint32_t((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq);
+      const uint32_t sq = uint32_t((f & VXM_ESDF_INSIDE) ? lim.cap_sq : lim.max_sq);
+      changed = true;  // a parented voxel: its offset is cleared
+      w[3 * v] = sq;
       w[3 * v + 1] = 0u;
       w[3 * v + 2] &= 0xffff0000u;
     }
@@ -578,6 +583,7 @@ __device__ inline void warp_reset_copy(const uint32_t* __restrict__ src, uint32_
     for (int j = 0; j < 3; ++j)
       __stcg(d4 + 3 * (lane + 32 * h) + j, make_uint4(w[12 * h + 4 * j], w[12 * h + 4 * j + 1],
                                                      w[12 * h + 4 * j + 2], w[12 * h + 4 * j + 3]));
+  return __any_sync(0xffffffffu, changed);
 }
 
 // ---- lowering v3: group-per-block sweeps with line masks --------------------------

@@ -182,9 +182,14 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           if (j >= n_ns) break;
           const int32_t s = __ldcg(a.list[1] + (n_blocks - 1u - j));
           ++j;
-          warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
+          const bool reset_chg = warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
           __syncwarp();
-          if (lane == 0) st_release(a.stamp_swept + s, ep);
+          if (lane == 0) {
+            // unchanged by round 1: if no later round writes it, the changed-set
+            // compare can skip it (every later writer marks it dirty)
+            if (!reset_chg) a.stamp_r1same[s] = a.call_epoch;
+            st_release(a.stamp_swept + s, ep);
+          }
         }
         if (a.trace && lane == 0) {  // VXM_TRACE_XR: end of the round-1 sweeps / copies
           unsigned long long tm;
@@ -437,7 +442,13 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
   for (uint32_t k = k0 + warp_in_cta; k < k1; k += kL3Threads / 32) {
     const int32_t s = a.sorted_slots[k];
     bool ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
-    if (!ch && lower) {
+    // a site-free block that round 1 copied unchanged and no later round wrote
+    // (every pair or sweep write after round 1 lists the block dirty, stamping
+    // it with an epoch of this launch above round 1's) is byte-identical
+    const bool late = a.stamp_dirty[0][s] > base_epoch + 1u || a.stamp_dirty[1][s] > base_epoch + 1u;
+    if (!ch && lower && !late && a.stamp_r1same[s] == a.call_epoch) {
+      // unchanged without reading the block
+    } else if (!ch && lower) {
       const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(s) * 1536);
       const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(s) * 1536);
       bool diff = false;

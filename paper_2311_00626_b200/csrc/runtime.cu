@@ -228,6 +228,7 @@ void Layer::ensure_capacity(uint64_t need) {
     for (int i = 0; i < 2; ++i) grow_copy(&dlist[i], capacity, 0, nc, 0, st);
     for (int i = 0; i < 3; ++i) grow_copy(&pair_face[i], capacity * 2ull, 0, nc * 2ull, 0, st);
     for (int a = 0; a < 3; ++a) grow_copy(&stamp_pair[a], capacity, live, nc, 0, st);
+    grow_copy(&stamp_r1same, capacity, live, nc, 0, st);
   }
   // hash: power of two >= 2 * capacity, rebuilt from slot_keys
   uint64_t hc = 1024;
@@ -284,6 +285,7 @@ Layer::~Layer() {
     if (p) cudaFree(p);
   for (uint32_t* p : stamp_pair)
     if (p) cudaFree(p);
+  if (stamp_r1same) cudaFree(stamp_r1same);
 }
 
 // ---- BlockList -----------------------------------------------------------------

@@ -134,6 +134,7 @@ struct Layer {
   uint32_t* stamp_swept = nullptr;          // round epoch of the block's last sweep
   uint8_t* site_any = nullptr;              // 0: the block holds no site (exact or conservative 1)
   uint32_t* stamp_pair[3] = {nullptr, nullptr, nullptr};  // round epoch of pair (b, b+axis)
+  uint32_t* stamp_r1same = nullptr;  // call epoch: round 1 left the block byte-identical
 
   // ESDF: while every block came from mark_sites against `subset_of`, the
   // block set is a subset of that TSDF layer's (so bounded by its capacity)
