@@ -7,8 +7,10 @@ integration) followed by update_esdf, for BASELINE config C2 by default
 
   value  device-resident frames/s: depth frames already in HBM, the changed
          block list stays on the device between integrate and ESDF.
-  e2e    the same frames through the public host API (host depth from pinned
-         memory copied in, changed lists copied out) — the reference-facing path.
+  e2e    the same frames through the public host API (vxm_integrate_depth_camera
+         + vxm_update_esdf: host depth from page-locked memory (vxm_host_alloc)
+         copied in, changed lists copied out each step) — the reference-facing
+         path.  N>1 runs N replicas (one independent map per GPU, weak scaling).
 
 Timing: W untimed warm-up frames, then K timed frames; before every timed
 frame a 256 MB buffer is written to flush L2; CUDA events on the library's
