@@ -237,7 +237,10 @@ vxm_status integrate_common(vxm_layer* L, const float* depth, int w, int h, cons
     tr.mark("synced");
     out->want_host = false;
     out->sorted_unique = true;
-    if (!on_device) out->fetch();
+    if (!on_device) {
+      out->fetch();
+      L->ctx->last_host_out = out;
+    }
     tr.mark("fetched");
   });
 }
@@ -924,7 +927,13 @@ vxm_status vxm_update_esdf(vxm_layer* E, vxm_layer* T, const vxm_grid_index* upd
     HostTrace tr("update_esdf");
     tr.dev_mark(ctx->stream, "start");
     vxm_blocklist* list = static_cast<vxm_blocklist*>(ctx->scratch_in);
-    list->assign_host(updated, n);
+    BlockList* last = ctx->last_host_out;
+    if (last && last != out && last->host_valid && last->sorted_unique && last->host.size() == n &&
+        (n == 0 || std::memcmp(last->host.data(), updated, sizeof(vxm_grid_index) * n) == 0)) {
+      list = static_cast<vxm_blocklist*>(last);  // the integrate's device keys, identical content
+    } else {
+      list->assign_host(updated, n);
+    }
     tr.mark("assigned");
     tr.dev_mark(ctx->stream, "h2d");
     out->want_host = true;  // unpacked to mapped host memory before the one sync

@@ -394,6 +394,7 @@ void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
 }
 
 BlockList::~BlockList() {
+  if (ctx && ctx->last_host_out == this) ctx->last_host_out = nullptr;
   if (ctx && (staging || mapped)) cudaStreamSynchronize(ctx->stream);
   if (staging) cudaFreeHost(staging);
   if (mapped) cudaFreeHost(mapped);

@@ -76,6 +76,10 @@ struct Context {
   const char* prof_name = nullptr;
   cudaEvent_t prof_a = nullptr;
   struct BlockList* scratch_in = nullptr;  // reused host-input list (C-ABI host paths)
+  // The changed list the last host-buffer integrate returned (device keys +
+  // host copy): an update_esdf on an identical host list reuses its device keys
+  // instead of uploading them again.  Cleared by the list's destructor.
+  struct BlockList* last_host_out = nullptr;
   // Deferred mode (fused frame update): drivers enqueue their work and leave
   // the status read, error checks and meta adoption to the caller's one sync.
   bool deferred = false;
