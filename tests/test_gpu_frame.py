@@ -95,3 +95,24 @@ def test_update_frame_rejects_before_mutation(vx):
         vx.update_frame_device(T, E, dd.data_ptr(), d.shape[1], d.shape[0], pose, cam, icfg, ecfg,
                                vx.BlockList(ctx), vx.BlockList(ctx))
     assert T.num_blocks() == 0
+
+
+def test_update_esdf_host_list_reuse_matches_oracle(vx, port):
+    """update_esdf on the host list the last integrate returned reuses its device
+    keys; an older (different) list is uploaded — both equal the oracle."""
+    from paper_2311_00626_b200 import _abi as A
+    from tests.helpers import camera_frames, layers_identical
+    cam, seq = camera_frames("sphere_in_box", 160, 120, 3, 8)
+    icfg = A.default_integrator_config(truncation=0.2)
+    ecfg = A.default_esdf_config(site_threshold=0.05)
+    T, E = vx.TsdfLayer(0.05), vx.EsdfLayer(0.05)
+    To, Eo = port.layer(A.LAYER_TSDF, 0.05), port.layer(A.LAYER_ESDF, 0.05)
+    lists = []
+    for pose, d in seq[:2]:
+        a = vx.integrate_depth(T, d, pose, cam, icfg)
+        assert np.array_equal(a, port.integrate_camera(To, d, pose, cam, icfg))
+        lists.append(a)
+    # stale list first (uploaded), then the last integrate's list (reused), then a subset
+    for u in (lists[0], lists[1], lists[1][: len(lists[1]) // 2]):
+        assert np.array_equal(vx.update_esdf(E, T, u, ecfg), port.update_esdf(Eo, To, u, ecfg))
+    assert layers_identical(*E.export(), *port.export(Eo))
