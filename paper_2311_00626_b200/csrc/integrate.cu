@@ -268,10 +268,23 @@ __global__ void __launch_bounds__(256, FASTCAM ? 4 : 3) k_integrate(IntegrateArg
         V ov[4];
         float dv[4];
         uint32_t live = 0;
+        // voxels j and j + 1 share z (j even): R(i, z) * c_z once per z
+        double Rz[2][3];
+#pragma unroll
+        for (int zi = 0; zi < 2; ++zi) {
+          const double cz = centre(gz, (j0 >> 1) + zi);
+          Rz[zi][0] = __dmul_rn(R[2], cz);
+          Rz[zi][1] = __dmul_rn(R[5], cz);
+          Rz[zi][2] = __dmul_rn(R[8], cz);
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          double px, py, pz;
-          centre_p(j0 + q, px, py, pz);
+          // p = (A_x + (A_y + R_z c_z)) + t — the pinned order of centre_p
+          const double* Ay = (q & 1) ? Ay1 : Ay0;
+          const double* rz = Rz[q >> 1];
+          const double pz = __dadd_rn(__dadd_rn(Ax[2], __dadd_rn(Ay[2], rz[2])), a.T_SL.t[2]);
+          const double px = __dadd_rn(__dadd_rn(Ax[0], __dadd_rn(Ay[0], rz[0])), a.T_SL.t[0]);
+          const double py = __dadd_rn(__dadd_rn(Ax[1], __dadd_rn(Ay[1], rz[1])), a.T_SL.t[1]);
           const int lin = lane + 32 * (j0 + q);
           sd[q] = 0.0f;
           ov[q] = Ops::zero();
