@@ -70,11 +70,24 @@ def log(*a):
 
 
 # ---------------------------------------------------------------------------
-def make_inputs(cfgname, n_frames, offset=0):
+def make_inputs(cfgname, n_frames, offset=0, ref=None):
+    """Scene, orbit poses and rendered frames of a config.  Our arm renders
+    with the product-side generator (libvoxmap_synth.so); the reference arm
+    passes `ref` (oracle/_ref) and renders with the reference's own
+    render_depth / orbit_pose, so it loads no library of ours (tests pin both
+    generators byte-identical: tests/test_abi.py)."""
     from paper_2311_00626_b200 import _abi as A
-    from paper_2311_00626_b200 import synth
     c = CONFIGS[cfgname]
-    S = synth.Scene(c["scene"])
+    lidar = c["sensor"] == "lidar"
+    if ref is None:
+        from paper_2311_00626_b200 import synth
+        S = synth.Scene(c["scene"])
+        pose = lambda k: S.orbit_pose(k, c["orbit"], lidar=lidar)  # noqa: E731
+        render = S.render_lidar if lidar else S.render_camera
+    else:
+        pose = lambda k: ref.orbit_pose(c["scene"], k, c["orbit"], lidar=lidar)  # noqa: E731
+        render = ((lambda T, s: ref.render_lidar(c["scene"], T, s)) if lidar
+                  else (lambda T, s: ref.render_camera(c["scene"], T, s)))
     if c["sensor"] == "camera":
         sensor = A.default_camera(c["w"], c["h"])
     else:
@@ -82,10 +95,8 @@ def make_inputs(cfgname, n_frames, offset=0):
         sensor.max_range = c["max_int"]
     frames = []
     for k in range(offset, offset + n_frames):
-        kk = k % c["orbit"]
-        T = S.orbit_pose(kk, c["orbit"], lidar=c["sensor"] == "lidar")
-        d = S.render_camera(T, sensor) if c["sensor"] == "camera" else S.render_lidar(T, sensor)
-        frames.append((T, d))
+        T = pose(k % c["orbit"])
+        frames.append((T, render(T, sensor)))
     icfg = A.default_integrator_config(truncation=c["trunc"], max_integration_distance=c["max_int"])
     ecfg = A.default_esdf_config(site_threshold=c["esdf"][0], max_distance=c["esdf"][1]) if c["esdf"] else None
     return sensor, frames, icfg, ecfg
@@ -327,7 +338,8 @@ def cpu_reference_run(cfgname, warmup, steps, budget_s=None):
     c = CONFIGS[cfgname]
     kind = "reference" if have_ref() else "port"
     o = RefOracle() if kind == "reference" else PortOracle()
-    sensor, frames, icfg, ecfg = make_inputs(cfgname, warmup + steps)
+    sensor, frames, icfg, ecfg = make_inputs(cfgname, warmup + steps,
+                                             ref=o if kind == "reference" else None)
     T = o.layer(A.LAYER_TSDF, c["vs"])
     E = o.layer(A.LAYER_ESDF, c["vs"]) if ecfg else None
     integ = o.integrate_camera if c["sensor"] == "camera" else o.integrate_lidar
@@ -370,10 +382,14 @@ def cpu_model():
 C5_SIDE = 512
 
 
-def c5_volumes(side=C5_SIDE):
-    from paper_2311_00626_b200 import synth
-    ka, va = synth.sphere_world(side, 0.02, 0.08, seed=2311)
-    kb, vb = synth.sphere_world(side, 0.02, 0.08, seed=2312)
+def c5_volumes(side=C5_SIDE, ref=None):
+    if ref is None:
+        from paper_2311_00626_b200 import synth
+        gen = synth.sphere_world
+    else:
+        gen = ref.sphere_world
+    ka, va = gen(side, 0.02, 0.08, seed=2311)
+    kb, vb = gen(side, 0.02, 0.08, seed=2312)
     assert np.array_equal(ka, kb)
     return ka, va, vb
 
@@ -454,7 +470,7 @@ def cpu_reference_c5(steps, side=C5_SIDE):
     from paper_2311_00626_b200 import _abi as A
     kind = "reference" if have_ref() else "port"
     o = RefOracle() if kind == "reference" else PortOracle()
-    keys, va, vb = c5_volumes(side)
+    keys, va, vb = c5_volumes(side, ref=o if kind == "reference" else None)
     Ts = [o.layer(A.LAYER_TSDF, 0.02), o.layer(A.LAYER_TSDF, 0.02)]
     o.write_blocks(Ts[0], keys, va)
     o.write_blocks(Ts[1], keys, vb)

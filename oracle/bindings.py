@@ -328,6 +328,16 @@ class RefOracle(_Base):
     def pose_valid(self, T):
         return bool(self.lib.vxr_pose_valid(C.byref(T)))
 
+    def sphere_world(self, side, vs, trunc, seed=2311, n_spheres=6):
+        """Dense C5 TSDF built by ref_driver.cpp (keys (nb^3,3), voxels (nb^3,512))."""
+        nb = side // 8
+        keys = np.zeros((nb ** 3, 3), np.int32)
+        vox = np.zeros((nb ** 3, A.VOXELS_PER_BLOCK), A.TSDF_DTYPE)
+        self._check(self.lib.vxr_sphere_world(C.c_int(side), C.c_double(vs), C.c_double(trunc),
+                                              C.c_uint(seed), C.c_int(n_spheres), A.ptr(keys),
+                                              A.ptr(vox)))
+        return keys, vox
+
     def brute_force_esdf(self, esdf, cfg):
         h = C.c_void_p()
         self._check(self.lib.vxr_brute_force_esdf(esdf.h, C.byref(cfg), C.byref(h)))

@@ -15,9 +15,14 @@
 //   query_batch / reference_query_batch
 //                              proj/src/query/query.cpp:147-161, reference.cpp:378-386
 //   render_depth / orbit_pose  proj/src/io/render.cpp:43-86, dataset.cpp:309-367
+//                              (+ builder scenes from the reference's primitives and the
+//                              C5 SphereWorld volume: the reference arm's inputs)
 //   brute_force_esdf / compare_esdf / esdf_identical
 //                              proj/src/eval/oracle.cpp:26-151
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <random>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -367,9 +372,103 @@ int vxr_query_batch(void* esdf, const double* xyz, uint64_t n, int want_gradient
 }
 
 // Scenes / rendering / trajectories (input generators of the reference).
+}  // extern "C"
+
+namespace {
+
+// Deterministic generator of the builder scenes (same stream as
+// paper_2311_00626_b200/csrc/synth.cpp; tests pin the rendered frames equal).
+struct SplitMix {
+  uint64_t s;
+  uint64_t next() {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  double uni(double a, double b) { return a + (b - a) * double(next() >> 11) * 0x1.0p-53; }
+};
+
+// add_room_shell (scene.cpp:31-41 is file-local, restated with the public make_plane)
+void room_shell(vr::SyntheticScene& sc, const Eigen::Vector3d& lo, const Eigen::Vector3d& hi) {
+  for (int axis = 0; axis < 3; ++axis) {
+    Eigen::Vector3d n = Eigen::Vector3d::Zero();
+    n[axis] = 1.0;
+    sc.primitives.push_back(vr::make_plane(lo, n));
+    sc.primitives.push_back(vr::make_plane(hi, -n));
+  }
+  sc.bbox_min = lo;
+  sc.bbox_max = hi;
+}
+
+// make_scene (scene.cpp:124-144) plus the builder scenes of configs the
+// reference has no scene for, assembled from the reference's own primitives
+// (make_box / make_sphere / make_plane, scene.cpp:56-102): "lidar_yard" (C3)
+// and "building" (C4).
+vr::SyntheticScene ref_scene(const std::string& name) {
+  if (name == "lidar_yard") {
+    vr::SyntheticScene sc;
+    sc.name = name;
+    sc.primitives.push_back(vr::make_plane({0, 0, 0}, {0, 0, 1}));
+    SplitMix rng{7};
+    int placed = 0;
+    while (placed < 40) {
+      const double cx = rng.uni(-95, 95), cy = rng.uni(-95, 95);
+      const double w = rng.uni(3, 15), d = rng.uni(3, 15), h = rng.uni(4, 20);
+      const double rr = std::sqrt(cx * cx + cy * cy);
+      if (std::abs(rr - 70.0) < 0.5 * std::max(w, d) + 4.0) continue;
+      sc.primitives.push_back(vr::make_box({cx - 0.5 * w, cy - 0.5 * d, 0.0}, {cx + 0.5 * w, cy + 0.5 * d, h}));
+      ++placed;
+    }
+    placed = 0;
+    while (placed < 8) {
+      const double cx = rng.uni(-90, 90), cy = rng.uni(-90, 90), r = rng.uni(1, 4);
+      if (std::abs(std::sqrt(cx * cx + cy * cy) - 70.0) < r + 4.0) continue;
+      sc.primitives.push_back(vr::make_sphere({cx, cy, r}, r));
+      ++placed;
+    }
+    sc.bbox_min = {-100, -100, 0};
+    sc.bbox_max = {100, 100, 3.6};
+    return sc;
+  }
+  if (name == "building") {
+    vr::SyntheticScene sc;
+    sc.name = name;
+    room_shell(sc, {0, 0, 0}, {24.0, 16.0, 3.0});
+    const double t = 0.15;
+    for (double x : {8.0, 16.0}) {
+      sc.primitives.push_back(vr::make_box({x - t, 0.0, 0.0}, {x + t, 3.5, 3.0}));
+      sc.primitives.push_back(vr::make_box({x - t, 4.7, 0.0}, {x + t, 11.3, 3.0}));
+      sc.primitives.push_back(vr::make_box({x - t, 12.5, 0.0}, {x + t, 16.0, 3.0}));
+    }
+    sc.primitives.push_back(vr::make_box({0.0, 8.0 - t, 0.0}, {2.5, 8.0 + t, 3.0}));
+    sc.primitives.push_back(vr::make_box({3.7, 8.0 - t, 0.0}, {10.5, 8.0 + t, 3.0}));
+    sc.primitives.push_back(vr::make_box({11.7, 8.0 - t, 0.0}, {18.5, 8.0 + t, 3.0}));
+    sc.primitives.push_back(vr::make_box({19.7, 8.0 - t, 0.0}, {24.0, 8.0 + t, 3.0}));
+    SplitMix rng{11};
+    for (int i = 0; i < 18; ++i) {
+      const int room = i % 6;
+      const double x0 = 8.0 * (room % 3), y0 = 8.0 * (room / 3);
+      const double cx = x0 + rng.uni(1.5, 6.5), cy = y0 + rng.uni(1.5, 6.5);
+      if (i % 3 == 2) {
+        sc.primitives.push_back(vr::make_sphere({cx, cy, 0.4}, 0.4));
+      } else {
+        const double w = rng.uni(0.4, 1.6), d = rng.uni(0.4, 1.2), h = rng.uni(0.5, 1.2);
+        sc.primitives.push_back(vr::make_box({cx - 0.5 * w, cy - 0.5 * d, 0.0}, {cx + 0.5 * w, cy + 0.5 * d, h}));
+      }
+    }
+    return sc;
+  }
+  return vr::make_scene(name);
+}
+
+}  // namespace
+
+extern "C" {
+
 int vxr_orbit_pose(const char* scene, int lidar, int k, int total, vxm_pose* out) {
   return guard([&] {
-    const auto sc = vr::make_scene(scene);
+    const auto sc = ref_scene(scene);
     from_pose(vr::orbit_pose(sc, lidar ? vr::SensorKind::kLidar : vr::SensorKind::kCamera, k, total),
               out);
   });
@@ -377,14 +476,48 @@ int vxr_orbit_pose(const char* scene, int lidar, int k, int total, vxm_pose* out
 int vxr_render_depth_camera(const char* scene, const vxm_pose* T, const vxm_camera* cam,
                             float* out) {
   return guard([&] {
-    const auto img = vr::render_depth(vr::make_scene(scene), to_pose(T), to_cam(cam));
+    const auto img = vr::render_depth(ref_scene(scene), to_pose(T), to_cam(cam));
     std::memcpy(out, img.data.data(), sizeof(float) * img.data.size());
   });
 }
 int vxr_render_depth_lidar(const char* scene, const vxm_pose* T, const vxm_lidar* li, float* out) {
   return guard([&] {
-    const auto img = vr::render_depth(vr::make_scene(scene), to_pose(T), to_lidar(li));
+    const auto img = vr::render_depth(ref_scene(scene), to_pose(T), to_lidar(li));
     std::memcpy(out, img.data.data(), sizeof(float) * img.data.size());
+  });
+}
+// SphereWorld-style dense TSDF of config C5 (tests/fixtures.hpp:34-98, the
+// add branch of random_edit): n spheres from std::mt19937(seed), distance =
+// float(clamp(min_i(|c - c_i| - r_i), +-trunc)) at each voxel centre
+// (indexing.hpp:113-119), weight 1; blocks in sorted (x-slowest) order.
+int vxr_sphere_world(int side, double vs, double trunc, unsigned seed, int n_spheres,
+                     vxm_grid_index* keys, vxm_tsdf_voxel* voxels) {
+  return guard([&] {
+    if (side <= 0 || side % 8) throw std::invalid_argument("sphere_world: side must be a multiple of 8");
+    const double E = side * vs;
+    std::mt19937 rng(seed);
+    std::uniform_real_distribution<double> pos(0.15 * E, 0.85 * E);
+    std::uniform_real_distribution<double> rad(0.08 * E, 0.25 * E);
+    std::vector<std::pair<Eigen::Vector3d, double>> sph;
+    for (int i = 0; i < n_spheres; ++i) {
+      const double cx = pos(rng), cy = pos(rng), cz = pos(rng);
+      sph.push_back({Eigen::Vector3d(cx, cy, cz), rad(rng)});
+    }
+    const int nb = side / 8;
+    const int64_t total = int64_t(nb) * nb * nb;
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < total; ++b) {
+      const vr::GridIndex g{int(b / (int64_t(nb) * nb)), int((b / nb) % nb), int(b % nb)};
+      if (keys) keys[b] = {g.x, g.y, g.z};
+      if (!voxels) continue;
+      for (int lin = 0; lin < 512; ++lin) {
+        const Eigen::Vector3d c = vr::voxel_center(g, vr::voxel_index_from_linear(lin), vs);
+        double d = 1e9;
+        for (const auto& s : sph) d = std::min(d, (c - s.first).norm() - s.second);
+        voxels[b * 512 + lin].distance = static_cast<float>(std::clamp(d, -trunc, trunc));
+        voxels[b * 512 + lin].weight = 1.0f;
+      }
+    }
   });
 }
 void vxr_default_camera(int w, int h, vxm_camera* out) {

@@ -1,13 +1,40 @@
 """Synthetic inputs (include/voxmap_b200_synth.h): scenes, orbit poses,
-sphere-traced depth frames, and the dense SphereWorld TSDF of config C5."""
+sphere-traced depth frames, and the dense SphereWorld TSDF of config C5.
+
+Test and bench input generation only: it lives in its own host library
+(_lib/libvoxmap_synth.so), not in the product library."""
 from __future__ import annotations
 
 import ctypes as C
+import os
+import threading
 
 import numpy as np
 
 from . import _abi as A
-from .voxmap import Pose, check, lib
+from .voxmap import Pose
+
+SYNTH_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libvoxmap_synth.so")
+_synth = None
+_synth_lock = threading.Lock()
+
+
+def lib():
+    """Loads libvoxmap_synth.so (the input generator)."""
+    global _synth
+    with _synth_lock:
+        if _synth is None:
+            if not os.path.exists(SYNTH_PATH):
+                raise ImportError(f"{SYNTH_PATH} missing: run __graft_entry__.build()")
+            L = C.CDLL(SYNTH_PATH)
+            L.vxm_synth_scene_sdf.restype = C.c_double
+            _synth = L
+        return _synth
+
+
+def check(rc):
+    if rc != A.VXM_OK:
+        raise ValueError(f"synthetic input generator failed (status {rc})")
 
 
 class Scene:

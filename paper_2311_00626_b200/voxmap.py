@@ -94,7 +94,6 @@ def lib():
             L.vxm_version.restype = C.c_char_p
             L.vxm_layer_voxel_size.restype = C.c_double
             L.vxm_context_launch_count.restype = C.c_uint64
-            L.vxm_synth_scene_sdf.restype = C.c_double
             L.vxm_pose_valid.restype = C.c_int
             _lib = L
         return _lib

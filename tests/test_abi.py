@@ -14,9 +14,9 @@ from paper_2311_00626_b200 import _abi as A
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_functions():
+def declared_functions(header="voxmap_b200.h"):
     names = set()
-    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+    for h in glob.glob(os.path.join(ROOT, "include", header)):
         text = open(h).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         for m in re.finditer(r"\b(vxm_[a-z0-9_]+)\s*\(", text):
@@ -30,6 +30,16 @@ def test_library_exports_every_declared_symbol(vx):
     assert len(names) > 40
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
+
+
+def test_synth_library_is_separate(vx):
+    """The input generator (voxmap_b200_synth.h) is its own library; the
+    product library exports none of it."""
+    from paper_2311_00626_b200 import synth
+    names = declared_functions("voxmap_b200_synth.h")
+    assert names and all(hasattr(synth.lib(), n) for n in names)
+    prod = open(os.path.join(ROOT, "paper_2311_00626_b200", "_lib", "libvoxmap_b200.so"), "rb").read()
+    assert not any(n.encode() in prod for n in names)
 
 
 def test_library_is_sm100a_only():
@@ -100,3 +110,28 @@ def test_synth_matches_reference_renderer(ref):
                 else:
                     cam = A.default_camera(160, 120)
                     assert S.render_camera(a, cam).tobytes() == ref.render_camera(scene, b, cam).tobytes()
+
+
+def test_builder_scenes_match_reference_primitives(ref):
+    """The builder scenes (C3 lidar_yard, C4 building) and the C5 SphereWorld
+    volume render identically through the product-side generator
+    (libvoxmap_synth.so) and through the reference's own primitives and
+    render_depth (oracle/_ref), so the bench's reference arm can take its
+    inputs from the reference build alone."""
+    from paper_2311_00626_b200 import synth
+    S = synth.Scene("building")
+    cam = A.default_camera(160, 120)
+    for k in (0, 37):
+        a, b = S.orbit_pose(k, 100), ref.orbit_pose("building", k, 100)
+        assert bytes(a) == bytes(b)
+        assert S.render_camera(a, cam).tobytes() == ref.render_camera("building", b, cam).tobytes()
+    S = synth.Scene("lidar_yard")
+    li = A.default_lidar(256, 16)
+    li.max_range = 100.0
+    for k in (0, 11):
+        a, b = S.orbit_pose(k, 100, lidar=True), ref.orbit_pose("lidar_yard", k, 100, lidar=True)
+        assert bytes(a) == bytes(b)
+        assert S.render_lidar(a, li).tobytes() == ref.render_lidar("lidar_yard", b, li).tobytes()
+    ka, va = synth.sphere_world(32, 0.02, 0.08, seed=5, n_spheres=4)
+    kb, vb = ref.sphere_world(32, 0.02, 0.08, seed=5, n_spheres=4)
+    assert np.array_equal(ka, kb) and va.tobytes() == vb.tobytes()
