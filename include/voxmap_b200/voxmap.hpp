@@ -240,8 +240,14 @@ class BlockList {
 
 // ---- Layer<V> — core/layer.hpp:47-125 ---------------------------------------------
 // Blocks live on the device.  Host reads (block_ptr/voxel_ptr/clone) sync a
-// lazy host mirror; blocks handed out through the non-const accessors are
-// uploaded again before the next device operation on the layer.
+// lazy host mirror whose block addresses never change (handles stay valid, as
+// layer.hpp:44-46 promises).  A block handed out through a non-const accessor
+// stays "writable" for the layer's lifetime: before every device operation
+// (and every mirror refresh) each writable block is compared with the bytes
+// last exchanged with the device; voxels the caller changed since are merged
+// into the device's current block voxel by voxel, so writes through a kept
+// handle persist across device operations exactly as writes into the
+// reference's host blocks do.
 template <typename V>
 class Layer {
  public:
@@ -268,7 +274,7 @@ class Layer {
     std::swap(max_blocks_, o.max_blocks_);
     std::swap(mirror_, o.mirror_);
     std::swap(mirror_valid_, o.mirror_valid_);
-    std::swap(host_dirty_, o.host_dirty_);
+    std::swap(writable_, o.writable_);
     return *this;
   }
 
@@ -301,7 +307,7 @@ class Layer {
     sync_mirror();
     auto it = mirror_.find(g);
     if (it == mirror_.end()) return nullptr;
-    host_dirty_.push_back(g);
+    make_writable(g, *it->second);
     return it->second.get();
   }
   BlockType& get_or_allocate(const GridIndex& g) {
@@ -313,7 +319,7 @@ class Layer {
       check(vxm_layer_write_blocks(h_, &k, 1, zero.voxels.data()));
       it = mirror_.emplace(g, std::make_unique<BlockType>()).first;
     }
-    host_dirty_.push_back(g);
+    make_writable(g, *it->second);
     return *it->second;
   }
   // voxel lookup by global voxel index; nullptr when the block is absent (layer.hpp:88-96)
@@ -356,18 +362,39 @@ class Layer {
 
  private:
   Layer() = default;
-  void flush() const {  // upload host-modified blocks
-    if (host_dirty_.empty()) return;
-    std::sort(host_dirty_.begin(), host_dirty_.end());
-    host_dirty_.erase(std::unique(host_dirty_.begin(), host_dirty_.end()), host_dirty_.end());
+  void make_writable(const GridIndex& g, const BlockType& b) {
+    writable_.try_emplace(g, b);  // base = the bytes the mirror holds now (device-equal)
+  }
+  // Uploads what the caller wrote through writable handles since the last
+  // exchange.  Mirror valid: no device op since, so the device block equals
+  // the base and the host block is uploaded whole.  Mirror stale: the device
+  // may have changed the block, so the caller's changed voxels are merged
+  // into the device's current bytes (and the handle sees the merge).
+  void flush() const {
     std::vector<vxm_grid_index> keys;
     std::vector<V> vox;
-    for (const GridIndex& g : host_dirty_) {
-      keys.push_back({g.x, g.y, g.z});
-      const auto& b = mirror_.at(g)->voxels;
-      vox.insert(vox.end(), b.begin(), b.end());
+    std::vector<const GridIndex*> gs;
+    for (auto& kv : writable_) {
+      const BlockType& host = *mirror_.at(kv.first);
+      if (std::memcmp(host.voxels.data(), kv.second.voxels.data(), sizeof(host.voxels)) == 0) continue;
+      gs.push_back(&kv.first);
     }
-    host_dirty_.clear();
+    if (gs.empty()) return;
+    for (const GridIndex* g : gs) {
+      BlockType& host = *mirror_.at(*g);
+      BlockType& base = writable_.at(*g);
+      const vxm_grid_index k{g->x, g->y, g->z};
+      if (!mirror_valid_) {  // three-way merge against the device's current block
+        BlockType dev;
+        check(vxm_layer_read_blocks(h_, &k, 1, dev.voxels.data(), nullptr));
+        for (int v = 0; v < kVoxelsPerBlock; ++v)
+          if (std::memcmp(&host.voxels[v], &base.voxels[v], sizeof(V)) != 0) dev.voxels[v] = host.voxels[v];
+        host = dev;
+      }
+      base = host;
+      keys.push_back(k);
+      vox.insert(vox.end(), host.voxels.begin(), host.voxels.end());
+    }
     check(vxm_layer_write_blocks(h_, keys.data(), keys.size(), vox.data()));
   }
   void sync_mirror() const {
@@ -383,6 +410,8 @@ class Layer {
       auto& slot = mirror_[g];  // existing blocks keep their address (handles stay valid)
       if (!slot) slot = std::make_unique<BlockType>();
       std::memcpy(slot->voxels.data(), vox.data() + i * kVoxelsPerBlock, sizeof(V) * kVoxelsPerBlock);
+      auto w = writable_.find(g);
+      if (w != writable_.end()) w->second = *slot;
     }
     mirror_valid_ = true;
   }
@@ -393,7 +422,8 @@ class Layer {
   size_t max_blocks_ = 0;
   mutable std::unordered_map<GridIndex, std::unique_ptr<BlockType>, GridHash> mirror_;
   mutable bool mirror_valid_ = false;
-  mutable std::vector<GridIndex> host_dirty_;
+  // blocks handed out writable -> the bytes last exchanged with the device
+  mutable std::unordered_map<GridIndex, BlockType, GridHash> writable_;
 };
 
 // ---- sensors / configs ---------------------------------------------------------

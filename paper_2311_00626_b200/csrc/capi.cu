@@ -226,7 +226,7 @@ vxm_status integrate_common(vxm_layer* L, const float* depth, int w, int h, cons
     const ViewArgs va = frame_args(L, depth, w, h, T, cam, li, cfg, on_device);
     tr.mark("staged");
     tr.dev_mark(L->ctx->stream, "h2d");
-    out->ctx = L->ctx;
+    out->bind(L->ctx);
     out->want_host = !on_device;  // unpacked to mapped host memory before the one sync
     try {
       run_integrate(L, va, *cfg, out);
@@ -265,8 +265,8 @@ vxm_status frame_common(vxm_layer* T, vxm_layer* E, const float* depth, int w, i
     }
     const ViewArgs va = frame_args(T, depth, w, h, pose, cam, li, icfg, true);
     Context* ctx = T->ctx;
-    tout->ctx = ctx;
-    if (E) eout->ctx = ctx;
+    tout->bind(ctx);
+    if (E) eout->bind(ctx);
     for (int attempt = 0; attempt < 4; ++attempt) {
       ctx->reset_status();
       const uint32_t nb_before = T->num_blocks;
@@ -688,7 +688,7 @@ vxm_status vxm_blocks_in_view_camera(vxm_context* ctx, const vxm_pose* T, const 
     ctx->sync_status();
     if (ctx->h_status->bitmap_overflow) throw Error(VXM_ERR_INTERNAL, "candidate bitmap overflow");
     const uint32_t n = ctx->h_status->n_candidates;
-    out->ctx = ctx;
+    out->bind(ctx);
     out->ensure(std::max<uint32_t>(n, 1));
     VXM_CUDA(cudaMemcpyAsync(out->keys.p, ctx->cand_keys.p, sizeof(uint64_t) * n,
                              cudaMemcpyDeviceToDevice, ctx->stream));
@@ -725,7 +725,7 @@ vxm_status vxm_blocks_in_view_lidar(vxm_context* ctx, const vxm_pose* T, const v
     ctx->sync_status();
     if (ctx->h_status->bitmap_overflow) throw Error(VXM_ERR_INTERNAL, "candidate bitmap overflow");
     const uint32_t n = ctx->h_status->n_candidates;
-    out->ctx = ctx;
+    out->bind(ctx);
     out->ensure(std::max<uint32_t>(n, 1));
     VXM_CUDA(cudaMemcpyAsync(out->keys.p, ctx->cand_keys.p, sizeof(uint64_t) * n,
                              cudaMemcpyDeviceToDevice, ctx->stream));
@@ -900,7 +900,7 @@ vxm_status vxm_update_esdf_list(vxm_layer* E, vxm_layer* T, vxm_blocklist* updat
     REQUIRE_ARG(E && T && updated && cfg && out, "null argument");
     REQUIRE_ARG(E->type == VXM_LAYER_ESDF && is_source(T),
                 "update_esdf: expects (ESDF layer, TSDF or occupancy layer)");
-    out->ctx = E->ctx;
+    out->bind(E->ctx);
     // esdf/integrator.cpp:371-378: empty input returns {} before the size check
     if (updated->count_hint == 0 || (updated->host_valid && updated->host.empty())) {
       out->assign_host(nullptr, 0);
@@ -928,7 +928,7 @@ vxm_status vxm_update_esdf(vxm_layer* E, vxm_layer* T, const vxm_grid_index* upd
     tr.dev_mark(ctx->stream, "start");
     vxm_blocklist* list = static_cast<vxm_blocklist*>(ctx->scratch_in);
     BlockList* last = ctx->last_host_out;
-    if (last && last != out && last->host_valid && last->sorted_unique && last->host.size() == n &&
+    if (last && last != out && last->ctx == ctx && last->host_valid && last->sorted_unique && last->host.size() == n &&
         (n == 0 || std::memcmp(last->host.data(), updated, sizeof(vxm_grid_index) * n) == 0)) {
       list = static_cast<vxm_blocklist*>(last);  // the integrate's device keys, identical content
     } else {
@@ -980,7 +980,7 @@ vxm_status vxm_esdf_mark_sites(vxm_layer* E, vxm_layer* T, const vxm_grid_index*
       ensure_sorted_unique(&list);
       run_mark_sites(E, T, &list, *cfg, st, &ch);
     }
-    changed->ctx = E->ctx;
+    changed->bind(E->ctx);
     changed->assign_host(ch.data(), ch.size());
   });
 }
@@ -989,7 +989,7 @@ vxm_status vxm_esdf_clear_invalid(vxm_layer* E, const vxm_esdf_config* cfg, vxm_
   return guard([&] {
     std::vector<vxm_grid_index> ch;
     run_clear_invalid(E, *cfg, st, &ch);
-    changed->ctx = E->ctx;
+    changed->bind(E->ctx);
     changed->assign_host(ch.data(), ch.size());
   });
 }
@@ -999,7 +999,7 @@ vxm_status vxm_esdf_lower(vxm_layer* E, vxm_esdf_state* st, const vxm_esdf_confi
     std::vector<vxm_grid_index> ch;
     const int r = run_lower_esdf(E, st, *cfg, &ch);
     if (rounds) *rounds = r;
-    changed->ctx = E->ctx;
+    changed->bind(E->ctx);
     changed->assign_host(ch.data(), ch.size());
   });
 }
@@ -1403,7 +1403,7 @@ vxm_status vxm_integrate_color(vxm_layer* C, const uint8_t* rgb, int w, int h, c
     va.block_size = C->vs * kVPS;
     va.cfg = {cfg->max_integration_distance, cfg->truncation, cfg->view_pixel_subsample};
     stage_depth(C->ctx, depth, w, h, false, &va.depth_dev);
-    out->ctx = C->ctx;
+    out->bind(C->ctx);
     run_integrate_color(C, tsdf, rgb, va, *cfg, out);
   });
 }
@@ -1478,7 +1478,7 @@ vxm_status vxm_update_mesh_list(vxm_mesh_layer* m, vxm_layer* T, vxm_blocklist* 
     REQUIRE_ARG(T->type == VXM_LAYER_TSDF, "update_mesh: source is not a TSDF layer");
     REQUIRE_ARG(!color || color->type == VXM_LAYER_COLOR, "update_mesh: color is not a color layer");
     const auto targets = run_update_mesh(m, T, updated, cfg->min_weight, color);
-    out->ctx = T->ctx;
+    out->bind(T->ctx);
     out->assign_host(targets.data(), targets.size());
     out->sorted_unique = true;
   });

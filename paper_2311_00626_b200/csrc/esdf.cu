@@ -1078,16 +1078,13 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.site_any = E->site_any;
   m.post = pa;
   ctx->prof_begin("k_mark");
-  static int mark_per_sm[2] = {0, 0};  // one wave of warps, each takes blocks until done
-  if (!mark_per_sm[occ]) {
-    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mark_per_sm[occ],
-                                                           occ ? k_mark<true> : k_mark<false>, 256, 0));
-    mark_per_sm[occ] = std::max(mark_per_sm[occ], 1);
-  }
+  // one wave of warps, each takes blocks until done
+  const int mark_per_sm =
+      ctx->resident_per_sm(occ ? (const void*)k_mark<true> : (const void*)k_mark<false>, 256);
   if (occ)
-    launch_pdl(ctx->stream, k_mark<true>, dim3(ctx->sm_count * mark_per_sm[occ]), dim3(256), 0, m);
+    launch_pdl(ctx->stream, k_mark<true>, dim3(ctx->sm_count * mark_per_sm), dim3(256), 0, m);
   else
-    launch_pdl(ctx->stream, k_mark<false>, dim3(ctx->sm_count * mark_per_sm[occ]), dim3(256), 0, m);
+    launch_pdl(ctx->stream, k_mark<false>, dim3(ctx->sm_count * mark_per_sm), dim3(256), 0, m);
   ctx->prof_end();
   ctx->count_launch();
   check_launch(ctx, "esdf mark phase");
@@ -1095,13 +1092,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
 }
 
 static int lower_grid(Context* ctx) {
-  static int cached = -1;
-  if (cached < 0) {
-    int bps = 0;
-    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lower3, kL3Threads, 0));
-    cached = std::max(1, std::min(bps, 4)) * ctx->sm_count;
-  }
-  return cached;
+  return ctx->resident_per_sm((const void*)k_lower3, kL3Threads, 0, 4) * ctx->sm_count;
 }
 
 bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint);  // lower_xr.cu: true when it compacted
@@ -1214,9 +1205,9 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
   // capacity for every effective block: at most 7 per updated block, and at
   // most one per TSDF block (effective blocks are allocated in the TSDF); when
   // the ESDF block set is known to be a subset of T's, T's pool bounds it
-  if (E->subset_of == nullptr && E->num_blocks == 0) E->subset_of = T;
+  E->note_esdf_source(T);
   uint64_t need = uint64_t(E->num_blocks) + std::min<uint64_t>(n7, T->capacity);
-  if (E->subset_valid && E->subset_of == T) need = std::min<uint64_t>(need, T->capacity);
+  if (E->bounded_by(T)) need = std::min<uint64_t>(need, T->capacity);
   E->ensure_capacity(std::min<uint64_t>(need, E->max_blocks));
   const uint32_t n_all_cap = E->capacity;
   EsdfScratch s = esdf_scratch(ctx, updated->count_hint, n_all_cap);
@@ -1318,6 +1309,7 @@ void run_mark_sites(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_confi
   const uint32_t epoch = ++ctx->call_epoch;
   ctx->reset_status();
   E->refresh();
+  E->note_esdf_source(T);
   E->ensure_capacity(std::min<uint64_t>(
       uint64_t(E->num_blocks) + 7ull * std::max<uint32_t>(updated->count_hint, 1), E->max_blocks));
   EsdfScratch s = esdf_scratch(ctx, updated->count_hint, 0);

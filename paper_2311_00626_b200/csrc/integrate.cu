@@ -8,18 +8,20 @@
 // CameraIntrinsics::project/contains (sensor/camera.hpp:35-46), LiDAR project
 // (sensor/lidar.hpp:43-55), sample_depth_nearest/linear (sensor/image.hpp:65-106).
 //
-// B200 design: persistent grid, one CTA (256 threads) per candidate block per
-// iteration.  The block's voxel centres are separable, so the 72 products
-// R_SL(i,a) * centre_a(v) are computed once per block into shared memory and
-// every voxel transform is 9 FP64 adds in the reference's association order
-// (bit-exact).  The camera projection's two FP64 divides are replaced by an
-// FP32 pre-filter with a rigorous error bound: nearest-pixel sampling only
-// needs floor(u), floor(v), so whenever [u-E, u+E] contains no integer the
-// FP32 floor is exact; otherwise (rare) the exact FP64 path runs.  Voxels are
-// read only when they project onto a valid pixel (new blocks are known-zero
-// and are not read at all) and written only when their bytes change; each
-// block's changed flag comes from __syncthreads_or and the changed list is an
-// order-preserving compaction of the (sorted) candidate list.
+// B200 design: persistent one-wave grid of 256-thread CTAs, ONE WARP PER
+// CANDIDATE BLOCK, 16 voxels per lane (lin = lane + 32 j; no shared memory and
+// no block-wide barrier).  The voxel centres are separable, so each lane forms
+// the per-axis products R_SL(i, a) * centre_a(v) for its x and two y rows once
+// and the z products per voxel pair: every voxel transform is then 9 FP64 adds
+// in the reference's association order (bit-exact).  The camera projection's
+// two FP64 divides are replaced by an FP32 pre-filter with a rigorous error
+// bound: nearest-pixel sampling only needs floor(u), floor(v), so whenever
+// [u-E, u+E] contains no integer the FP32 floor is exact; otherwise (rare) the
+// exact FP64 path runs.  Voxels are read only when they project onto a valid
+// pixel (new blocks are known-zero and are not read at all) and written only
+// when their bytes change; each block's changed flag is a warp vote
+// (__any_sync) and the changed list is an order-preserving compaction of the
+// (sorted) candidate list.
 #include <cmath>
 
 #include "runtime.cuh"
@@ -448,13 +450,9 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   const bool fast = !a.lidar && !a.linear;
   void (*kern)(IntegrateArgs) = occ ? (fast ? k_integrate<true, true> : k_integrate<true, false>)
                                     : (fast ? k_integrate<false, true> : k_integrate<false, false>);
-  static int per_sm[4] = {0, 0, 0, 0};  // resident CTAs per SM: the persistent grid is one wave
-  const int kv = 2 * int(occ) + int(fast);
-  if (!per_sm[kv]) {
-    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[kv], kern, 256, 0));
-    per_sm[kv] = std::max(per_sm[kv], 1);
-  }
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * per_sm[kv]));
+  // resident CTAs per SM: the persistent grid is one wave
+  const int per_sm = ctx->resident_per_sm((const void*)kern, 256);
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * per_sm));
   host_trace_dev(ctx, "dilate");
   ctx->prof_begin("k_integrate");
   launch_pdl(ctx->stream, kern, dim3(grid), dim3(256), 0, a);

@@ -540,13 +540,7 @@ bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
   }();
   const bool wide = wide_mode == 2 || (wide_mode == 1 && n_blocks_hint > kXrWideBlocks);
   void (*kern)(LowerArgs) = wide ? k_lower_xr<3> : k_lower_xr<2>;
-  static int grids[2] = {0, 0};
-  int& grid = grids[wide];
-  if (!grid) {
-    int bps = 0;
-    VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kL3Threads, 0));
-    grid = std::max(1, std::min(bps, 4)) * ctx->sm_count;
-  }
+  const int grid = ctx->resident_per_sm((const void*)kern, kL3Threads, 0, 4) * ctx->sm_count;
   ctx->lower_cta.ensure(sizeof(uint32_t) * grid);  // per-CTA counts of the in-kernel compaction
   la.cta_cnt = ctx->lower_cta.as<uint32_t>();
   void* args[] = {&la};

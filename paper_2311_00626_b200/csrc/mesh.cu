@@ -363,14 +363,12 @@ void mesh_sorted_keys(MeshLayerH* M, Layer* T, const std::vector<uint64_t>& targ
   Context* ctx = T->ctx;
   const uint32_t n = uint32_t(targets.size());
   if (!n) return;
-  static bool attr = false;
-  if (!attr) {
+  ctx->once_attr((const void*)k_mesh<true>, [] {  // per device (function attributes are per context)
     VXM_CUDA(cudaFuncSetAttribute(k_mesh<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sizeof(MeshSmem))));
     VXM_CUDA(cudaFuncSetAttribute(k_mesh<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kCountSmem)));
-    attr = true;
-  }
+  });
   DevBuf dkeys, dcounts, doff;
   dkeys.ensure(sizeof(uint64_t) * n);
   dcounts.ensure(sizeof(uint32_t) * 2 * n);

@@ -1,5 +1,6 @@
 // Host runtime: device memory management for layers (block pool + hash +
 // ESDF side arrays), contexts, block lists and small device utilities.
+#include <atomic>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -35,6 +36,23 @@ void check_launch(Context* ctx, const char* what) {
 }
 
 // ---- Context -------------------------------------------------------------------
+uint64_t Layer::next_layer_uid() {
+  static std::atomic<uint64_t> next{1};
+  return next.fetch_add(1, std::memory_order_relaxed);
+}
+
+int Context::resident_per_sm(const void* kernel, int threads, size_t smem, int cap) {
+  std::lock_guard<std::mutex> g(geo_mu);
+  auto it = resident.find(kernel);
+  if (it != resident.end()) return it->second;
+  int bps = 0;
+  VXM_CUDA(cudaSetDevice(device));
+  VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, threads, smem));
+  bps = std::max(1, std::min(bps, cap));
+  resident.emplace(kernel, bps);
+  return bps;
+}
+
 ScanTiles Context::next_scan(uint32_t tiles) {
   tiles = std::max<uint32_t>(tiles, 1);
   if (tiles > scan.cap) {

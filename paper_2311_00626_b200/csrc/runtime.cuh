@@ -7,6 +7,8 @@
 
 #include <cstdint>
 #include <map>
+#include <mutex>
+#include <set>
 #include <string>
 #include <utility>
 #include <vector>
@@ -84,6 +86,20 @@ struct Context {
   // the status read, error checks and meta adoption to the caller's one sync.
   bool deferred = false;
 
+  // Launch geometry per kernel on THIS context's device (resident CTAs per
+  // SM; one-time function attributes).  Keyed by context, not process-wide:
+  // contexts on different devices (or threads) never share a stale entry.
+  std::mutex geo_mu;
+  std::map<const void*, int> resident;
+  std::set<const void*> attr_done;
+  int resident_per_sm(const void* kernel, int threads, size_t smem = 0, int cap = 1 << 30);
+  // runs `set` once per kernel on this context (cudaFuncSetAttribute etc.)
+  template <typename F>
+  void once_attr(const void* kernel, F&& set) {
+    std::lock_guard<std::mutex> g(geo_mu);
+    if (attr_done.insert(kernel).second) set();
+  }
+
   // Scan pass bookkeeping: returns the ScanTiles for the next pass with at
   // most `tiles` tiles, clearing the other buffer for the pass after.
   ScanTiles next_scan(uint32_t tiles);
@@ -140,10 +156,25 @@ struct Layer {
   uint32_t* stamp_pair[3] = {nullptr, nullptr, nullptr};  // round epoch of pair (b, b+axis)
   uint32_t* stamp_r1same = nullptr;  // call epoch: round 1 left the block byte-identical
 
-  // ESDF: while every block came from mark_sites against `subset_of`, the
-  // block set is a subset of that TSDF layer's (so bounded by its capacity)
-  const Layer* subset_of = nullptr;
+  // Process-unique identity (never reused, unlike the address of a destroyed
+  // layer).
+  uint64_t uid = next_layer_uid();
+  // ESDF: while every block came from mark_sites against the source layer
+  // `subset_uid`, the block set is a subset of that TSDF layer's (so bounded
+  // by its capacity).  Any call against another source, or any user write,
+  // clears subset_valid for good (an empty layer starts over).
+  uint64_t subset_uid = 0;
   bool subset_valid = true;
+  void note_esdf_source(const Layer* src) {
+    if (num_blocks == 0) {
+      subset_uid = src->uid;
+      subset_valid = true;
+    } else if (subset_uid != src->uid) {
+      subset_valid = false;
+    }
+  }
+  bool bounded_by(const Layer* src) const { return subset_valid && subset_uid == src->uid; }
+  static uint64_t next_layer_uid();
 
   size_t voxel_bytes() const {
     return type == VXM_LAYER_ESDF ? 12 : type == VXM_LAYER_OCCUPANCY ? 4 : 8;  // TSDF, color: 8
@@ -183,6 +214,12 @@ struct BlockList {
   uint32_t* mapped_count = nullptr;
   uint32_t mapped_cap = 0;
   void enqueue_host();
+  // Re-binds the list to context c; a context that still remembers this list
+  // as its last host result forgets it (no dangling last_host_out).
+  void bind(Context* c) {
+    if (ctx && ctx != c && ctx->last_host_out == this) ctx->last_host_out = nullptr;
+    ctx = c;
+  }
   void ensure(uint32_t n);
   const std::vector<vxm_grid_index>& fetch();   // sync + download + unpack
   void assign_host(const vxm_grid_index* data, uint64_t n);  // upload (sorted as given)

@@ -342,9 +342,7 @@ ShardRound round_args(ShardUpdate& x, uint32_t r) {
 }
 
 int grid_of(const void* kernel, Context* c) {
-  int bps = 0;
-  VXM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, kL3Threads, 0));
-  return std::max(1, std::min(bps, 4)) * c->sm_count;
+  return c->resident_per_sm(kernel, kL3Threads, 0, 4) * c->sm_count;
 }
 
 }  // namespace
@@ -358,6 +356,7 @@ void shard_begin(ShardUpdate& x, const vxm_esdf_config& cfg) {
   ctx->reset_status();
   x.epoch = ++ctx->call_epoch;
   const uint32_t n7 = 7u * std::max<uint32_t>(x.uni.count_hint, 1);
+  x.E->note_esdf_source(x.T);
   x.E->ensure_capacity(std::min<uint64_t>(uint64_t(x.E->num_blocks) + n7, x.E->max_blocks));
   x.n_all_cap = x.E->capacity;
   x.s = esdf_scratch(ctx, x.uni.count_hint, x.n_all_cap);
@@ -428,8 +427,7 @@ void shard_set_neighbours(ShardUpdate& x, uint32_t n_left, uint32_t n_right) {
 void shard_sweep(ShardUpdate& x, uint32_t r) {
   use(x.ctx);
   cudaStream_t st = x.ctx->stream;
-  static int g_sweep = 0;
-  if (!g_sweep) g_sweep = grid_of((const void*)k_shard_sweep, x.ctx);
+  const int g_sweep = grid_of((const void*)k_shard_sweep, x.ctx);
   VXM_CUDA(cudaMemsetAsync(x.ctr.p, 0, 4 * sizeof(uint32_t), st));
   ShardRound sr = round_args(x, r);
   k_shard_sweep<<<g_sweep, kL3Threads, 0, st>>>(x.la, sr);
@@ -444,8 +442,7 @@ void shard_sweep(ShardUpdate& x, uint32_t r) {
 uint32_t shard_border(ShardUpdate& x, uint32_t r) {
   use(x.ctx);
   cudaStream_t st = x.ctx->stream;
-  static int g_border = 0;
-  if (!g_border) g_border = grid_of((const void*)k_shard_border, x.ctx);
+  const int g_border = grid_of((const void*)k_shard_border, x.ctx);
   VXM_CUDA(cudaMemsetAsync(x.la.count + (r + 1u) % 3u, 0, sizeof(uint32_t), st));
   ShardRound sr = round_args(x, r);
   void* args[] = {&x.la, &sr};

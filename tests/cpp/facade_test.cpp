@@ -269,6 +269,57 @@ int main() {
     vxo_layer_destroy(oe2);
   }
 
+  // A writable handle kept across device operations (layer.hpp:44-46): the
+  // reference's host blocks ARE the map, so a write through a handle taken
+  // before integrate_depth and made after it must persist and compose voxel
+  // by voxel with the integration's own changes.  The oracle does the same
+  // writes on its own layer.
+  {
+    vb::Layer<vb::TsdfVoxel> t2(0.05);
+    vxo_layer* o2 = nullptr;
+    vxo_layer_create(VXM_LAYER_TSDF, 0.05, 0, &o2);
+    auto frame = [&](int k) {
+      vxm_pose p;
+      vxm_synth_orbit_pose(scene, 0, k, 8, &p);
+      vb::DepthImage depth(cam.width, cam.height);
+      vxm_synth_render_camera(scene, &p, &cam_c, depth.data.data());
+      const auto a = vb::integrate_depth(t2, depth, pose_of(p), cam, cfg);
+      vxm_grid_index* ob = nullptr;
+      uint64_t on = 0;
+      vxo_integrate_camera(o2, depth.data.data(), depth.width, depth.height, &p, &cam_c, &cfg_c, &ob, &on);
+      CHECK(a == oracle_list(ob, on));
+      return a;
+    };
+    auto oracle_write = [&](const vb::GridIndex& g, int lin, vb::TsdfVoxel v) {
+      const uint64_t n = vxo_layer_num_blocks(o2);
+      std::vector<vxm_grid_index> ok(n);
+      std::vector<vb::TsdfVoxel> ov(n * 512);
+      vxo_layer_export(o2, ok.data(), ov.data());
+      for (uint64_t i = 0; i < n; ++i)
+        if (ok[i].x == g.x && ok[i].y == g.y && ok[i].z == g.z) {
+          ov[i * 512 + lin] = v;
+          vxo_layer_write_blocks(o2, &ok[i], 1, ov.data() + i * 512);
+        }
+    };
+    const auto first = frame(0);
+    CHECK(!first.empty());
+    const vb::GridIndex g = first[first.size() / 2];
+    vb::VoxelBlock<vb::TsdfVoxel>* h = t2.block_ptr(g);  // kept across the frames below
+    CHECK(h != nullptr);
+    const auto second = frame(1);                         // device op (may change block g)
+    const vb::TsdfVoxel w1{0.0625f, 3.0f};
+    h->voxels[7] = w1;                                    // write AFTER the device op
+    oracle_write(g, 7, w1);
+    const auto third = frame(2);                          // must see the write
+    const vb::TsdfVoxel w2{-0.03125f, 5.0f};
+    h->voxels[300] = w2;
+    oracle_write(g, 300, w2);
+    CHECK(t2.block_ptr(g) == h);                          // the handle stays valid
+    CHECK(std::memcmp(&h->voxels[300], &w2, sizeof w2) == 0);
+    CHECK(same_layer(t2, o2));
+    vxo_layer_destroy(o2);
+  }
+
   vxo_layer_destroy(otsdf);
   vxo_layer_destroy(oesdf);
   vxm_synth_scene_destroy(scene);
