@@ -511,8 +511,8 @@ vxm_status vxm_layer_create(vxm_context* ctx, vxm_layer_type type, double vs, ui
     if (type == VXM_LAYER_ESDF) {
       // [0..2] dirty-list counts, [3..6] sweep / pair work counters by parity,
       // [7..10] round-1 split counters (zero between launches)
-      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * 64));
-      VXM_CUDA(cudaMemsetAsync(L->dirty_count, 0, sizeof(uint32_t) * 64, ctx->stream));
+      VXM_CUDA(cudaMalloc(&L->dirty_count, sizeof(uint32_t) * kDirtyCountWords));
+      VXM_CUDA(cudaMemsetAsync(L->dirty_count, 0, sizeof(uint32_t) * kDirtyCountWords, ctx->stream));
     }
     L->ensure_capacity(std::min<uint64_t>(4096, L->max_blocks));
     *out = L;

@@ -1178,7 +1178,7 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.stamp_swept = E->stamp_swept;
   la.site_any = E->site_any;
   la.r1 = E->dirty_count + 7;
-  la.ring = E->dirty_count + 16;
+  la.ring = E->dirty_count + kRingOffset;
   la.dlist[0] = E->dlist[0];
   la.dlist[1] = E->dlist[1];
   la.capacity = E->capacity;

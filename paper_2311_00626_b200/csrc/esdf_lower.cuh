@@ -588,6 +588,7 @@ __device__ inline bool warp_reset_copy(const uint32_t* __restrict__ src, uint32_
 
 // ---- lowering v3: group-per-block sweeps with line masks --------------------------
 constexpr int kL3Threads = 256;
+
 constexpr int kL3Groups = kL3Threads / 64;
 
 __device__ inline void line_bits(int x, int y, int z, unsigned long long m[3]) {

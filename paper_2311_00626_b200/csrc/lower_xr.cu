@@ -33,6 +33,11 @@ namespace vxm {
 namespace {
 
 constexpr int kRingCnt = 0, kRingSwc = 4, kRingPc = 8, kRingDone = 12, kRingLast = 16;
+// Every ring counter sits on its own 256-byte line (kRingStride words): the
+// counters are polled by every idle warp between rounds, and co-located
+// counters would serialise the critical atomics behind those polls in one
+// L2 slice.
+__device__ __forceinline__ uint32_t* RG(uint32_t* ring, int i) { return ring + i * kRingStride; }
 
 // Lines of a block through the voxels of one face (bit i0 + 8 j0 of F) that a
 // pair along `axis` changed; `face` is the face's coordinate (0 or 7).  The
@@ -58,6 +63,27 @@ __device__ inline void face_lines(unsigned long long F, int axis, int face, unsi
     m[1] |= (unsigned long long)cols << (8 * face);
     m[2] |= F;
   }
+}
+
+// VXM_TRACE_XR phase stamps of round R < 24: trace[128 + 16 R + k], k = 0 first
+// sweep claimed (min), 1 last sweep released, 2 first pair claimed (min),
+// 3 / 4 / 5 last x / y / z pair released, 6 / 7 sum / count of sweep durations,
+// 8 / 9 / 10 / 11 sums of the sweeps' dependency wait / load + stage / sweep /
+// store + release, 12 / 13 / 14 sums of the x / y / z pairs' work after their
+// waits, 15 count of non-identity pairs.
+__device__ inline unsigned long long gtime() {
+  unsigned long long tm;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+  return tm;
+}
+__device__ inline void tr_max(unsigned long long* tr, uint32_t R, int k, unsigned long long v) {
+  if (tr && R < 24) atomicMax(tr + 128 + 16 * R + k, v);
+}
+__device__ inline void tr_min(unsigned long long* tr, uint32_t R, int k, unsigned long long v) {
+  if (tr && R < 24) atomicMax(tr + 128 + 16 * R + k, ~v);
+}
+__device__ inline void tr_add(unsigned long long* tr, uint32_t R, int k, unsigned long long v) {
+  if (tr && R < 24) atomicAdd(tr + 128 + 16 * R + k, v);
 }
 
 __device__ inline unsigned long long ld_relaxed64(const unsigned long long* p) {
@@ -92,12 +118,15 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
   uint32_t* const work = pnxt;
   const Limits lim = a.lim;
   uint32_t* const ring = a.ring;
+  // "round R complete": polled relaxed (an acquire per poll would invalidate L1
+  // each time), then one acquire once seen
+  const uint32_t* const last_rep = RG(ring, kRingLast);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int q = 1; q <= 2; ++q) {  // rounds 1 and 2; later rounds are zeroed by round R - 2
-      ring[kRingCnt + q] = 0u;
-      ring[kRingSwc + q] = ring[kRingPc + q] = ring[kRingDone + q] = 0u;
+      *RG(ring, kRingCnt + q) = 0u;
+      *RG(ring, kRingSwc + q) = *RG(ring, kRingPc + q) = *RG(ring, kRingDone + q) = 0u;
     }
-    ring[kRingLast] = 0u;
+    *RG(ring, kRingLast) = 0u;
   }
   // round-1 split by site_any (as k_lower3)
   if (lower) {
@@ -203,7 +232,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             // claim the next dirty block of round R; its slot is written by the
             // round R - 1 pair that changed it (epoch-tagged), or the list ends
             // once round R - 1 is complete
-            const uint32_t i = atomicAdd(ring + kRingSwc + q4, 1u);
+            const uint32_t i = atomicAdd(RG(ring, kRingSwc + q4), 1u);
             int32_t s = -1;
             for (uint32_t it = 0; i < a.capacity; ++it) {  // (a round never lists more)
               const unsigned long long e = ld_relaxed64(dl + i);
@@ -211,8 +240,8 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
                 s = int32_t(uint32_t(e));
                 break;
               }
-              if (ld_acquire(ring + kRingLast) + 1u >= R &&
-                  i >= *((volatile uint32_t*)(ring + kRingCnt + q4))) {
+              if (ld_relaxed(last_rep) + 1u >= R && ld_acquire(last_rep) + 1u >= R &&
+                  i >= *((volatile uint32_t*)(RG(ring, kRingCnt + q4)))) {
                 const unsigned long long e2 = ld_relaxed64(dl + i);  // (written before the count)
                 if (uint32_t(e2 >> 32) == ep) s = int32_t(uint32_t(e2));
                 break;
@@ -228,6 +257,11 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           group_sync(bar);
           const int32_t s = int32_t(G.bcast);
           if (s < 0) break;
+          unsigned long long tsw0 = 0;
+          if (a.trace && t == 0) {
+            tsw0 = gtime();
+            tr_min(a.trace, R, 0, tsw0);
+          }
           // the block's round R - 1 pairs (the reference's only writers of it since
           // its last sweep) must be complete: lanes 0-5 of the group's first warp;
           // the faces they changed give the lines to sweep first
@@ -259,18 +293,33 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             }
           }
           group_sync(bar);  // every wait done before the masks and voxels are read
+          unsigned long long tsa = 0, tsb = 0, tsc = 0;
+          if (a.trace && t == 0) tsa = gtime();
           RawBlock rb;
           bool any_site, fast;
           load_raw3(rb, work + size_t(s) * 1536, t, bar, lim, false, &any_site, &fast);
           stage_block3(G, rb, t, bar, lim, fast);
-          if (sweep_block3(G, t, bar, lim)) store_block3(G, work + size_t(s) * 1536, t);
+          if (a.trace && t == 0) tsb = gtime();
+          const bool sw_chg = sweep_block3(G, t, bar, lim);
+          if (a.trace && t == 0) tsc = gtime();
+          if (sw_chg) store_block3(G, work + size_t(s) * 1536, t);
           group_sync(bar);  // the group's stores before the release of its sweep stamp
           if (t == 0) st_release(a.stamp_swept + s, ep);
+          if (a.trace && t == 0) {
+            const unsigned long long tsw1 = gtime();
+            tr_max(a.trace, R, 1, tsw1);
+            tr_add(a.trace, R, 6, tsw1 - tsw0);
+            tr_add(a.trace, R, 7, 1ull);
+            tr_add(a.trace, R, 8, tsa - tsw0);
+            tr_add(a.trace, R, 9, tsb - tsa);
+            tr_add(a.trace, R, 10, tsc - tsb);
+            tr_add(a.trace, R, 11, tsw1 - tsc);
+          }
         }
       }
       // ---- border phase of round R (esdf/integrator.cpp:517-559) ----------------
       if (!r1) {  // enumeration needs the final round-R list: round R - 1 complete
-        for (uint32_t it = 0; ld_acquire(ring + kRingLast) + 1u < R; ++it) {
+        for (uint32_t it = 0; ld_relaxed(last_rep) + 1u < R; ++it) {
           if (it > (1u << 24)) {
             if (atomicExch(&a.status->watchdog, 1u) == 0u) a.status->pad3[0] = 41u;
             break;
@@ -278,7 +327,8 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           __nanosleep(32);
         }
       }
-      const uint32_t n_dirty = r1 ? n_blocks : *((volatile uint32_t*)(ring + kRingCnt + q4));
+      if (!r1) (void)ld_acquire(last_rep);  // the round's list and counts are visible
+      const uint32_t n_dirty = r1 ? n_blocks : *((volatile uint32_t*)(RG(ring, kRingCnt + q4)));
       if (n_dirty == 0) break;  // while (!dirty.empty()) — esdf/integrator.cpp:506
       rounds = R;
       const unsigned long long* dl = a.dlist[cp];
@@ -293,9 +343,10 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
       // prefetching the next claim during the current item costs 4 %)
       while (true) {
         uint32_t wi = 0;
-        if (lane == 0) wi = atomicAdd(ring + kRingPc + q4, 1u);
+        if (lane == 0) wi = atomicAdd(RG(ring, kRingPc + q4), 1u);
         wi = __shfl_sync(0xffffffffu, wi, 0);
         if (wi >= n_items) break;
+        if (a.trace && lane == 0 && wi == 0) tr_min(a.trace, R, 2, gtime());
         const int axis = int(wi / per_axis);
         const uint32_t rest = wi - uint32_t(axis) * per_axis;
         const uint32_t i = r1 ? rest : rest >> 1;
@@ -343,6 +394,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           }
           const uint32_t chg_mask = __ballot_sync(0xffffffffu, dep_chg);
           __syncwarp();
+          const unsigned long long tp0 = a.trace ? gtime() : 0ull;
           bool skip = false;
           if (r1) {  // no giver on either face: the pair is the identity (k_lower3)
             constexpr uint32_t lo_lanes = 0x0ccu, hi_lanes = 0x330u;
@@ -383,12 +435,16 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             __syncwarp();
             if (lane == 0)
               st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));
+            if (a.trace && lane == 0) {
+              tr_add(a.trace, R, 12 + axis, gtime() - tp0);
+              tr_add(a.trace, R, 15, 1ull);
+            }
             if (lane == 0) {
 #pragma unroll
               for (int qq = 0; qq < 2; ++qq) {
                 if (!chg[qq]) continue;
                 if (atomicMax(a.stamp_dirty[np] + who[qq], ep_next) < ep_next) {
-                  const uint32_t slot = atomicAdd(ring + kRingCnt + q4n, 1u);
+                  const uint32_t slot = atomicAdd(RG(ring, kRingCnt + q4n), 1u);
                   *(volatile unsigned long long*)(a.dlist[np] + slot) =
                       (unsigned long long)ep_next << 32 | uint32_t(who[qq]);
                 }
@@ -396,18 +452,19 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             }
           }
         }
+        if (a.trace && lane == 0) tr_max(a.trace, R, 3 + axis, gtime());
         ++my_done;
       }
       // round accounting, one atomic per warp: the warp whose items complete
       // round R publishes it (every item this warp claimed is done here)
       if (lane == 0 && my_done) {
         __threadfence();
-        const uint32_t done = atomicAdd(ring + kRingDone + q4, my_done) + my_done;
+        const uint32_t done = atomicAdd(RG(ring, kRingDone + q4), my_done) + my_done;
         if (done == n_items) {
           __threadfence();
           const int q4nn = int((R + 2u) & 3u);
-          ring[kRingCnt + q4nn] = 0u;
-          ring[kRingSwc + q4nn] = ring[kRingPc + q4nn] = ring[kRingDone + q4nn] = 0u;
+          *RG(ring, kRingCnt + q4nn) = 0u;
+          *RG(ring, kRingSwc + q4nn) = *RG(ring, kRingPc + q4nn) = *RG(ring, kRingDone + q4nn) = 0u;
           if (R > 1) a.status->sum_dirty += n_dirty;
           if (a.trace && R < 54) {  // VXM_TRACE_XR: round completion times
             unsigned long long tm;
@@ -416,7 +473,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             a.trace[64 + R] = n_dirty;
           }
           __threadfence();
-          st_release(ring + kRingLast, R);
+          st_release(RG(ring, kRingLast), R);
         }
       }
       // the next round's sweeps re-form the groups (both warps)
@@ -530,8 +587,8 @@ bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
   static const bool trace = std::getenv("VXM_TRACE_XR") != nullptr;
   static DevBuf trace_buf;
   if (trace) {
-    trace_buf.ensure(128 * sizeof(unsigned long long));
-    VXM_CUDA(cudaMemsetAsync(trace_buf.p, 0, 128 * sizeof(unsigned long long), ctx->stream));
+    trace_buf.ensure(512 * sizeof(unsigned long long));
+    VXM_CUDA(cudaMemsetAsync(trace_buf.p, 0, 512 * sizeof(unsigned long long), ctx->stream));
     la.trace = trace_buf.as<unsigned long long>();
   }
   static const int wide_mode = [] {  // VXM_XR_WIDE: 0 never, 1 by map size (default), 2 always
@@ -565,7 +622,7 @@ bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
   ctx->prof_end();
   ctx->count_launch();
   if (trace) {
-    unsigned long long h[128];
+    unsigned long long h[512];
     VXM_CUDA(cudaMemcpyAsync(h, trace_buf.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     VXM_CUDA(cudaStreamSynchronize(ctx->stream));
     std::fprintf(stderr, "[k_lower_xr] round ends (us) / dirty blocks:");
@@ -577,6 +634,19 @@ bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
     if (h[62] && h[63])
       std::fprintf(stderr, " | lowered %.1f, compared %.1f", (h[62] - h[0]) * 1e-3, (h[63] - h[0]) * 1e-3);
     std::fprintf(stderr, "\n");
+    // per-round phases (us from the kernel's start): sweeps [first claim, last
+    // release] avg duration | pairs first claim | last x / y / z release
+    for (int r = 2; r < 24 && h[r]; ++r) {
+      const unsigned long long* p = h + 128 + 16 * r;
+      auto us = [&](unsigned long long v) { return v ? (double(v) - double(h[0])) * 1e-3 : -1.0; };
+      std::fprintf(stderr, "  [xr r%d n=%llu] sw %.1f-%.1f (avg %.2f, %llu) pairs %.1f x %.1f y %.1f z %.1f end %.1f\n", r,
+                   h[64 + r], us(p[0] ? ~p[0] : 0), us(p[1]), p[7] ? double(p[6]) * 1e-3 / double(p[7]) : 0.0, p[7],
+                   us(p[2] ? ~p[2] : 0), us(p[3]), us(p[4]), us(p[5]), us(h[r]));
+      if (p[7] && p[15])
+        std::fprintf(stderr, "      sweep avg: wait %.2f load %.2f sweep %.2f store %.2f | pair work avg (all axes) %.2f us over %llu\n",
+                     p[8] * 1e-3 / p[7], p[9] * 1e-3 / p[7], p[10] * 1e-3 / p[7], p[11] * 1e-3 / p[7],
+                     (p[12] + p[13] + p[14]) * 1e-3 / p[15], p[15]);
+    }
     la.trace = nullptr;
   }
   return la.out_keys != nullptr;

@@ -123,6 +123,12 @@ struct Context {
   void prof_resolve();  // after a stream sync
 };
 
+// Cross-round ring counters (lower_xr.cu): 17 counters, one 256-byte line
+// each, after 64 words of list / work counters in Layer::dirty_count.
+constexpr int kRingStride = 64;
+constexpr int kRingOffset = 64;
+constexpr int kDirtyCountWords = kRingOffset + 17 * kRingStride;
+
 struct Layer {
   Context* ctx = nullptr;
   int type = VXM_LAYER_TSDF;
@@ -146,8 +152,8 @@ struct Layer {
   uint32_t* stamp_new = nullptr;    // call epoch when the block was allocated
   uint32_t* stamp_lchg = nullptr;   // round epoch of the last lowering change
   int32_t* dirty_list[2] = {nullptr, nullptr};
-  uint32_t* dirty_count = nullptr;  // [64]: list counts, work counters, round-1 split counters,
-                                    // [16..32] the cross-round lowering's per-round ring
+  uint32_t* dirty_count = nullptr;  // [kDirtyCountWords]: list counts, work counters, round-1
+                                    // split counters; from kRingOffset the cross-round ring
   unsigned long long* dlist[2] = {nullptr, nullptr};  // [cap] (epoch << 32 | slot) dirty lists
   unsigned long long* pair_face[3] = {nullptr, nullptr, nullptr};  // [cap][2] faces a pair changed
   unsigned long long* line_mask = nullptr;  // [cap][3] lines changed by border phases
