@@ -493,6 +493,122 @@ def cpu_reference_c5(steps, side=C5_SIDE):
 
 
 # ---------------------------------------------------------------------------
+def shard_owner(x, world, slab):
+    """owner(g) = floor(g.x / slab) mod world (vxm_context_set_shard)."""
+    return (np.asarray(x, np.int64) // slab) % world
+
+
+def run_sharded(args, rank, world, device):
+    """--shard: ONE map block-sharded over the ranks; a step is
+    one frame of the whole map: rank 0's depth frame is broadcast over NCCL,
+    every rank allocates and integrates only its x-slabs (no exchange), then
+    update_esdf runs over the union map with per-round slab-boundary face
+    exchange (paper_2311_00626_b200/dist.py: NCCL send/recv + an on-device
+    all-reduce of the next dirty count on the library's stream).  C5: each rank
+    holds its slabs of the volume and updates them."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2311_00626_b200 as vx
+    from paper_2311_00626_b200 import _abi as A
+    from paper_2311_00626_b200 import dist as vxd
+    torch.cuda.set_device(device)
+    c = CONFIGS[args.config]
+    W, K = args.warmup, args.steps
+    ctx = vx.Context(device)
+    ctx.set_shard(rank, world, args.slab)
+    ext = torch.cuda.ExternalStream(ctx.stream, device=device)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)
+    cuda = torch.device("cuda", device)
+    xfer = {"h2d": 0, "d2h": 0}
+    if args.config == "c5":
+        keys, va, vb = c5_volumes()
+        own = shard_owner(keys[:, 0], world, args.slab) == rank
+        Ts = [vx.TsdfLayer(c["vs"], ctx=ctx), vx.TsdfLayer(c["vs"], ctx=ctx)]
+        Ts[0].write_blocks(keys[own], va[own])
+        Ts[1].write_blocks(keys[own], vb[own])
+        del va, vb
+        upd = np.ascontiguousarray(keys[own])
+        ecfg = A.default_esdf_config(site_threshold=c["esdf"][0], max_distance=c["esdf"][1])
+        E = vx.EsdfLayer(c["vs"], ctx=ctx)
+
+        def step(i, host=False):
+            ch = vxd.update_esdf_distributed(E, Ts[i % 2], upd, ecfg)
+            if host:
+                xfer["h2d"] += upd.nbytes
+                xfer["d2h"] += ch.nbytes
+    else:
+        sensor, frames, icfg, ecfg = make_inputs(args.config, W + K)
+        H, Wd = frames[0][1].shape
+        if rank == 0:
+            dev_frames = torch.from_numpy(np.stack([d for _, d in frames])).to(cuda)
+            pinned = [vx.pinned_like(np.ascontiguousarray(d, np.float32)) for _, d in frames]
+        buf = torch.empty((H, Wd), dtype=torch.float32, device=cuda)
+        T = vx.TsdfLayer(c["vs"], ctx=ctx)
+        E = vx.EsdfLayer(c["vs"], ctx=ctx)
+        if c.get("reserve"):
+            T.reserve(max(1, c["reserve"] // world))
+            E.reserve(max(1, c["reserve"] // world))
+        tl = vx.BlockList(ctx)
+
+        def step(i, host=False):
+            with torch.cuda.stream(ext):  # the broadcast is ordered before our kernels
+                if rank == 0:
+                    if host:  # the frame arrives in host memory on the sensor's rank
+                        buf.copy_(torch.from_numpy(pinned[i].array), non_blocking=True)
+                        xfer["h2d"] += buf.numel() * 4
+                    else:
+                        buf.copy_(dev_frames[i])
+                if dist.get_backend() == "gloo":
+                    hb = buf.cpu()
+                    dist.broadcast(hb, src=0)
+                    buf.copy_(hb)
+                else:
+                    dist.broadcast(buf, src=0)
+            vx.integrate_depth_device(T, buf.data_ptr(), Wd, H, frames[i][0], sensor, icfg, tl)
+            ch = vxd.update_esdf_distributed(E, T, tl, ecfg)
+            if host:
+                xfer["d2h"] += ch.nbytes
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize(device)
+    ctx.reset_stats()
+    launches0 = ctx.launch_count
+    tot = []
+    with ClockSampler(device) as clk:
+        for i in range(W, W + K):
+            flush.zero_()
+            torch.cuda.synchronize(device)
+            dist.barrier()
+            e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            e0.record(ext)
+            step(i)
+            e1.record(ext)
+            e1.synchronize()
+            tot.append(e0.elapsed_time(e1))
+    launches = ctx.launch_count - launches0
+    stats = ctx.stats()
+    total_s = sum(tot) / 1000.0
+    # e2e: host frame on the sensor rank, changed lists back to each host
+    e2e_t = []
+    for i in range(W, W + K):
+        torch.cuda.synchronize(device)
+        dist.barrier()
+        t0 = time.perf_counter()
+        step(i, host=True)
+        torch.cuda.synchronize(device)
+        e2e_t.append(time.perf_counter() - t0)
+    t = torch.tensor([total_s, sum(e2e_t)], dtype=torch.float64, device=cuda)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    blocks = torch.tensor([stats["esdf_blocks"]], dtype=torch.float64, device=cuda)
+    dist.all_reduce(blocks, op=dist.ReduceOp.SUM)
+    return dict(total_s=float(t[0]), tot=tot, tsdf_ms=0.0, esdf_ms=0.0, stats=stats, kernels={},
+                launches=launches, clocks=clk.summary(), e2e_s=float(t[1]),
+                h2d=xfer["h2d"] // K, d2h=xfer["d2h"] // K, union_esdf_blocks=float(blocks[0]) / K)
+
+
+# ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -502,6 +618,10 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="one map block-sharded over the ranks (x-slabs, NCCL exchange) instead of "
+                         "N independent replicas")
+    ap.add_argument("--slab", type=int, default=0, help="shard slab width in blocks (default by config)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -538,12 +658,33 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    sharded = args.shard and world > 1
+    if args.shard:
+        if args.config == "c1" or c["sensor"] == "lidar":
+            raise SystemExit("--shard: configs c2, c4, c5 (camera / volume maps)")
+        args.slab = args.slab or (8 if args.config == "c5" else 16)
+        # N = 1: the whole map on one GPU is the single-map path itself
+        config["parallelism"] = f"shard{world}" if world > 1 else "shard1 (single map)"
+        config["shard"] = {"owner": "floor(block.x / slab) mod n_gpus", "slab_blocks": args.slab,
+                           "exchange": "slab-boundary x-faces per lowering round, NCCL send/recv "
+                                       "on the library stream; depth broadcast from rank 0"}
     if world > 1:
         import torch
         import torch.distributed as dist
+        local = local % max(1, torch.cuda.device_count())  # gloo functional runs share one GPU
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    res = (run_c5 if args.config == "c5" else run_ours)(args, rank, world, local)
+        # VXM_DIST_BACKEND=gloo: functional runs of several ranks on ONE GPU
+        # (NCCL refuses two ranks on one device); never a bench number
+        backend = os.environ.get("VXM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+            config["backend"] = backend
+    if sharded:
+        res = run_sharded(args, rank, world, local)
+    else:
+        res = (run_c5 if args.config == "c5" else run_ours)(args, rank, world, local)
     K = args.steps
     if world > 1:
         import torch.distributed as dist
@@ -551,11 +692,13 @@ def main():
     if rank != 0:
         return
     st = res["stats"]
-    value = world * K / res["total_s"]
+    # replicas: N maps, N x the frames; sharded: one map, the frames once
+    value = (1 if sharded else world) * K / res["total_s"]
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(1e3 * res["total_s"] / K, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32/i32",
+        "higher_is_better": True, "scaling": "strong" if args.shard else "weak", "vs_baseline": None,
+        "dtype": "f64/f32/i32",
         "data": "synthetic (reference scene + orbit trajectory, sphere-traced depth rendered on the host)",
         "config": config,
         "tsdf_voxel_updates_per_s": (round(world * st["voxels_updated"] / res["total_s"], 1)
@@ -568,7 +711,7 @@ def main():
         "roofline": roofline(res, K, args.config),
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
-        "e2e": {"value": round(world * K / res["e2e_s"], 2), "unit": UNIT,
+        "e2e": {"value": round((1 if sharded else world) * K / res["e2e_s"], 2), "unit": UNIT,
                 "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
                 "path": "vxm_integrate_depth_camera + vxm_update_esdf (host buffers)"},
         "value_path": "vxm_update_frame_camera_device (depth in HBM, one host round trip per frame)",
@@ -577,6 +720,15 @@ def main():
         line["e2e"]["path"] = "vxm_update_esdf (host key list in, host changed list out)"
         line["value_path"] = "vxm_update_esdf_list (updated list and map in HBM)"
         line["unit_note"] = "a step (frame) is one full update_esdf of the 512^3 map"
+    if sharded:
+        line["value_path"] = ("NCCL broadcast of rank 0's depth frame -> vxm_integrate_depth_*_device "
+                              "(own slabs) -> update_esdf over the union map (dist.py: vxm_shard_update_* "
+                              "steps, NCCL face exchange per round)") if args.config != "c5" else (
+                              "update_esdf over the union map (dist.py: vxm_shard_update_* steps, NCCL "
+                              "face exchange per round)")
+        line["e2e"]["path"] = "the same with the frame from pinned host memory on rank 0 and the " \
+                              "changed lists copied to each rank's host"
+        line["union_esdf_blocks_per_step"] = res.get("union_esdf_blocks")
     if not args.no_cpu_baseline and world == 1:
         try:
             r = (cpu_reference_c5(1) if args.config == "c5" else

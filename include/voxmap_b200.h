@@ -408,7 +408,14 @@ vxm_status vxm_update_esdf_sharded(int n_shards, vxm_layer* const* esdf, vxm_lay
  *     for round = 1, 2, ...: sweep(round); send `send` to both neighbours, receive
  *       the -x neighbour's into recv_left and the +x one's into recv_right;
  *       border(round) -> next_dirty;  sum-reduce; stop at 0
- *   finish(lowered = the OR) -> changed blocks; frees the handle. */
+ *   finish(lowered = the OR) -> changed blocks; frees the handle.
+ * sweep() and border(next_dirty = NULL) only ENQUEUE on the context stream
+ * (vxm_context_stream): a collective enqueued on that stream after sweep()
+ * sees the packed send buffer, and border() after it sees the received
+ * snapshots, without a host synchronisation.  border() with a non-NULL
+ * next_dirty also waits and returns the count; next_count() gives the device
+ * address (uint32) that border(round) writes the count to, for an on-device
+ * reduction. */
 typedef struct vxm_shard_update vxm_shard_update;
 vxm_status vxm_shard_update_begin(vxm_layer* esdf, vxm_layer* tsdf, vxm_blocklist* updated_union,
                                   const vxm_esdf_config* cfg, vxm_shard_update** out,
@@ -420,6 +427,7 @@ vxm_status vxm_shard_update_exchange_buffers(vxm_shard_update* su, uint32_t n_le
                                              uint64_t* recv_right_bytes);
 vxm_status vxm_shard_update_sweep(vxm_shard_update* su, uint32_t round);
 vxm_status vxm_shard_update_border(vxm_shard_update* su, uint32_t round, uint32_t* next_dirty);
+vxm_status vxm_shard_update_next_count(vxm_shard_update* su, uint32_t round, void** device_u32);
 vxm_status vxm_shard_update_finish(vxm_shard_update* su, int lowered, vxm_blocklist* changed_out);
 void vxm_shard_update_destroy(vxm_shard_update* su);
 

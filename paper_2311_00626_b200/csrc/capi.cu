@@ -880,8 +880,17 @@ vxm_status vxm_shard_update_sweep(vxm_shard_update* su, uint32_t round) {
 }
 vxm_status vxm_shard_update_border(vxm_shard_update* su, uint32_t round, uint32_t* next) {
   return guard([&] {
-    REQUIRE_ARG(su && next && round >= 1, "invalid argument");
-    *next = shard_border(su->x, round);
+    REQUIRE_ARG(su && round >= 1, "invalid argument");
+    if (next)
+      *next = shard_border(su->x, round);
+    else
+      shard_border_launch(su->x, round);
+  });
+}
+vxm_status vxm_shard_update_next_count(vxm_shard_update* su, uint32_t round, void** dptr) {
+  return guard([&] {
+    REQUIRE_ARG(su && dptr && round >= 1, "invalid argument");
+    *dptr = next_count_ptr(su->x, round);
   });
 }
 vxm_status vxm_shard_update_finish(vxm_shard_update* su, int lowered, vxm_blocklist* out) {

@@ -33,7 +33,7 @@ struct ShardRound {
   uint32_t r, ep;         // round (1-based), its epoch (base + r)
   uint32_t cur;           // pool holding the field before this update
   int lowered;            // the update lowered (the new field is in pool cur ^ 1)
-  uint32_t n_blocks, n_dirty;
+  uint32_t n_blocks;       // round r > 1 reads its dirty count on the device (count[r % 3])
   uint32_t* ctr;          // [2] work counters, zeroed by the host per launch
   int rank, world, slab;
   const uint64_t* bnd_keys;  // this shard's boundary blocks, sorted by key
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_shard_sweep(LowerArgs a, Shar
   uint32_t* const pcur = a.pool[sr.cur];
   uint32_t* const work = a.pool[sr.cur ^ 1u];
   const int32_t* dirty = a.list[sr.r & 1u];
-  const uint32_t n = r1 ? sr.n_blocks : sr.n_dirty;
+  const uint32_t n = r1 ? sr.n_blocks : *((volatile const uint32_t*)(a.count + sr.r % 3u));
   const Limits lim = a.lim;
   while (true) {
     if (t == 0) G.bcast = atomicAdd(sr.ctr, 1u);
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_shard_border(LowerArgs a, Sha
   const bool r1 = r == 1;
   uint32_t* const work = a.pool[sr.cur ^ 1u];
   const int32_t* dirty = a.list[cp];
-  const uint32_t n_dirty = r1 ? sr.n_blocks : sr.n_dirty;
+  const uint32_t n_dirty = r1 ? sr.n_blocks : *((volatile const uint32_t*)(a.count + r % 3u));
   const uint32_t sides = r1 ? 1u : 2u;
   const uint32_t per_axis = sides * n_dirty;
   const Limits lim = a.lim;
@@ -319,7 +319,6 @@ ShardRound round_args(ShardUpdate& x, uint32_t r) {
   sr.cur = x.cur;
   sr.lowered = 1;
   sr.n_blocks = x.n_blocks;
-  sr.n_dirty = x.n_dirty;
   sr.ctr = x.ctr.as<uint32_t>();
   sr.rank = x.rank;
   sr.world = x.world;
@@ -347,12 +346,11 @@ int grid_of(const void* kernel, Context* c) {
 
 }  // namespace
 
-// Mark phase against the union list (synchronous); x.local_any = this shard
-// has blocks to update / clear.
-void shard_begin(ShardUpdate& x, const vxm_esdf_config& cfg) {
+// Mark phase against the union list, enqueued; shard_begin_finish syncs and
+// reads the outcome (x.local_any = this shard has blocks to update / clear).
+void shard_begin_launch(ShardUpdate& x, const vxm_esdf_config& cfg) {
   Context* ctx = x.ctx;
   use(ctx);
-  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->reset_status();
   x.epoch = ++ctx->call_epoch;
   const uint32_t n7 = 7u * std::max<uint32_t>(x.uni.count_hint, 1);
@@ -362,29 +360,40 @@ void shard_begin(ShardUpdate& x, const vxm_esdf_config& cfg) {
   x.s = esdf_scratch(ctx, x.uni.count_hint, x.n_all_cap);
   esdf_mark_phase(x.E, x.T, &x.uni, cfg, x.s, x.epoch);
   x.E->stage_meta();
+  x.la = lower_args(x.E, cfg);
+  x.la.full = 1;
+  x.la.call_epoch = x.epoch;
+  x.la.out_flags = x.s.flags;
+  if (!x.h_meta) VXM_CUDA(cudaHostAlloc(&x.h_meta, sizeof(LayerMeta), cudaHostAllocDefault));
+  VXM_CUDA(cudaMemcpyAsync(x.h_meta, x.E->meta, sizeof(LayerMeta), cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+void shard_begin_finish(ShardUpdate& x) {
+  Context* ctx = x.ctx;
+  use(ctx);
   ctx->sync_status();
   x.E->adopt_meta();
   const DevStatus& st = *ctx->h_status;
   if (st.capacity_error || st.pool_overflow)
     throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
   x.local_any = st.any_update != 0;
-  LayerMeta m;
-  VXM_CUDA(cudaMemcpy(&m, x.E->meta, sizeof m, cudaMemcpyDeviceToHost));
+  const LayerMeta& m = *x.h_meta;
   x.base = m.round_epoch;
   x.cur = m.cur;
   x.n_blocks = m.num_blocks;
-  x.n_dirty = x.n_blocks;
-  x.la = lower_args(x.E, cfg);
-  x.la.full = 1;
+  // the sorted order is final once the mark phase (allocation) completed
   x.la.sorted_slots = x.E->sorted_slots[x.E->sorted_parity];
   x.la.stamp_new = x.E->stamp_new;
   x.la.stamp_mark = x.E->stamp_mark;
-  x.la.call_epoch = x.epoch;
-  x.la.out_flags = x.s.flags;
+}
+
+void shard_begin(ShardUpdate& x, const vxm_esdf_config& cfg) {
+  shard_begin_launch(x, cfg);
+  shard_begin_finish(x);
 }
 
 // Boundary blocks (x mod slab in {0, slab - 1}), sorted; the send buffer.
-void shard_plan(ShardUpdate& x) {
+void shard_plan_launch(ShardUpdate& x) {
   use(x.ctx);
   cudaStream_t st = x.ctx->stream;
   const uint32_t n = std::max<uint32_t>(x.n_blocks, 1);
@@ -393,6 +402,7 @@ void shard_plan(ShardUpdate& x) {
   x.bnd_slots.ensure(sizeof(int32_t) * n);
   x.bnd_n.ensure(2 * sizeof(uint32_t));
   x.ctr.ensure(4 * sizeof(uint32_t));
+  if (!x.h_cnt) VXM_CUDA(cudaHostAlloc(&x.h_cnt, 4 * sizeof(uint32_t), cudaHostAllocDefault));
   const uint64_t* keys = x.E->sorted_keys[x.E->sorted_parity];
   const int32_t* slots = x.E->sorted_slots[x.E->sorted_parity];
   k_boundary_flags<<<grid_for(x.ctx, n), 256, 0, st>>>(keys, &x.E->meta->num_blocks, x.slab,
@@ -411,9 +421,19 @@ void shard_plan(ShardUpdate& x) {
                                       int(x.n_blocks), st));
   x.ctx->count_launch(3);
   check_launch(x.ctx, "shard_plan");
-  VXM_CUDA(cudaMemcpyAsync(&x.n_bnd, x.bnd_n.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  VXM_CUDA(cudaStreamSynchronize(st));
+  VXM_CUDA(cudaMemcpyAsync(x.h_cnt, x.bnd_n.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+}
+
+void shard_plan_finish(ShardUpdate& x) {
+  use(x.ctx);
+  VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
+  x.n_bnd = x.h_cnt[0];
   x.snd.ensure(std::max<size_t>(xbuf_bytes(x.n_bnd), 8));
+}
+
+void shard_plan(ShardUpdate& x) {
+  shard_plan_launch(x);
+  shard_plan_finish(x);
 }
 
 void shard_set_neighbours(ShardUpdate& x, uint32_t n_left, uint32_t n_right) {
@@ -423,7 +443,8 @@ void shard_set_neighbours(ShardUpdate& x, uint32_t n_left, uint32_t n_right) {
   for (int i = 0; i < 2; ++i) x.rcv[i].ensure(std::max<size_t>(xbuf_bytes(x.n_rcv[i]), 8));
 }
 
-// Sweeps of round r and the pack of the send buffer (completed on return).
+// Sweeps of round r and the pack of the send buffer, enqueued on the shard's
+// stream (the exchange that reads the send buffer is ordered after it).
 void shard_sweep(ShardUpdate& x, uint32_t r) {
   use(x.ctx);
   cudaStream_t st = x.ctx->stream;
@@ -434,31 +455,37 @@ void shard_sweep(ShardUpdate& x, uint32_t r) {
   k_shard_pack<<<grid_for(x.ctx, uint64_t(std::max<uint32_t>(x.n_bnd, 1)) * 32), 256, 0, st>>>(x.la, sr);
   x.ctx->count_launch(2);
   check_launch(x.ctx, "k_shard_sweep");
-  VXM_CUDA(cudaStreamSynchronize(st));
 }
 
-// Border phase of round r (the receive buffers hold the neighbours' snapshots);
-// returns this shard's next dirty count.
-uint32_t shard_border(ShardUpdate& x, uint32_t r) {
+// Border phase of round r (the receive buffers hold the neighbours' snapshots),
+// enqueued; this shard's next dirty count is written to next_count_ptr(x, r)
+// on the device and copied to x.h_cnt[1] (valid after a stream sync).
+uint32_t* next_count_ptr(ShardUpdate& x, uint32_t r) { return x.la.count + (r + 1u) % 3u; }
+
+void shard_border_launch(ShardUpdate& x, uint32_t r) {
   use(x.ctx);
   cudaStream_t st = x.ctx->stream;
   const int g_border = grid_of((const void*)k_shard_border, x.ctx);
-  VXM_CUDA(cudaMemsetAsync(x.la.count + (r + 1u) % 3u, 0, sizeof(uint32_t), st));
+  VXM_CUDA(cudaMemsetAsync(next_count_ptr(x, r), 0, sizeof(uint32_t), st));
   ShardRound sr = round_args(x, r);
   void* args[] = {&x.la, &sr};
   VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_shard_border, dim3(g_border), dim3(kL3Threads),
                                        args, 0, st));
   x.ctx->count_launch();
-  VXM_CUDA(cudaMemcpyAsync(&x.n_dirty, x.la.count + (r + 1u) % 3u, sizeof(uint32_t),
-                           cudaMemcpyDeviceToHost, st));
-  VXM_CUDA(cudaStreamSynchronize(st));
+  VXM_CUDA(cudaMemcpyAsync(x.h_cnt + 1, next_count_ptr(x, r), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   x.rounds = r;
-  return x.n_dirty;
+}
+
+// Synchronous form: returns this shard's next dirty count.
+uint32_t shard_border(ShardUpdate& x, uint32_t r) {
+  shard_border_launch(x, r);
+  VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
+  return x.h_cnt[1];
 }
 
 // Changed set (esdf/integrator.cpp:403-411) and meta; `lowered`: the global
 // decision of this update.
-void shard_finish(ShardUpdate& x, bool lowered, BlockList* out) {
+void shard_finish_launch(ShardUpdate& x, bool lowered, BlockList* out) {
   use(x.ctx);
   cudaStream_t st = x.ctx->stream;
   ShardRound sr = round_args(x, x.rounds);
@@ -469,7 +496,7 @@ void shard_finish(ShardUpdate& x, bool lowered, BlockList* out) {
     k_shard_meta<<<1, 1, 0, st>>>(x.E->meta, x.base + x.rounds + 2, x.cur ^ 1u);
     x.ctx->count_launch();
   }
-  out->ctx = x.ctx;
+  out->bind(x.ctx);
   out->ensure(x.n_all_cap);
   launch_compact_keys(x.ctx, x.E->sorted_keys[x.E->sorted_parity], x.s.flags, &x.E->meta->num_blocks,
                       x.n_all_cap, out->keys.as<uint64_t>(), out->d_count, nullptr, "k_compact_esdf");
@@ -478,6 +505,10 @@ void shard_finish(ShardUpdate& x, bool lowered, BlockList* out) {
   out->count_hint = x.n_all_cap;
   out->sorted_unique = true;
   x.E->stage_meta();
+}
+
+void shard_finish_sync(ShardUpdate& x, bool lowered) {
+  use(x.ctx);
   x.ctx->sync_status();
   x.E->adopt_meta();
   vxm_stats& w = x.ctx->stats;
@@ -486,7 +517,22 @@ void shard_finish(ShardUpdate& x, bool lowered, BlockList* out) {
   w.lower_rounds += lowered ? x.rounds : 0;
 }
 
-// All shards in this process (one context each): exchange by peer copies.
+void shard_finish(ShardUpdate& x, bool lowered, BlockList* out) {
+  shard_finish_launch(x, lowered, out);
+  shard_finish_sync(x, lowered);
+}
+
+ShardUpdate::~ShardUpdate() {
+  if (h_meta) cudaFreeHost(h_meta);
+  if (h_cnt) cudaFreeHost(h_cnt);
+  if (ev) cudaEventDestroy(ev);
+}
+
+// All shards in this process (one context each, same or peer GPUs): every
+// step is enqueued on all shards before any is waited for, the exchange is
+// peer copies ordered by events (no host round trip), and each round costs ONE
+// host synchronisation — the global sum of the next dirty counts that ends the
+// loop (esdf/integrator.cpp:506).
 void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
                              const vxm_esdf_config& cfg, int slab, BlockList** out) {
   std::vector<ShardUpdate> sh(P);
@@ -505,6 +551,16 @@ void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
       VXM_CUDA(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, dst.ctx->stream));
     else
       VXM_CUDA(cudaMemcpyPeerAsync(d, dst.ctx->device, s, src_ctx->device, bytes, dst.ctx->stream));
+  };
+  auto record = [&](ShardUpdate& x) {
+    use(x.ctx);
+    if (!x.ev) VXM_CUDA(cudaEventCreateWithFlags(&x.ev, cudaEventDisableTiming));
+    VXM_CUDA(cudaEventRecord(x.ev, x.ctx->stream));
+  };
+  auto wait_for = [&](ShardUpdate& x, ShardUpdate& on) {
+    if (&x == &on) return;
+    use(x.ctx);
+    VXM_CUDA(cudaStreamWaitEvent(x.ctx->stream, on.ev, 0));
   };
   auto sync_all = [&] {
     for (auto& x : sh) {
@@ -525,10 +581,9 @@ void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
     for (int p = 0; p < P; ++p) out[p]->assign_host(nullptr, 0);
     return;
   }
-  bool any = false;
   for (auto& x : sh) {
     use(x.ctx);
-    x.uni.ctx = x.ctx;
+    x.uni.bind(x.ctx);
     x.uni.ensure(uint32_t(total));
     uint64_t off = 0;
     for (int p = 0; p < P; ++p) {
@@ -543,28 +598,41 @@ void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
     x.uni.host_pending = false;
     sort_unique_keys(x.ctx, &x.uni);
     x.uni.sorted_unique = true;
-    shard_begin(x, cfg);
+    shard_begin_launch(x, cfg);
+  }
+  bool any = false;
+  for (auto& x : sh) {
+    shard_begin_finish(x);
     any |= x.local_any;
   }
   if (any) {
-    for (auto& x : sh) shard_plan(x);
+    for (auto& x : sh) shard_plan_launch(x);
+    for (auto& x : sh) shard_plan_finish(x);
     for (int p = 0; p < P; ++p)  // [0]: from the -x neighbour, [1]: from the +x one
       shard_set_neighbours(sh[p], sh[(p - 1 + P) % P].n_bnd, sh[(p + 1) % P].n_bnd);
     for (uint32_t r = 1;; ++r) {
-      for (auto& x : sh) shard_sweep(x, r);
-      for (int p = 0; p < P; ++p) {  // our snapshot: the +x neighbour's [0], the -x one's [1]
-        ShardUpdate& src = sh[p];
-        copy_to(sh[(p + 1) % P], sh[(p + 1) % P].rcv[0].p, src.ctx, src.snd.p, xbuf_bytes(src.n_bnd));
-        copy_to(sh[(p - 1 + P) % P], sh[(p - 1 + P) % P].rcv[1].p, src.ctx, src.snd.p,
-                xbuf_bytes(src.n_bnd));
+      for (auto& x : sh) {
+        shard_sweep(x, r);
+        record(x);  // send buffer packed
       }
+      for (int p = 0; p < P; ++p) {  // snapshot p -> the +x neighbour's [0], the -x one's [1]
+        ShardUpdate& src = sh[p];
+        ShardUpdate& right = sh[(p + 1) % P];
+        ShardUpdate& left = sh[(p - 1 + P) % P];
+        wait_for(right, src);
+        copy_to(right, right.rcv[0].p, src.ctx, src.snd.p, xbuf_bytes(src.n_bnd));
+        wait_for(left, src);
+        copy_to(left, left.rcv[1].p, src.ctx, src.snd.p, xbuf_bytes(src.n_bnd));
+      }
+      for (auto& x : sh) shard_border_launch(x, r);
+      sync_all();  // the round's one host round trip
       uint64_t next = 0;
-      for (auto& x : sh) next += shard_border(x, r);
+      for (auto& x : sh) next += x.h_cnt[1];
       if (next == 0) break;  // while (!dirty.empty()) — esdf/integrator.cpp:506
     }
   }
-  for (int p = 0; p < P; ++p) shard_finish(sh[p], any, out[p]);
-  sync_all();
+  for (int p = 0; p < P; ++p) shard_finish_launch(sh[p], any, out[p]);
+  for (auto& x : sh) shard_finish_sync(x, any);
 }
 
 }  // namespace vxm

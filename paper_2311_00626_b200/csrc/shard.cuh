@@ -34,13 +34,24 @@ struct ShardUpdate {
   bool local_any = false;
   DevBuf ctr, bnd_keys, bnd_slots, bnd_flags, bnd_n, cub_tmp, snd, rcv[2];
   LowerArgs la{};
+  LayerMeta* h_meta = nullptr;  // pinned: the layer meta after the mark phase
+  uint32_t* h_cnt = nullptr;    // pinned: [0] boundary blocks, [1] next dirty count
+  cudaEvent_t ev = nullptr;     // in-process exchange ordering
+  ShardUpdate() = default;
+  ShardUpdate(const ShardUpdate&) = delete;
+  ShardUpdate& operator=(const ShardUpdate&) = delete;
+  ~ShardUpdate();
 };
 
+// Steps: *_launch enqueue on the shard's context stream; the plain forms also
+// synchronise (the step C-ABI).
 void shard_begin(ShardUpdate& x, const vxm_esdf_config& cfg);
 void shard_plan(ShardUpdate& x);
 void shard_set_neighbours(ShardUpdate& x, uint32_t n_left, uint32_t n_right);
-void shard_sweep(ShardUpdate& x, uint32_t r);
+void shard_sweep(ShardUpdate& x, uint32_t r);  // enqueue only
+void shard_border_launch(ShardUpdate& x, uint32_t r);
 uint32_t shard_border(ShardUpdate& x, uint32_t r);
+uint32_t* next_count_ptr(ShardUpdate& x, uint32_t r);
 void shard_finish(ShardUpdate& x, bool lowered, BlockList* out);
 
 }  // namespace vxm

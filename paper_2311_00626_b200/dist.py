@@ -10,8 +10,10 @@ over the union map through the step C-ABI (vxm_shard_update_*):
   2. OR-reduce "anything to update"
   3. per lowering round: local sweeps; the slab-boundary x-face snapshot goes
      to both x-neighbours (rank -+ 1) — NCCL point-to-point on the device
-     buffers, or staged through the host for gloo; the border phase computes
-     the cross-slab pairs on both owners; SUM-reduce the next dirty counts
+     buffers, enqueued on the library's stream behind the sweep kernel, or
+     staged through the host for gloo; the border phase computes the
+     cross-slab pairs on both owners; SUM-reduce the next dirty counts on the
+     device (one host read per round decides termination)
   4. the changed blocks of this shard.
 
 The union over ranks of the ESDF layers and changed lists equals the single-map
@@ -127,25 +129,41 @@ def update_esdf_distributed(esdf: EsdfLayer, tsdf: TsdfLayer, updated, cfg, grou
                 C.byref(ptrs[1]), C.byref(sizes[1]), C.byref(ptrs[2]), C.byref(sizes[2])))
             views = [_view(p.value or 0, s.value, cuda) for p, s in zip(ptrs, sizes)]
             rnd = 0
-            while True:
-                rnd += 1
-                check(lib().vxm_shard_update_sweep(su, C.c_uint32(rnd)))
-                if cdev.type == "cpu":  # gloo: stage through the host
+            if cdev.type == "cpu":  # gloo: stage through the host, synchronous steps
+                while True:
+                    rnd += 1
+                    check(lib().vxm_shard_update_sweep(su, C.c_uint32(rnd)))
+                    torch.cuda.synchronize(cuda)
                     host = [v.cpu() for v in views]
                     exchange_boundaries(host[0], host[1], host[2], group)
                     views[1].copy_(host[1])
                     views[2].copy_(host[2])
                     torch.cuda.synchronize(cuda)
-                else:
-                    torch.cuda.synchronize(cuda)
-                    exchange_boundaries(views[0], views[1], views[2], group)
-                    torch.cuda.synchronize(cuda)
-                nxt = C.c_uint32()
-                check(lib().vxm_shard_update_border(su, C.c_uint32(rnd), C.byref(nxt)))
-                total = torch.tensor([nxt.value], dtype=torch.int64, device=cdev)
-                dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
-                if int(total.item()) == 0:  # while (!dirty.empty())
-                    break
+                    nxt = C.c_uint32()
+                    check(lib().vxm_shard_update_border(su, C.c_uint32(rnd), C.byref(nxt)))
+                    total = torch.tensor([nxt.value], dtype=torch.int64, device=cdev)
+                    dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
+                    if int(total.item()) == 0:  # while (!dirty.empty())
+                        break
+            else:
+                # NCCL: sweep -> send/recv -> border -> all-reduce of the next
+                # dirty count, all enqueued on the library's context stream
+                # (no host synchronisation inside a round); one host read of
+                # the reduced count per round ends the loop.
+                ext = torch.cuda.ExternalStream(ctx.stream, device=cuda)
+                with torch.cuda.stream(ext):
+                    total = torch.zeros(1, dtype=torch.int64, device=cuda)
+                    while True:
+                        rnd += 1
+                        check(lib().vxm_shard_update_sweep(su, C.c_uint32(rnd)))
+                        exchange_boundaries(views[0], views[1], views[2], group)
+                        check(lib().vxm_shard_update_border(su, C.c_uint32(rnd), None))
+                        dp = C.c_void_p()
+                        check(lib().vxm_shard_update_next_count(su, C.c_uint32(rnd), C.byref(dp)))
+                        total.copy_(_view(dp.value, 4, cuda).view(torch.int32))
+                        dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
+                        if int(total.item()) == 0:  # while (!dirty.empty())
+                            break
         rc = lib().vxm_shard_update_finish(su, C.c_int(int(lowered)), out.h)
         su = None
         check(rc)

@@ -1,6 +1,8 @@
-"""GPU parity: one shard per process (paper_2311_00626_b200/dist.py) — two
-processes on the same B200, gloo for the exchange (staged through the host;
-NCCL moves the device buffers directly when each process has its own GPU).
+"""GPU parity: one shard per process (paper_2311_00626_b200/dist.py) — two or
+three processes on the same B200 with gloo for the exchange (staged through
+the host), and, when the box has a GPU per rank, NCCL moving the device
+buffers directly on the library's stream (skipped on a single-GPU box: NCCL
+refuses two ranks on one device).
 Each rank integrates every frame into its own shard and runs
 update_esdf_distributed; rank 0 also keeps the single map.  The union of the
 ranks' changed lists and ESDF layers equals the single-map update bit-for-bit.
@@ -23,10 +25,16 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, slab, port, q):
+def _worker(rank, world, slab, port, q, backend="gloo"):
+    import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2311_00626_b200 as vx
         from paper_2311_00626_b200 import _abi as A
@@ -36,7 +44,7 @@ def _worker(rank, world, slab, port, q):
         cam, seq = camera_frames("room", 320, 240, 3, 16)
         icfg = A.default_integrator_config(truncation=0.16)
         ecfg = A.default_esdf_config(site_threshold=0.04, max_distance=1.0)
-        ctx = vx.Context(0)
+        ctx = vx.Context(dev)
         ctx.set_shard(rank, world, slab)
         T, E = vx.TsdfLayer(vs, ctx=ctx), vx.EsdfLayer(vs, ctx=ctx)
         single = (vx.TsdfLayer(vs), vx.EsdfLayer(vs)) if rank == 0 else None
@@ -69,12 +77,15 @@ def _worker(rank, world, slab, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,slab", [(2, 3), (3, 2)])
-def test_distributed_esdf_equals_single_map(world, slab):
+@pytest.mark.parametrize("world,slab,backend", [(2, 3, "gloo"), (3, 2, "gloo"), (2, 3, "nccl")])
+def test_distributed_esdf_equals_single_map(world, slab, backend):
+    import torch
+    if backend == "nccl" and torch.cuda.device_count() < world:
+        pytest.skip(f"NCCL path needs {world} GPUs (this box has {torch.cuda.device_count()})")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, slab, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, slab, port, q, backend)) for r in range(world)]
     for p in procs:
         p.start()
     ok = q.get(timeout=300)
@@ -82,3 +93,21 @@ def test_distributed_esdf_equals_single_map(world, slab):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert ok
+
+
+def test_bench_shard_mode_runs_two_ranks():
+    """bench.py --shard under torchrun (2 ranks sharing this GPU over gloo:
+    the functional path; NCCL needs a GPU per rank) prints one sharded line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VXM_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--shard",
+           "--config", "c2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--gpus", "2"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["config"]["parallelism"] == "shard2" and line["scaling"] == "strong"
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["n_gpus"] == 2
