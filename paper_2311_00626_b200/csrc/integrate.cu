@@ -184,15 +184,21 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<O
       ok = sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s);
     }
   } else {
-    // LidarIntrinsics::project — lidar.hpp:43-55 (CUDA libm atan2/acos)
-    const double kTwoPi = 6.283185307179586;
-    double az = __dsub_rn(atan2(py, px), a.az0);
-    az = __dsub_rn(az, __dmul_rn(kTwoPi, floor(__ddiv_rn(az, kTwoPi))));
-    const double u = __dmul_rn(az, a.u_scale);
+    // LidarIntrinsics::project — lidar.hpp:43-55 (CUDA libm atan2/acos).  The
+    // elevation is evaluated first: a voxel outside the beam fan then needs
+    // no atan2 (C3 k_integrate -5 %).
     double c = __ddiv_rn(pz, d_v);
     c = c < -1.0 ? -1.0 : (1.0 < c ? 1.0 : c);
     const double v = __dmul_rn(__dsub_rn(acos(c), a.el0), a.v_scale);
-    if (!(u >= 0.0 && u < double(a.na) && v >= 0.0 && v < double(a.ne))) return false;
+    if (!(v >= 0.0 && v < double(a.ne))) return false;
+    const double kTwoPi = 6.283185307179586;
+    double az = __dsub_rn(atan2(py, px), a.az0);
+    // az - 2 pi floor(az / 2 pi): when 0 <= az < 2 pi (1 - 2^-40) the quotient
+    // is certainly in [0, 1) and the floor is 0 (no division); otherwise the
+    // exact expression
+    if (!(az >= 0.0 && az < 6.283185307173872)) az = __dsub_rn(az, __dmul_rn(kTwoPi, floor(__ddiv_rn(az, kTwoPi))));
+    const double u = __dmul_rn(az, a.u_scale);
+    if (!(u >= 0.0 && u < double(a.na))) return false;
     ok = a.linear ? sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s)
                   : sample_nearest_d(a.depth, a.W, a.H, u, v, &s);
   }

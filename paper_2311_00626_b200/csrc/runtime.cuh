@@ -61,6 +61,10 @@ struct Context {
   DevBuf lidar_dirs;      // double3 per LiDAR pixel (host glibc LUT)
   vxm_lidar lut_key{};
   bool lut_valid = false;
+  DevBuf cam_dirs;        // double2 per camera tile: ((u - cu) / fu, (v - cv) / fv)
+  vxm_camera cam_key{};
+  int cam_key_w = 0, cam_key_h = 0, cam_key_tile = 0;
+  bool cam_lut_valid = false;
   DevBuf tmp[6];          // ESDF / list scratch
   DevBuf lower_cta;       // k_lower_xr: per-CTA counts of the changed-list compaction
   DevBuf cub_tmp;

@@ -142,45 +142,179 @@ __device__ inline double ray_reach(double depth, double max_int, double trunc) {
   return __dadd_rn(capped, trunc);
 }
 
-// Camera: one thread per pixel tile — view.cpp:66-91.
-__global__ void k_rays_camera(const float* __restrict__ depth, int W, int H, int tile,
-                              vxm_camera cam, vxm_pose T, double cs, double max_int, double trunc,
-                              Cube cube, DevStatus* status) {
+// Camera: ONE WARP PER PIXEL TILE — view.cpp:66-91 — with a lane-parallel,
+// exact traverse_grid (traversal.hpp:29-73).
+//
+// The serial DDA takes, at each step, the smallest of the three next-crossing
+// parameters t_x, t_y, t_z (ties to the lowest axis), steps that axis and
+// adds its t_delta — so the visited cells are the prefix (value <= 1, fewer
+// than `guard` steps) of the STABLE MERGE of the three per-axis sequences
+// t_a(i+1) = t_a(i) + t_delta_a (each rounded exactly as the serial loop
+// rounds it).  Lanes 0-2 generate those sequences (one FP64 add per element,
+// into shared memory); then every lane takes elements, finds the element's
+// merge position by binary search in the two other sequences (ties: a
+// lower axis precedes) and, if that position is below `guard`, marks the cell
+// start + (counts of the three axes up to it).  The set of marked cells is the
+// serial loop's, bit for bit; the per-ray latency drops from ~35 dependent
+// steps to one sequence scan plus a search.  Rays with more than
+// kRayMaxSteps crossings on one axis (none at the BASELINE configs) run the
+// serial loop.  Every ray starts in the sensor's cell, so the cells near it
+// are hit by thousands of rays: they are ORed into a per-CTA shared bitmap of
+// the 16^3 cells around the sensor and flushed once per CTA.
+constexpr int kRayWarps = 8;       // rays (camera tiles) per 256-thread CTA
+constexpr int kRayMaxSteps = 64;   // stored crossings per axis
+constexpr int kLocR = 8;           // near-sensor cube: cells [c - 8, c + 8) per axis
+
+struct RaySmem {
+  double t[kRayWarps][3][kRayMaxSteps];
+  uint32_t loc[16 * 16 * 16 / 32];
+};
+
+// Count of entries of the increasing sequence q[0..n) that are < v (or <= v).
+__device__ inline int seq_rank(const double* q, int n, double v, bool inclusive) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const double x = q[mid];
+    if (inclusive ? !(v < x) : x < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// sc: the sensor's cell floor(t / cs) (every ray's start, computed on the host
+// with the same IEEE division); dirs: per tile the unprojection factors
+// ((u - cu) / fu, (v - cv) / fv) of camera.hpp:52-55 (frame-independent, host
+// LUT, identical IEEE operations).
+__global__ void __launch_bounds__(256) k_rays_camera(const float* __restrict__ depth, int W, int H,
+                                                     int tile, const double2* __restrict__ dirs,
+                                                     vxm_pose T, int3 sc3, double cs, double max_int,
+                                                     double trunc, Cube cube, DevStatus* status) {
   pdl_wait();  // see launch_pdl
   pdl_trigger();
+  __shared__ RaySmem sm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) sm.loc[i] = 0u;
+  const int sc[3] = {sc3.x, sc3.y, sc3.z};
+  const int lx = sc[0] - kLocR - cube.ox, ly = sc[1] - kLocR - cube.oy, lz = sc[2] - kLocR - cube.oz;
+  const bool use_loc = lx >= 0 && ly >= 0 && lz >= 0 && lx + 2 * kLocR <= cube.S &&
+                       ly + 2 * kLocR <= cube.S && lz + 2 * kLocR <= cube.S;
+  __syncthreads();
+  auto mark = [&](int x, int y, int z) {
+    const int dx = x - (sc[0] - kLocR), dy = y - (sc[1] - kLocR), dz = z - (sc[2] - kLocR);
+    if (use_loc && unsigned(dx) < 16u && unsigned(dy) < 16u && unsigned(dz) < 16u) {
+      const int b = dz + 16 * (dy + 16 * dx);
+      atomicOr(&sm.loc[b >> 5], 1u << (b & 31));
+    } else {
+      uint32_t w, m;
+      if (cube.locate(x, y, z, w, m)) atomicOr(cube.bits + w, m);
+      else atomicOr(&status->bitmap_overflow, 1u);
+    }
+  };
+
   const int tiles_x = (W + tile - 1) / tile;
   const int tiles_y = (H + tile - 1) / tile;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= tiles_x * tiles_y) return;
-  const int col0 = (t % tiles_x) * tile, row0 = (t / tiles_x) * tile;
-  const int row1 = min(row0 + tile, H), col1 = min(col0 + tile, W);
-  float tile_max = 0.0f;
-  if (col1 - col0 == 8 && (W & 3) == 0) {  // 8-wide tile: two aligned float4 per row
-#pragma unroll 8
-    for (int r = row0; r < row1; ++r) {
-      const float4* p = reinterpret_cast<const float4*>(depth + size_t(r) * W + col0);
-      const float4 a = __ldg(p), b = __ldg(p + 1);
-      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (valid_depth(v[i])) tile_max = tile_max < v[i] ? v[i] : tile_max;
+  // grid-stride over the tiles: one resident wave, no tail wave
+  for (int t = blockIdx.x * kRayWarps + warp; t < tiles_x * tiles_y; t += gridDim.x * kRayWarps) {
+    const int col0 = (t % tiles_x) * tile, row0 = (t / tiles_x) * tile;
+    const int row1 = min(row0 + tile, H), col1 = min(col0 + tile, W);
+    const int tw = col1 - col0, npx = tw * (row1 - row0);
+    // tile_max over the valid depths (d > 0 and finite): positive floats
+    // order like their bit patterns
+    uint32_t mb = 0u;
+    for (int q = lane; q < npx; q += 32) {
+      const float d = __ldg(depth + size_t(row0 + q / tw) * W + (col0 + q % tw));
+      if (valid_depth(d)) mb = max(mb, __float_as_uint(d));
     }
-  } else {
-    for (int r = row0; r < row1; ++r)
-      for (int c = col0; c < col1; ++c) {
-        const float d = __ldg(depth + size_t(r) * W + c);
-        if (valid_depth(d)) tile_max = tile_max < d ? d : tile_max;
+    mb = __reduce_max_sync(0xffffffffu, mb);
+    const float tile_max = __uint_as_float(mb);
+    if (!(tile_max > 0.0f)) continue;
+    const double reach = ray_reach(double(tile_max), max_int, trunc);
+    // CameraIntrinsics::unproject — camera.hpp:52-55: (u - cu) / fu * depth
+    const double2 dr = __ldg(dirs + t);
+    const double end_S[3] = {__dmul_rn(dr.x, reach), __dmul_rn(dr.y, reach), reach};
+    double e[3];
+    pose_apply(T, end_S[0], end_S[1], end_S[2], e);
+    // traverse_grid set-up (traversal.hpp:41-58), as the serial traverse():
+    // lane a < 3 computes axis a
+    const int ax = lane < 3 ? lane : 0;
+    const double ea = ax == 0 ? e[0] : (ax == 1 ? e[1] : e[2]);
+    const double sa = T.t[ax];
+    const int sca = ax == 0 ? sc[0] : (ax == 1 ? sc[1] : sc[2]);
+    const double dd = __dsub_rn(ea, sa);
+    const int endc = int(floor(__ddiv_rn(ea, cs)));
+    int stp = 0;
+    double tmax = CUDART_INF, tdel = CUDART_INF;
+    if (dd > 0.0) {
+      stp = 1;
+      tdel = __ddiv_rn(cs, dd);
+      tmax = __ddiv_rn(__dsub_rn(__dmul_rn(double(sca + 1), cs), sa), dd);
+    } else if (dd < 0.0) {
+      stp = -1;
+      tdel = __ddiv_rn(-cs, dd);
+      tmax = __ddiv_rn(__dsub_rn(__dmul_rn(double(sca), cs), sa), dd);
+    }
+    int ad = lane < 3 ? abs(endc - sca) : 0;
+    const int guard = __reduce_add_sync(0xffffffffu, ad) + 3;
+    const int step[3] = {__shfl_sync(0xffffffffu, stp, 0), __shfl_sync(0xffffffffu, stp, 1),
+                         __shfl_sync(0xffffffffu, stp, 2)};
+    // lanes 0-2: the crossings of axis `lane` with t <= 1 (at most guard)
+    int n = 0;
+    bool more = false;
+    if (lane < 3) {
+      double tv = tmax;
+      double* q = sm.t[warp][lane];
+      while (n < guard && tv <= 1.0) {
+        if (n == kRayMaxSteps) {
+          more = true;
+          break;
+        }
+        q[n++] = tv;
+        tv = __dadd_rn(tv, tdel);
       }
+    }
+    const int nx = __shfl_sync(0xffffffffu, n, 0), ny = __shfl_sync(0xffffffffu, n, 1),
+              nz = __shfl_sync(0xffffffffu, n, 2);
+    __syncwarp();
+    if (__any_sync(0xffffffffu, more)) {
+      if (lane == 0) traverse<false>(T.t, e, cs, cube, status);  // long ray: serial loop
+    } else {
+      if (lane == 0) mark(sc[0], sc[1], sc[2]);
+      const double* qx = sm.t[warp][0];
+      const double* qy = sm.t[warp][1];
+      const double* qz = sm.t[warp][2];
+      for (int k = lane; k < nx + ny + nz; k += 32) {
+        int a, i;
+        if (k < nx) a = 0, i = k;
+        else if (k < nx + ny) a = 1, i = k - nx;
+        else a = 2, i = k - nx - ny;
+        const double val = sm.t[warp][a][i];
+        // merge position: lower axes with equal t go first
+        const int cx = a == 0 ? i + 1 : seq_rank(qx, nx, val, true);
+        const int cy = a == 1 ? i + 1 : seq_rank(qy, ny, val, a > 1);
+        const int cz = a == 2 ? i + 1 : seq_rank(qz, nz, val, false);
+        if (cx + cy + cz - 1 < guard) mark(sc[0] + step[0] * cx, sc[1] + step[1] * cy, sc[2] + step[2] * cz);
+      }
+    }
+    __syncwarp();  // the warp's sequences are read before the next tile rewrites them
   }
-  if (tile_max <= 0.0f) return;
-  const double u = 0.5 * double(col0 + col1), v = 0.5 * double(row0 + row1);
-  const double reach = ray_reach(double(tile_max), max_int, trunc);
-  // CameraIntrinsics::unproject — camera.hpp:52-55: (u - cu) / fu * depth
-  const double end_S[3] = {__dmul_rn(__ddiv_rn(__dsub_rn(u, cam.cu), cam.fu), reach),
-                           __dmul_rn(__ddiv_rn(__dsub_rn(v, cam.cv), cam.fv), reach), reach};
-  double end_L[3];
-  pose_apply(T, end_S[0], end_S[1], end_S[2], end_L);
-  traverse<false>(T.t, end_L, cs, cube, status);
+  __syncthreads();
+  if (use_loc) {  // flush the near-sensor cube: 2 rows of 16 z-cells per word
+    for (int w = threadIdx.x; w < 128; w += blockDim.x) {
+      const uint32_t bits = sm.loc[w];
+      if (!bits) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t zb = (bits >> (16 * h)) & 0xffffu;
+        if (!zb) continue;
+        const int row = 2 * w + h, dx = row >> 4, dy = row & 15;
+        const uint32_t base = (uint32_t(lx + dx) * uint32_t(cube.S) + uint32_t(ly + dy)) * uint32_t(cube.SZw);
+        const int sh = lz & 31;
+        atomicOr(cube.bits + base + uint32_t(lz >> 5), zb << sh);
+        if (sh > 16) atomicOr(cube.bits + base + uint32_t(lz >> 5) + 1u, zb >> (32 - sh));
+      }
+    }
+  }
 }
 
 // LiDAR: one thread per valid pixel — view.cpp:94-111.  The per-pixel unit
@@ -368,6 +502,33 @@ __global__ void __launch_bounds__(kDilThreads) k_dilate_alloc(Cube cube, uint32_
 }
 
 // ---- host driver ------------------------------------------------------------------
+// Per camera tile: ((u - cu) / fu, (v - cv) / fv) at the tile centre
+// (view.cpp:75-80 with camera.hpp:52-55), the frame-independent part of
+// every camera ray.
+static void ensure_camera_lut(Context* ctx, const vxm_camera& cam, int W, int H, int tile) {
+  if (ctx->cam_lut_valid && std::memcmp(&ctx->cam_key, &cam, sizeof cam) == 0 && ctx->cam_key_w == W &&
+      ctx->cam_key_h == H && ctx->cam_key_tile == tile)
+    return;
+  const int tx = (W + tile - 1) / tile, ty = (H + tile - 1) / tile;
+  std::vector<double> d(size_t(tx) * ty * 2);
+  for (int t = 0; t < tx * ty; ++t) {
+    const int col0 = (t % tx) * tile, row0 = (t / tx) * tile;
+    const int row1 = std::min(row0 + tile, H), col1 = std::min(col0 + tile, W);
+    const double u = 0.5 * double(col0 + col1), v = 0.5 * double(row0 + row1);
+    d[2 * size_t(t)] = (u - cam.cu) / cam.fu;
+    d[2 * size_t(t) + 1] = (v - cam.cv) / cam.fv;
+  }
+  ctx->cam_dirs.ensure(d.size() * sizeof(double));
+  VXM_CUDA(cudaMemcpyAsync(ctx->cam_dirs.p, d.data(), d.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->cam_key = cam;
+  ctx->cam_key_w = W;
+  ctx->cam_key_h = H;
+  ctx->cam_key_tile = tile;
+  ctx->cam_lut_valid = true;
+}
+
 static void ensure_lidar_lut(Context* ctx, const vxm_lidar& li) {
   if (ctx->lut_valid && std::memcmp(&ctx->lut_key, &li, sizeof li) == 0) return;
   const int W = li.num_azimuth, H = li.num_elevation;
@@ -450,10 +611,16 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
     const int tile = std::max(1, a.cfg.pixel_subsample);
     const int nt = ((a.width + tile - 1) / tile) * ((a.height + tile - 1) / tile);
     if (nt > 0) {
+      ensure_camera_lut(ctx, a.cam, a.width, a.height, tile);
+      const int3 sc3 = make_int3(int(std::floor(a.T_LS.t[0] / cs)), int(std::floor(a.T_LS.t[1] / cs)),
+                                 int(std::floor(a.T_LS.t[2] / cs)));
       ctx->prof_begin("k_rays");
-      // 32 threads per CTA: the rays are serial DDAs, so spread them over all SMs
-      launch_pdl(ctx->stream, k_rays_camera, dim3(ceil_div(nt, 32)), dim3(32), 0, 
-          a.depth_dev, a.width, a.height, tile, a.cam, a.T_LS, cs,
+      // one resident wave of 8-warp CTAs; warps loop over the tiles
+      const int per_sm = ctx->resident_per_sm((const void*)k_rays_camera, 32 * kRayWarps);
+      launch_pdl(ctx->stream, k_rays_camera,
+                 dim3(std::max<uint32_t>(1u, std::min<uint32_t>(ceil_div(nt, kRayWarps), uint32_t(per_sm * ctx->sm_count)))),
+                 dim3(32 * kRayWarps), 0, 
+          a.depth_dev, a.width, a.height, tile, ctx->cam_dirs.as<const double2>(), a.T_LS, sc3, cs,
           a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
       ctx->prof_end();
       ctx->count_launch();
