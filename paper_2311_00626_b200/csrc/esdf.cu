@@ -1177,6 +1177,8 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.line_mask = E->line_mask;
   la.stamp_swept = E->stamp_swept;
   la.site_any = E->site_any;
+  la.site_near = E->site_near;
+  la.r1_list = E->r1_list;
   la.r1 = E->dirty_count + 7;
   la.ring = E->dirty_count + kRingOffset;
   la.dlist[0] = E->dlist[0];

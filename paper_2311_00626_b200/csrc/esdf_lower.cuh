@@ -488,7 +488,11 @@ struct LowerArgs {
   uint32_t* stamp_r1same;     // [cap] call epoch: the round-1 reset + copy left the block unchanged
   int dataflow;               // 1: pair items wait on dependencies; 0: phased barriers
   const uint8_t* site_any;    // [cap] 0: the block holds no site
-  uint32_t* r1;               // [4] round-1 split: #site, #no-site, group / warp work counters
+  uint8_t* site_near;         // [cap] k_lower_xr: bit 0 a site within +-x, bit 1 within the 3x3 (x, y)
+  int32_t* r1_list;           // [3][cap] k_lower_xr: round 1's pairs that may change something
+  uint32_t r1_compact_min;    // k_lower_xr: maps above this many blocks use r1_list
+  uint32_t* r1;               // [8] round-1 split: #site, #no-site, group / warp work counters,
+                              //     completed sweeps + copies, x / y / z compact pair counts
   uint32_t* ring;             // cross-round lowering: [0..3] dirty counts, [4..7] sweep claims,
                               // [8..11] pair claims, [12..15] pairs done (by round % 4), [16] last
                               // completed round

@@ -86,6 +86,15 @@ __device__ inline void tr_add(unsigned long long* tr, uint32_t R, int k, unsigne
   if (tr && R < 24) atomicAdd(tr + 128 + 16 * R + k, v);
 }
 
+// Round 1's compact pair lists (x, y, z), capacity entries each.
+__device__ inline int32_t* r1_pairs(const LowerArgs& a, int axis) {
+  return a.r1_list + size_t(axis) * a.capacity;
+}
+
+// Maps above this many blocks precompute round 1's pair lists
+// (VXM_XR_R1_COMPACT_MIN overrides, for the variant tests).
+constexpr uint32_t kR1CompactMin = 32 * 1024;
+
 __device__ inline unsigned long long ld_relaxed64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -128,7 +137,56 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
     }
     *RG(ring, kRingLast) = 0u;
   }
-  // round-1 split by site_any (as k_lower3)
+  // round-1 split by site_any (as k_lower3), and each block's static "a site
+  // nearby" bits for round 1's pairs: after reset_parented only sites give,
+  // and a block can take parents in round 1's x phase only from its x
+  // neighbours, in its y phase only from blocks whose x-neighbourhood holds a
+  // site.  So a round-1 y pair is certainly the identity when neither block
+  // has a site within +-x (bit 0), a z pair when neither has one in its 3 x 3
+  // (x, y) neighbourhood (bit 1); such items are released without any wait.
+  // (only on large maps: on a small one — C2, 9k blocks — the extra pass and
+  // grid barrier cost more than the claims they save)
+  const bool r1c = n_blocks > a.r1_compact_min;
+  if (lower && r1c) {
+    auto sa = [&](int32_t c) -> uint32_t { return c >= 0 ? uint32_t(a.site_any[c] != 0) : 0u; };
+    auto near_x = [&](int32_t c) -> uint32_t {
+      if (c < 0) return 0u;
+      return sa(c) | sa(__ldg(a.nbr + size_t(c) * 6 + 0)) | sa(__ldg(a.nbr + size_t(c) * 6 + 1));
+    };
+    for (uint32_t b = blockIdx.x * kL3Threads + threadIdx.x; b < n_blocks; b += gridDim.x * kL3Threads) {
+      const uint32_t nx = near_x(int32_t(b));
+      const uint32_t nxy = nx | near_x(__ldg(a.nbr + size_t(b) * 6 + 2)) | near_x(__ldg(a.nbr + size_t(b) * 6 + 3));
+      a.site_near[b] = uint8_t(nx | (nxy << 1));
+    }
+    grid.sync();
+    // Round 1's pair items: the certainly-identity pairs (b, b + axis) are
+    // released here, before any sweep (their readers see below); the others
+    // go to one compact list per axis, so round 1 claims only those — on a
+    // mostly site-free map (C5: 262k blocks, ~7k with sites) that removes
+    // most of the 3 x N claims that would otherwise serialise on one counter.
+    const uint32_t ep1 = base_epoch + 1u;
+    for (uint32_t b0 = blockIdx.x * kL3Threads + (threadIdx.x & ~31u); b0 < n_blocks;
+         b0 += gridDim.x * kL3Threads) {
+      const uint32_t b = b0 + lane;
+      const bool in = b < n_blocks;
+#pragma unroll
+      for (int axis = 0; axis < 3; ++axis) {
+        const int32_t hi = in ? __ldg(a.nbr + size_t(b) * 6 + 2 * axis) : -1;
+        bool keep = false;
+        if (hi >= 0) {
+          const bool ident = axis == 0 ? (a.site_any[b] == 0 && a.site_any[hi] == 0)
+                                       : ((a.site_near[b] | a.site_near[hi]) & (axis == 1 ? 1u : 2u)) == 0u;
+          if (ident) a.stamp_pair[axis][b] = ep1;
+          keep = !ident;
+        }
+        const uint32_t mk = __ballot_sync(0xffffffffu, keep);
+        uint32_t base = 0;
+        if (lane == 0 && mk) base = atomicAdd(a.r1 + 5 + axis, __popc(mk));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) r1_pairs(a, axis)[base + __popc(mk & ((1u << lane) - 1u))] = int32_t(b);
+      }
+    }
+  }
   if (lower) {
     for (uint32_t b0 = blockIdx.x * kL3Threads + (threadIdx.x & ~31u); b0 < n_blocks;
          b0 += gridDim.x * kL3Threads) {
@@ -154,7 +212,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
     a.trace[0] = tm;
   }
-  uint32_t n_pairs = 0, n_cmp = 0, rounds = 0;
+  uint32_t n_pairs = 0, n_cmp = 0, rounds = 0, r1_mine = 0;
   if (lower && n_blocks > 0) {
     for (uint32_t R = 1;; ++R) {
       const uint32_t ep = base_epoch + R, ep_next = ep + 1;
@@ -197,8 +255,17 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             store_block3(G, work + size_t(s) * 1536, t);
           }
           group_sync(bar);
-          if (t == 0) st_release(a.stamp_swept + s, ep);
+          if (t == 0) {
+            st_release(a.stamp_swept + s, ep);
+            ++r1_mine;
+          }
         }
+        // round 1 completes only after every sweep / copy: counted per group
+        if (t == 0 && r1_mine) {
+          __threadfence();  // (release: the group's block writes before the count)
+          atomicAdd(a.r1 + 4, r1_mine);
+        }
+        r1_mine = 0;
         const uint32_t n_ns = *((volatile uint32_t*)(a.r1 + 1));
         constexpr uint32_t kCopyChunk = 2;
         uint32_t j = 0, j_end = 0;
@@ -218,7 +285,12 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             // compare can skip it (every later writer marks it dirty)
             if (!reset_chg) a.stamp_r1same[s] = a.call_epoch;
             st_release(a.stamp_swept + s, ep);
+            ++r1_mine;
           }
+        }
+        if (lane == 0 && r1_mine) {  // (per warp)
+          __threadfence();
+          atomicAdd(a.r1 + 4, r1_mine);
         }
         if (a.trace && lane == 0) {  // VXM_TRACE_XR: end of the round-1 sweeps / copies
           unsigned long long tm;
@@ -336,7 +408,13 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
       auto is_dirty = [&](int32_t b) { return r1 || __ldcg(a.stamp_dirty[cp] + b) == ep; };
       const uint32_t sides = r1 ? 1u : 2u;
       const uint32_t per_axis = sides * n_dirty;
-      const uint32_t n_items = 3u * per_axis;
+      // round 1 on a large map: the compact lists (x, y, z) of the pairs that
+      // may change something
+      const bool r1l = r1 && r1c;
+      const uint32_t c1x = r1l ? *((volatile uint32_t*)(a.r1 + 5)) : 0u;
+      const uint32_t c1y = r1l ? *((volatile uint32_t*)(a.r1 + 6)) : 0u;
+      const uint32_t c1z = r1l ? *((volatile uint32_t*)(a.r1 + 7)) : 0u;
+      const uint32_t n_items = r1l ? c1x + c1y + c1z : 3u * per_axis;
       uint32_t my_done = 0;
       // one item per claim: a warp blocked on a dependency must not hold later
       // items (measured on C2: chunks of 4 / 16 in round 1 cost 2 % / 34 %;
@@ -347,11 +425,18 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         wi = __shfl_sync(0xffffffffu, wi, 0);
         if (wi >= n_items) break;
         if (a.trace && lane == 0 && wi == 0) tr_min(a.trace, R, 2, gtime());
-        const int axis = int(wi / per_axis);
-        const uint32_t rest = wi - uint32_t(axis) * per_axis;
+        int axis;
+        uint32_t rest;
+        if (r1l) {
+          axis = wi < c1x ? 0 : (wi < c1x + c1y ? 1 : 2);
+          rest = wi - (axis == 0 ? 0u : (axis == 1 ? c1x : c1x + c1y));
+        } else {
+          axis = int(wi / per_axis);
+          rest = wi - uint32_t(axis) * per_axis;
+        }
         const uint32_t i = r1 ? rest : rest >> 1;
         const int side = r1 ? 0 : int(rest & 1u);
-        const int32_t d = dirty_at(i);
+        const int32_t d = r1l ? __ldcg(r1_pairs(a, axis) + i) : dirty_at(i);
         int32_t lo = -1, hi = -1;
         if (side == 0) {
           hi = __ldg(a.nbr + size_t(d) * 6 + 2 * axis);  // d + axis
@@ -365,10 +450,14 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         // reset only sites give); the loads are issued ahead of the waits
         const bool site_lo = r1 && lo >= 0 && a.site_any[lo] != 0;
         const bool site_hi = r1 && hi >= 0 && a.site_any[hi] != 0;
-        if (lo >= 0 && hi >= 0 && r1 && axis == 0 && !site_lo && !site_hi) {
-          // identity x pair of round 1 (no giver on either face, no lower axis):
-          // released without waiting — every reader of lo / hi also waits for
-          // the blocks' own sweep stamps, or for a non-identity pair that did
+        // Round 1's certainly-identity pairs are released without waiting (on
+        // a large map before the sweeps, from the static site bits; on a small
+        // one the x pairs here).  Their readers: the pairs of later axes, which
+        // also wait for the blocks' sweeps and their non-identity x / y pairs
+        // — the only writers; round-2 sweeps, of blocks some non-identity pair
+        // changed; round-2 pairs, which start once round 1 is complete — and
+        // round 1 completes only after every round-1 sweep and copy.
+        if (lo >= 0 && hi >= 0 && r1 && !r1c && axis == 0 && !site_lo && !site_hi) {
           if (lane == 0) st_release(a.stamp_pair[0] + lo, ep);
         } else if (lo >= 0 && hi >= 0) {
           bool dep_chg = false;
@@ -461,6 +550,15 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         __threadfence();
         const uint32_t done = atomicAdd(RG(ring, kRingDone + q4), my_done) + my_done;
         if (done == n_items) {
+          if (R == 1) {  // and every round-1 sweep / copy (see r1_ident)
+            for (uint32_t it = 0; ld_acquire(a.r1 + 4) < n_blocks; ++it) {
+              if (it > (1u << 24)) {
+                if (atomicExch(&a.status->watchdog, 1u) == 0u) a.status->pad3[0] = 42u;
+                break;
+              }
+              __nanosleep(64);
+            }
+          }
           __threadfence();
           const int q4nn = int((R + 2u) & 3u);
           *RG(ring, kRingCnt + q4nn) = 0u;
@@ -572,7 +670,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
       a.trace[58] = a.r1[0];  // round-1 blocks with sites (swept) / without (copied)
       a.trace[59] = a.r1[1];
     }
-    a.r1[0] = a.r1[1] = a.r1[2] = a.r1[3] = 0u;  // zero for the next launch
+    for (int q = 0; q < 8; ++q) a.r1[q] = 0u;  // zero for the next launch
     a.status->rounds = rounds;
     a.status->n_esdf_blocks = n_blocks;
     a.meta->round_epoch = base_epoch + rounds + 2;
@@ -596,6 +694,11 @@ bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
     return e ? std::atoi(e) : 1;
   }();
   const bool wide = wide_mode == 2 || (wide_mode == 1 && n_blocks_hint > kXrWideBlocks);
+  static const uint32_t r1_compact_min = [] {
+    const char* e = std::getenv("VXM_XR_R1_COMPACT_MIN");
+    return e ? uint32_t(std::strtoul(e, nullptr, 10)) : kR1CompactMin;
+  }();
+  la.r1_compact_min = r1_compact_min;
   void (*kern)(LowerArgs) = wide ? k_lower_xr<3> : k_lower_xr<2>;
   const int grid = ctx->resident_per_sm((const void*)kern, kL3Threads, 0, 4) * ctx->sm_count;
   ctx->lower_cta.ensure(sizeof(uint32_t) * grid);  // per-CTA counts of the in-kernel compaction

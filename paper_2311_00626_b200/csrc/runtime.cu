@@ -243,6 +243,8 @@ void Layer::ensure_capacity(uint64_t need) {
     grow_copy(&line_mask, capacity * 3ull, live * 3ull, nc * 3ull, 0, st);
     grow_copy(&stamp_swept, capacity, live, nc, 0, st);
     grow_copy(&site_any, capacity, live, nc, 0, st);
+    grow_copy(&site_near, capacity, 0, nc, -1, st);
+    grow_copy(&r1_list, capacity * 3ull, 0, nc * 3ull, -1, st);
     for (int i = 0; i < 2; ++i) grow_copy(&dlist[i], capacity, 0, nc, 0, st);
     for (int i = 0; i < 3; ++i) grow_copy(&pair_face[i], capacity * 2ull, 0, nc * 2ull, 0, st);
     for (int a = 0; a < 3; ++a) grow_copy(&stamp_pair[a], capacity, live, nc, 0, st);
@@ -297,6 +299,8 @@ Layer::~Layer() {
   if (line_mask) cudaFree(line_mask);
   if (stamp_swept) cudaFree(stamp_swept);
   if (site_any) cudaFree(site_any);
+  if (site_near) cudaFree(site_near);
+  if (r1_list) cudaFree(r1_list);
   for (unsigned long long* p : dlist)
     if (p) cudaFree(p);
   for (unsigned long long* p : pair_face)

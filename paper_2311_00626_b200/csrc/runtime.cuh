@@ -163,6 +163,8 @@ struct Layer {
   unsigned long long* line_mask = nullptr;  // [cap][3] lines changed by border phases
   uint32_t* stamp_swept = nullptr;          // round epoch of the block's last sweep
   uint8_t* site_any = nullptr;              // 0: the block holds no site (exact or conservative 1)
+  uint8_t* site_near = nullptr;             // k_lower_xr scratch: sites near the block (per launch)
+  int32_t* r1_list = nullptr;               // k_lower_xr scratch: [3][cap] round-1 pair lists
   uint32_t* stamp_pair[3] = {nullptr, nullptr, nullptr};  // round epoch of pair (b, b+axis)
   uint32_t* stamp_r1same = nullptr;  // call epoch: round 1 left the block byte-identical
 
