@@ -21,6 +21,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "shard.cuh"
@@ -54,8 +56,7 @@ __device__ inline int shard_owner(int32_t x, int world, int slab) {
 }
 
 // ---- sweeps of round r (round 1: reset_parented + sweep of every block) ------
-__global__ void __launch_bounds__(kL3Threads, 2) k_shard_sweep(LowerArgs a, ShardRound sr) {
-  __shared__ GroupSmem s_grp[kL3Groups];
+__device__ void shard_sweep_body(const LowerArgs& a, const ShardRound& sr, GroupSmem* s_grp) {
   const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
   const int bar = 1 + g;
   GroupSmem& G = s_grp[g];
@@ -96,31 +97,57 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_shard_sweep(LowerArgs a, Shar
     group_sync(bar);
   }
 }
+__global__ void __launch_bounds__(kL3Threads, 2) k_shard_sweep(LowerArgs a, ShardRound sr) {
+  __shared__ GroupSmem s_grp[kL3Groups];
+  shard_sweep_body(a, sr, s_grp);
+}
 
 // ---- boundary faces + dirty bits, after the sweeps -----------------------------
-__global__ void k_shard_pack(LowerArgs a, ShardRound sr) {
+// Written to n_dst snapshot buffers: the local send buffer (host-driven
+// exchange), or directly into both neighbours' receive buffers over peer
+// memory (the fused in-kernel exchange).
+__device__ void shard_pack_body(const LowerArgs& a, const ShardRound& sr, const XView* dst_v, int n_dst) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t* work = a.pool[sr.cur ^ 1u];
   const uint32_t cp = sr.r & 1u;
   for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < sr.n_bnd; k += nwarps) {
     const int32_t s = sr.bnd_slots[k];
-    if (lane == 0) {
-      sr.snd_keys[k] = sr.bnd_keys[k];
-      sr.snd_dirty[k] = uint8_t(sr.r == 1 || __ldcg(a.stamp_dirty[cp] + s) == sr.ep);
-    }
+    const uint8_t dirty = uint8_t(sr.r == 1 || __ldcg(a.stamp_dirty[cp] + s) == sr.ep);
+    const uint64_t key = sr.bnd_keys[k];
+    uint32_t w[12];
 #pragma unroll
     for (int f = 0; f < 2; ++f)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int q = lane + 32 * j, lin = (f ? 7 : 0) + 8 * (q & 7) + 64 * (q >> 3);
         const uint32_t* src = work + size_t(s) * 1536 + lin * 3;
-        uint32_t* dst = sr.snd_faces + ((size_t(k) * 2 + f) * 64 + q) * 3;
-        dst[0] = __ldcg(src);
-        dst[1] = __ldcg(src + 1);
-        dst[2] = __ldcg(src + 2);
+        w[6 * f + 3 * j] = __ldcg(src);
+        w[6 * f + 3 * j + 1] = __ldcg(src + 1);
+        w[6 * f + 3 * j + 2] = __ldcg(src + 2);
       }
+    for (int d = 0; d < n_dst; ++d) {
+      const XView& v = dst_v[d];
+      if (lane == 0) {
+        v.keys[k] = key;
+        v.dirty[k] = dirty;
+      }
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = lane + 32 * j;
+          uint32_t* dst = v.faces + ((size_t(k) * 2 + f) * 64 + q) * 3;
+          dst[0] = w[6 * f + 3 * j];
+          dst[1] = w[6 * f + 3 * j + 1];
+          dst[2] = w[6 * f + 3 * j + 2];
+        }
+    }
   }
+}
+__global__ void k_shard_pack(LowerArgs a, ShardRound sr) {
+  const XView v{sr.snd_keys, sr.snd_dirty, sr.snd_faces};
+  shard_pack_body(a, sr, &v, 1);
 }
 
 __device__ inline int64_t find_key(const uint64_t* keys, uint32_t n, uint64_t k) {
@@ -150,8 +177,7 @@ __device__ inline void mark_changed(const LowerArgs& a, uint32_t r, uint32_t ep_
 }
 
 // ---- border phase of round r: x (local + cross-shard), y, z ---------------------
-__global__ void __launch_bounds__(kL3Threads, 2) k_shard_border(LowerArgs a, ShardRound sr) {
-  cg::grid_group grid = cg::this_grid();
+__device__ void shard_border_body(const LowerArgs& a, const ShardRound& sr, cg::grid_group& grid) {
   const int lane = threadIdx.x & 31;
   const uint32_t wid = (blockIdx.x * kL3Threads + threadIdx.x) >> 5;
   const uint32_t nwarps = gridDim.x * (kL3Threads >> 5);
@@ -263,6 +289,121 @@ __global__ void __launch_bounds__(kL3Threads, 2) k_shard_border(LowerArgs a, Sha
   }
   if (lane == 0 && n_pairs) atomicAdd(&a.status->sum_pairs, n_pairs);
 }
+__global__ void __launch_bounds__(kL3Threads, 2) k_shard_border(LowerArgs a, ShardRound sr) {
+  cg::grid_group grid = cg::this_grid();
+  shard_border_body(a, sr, grid);
+}
+
+// ---- the whole lowering in one persistent kernel per shard ------------------------
+// Fused exchange over peer memory (NVLink P2P between GPUs, plain device
+// memory between shards on one GPU): each round a shard writes its boundary
+// snapshot straight into both neighbours' receive buffers, publishes the
+// round on their flags with a system-scope release and acquires its own two
+// flags before the border phase; the next-dirty counts go to every shard's
+// count board (by round parity) and each shard sums the board — so the
+// round loop, the exchange and the termination test (esdf/integrator.cpp:506)
+// run with no host involvement.  A shard cannot run two rounds ahead: its
+// next pack needs the whole board of the current round, which every other
+// shard writes only after its own border phase.
+constexpr int kFusedMaxShards = 8;
+struct ShardPeers {
+  XView to_right, to_left;            // the +x neighbour's rcv[0], the -x one's rcv[1]
+  uint32_t* flag_right;               // their receive flags ([0] / [1])
+  uint32_t* flag_left;
+  const uint32_t* my_flag;            // [2] mine (written by the -x / +x neighbours)
+  unsigned long long* board[kFusedMaxShards];  // every shard's [2][kFusedMaxShards] count board
+  const unsigned long long* my_board;
+  uint32_t* go;                       // [2] this shard's "another round" word by parity
+  uint32_t* rounds_out;
+  uint32_t* ctr;                      // [4] sweep claim counters, 2 per round parity
+  int rank, world;
+};
+
+__device__ inline void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ inline void st_release_sys64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ inline uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ inline unsigned long long ld_acquire_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Bounded waits (2 s of globaltimer): a lost peer is an error, never a hang.
+__device__ inline unsigned long long now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kL3Threads, 2) k_shard_fused(LowerArgs a, ShardRound sr0, ShardPeers pe) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ GroupSmem s_grp[kL3Groups];
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  for (uint32_t r = 1;; ++r) {
+    ShardRound sr = sr0;
+    sr.r = r;
+    sr.ep = sr0.ep + r;  // (sr0.ep = the base epoch)
+    sr.ctr = pe.ctr + 2 * (r & 1u);
+    if (lead) {  // the next round's claim counters and this border's next count
+      pe.ctr[2 * ((r + 1u) & 1u)] = pe.ctr[2 * ((r + 1u) & 1u) + 1] = 0u;
+      a.count[(r + 1u) % 3u] = 0u;
+    }
+    shard_sweep_body(a, sr, s_grp);
+    grid.sync();
+    const XView dst[2] = {pe.to_right, pe.to_left};
+    shard_pack_body(a, sr, dst, 2);
+    grid.sync();
+    if (lead) {
+      __threadfence_system();  // every CTA's snapshot stores (ordered by grid.sync) before the flags
+      st_release_sys(pe.flag_right, r);
+      st_release_sys(pe.flag_left, r);
+      const unsigned long long t0 = now_ns();
+      while (ld_acquire_sys(pe.my_flag) < r || ld_acquire_sys(pe.my_flag + 1) < r) {
+        if (now_ns() - t0 > 2000000000ull) {
+          if (atomicExch(&a.status->watchdog, 1u) == 0u) a.status->pad3[0] = 60u;
+          break;
+        }
+        __nanosleep(100);
+      }
+    }
+    grid.sync();
+    shard_border_body(a, sr, grid);
+    grid.sync();
+    if (lead) {
+      const uint32_t cnt = *((volatile uint32_t*)(a.count + (r + 1u) % 3u));
+      const unsigned long long e = (unsigned long long)r << 32 | cnt;
+      const int par = int(r & 1u) * kFusedMaxShards;
+      for (int q = 0; q < pe.world; ++q) st_release_sys64(pe.board[q] + par + pe.rank, e);
+      unsigned long long sum = 0;
+      const unsigned long long t0 = now_ns();
+      for (int q = 0; q < pe.world; ++q) {
+        unsigned long long v;
+        while (((v = ld_acquire_sys64(pe.my_board + par + q)) >> 32) != r) {
+          if (now_ns() - t0 > 2000000000ull) {
+            if (atomicExch(&a.status->watchdog, 1u) == 0u) a.status->pad3[0] = 61u;
+            v = 0;
+            break;
+          }
+          __nanosleep(100);
+        }
+        sum += v & 0xffffffffull;
+      }
+      pe.go[r & 1u] = sum != 0 && a.status->watchdog == 0u ? 1u : 0u;
+    }
+    grid.sync();
+    if (*((volatile uint32_t*)(pe.go + (r & 1u))) == 0u) {  // while (!dirty.empty())
+      if (lead) *pe.rounds_out = r;
+      break;
+    }
+  }
+}
 
 // ---- changed set of the update (esdf/integrator.cpp:403-411) -------------------
 __global__ void k_shard_changed(LowerArgs a, ShardRound sr) {
@@ -289,6 +430,11 @@ __global__ void k_shard_changed(LowerArgs a, ShardRound sr) {
 
 __global__ void k_shard_meta(LayerMeta* meta, uint32_t round_epoch, uint32_t cur) {
   meta->round_epoch = round_epoch;
+  meta->cur = cur;
+}
+// (fused path: the round count is on the device)
+__global__ void k_shard_meta_dev(LayerMeta* meta, uint32_t base, const uint32_t* rounds, uint32_t cur) {
+  meta->round_epoch = base + *rounds + 2u;
   meta->cur = cur;
 }
 
@@ -511,6 +657,9 @@ void shard_finish_sync(ShardUpdate& x, bool lowered) {
   use(x.ctx);
   x.ctx->sync_status();
   x.E->adopt_meta();
+  if (x.ctx->h_status->watchdog)
+    throw Error(VXM_ERR_INTERNAL, "sharded ESDF lowering: a peer wait expired (code " +
+                                      std::to_string(x.ctx->h_status->pad3[0]) + ")");
   vxm_stats& w = x.ctx->stats;
   w.esdf_calls += 1;
   w.esdf_blocks += x.n_blocks;
@@ -526,6 +675,82 @@ ShardUpdate::~ShardUpdate() {
   if (h_meta) cudaFreeHost(h_meta);
   if (h_cnt) cudaFreeHost(h_cnt);
   if (ev) cudaEventDestroy(ev);
+}
+
+// ---- fused path: one persistent kernel per shard (k_shard_fused) ---------------
+namespace {
+constexpr size_t kMboxFlags = 0, kMboxBoard = 64, kMboxGo = 64 + 16 * 8, kMboxRounds = kMboxGo + 8,
+                 kMboxBytes = 512;
+template <typename T>
+T* mbox_at(ShardUpdate& x, size_t off) {
+  return reinterpret_cast<T*>(static_cast<unsigned char*>(x.mbox.p) + off);
+}
+
+// Peer access between every pair of the shards' devices (the count board is
+// written by every shard); false when some pair cannot.
+bool enable_peers(std::vector<ShardUpdate>& sh) {
+  std::vector<int> devs;
+  for (auto& x : sh)
+    if (std::find(devs.begin(), devs.end(), x.ctx->device) == devs.end()) devs.push_back(x.ctx->device);
+  for (int a : devs)
+    for (int b : devs) {
+      if (a == b) continue;
+      int ok = 0;
+      VXM_CUDA(cudaDeviceCanAccessPeer(&ok, a, b));
+      if (!ok) return false;
+      VXM_CUDA(cudaSetDevice(a));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+      else VXM_CUDA(e);
+    }
+  return true;
+}
+}  // namespace
+
+// The whole round loop on the device: launches k_shard_fused on every shard
+// (all resident at once: shards on one GPU split its SMs) and the changed-set
+// kernels; the caller synchronises once.
+void shard_lower_fused(std::vector<ShardUpdate>& sh) {
+  const int P = int(sh.size());
+  for (auto& x : sh) {  // fresh mailboxes (the host syncs before any kernel runs)
+    use(x.ctx);
+    x.mbox.ensure(kMboxBytes);
+    VXM_CUDA(cudaMemsetAsync(x.mbox.p, 0, kMboxBytes, x.ctx->stream));
+    VXM_CUDA(cudaMemsetAsync(x.ctr.p, 0, 4 * sizeof(uint32_t), x.ctx->stream));
+  }
+  for (auto& x : sh) {
+    use(x.ctx);
+    VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
+  }
+  for (int p = 0; p < P; ++p) {
+    ShardUpdate& x = sh[p];
+    ShardUpdate& right = sh[(p + 1) % P];
+    ShardUpdate& left = sh[(p - 1 + P) % P];
+    ShardPeers pe{};
+    pe.to_right = xview(right.rcv[0].p, x.n_bnd);
+    pe.to_left = xview(left.rcv[1].p, x.n_bnd);
+    pe.flag_right = mbox_at<uint32_t>(right, kMboxFlags);
+    pe.flag_left = mbox_at<uint32_t>(left, kMboxFlags) + 1;
+    pe.my_flag = mbox_at<uint32_t>(x, kMboxFlags);
+    for (int q = 0; q < P; ++q) pe.board[q] = mbox_at<unsigned long long>(sh[q], kMboxBoard);
+    pe.my_board = mbox_at<unsigned long long>(x, kMboxBoard);
+    pe.go = mbox_at<uint32_t>(x, kMboxGo);
+    pe.rounds_out = mbox_at<uint32_t>(x, kMboxRounds);
+    pe.ctr = x.ctr.as<uint32_t>();
+    pe.rank = p;
+    pe.world = P;
+    int same = 0;  // shards sharing this GPU share its SMs
+    for (auto& y : sh) same += y.ctx->device == x.ctx->device;
+    use(x.ctx);
+    const int per_sm = x.ctx->resident_per_sm((const void*)k_shard_fused, kL3Threads, 0, 4);
+    const int grid = std::max(1, per_sm * x.ctx->sm_count / same);
+    ShardRound sr0 = round_args(x, 0);  // ep = the base epoch
+    void* args[] = {&x.la, &sr0, &pe};
+    VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_shard_fused, dim3(grid), dim3(kL3Threads), args, 0,
+                                         x.ctx->stream));
+    x.ctx->count_launch();
+    check_launch(x.ctx, "k_shard_fused");
+  }
 }
 
 // All shards in this process (one context each, same or peer GPUs): every
@@ -605,11 +830,51 @@ void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
     shard_begin_finish(x);
     any |= x.local_any;
   }
+  static const bool fused_env = [] {  // VXM_SHARD_FUSED=0: host-driven rounds
+    const char* e = std::getenv("VXM_SHARD_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  const bool fused = any && fused_env && P >= 2 && P <= kFusedMaxShards && enable_peers(sh);
   if (any) {
     for (auto& x : sh) shard_plan_launch(x);
     for (auto& x : sh) shard_plan_finish(x);
     for (int p = 0; p < P; ++p)  // [0]: from the -x neighbour, [1]: from the +x one
       shard_set_neighbours(sh[p], sh[(p - 1 + P) % P].n_bnd, sh[(p + 1) % P].n_bnd);
+  }
+  if (fused) {
+    shard_lower_fused(sh);
+    for (int p = 0; p < P; ++p) {
+      ShardUpdate& x = sh[p];
+      use(x.ctx);
+      ShardRound sr = round_args(x, 1);
+      sr.lowered = 1;
+      k_shard_changed<<<grid_for(x.ctx, uint64_t(std::max<uint32_t>(x.n_blocks, 1)) * 32), 256, 0,
+                        x.ctx->stream>>>(x.la, sr);
+      k_shard_meta_dev<<<1, 1, 0, x.ctx->stream>>>(x.E->meta, x.base, mbox_at<uint32_t>(x, kMboxRounds),
+                                                   x.cur ^ 1u);
+      x.ctx->count_launch(2);
+      BlockList* o = out[p];
+      o->bind(x.ctx);
+      o->ensure(x.n_all_cap);
+      launch_compact_keys(x.ctx, x.E->sorted_keys[x.E->sorted_parity], x.s.flags, &x.E->meta->num_blocks,
+                          x.n_all_cap, o->keys.as<uint64_t>(), o->d_count, nullptr, "k_compact_esdf");
+      o->host_valid = false;
+      o->host_pending = false;
+      o->count_hint = x.n_all_cap;
+      o->sorted_unique = true;
+      VXM_CUDA(cudaMemcpyAsync(x.h_cnt + 2, mbox_at<uint32_t>(x, kMboxRounds), sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, x.ctx->stream));
+      x.E->stage_meta();
+    }
+    for (auto& x : sh) {
+      x.rounds = 0;
+      shard_finish_sync(x, false);  // (status, meta, watchdog)
+      x.rounds = x.h_cnt[2];
+      x.ctx->stats.lower_rounds += x.rounds;
+    }
+    return;
+  }
+  if (any) {
     for (uint32_t r = 1;; ++r) {
       for (auto& x : sh) {
         shard_sweep(x, r);

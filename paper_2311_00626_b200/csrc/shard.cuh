@@ -37,6 +37,7 @@ struct ShardUpdate {
   LayerMeta* h_meta = nullptr;  // pinned: the layer meta after the mark phase
   uint32_t* h_cnt = nullptr;    // pinned: [0] boundary blocks, [1] next dirty count
   cudaEvent_t ev = nullptr;     // in-process exchange ordering
+  DevBuf mbox;                  // fused exchange: receive flags, count board, go, rounds
   ShardUpdate() = default;
   ShardUpdate(const ShardUpdate&) = delete;
   ShardUpdate& operator=(const ShardUpdate&) = delete;

@@ -1,11 +1,19 @@
 """GPU parity: block-sharded ESDF update (vxm_update_esdf_sharded).
 
-P shards (one context each, on the same B200 here; the peer copies become
-NVLink transfers across GPUs) own the blocks with floor(x / slab) mod P == p.
+P shards (one context each, on the same B200 here; across GPUs the peer
+accesses become NVLink transfers) own the blocks with floor(x / slab) mod P == p.
+By default the whole round loop runs in one persistent kernel per shard with
+the face exchange over peer memory (k_shard_fused); VXM_SHARD_FUSED=0 selects
+the host-driven rounds (event-ordered peer copies), run by the last test in a
+subprocess.
 Every frame is integrated by every shard (each keeps its own blocks) and by a
 single map; the shards' ESDF update must reproduce update_esdf over the single
 map bit-for-bit: the union of their changed lists and of their ESDF layers.
 """
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
@@ -92,3 +100,12 @@ def test_sharded_esdf_rejects_misconfigured_contexts(vx):
     Es = [vx.EsdfLayer(0.05, ctx=c) for c in (c0, c1)]
     with pytest.raises(vx.InvalidArgumentError):
         vx.update_esdf_sharded(Es, Ts, [np.zeros((1, 3), np.int32)] * 2, A.default_esdf_config())
+
+
+def test_sharded_host_driven_rounds_bitwise():
+    """The same tests through the host-driven round loop (VXM_SHARD_FUSED=0)."""
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-m", "gpu",
+                        "-k", "not host_driven"], env={**os.environ, "VXM_SHARD_FUSED": "0"},
+                       capture_output=True, text=True, timeout=900,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
