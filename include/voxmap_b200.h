@@ -428,6 +428,18 @@ vxm_status vxm_shard_update_exchange_buffers(vxm_shard_update* su, uint32_t n_le
 vxm_status vxm_shard_update_sweep(vxm_shard_update* su, uint32_t round);
 vxm_status vxm_shard_update_border(vxm_shard_update* su, uint32_t round, uint32_t* next_dirty);
 vxm_status vxm_shard_update_next_count(vxm_shard_update* su, uint32_t round, void** device_u32);
+/* Fused alternative to the round loop above (one persistent kernel per rank,
+ * the faces written straight into the neighbours' receive buffers over peer
+ * memory, system-scope flags and a count board for termination — no host step
+ * per round): after exchange_buffers(), ipc_handles() writes this rank's three
+ * CUDA IPC handles (3 x 64 bytes; it also clears the rank's mailbox, so every
+ * rank must call it before the all-gather, which is the barrier); the caller
+ * all-gathers them (world x 192 bytes in rank order) into lower_fused(), which
+ * enqueues the whole lowering; then finish(lowered = 1).  ranks_on_device: the
+ * ranks sharing this GPU (their kernels split its SMs; all ranks' kernels must
+ * run concurrently).  2..8 ranks. */
+vxm_status vxm_shard_update_ipc_handles(vxm_shard_update* su, void* handles_out);
+vxm_status vxm_shard_update_lower_fused(vxm_shard_update* su, const void* all_handles, int ranks_on_device);
 vxm_status vxm_shard_update_finish(vxm_shard_update* su, int lowered, vxm_blocklist* changed_out);
 void vxm_shard_update_destroy(vxm_shard_update* su);
 

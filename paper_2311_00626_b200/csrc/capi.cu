@@ -887,6 +887,18 @@ vxm_status vxm_shard_update_border(vxm_shard_update* su, uint32_t round, uint32_
       shard_border_launch(su->x, round);
   });
 }
+vxm_status vxm_shard_update_ipc_handles(vxm_shard_update* su, void* handles_out) {
+  return guard([&] {
+    REQUIRE_ARG(su && handles_out, "null argument");
+    shard_ipc_handles(su->x, handles_out);
+  });
+}
+vxm_status vxm_shard_update_lower_fused(vxm_shard_update* su, const void* all_handles, int ranks_on_device) {
+  return guard([&] {
+    REQUIRE_ARG(su && all_handles && ranks_on_device >= 1, "invalid argument");
+    shard_lower_fused_ipc(su->x, all_handles, ranks_on_device);
+  });
+}
 vxm_status vxm_shard_update_next_count(vxm_shard_update* su, uint32_t round, void** dptr) {
   return guard([&] {
     REQUIRE_ARG(su && dptr && round >= 1, "invalid argument");

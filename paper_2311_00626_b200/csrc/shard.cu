@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstring>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -631,14 +632,20 @@ uint32_t shard_border(ShardUpdate& x, uint32_t r) {
 
 // Changed set (esdf/integrator.cpp:403-411) and meta; `lowered`: the global
 // decision of this update.
+uint32_t* fused_rounds_ptr(ShardUpdate& x);
+
 void shard_finish_launch(ShardUpdate& x, bool lowered, BlockList* out) {
   use(x.ctx);
   cudaStream_t st = x.ctx->stream;
-  ShardRound sr = round_args(x, x.rounds);
+  ShardRound sr = round_args(x, std::max<uint32_t>(x.rounds, 1));
   sr.lowered = lowered ? 1 : 0;
   k_shard_changed<<<grid_for(x.ctx, uint64_t(std::max<uint32_t>(x.n_blocks, 1)) * 32), 256, 0, st>>>(x.la, sr);
   x.ctx->count_launch();
-  if (lowered) {
+  if (lowered && x.fused) {  // the round count is on the device
+    k_shard_meta_dev<<<1, 1, 0, st>>>(x.E->meta, x.base, fused_rounds_ptr(x), x.cur ^ 1u);
+    VXM_CUDA(cudaMemcpyAsync(x.h_cnt + 2, fused_rounds_ptr(x), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    x.ctx->count_launch();
+  } else if (lowered) {
     k_shard_meta<<<1, 1, 0, st>>>(x.E->meta, x.base + x.rounds + 2, x.cur ^ 1u);
     x.ctx->count_launch();
   }
@@ -657,6 +664,11 @@ void shard_finish_sync(ShardUpdate& x, bool lowered) {
   use(x.ctx);
   x.ctx->sync_status();
   x.E->adopt_meta();
+  if (x.fused) {
+    x.rounds = x.h_cnt[2];
+    for (void* p : x.ipc_open) cudaIpcCloseMemHandle(p);
+    x.ipc_open.clear();
+  }
   if (x.ctx->h_status->watchdog)
     throw Error(VXM_ERR_INTERNAL, "sharded ESDF lowering: a peer wait expired (code " +
                                       std::to_string(x.ctx->h_status->pad3[0]) + ")");
@@ -672,6 +684,7 @@ void shard_finish(ShardUpdate& x, bool lowered, BlockList* out) {
 }
 
 ShardUpdate::~ShardUpdate() {
+  for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
   if (h_meta) cudaFreeHost(h_meta);
   if (h_cnt) cudaFreeHost(h_cnt);
   if (ev) cudaEventDestroy(ev);
@@ -707,6 +720,80 @@ bool enable_peers(std::vector<ShardUpdate>& sh) {
 }
 }  // namespace
 
+uint32_t* fused_rounds_ptr(ShardUpdate& x) { return mbox_at<uint32_t>(x, kMboxRounds); }
+
+namespace {
+ShardPeers make_peers(ShardUpdate& x, ShardUpdate* right, ShardUpdate* left, void* right_rcv0, void* left_rcv1,
+                      void* right_mbox, void* left_mbox, void* const* boards, int world) {
+  (void)right;
+  (void)left;
+  ShardPeers pe{};
+  pe.to_right = xview(right_rcv0, x.n_bnd);
+  pe.to_left = xview(left_rcv1, x.n_bnd);
+  pe.flag_right = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(right_mbox) + kMboxFlags);
+  pe.flag_left = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(left_mbox) + kMboxFlags) + 1;
+  pe.my_flag = mbox_at<uint32_t>(x, kMboxFlags);
+  for (int q = 0; q < world; ++q)
+    pe.board[q] = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(boards[q]) + kMboxBoard);
+  pe.my_board = mbox_at<unsigned long long>(x, kMboxBoard);
+  pe.go = mbox_at<uint32_t>(x, kMboxGo);
+  pe.rounds_out = mbox_at<uint32_t>(x, kMboxRounds);
+  pe.ctr = x.ctr.as<uint32_t>();
+  pe.rank = x.rank;
+  pe.world = world;
+  return pe;
+}
+
+void launch_fused(ShardUpdate& x, ShardPeers& pe, int sharing) {
+  use(x.ctx);
+  const int per_sm = x.ctx->resident_per_sm((const void*)k_shard_fused, kL3Threads, 0, 4);
+  const int grid = std::max(1, per_sm * x.ctx->sm_count / std::max(1, sharing));
+  ShardRound sr0 = round_args(x, 0);  // ep = the base epoch
+  void* args[] = {&x.la, &sr0, &pe};
+  VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_shard_fused, dim3(grid), dim3(kL3Threads), args, 0,
+                                       x.ctx->stream));
+  x.ctx->count_launch();
+  check_launch(x.ctx, "k_shard_fused");
+  x.fused = true;
+}
+}  // namespace
+
+void shard_ipc_handles(ShardUpdate& x, void* out192) {
+  use(x.ctx);
+  x.mbox.ensure(kMboxBytes);
+  VXM_CUDA(cudaMemsetAsync(x.mbox.p, 0, kMboxBytes, x.ctx->stream));
+  VXM_CUDA(cudaMemsetAsync(x.ctr.p, 0, 4 * sizeof(uint32_t), x.ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
+  cudaIpcMemHandle_t h[3];
+  VXM_CUDA(cudaIpcGetMemHandle(&h[0], x.rcv[0].p));
+  VXM_CUDA(cudaIpcGetMemHandle(&h[1], x.rcv[1].p));
+  VXM_CUDA(cudaIpcGetMemHandle(&h[2], x.mbox.p));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  std::memcpy(out192, h, sizeof h);
+}
+
+void shard_lower_fused_ipc(ShardUpdate& x, const void* all, int ranks_on_device) {
+  use(x.ctx);
+  const int P = x.world, me = x.rank;
+  if (P < 2 || P > kFusedMaxShards)
+    throw Error(VXM_ERR_INVALID_ARGUMENT, "fused shard exchange: 2..8 shards");
+  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(all);
+  auto open = [&](int rank, int which) -> void* {
+    if (rank == me) return which == 0 ? x.rcv[0].p : which == 1 ? x.rcv[1].p : x.mbox.p;
+    void* p = nullptr;
+    VXM_CUDA(cudaIpcOpenMemHandle(&p, h[3 * rank + which], cudaIpcMemLazyEnablePeerAccess));
+    x.ipc_open.push_back(p);
+    return p;
+  };
+  const int right = (me + 1) % P, left = (me - 1 + P) % P;
+  std::vector<void*> boards(P);
+  for (int q = 0; q < P; ++q) boards[q] = open(q, 2);
+  void* r0 = open(right, 0);
+  void* l1 = open(left, 1);
+  ShardPeers pe = make_peers(x, nullptr, nullptr, r0, l1, boards[right], boards[left], boards.data(), P);
+  launch_fused(x, pe, ranks_on_device);
+}
+
 // The whole round loop on the device: launches k_shard_fused on every shard
 // (all resident at once: shards on one GPU split its SMs) and the changed-set
 // kernels; the caller synchronises once.
@@ -722,34 +809,17 @@ void shard_lower_fused(std::vector<ShardUpdate>& sh) {
     use(x.ctx);
     VXM_CUDA(cudaStreamSynchronize(x.ctx->stream));
   }
+  std::vector<void*> boards(P);
+  for (int q = 0; q < P; ++q) boards[q] = sh[q].mbox.p;
   for (int p = 0; p < P; ++p) {
     ShardUpdate& x = sh[p];
     ShardUpdate& right = sh[(p + 1) % P];
     ShardUpdate& left = sh[(p - 1 + P) % P];
-    ShardPeers pe{};
-    pe.to_right = xview(right.rcv[0].p, x.n_bnd);
-    pe.to_left = xview(left.rcv[1].p, x.n_bnd);
-    pe.flag_right = mbox_at<uint32_t>(right, kMboxFlags);
-    pe.flag_left = mbox_at<uint32_t>(left, kMboxFlags) + 1;
-    pe.my_flag = mbox_at<uint32_t>(x, kMboxFlags);
-    for (int q = 0; q < P; ++q) pe.board[q] = mbox_at<unsigned long long>(sh[q], kMboxBoard);
-    pe.my_board = mbox_at<unsigned long long>(x, kMboxBoard);
-    pe.go = mbox_at<uint32_t>(x, kMboxGo);
-    pe.rounds_out = mbox_at<uint32_t>(x, kMboxRounds);
-    pe.ctr = x.ctr.as<uint32_t>();
-    pe.rank = p;
-    pe.world = P;
+    ShardPeers pe = make_peers(x, &right, &left, right.rcv[0].p, left.rcv[1].p, right.mbox.p, left.mbox.p,
+                               boards.data(), P);
     int same = 0;  // shards sharing this GPU share its SMs
     for (auto& y : sh) same += y.ctx->device == x.ctx->device;
-    use(x.ctx);
-    const int per_sm = x.ctx->resident_per_sm((const void*)k_shard_fused, kL3Threads, 0, 4);
-    const int grid = std::max(1, per_sm * x.ctx->sm_count / same);
-    ShardRound sr0 = round_args(x, 0);  // ep = the base epoch
-    void* args[] = {&x.la, &sr0, &pe};
-    VXM_CUDA(cudaLaunchCooperativeKernel((const void*)k_shard_fused, dim3(grid), dim3(kL3Threads), args, 0,
-                                         x.ctx->stream));
-    x.ctx->count_launch();
-    check_launch(x.ctx, "k_shard_fused");
+    launch_fused(x, pe, same);
   }
 }
 
@@ -843,35 +913,8 @@ void run_update_esdf_sharded(int P, Layer** E, Layer** T, BlockList** updated,
   }
   if (fused) {
     shard_lower_fused(sh);
-    for (int p = 0; p < P; ++p) {
-      ShardUpdate& x = sh[p];
-      use(x.ctx);
-      ShardRound sr = round_args(x, 1);
-      sr.lowered = 1;
-      k_shard_changed<<<grid_for(x.ctx, uint64_t(std::max<uint32_t>(x.n_blocks, 1)) * 32), 256, 0,
-                        x.ctx->stream>>>(x.la, sr);
-      k_shard_meta_dev<<<1, 1, 0, x.ctx->stream>>>(x.E->meta, x.base, mbox_at<uint32_t>(x, kMboxRounds),
-                                                   x.cur ^ 1u);
-      x.ctx->count_launch(2);
-      BlockList* o = out[p];
-      o->bind(x.ctx);
-      o->ensure(x.n_all_cap);
-      launch_compact_keys(x.ctx, x.E->sorted_keys[x.E->sorted_parity], x.s.flags, &x.E->meta->num_blocks,
-                          x.n_all_cap, o->keys.as<uint64_t>(), o->d_count, nullptr, "k_compact_esdf");
-      o->host_valid = false;
-      o->host_pending = false;
-      o->count_hint = x.n_all_cap;
-      o->sorted_unique = true;
-      VXM_CUDA(cudaMemcpyAsync(x.h_cnt + 2, mbox_at<uint32_t>(x, kMboxRounds), sizeof(uint32_t),
-                               cudaMemcpyDeviceToHost, x.ctx->stream));
-      x.E->stage_meta();
-    }
-    for (auto& x : sh) {
-      x.rounds = 0;
-      shard_finish_sync(x, false);  // (status, meta, watchdog)
-      x.rounds = x.h_cnt[2];
-      x.ctx->stats.lower_rounds += x.rounds;
-    }
+    for (int p = 0; p < P; ++p) shard_finish_launch(sh[p], true, out[p]);
+    for (auto& x : sh) shard_finish_sync(x, true);
     return;
   }
   if (any) {

@@ -38,6 +38,8 @@ struct ShardUpdate {
   uint32_t* h_cnt = nullptr;    // pinned: [0] boundary blocks, [1] next dirty count
   cudaEvent_t ev = nullptr;     // in-process exchange ordering
   DevBuf mbox;                  // fused exchange: receive flags, count board, go, rounds
+  bool fused = false;           // the round loop ran in k_shard_fused (rounds on the device)
+  std::vector<void*> ipc_open;  // peer allocations opened for the fused multi-process exchange
   ShardUpdate() = default;
   ShardUpdate(const ShardUpdate&) = delete;
   ShardUpdate& operator=(const ShardUpdate&) = delete;
@@ -54,5 +56,10 @@ void shard_border_launch(ShardUpdate& x, uint32_t r);
 uint32_t shard_border(ShardUpdate& x, uint32_t r);
 uint32_t* next_count_ptr(ShardUpdate& x, uint32_t r);
 void shard_finish(ShardUpdate& x, bool lowered, BlockList* out);
+// Fused multi-process exchange over CUDA IPC: this rank's handles (rcv[0],
+// rcv[1], mailbox; 3 x 64 bytes — also clears the mailbox, so call before the
+// all-gather that acts as the barrier) and the launch of the round loop.
+void shard_ipc_handles(ShardUpdate& x, void* out192);
+void shard_lower_fused_ipc(ShardUpdate& x, const void* all_handles, int ranks_on_device);
 
 }  // namespace vxm

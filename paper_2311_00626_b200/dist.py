@@ -8,12 +8,17 @@ over the union map through the step C-ABI (vxm_shard_update_*):
 
   1. all-gather the updated lists; every shard marks against the union
   2. OR-reduce "anything to update"
-  3. per lowering round: local sweeps; the slab-boundary x-face snapshot goes
-     to both x-neighbours (rank -+ 1) — NCCL point-to-point on the device
-     buffers, enqueued on the library's stream behind the sweep kernel, or
-     staged through the host for gloo; the border phase computes the
-     cross-slab pairs on both owners; SUM-reduce the next dirty counts on the
-     device (one host read per round decides termination)
+  3. the lowering rounds: local sweeps; the slab-boundary x-face snapshot goes
+     to both x-neighbours (rank -+ 1); the border phase computes the
+     cross-slab pairs on both owners; the next dirty counts are summed.  By
+     default (2..8 ranks) the whole loop is ONE persistent kernel per rank
+     (vxm_shard_update_lower_fused): the snapshots are written straight into
+     the neighbours' receive buffers over peer memory (CUDA IPC handles
+     exchanged once per update), with system-scope release / acquire flags and
+     a count board for termination — no host step per round.  VXM_SHARD_FUSED=0
+     keeps the per-round steps: NCCL point-to-point on the device buffers
+     enqueued on the library's stream behind the sweep kernel (or staged
+     through the host for gloo) and an on-device SUM of the counts
   4. the changed blocks of this shard.
 
 The union over ranks of the ESDF layers and changed lists equals the single-map
@@ -22,6 +27,8 @@ update bit-for-bit (tests/test_gpu_dist_esdf.py).
 from __future__ import annotations
 
 import ctypes as C
+import os
+import socket
 
 import numpy as np
 import torch
@@ -93,6 +100,17 @@ def exchange_boundaries(send: torch.Tensor, recv_left: torch.Tensor, recv_right:
             req.wait()
 
 
+def _fused_enabled(world: int) -> bool:
+    """The fused exchange (vxm_shard_update_lower_fused) for 2..8 ranks unless
+    VXM_SHARD_FUSED=0 (then the per-round NCCL / gloo steps)."""
+    return 2 <= world <= 8 and os.environ.get("VXM_SHARD_FUSED", "1") != "0"
+
+
+def _device_key(cuda) -> tuple:
+    """(host, GPU uuid): ranks with equal keys share a GPU."""
+    return (socket.gethostname(), str(torch.cuda.get_device_properties(cuda).uuid))
+
+
 def update_esdf_distributed(esdf: EsdfLayer, tsdf: TsdfLayer, updated, cfg, group=None) -> np.ndarray:
     """update_esdf over the union of the ranks' shards; returns this shard's
     changed blocks.  `updated`: this shard's changed TSDF blocks ((N, 3) array or
@@ -129,7 +147,19 @@ def update_esdf_distributed(esdf: EsdfLayer, tsdf: TsdfLayer, updated, cfg, grou
                 C.byref(ptrs[1]), C.byref(sizes[1]), C.byref(ptrs[2]), C.byref(sizes[2])))
             views = [_view(p.value or 0, s.value, cuda) for p, s in zip(ptrs, sizes)]
             rnd = 0
-            if cdev.type == "cpu":  # gloo: stage through the host, synchronous steps
+            if _fused_enabled(world):
+                # the whole round loop in one persistent kernel per rank: the
+                # faces go straight into the neighbours' receive buffers over
+                # peer memory (CUDA IPC), termination through a count board
+                mine = (C.c_uint8 * 192)()
+                check(lib().vxm_shard_update_ipc_handles(su, mine))
+                gathered = [None] * world
+                dist.all_gather_object(gathered, (bytes(mine), _device_key(cuda)), group=group)
+                handles = b"".join(g[0] for g in gathered)
+                sharing = sum(1 for g in gathered if g[1] == gathered[rank][1])
+                hbuf = (C.c_uint8 * len(handles)).from_buffer_copy(handles)
+                check(lib().vxm_shard_update_lower_fused(su, hbuf, C.c_int(sharing)))
+            elif cdev.type == "cpu":  # gloo: stage through the host, synchronous steps
                 while True:
                     rnd += 1
                     check(lib().vxm_shard_update_sweep(su, C.c_uint32(rnd)))

@@ -77,8 +77,13 @@ def _worker(rank, world, slab, port, q, backend="gloo"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,slab,backend", [(2, 3, "gloo"), (3, 2, "gloo"), (2, 3, "nccl")])
-def test_distributed_esdf_equals_single_map(world, slab, backend):
+@pytest.mark.parametrize("world,slab,backend,fused", [(2, 3, "gloo", True), (3, 2, "gloo", True),
+                                                      (2, 3, "gloo", False), (3, 2, "gloo", False),
+                                                      (2, 3, "nccl", True), (2, 3, "nccl", False)])
+def test_distributed_esdf_equals_single_map(world, slab, backend, fused):
+    """fused: the round loop in one persistent kernel per rank with the faces
+    exchanged over peer memory (CUDA IPC; the ranks share this GPU here);
+    otherwise the per-round steps with the exchange by the collective backend."""
     import torch
     if backend == "nccl" and torch.cuda.device_count() < world:
         pytest.skip(f"NCCL path needs {world} GPUs (this box has {torch.cuda.device_count()})")
@@ -86,8 +91,16 @@ def test_distributed_esdf_equals_single_map(world, slab, backend):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, slab, port, q, backend)) for r in range(world)]
-    for p in procs:
-        p.start()
+    old = os.environ.get("VXM_SHARD_FUSED")
+    os.environ["VXM_SHARD_FUSED"] = "1" if fused else "0"
+    try:
+        for p in procs:
+            p.start()
+    finally:
+        if old is None:
+            os.environ.pop("VXM_SHARD_FUSED", None)
+        else:
+            os.environ["VXM_SHARD_FUSED"] = old
     ok = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
