@@ -211,6 +211,14 @@ __device__ void shard_border_body(const LowerArgs& a, const ShardRound& sr, cg::
         if (lo < 0) continue;
         if (__ldcg(a.stamp_dirty[cp] + lo) == ep) continue;  // lo's side-0 item has it
       }
+      if (r1) {
+        // after reset_parented only sites give, and blocks an earlier axis of
+        // this round changed (listed for round 2 by mark_changed, visible after
+        // the grid barrier): a pair with no giver on either face is the identity
+        const bool g_lo = a.site_any[lo] != 0 || (axis > 0 && __ldcg(a.stamp_dirty[np] + lo) == ep_next);
+        const bool g_hi = a.site_any[hi] != 0 || (axis > 0 && __ldcg(a.stamp_dirty[np] + hi) == ep_next);
+        if (!g_lo && !g_hi) continue;
+      }
       bool ac = false, bc = false;
       unsigned long long mlo[3] = {0, 0, 0}, mhi[3] = {0, 0, 0};
 #pragma unroll
