@@ -19,4 +19,7 @@ full c2_dilate k_dilate 5 python tools/frames.py c2 7
 full c3_integrate k_integrate 4 python tools/frames.py c3 6
 full c3_lower k_lower 4 python tools/frames.py c3 6
 full c5_lower k_lower 2 python tools/c5_steps.py 3
+full c4_lower k_lower 5 python tools/frames.py c4 7
+full c1_rays k_rays 5 python tools/frames.py c1 7
+full c1_integrate k_integrate 5 python tools/frames.py c1 7
 ls -la gpurun_out/*.ncu-rep
