@@ -144,6 +144,7 @@ struct DevStatus {
   uint32_t pad3[3];
   uint32_t meta2_blocks;     // second layer's meta (fused frame update: TSDF + ESDF)
   uint32_t meta2_cur;
+  uint32_t integ_claim;      // k_integrate: candidate blocks claimed (dynamic schedule)
 };
 
 // ---- decoupled look-back scan over (a, b) count pairs ------------------------
