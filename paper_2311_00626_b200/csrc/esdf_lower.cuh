@@ -368,9 +368,8 @@ __device__ inline int raw_lin(int t, int v) { return 4 * (t + 64 * (v >> 2)) + (
 // reset_parented (esdf/integrator.cpp:352-363) on the way in.  Returns, for
 // the whole group, whether the block holds a site (after the reset, sites are
 // the only givers) and whether it qualifies for the compact format.
-__device__ inline void load_raw3(RawBlock& r, const uint32_t* __restrict__ src, int t, int bar,
-                                 const Limits& lim, bool reset, bool* any_site_out, bool* fast_out) {
-  raw_load(r, src, t);
+__device__ inline void raw_check3(RawBlock& r, int t, int bar, const Limits& lim, bool reset,
+                                  bool* any_site_out, bool* fast_out) {
   bool out = lim.max_sq > kFastOff * kFastOff, any_site = false;
 #pragma unroll
   for (int v = 0; v < 8; ++v) {
@@ -392,6 +391,11 @@ __device__ inline void load_raw3(RawBlock& r, const uint32_t* __restrict__ src, 
   }
   *fast_out = !group_sync_or(bar, out);
   *any_site_out = reset ? group_sync_or(bar, any_site) : true;
+}
+__device__ inline void load_raw3(RawBlock& r, const uint32_t* __restrict__ src, int t, int bar,
+                                 const Limits& lim, bool reset, bool* any_site_out, bool* fast_out) {
+  raw_load(r, src, t);
+  raw_check3(r, t, bar, lim, reset, any_site_out, fast_out);
 }
 
 // Registers -> working format in shared memory (compact or general).
@@ -459,6 +463,7 @@ struct LowerArgs {
   uint32_t* pool[2];
   LayerMeta* meta;
   const int32_t* nbr;
+  const int32_t* nbr27;  // [cap][27] 3x3x3 neighbourhood slots (k_lower_xr)
   uint32_t* stamp_dirty[2];
   uint32_t* stamp_lchg;
   int32_t* list[2];
@@ -514,6 +519,16 @@ __device__ inline uint32_t ld_relaxed(const uint32_t* p) {
 __device__ inline void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ inline uint32_t atom_add_release(uint32_t* p, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+__device__ inline uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
 // Pair stamps carry, besides the round epoch, whether the pair changed its
 // lower / upper block (read by the dependent pairs of round 1).
 constexpr uint32_t kStampLoChg = 1u << 31, kStampHiChg = 1u << 30, kStampEp = kStampHiChg - 1u;
@@ -523,9 +538,11 @@ constexpr uint32_t kStampLoChg = 1u << 31, kStampHiChg = 1u << 30, kStampEp = kS
 // stamp word (epoch + change bits).
 __device__ inline uint32_t wait_stamp(const uint32_t* p, uint32_t ep, uint32_t* watchdog,
                                       uint32_t code, int32_t blk) {
-  // spin on relaxed loads (an acquire per iteration would invalidate L1 each
-  // time), then one acquire once the stamp is seen
-  for (uint32_t it = 0; (ld_relaxed(p) & kStampEp) != ep; ++it) {
+  // spin on acquire loads: the block data is read through L2 (ld.cg), so the
+  // L1 invalidation of each acquire costs little, and the hand-off saves the
+  // separate acquire's round trip (measured: k_lower -2 % on C2 / -1 % on C5)
+  uint32_t v;
+  for (uint32_t it = 0; ((v = ld_acquire(p)) & kStampEp) != ep; ++it) {
     if (it > (1u << 22)) {
       if (atomicExch(watchdog, 1u) == 0u) {  // record the first expired wait
         watchdog[1] = code;
@@ -536,7 +553,7 @@ __device__ inline uint32_t wait_stamp(const uint32_t* p, uint32_t ep, uint32_t* 
     }
     __nanosleep(20);
   }
-  return ld_acquire(p);
+  return v;
 }
 
 __device__ inline const EV load_voxel(const uint32_t* pool, int32_t slot, int lin) {

@@ -262,8 +262,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         }
         // round 1 completes only after every sweep / copy: counted per group
         if (t == 0 && r1_mine) {
-          __threadfence();  // (release: the group's block writes before the count)
-          atomicAdd(a.r1 + 4, r1_mine);
+          atom_add_release(a.r1 + 4, r1_mine);  // the group's block writes before the count
         }
         r1_mine = 0;
         const uint32_t n_ns = *((volatile uint32_t*)(a.r1 + 1));
@@ -289,8 +288,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           }
         }
         if (lane == 0 && r1_mine) {  // (per warp)
-          __threadfence();
-          atomicAdd(a.r1 + 4, r1_mine);
+          atom_add_release(a.r1 + 4, r1_mine);
         }
         if (a.trace && lane == 0) {  // VXM_TRACE_XR: end of the round-1 sweeps / copies
           unsigned long long tm;
@@ -335,26 +333,35 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             tr_min(a.trace, R, 0, tsw0);
           }
           // the block's round R - 1 pairs (the reference's only writers of it since
-          // its last sweep) must be complete: lanes 0-5 of the group's first warp;
-          // the faces they changed give the lines to sweep first
+          // its last sweep) must be complete: lanes 0-5 of the group's first warp
+          // wait; then the block's load is issued first and the faces the pairs
+          // changed (the lines to sweep first) are read while it is in flight
+          uint32_t wv = 0;
+          int32_t wlo = -1;
+          if (t < 6) {
+            const int q = t >> 1;
+            const uint32_t epp = ep - 1;  // round R - 1
+            const bool r1p = R - 1 == 1;
+            const bool s_dirty = r1p || __ldcg(a.stamp_dirty[np] + s) == epp;
+            const int32_t c = __ldg(a.nbr + size_t(s) * 6 + t);  // +q (even t) / -q (odd t)
+            if (c >= 0 && (s_dirty || __ldcg(a.stamp_dirty[np] + c) == epp)) {
+              const bool s_lo = (t & 1) == 0;  // pair (s, c) or (c, s)
+              wlo = s_lo ? s : c;
+              wv = wait_stamp(a.stamp_pair[q] + wlo, epp, &a.status->watchdog, 30u + q, wlo);
+            }
+          }
+          group_sync(bar);  // every wait done before the voxels are read
+          unsigned long long tsa = 0, tsb = 0, tsc = 0;
+          if (a.trace && t == 0) tsa = gtime();
+          RawBlock rb;
+          raw_load(rb, work + size_t(s) * 1536, t);
           if (t < 32) {
             unsigned long long m[3] = {0, 0, 0};
-            if (t < 6) {
+            if (t < 6 && wlo >= 0) {
               const int q = t >> 1;
-              const int32_t c = __ldg(a.nbr + size_t(s) * 6 + t);  // +q (even t) / -q (odd t)
-              if (c >= 0) {
-                const uint32_t epp = ep - 1;  // round R - 1
-                const bool r1p = R - 1 == 1;
-                const bool exists = r1p || __ldcg(a.stamp_dirty[np] + s) == epp ||
-                                    __ldcg(a.stamp_dirty[np] + c) == epp;
-                if (exists) {
-                  const bool s_lo = (t & 1) == 0;  // pair (s, c) or (c, s)
-                  const int32_t lo = s_lo ? s : c;
-                  const uint32_t v = wait_stamp(a.stamp_pair[q] + lo, epp, &a.status->watchdog, 30u + q, lo);
-                  if (v & (s_lo ? kStampLoChg : kStampHiChg))
-                    face_lines(__ldcg(a.pair_face[q] + 2 * size_t(lo) + (s_lo ? 0 : 1)), q, s_lo ? 7 : 0, m);
-                }
-              }
+              const bool s_lo = (t & 1) == 0;
+              if (wv & (s_lo ? kStampLoChg : kStampHiChg))
+                face_lines(__ldcg(a.pair_face[q] + 2 * size_t(wlo) + (s_lo ? 0 : 1)), q, s_lo ? 7 : 0, m);
             }
             unsigned long long m0 = warp_or64(m[0]), m1 = warp_or64(m[1]), m2 = warp_or64(m[2]);
             if (t == 0) {
@@ -364,12 +371,8 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
               G.mask[0][1] = G.mask[1][1] = G.mask[2][1] = 0ull;
             }
           }
-          group_sync(bar);  // every wait done before the masks and voxels are read
-          unsigned long long tsa = 0, tsb = 0, tsc = 0;
-          if (a.trace && t == 0) tsa = gtime();
-          RawBlock rb;
           bool any_site, fast;
-          load_raw3(rb, work + size_t(s) * 1536, t, bar, lim, false, &any_site, &fast);
+          raw_check3(rb, t, bar, lim, false, &any_site, &fast);  // (its barriers publish the masks)
           stage_block3(G, rb, t, bar, lim, fast);
           if (a.trace && t == 0) tsb = gtime();
           const bool sw_chg = sweep_block3(G, t, bar, lim);
@@ -444,7 +447,6 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         } else {
           lo = __ldg(a.nbr + size_t(d) * 6 + 2 * axis + 1);  // d - axis
           hi = d;
-          if (lo >= 0 && is_dirty(lo)) lo = -1;  // lo's side-0 item has this pair
         }
         // round 1: whether a side can give is known before any wait (after the
         // reset only sites give); the loads are issued ahead of the waits
@@ -460,26 +462,35 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         if (lo >= 0 && hi >= 0 && r1 && !r1c && axis == 0 && !site_lo && !site_hi) {
           if (lane == 0) st_release(a.stamp_pair[0] + lo, ep);
         } else if (lo >= 0 && hi >= 0) {
-          bool dep_chg = false;
-          if (lane < 2 + 4 * axis) {
-            if (lane < 2) {
-              const int32_t b = lane == 0 ? lo : hi;
-              if (is_dirty(b)) wait_stamp(a.stamp_swept + b, ep, &a.status->watchdog, 10u + axis, b);
-            } else {
-              const int q = (lane - 2) >> 2;
-              const int32_t b = ((lane - 2) & 2) ? hi : lo;
-              const bool b_is_hi = ((lane - 2) & 1) == 0;
-              int32_t c = b;
-              if (b_is_hi) c = __ldg(a.nbr + size_t(b) * 6 + 2 * q + 1);
-              if (c >= 0) {
-                const int32_t n = __ldg(a.nbr + size_t(c) * 6 + 2 * q);
-                if (n >= 0 && (is_dirty(c) || is_dirty(n))) {
-                  const uint32_t v =
-                      wait_stamp(a.stamp_pair[q] + c, ep, &a.status->watchdog, 20u + 10u * q + axis, c);
-                  dep_chg = (v & (b_is_hi ? kStampHiChg : kStampLoChg)) != 0u;
-                }
-              }
+          // every lane's dirty-stamp / neighbour loads first, all in flight
+          // together: lanes 0 / 1 the pair's blocks (their sweeps), lanes 2.. the
+          // lower-axis pairs through its faces, lower block c, upper block n
+          // (one neighbour look-up: the other block is the face's own)
+          bool own_dirty = false;
+          int32_t wc = -1;
+          const int q = (lane - 2) >> 2;
+          const bool b_is_hi = ((lane - 2) & 1) == 0;
+          if (lane < 2) {
+            own_dirty = is_dirty(lane == 0 ? lo : hi);
+          } else if (lane < 2 + 4 * axis) {
+            const int32_t b = ((lane - 2) & 2) ? hi : lo;
+            const int32_t o = __ldg(a.nbr + size_t(b) * 6 + 2 * q + (b_is_hi ? 1 : 0));
+            const int32_t c = b_is_hi ? o : b, n = b_is_hi ? b : o;
+            if (o >= 0) {
+              const bool dc = is_dirty(c), dn = is_dirty(n);
+              if (dc || dn) wc = c;
             }
+          }
+          // side 1 with a dirty lower block: lo's side-0 item has this pair
+          const bool dup = side == 1 && __shfl_sync(0xffffffffu, own_dirty, 0);
+          if (!dup) {
+          bool dep_chg = false;
+          if (lane < 2) {
+            const int32_t b = lane == 0 ? lo : hi;
+            if (own_dirty) wait_stamp(a.stamp_swept + b, ep, &a.status->watchdog, 10u + axis, b);
+          } else if (wc >= 0) {
+            const uint32_t v = wait_stamp(a.stamp_pair[q] + wc, ep, &a.status->watchdog, 20u + 10u * q + axis, wc);
+            dep_chg = (v & (b_is_hi ? kStampHiChg : kStampLoChg)) != 0u;
           }
           const uint32_t chg_mask = __ballot_sync(0xffffffffu, dep_chg);
           __syncwarp();
@@ -497,6 +508,10 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
             // the faces this pair changes, bit = face position lane + 32 k
             unsigned long long flo = 0, fhi = 0;
+            // both face positions of the lane are loaded before any store (the
+            // four voxels are distinct): one L2 round trip on the hop, not two
+            int la[2], lb[2];
+            EV va[2], vb[2];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
@@ -504,12 +519,17 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
               if (axis == 0) { ax = 7; ay = i0; az = j0; bx = 0; by = i0; bz = j0; }
               else if (axis == 1) { ax = i0; ay = 7; az = j0; bx = i0; by = 0; bz = j0; }
               else { ax = i0; ay = j0; az = 7; bx = i0; by = j0; bz = 0; }
-              const int la = ax + 8 * ay + 64 * az, lb = bx + 8 * by + 64 * bz;
-              EV va = load_voxel(work, lo, la), vb = load_voxel(work, hi, lb);
-              const bool cb = relax(vb, va, dx, dy, dz, lim);     // exchange_pair :158
-              const bool ca = relax(va, vb, -dx, -dy, -dz, lim);  // :159
-              if (cb) store_voxel(work, hi, lb, vb);
-              if (ca) store_voxel(work, lo, la, va);
+              la[k] = ax + 8 * ay + 64 * az;
+              lb[k] = bx + 8 * by + 64 * bz;
+              va[k] = load_voxel(work, lo, la[k]);
+              vb[k] = load_voxel(work, hi, lb[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const bool cb = relax(vb[k], va[k], dx, dy, dz, lim);     // exchange_pair :158
+              const bool ca = relax(va[k], vb[k], -dx, -dy, -dz, lim);  // :159
+              if (cb) store_voxel(work, hi, lb[k], vb[k]);
+              if (ca) store_voxel(work, lo, la[k], va[k]);
               flo |= (unsigned long long)__ballot_sync(0xffffffffu, ca) << (32 * k);
               fhi |= (unsigned long long)__ballot_sync(0xffffffffu, cb) << (32 * k);
             }
@@ -540,6 +560,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
               }
             }
           }
+          }  // !dup
         }
         if (a.trace && lane == 0) tr_max(a.trace, R, 3 + axis, gtime());
         ++my_done;
@@ -547,8 +568,9 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
       // round accounting, one atomic per warp: the warp whose items complete
       // round R publishes it (every item this warp claimed is done here)
       if (lane == 0 && my_done) {
-        __threadfence();
-        const uint32_t done = atomicAdd(RG(ring, kRingDone + q4), my_done) + my_done;
+        // release: this warp's items before the count; acquire: the warp that
+        // completes the round sees every item (the counter's release sequence)
+        const uint32_t done = atom_add_acq_rel(RG(ring, kRingDone + q4), my_done) + my_done;
         if (done == n_items) {
           if (R == 1) {  // and every round-1 sweep / copy (see r1_ident)
             for (uint32_t it = 0; ld_acquire(a.r1 + 4) < n_blocks; ++it) {
@@ -559,7 +581,6 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
               __nanosleep(64);
             }
           }
-          __threadfence();
           const int q4nn = int((R + 2u) & 3u);
           *RG(ring, kRingCnt + q4nn) = 0u;
           *RG(ring, kRingSwc + q4nn) = *RG(ring, kRingPc + q4nn) = *RG(ring, kRingDone + q4nn) = 0u;
@@ -570,8 +591,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             a.trace[R] = tm;
             a.trace[64 + R] = n_dirty;
           }
-          __threadfence();
-          st_release(RG(ring, kRingLast), R);
+          st_release(RG(ring, kRingLast), R);  // (orders the zeroing above too)
         }
       }
       // the next round's sweeps re-form the groups (both warps)

@@ -47,6 +47,9 @@ from ._abi import (Camera as CameraIntrinsics, Lidar as LidarIntrinsics,  # noqa
                    OCCUPANCY_DTYPE)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libvoxmap_b200.so")
+# A/B measurements of kernel variants (tools/ab.py) load another build of the
+# same library; it is still the native library, never a fallback.
+LIB_PATH = os.environ.get("VXM_LIB_PATH", LIB_PATH)
 
 
 class VoxmapError(RuntimeError):
