@@ -36,6 +36,7 @@ struct IntegrateArgs {
   void* pool;  // float2 (TSDF) or float (occupancy log-odds) per voxel
   uint8_t* changed;
   const float* depth;
+  const double4* atab;  // LiDAR: atan2 table (vxm_atan2)
   int W, H;
   vxm_pose T_SL;
   int lidar;
@@ -88,6 +89,59 @@ struct VoxOps<true> {  // occupancy_update — updates.hpp:59-72
 };
 
 __device__ inline bool valid_depth_i(float d) { return d > 0.0f && isfinite(d); }
+
+// ---- FP64 atan2 for the LiDAR projection ----------------------------------------
+// lidar.hpp:43-55 evaluates atan2 (azimuth) and acos (polar angle) per voxel;
+// the CUDA libm versions were half of k_integrate's LiDAR instructions (one in
+// six of them materialising polynomial constants).  vxm_atan2 instead rotates
+// (x, y) by a table vector near its angle and sums a short series:
+//   k     = nearest multiple of pi/512 to an FP32 estimate of the angle
+//   (c,s) = (cos, sin)(k pi/512) rounded to double; psi = its exact angle
+//           atan2(s, c) as a double-double (host long double, kAtanTabN entries)
+//   x' = x c + y s,  y' = y c - x s      (y' by Kahan's difference of products)
+//   atan2(y, x) = psi + atan(y'/x'),  |y'/x'| < 0.005:  q - q^3/3 + q^5/5 - q^7/7
+// Accuracy ~1 ulp (libm class: glibc and CUDA libm also differ in the last
+// ulp); the tolerance tests (tests/helpers.py:36) cover it.
+// y == 0 (signed zero / -pi vs pi) goes to the libm routine.
+constexpr int kAtanTabN = 1025;  // k = -512 .. 512
+
+// sqrt to ~1 ulp (an atan2 argument; not the depth, which stays correctly
+// rounded): MUFU.RSQ64H seed + two Newton steps, 0 for 0.
+__device__ inline double sqrt_approx(double h2) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h2));
+  y = y * fma(-0.5 * h2, y * y, 1.5);
+  y = y * fma(-0.5 * h2, y * y, 1.5);
+  return h2 > 0.0 ? h2 * y : 0.0;
+}
+__constant__ double kAtanQ[3] = {-1.0 / 3.0, 1.0 / 5.0, -1.0 / 7.0};
+
+__device__ inline double vxm_atan2(double y, double x, const double4* __restrict__ tab) {
+  if (y == 0.0) return atan2(y, x);
+  // FP32 estimate (|error| < 1e-4 rad): octant reduction + odd polynomial
+  const float fx = float(x), fy = float(y);
+  const float ax = fabsf(fx), ay = fabsf(fy);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float t = __fdividef(mn, mx), t2 = t * t;
+  float e = t * (0.99978784f + t2 * (-0.32580840f + t2 * (0.15557865f + t2 * (-0.04432655f))));
+  if (ay > ax) e = 1.57079633f - e;
+  if (fx < 0.0f) e = 3.14159265f - e;
+  if (fy < 0.0f) e = -e;
+  const int k = __float2int_rn(e * 162.97466f);  // 512 / pi
+  const double2* tp = reinterpret_cast<const double2*>(tab + (k + 512));
+  const double2 CS = __ldg(tp), PSI = __ldg(tp + 1);  // (c, s), (psi_hi, psi_lo)
+  const double xr = fma(x, CS.x, y * CS.y);
+  const double w = x * CS.y;
+  const double yr = fma(y, CS.x, -w) - fma(x, CS.y, -w);
+  // q = yr / xr (xr > 0): approximate reciprocal (MUFU.RCP64H) + two Newton steps
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(xr));
+  r = fma(r, fma(-xr, r, 1.0), r);
+  r = fma(r, fma(-xr, r, 1.0), r);
+  const double q = yr * r, q2 = q * q;
+  const double d = fma(q * q2, fma(q2, fma(q2, kAtanQ[2], kAtanQ[1]), kAtanQ[0]), q);
+  return PSI.x + (PSI.y + d);
+}
 
 __device__ inline bool sample_nearest_d(const float* img, int W, int H, double u, double v,
                                         float* out) {
@@ -184,15 +238,16 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<O
       ok = sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s);
     }
   } else {
-    // LidarIntrinsics::project — lidar.hpp:43-55 (CUDA libm atan2/acos).  The
-    // elevation is evaluated first: a voxel outside the beam fan then needs
-    // no atan2 (C3 k_integrate -5 %).
-    double c = __ddiv_rn(pz, d_v);
-    c = c < -1.0 ? -1.0 : (1.0 < c ? 1.0 : c);
-    const double v = __dmul_rn(__dsub_rn(acos(c), a.el0), a.v_scale);
+    // LidarIntrinsics::project — lidar.hpp:43-55: polar = acos(z / |p|)
+    // (= atan2(|(x, y)|, z)) and azimuth = atan2(y, x), both by vxm_atan2.
+    // The elevation is evaluated first: a voxel outside the beam fan then
+    // needs no azimuth (C3 k_integrate -5 %).
+    const double hxy = sqrt_approx(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)));
+    const double polar = hxy == 0.0 ? (pz > 0.0 ? 0.0 : 3.141592653589793) : vxm_atan2(hxy, pz, a.atab);
+    const double v = __dmul_rn(__dsub_rn(polar, a.el0), a.v_scale);
     if (!(v >= 0.0 && v < double(a.ne))) return false;
     const double kTwoPi = 6.283185307179586;
-    double az = __dsub_rn(atan2(py, px), a.az0);
+    double az = __dsub_rn(vxm_atan2(py, px, a.atab), a.az0);
     // az - 2 pi floor(az / 2 pi): when 0 <= az < 2 pi (1 - 2^-40) the quotient
     // is certainly in [0, 1) and the floor is 0 (no division); otherwise the
     // exact expression
@@ -226,7 +281,10 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<O
 // occupancy is the measured optimum of each (C2 -13 %, C3 -8 % kernel time vs
 // the register-unbounded build).
 template <bool OCC, bool FASTCAM>
-__global__ void __launch_bounds__(256, FASTCAM ? 4 : 3) k_integrate(IntegrateArgs a) {
+#ifndef VXM_INTEG_GEN_MINB
+#define VXM_INTEG_GEN_MINB 4
+#endif
+__global__ void __launch_bounds__(256, FASTCAM ? 4 : VXM_INTEG_GEN_MINB) k_integrate(IntegrateArgs a) {
   pdl_wait();  // see launch_pdl
   pdl_trigger();
   using Ops = VoxOps<OCC>;
@@ -426,6 +484,28 @@ static float quantize_log_odds(float v) {
   return static_cast<float>(std::nearbyint(double(v) * 4096.0) / 4096.0);
 }
 
+// The vxm_atan2 table (host long double): entry k + 512 holds (c, s) =
+// (cos, sin)(k pi / 512) rounded to double and the exact angle of that rounded
+// vector as a double-double.
+static const double4* ensure_atan_table(Context* ctx) {
+  if (ctx->atan_tab.p) return ctx->atan_tab.as<const double4>();
+  std::vector<double4> t(kAtanTabN);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int i = 0; i < kAtanTabN; ++i) {
+    const long double phi = (long double)(i - 512) * pi / 512.0L;
+    const double c = double(cosl(phi)), s = double(sinl(phi));
+    long double psi = atan2l((long double)s, (long double)c);
+    psi += 2.0L * pi * roundl((phi - psi) / (2.0L * pi));  // k = +-512: the side of +-pi k is on
+    const double hi = double(psi);
+    t[i] = make_double4(c, s, hi, double(psi - (long double)hi));
+  }
+  ctx->atan_tab.ensure(sizeof(double4) * t.size());
+  VXM_CUDA(cudaMemcpyAsync(ctx->atan_tab.p, t.data(), sizeof(double4) * t.size(), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ctx->atan_tab.as<const double4>();
+}
+
 uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_config& cfg,
                           BlockList* changed_out) {
   Context* ctx = L->ctx;
@@ -442,6 +522,7 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   a.pool = L->pool[0];
   a.changed = ctx->cand_flags.as<uint8_t>();
   a.depth = va.depth_dev;
+  if (va.lidar) a.atab = ensure_atan_table(ctx);
   a.W = va.width;
   a.H = va.height;
   vxm_pose_inverse(&va.T_LS, &a.T_SL);  // integrator.cpp:89 (host, pinned order)

@@ -59,6 +59,7 @@ struct Context {
   DevBuf cand_slots;      // int32 slot | new flag
   DevBuf cand_flags;      // uint8 per candidate (changed)
   DevBuf lidar_dirs;      // double3 per LiDAR pixel (host glibc LUT)
+  DevBuf atan_tab;        // double4 x kAtanTabN: the LiDAR projection's atan2 table (integrate.cu)
   vxm_lidar lut_key{};
   bool lut_valid = false;
   DevBuf cam_dirs;        // double2 per camera tile: ((u - cu) / fu, (v - cv) / fv)
