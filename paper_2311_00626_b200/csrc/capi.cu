@@ -387,7 +387,8 @@ vxm_status vxm_context_create(int device, vxm_context** out) {
       VXM_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     VXM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DevStatus)));
-    VXM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DevStatus)));
+    VXM_CUDA(cudaHostAlloc(&ctx->h_status, sizeof(DevStatus), cudaHostAllocMapped));
+    VXM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->h_status_dev), ctx->h_status, 0));
     // The context stream is non-blocking: every initialisation is ordered on
     // it, never on the legacy stream (which it does not synchronise with).
     VXM_CUDA(cudaMemsetAsync(ctx->d_status, 0, sizeof(DevStatus), ctx->stream));

@@ -112,9 +112,39 @@ void Context::flush_copies() {
   }
   status_copies.clear();
 }
+// The last queued word copies, then the whole status written straight into
+// the mapped pinned host copy: the call's one host read needs no separate
+// device-to-host DMA (whose small-copy latency is several microseconds).
+constexpr int kStatusWords = int(sizeof(DevStatus) / sizeof(uint32_t));
+static_assert(kStatusWords <= 32, "DevStatus fits one warp");
+__global__ void k_status_out(WordCopies c, const uint32_t* __restrict__ st, uint32_t* __restrict__ host) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x < c.n) *c.dst[threadIdx.x] = *c.src[threadIdx.x];
+  __syncwarp();
+  if (threadIdx.x < kStatusWords) host[threadIdx.x] = st[threadIdx.x];
+}
 void Context::sync_status() {
-  flush_copies();
-  VXM_CUDA(cudaMemcpyAsync(h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
+  // all but the last batch of queued copies, then the last batch + status out
+  WordCopies last{};
+  size_t i = 0;
+  while (status_copies.size() - i > 16) {
+    WordCopies c{};
+    for (; c.n < 16; ++i, ++c.n) {
+      c.src[c.n] = status_copies[i].src;
+      c.dst[c.n] = status_copies[i].dst;
+    }
+    launch_pdl(stream, k_copy_words, dim3(1), dim3(32), 0, c);
+    count_launch();
+  }
+  for (; i < status_copies.size(); ++i, ++last.n) {
+    last.src[last.n] = status_copies[i].src;
+    last.dst[last.n] = status_copies[i].dst;
+  }
+  status_copies.clear();
+  launch_pdl(stream, k_status_out, dim3(1), dim3(32), 0, last, reinterpret_cast<const uint32_t*>(d_status),
+             reinterpret_cast<uint32_t*>(h_status_dev));
+  count_launch();
   VXM_CUDA(cudaStreamSynchronize(stream));
   prof_resolve();
 }

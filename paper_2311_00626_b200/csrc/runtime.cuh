@@ -44,7 +44,8 @@ struct Context {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   DevStatus* d_status = nullptr;
-  DevStatus* h_status = nullptr;  // pinned
+  DevStatus* h_status = nullptr;      // pinned, mapped: written by k_status_out
+  DevStatus* h_status_dev = nullptr;  // its device address
   uint64_t launches = 0;
   ScanState scan;
   uint32_t call_epoch = 0;
