@@ -179,6 +179,12 @@ vxm_status vxm_context_set_profiling(vxm_context* ctx, int enable);
  * ("k_integrate", "k_lower", "k_dilate_alloc", "k_rays", "k_mark", ...). */
 vxm_status vxm_context_kernel_time(vxm_context* ctx, const char* kernel, double* ms,
                                    uint64_t* launches);
+/* Diagnostics (parity tests): the LiDAR projection's angles exactly as
+ * k_integrate computes them for p = (x, y, z) in the sensor frame —
+ * azimuth = atan2(y, x) and polar = acos(z / |p|) of LidarIntrinsics::project
+ * (lidar.hpp:43-55) — for n points (xyz: n x 3 doubles, host memory). */
+vxm_status vxm_diag_lidar_angles(vxm_context* ctx, const double* xyz, uint64_t n, double* azimuth,
+                                 double* polar);
 void vxm_context_reset_kernel_times(vxm_context* ctx);
 
 /* ---- block lists ------------------------------------------------------- */

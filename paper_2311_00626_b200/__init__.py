@@ -17,4 +17,4 @@ from .voxmap import (BlockList, CameraIntrinsics, Context, EsdfConfig, EsdfLayer
                      save_mesh_ply, replay_cake, HostBuffer, pinned_like,
                      linear_voxel_index, voxel_index_from_linear, global_voxel_index,
                      block_of_global_voxel, local_voxel_of_global, position_to_global_voxel,
-                     position_to_indices, voxel_center, block_origin)
+                     position_to_indices, voxel_center, block_origin, diag_lidar_angles)

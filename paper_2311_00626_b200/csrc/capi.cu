@@ -455,6 +455,13 @@ vxm_status vxm_context_kernel_time(vxm_context* ctx, const char* kernel, double*
     *launches = it == ctx->ktime.end() ? 0 : it->second.second;
   });
 }
+vxm_status vxm_diag_lidar_angles(vxm_context* ctx, const double* xyz, uint64_t n, double* azimuth,
+                                 double* polar) {
+  return guard([&] {
+    REQUIRE_ARG(ctx && (n == 0 || (xyz && azimuth && polar)), "diag_lidar_angles: null argument");
+    diag_lidar_angles(ctx, xyz, n, azimuth, polar);
+  });
+}
 void vxm_context_reset_kernel_times(vxm_context* ctx) {
   if (ctx) ctx->ktime.clear();
 }

@@ -143,6 +143,12 @@ __device__ inline double vxm_atan2(double y, double x, const double4* __restrict
   return PSI.x + (PSI.y + d);
 }
 
+// polar angle acos(z / |p|) = atan2(|(x, y)|, z) (lidar.hpp:53)
+__device__ inline double lidar_polar(double px, double py, double pz, const double4* tab) {
+  const double hxy = sqrt_approx(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)));
+  return hxy == 0.0 ? (pz > 0.0 ? 0.0 : 3.141592653589793) : vxm_atan2(hxy, pz, tab);
+}
+
 __device__ inline bool sample_nearest_d(const float* img, int W, int H, double u, double v,
                                         float* out) {
   const int col = int(floor(u)), row = int(floor(v));
@@ -242,8 +248,7 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<O
     // (= atan2(|(x, y)|, z)) and azimuth = atan2(y, x), both by vxm_atan2.
     // The elevation is evaluated first: a voxel outside the beam fan then
     // needs no azimuth (C3 k_integrate -5 %).
-    const double hxy = sqrt_approx(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)));
-    const double polar = hxy == 0.0 ? (pz > 0.0 ? 0.0 : 3.141592653589793) : vxm_atan2(hxy, pz, a.atab);
+    const double polar = lidar_polar(px, py, pz, a.atab);
     const double v = __dmul_rn(__dsub_rn(polar, a.el0), a.v_scale);
     if (!(v >= 0.0 && v < double(a.ne))) return false;
     const double kTwoPi = 6.283185307179586;
@@ -504,6 +509,31 @@ static const double4* ensure_atan_table(Context* ctx) {
                            ctx->stream));
   VXM_CUDA(cudaStreamSynchronize(ctx->stream));
   return ctx->atan_tab.as<const double4>();
+}
+
+// vxm_diag_lidar_angles: the projection's two angles, as integrate_voxel
+// evaluates them.
+__global__ void k_diag_angles(const double* __restrict__ xyz, uint64_t n, const double4* tab, double* az,
+                              double* polar) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    az[i] = vxm_atan2(y, x, tab);
+    polar[i] = lidar_polar(x, y, z, tab);
+  }
+}
+void diag_lidar_angles(Context* ctx, const double* xyz, uint64_t n, double* az, double* polar) {
+  if (n == 0) return;
+  const double4* tab = ensure_atan_table(ctx);
+  DevBuf d;
+  d.ensure(sizeof(double) * 5 * n);
+  double* dx = d.as<double>();
+  VXM_CUDA(cudaMemcpyAsync(dx, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+  k_diag_angles<<<std::max<uint64_t>(1, std::min<uint64_t>(4096, (n + 255) / 256)), 256, 0, ctx->stream>>>(
+      dx, n, tab, dx + 3 * n, dx + 4 * n);
+  ctx->count_launch();
+  VXM_CUDA(cudaMemcpyAsync(az, dx + 3 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VXM_CUDA(cudaMemcpyAsync(polar, dx + 4 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VXM_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_config& cfg,

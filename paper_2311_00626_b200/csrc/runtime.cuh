@@ -267,6 +267,7 @@ inline void launch_pdl(cudaStream_t s, void (*k)(P...), dim3 g, dim3 b, size_t s
 }
 
 // ---- drivers (implemented in the kernel TUs) ----------------------------------
+void diag_lidar_angles(Context* ctx, const double* xyz, uint64_t n, double* az, double* polar);  // integrate.cu
 // view.cu — candidate blocks; when `alloc` != null the candidates are also
 // looked up / allocated in that layer (fused allocation, integrator.cpp:84-87).
 struct ViewArgs {

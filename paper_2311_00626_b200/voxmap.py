@@ -639,6 +639,18 @@ def integrate_depth_device(layer: TsdfLayer, depth_dev_ptr: int, width: int, hei
     return out
 
 
+def diag_lidar_angles(xyz, ctx: Context | None = None):
+    """(azimuth, polar) of sensor-frame points exactly as the LiDAR integration
+    computes them on the device (lidar.hpp:43-55): atan2(y, x) and
+    acos(z / |p|).  Diagnostics for the parity tests."""
+    ctx = ctx or default_context()
+    p = np.ascontiguousarray(np.asarray(xyz, np.float64).reshape(-1, 3))
+    az = np.empty(len(p), np.float64)
+    po = np.empty(len(p), np.float64)
+    check(lib().vxm_diag_lidar_angles(ctx.h, A.ptr(p), C.c_uint64(len(p)), A.ptr(az), A.ptr(po)))
+    return az, po
+
+
 def blocks_in_view(T_LS, intrinsics, depth, block_size, cfg=None, ctx: Context | None = None):
     """blocks_in_view (sensor/view.hpp:38-48): sorted unique candidate blocks."""
     ctx = ctx or default_context()
