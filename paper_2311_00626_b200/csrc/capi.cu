@@ -275,7 +275,7 @@ vxm_status frame_common(vxm_layer* T, vxm_layer* E, const float* depth, int w, i
       if (E) esdf_launch(E, T, tout, *ecfg, eout);
       T->stage_meta(0);
       if (E) E->stage_meta(1);
-      ctx->sync_status();
+      ctx->sync_status(true);
       T->adopt_meta(0);
       if (E) E->adopt_meta(1);
       if (!integrate_finish(T, va, tout, nb_before)) continue;

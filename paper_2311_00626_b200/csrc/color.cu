@@ -142,7 +142,7 @@ void run_integrate_color(Layer* C, Layer* T, const uint8_t* rgb_host, const View
   if (cand_cap) {
     ctx->prof_begin("k_color_band");
     k_color_band<<<grid_for(ctx, uint64_t(cand_cap) * 32), 256, 0, ctx->stream>>>(
-        ctx->cand_keys.as<uint64_t>(), ctx->d_status, T->hash, static_cast<const float2*>(T->pool[0]),
+        ctx->cand_keys.as<uint64_t>(), ctx->status_w(), T->hash, static_cast<const float2*>(T->pool[0]),
         eps, flags.as<uint8_t>());
     ctx->prof_end();
     ctx->count_launch();
@@ -153,7 +153,7 @@ void run_integrate_color(Layer* C, Layer* T, const uint8_t* rgb_host, const View
   work.ensure(std::max<uint32_t>(cand_cap, 1));
   launch_compact_keys(ctx, ctx->cand_keys.as<uint64_t>(), flags.as<uint8_t>(),
                       &ctx->d_status->n_candidates, cand_cap, work.keys.as<uint64_t>(), work.d_count,
-                      ctx->d_status, "k_compact");
+                      ctx->status_w(), "k_compact");
   work.count_hint = cand_cap;
   work.host_valid = false;
   work.host_pending = false;
@@ -190,7 +190,7 @@ void run_integrate_color(Layer* C, Layer* T, const uint8_t* rgb_host, const View
   changed_out->ctx = ctx;
   changed_out->ensure(std::max<uint32_t>(cand_cap, 1));
   launch_compact_keys(ctx, work.keys.as<uint64_t>(), changed.as<uint8_t>(), work.d_count, cand_cap,
-                      changed_out->keys.as<uint64_t>(), changed_out->d_count, ctx->d_status,
+                      changed_out->keys.as<uint64_t>(), changed_out->d_count, ctx->status_w(),
                       "k_compact");
   changed_out->count_hint = cand_cap;
   changed_out->host_valid = false;

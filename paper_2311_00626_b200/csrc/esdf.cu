@@ -1044,7 +1044,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
     al.n_old_out = s.counts + 2;
     al.stamp_new = E->stamp_new;
     al.call_epoch = epoch;
-    al.status = ctx->d_status;
+    al.status = ctx->status_w();
     const ScanTiles st = ctx->next_scan(ceil_div(n7, 256));
     ctx->prof_begin("k_effective_alloc");
     launch_pdl(ctx->stream, k_effective_alloc, dim3(grid_for(ctx, n7, 4)), dim3(256), 0, 
@@ -1074,7 +1074,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.stamp_mark = E->stamp_mark;
   m.call_epoch = epoch;
   m.flags = s.flags;
-  m.status = ctx->d_status;
+  m.status = ctx->status_w();
   m.site_any = E->site_any;
   m.post = pa;
   ctx->prof_begin("k_mark");
@@ -1194,7 +1194,7 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   for (int i = 0; i < 3; ++i) la.stamp_pair[i] = E->stamp_pair[i];
   la.stamp_r1same = E->stamp_r1same;
   la.lim = limits_for(cfg, E->vs);
-  la.status = E->ctx->d_status;
+  la.status = E->ctx->status_w();
   return la;
 }
 
@@ -1269,7 +1269,7 @@ void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_conf
   E->stage_meta();
   host_trace_mark("launched");
   host_trace_dev(ctx, "kernels");
-  ctx->sync_status();
+  ctx->sync_status(true);
   E->adopt_meta();
   esdf_finish(E, changed_out);
 }
@@ -1471,7 +1471,7 @@ void alloc_key_list(Layer* L, BlockList* keys, int32_t* d_slots_out) {
   al.n_old_out = s.counts + 2;
   al.stamp_new = L->type == VXM_LAYER_ESDF ? L->stamp_new : nullptr;
   al.call_epoch = ++ctx->call_epoch;
-  al.status = ctx->d_status;
+  al.status = ctx->status_w();
   const ScanTiles st = ctx->next_scan(ceil_div(n, 256));
   k_alloc_list<<<grid_for(ctx, n, 4), 256, 0, ctx->stream>>>(al, st);
   ctx->count_launch();

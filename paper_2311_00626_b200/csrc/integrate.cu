@@ -548,7 +548,7 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   IntegrateArgs a{};
   a.cand_keys = ctx->cand_keys.as<uint64_t>();
   a.cand_slots = ctx->cand_slots.as<int32_t>();
-  a.status_ro = ctx->d_status;
+  a.status_ro = ctx->status_w();
   a.pool = L->pool[0];
   a.changed = ctx->cand_flags.as<uint8_t>();
   a.depth = va.depth_dev;
@@ -593,7 +593,7 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   changed_out->ensure(cand_cap);
   launch_compact_keys(ctx, ctx->cand_keys.as<uint64_t>(), ctx->cand_flags.as<uint8_t>(),
                       &ctx->d_status->n_candidates, cand_cap, changed_out->keys.as<uint64_t>(),
-                      changed_out->d_count, ctx->d_status, "k_compact");
+                      changed_out->d_count, ctx->status_w(), "k_compact");
   changed_out->host_valid = false;
   changed_out->host_pending = false;
   // changed blocks are distinct allocated blocks: bounded by the pool too
@@ -637,7 +637,7 @@ void run_integrate(Layer* L, const ViewArgs& va, const vxm_integrator_config& cf
     L->stage_meta();
     host_trace_mark("launched");
     host_trace_dev(ctx, "kernels");
-    ctx->sync_status();
+    ctx->sync_status(true);
     L->adopt_meta();
     if (integrate_finish(L, va, changed_out, nb_before)) return;
   }

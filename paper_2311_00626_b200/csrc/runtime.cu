@@ -87,7 +87,8 @@ bool pdl_enabled() {
 
 void Context::reset_status() {
   status_copies.clear();  // (copies queued by an operation that threw are dropped)
-  VXM_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), stream));
+  if (!status_zero) VXM_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), stream));
+  status_zero = false;  // the call's kernels write it from here on
 }
 struct WordCopies {
   const uint32_t* src[16];
@@ -117,16 +118,19 @@ void Context::flush_copies() {
 // device-to-host DMA (whose small-copy latency is several microseconds).
 constexpr int kStatusWords = int(sizeof(DevStatus) / sizeof(uint32_t));
 static_assert(kStatusWords <= 32, "DevStatus fits one warp");
-__global__ void k_status_out(WordCopies c, const uint32_t* __restrict__ st, uint32_t* __restrict__ host) {
+__global__ void k_status_out(WordCopies c, uint32_t* __restrict__ st, uint32_t* __restrict__ host, int zero) {
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x < c.n) *c.dst[threadIdx.x] = *c.src[threadIdx.x];
   __syncwarp();
-  if (threadIdx.x < kStatusWords) host[threadIdx.x] = st[threadIdx.x];
+  if (threadIdx.x < kStatusWords) {
+    host[threadIdx.x] = st[threadIdx.x];
+    if (zero) st[threadIdx.x] = 0u;
+  }
 }
-void Context::sync_status() {
+void Context::sync_status(bool last) {
   // all but the last batch of queued copies, then the last batch + status out
-  WordCopies last{};
+  WordCopies tail{};
   size_t i = 0;
   while (status_copies.size() - i > 16) {
     WordCopies c{};
@@ -137,15 +141,16 @@ void Context::sync_status() {
     launch_pdl(stream, k_copy_words, dim3(1), dim3(32), 0, c);
     count_launch();
   }
-  for (; i < status_copies.size(); ++i, ++last.n) {
-    last.src[last.n] = status_copies[i].src;
-    last.dst[last.n] = status_copies[i].dst;
+  for (; i < status_copies.size(); ++i, ++tail.n) {
+    tail.src[tail.n] = status_copies[i].src;
+    tail.dst[tail.n] = status_copies[i].dst;
   }
   status_copies.clear();
-  launch_pdl(stream, k_status_out, dim3(1), dim3(32), 0, last, reinterpret_cast<const uint32_t*>(d_status),
-             reinterpret_cast<uint32_t*>(h_status_dev));
+  launch_pdl(stream, k_status_out, dim3(1), dim3(32), 0, tail, reinterpret_cast<uint32_t*>(d_status),
+             reinterpret_cast<uint32_t*>(h_status_dev), int(last));
   count_launch();
   VXM_CUDA(cudaStreamSynchronize(stream));
+  status_zero = last;
   prof_resolve();
 }
 

@@ -110,7 +110,16 @@ struct Context {
   // most `tiles` tiles, clearing the other buffer for the pass after.
   ScanTiles next_scan(uint32_t tiles);
   void count_launch(int n = 1) { launches += uint64_t(n); }
-  void sync_status();  // flush the queued status copies, copy status to the host, sync
+  // flush the queued status copies, copy status to the host, sync; with
+  // `last` (the call's final read) the same kernel zeroes the device status,
+  // so the next call's reset_status needs no memset
+  void sync_status(bool last = false);
+  bool status_zero = false;  // the device status is known to be zero
+  // the device status for a kernel that writes it (no longer known zero)
+  DevStatus* status_w() {
+    status_zero = false;
+    return d_status;
+  }
   // Small device-to-device word copies into the status (counts, metas) are
   // queued and done by ONE kernel before the status read, instead of one
   // cudaMemcpyAsync each (each is a separate stream operation).

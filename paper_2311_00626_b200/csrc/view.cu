@@ -621,7 +621,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
                  dim3(std::max<uint32_t>(1u, std::min<uint32_t>(ceil_div(nt, kRayWarps), uint32_t(per_sm * ctx->sm_count)))),
                  dim3(32 * kRayWarps), 0, 
           a.depth_dev, a.width, a.height, tile, ctx->cam_dirs.as<const double2>(), a.T_LS, sc3, cs,
-          a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
+          a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->status_w());
       ctx->prof_end();
       ctx->count_launch();
     }
@@ -632,7 +632,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
       ctx->prof_begin("k_rays");
       launch_pdl(ctx->stream, k_rays_lidar, dim3(ceil_div(np, 64)), dim3(64), 0, 
           a.depth_dev, a.width, a.height, ctx->lidar_dirs.as<double>(), a.T_LS, cs,
-          a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->d_status);
+          a.cfg.max_integration_distance, a.cfg.truncation, cube, ctx->status_w());
       ctx->prof_end();
       ctx->count_launch();
     }
@@ -658,7 +658,7 @@ void run_view(Context* ctx, const ViewArgs& a, Layer* L, uint32_t* cand_cap_out)
   ctx->prof_begin("k_dilate_alloc");
   launch_pdl(ctx->stream, k_dilate_alloc, dim3(tiles), dim3(256), 0, cube, uint32_t(n_words), al, ctx->rank, ctx->world,
                                                  ctx->slab, ctx->cand_keys.as<uint64_t>(),
-                                                 ctx->cand_slots.as<int32_t>(), ctx->d_status, st,
+                                                 ctx->cand_slots.as<int32_t>(), ctx->status_w(), st,
                                                  other.as<uint32_t>(), uint32_t(other_words));
   ctx->bitmap_clean[bp ^ 1] = other_words;
   ctx->prof_end();
