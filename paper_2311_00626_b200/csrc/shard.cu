@@ -221,24 +221,32 @@ __device__ void shard_border_body(const LowerArgs& a, const ShardRound& sr, cg::
       }
       bool ac = false, bc = false;
       unsigned long long mlo[3] = {0, 0, 0}, mhi[3] = {0, 0, 0};
+      // both face positions of the lane loaded before any store (the four
+      // voxels are distinct): one L2 round trip, not two
+      int co[2][6];
+      EV va[2], vb[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
-        int ax, ay, az, bx, by, bz;
-        if (axis == 0) { ax = 7; ay = i0; az = j0; bx = 0; by = i0; bz = j0; }
-        else if (axis == 1) { ax = i0; ay = 7; az = j0; bx = i0; by = 0; bz = j0; }
-        else { ax = i0; ay = j0; az = 7; bx = i0; by = j0; bz = 0; }
-        const int la = ax + 8 * ay + 64 * az, lb = bx + 8 * by + 64 * bz;
-        EV va = load_voxel(work, lo, la), vb = load_voxel(work, hi, lb);
-        const bool cb = relax(vb, va, dx, dy, dz, lim);     // exchange_pair :158
-        const bool ca = relax(va, vb, -dx, -dy, -dz, lim);  // :159
+        int* c = co[k];  // ax, ay, az, bx, by, bz
+        if (axis == 0) { c[0] = 7; c[1] = i0; c[2] = j0; c[3] = 0; c[4] = i0; c[5] = j0; }
+        else if (axis == 1) { c[0] = i0; c[1] = 7; c[2] = j0; c[3] = i0; c[4] = 0; c[5] = j0; }
+        else { c[0] = i0; c[1] = j0; c[2] = 7; c[3] = i0; c[4] = j0; c[5] = 0; }
+        va[k] = load_voxel(work, lo, c[0] + 8 * c[1] + 64 * c[2]);
+        vb[k] = load_voxel(work, hi, c[3] + 8 * c[4] + 64 * c[5]);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int* c = co[k];
+        const bool cb = relax(vb[k], va[k], dx, dy, dz, lim);     // exchange_pair :158
+        const bool ca = relax(va[k], vb[k], -dx, -dy, -dz, lim);  // :159
         if (cb) {
-          store_voxel(work, hi, lb, vb);
-          line_bits(bx, by, bz, mhi);
+          store_voxel(work, hi, c[3] + 8 * c[4] + 64 * c[5], vb[k]);
+          line_bits(c[3], c[4], c[5], mhi);
         }
         if (ca) {
-          store_voxel(work, lo, la, va);
-          line_bits(ax, ay, az, mlo);
+          store_voxel(work, lo, c[0] + 8 * c[1] + 64 * c[2], va[k]);
+          line_bits(c[0], c[1], c[2], mlo);
         }
         ac |= ca;
         bc |= cb;
