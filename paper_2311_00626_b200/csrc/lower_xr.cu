@@ -484,82 +484,82 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           // side 1 with a dirty lower block: lo's side-0 item has this pair
           const bool dup = side == 1 && __shfl_sync(0xffffffffu, own_dirty, 0);
           if (!dup) {
-          bool dep_chg = false;
-          if (lane < 2) {
-            const int32_t b = lane == 0 ? lo : hi;
-            if (own_dirty) wait_stamp(a.stamp_swept + b, ep, &a.status->watchdog, 10u + axis, b);
-          } else if (wc >= 0) {
-            const uint32_t v = wait_stamp(a.stamp_pair[q] + wc, ep, &a.status->watchdog, 20u + 10u * q + axis, wc);
-            dep_chg = (v & (b_is_hi ? kStampHiChg : kStampLoChg)) != 0u;
-          }
-          const uint32_t chg_mask = __ballot_sync(0xffffffffu, dep_chg);
-          __syncwarp();
-          const unsigned long long tp0 = a.trace ? gtime() : 0ull;
-          bool skip = false;
-          if (r1) {  // no giver on either face: the pair is the identity (k_lower3)
-            constexpr uint32_t lo_lanes = 0x0ccu, hi_lanes = 0x330u;
-            const bool g_lo = site_lo || (chg_mask & lo_lanes) != 0u;
-            const bool g_hi = site_hi || (chg_mask & hi_lanes) != 0u;
-            skip = !g_lo && !g_hi;
-          }
-          if (skip) {
-            if (lane == 0) st_release(a.stamp_pair[axis] + lo, ep);
-          } else {
-            const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
-            // the faces this pair changes, bit = face position lane + 32 k
-            unsigned long long flo = 0, fhi = 0;
-            // both face positions of the lane are loaded before any store (the
-            // four voxels are distinct): one L2 round trip on the hop, not two
-            int la[2], lb[2];
-            EV va[2], vb[2];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
-              int ax, ay, az, bx, by, bz;
-              if (axis == 0) { ax = 7; ay = i0; az = j0; bx = 0; by = i0; bz = j0; }
-              else if (axis == 1) { ax = i0; ay = 7; az = j0; bx = i0; by = 0; bz = j0; }
-              else { ax = i0; ay = j0; az = 7; bx = i0; by = j0; bz = 0; }
-              la[k] = ax + 8 * ay + 64 * az;
-              lb[k] = bx + 8 * by + 64 * bz;
-              va[k] = load_voxel(work, lo, la[k]);
-              vb[k] = load_voxel(work, hi, lb[k]);
+            bool dep_chg = false;
+            if (lane < 2) {
+              const int32_t b = lane == 0 ? lo : hi;
+              if (own_dirty) wait_stamp(a.stamp_swept + b, ep, &a.status->watchdog, 10u + axis, b);
+            } else if (wc >= 0) {
+              const uint32_t v = wait_stamp(a.stamp_pair[q] + wc, ep, &a.status->watchdog, 20u + 10u * q + axis, wc);
+              dep_chg = (v & (b_is_hi ? kStampHiChg : kStampLoChg)) != 0u;
             }
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const bool cb = relax(vb[k], va[k], dx, dy, dz, lim);     // exchange_pair :158
-              const bool ca = relax(va[k], vb[k], -dx, -dy, -dz, lim);  // :159
-              if (cb) store_voxel(work, hi, lb[k], vb[k]);
-              if (ca) store_voxel(work, lo, la[k], va[k]);
-              flo |= (unsigned long long)__ballot_sync(0xffffffffu, ca) << (32 * k);
-              fhi |= (unsigned long long)__ballot_sync(0xffffffffu, cb) << (32 * k);
-            }
-            ++n_pairs;
-            const bool ac = flo != 0ull, bc = fhi != 0ull;
-            const int32_t who[2] = {lo, hi};
-            const bool chg[2] = {ac, bc};
-            if (lane == 0) {  // the changed faces, published by the release below
-              if (ac) a.pair_face[axis][2 * size_t(lo)] = flo;
-              if (bc) a.pair_face[axis][2 * size_t(lo) + 1] = fhi;
-            }
+            const uint32_t chg_mask = __ballot_sync(0xffffffffu, dep_chg);
             __syncwarp();
-            if (lane == 0)
-              st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));
-            if (a.trace && lane == 0) {
-              tr_add(a.trace, R, 12 + axis, gtime() - tp0);
-              tr_add(a.trace, R, 15, 1ull);
+            const unsigned long long tp0 = a.trace ? gtime() : 0ull;
+            bool skip = false;
+            if (r1) {  // no giver on either face: the pair is the identity (k_lower3)
+              constexpr uint32_t lo_lanes = 0x0ccu, hi_lanes = 0x330u;
+              const bool g_lo = site_lo || (chg_mask & lo_lanes) != 0u;
+              const bool g_hi = site_hi || (chg_mask & hi_lanes) != 0u;
+              skip = !g_lo && !g_hi;
             }
-            if (lane == 0) {
-#pragma unroll
-              for (int qq = 0; qq < 2; ++qq) {
-                if (!chg[qq]) continue;
-                if (atomicMax(a.stamp_dirty[np] + who[qq], ep_next) < ep_next) {
-                  const uint32_t slot = atomicAdd(RG(ring, kRingCnt + q4n), 1u);
-                  *(volatile unsigned long long*)(a.dlist[np] + slot) =
-                      (unsigned long long)ep_next << 32 | uint32_t(who[qq]);
+            if (skip) {
+              if (lane == 0) st_release(a.stamp_pair[axis] + lo, ep);
+            } else {
+              const int dx = axis == 0, dy = axis == 1, dz = axis == 2;
+              // the faces this pair changes, bit = face position lane + 32 k
+              unsigned long long flo = 0, fhi = 0;
+              // both face positions of the lane are loaded before any store (the
+              // four voxels are distinct): one L2 round trip on the hop, not two
+              int la[2], lb[2];
+              EV va[2], vb[2];
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                const int f = lane + 32 * k, i0 = f & 7, j0 = f >> 3;
+                int ax, ay, az, bx, by, bz;
+                if (axis == 0) { ax = 7; ay = i0; az = j0; bx = 0; by = i0; bz = j0; }
+                else if (axis == 1) { ax = i0; ay = 7; az = j0; bx = i0; by = 0; bz = j0; }
+                else { ax = i0; ay = j0; az = 7; bx = i0; by = j0; bz = 0; }
+                la[k] = ax + 8 * ay + 64 * az;
+                lb[k] = bx + 8 * by + 64 * bz;
+                va[k] = load_voxel(work, lo, la[k]);
+                vb[k] = load_voxel(work, hi, lb[k]);
+              }
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                const bool cb = relax(vb[k], va[k], dx, dy, dz, lim);     // exchange_pair :158
+                const bool ca = relax(va[k], vb[k], -dx, -dy, -dz, lim);  // :159
+                if (cb) store_voxel(work, hi, lb[k], vb[k]);
+                if (ca) store_voxel(work, lo, la[k], va[k]);
+                flo |= (unsigned long long)__ballot_sync(0xffffffffu, ca) << (32 * k);
+                fhi |= (unsigned long long)__ballot_sync(0xffffffffu, cb) << (32 * k);
+              }
+              ++n_pairs;
+              const bool ac = flo != 0ull, bc = fhi != 0ull;
+              const int32_t who[2] = {lo, hi};
+              const bool chg[2] = {ac, bc};
+              if (lane == 0) {  // the changed faces, published by the release below
+                if (ac) a.pair_face[axis][2 * size_t(lo)] = flo;
+                if (bc) a.pair_face[axis][2 * size_t(lo) + 1] = fhi;
+              }
+              __syncwarp();
+              if (lane == 0)
+                st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));
+              if (a.trace && lane == 0) {
+                tr_add(a.trace, R, 12 + axis, gtime() - tp0);
+                tr_add(a.trace, R, 15, 1ull);
+              }
+              if (lane == 0) {
+  #pragma unroll
+                for (int qq = 0; qq < 2; ++qq) {
+                  if (!chg[qq]) continue;
+                  if (atomicMax(a.stamp_dirty[np] + who[qq], ep_next) < ep_next) {
+                    const uint32_t slot = atomicAdd(RG(ring, kRingCnt + q4n), 1u);
+                    *(volatile unsigned long long*)(a.dlist[np] + slot) =
+                        (unsigned long long)ep_next << 32 | uint32_t(who[qq]);
+                  }
                 }
               }
             }
-          }
           }  // !dup
         }
         if (a.trace && lane == 0) tr_max(a.trace, R, 3 + axis, gtime());
