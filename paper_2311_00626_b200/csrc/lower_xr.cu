@@ -106,10 +106,13 @@ __device__ inline unsigned long long ld_relaxed64(const unsigned long long* p) {
 // MINB resident CTAs per SM: 2 (124 registers, no spills) for latency-bound
 // maps, 3 (80 registers, small spills, +50 % sweep groups) for throughput-bound
 // large maps — measured: C2 -7 % with 3, C4 / C5 +9 % / +11 % with 3.
-template <int MINB>
+template <int MINB, bool TRACE>
 __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
   pdl_wait();  // see launch_pdl
   pdl_trigger();
+  // VXM_TRACE_XR instrumentation only in the TRACE instantiations (the
+  // production kernels carry none of it)
+  unsigned long long* const trace = TRACE ? a.trace : nullptr;
   cg::grid_group grid = cg::this_grid();
   __shared__ GroupSmem s_grp[kL3Groups];
   const int g = threadIdx.x >> 6, t = threadIdx.x & 63, lane = threadIdx.x & 31;
@@ -207,10 +210,10 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
     }
   }
   grid.sync();
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long tm;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
-    a.trace[0] = tm;
+    trace[0] = tm;
   }
   uint32_t n_pairs = 0, n_cmp = 0, rounds = 0, r1_mine = 0;
   if (lower && n_blocks > 0) {
@@ -235,22 +238,22 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           RawBlock rb;
           bool any_site, fast;
           unsigned long long tm0 = 0, tm1 = 0;
-          if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm0));
+          if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm0));
           load_raw3(rb, pcur + size_t(s) * 1536, t, bar, lim, true, &any_site, &fast);
           if (!any_site) {
             raw_store(rb, work + size_t(s) * 1536, t);
           } else {
             stage_block3(G, rb, t, bar, lim, fast);
             int passes = 0;
-            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm1));
+            if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm1));
             sweep_block3(G, t, bar, lim, &passes);
-            if (a.trace && t == 0) {  // VXM_TRACE_XR: round-1 sweep statistics
+            if (trace && t == 0) {  // VXM_TRACE_XR: round-1 sweep statistics
               unsigned long long tm2;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm2));
-              atomicAdd(a.trace + 54, tm1 - tm0);
-              atomicAdd(a.trace + 55, tm2 - tm1);
-              atomicAdd(a.trace + 56, (unsigned long long)passes);
-              atomicAdd(a.trace + 57, 1ull);
+              atomicAdd(trace + 54, tm1 - tm0);
+              atomicAdd(trace + 55, tm2 - tm1);
+              atomicAdd(trace + 56, (unsigned long long)passes);
+              atomicAdd(trace + 57, 1ull);
             }
             store_block3(G, work + size_t(s) * 1536, t);
           }
@@ -290,10 +293,10 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         if (lane == 0 && r1_mine) {  // (per warp)
           atom_add_release(a.r1 + 4, r1_mine);
         }
-        if (a.trace && lane == 0) {  // VXM_TRACE_XR: end of the round-1 sweeps / copies
+        if (trace && lane == 0) {  // VXM_TRACE_XR: end of the round-1 sweeps / copies
           unsigned long long tm;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
-          atomicMax(a.trace + 60, tm);
+          atomicMax(trace + 60, tm);
         }
       } else {
         const unsigned long long* dl = a.dlist[cp];
@@ -328,9 +331,9 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           const int32_t s = int32_t(G.bcast);
           if (s < 0) break;
           unsigned long long tsw0 = 0;
-          if (a.trace && t == 0) {
+          if (trace && t == 0) {
             tsw0 = gtime();
-            tr_min(a.trace, R, 0, tsw0);
+            tr_min(trace, R, 0, tsw0);
           }
           // the block's round R - 1 pairs (the reference's only writers of it since
           // its last sweep) must be complete: lanes 0-5 of the group's first warp
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           }
           group_sync(bar);  // every wait done before the voxels are read
           unsigned long long tsa = 0, tsb = 0, tsc = 0;
-          if (a.trace && t == 0) tsa = gtime();
+          if (trace && t == 0) tsa = gtime();
           RawBlock rb;
           raw_load(rb, work + size_t(s) * 1536, t);
           if (t < 32) {
@@ -374,21 +377,21 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           bool any_site, fast;
           raw_check3(rb, t, bar, lim, false, &any_site, &fast);  // (its barriers publish the masks)
           stage_block3(G, rb, t, bar, lim, fast);
-          if (a.trace && t == 0) tsb = gtime();
+          if (trace && t == 0) tsb = gtime();
           const bool sw_chg = sweep_block3(G, t, bar, lim);
-          if (a.trace && t == 0) tsc = gtime();
+          if (trace && t == 0) tsc = gtime();
           if (sw_chg) store_block3(G, work + size_t(s) * 1536, t);
           group_sync(bar);  // the group's stores before the release of its sweep stamp
           if (t == 0) st_release(a.stamp_swept + s, ep);
-          if (a.trace && t == 0) {
+          if (trace && t == 0) {
             const unsigned long long tsw1 = gtime();
-            tr_max(a.trace, R, 1, tsw1);
-            tr_add(a.trace, R, 6, tsw1 - tsw0);
-            tr_add(a.trace, R, 7, 1ull);
-            tr_add(a.trace, R, 8, tsa - tsw0);
-            tr_add(a.trace, R, 9, tsb - tsa);
-            tr_add(a.trace, R, 10, tsc - tsb);
-            tr_add(a.trace, R, 11, tsw1 - tsc);
+            tr_max(trace, R, 1, tsw1);
+            tr_add(trace, R, 6, tsw1 - tsw0);
+            tr_add(trace, R, 7, 1ull);
+            tr_add(trace, R, 8, tsa - tsw0);
+            tr_add(trace, R, 9, tsb - tsa);
+            tr_add(trace, R, 10, tsc - tsb);
+            tr_add(trace, R, 11, tsw1 - tsc);
           }
         }
       }
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         if (lane == 0) wi = atomicAdd(RG(ring, kRingPc + q4), 1u);
         wi = __shfl_sync(0xffffffffu, wi, 0);
         if (wi >= n_items) break;
-        if (a.trace && lane == 0 && wi == 0) tr_min(a.trace, R, 2, gtime());
+        if (trace && lane == 0 && wi == 0) tr_min(trace, R, 2, gtime());
         int axis;
         uint32_t rest;
         if (r1l) {
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             }
             const uint32_t chg_mask = __ballot_sync(0xffffffffu, dep_chg);
             __syncwarp();
-            const unsigned long long tp0 = a.trace ? gtime() : 0ull;
+            const unsigned long long tp0 = trace ? gtime() : 0ull;
             bool skip = false;
             if (r1) {  // no giver on either face: the pair is the identity (k_lower3)
               constexpr uint32_t lo_lanes = 0x0ccu, hi_lanes = 0x330u;
@@ -544,9 +547,9 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
               __syncwarp();
               if (lane == 0)
                 st_release(a.stamp_pair[axis] + lo, ep | (ac ? kStampLoChg : 0u) | (bc ? kStampHiChg : 0u));
-              if (a.trace && lane == 0) {
-                tr_add(a.trace, R, 12 + axis, gtime() - tp0);
-                tr_add(a.trace, R, 15, 1ull);
+              if (trace && lane == 0) {
+                tr_add(trace, R, 12 + axis, gtime() - tp0);
+                tr_add(trace, R, 15, 1ull);
               }
               if (lane == 0) {
   #pragma unroll
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             }
           }  // !dup
         }
-        if (a.trace && lane == 0) tr_max(a.trace, R, 3 + axis, gtime());
+        if (trace && lane == 0) tr_max(trace, R, 3 + axis, gtime());
         ++my_done;
       }
       // round accounting, one atomic per warp: the warp whose items complete
@@ -585,11 +588,11 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           *RG(ring, kRingCnt + q4nn) = 0u;
           *RG(ring, kRingSwc + q4nn) = *RG(ring, kRingPc + q4nn) = *RG(ring, kRingDone + q4nn) = 0u;
           if (R > 1) a.status->sum_dirty += n_dirty;
-          if (a.trace && R < 54) {  // VXM_TRACE_XR: round completion times
+          if (trace && R < 54) {  // VXM_TRACE_XR: round completion times
             unsigned long long tm;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
-            a.trace[R] = tm;
-            a.trace[64 + R] = n_dirty;
+            trace[R] = tm;
+            trace[64 + R] = n_dirty;
           }
           st_release(RG(ring, kRingLast), R);  // (orders the zeroing above too)
         }
@@ -599,10 +602,10 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
     }
   }
   grid.sync();
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long tm;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
-    a.trace[62] = tm;
+    trace[62] = tm;
   }
   // ---- changed set of update_esdf (esdf/integrator.cpp:403-411) ------------------
   // Each CTA compares a contiguous chunk of the sorted order (one warp per
@@ -683,12 +686,12 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
   }
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (a.trace) {
+    if (trace) {
       unsigned long long tm;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
-      a.trace[63] = tm;
-      a.trace[58] = a.r1[0];  // round-1 blocks with sites (swept) / without (copied)
-      a.trace[59] = a.r1[1];
+      trace[63] = tm;
+      trace[58] = a.r1[0];  // round-1 blocks with sites (swept) / without (copied)
+      trace[59] = a.r1[1];
     }
     for (int q = 0; q < 8; ++q) a.r1[q] = 0u;  // zero for the next launch
     a.status->rounds = rounds;
@@ -719,7 +722,8 @@ bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
     return e ? uint32_t(std::strtoul(e, nullptr, 10)) : kR1CompactMin;
   }();
   la.r1_compact_min = r1_compact_min;
-  void (*kern)(LowerArgs) = wide ? k_lower_xr<3> : k_lower_xr<2>;
+  void (*kern)(LowerArgs) = trace ? (wide ? k_lower_xr<3, true> : k_lower_xr<2, true>)
+                                  : (wide ? k_lower_xr<3, false> : k_lower_xr<2, false>);
   const int grid = ctx->resident_per_sm((const void*)kern, kL3Threads, 0, 4) * ctx->sm_count;
   ctx->lower_cta.ensure(sizeof(uint32_t) * grid);  // per-CTA counts of the in-kernel compaction
   la.cta_cnt = ctx->lower_cta.as<uint32_t>();
