@@ -149,7 +149,9 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
   // (x, y) neighbourhood (bit 1); such items are released without any wait.
   // (only on large maps: on a small one — C2, 9k blocks — the extra pass and
   // grid barrier cost more than the claims they save)
-  const bool r1c = n_blocks > a.r1_compact_min;
+  // (the 2-CTA instantiation, for maps of at most kXrWideBlocks, never
+  // plans: compiled out of it)
+  const bool r1c = MINB == 3 && n_blocks > a.r1_compact_min;
   if (lower && r1c) {
     auto sa = [&](int32_t c) -> uint32_t { return c >= 0 ? uint32_t(a.site_any[c] != 0) : 0u; };
     auto near_x = [&](int32_t c) -> uint32_t {

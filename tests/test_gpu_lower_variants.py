@@ -4,7 +4,8 @@ its 2- and 3-CTA-per-SM instantiations, VXM_XR_WIDE), the
 barrier-per-round dataflow kernel (k_lower3, VXM_LOWER_XROUND=0/1) and its phased form
 (grid barrier before every border axis), plain launches instead of
 programmatic dependent launch (VXM_NO_PDL), and the cross-round kernel's
-precomputed round-1 pair lists forced on small maps (VXM_XR_R1_COMPACT_MIN=0).  The selection is process-wide, so
+precomputed round-1 pair lists forced on small maps (VXM_XR_R1_COMPACT_MIN=0; they
+exist only in the 3-CTA instantiation, so VXM_XR_WIDE=2 with it).  The selection is process-wide, so
 each variant runs tests/lower_variant_check.py in its own process."""
 import os
 import subprocess
