@@ -627,6 +627,7 @@ vxm_status vxm_layer_write_blocks(vxm_layer* L, const vxm_grid_index* keys, uint
     dslots.ensure(sizeof(int32_t) * m);
     ctx->reset_status();
     L->subset_valid = false;  // blocks not produced by mark_sites
+    L->esdf_user_data = true;  // (any layer type; read for ESDF layers)
     alloc_key_list(L, &list, dslots.as<int32_t>());
     const uint32_t bb = uint32_t(L->block_bytes());
     std::vector<unsigned char> packed(size_t(bb) * m);

@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 
 #include "runtime.cuh"
@@ -990,6 +991,15 @@ Limits limits_for(const vxm_esdf_config& cfg, double vs) {
   return l;
 }
 
+// The limits of a call on layer E, noting the largest max_sq the layer's data
+// may have been saturated with (k_lower_xr's compact-format rule).
+static Limits esdf_limits(Layer* E, const vxm_esdf_config& cfg) {
+  const Limits l = limits_for(cfg, E->vs);
+  const int m = l.max_sq < 0 ? INT32_MAX : l.max_sq;
+  if (m > E->esdf_max_sq_seen) E->esdf_max_sq_seen = m;
+  return l;
+}
+
 uint32_t grid_for(Context* ctx, uint64_t n, int per_sm) {
   return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(std::max<uint64_t>(n, 1), 256),
                                                            uint64_t(ctx->sm_count) * per_sm)));
@@ -1070,7 +1080,7 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.pools[1] = static_cast<uint32_t*>(E->pool[1]);
   m.meta = E->meta;
   m.site_threshold = float(cfg.site_threshold);
-  m.lim = limits_for(cfg, E->vs);
+  m.lim = esdf_limits(E, cfg);
   m.stamp_mark = E->stamp_mark;
   m.call_epoch = epoch;
   m.flags = s.flags;
@@ -1193,8 +1203,9 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.dataflow = dataflow;
   for (int i = 0; i < 3; ++i) la.stamp_pair[i] = E->stamp_pair[i];
   la.stamp_r1same = E->stamp_r1same;
-  la.lim = limits_for(cfg, E->vs);
+  la.lim = esdf_limits(E, cfg);
   la.status = E->ctx->status_w();
+  la.fast_only = !E->esdf_user_data && E->esdf_max_sq_seen <= kFastOff * kFastOff;
   return la;
 }
 
@@ -1375,7 +1386,7 @@ void run_clear_invalid(Layer* E, const vxm_esdf_config& cfg, EsdfState* st,
   a.radius = int(std::ceil(cfg.max_distance / E->vs / kVPS));
   a.hash = E->hash;
   a.pool = static_cast<uint32_t*>(E->pool[E->cur_host]);
-  a.lim = limits_for(cfg, E->vs);
+  a.lim = esdf_limits(E, cfg);
   a.flags = dflags.as<uint8_t>();
   if (n_all) {
     k_clear<<<std::max<uint32_t>(1, std::min<uint32_t>(n_all, ctx->sm_count * 8)), 256, 0,

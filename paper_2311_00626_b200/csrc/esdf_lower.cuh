@@ -274,10 +274,14 @@ __device__ inline uint32_t sweep_line_fast(GroupSmem& g, int q) {
   return ch;
 }
 
-template <int AXIS>
+// FASTONLY: every staged block is in the compact format (the caller
+// guarantees it; see k_lower_xr), so the general format's code is not
+// compiled in.
+template <int AXIS, bool FASTONLY = false>
 __device__ inline uint32_t sweep_phase3(GroupSmem& g, int t, int bar, int p, const Limits& lim) {
   uint32_t ch = 0;
-  if ((g.mask[AXIS][p] >> t) & 1ull) ch = g.fast ? sweep_line_fast<AXIS>(g, t) : sweep_line3<AXIS>(g, t, lim);
+  if ((g.mask[AXIS][p] >> t) & 1ull)
+    ch = (FASTONLY || g.fast) ? sweep_line_fast<AXIS>(g, t) : sweep_line3<AXIS>(g, t, lim);
   // Line bits for the phases that follow, OR-reduced over the warp first and
   // then merged with 32-bit shared atomics (a 64-bit shared atomicOr is a CAS
   // loop, which serialises under this contention).
@@ -313,19 +317,20 @@ __device__ inline uint32_t sweep_phase3(GroupSmem& g, int t, int bar, int p, con
 
 // sweep_block (esdf/integrator.cpp:96-139) for one group; masks[.][0] hold the
 // initially dirty lines.  Returns whether any voxel changed.
+template <bool FASTONLY = false>
 __device__ inline bool sweep_block3(GroupSmem& g, int t, int bar, const Limits& lim,
                                     int* n_passes = nullptr) {
   bool block_changed = false;
   for (int pass = 0;; ++pass) {
     if (n_passes) *n_passes = pass + 1;
     const int p = pass & 1;
-    uint32_t c = sweep_phase3<0>(g, t, bar, p, lim);
+    uint32_t c = sweep_phase3<0, FASTONLY>(g, t, bar, p, lim);
     group_sync(bar);
     if (t == 0) g.mask[0][p] = 0ull;
-    c |= sweep_phase3<1>(g, t, bar, p, lim);
+    c |= sweep_phase3<1, FASTONLY>(g, t, bar, p, lim);
     group_sync(bar);
     if (t == 0) g.mask[1][p] = 0ull;
-    c |= sweep_phase3<2>(g, t, bar, p, lim);
+    c |= sweep_phase3<2, FASTONLY>(g, t, bar, p, lim);
     const bool pass_changed = group_sync_or(bar, c != 0);
     if (t == 0) g.mask[2][p] = 0ull;
     block_changed |= pass_changed;
@@ -399,8 +404,10 @@ __device__ inline void load_raw3(RawBlock& r, const uint32_t* __restrict__ src, 
 }
 
 // Registers -> working format in shared memory (compact or general).
+template <bool FASTONLY = false>
 __device__ inline void stage_block3(GroupSmem& g, const RawBlock& r, int t, int bar, const Limits& lim,
                                     bool fast) {
+  if (FASTONLY) fast = true;
 #pragma unroll
   for (int v = 0; v < 8; ++v) {
     const int si = swz_lin(raw_lin(t, v));
@@ -431,9 +438,10 @@ __device__ inline void stage_block3(GroupSmem& g, const RawBlock& r, int t, int 
 }
 
 // Working format in shared memory -> global block (reference layout).
+template <bool FASTONLY = false>
 __device__ inline void store_block3(const GroupSmem& g, uint32_t* __restrict__ dst, int t) {
   RawBlock r;
-  const bool fast = g.fast;
+  const bool fast = FASTONLY || g.fast;
 #pragma unroll
   for (int v = 0; v < 8; ++v) {
     const int si = swz_lin(raw_lin(t, v));
@@ -463,7 +471,7 @@ struct LowerArgs {
   uint32_t* pool[2];
   LayerMeta* meta;
   const int32_t* nbr;
-  const int32_t* nbr27;  // [cap][27] 3x3x3 neighbourhood slots (k_lower_xr)
+  int fast_only;         // k_lower_xr: every block is compact-format eligible (see launch_lower_xr)
   uint32_t* stamp_dirty[2];
   uint32_t* stamp_lchg;
   int32_t* list[2];

@@ -101,12 +101,19 @@ __device__ inline unsigned long long ld_relaxed64(const unsigned long long* p) {
   return v;
 }
 
+// A FASTONLY kernel met a block outside the compact format: the host's
+// eligibility rule (launch_lower_xr) was wrong — reported as an internal
+// error (VXM_ERR_INTERNAL via the watchdog word), never a silent result.
+__device__ inline void format_violation(const LowerArgs& a, int t) {
+  if (t == 0 && atomicExch(&a.status->watchdog, 1u) == 0u) a.status->pad3[0] = 50u;
+}
+
 }  // namespace
 
 // MINB resident CTAs per SM: 2 (124 registers, no spills) for latency-bound
 // maps, 3 (80 registers, small spills, +50 % sweep groups) for throughput-bound
 // large maps — measured: C2 -7 % with 3, C4 / C5 +9 % / +11 % with 3.
-template <int MINB, bool TRACE>
+template <int MINB, bool TRACE, bool FASTONLY>
 __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
   pdl_wait();  // see launch_pdl
   pdl_trigger();
@@ -242,13 +249,14 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           unsigned long long tm0 = 0, tm1 = 0;
           if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm0));
           load_raw3(rb, pcur + size_t(s) * 1536, t, bar, lim, true, &any_site, &fast);
+          if (FASTONLY && !fast) format_violation(a, t);
           if (!any_site) {
             raw_store(rb, work + size_t(s) * 1536, t);
           } else {
-            stage_block3(G, rb, t, bar, lim, fast);
+            stage_block3<FASTONLY>(G, rb, t, bar, lim, fast);
             int passes = 0;
             if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm1));
-            sweep_block3(G, t, bar, lim, &passes);
+            sweep_block3<FASTONLY>(G, t, bar, lim, &passes);
             if (trace && t == 0) {  // VXM_TRACE_XR: round-1 sweep statistics
               unsigned long long tm2;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm2));
@@ -257,7 +265,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
               atomicAdd(trace + 56, (unsigned long long)passes);
               atomicAdd(trace + 57, 1ull);
             }
-            store_block3(G, work + size_t(s) * 1536, t);
+            store_block3<FASTONLY>(G, work + size_t(s) * 1536, t);
           }
           group_sync(bar);
           if (t == 0) {
@@ -378,11 +386,12 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           }
           bool any_site, fast;
           raw_check3(rb, t, bar, lim, false, &any_site, &fast);  // (its barriers publish the masks)
-          stage_block3(G, rb, t, bar, lim, fast);
+          if (FASTONLY && !fast) format_violation(a, t);
+          stage_block3<FASTONLY>(G, rb, t, bar, lim, fast);
           if (trace && t == 0) tsb = gtime();
-          const bool sw_chg = sweep_block3(G, t, bar, lim);
+          const bool sw_chg = sweep_block3<FASTONLY>(G, t, bar, lim);
           if (trace && t == 0) tsc = gtime();
-          if (sw_chg) store_block3(G, work + size_t(s) * 1536, t);
+          if (sw_chg) store_block3<FASTONLY>(G, work + size_t(s) * 1536, t);
           group_sync(bar);  // the group's stores before the release of its sweep stamp
           if (t == 0) st_release(a.stamp_swept + s, ep);
           if (trace && t == 0) {
@@ -724,8 +733,17 @@ bool launch_lower_xr(Context* ctx, LowerArgs& la, uint32_t n_blocks_hint) {
     return e ? uint32_t(std::strtoul(e, nullptr, 10)) : kR1CompactMin;
   }();
   la.r1_compact_min = r1_compact_min;
-  void (*kern)(LowerArgs) = trace ? (wide ? k_lower_xr<3, true> : k_lower_xr<2, true>)
-                                  : (wide ? k_lower_xr<3, false> : k_lower_xr<2, false>);
+  // Every block of a layer that only the library has written (mark_sites
+  // and the lowering itself) is in the compact sweep format as long as no
+  // configuration has had max_sq > kFastOff^2 (parents beyond +-kFastOff,
+  // saturation values >= 2^29): then the kernel without the general format
+  // runs (C2 k_lower -6 %, C5 -15 %); user-written ESDF data keeps the general
+  // kernel for the layer's lifetime.  (VXM_XR_GENERAL=1 forces the general one.)
+  static const bool force_general = std::getenv("VXM_XR_GENERAL") != nullptr;
+  const bool fast = la.fast_only && !force_general && !trace;
+  void (*kern)(LowerArgs) = trace ? (wide ? k_lower_xr<3, true, false> : k_lower_xr<2, true, false>)
+                            : fast ? (wide ? k_lower_xr<3, false, true> : k_lower_xr<2, false, true>)
+                                   : (wide ? k_lower_xr<3, false, false> : k_lower_xr<2, false, false>);
   const int grid = ctx->resident_per_sm((const void*)kern, kL3Threads, 0, 4) * ctx->sm_count;
   ctx->lower_cta.ensure(sizeof(uint32_t) * grid);  // per-CTA counts of the in-kernel compaction
   la.cta_cnt = ctx->lower_cta.as<uint32_t>();

@@ -188,6 +188,11 @@ struct Layer {
   // clears subset_valid for good (an empty layer starts over).
   uint64_t subset_uid = 0;
   bool subset_valid = true;
+  // ESDF: user-written voxel data (vxm_layer_write_blocks) at any time, and the
+  // largest max_sq any update used — together they decide whether every block
+  // is in the lowering's compact sweep format (k_lower_xr FASTONLY)
+  bool esdf_user_data = false;
+  int esdf_max_sq_seen = 0;
   void note_esdf_source(const Layer* src) {
     if (num_blocks == 0) {
       subset_uid = src->uid;
