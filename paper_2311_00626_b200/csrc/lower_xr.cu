@@ -17,6 +17,7 @@
 // cycle.  The result is bit-identical to the barrier schedule.
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "esdf_lower.cuh"
 
@@ -225,11 +226,14 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
     trace[0] = tm;
   }
   uint32_t n_pairs = 0, n_cmp = 0, rounds = 0, r1_mine = 0;
-  if (lower && n_blocks > 0) {
-    for (uint32_t R = 1;; ++R) {
+  // One round of the loop; round 1 and the later rounds are separate
+  // instantiations (r1 a compile-time constant in each), so the steady-state
+  // loop carries none of round 1's code.  Returns false once the round's
+  // dirty list is empty.
+  auto round_body = [&](const uint32_t R, auto r1_tag) -> bool {
+      constexpr bool r1 = decltype(r1_tag)::value;
       const uint32_t ep = base_epoch + R, ep_next = ep + 1;
       const int cp = int(R & 1u), np = cp ^ 1;
-      const bool r1 = R == 1;
       const int q4 = int(R & 3u), q4n = int((R + 1u) & 3u);
       // ---- sweeps of round R (esdf/integrator.cpp:509-513) -------------------
       if (r1) {
@@ -418,7 +422,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
       }
       if (!r1) (void)ld_acquire(last_rep);  // the round's list and counts are visible
       const uint32_t n_dirty = r1 ? n_blocks : *((volatile uint32_t*)(RG(ring, kRingCnt + q4)));
-      if (n_dirty == 0) break;  // while (!dirty.empty()) — esdf/integrator.cpp:506
+      if (n_dirty == 0) return false;  // while (!dirty.empty()) — esdf/integrator.cpp:506
       rounds = R;
       const unsigned long long* dl = a.dlist[cp];
       auto dirty_at = [&](uint32_t i) -> int32_t { return r1 ? int32_t(i) : int32_t(uint32_t(__ldcg(dl + i))); };
@@ -610,8 +614,11 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
       }
       // the next round's sweeps re-form the groups (both warps)
       group_sync(bar);
+      return true;
+  };
+  if (lower && n_blocks > 0 && round_body(1u, std::true_type{}))
+    for (uint32_t R = 2; round_body(R, std::false_type{}); ++R) {
     }
-  }
   grid.sync();
   if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long tm;
