@@ -447,13 +447,17 @@ def run_c5(args, rank, world, device):
         if n:
             kernels[name] = {"ms_total": ms, "launches": n, "ms_per_launch": ms / n}
     ctx.set_profiling(False)
-    # e2e: the public host API (host key list in, host changed list out)
+    # e2e: the public host API (host key list in, host changed list out); the
+    # key list is staged in page-locked memory (vxm_host_alloc, as C2's frames),
+    # one untimed call warms the host path's staging buffers
+    hkeys = vx.pinned_like(np.ascontiguousarray(keys, np.int32))
+    vx.update_esdf(E, Ts[(W + 2 * K + 1) % 2], hkeys.array, ecfg)
     e2e_t, h2d, d2h = [], 0, 0
     for i in range(W + 2 * K, W + 3 * K):
         flush.zero_()
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
-        ch = vx.update_esdf(E, Ts[i % 2], keys, ecfg)
+        ch = vx.update_esdf(E, Ts[i % 2], hkeys.array, ecfg)
         e2e_t.append(time.perf_counter() - t0)
         h2d += keys.nbytes
         d2h += ch.nbytes

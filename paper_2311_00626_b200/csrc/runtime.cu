@@ -118,15 +118,30 @@ void Context::flush_copies() {
 // device-to-host DMA (whose small-copy latency is several microseconds).
 constexpr int kStatusWords = int(sizeof(DevStatus) / sizeof(uint32_t));
 static_assert(kStatusWords <= 32, "DevStatus fits one warp");
-__global__ void k_status_out(WordCopies c, uint32_t* __restrict__ st, uint32_t* __restrict__ host, int zero) {
+// k_emit_host's loop (the changed list unpacked into mapped pinned memory)
+__device__ inline void emit_host(const Context::EmitHost& e) {
+  const uint32_t n = min(*e.n_ptr, e.cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *e.out_n = n;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t k = e.keys[i];
+    e.out[i] = vxm_grid_index{key_x(k), key_y(k), key_z(k)};
+  }
+}
+// CTA 0's first warp: the queued word copies, then the status into the host
+// copy; every CTA: the deferred unpack of a host-bound list (if any)
+__global__ void k_status_out(WordCopies c, uint32_t* __restrict__ st, uint32_t* __restrict__ host, int zero,
+                             Context::EmitHost e) {
   pdl_wait();
   pdl_trigger();
-  if (threadIdx.x < c.n) *c.dst[threadIdx.x] = *c.src[threadIdx.x];
-  __syncwarp();
-  if (threadIdx.x < kStatusWords) {
-    host[threadIdx.x] = st[threadIdx.x];
-    if (zero) st[threadIdx.x] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    if (threadIdx.x < c.n) *c.dst[threadIdx.x] = *c.src[threadIdx.x];
+    __syncwarp();
+    if (threadIdx.x < kStatusWords) {
+      host[threadIdx.x] = st[threadIdx.x];
+      if (zero) st[threadIdx.x] = 0u;
+    }
   }
+  if (e.grid) emit_host(e);
 }
 void Context::sync_status(bool last) {
   // all but the last batch of queued copies, then the last batch + status out
@@ -146,8 +161,10 @@ void Context::sync_status(bool last) {
     tail.dst[tail.n] = status_copies[i].dst;
   }
   status_copies.clear();
-  launch_pdl(stream, k_status_out, dim3(1), dim3(32), 0, tail, reinterpret_cast<uint32_t*>(d_status),
-             reinterpret_cast<uint32_t*>(h_status_dev), int(last));
+  const EmitHost e = emit;
+  emit = EmitHost{};
+  launch_pdl(stream, k_status_out, dim3(std::max<uint32_t>(e.grid, 1)), dim3(e.grid ? 256 : 32), 0, tail,
+             reinterpret_cast<uint32_t*>(d_status), reinterpret_cast<uint32_t*>(h_status_dev), int(last), e);
   count_launch();
   VXM_CUDA(cudaStreamSynchronize(stream));
   status_zero = last;
@@ -347,6 +364,7 @@ Layer::~Layer() {
 
 // ---- BlockList -----------------------------------------------------------------
 void BlockList::ensure(uint32_t n) {
+  if (ctx && ctx->emit.list == this) ctx->flush_emit();  // (its keys may move)
   if (!d_count) {
     VXM_CUDA(cudaMalloc(&d_count, sizeof(uint32_t)));
     VXM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), ctx->stream));
@@ -358,19 +376,23 @@ void BlockList::ensure(uint32_t n) {
   }
 }
 
-__global__ void k_emit_host(const uint64_t* __restrict__ keys, const uint32_t* n_ptr,
-                            vxm_grid_index* out, uint32_t* out_n, uint32_t cap) {
+__global__ void k_emit_host(Context::EmitHost e) {
   pdl_wait();
   pdl_trigger();
-  const uint32_t n = min(*n_ptr, cap);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *out_n = n;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    out[i] = vxm_grid_index{key_x(k), key_y(k), key_z(k)};
-  }
+  emit_host(e);
+}
+
+void Context::flush_emit() {
+  if (!emit.grid) return;
+  const EmitHost e = emit;
+  emit = EmitHost{};
+  launch_pdl(stream, k_emit_host, dim3(e.grid), dim3(256), 0, e);
+  count_launch();
+  check_launch(this, "k_emit_host");
 }
 
 void BlockList::enqueue_host() {
+  ctx->flush_emit();  // one deferred unpack at a time (and before mapped may move)
   const uint32_t need = std::max<uint32_t>(count_hint, 1);
   if (need > mapped_cap) {
     if (mapped) VXM_CUDA(cudaFreeHost(mapped));
@@ -381,17 +403,15 @@ void BlockList::enqueue_host() {
   if (!mapped_count)
     VXM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mapped_count), sizeof(uint32_t), cudaHostAllocMapped));
   const uint32_t grid = std::min<uint32_t>(ceil_div(need, 256), uint32_t(ctx->sm_count));
-  launch_pdl(ctx->stream, k_emit_host, dim3(std::max<uint32_t>(grid, 1)), dim3(256), 0,
-             keys.as<const uint64_t>(), static_cast<const uint32_t*>(d_count), mapped, mapped_count,
-             mapped_cap);
-  ctx->count_launch();
-  check_launch(ctx, "k_emit_host");
+  ctx->emit = Context::EmitHost{keys.as<const uint64_t>(), static_cast<const uint32_t*>(d_count), mapped,
+                                mapped_count, mapped_cap, std::max<uint32_t>(grid, 1), this};
   host_pending = true;
 }
 
 const std::vector<vxm_grid_index>& BlockList::fetch() {
   if (host_valid) return host;
-  if (host_pending) {  // unpacked by k_emit_host into mapped memory
+  if (host_pending) {  // unpacked by k_emit_host / k_status_out into mapped memory
+    if (ctx->emit.list == this) ctx->flush_emit();
     VXM_CUDA(cudaStreamSynchronize(ctx->stream));
     const uint32_t n = *mapped_count;
     host.assign(mapped, mapped + n);
@@ -452,6 +472,7 @@ void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
 
 BlockList::~BlockList() {
   if (ctx && ctx->last_host_out == this) ctx->last_host_out = nullptr;
+  if (ctx && ctx->emit.list == this) ctx->emit = Context::EmitHost{};  // (nobody reads it)
   if (ctx && (staging || mapped)) cudaStreamSynchronize(ctx->stream);
   if (staging) cudaFreeHost(staging);
   if (mapped) cudaFreeHost(mapped);

@@ -128,6 +128,19 @@ struct Context {
     uint32_t* dst;
   };
   std::vector<WordCopy> status_copies;
+  // A host-bound list's unpack (BlockList::enqueue_host), deferred into the
+  // status-out kernel of the next sync_status: one launch fewer per host call.
+  struct EmitHost {
+    const uint64_t* keys = nullptr;
+    const uint32_t* n_ptr = nullptr;
+    vxm_grid_index* out = nullptr;
+    uint32_t* out_n = nullptr;
+    uint32_t cap = 0;
+    uint32_t grid = 0;  // 0: none pending
+    const void* list = nullptr;
+  };
+  EmitHost emit;
+  void flush_emit();  // launches a pending unpack on its own
   void queue_copy(const uint32_t* src, uint32_t* dst, int n_words = 1) {
     for (int i = 0; i < n_words; ++i) status_copies.push_back({src + i, dst + i});
   }
