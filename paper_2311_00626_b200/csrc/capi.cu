@@ -962,7 +962,7 @@ vxm_status vxm_update_esdf(vxm_layer* E, vxm_layer* T, const vxm_grid_index* upd
         (n == 0 || std::memcmp(last->host.data(), updated, sizeof(vxm_grid_index) * n) == 0)) {
       list = static_cast<vxm_blocklist*>(last);  // the integrate's device keys, identical content
     } else {
-      list->assign_host(updated, n);
+      list->assign_host(updated, n, false);  // (an input only: no host copy)
     }
     tr.mark("assigned");
     tr.dev_mark(ctx->stream, "h2d");

@@ -408,13 +408,27 @@ void BlockList::enqueue_host() {
   host_pending = true;
 }
 
+// dst = src[0, n): large lists copied by the host cores in parallel
+static void host_copy(std::vector<vxm_grid_index>& dst, const vxm_grid_index* src, uint64_t n) {
+  dst.resize(n);
+  const int64_t nn = int64_t(n);
+  if (nn < kHostParMin) {
+    if (n) std::memcpy(dst.data(), src, sizeof(vxm_grid_index) * n);
+    return;
+  }
+  constexpr int64_t kChunk = 16384;
+#pragma omp parallel for schedule(static)
+  for (int64_t c = 0; c < nn; c += kChunk)
+    std::memcpy(dst.data() + c, src + c, sizeof(vxm_grid_index) * size_t(std::min(kChunk, nn - c)));
+}
+
 const std::vector<vxm_grid_index>& BlockList::fetch() {
   if (host_valid) return host;
   if (host_pending) {  // unpacked by k_emit_host / k_status_out into mapped memory
     if (ctx->emit.list == this) ctx->flush_emit();
     VXM_CUDA(cudaStreamSynchronize(ctx->stream));
     const uint32_t n = *mapped_count;
-    host.assign(mapped, mapped + n);
+    host_copy(host, mapped, n);
     host_pending = false;
     host_valid = true;
     count_hint = n;
@@ -438,7 +452,7 @@ const std::vector<vxm_grid_index>& BlockList::fetch() {
   return host;
 }
 
-void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
+void BlockList::assign_host(const vxm_grid_index* data, uint64_t n, bool keep_host) {
   ensure(uint32_t(std::max<uint64_t>(n, 1)));
   host_pending = false;
   if (n + 1 > staging_cap) {
@@ -449,13 +463,20 @@ void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
     staging_cap = std::max<uint64_t>(n + 1, 4096);
     VXM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&staging), sizeof(uint64_t) * staging_cap));
   }
-  bool sorted = true;
-  for (uint64_t i = 0; i < n; ++i) {
-    if (!coord_ok(data[i].x) || !coord_ok(data[i].y) || !coord_ok(data[i].z))
-      throw Error(VXM_ERR_INVALID_ARGUMENT, "block index outside the supported range (+-2^20)");
-    staging[i] = pack_key(data[i].x, data[i].y, data[i].z);
-    sorted &= i == 0 || staging[i - 1] < staging[i];  // input validation only
+  // range check + packing, then the order check (input validation only):
+  // branch-free, and over the host cores for large lists (C5: 262k keys)
+  const int64_t nn = int64_t(n);
+  uint32_t bad = 0, unsorted = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad) if (nn >= kHostParMin)
+  for (int64_t i = 0; i < nn; ++i) {
+    const vxm_grid_index g = data[i];
+    bad |= uint32_t(!coord_ok(g.x)) | uint32_t(!coord_ok(g.y)) | uint32_t(!coord_ok(g.z));
+    staging[i] = pack_key(g.x, g.y, g.z);
   }
+  if (bad) throw Error(VXM_ERR_INVALID_ARGUMENT, "block index outside the supported range (+-2^20)");
+#pragma omp parallel for schedule(static) reduction(| : unsorted) if (nn >= kHostParMin)
+  for (int64_t i = 1; i < nn; ++i) unsorted |= uint32_t(staging[i - 1] >= staging[i]);
+  const bool sorted = unsorted == 0u;
   staging[n] = n;  // count travels in the same copy (low 32 bits)
   const uint32_t n32 = uint32_t(n);
   VXM_CUDA(cudaMemcpyAsync(keys.p, staging, sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
@@ -464,8 +485,13 @@ void BlockList::assign_host(const vxm_grid_index* data, uint64_t n) {
                            ctx->stream));
   // staging (pinned) stays alive until the next assign; calls that reuse the
   // list synchronise the stream before returning
-  host.assign(data, data + n);
-  host_valid = true;
+  if (keep_host) {
+    host_copy(host, data, n);
+    host_valid = true;
+  } else {
+    host.clear();
+    host_valid = false;  // (fetch() downloads it if ever asked)
+  }
   count_hint = n32;
   sorted_unique = sorted;
 }

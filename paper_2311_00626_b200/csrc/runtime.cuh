@@ -263,9 +263,14 @@ struct BlockList {
   }
   void ensure(uint32_t n);
   const std::vector<vxm_grid_index>& fetch();   // sync + download + unpack
-  void assign_host(const vxm_grid_index* data, uint64_t n);  // upload (sorted as given)
+  // upload (sorted as given); keep_host = false: no host copy kept (an input
+  // list the caller never reads back)
+  void assign_host(const vxm_grid_index* data, uint64_t n, bool keep_host = true);
   ~BlockList();
 };
+
+// Host-side loops over lists at least this long run on the host cores (OpenMP).
+constexpr int64_t kHostParMin = 65536;
 
 struct EsdfState {
   std::vector<vxm_grid_index> lists[3];
