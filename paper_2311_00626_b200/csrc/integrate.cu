@@ -200,12 +200,12 @@ __device__ inline bool fast_floor(float f, float c, float xf, float zf, int* idx
 
 // One voxel: projection, sample, update (integrator.cpp:98-123); returns
 // whether its bytes changed.  p = T_SL * centre (FP64, pinned order).
-template <bool OCC>
+template <bool OCC, bool LIDAR, bool LINEAR>
 __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<OCC>::V* blk, int lin, double px,
                                        double py, double pz, bool is_new, uint32_t& n_read,
                                        uint32_t& n_upd) {
   double d_v;
-  if (!a.lidar) {
+  if (!LIDAR) {
     d_v = pz;  // CameraIntrinsics::depth_of — camera.hpp:49
   } else {     // LidarIntrinsics::depth_of — lidar.hpp:62
     d_v = __dsqrt_rn(__dadd_rn(__dmul_rn(px, px), __dadd_rn(__dmul_rn(py, py), __dmul_rn(pz, pz))));
@@ -217,8 +217,8 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<O
   bool ok;
   V old = Ops::zero();
   bool have_old = false;
-  if (!a.lidar) {
-    if (!a.linear) {
+  if (!LIDAR) {
+    if (!LINEAR) {
       int col, row;
       const float xf = __double2float_rn(px), yf = __double2float_rn(py), zf = __double2float_rn(pz);
       if (!(fast_floor(a.fu_f, a.cu_f, xf, zf, &col) && fast_floor(a.fv_f, a.cv_f, yf, zf, &row))) {
@@ -259,8 +259,8 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<O
     if (!(az >= 0.0 && az < 6.283185307173872)) az = __dsub_rn(az, __dmul_rn(kTwoPi, floor(__ddiv_rn(az, kTwoPi))));
     const double u = __dmul_rn(az, a.u_scale);
     if (!(u >= 0.0 && u < double(a.na))) return false;
-    ok = a.linear ? sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s)
-                  : sample_nearest_d(a.depth, a.W, a.H, u, v, &s);
+    ok = LINEAR ? sample_linear_d(a.depth, a.W, a.H, u, v, a.max_gap, &s)
+                : sample_nearest_d(a.depth, a.W, a.H, u, v, &s);
   }
   if (!ok) return false;
   const float d_p = __fsub_rn(s, __double2float_rn(d_v));  // integrator.cpp:116
@@ -285,11 +285,17 @@ __device__ inline bool integrate_voxel(const IntegrateArgs& a, typename VoxOps<O
 // otherwise the general per-voxel path (LiDAR / linear: 3 CTAs / SM).  The
 // occupancy is the measured optimum of each (C2 -13 %, C3 -8 % kernel time vs
 // the register-unbounded build).
-template <bool OCC, bool FASTCAM>
+// MODE: kIntegCamNearest (FASTCAM), kIntegCamLinear, kIntegLidarNearest,
+// kIntegLidarLinear — the sensor and sampling are compile-time in each.
+constexpr int kIntegCamNearest = 0, kIntegCamLinear = 1, kIntegLidarNearest = 2, kIntegLidarLinear = 3;
+template <bool OCC, int MODE>
 #ifndef VXM_INTEG_GEN_MINB
 #define VXM_INTEG_GEN_MINB 4
 #endif
-__global__ void __launch_bounds__(256, FASTCAM ? 4 : VXM_INTEG_GEN_MINB) k_integrate(IntegrateArgs a) {
+__global__ void __launch_bounds__(256, MODE == kIntegCamNearest ? 4 : VXM_INTEG_GEN_MINB) k_integrate(IntegrateArgs a) {
+  constexpr bool FASTCAM = MODE == kIntegCamNearest;
+  constexpr bool LIDAR = MODE >= kIntegLidarNearest;
+  constexpr bool LINEAR = MODE == kIntegCamLinear || MODE == kIntegLidarLinear;
   pdl_wait();  // see launch_pdl
   pdl_trigger();
   using Ops = VoxOps<OCC>;
@@ -337,13 +343,6 @@ __global__ void __launch_bounds__(256, FASTCAM ? 4 : VXM_INTEG_GEN_MINB) k_integ
     }
     const int32_t gz = key_z(key);
     bool any = false;
-    auto centre_p = [&](int j, double& px, double& py, double& pz) {
-      const double cz = centre(gz, j >> 1);
-      const double* Ay = (j & 1) ? Ay1 : Ay0;
-      pz = __dadd_rn(__dadd_rn(Ax[2], __dadd_rn(Ay[2], __dmul_rn(R[8], cz))), a.T_SL.t[2]);
-      px = __dadd_rn(__dadd_rn(Ax[0], __dadd_rn(Ay[0], __dmul_rn(R[2], cz))), a.T_SL.t[0]);
-      py = __dadd_rn(__dadd_rn(Ax[1], __dadd_rn(Ay[1], __dmul_rn(R[5], cz))), a.T_SL.t[1]);
-    };
     if (FASTCAM) {
       // camera, nearest sampling (the hot configuration): per chunk of 4 voxels
       // all depth samples and old voxels are loaded before any is used
@@ -364,7 +363,7 @@ __global__ void __launch_bounds__(256, FASTCAM ? 4 : VXM_INTEG_GEN_MINB) k_integ
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          // p = (A_x + (A_y + R_z c_z)) + t — the pinned order of centre_p
+          // p = (A_x + (A_y + R_z c_z)) + t — pose.hpp:58-60, the pinned a0 + (a1 + a2) order
           const double* Ay = (q & 1) ? Ay1 : Ay0;
           const double* rz = Rz[q >> 1];
           const double pz = __dadd_rn(__dadd_rn(Ax[2], __dadd_rn(Ay[2], rz[2])), a.T_SL.t[2]);
@@ -404,11 +403,21 @@ __global__ void __launch_bounds__(256, FASTCAM ? 4 : VXM_INTEG_GEN_MINB) k_integ
         }
       }
     } else {
+      // voxels j and j + 1 share z: R(i, z) * c_z once per pair;
+      // p = (A_x + (A_y + R_z c_z)) + t as in the camera path
 #pragma unroll 1
-      for (int j = 0; j < 16; ++j) {
-        double px, py, pz;
-        centre_p(j, px, py, pz);
-        any |= integrate_voxel<OCC>(a, blk, lane + 32 * j, px, py, pz, is_new, n_read, n_upd);
+      for (int j0 = 0; j0 < 16; j0 += 2) {
+        const double cz = centre(gz, j0 >> 1);
+        const double rz0 = __dmul_rn(R[2], cz), rz1 = __dmul_rn(R[5], cz), rz2 = __dmul_rn(R[8], cz);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double* Ay = q ? Ay1 : Ay0;
+          const double pz = __dadd_rn(__dadd_rn(Ax[2], __dadd_rn(Ay[2], rz2)), a.T_SL.t[2]);
+          const double px = __dadd_rn(__dadd_rn(Ax[0], __dadd_rn(Ay[0], rz0)), a.T_SL.t[0]);
+          const double py = __dadd_rn(__dadd_rn(Ax[1], __dadd_rn(Ay[1], rz1)), a.T_SL.t[1]);
+          any |= integrate_voxel<OCC, LIDAR, LINEAR>(a, blk, lane + 32 * (j0 + q), px, py, pz, is_new, n_read,
+                                                    n_upd);
+        }
       }
     }
     any = __any_sync(0xffffffffu, any);
@@ -578,9 +587,14 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   a.lo_min = quantize_log_odds(cfg.log_odds_min);
   a.lo_max = quantize_log_odds(cfg.log_odds_max);
   const bool occ = L->type == VXM_LAYER_OCCUPANCY;
-  const bool fast = !a.lidar && !a.linear;
-  void (*kern)(IntegrateArgs) = occ ? (fast ? k_integrate<true, true> : k_integrate<true, false>)
-                                    : (fast ? k_integrate<false, true> : k_integrate<false, false>);
+  const int mode = a.lidar ? (a.linear ? kIntegLidarLinear : kIntegLidarNearest)
+                           : (a.linear ? kIntegCamLinear : kIntegCamNearest);
+  void (*const kerns[2][4])(IntegrateArgs) = {
+      {k_integrate<false, kIntegCamNearest>, k_integrate<false, kIntegCamLinear>,
+       k_integrate<false, kIntegLidarNearest>, k_integrate<false, kIntegLidarLinear>},
+      {k_integrate<true, kIntegCamNearest>, k_integrate<true, kIntegCamLinear>,
+       k_integrate<true, kIntegLidarNearest>, k_integrate<true, kIntegLidarLinear>}};
+  void (*kern)(IntegrateArgs) = kerns[occ ? 1 : 0][mode];
   // resident CTAs per SM: the persistent grid is one wave
   const int per_sm = ctx->resident_per_sm((const void*)kern, 256);
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(cand_cap, ctx->sm_count * per_sm));
