@@ -95,15 +95,21 @@ __device__ inline bool valid_depth_i(float d) { return d > 0.0f && isfinite(d); 
 // the CUDA libm versions were half of k_integrate's LiDAR instructions (one in
 // six of them materialising polynomial constants).  vxm_atan2 instead rotates
 // (x, y) by a table vector near its angle and sums a short series:
-//   k     = nearest multiple of pi/512 to an FP32 estimate of the angle
-//   (c,s) = (cos, sin)(k pi/512) rounded to double; psi = its exact angle
-//           atan2(s, c) as a double-double (host long double, kAtanTabN entries)
+//   octant o = (|y| > |x|, x < 0, y < 0), t = min/max of |x|, |y| in FP32,
+//   k     = round(128 t): the table direction of octant o at base angle
+//           atan(k/128) (mirrored into the octant: pi/2 - a, pi - a, -a)
+//   (c,s) = that direction's (cos, sin) rounded to double; psi = the exact
+//           angle atan2(s, c) of the rounded vector as a double-double
+//           (host long double, kAtanTabN = 8 x 129 entries)
 //   x' = x c + y s,  y' = y c - x s      (y' by Kahan's difference of products)
 //   atan2(y, x) = psi + atan(y'/x'),  |y'/x'| < 0.005:  q - q^3/3 + q^5/5 - q^7/7
-// Accuracy ~1 ulp (libm class: glibc and CUDA libm also differ in the last
-// ulp); the tolerance tests (tests/helpers.py:36) cover it.
+// (the octant and t replace an FP32 polynomial estimate of the angle: the
+// table index needs no arctangent).  Accuracy ~1 ulp (libm class: glibc and
+// CUDA libm also differ in the last ulp); the tolerance
+// tests (tests/helpers.py:36) and tests/test_gpu_lidar_angles.py cover it.
 // y == 0 (signed zero / -pi vs pi) goes to the libm routine.
-constexpr int kAtanTabN = 1025;  // k = -512 .. 512
+constexpr int kAtanK = 128;
+constexpr int kAtanTabN = 8 * (kAtanK + 1);
 
 // sqrt to ~1 ulp (an atan2 argument; not the depth, which stays correctly
 // rounded): MUFU.RSQ64H seed + two Newton steps, 0 for 0.
@@ -118,17 +124,12 @@ __constant__ double kAtanQ[3] = {-1.0 / 3.0, 1.0 / 5.0, -1.0 / 7.0};
 
 __device__ inline double vxm_atan2(double y, double x, const double4* __restrict__ tab) {
   if (y == 0.0) return atan2(y, x);
-  // FP32 estimate (|error| < 1e-4 rad): octant reduction + odd polynomial
-  const float fx = float(x), fy = float(y);
-  const float ax = fabsf(fx), ay = fabsf(fy);
-  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  const float t = __fdividef(mn, mx), t2 = t * t;
-  float e = t * (0.99978784f + t2 * (-0.32580840f + t2 * (0.15557865f + t2 * (-0.04432655f))));
-  if (ay > ax) e = 1.57079633f - e;
-  if (fx < 0.0f) e = 3.14159265f - e;
-  if (fy < 0.0f) e = -e;
-  const int k = __float2int_rn(e * 162.97466f);  // 512 / pi
-  const double2* tp = reinterpret_cast<const double2*>(tab + (k + 512));
+  const float ax = fabsf(float(x)), ay = fabsf(float(y));
+  const bool sw = ay > ax;
+  const float t = __fdividef(sw ? ax : ay, sw ? ay : ax);
+  const int k = __float2int_rn(t * float(kAtanK));
+  const int o = (sw ? 1 : 0) | (x < 0.0 ? 2 : 0) | (y < 0.0 ? 4 : 0);
+  const double2* tp = reinterpret_cast<const double2*>(tab + (o * (kAtanK + 1) + k));
   const double2 CS = __ldg(tp), PSI = __ldg(tp + 1);  // (c, s), (psi_hi, psi_lo)
   const double xr = fma(x, CS.x, y * CS.y);
   const double w = x * CS.y;
@@ -498,20 +499,25 @@ static float quantize_log_odds(float v) {
   return static_cast<float>(std::nearbyint(double(v) * 4096.0) / 4096.0);
 }
 
-// The vxm_atan2 table (host long double): entry k + 512 holds (c, s) =
-// (cos, sin)(k pi / 512) rounded to double and the exact angle of that rounded
-// vector as a double-double.
+// The vxm_atan2 table (host long double): entry o * 129 + k holds (c, s) =
+// (cos, sin) of octant o's direction at base angle atan(k / 128), rounded to
+// double, and the exact angle of that rounded vector as a double-double.
 static const double4* ensure_atan_table(Context* ctx) {
   if (ctx->atan_tab.p) return ctx->atan_tab.as<const double4>();
   std::vector<double4> t(kAtanTabN);
   const long double pi = 3.141592653589793238462643383279502884L;
-  for (int i = 0; i < kAtanTabN; ++i) {
-    const long double phi = (long double)(i - 512) * pi / 512.0L;
-    const double c = double(cosl(phi)), s = double(sinl(phi));
-    long double psi = atan2l((long double)s, (long double)c);
-    psi += 2.0L * pi * roundl((phi - psi) / (2.0L * pi));  // k = +-512: the side of +-pi k is on
-    const double hi = double(psi);
-    t[i] = make_double4(c, s, hi, double(psi - (long double)hi));
+  for (int o = 0; o < 8; ++o) {
+    for (int k = 0; k <= kAtanK; ++k) {
+      long double phi = atanl((long double)k / kAtanK);
+      if (o & 1) phi = pi / 2 - phi;  // |y| > |x|
+      if (o & 2) phi = pi - phi;      // x < 0
+      if (o & 4) phi = -phi;          // y < 0
+      const double c = double(cosl(phi)), s = double(sinl(phi));
+      long double psi = atan2l((long double)s, (long double)c);
+      psi += 2.0L * pi * roundl((phi - psi) / (2.0L * pi));  // phi = +-pi: the side of +-pi it is on
+      const double hi = double(psi);
+      t[o * (kAtanK + 1) + k] = make_double4(c, s, hi, double(psi - (long double)hi));
+    }
   }
   ctx->atan_tab.ensure(sizeof(double4) * t.size());
   VXM_CUDA(cudaMemcpyAsync(ctx->atan_tab.p, t.data(), sizeof(double4) * t.size(), cudaMemcpyHostToDevice,
