@@ -88,7 +88,8 @@ struct VoxOps<true> {  // occupancy_update — updates.hpp:59-72
   }
 };
 
-__device__ inline bool valid_depth_i(float d) { return d > 0.0f && isfinite(d); }
+// d > 0 && isfinite(d): the positive finite floats are the bit patterns 1 .. 0x7f7fffff
+__device__ inline bool valid_depth_i(float d) { return __float_as_uint(d) - 1u < 0x7f7fffffu; }
 
 // ---- FP64 atan2 for the LiDAR projection ----------------------------------------
 // lidar.hpp:43-55 evaluates atan2 (azimuth) and acos (polar angle) per voxel;
@@ -126,9 +127,12 @@ __device__ inline double vxm_atan2(double y, double x, const double4* __restrict
   if (y == 0.0) return atan2(y, x);
   const float ax = fabsf(float(x)), ay = fabsf(float(y));
   const bool sw = ay > ax;
-  const float t = __fdividef(sw ? ax : ay, sw ? ay : ax);
-  const int k = __float2int_rn(t * float(kAtanK));
-  const int o = (sw ? 1 : 0) | (x < 0.0 ? 2 : 0) | (y < 0.0 ? 4 : 0);
+  float rm;  // 1 / max (MUFU.RCP): t only picks the table entry
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rm) : "f"(sw ? ay : ax));
+  const int k = __float2int_rn((sw ? ax : ay) * rm * float(kAtanK));
+  // octant from the sign bits (y != 0 here; x = -0 and +0 give the same
+  // direction, pi / 2, at t = 0)
+  const int o = (sw ? 1 : 0) | ((__double2hiint(x) >> 30) & 2) | ((__double2hiint(y) >> 29) & 4);
   const double2* tp = reinterpret_cast<const double2*>(tab + (o * (kAtanK + 1) + k));
   const double2 CS = __ldg(tp), PSI = __ldg(tp + 1);  // (c, s), (psi_hi, psi_lo)
   const double xr = fma(x, CS.x, y * CS.y);
