@@ -168,8 +168,10 @@ __device__ inline bool sample_nearest_d(const float* img, int W, int H, double u
 __device__ inline bool sample_linear_d(const float* img, int W, int H, double u, double v,
                                        float gap, float* out) {
   const double gu = __dsub_rn(u, 0.5), gv = __dsub_rn(v, 0.5);
-  const int x0 = int(floor(gu)), y0 = int(floor(gv));
-  if (x0 < 0 || y0 < 0 || x0 + 1 >= W || y0 + 1 >= H) return false;
+  const double fx0 = floor(gu), fy0 = floor(gv);
+  const int x0 = int(fx0), y0 = int(fy0);
+  // x0 < 0 || x0 + 1 >= W (and the same for y) as one unsigned compare each
+  if (unsigned(x0) >= unsigned(W - 1) || unsigned(y0) >= unsigned(H - 1)) return false;
   const float d00 = __ldg(img + size_t(y0) * W + x0), d10 = __ldg(img + size_t(y0) * W + x0 + 1);
   const float d01 = __ldg(img + size_t(y0 + 1) * W + x0);
   const float d11 = __ldg(img + size_t(y0 + 1) * W + x0 + 1);
@@ -180,7 +182,7 @@ __device__ inline bool sample_linear_d(const float* img, int W, int H, double u,
   lo = d01 < lo ? d01 : lo; hi = hi < d01 ? d01 : hi;
   lo = d11 < lo ? d11 : lo; hi = hi < d11 ? d11 : hi;
   if (__fsub_rn(hi, lo) > gap) return false;
-  const double wx = __dsub_rn(gu, double(x0)), wy = __dsub_rn(gv, double(y0));
+  const double wx = __dsub_rn(gu, fx0), wy = __dsub_rn(gv, fy0);  // (fx0 == double(x0))
   const double omx = __dsub_rn(1.0, wx), omy = __dsub_rn(1.0, wy);
   const double top = __dadd_rn(__dmul_rn(omx, double(d00)), __dmul_rn(wx, double(d10)));
   const double bot = __dadd_rn(__dmul_rn(omx, double(d01)), __dmul_rn(wx, double(d11)));
@@ -410,9 +412,12 @@ __global__ void __launch_bounds__(256, MODE == kIntegCamNearest ? 4 : VXM_INTEG_
     } else {
       // voxels j and j + 1 share z: R(i, z) * c_z once per pair;
       // p = (A_x + (A_y + R_z c_z)) + t as in the camera path
+      // voxel_center's ((g * 8 + v) + 0.5) * vs with g * 8 once per block
+      // (the same operands as centre())
+      const double gz8 = __dmul_rn(double(gz), 8.0);
 #pragma unroll 1
       for (int j0 = 0; j0 < 16; j0 += 2) {
-        const double cz = centre(gz, j0 >> 1);
+        const double cz = __dmul_rn(__dadd_rn(__dadd_rn(gz8, double(j0 >> 1)), 0.5), a.vs);
         const double rz0 = __dmul_rn(R[2], cz), rz1 = __dmul_rn(R[5], cz), rz2 = __dmul_rn(R[8], cz);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
