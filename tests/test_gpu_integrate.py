@@ -75,6 +75,29 @@ def test_lidar_inverse_square(vx, port):
     assert tsdf_close(va, vb)
 
 
+@pytest.mark.parametrize("scene", ["sphere_in_box", "lidar_yard"])
+def test_lidar_nearest_sampling(vx, port, scene):
+    """sample_depth_nearest for LiDAR (image.hpp:65-77; the LiDAR-nearest
+    instantiation of k_integrate): block set and observed mask exact, TSDF
+    within the LiDAR tolerance."""
+    li, seq = lidar_frames(scene, 360, 24, 3, 8)
+    cfg = A.default_integrator_config(truncation=0.2, lidar_sample=A.SAMPLE_NEAREST)
+    g = vx.TsdfLayer(0.05)
+    o = port.layer(A.LAYER_TSDF, 0.05)
+    n = 0
+    for T, d in seq:
+        a = vx.integrate_depth(g, d, T, li, cfg)
+        b = port.integrate_lidar(o, d, T, li, cfg)
+        n += len(a)
+        assert np.array_equal(a, b)
+    assert n > 0
+    ka, va = g.export()
+    kb, vb = o.export()
+    assert np.array_equal(ka, kb)
+    assert np.array_equal(va["weight"] > 0, vb["weight"] > 0)
+    assert tsdf_close(va, vb)
+
+
 def test_changed_list_names_exactly_changed_blocks(vx):
     """integrate_test.cpp:324-363."""
     cam, seq = camera_frames("sphere_in_box", 160, 120, 1, 8)
