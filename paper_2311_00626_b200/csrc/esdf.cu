@@ -1033,6 +1033,7 @@ EsdfScratch esdf_scratch(Context* ctx, uint32_t n_upd_cap, uint32_t n_all_cap) {
 uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
                                 const vxm_esdf_config& cfg, EsdfScratch& s, uint32_t epoch) {
   Context* ctx = E->ctx;
+  ++E->esdf_gen;
   const uint32_t nu_cap = std::max<uint32_t>(updated->count_hint, 1);
   const uint32_t n7 = 7u * nu_cap;
   const uint64_t* upd = updated->keys.as<uint64_t>();
@@ -1203,6 +1204,8 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.dataflow = dataflow;
   for (int i = 0; i < 3; ++i) la.stamp_pair[i] = E->stamp_pair[i];
   la.stamp_r1same = E->stamp_r1same;
+  la.stamp_quiet = E->stamp_quiet;
+  la.quiet_epoch = 0;
   la.lim = esdf_limits(E, cfg);
   la.status = E->ctx->status_w();
   la.fast_only = !E->esdf_user_data && E->esdf_max_sq_seen <= kFastOff * kFastOff;
@@ -1224,8 +1227,14 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
   E->ensure_capacity(std::min<uint64_t>(need, E->max_blocks));
   const uint32_t n_all_cap = E->capacity;
   EsdfScratch s = esdf_scratch(ctx, updated->count_hint, n_all_cap);
+  // the quiet chain (Layer::stamp_quiet): unbroken since the last k_lower_xr
+  // update (growth above breaks it), same limits
+  const Limits qlim = esdf_limits(E, cfg);
+  const uint32_t quiet_epoch = E->xr_gen == E->esdf_gen && E->xr_max_sq == qlim.max_sq &&
+                               E->xr_cap_sq == qlim.cap_sq ? E->xr_epoch : 0u;
   esdf_mark_phase(E, T, updated, cfg, s, epoch);
   LowerArgs la = lower_args(E, cfg);
+  la.quiet_epoch = quiet_epoch;
   la.full = 1;
   la.sorted_slots = E->sorted_slots[E->sorted_parity];
   la.stamp_new = E->stamp_new;
@@ -1236,10 +1245,16 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
   la.sorted_keys = E->sorted_keys[E->sorted_parity];
   la.out_keys = changed_out->keys.as<uint64_t>();
   la.out_n = changed_out->d_count;
-  if (!launch_lower(ctx, la, E->num_blocks))  // the cross-round kernel compacts in-kernel
+  if (!launch_lower(ctx, la, E->num_blocks)) {  // the cross-round kernel compacts in-kernel
     launch_compact_keys(ctx, E->sorted_keys[E->sorted_parity], s.flags, &E->meta->num_blocks,
                         n_all_cap, changed_out->keys.as<uint64_t>(), changed_out->d_count, nullptr,
                         "k_compact_esdf");
+  } else {  // k_lower_xr: the chain continues from this update
+    E->xr_gen = E->esdf_gen;
+    E->xr_epoch = epoch;
+    E->xr_max_sq = qlim.max_sq;
+    E->xr_cap_sq = qlim.cap_sq;
+  }
   check_launch(ctx, "k_lower");
   changed_out->host_valid = false;
   changed_out->host_pending = false;
@@ -1252,6 +1267,7 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
 void esdf_finish(Layer* E, BlockList* changed_out) {
   Context* ctx = E->ctx;
   const DevStatus& st = *ctx->h_status;
+  if (st.capacity_error || st.pool_overflow || st.watchdog) ++E->esdf_gen;  // (breaks the quiet chain)
   if (st.capacity_error || st.pool_overflow)
     throw Error(VXM_ERR_CAPACITY, "Layer: block capacity exhausted");
   if (st.watchdog)
@@ -1363,6 +1379,7 @@ void esdf_sorted_export(Layer* E, std::vector<uint64_t>* keys, std::vector<int32
 
 void run_clear_invalid(Layer* E, const vxm_esdf_config& cfg, EsdfState* st,
                        std::vector<vxm_grid_index>* changed) {
+  ++E->esdf_gen;  // k_clear writes blocks
   if (st->lists[1].empty()) return;  // esdf/integrator.cpp:435-437
   Context* ctx = E->ctx;
   E->refresh();
@@ -1435,6 +1452,7 @@ int run_lower_esdf(Layer* E, EsdfState* st, const vxm_esdf_config& cfg,
   }
   VXM_CUDA(cudaMemcpyAsync(dn.p, &nl, sizeof nl, cudaMemcpyHostToDevice, ctx->stream));
   const uint32_t tag = ++ctx->call_epoch;
+  ++E->esdf_gen;  // (a seeded lowering writes blocks)
   LowerArgs la = lower_args(E, cfg);
   la.full = 0;
   la.seeds = dslots.as<int32_t>();

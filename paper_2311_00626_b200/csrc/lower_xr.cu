@@ -294,7 +294,17 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
           if (j >= n_ns) break;
           const int32_t s = __ldcg(a.list[1] + (n_blocks - 1u - j));
           ++j;
-          const bool reset_chg = warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
+          // a quiet block (Layer::stamp_quiet: the previous update left it
+          // untouched, its reset the identity, the same bytes in both pools,
+          // and neither mark nor allocation touched it since) is already its
+          // own round-1 result in the work pool: no read, no copy
+          bool quiet = false;
+          if (a.quiet_epoch != 0u && lane == 0)
+            quiet = a.stamp_quiet[s] == a.quiet_epoch && a.stamp_mark[s] != a.call_epoch &&
+                    a.stamp_new[s] != a.call_epoch;
+          quiet = __shfl_sync(0xffffffffu, quiet, 0);
+          const bool reset_chg =
+              quiet ? false : warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
           __syncwarp();
           if (lane == 0) {
             // unchanged by round 1: if no later round writes it, the changed-set
@@ -643,7 +653,8 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
     // it with an epoch of this launch above round 1's) is byte-identical
     const bool late = a.stamp_dirty[0][s] > base_epoch + 1u || a.stamp_dirty[1][s] > base_epoch + 1u;
     if (!ch && lower && !late && a.stamp_r1same[s] == a.call_epoch) {
-      // unchanged without reading the block
+      // unchanged without reading the block: and quiet for the next update
+      if (lane == 0) a.stamp_quiet[s] = a.call_epoch;
     } else if (!ch && lower) {
       const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(s) * 1536);
       const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(s) * 1536);

@@ -301,6 +301,8 @@ void Layer::ensure_capacity(uint64_t need) {
     for (int i = 0; i < 3; ++i) grow_copy(&pair_face[i], capacity * 2ull, 0, nc * 2ull, 0, st);
     for (int a = 0; a < 3; ++a) grow_copy(&stamp_pair[a], capacity, live, nc, 0, st);
     grow_copy(&stamp_r1same, capacity, live, nc, 0, st);
+    grow_copy(&stamp_quiet, capacity, live, nc, 0, st);
+    ++esdf_gen;  // the scratch pool's blocks are not kept: no quiet block survives
   }
   // hash: power of two >= 2 * capacity, rebuilt from slot_keys
   uint64_t hc = 1024;
@@ -360,6 +362,7 @@ Layer::~Layer() {
   for (uint32_t* p : stamp_pair)
     if (p) cudaFree(p);
   if (stamp_r1same) cudaFree(stamp_r1same);
+  if (stamp_quiet) cudaFree(stamp_quiet);
 }
 
 // ---- BlockList -----------------------------------------------------------------

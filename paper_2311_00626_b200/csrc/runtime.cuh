@@ -191,6 +191,17 @@ struct Layer {
   int32_t* r1_list = nullptr;               // k_lower_xr scratch: [3][cap] round-1 pair lists
   uint32_t* stamp_pair[3] = {nullptr, nullptr, nullptr};  // round epoch of pair (b, b+axis)
   uint32_t* stamp_r1same = nullptr;  // call epoch: round 1 left the block byte-identical
+  uint32_t* stamp_quiet = nullptr;   // call epoch: both pools hold the block and reset is its identity
+  // The quiet chain (k_lower_xr): a block an update left untouched, whose
+  // round-1 reset was the identity, has the same bytes in both pools, so the
+  // next update's round 1 need neither read nor copy it — as long as nothing
+  // else wrote the layer in between.  esdf_gen counts every writer of ESDF
+  // blocks (mark, lowering, clear, growth, user writes, shards); the chain
+  // holds while it equals xr_gen, its value right after the last k_lower_xr
+  // update (epoch xr_epoch, limits xr_max_sq / xr_cap_sq).
+  uint64_t esdf_gen = 0, xr_gen = ~uint64_t(0);
+  uint32_t xr_epoch = 0;
+  int xr_max_sq = 0, xr_cap_sq = 0;
 
   // Process-unique identity (never reused, unlike the address of a destroyed
   // layer).
