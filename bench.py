@@ -302,7 +302,7 @@ def roofline(res, K, config="c2"):
     # algorithmic bytes per launch
     bytes_by_kernel = {
         "k_integrate": 8 * st["voxels_read"] + 8 * st["voxels_updated"] + 4 * st["depth_pixels"],
-        "k_lower": 12288 * st["esdf_blocks"] + 12288 * st["dirty_blocks_after_round1"]
+        "k_lower": 12288 * (st["esdf_blocks"] - st.get("quiet_blocks", 0)) + 12288 * st["dirty_blocks_after_round1"]
                    + 3072 * st["pair_exchanges"] + 12288 * st["compared_blocks"],
     }
     cand = [k for k in bytes_by_kernel if k in ks]

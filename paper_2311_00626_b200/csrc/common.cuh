@@ -145,6 +145,7 @@ struct DevStatus {
   uint32_t meta2_blocks;     // second layer's meta (fused frame update: TSDF + ESDF)
   uint32_t meta2_cur;
   uint32_t integ_claim;      // k_integrate: candidate blocks claimed (dynamic schedule)
+  uint32_t quiet_blocks;     // lower: round-1 blocks skipped by the quiet chain (no read, no copy)
 };
 
 // ---- decoupled look-back scan over (a, b) count pairs ------------------------

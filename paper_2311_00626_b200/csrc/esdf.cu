@@ -1286,6 +1286,7 @@ void esdf_finish(Layer* E, BlockList* changed_out) {
   w.pair_exchanges += st.sum_pairs;
   w.compared_blocks += st.cmp_blocks;
   w.reserved[0] += st.n_out;  // ESDF changed blocks
+  w.reserved[1] += st.quiet_blocks;  // round-1 blocks skipped by the quiet chain
 }
 
 void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
     trace[0] = tm;
   }
-  uint32_t n_pairs = 0, n_cmp = 0, rounds = 0, r1_mine = 0;
+  uint32_t n_pairs = 0, n_cmp = 0, rounds = 0, r1_mine = 0, n_quiet = 0;
   // One round of the loop; round 1 and the later rounds are separate
   // instantiations (r1 a compile-time constant in each), so the steady-state
   // loop carries none of round 1's code.  Returns false once the round's
@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
             // unchanged by round 1: if no later round writes it, the changed-set
             // compare can skip it (every later writer marks it dirty)
             if (!reset_chg) a.stamp_r1same[s] = a.call_epoch;
+            n_quiet += quiet ? 1u : 0u;
             st_release(a.stamp_swept + s, ep);
             ++r1_mine;
           }
@@ -677,9 +678,10 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
       if (ch) atomicAdd(&s_cnt, 1u);
     }
   }
-  if (lane == 0 && (n_pairs | n_cmp)) {
+  if (lane == 0 && (n_pairs | n_cmp | n_quiet)) {
     atomicAdd(&a.status->sum_pairs, n_pairs);
     atomicAdd(&a.status->cmp_blocks, n_cmp);
+    if (n_quiet) atomicAdd(&a.status->quiet_blocks, n_quiet);
   }
   __syncthreads();
   if (a.out_keys && threadIdx.x == 0) a.cta_cnt[blockIdx.x] = s_cnt;

@@ -170,7 +170,7 @@ class Context:
         s = Stats()
         check(lib().vxm_context_stats(self.h, C.byref(s)))
         return {f: int(getattr(s, f)) for f, _ in Stats._fields_ if f != "reserved"} | {
-            "esdf_changed_blocks": int(s.reserved[0])}
+            "esdf_changed_blocks": int(s.reserved[0]), "quiet_blocks": int(s.reserved[1])}
 
     def reset_stats(self):
         lib().vxm_context_reset_stats(self.h)
