@@ -646,19 +646,36 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
   const int warp_in_cta = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_cnt = 0u;
   __syncthreads();
-  for (uint32_t k = k0 + warp_in_cta; k < k1; k += kL3Threads / 32) {
-    const int32_t s = a.sorted_slots[k];
-    bool ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
-    // a site-free block that round 1 copied unchanged and no later round wrote
-    // (every pair or sweep write after round 1 lists the block dirty, stamping
-    // it with an epoch of this launch above round 1's) is byte-identical
-    const bool late = a.stamp_dirty[0][s] > base_epoch + 1u || a.stamp_dirty[1][s] > base_epoch + 1u;
-    if (!ch && lower && !late && a.stamp_r1same[s] == a.call_epoch) {
-      // unchanged without reading the block: and quiet for the next update
-      if (lane == 0) a.stamp_quiet[s] = a.call_epoch;
-    } else if (!ch && lower) {
-      const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(s) * 1536);
-      const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(s) * 1536);
+  // The per-block decisions from stamps are lane-parallel (32 blocks of the
+  // chunk per warp at once: on a large map most blocks are decided by their
+  // stamps, and one warp per block made that a chain of dependent L2 trips per
+  // block); the blocks that need their bytes compared are then compared one
+  // after the other by the whole warp.
+  // (block k0 + w + 8 (lane + 32 i) to warp w: the CTA's warps share even a
+  // short chunk)
+  constexpr uint32_t kW = kL3Threads / 32;
+  for (uint32_t kb = k0 + uint32_t(warp_in_cta); kb < k1; kb += kW * 32u) {
+    const uint32_t k = kb + kW * uint32_t(lane);
+    const bool in = k < k1;
+    const int32_t s = in ? a.sorted_slots[k] : 0;
+    bool ch = false, need = false;
+    if (in) {
+      ch = a.stamp_new[s] == a.call_epoch || a.stamp_mark[s] == a.call_epoch;
+      if (!ch && lower) {
+        // a site-free block that round 1 copied unchanged and no later round
+        // wrote (every pair or sweep write after round 1 lists the block dirty,
+        // stamping it with an epoch of this launch above round 1's) is
+        // byte-identical — and quiet for the next update
+        const bool late = a.stamp_dirty[0][s] > base_epoch + 1u || a.stamp_dirty[1][s] > base_epoch + 1u;
+        if (!late && a.stamp_r1same[s] == a.call_epoch) a.stamp_quiet[s] = a.call_epoch;
+        else need = true;
+      }
+    }
+    for (unsigned m = __ballot_sync(0xffffffffu, need); m; m &= m - 1u) {
+      const int src = __ffs(m) - 1;
+      const int32_t sc = __shfl_sync(0xffffffffu, s, src);
+      const uint4* p0 = reinterpret_cast<const uint4*>(pcur + size_t(sc) * 1536);
+      const uint4* p1 = reinterpret_cast<const uint4*>(pnxt + size_t(sc) * 1536);
       bool diff = false;
       // all 24 loads of the lane in flight at once (the phase is latency-bound)
       uint4 x[12], y[12];
@@ -670,13 +687,13 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
 #pragma unroll
       for (int q = 0; q < 12; ++q)
         diff |= (x[q].x != y[q].x) | (x[q].y != y[q].y) | (x[q].z != y[q].z) | (x[q].w != y[q].w);
-      ch = __any_sync(0xffffffffu, diff);
+      diff = __any_sync(0xffffffffu, diff);
+      if (lane == src) ch = diff;
       ++n_cmp;
     }
-    if (lane == 0) {
-      a.out_flags[k] = uint8_t(ch);
-      if (ch) atomicAdd(&s_cnt, 1u);
-    }
+    if (in) a.out_flags[k] = uint8_t(ch);
+    const uint32_t nch = __popc(__ballot_sync(0xffffffffu, in && ch));
+    if (lane == 0 && nch) atomicAdd(&s_cnt, nch);
   }
   if (lane == 0 && (n_pairs | n_cmp | n_quiet)) {
     atomicAdd(&a.status->sum_pairs, n_pairs);
