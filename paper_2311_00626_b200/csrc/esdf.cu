@@ -1206,6 +1206,7 @@ LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg) {
   la.stamp_r1same = E->stamp_r1same;
   la.stamp_quiet = E->stamp_quiet;
   la.quiet_epoch = 0;
+  la.quiet_dense = 0;
   la.lim = esdf_limits(E, cfg);
   la.status = E->ctx->status_w();
   la.fast_only = !E->esdf_user_data && E->esdf_max_sq_seen <= kFastOff * kFastOff;
@@ -1235,6 +1236,7 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
   esdf_mark_phase(E, T, updated, cfg, s, epoch);
   LowerArgs la = lower_args(E, cfg);
   la.quiet_epoch = quiet_epoch;
+  la.quiet_dense = quiet_epoch != 0u && uint64_t(E->xr_quiet) * 2u > E->num_blocks;
   la.full = 1;
   la.sorted_slots = E->sorted_slots[E->sorted_parity];
   la.stamp_new = E->stamp_new;
@@ -1287,6 +1289,7 @@ void esdf_finish(Layer* E, BlockList* changed_out) {
   w.compared_blocks += st.cmp_blocks;
   w.reserved[0] += st.n_out;  // ESDF changed blocks
   w.reserved[1] += st.quiet_blocks;  // round-1 blocks skipped by the quiet chain
+  E->xr_quiet = st.quiet_blocks;
 }
 
 void run_update_esdf(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,

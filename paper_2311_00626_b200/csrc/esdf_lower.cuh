@@ -501,6 +501,7 @@ struct LowerArgs {
   uint32_t* stamp_r1same;     // [cap] call epoch: the round-1 reset + copy left the block unchanged
   uint32_t* stamp_quiet;      // [cap] call epoch: untouched by that update, reset its identity (k_lower_xr)
   uint32_t quiet_epoch;       // the previous k_lower_xr update of an unbroken quiet chain, else 0
+  uint32_t quiet_dense;       // most blocks were quiet last time: round-1 copies claimed 32 at a time
   int dataflow;               // 1: pair items wait on dependencies; 0: phased barriers
   const uint8_t* site_any;    // [cap] 0: the block holds no site
   uint8_t* site_near;         // [cap] k_lower_xr: bit 0 a site within +-x, bit 1 within the 3x3 (x, y)

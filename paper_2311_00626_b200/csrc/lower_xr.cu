@@ -283,38 +283,48 @@ __global__ void __launch_bounds__(kL3Threads, MINB) k_lower_xr(LowerArgs a) {
         }
         r1_mine = 0;
         const uint32_t n_ns = *((volatile uint32_t*)(a.r1 + 1));
-        constexpr uint32_t kCopyChunk = 2;
-        uint32_t j = 0, j_end = 0;
-        while (true) {  // site-free blocks: reset + copy, one warp each
-          if (j == j_end) {
-            if (lane == 0) j = atomicAdd(a.r1 + 3, kCopyChunk);
-            j = __shfl_sync(0xffffffffu, j, 0);
-            j_end = j + kCopyChunk;
-          }
-          if (j >= n_ns) break;
-          const int32_t s = __ldcg(a.list[1] + (n_blocks - 1u - j));
-          ++j;
-          // a quiet block (Layer::stamp_quiet: the previous update left it
-          // untouched, its reset the identity, the same bytes in both pools,
-          // and neither mark nor allocation touched it since) is already its
-          // own round-1 result in the work pool: no read, no copy
-          bool quiet = false;
-          if (a.quiet_epoch != 0u && lane == 0)
-            quiet = a.stamp_quiet[s] == a.quiet_epoch && a.stamp_mark[s] != a.call_epoch &&
-                    a.stamp_new[s] != a.call_epoch;
-          quiet = __shfl_sync(0xffffffffu, quiet, 0);
-          const bool reset_chg =
-              quiet ? false : warp_reset_copy(pcur + size_t(s) * 1536, work + size_t(s) * 1536, lane, lim);
-          __syncwarp();
-          if (lane == 0) {
-            // unchanged by round 1: if no later round writes it, the changed-set
-            // compare can skip it (every later writer marks it dirty)
-            if (!reset_chg) a.stamp_r1same[s] = a.call_epoch;
-            n_quiet += quiet ? 1u : 0u;
+        // site-free blocks: reset + copy, one warp each.  A quiet block
+        // (Layer::stamp_quiet: the previous update left it untouched, its reset
+        // the identity, the same bytes in both pools, and neither mark nor
+        // allocation touched it since) is already its own round-1 result in
+        // the work pool: no read, no copy.  On a large map with a quiet chain a
+        // warp claims 32 blocks and its lanes decide them together when most
+        // blocks were quiet in the previous update (C3's far field); otherwise
+        // 2 at a time (the copies spread over all warps).
+        const uint32_t chunk = (MINB >= 3 && a.quiet_dense != 0u) ? 32u : 2u;
+        while (true) {
+          uint32_t j0 = 0;
+          if (lane == 0) j0 = atomicAdd(a.r1 + 3, chunk);
+          j0 = __shfl_sync(0xffffffffu, j0, 0);
+          if (j0 >= n_ns) break;
+          const uint32_t jl = j0 + uint32_t(lane);
+          const bool in = uint32_t(lane) < chunk && jl < n_ns;
+          const int32_t s = in ? __ldcg(a.list[1] + (n_blocks - 1u - jl)) : 0;
+          const bool quiet = in && a.quiet_epoch != 0u && a.stamp_quiet[s] == a.quiet_epoch &&
+                             a.stamp_mark[s] != a.call_epoch && a.stamp_new[s] != a.call_epoch;
+          if (quiet) {
+            a.stamp_r1same[s] = a.call_epoch;
             st_release(a.stamp_swept + s, ep);
-            ++r1_mine;
+          }
+          for (unsigned m = __ballot_sync(0xffffffffu, in && !quiet); m; m &= m - 1u) {
+            const int32_t sc = __shfl_sync(0xffffffffu, s, __ffs(m) - 1);
+            const bool reset_chg = warp_reset_copy(pcur + size_t(sc) * 1536, work + size_t(sc) * 1536, lane, lim);
+            __syncwarp();
+            if (lane == 0) {
+              // unchanged by round 1: if no later round writes it, the changed-set
+              // compare can skip it (every later writer marks it dirty)
+              if (!reset_chg) a.stamp_r1same[sc] = a.call_epoch;
+              st_release(a.stamp_swept + sc, ep);
+            }
+          }
+          const uint32_t nq = __popc(__ballot_sync(0xffffffffu, quiet));
+          const uint32_t nin = __popc(__ballot_sync(0xffffffffu, in));
+          if (lane == 0) {
+            n_quiet += nq;
+            r1_mine += nin;
           }
         }
+        __syncwarp();  // every lane's releases before the warp's count
         if (lane == 0 && r1_mine) {  // (per warp)
           atom_add_release(a.r1 + 4, r1_mine);
         }

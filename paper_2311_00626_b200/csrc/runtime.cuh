@@ -201,6 +201,7 @@ struct Layer {
   // update (epoch xr_epoch, limits xr_max_sq / xr_cap_sq).
   uint64_t esdf_gen = 0, xr_gen = ~uint64_t(0);
   uint32_t xr_epoch = 0;
+  uint32_t xr_quiet = 0;  // blocks the last update's round 1 found quiet
   int xr_max_sq = 0, xr_cap_sq = 0;
 
   // Process-unique identity (never reused, unlike the address of a destroyed
