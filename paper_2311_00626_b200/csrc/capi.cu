@@ -607,7 +607,8 @@ vxm_status vxm_layer_read_blocks(vxm_layer* L, const vxm_grid_index* keys, uint6
 vxm_status vxm_layer_write_blocks(vxm_layer* L, const vxm_grid_index* keys, uint64_t n,
                                   const void* voxels) {
   return guard([&] {
-    ++L->esdf_gen;  // (user data: breaks the ESDF quiet chain)
+    ++L->esdf_gen;                 // (user data: breaks the ESDF quiet chain)
+    L->mod_floor = next_mod_tick();  // (and, on a source layer, every mark-skip stamp)
     Context* ctx = L->ctx;
     if (!n) return;
     // last write of a duplicated key wins (sequential get_or_allocate + copy)

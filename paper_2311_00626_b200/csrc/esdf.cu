@@ -749,6 +749,13 @@ struct MarkArgs {
   DevStatus* status;
   uint8_t* site_any;  // per ESDF slot: the block holds a site after marking
   PostAllocArgs post;
+  // mark skip (Layer::mark_stamp): null mark_stamp = off; skip_on = 0: the
+  // stamps are only written (every stamp is below the floor anyway)
+  uint32_t* mark_stamp;
+  int skip_on;
+  const uint32_t* src_stamp;  // the source's stamp_mod
+  uint32_t skip_floor;        // stamps at or below it are not trusted
+  uint32_t mark_now;          // this marking's tick
 };
 
 // OccupancyClassifier (esdf/integrator.cpp:200-266): observed = log_odds != 0;
@@ -783,7 +790,7 @@ __device__ inline bool occ_has_free_neighbour(const float* src, int32_t self, co
 // and the source block (TSDF: 2, occupancy: 1 x 16-byte words per 4 voxels)
 // load and store coalesced, all in flight at once; the block flags are warp
 // ballots.
-template <bool OCC>
+template <bool OCC, bool SKIP = false>
 __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
   pdl_wait();  // see launch_pdl
   pdl_trigger();
@@ -798,6 +805,17 @@ __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
       continue;
     }
     const int32_t ts = a.eff_tslot[e];
+    if (!OCC && SKIP) {  // unchanged source block since its last marking: same bytes
+      // (lanes 0 / 1 load the two stamps side by side: one L2 trip)
+      uint32_t st = 0;
+      if (lane == 0) st = a.mark_stamp[es];
+      else if (lane == 1) st = a.src_stamp[ts];
+      const uint32_t ms = __shfl_sync(0xffffffffu, st, 0), sm = __shfl_sync(0xffffffffu, st, 1);
+      if (ms > a.skip_floor && sm <= ms) {
+        if (lane == 0) a.flags[e] = 0;
+        continue;
+      }
+    }
     constexpr int kSrcWords = OCC ? 1 : 2;  // 16-byte source words per 4 voxels
     const uint4* t4 = reinterpret_cast<const uint4*>(
         static_cast<const unsigned char*>(a.src_pool) + size_t(ts) * kVPB * 4 * kSrcWords);
@@ -894,6 +912,7 @@ __global__ void __launch_bounds__(256) k_mark(MarkArgs a) {
     bcl = __any_sync(0xffffffffu, bcl);
     bsite = __any_sync(0xffffffffu, bsite);
     if (lane == 0) {
+      if (a.mark_stamp) a.mark_stamp[es] = a.mark_now;
       a.site_any[es] = bsite ? 1 : 0;
       a.flags[e] = uint8_t((bch ? 1 : 0) | (bup ? 2 : 0) | (bcl ? 4 : 0));
       if (bch) a.stamp_mark[es] = a.call_epoch;
@@ -1031,7 +1050,7 @@ EsdfScratch esdf_scratch(Context* ctx, uint32_t n_upd_cap, uint32_t n_all_cap) {
 // `updated` must hold sorted unique keys (device).  Returns the upper bound of
 // the effective count.
 uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
-                                const vxm_esdf_config& cfg, EsdfScratch& s, uint32_t epoch) {
+                                const vxm_esdf_config& cfg, EsdfScratch& s, uint32_t epoch, bool mark_skip) {
   Context* ctx = E->ctx;
   ++E->esdf_gen;
   const uint32_t nu_cap = std::max<uint32_t>(updated->count_hint, 1);
@@ -1088,12 +1107,21 @@ uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated,
   m.status = ctx->status_w();
   m.site_any = E->site_any;
   m.post = pa;
+  if (mark_skip && !occ) {  // (the fused update decides whether the stamps are trustworthy)
+    m.mark_stamp = E->mark_stamp;
+    m.src_stamp = T->stamp_mod;
+    m.skip_floor = std::max(E->mark_floor, T->mod_floor);
+    m.mark_now = next_mod_tick();
+    m.skip_on = E->mark_chain ? 1 : 0;
+  }
   ctx->prof_begin("k_mark");
   // one wave of warps, each takes blocks until done
   const int mark_per_sm =
       ctx->resident_per_sm(occ ? (const void*)k_mark<true> : (const void*)k_mark<false>, 256);
   if (occ)
     launch_pdl(ctx->stream, k_mark<true>, dim3(ctx->sm_count * mark_per_sm), dim3(256), 0, m);
+  else if (m.skip_on)  // (its own instantiation: the marking without the skip test is unchanged)
+    launch_pdl(ctx->stream, k_mark<false, true>, dim3(ctx->sm_count * mark_per_sm), dim3(256), 0, m);
   else
     launch_pdl(ctx->stream, k_mark<false>, dim3(ctx->sm_count * mark_per_sm), dim3(256), 0, m);
   ctx->prof_end();
@@ -1233,7 +1261,15 @@ void esdf_launch(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& 
   const Limits qlim = esdf_limits(E, cfg);
   const uint32_t quiet_epoch = E->xr_gen == E->esdf_gen && E->xr_max_sq == qlim.max_sq &&
                                E->xr_cap_sq == qlim.cap_sq ? E->xr_epoch : 0u;
-  esdf_mark_phase(E, T, updated, cfg, s, epoch);
+  // the mark skip's stamps hold while the quiet chain does and the source and
+  // site threshold are the last update's; otherwise every stamp is dropped
+  const bool occ_src = T->type == VXM_LAYER_OCCUPANCY;
+  E->mark_chain = E->xr_gen == E->esdf_gen && E->mark_src_uid == T->uid &&
+                  E->mark_site_threshold == float(cfg.site_threshold);
+  if (!E->mark_chain) E->mark_floor = next_mod_tick();
+  E->mark_src_uid = T->uid;
+  E->mark_site_threshold = float(cfg.site_threshold);
+  esdf_mark_phase(E, T, updated, cfg, s, epoch, !occ_src);
   LowerArgs la = lower_args(E, cfg);
   la.quiet_epoch = quiet_epoch;
   la.quiet_dense = quiet_epoch != 0u && uint64_t(E->xr_quiet) * 2u > E->num_blocks;

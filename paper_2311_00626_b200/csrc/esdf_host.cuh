@@ -22,7 +22,7 @@ uint32_t grid_for(Context* ctx, uint64_t n, int per_sm = 8);
 EsdfScratch esdf_scratch(Context* ctx, uint32_t n_upd_cap, uint32_t n_all_cap);
 // effective set + ESDF allocation + neighbour table + sorted-set merge + mark
 uint32_t esdf_mark_phase(Layer* E, Layer* T, BlockList* updated, const vxm_esdf_config& cfg,
-                         EsdfScratch& s, uint32_t epoch);
+                         EsdfScratch& s, uint32_t epoch, bool mark_skip = false);
 LowerArgs lower_args(Layer* E, const vxm_esdf_config& cfg);
 void launch_compact_keys(Context* ctx, const uint64_t* in, const uint8_t* flags,
                          const uint32_t* n_ptr, uint32_t n_cap, uint64_t* out, uint32_t* n_out,

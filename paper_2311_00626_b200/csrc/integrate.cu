@@ -35,6 +35,8 @@ struct IntegrateArgs {
   const DevStatus* status_ro;
   void* pool;  // float2 (TSDF) or float (occupancy log-odds) per voxel
   uint8_t* changed;
+  uint32_t* stamp_mod;  // Layer::stamp_mod of the changed blocks := mod_epoch
+  uint32_t mod_epoch;
   const float* depth;
   const double4* atab;  // LiDAR: atan2 table (vxm_atan2)
   int W, H;
@@ -431,7 +433,10 @@ __global__ void __launch_bounds__(256, MODE == kIntegCamNearest ? 4 : VXM_INTEG_
       }
     }
     any = __any_sync(0xffffffffu, any);
-    if (lane == 0) a.changed[ci] = uint8_t(any);
+    if (lane == 0) {
+      a.changed[ci] = uint8_t(any);
+      if (any) a.stamp_mod[slot] = a.mod_epoch;
+    }
   }
   n_read = __reduce_add_sync(0xffffffffu, n_read);
   n_upd = __reduce_add_sync(0xffffffffu, n_upd);
@@ -575,6 +580,8 @@ uint32_t integrate_launch(Layer* L, const ViewArgs& va, const vxm_integrator_con
   a.status_ro = ctx->status_w();
   a.pool = L->pool[0];
   a.changed = ctx->cand_flags.as<uint8_t>();
+  a.stamp_mod = L->stamp_mod;
+  a.mod_epoch = next_mod_tick();
   a.depth = va.depth_dev;
   if (va.lidar) a.atab = ensure_atan_table(ctx);
   a.W = va.width;

@@ -281,7 +281,9 @@ void Layer::ensure_capacity(uint64_t need) {
     }
   }
   grow_copy(&slot_keys, capacity, live, nc, 0xFF, st);
+  if (type == VXM_LAYER_TSDF || type == VXM_LAYER_OCCUPANCY) grow_copy(&stamp_mod, capacity, live, nc, 0, st);
   if (type == VXM_LAYER_ESDF) {
+    grow_copy(&mark_stamp, capacity, live, nc, 0, st);
     grow_copy(&nbr, capacity * 6ull, live * 6ull, nc * 6ull, 0xFF, st);
     for (int i = 0; i < 2; ++i) {
       grow_copy(&sorted_keys[i], capacity, i == sorted_parity ? live : 0, nc, -1, st);
@@ -363,6 +365,13 @@ Layer::~Layer() {
     if (p) cudaFree(p);
   if (stamp_r1same) cudaFree(stamp_r1same);
   if (stamp_quiet) cudaFree(stamp_quiet);
+  if (stamp_mod) cudaFree(stamp_mod);
+  if (mark_stamp) cudaFree(mark_stamp);
+}
+
+uint32_t next_mod_tick() {
+  static std::atomic<uint32_t> clock{0};
+  return clock.fetch_add(1u, std::memory_order_relaxed) + 1u;
 }
 
 // ---- BlockList -----------------------------------------------------------------

@@ -202,6 +202,21 @@ struct Layer {
   uint64_t esdf_gen = 0, xr_gen = ~uint64_t(0);
   uint32_t xr_epoch = 0;
   uint32_t xr_quiet = 0;  // blocks the last update's round 1 found quiet
+  // Mark skip, on one process-wide clock (next_mod_tick): a source layer
+  // stamps every block an integrate changed (stamp_mod; a host write of its
+  // blocks raises mod_floor over all earlier stamps), an ESDF block the tick
+  // of its last marking (mark_stamp).  A block whose TSDF source block is
+  // unchanged since then re-marks to the same bytes (mark_sites is voxel-local
+  // for a TSDF source, and only marking writes the flags), so k_mark skips it
+  // — while the quiet chain holds and the source and site threshold are those
+  // of the last update (else mark_floor invalidates every stamp).
+  uint32_t* stamp_mod = nullptr;   // source layers: [cap] tick of the block's last change
+  uint32_t mod_floor = 0;
+  uint32_t* mark_stamp = nullptr;  // ESDF: [cap] tick of the block's last marking
+  uint32_t mark_floor = 0;
+  bool mark_chain = false;         // ESDF: this update may trust the stamps
+  uint64_t mark_src_uid = 0;       // ESDF: the source of the last fused update
+  float mark_site_threshold = 0.0f;
   int xr_max_sq = 0, xr_cap_sq = 0;
 
   // Process-unique identity (never reused, unlike the address of a destroyed
@@ -283,6 +298,9 @@ struct BlockList {
 
 // Host-side loops over lists at least this long run on the host cores (OpenMP).
 constexpr int64_t kHostParMin = 65536;
+
+// The process-wide modification clock of the mark skip (Layer::stamp_mod).
+uint32_t next_mod_tick();
 
 struct EsdfState {
   std::vector<vxm_grid_index> lists[3];

@@ -105,3 +105,42 @@ def test_chain_breaks_on_pool_growth(vx, port):
     for pose, d in seq:
         _step(vx, port, T, E, To, Eo, cam, pose, d, icfg, ecfg)
     assert layers_identical(*E.export(), *Eo.export())
+
+
+def test_mark_skip_source_writes_and_switch(vx, port):
+    """k_mark skips effective blocks whose TSDF block is unchanged since their
+    last marking (Layer::mark_stamp): a host write of TSDF blocks, and a switch
+    of the source layer, must make them marked again (mark_impl,
+    esdf/integrator.cpp:268-348, marks every effective block)."""
+    cam, seq = _frames(5)
+    icfg = A.default_integrator_config(truncation=0.16)
+    ecfg = A.default_esdf_config(site_threshold=0.04, max_distance=0.3)
+    T, E, To, Eo = _pair(vx, port)
+    E.reserve(1 << 16)
+    for pose, d in seq[:3]:
+        _step(vx, port, T, E, To, Eo, cam, pose, d, icfg, ecfg)
+    # host write of TSDF blocks (a surface sheet moved): then an update whose
+    # list names only some of them — the others are effective as neighbours
+    kt, vt = T.export()
+    pick = kt[::7]
+    w = vt[::7].copy()
+    w["distance"] = np.where(w["weight"] > 0, -w["distance"], w["distance"])
+    T.write_blocks(pick, w)
+    port.write_blocks(To, pick, w)
+    listed = pick[::3]
+    assert np.array_equal(vx.update_esdf(E, T, listed, ecfg), port.update_esdf(Eo, To, listed, ecfg))
+    assert layers_identical(*E.export(), *Eo.export())
+    # another source layer, then back (the blocks' flags follow each source)
+    T2, To2 = vx.TsdfLayer(VS), port.layer(A.LAYER_TSDF, VS)
+    a = vx.integrate_depth(T2, seq[3][1], seq[3][0], cam, icfg)
+    b = port.integrate_camera(To2, seq[3][1], seq[3][0], cam, icfg)
+    assert np.array_equal(vx.update_esdf(E, T2, a, ecfg), port.update_esdf(Eo, To2, b, ecfg))
+    keys = T.export()[0]
+    assert np.array_equal(vx.update_esdf(E, T, keys, ecfg), port.update_esdf(Eo, To, keys, ecfg))
+    assert layers_identical(*E.export(), *Eo.export())
+    # another site threshold
+    ecfg2 = A.default_esdf_config(site_threshold=0.06, max_distance=0.3)
+    assert np.array_equal(vx.update_esdf(E, T, keys, ecfg2), port.update_esdf(Eo, To, keys, ecfg2))
+    assert layers_identical(*E.export(), *Eo.export())
+    _step(vx, port, T, E, To, Eo, cam, seq[4][0], seq[4][1], icfg, ecfg2)
+    assert layers_identical(*E.export(), *Eo.export())
