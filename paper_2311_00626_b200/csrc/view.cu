@@ -113,6 +113,13 @@ __device__ void traverse(const double s[3], const double e[3], double cs, const 
   // would put them in local memory, one load per step on the critical path)
   int cx = cell[0], cy = cell[1], cz = cell[2];
   double tx = t_max[0], ty = t_max[1], tz = t_max[2];
+  // DEDUP only over a ray's first kDedupSteps cells: near the sensor the rays
+  // of a warp share cells (one RED per word instead of one per ray), farther
+  // out they have spread and the match costs more than the REDs it saves
+  // (measured on C3, 0.8 m cells: k_rays_lidar 88 us always, 77 / 58 / 47 /
+  // 46 / 61 us for 8 / 16 / 32 / 48 / 96 cells)
+  constexpr int kDedupSteps = 48;
+  int steps = 0;
   while (guard-- > 0) {
     // axis = 0; if (t_max[1] < t_max[0]) axis = 1; if (t_max[2] < t_max[axis]) axis = 2;
     const bool y_first = ty < tx;
@@ -130,7 +137,8 @@ __device__ void traverse(const double s[3], const double e[3], double cs, const 
       cx += step[0];
       tx = __dadd_rn(tx, t_delta[0]);
     }
-    mark_cell<DEDUP>(cube, cx, cy, cz, status);
+    if (DEDUP && ++steps <= kDedupSteps) mark_cell<true>(cube, cx, cy, cz, status);
+    else mark_cell<false>(cube, cx, cy, cz, status);
   }
 }
 
